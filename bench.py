@@ -1,0 +1,390 @@
+#!/usr/bin/env python
+"""Benchmark: tokens/s of forward+backward of one DeltaNet layer
+(H=16, d=128, L=4096, C=64, bf16 I/O, fp32 accumulate) on 1..8 B200.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+One "step" = deltanet_fwd (save states) + deltanet_bwd over one batch of
+synthetic inputs resident in HBM, i.e. every row of SURVEY §8(a).  Each rank
+owns B=8 batch rows (weak scaling: per-GPU work fixed; at N=8 this is the
+BASELINE "sharded" B=64 config).  The (b, h) units are independent, so there
+is no collective in the timed region; the NCCL all-gather of outputs and
+gradients (north_star) is timed separately and reported as "gather".
+
+Prints ONE JSON line on rank 0 (contract in the task statement / DESIGN.md).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tokens/s fwd+bwd DeltaNet layer (H=16,d=128,L=4K) at 1/2/4/8 B200; % bf16 TC peak"
+B_PER_RANK, H, L, D, C = 8, 16, 4096, 128, 64
+
+
+def per_token_head(dk, dv, c, s):
+    """Algorithmic work per token x head."""
+    f_fwd = 6 * dk * dv + 2 * c * (3 * dk + 2 * dv) + c * c / 3
+    f_bwd = 12 * dk * dv + 2 * c * (6 * dk + 4 * dv) + 4 * c * c
+    b_fwd = s * (2 * dk + 2 * dv + 1)          # read q,k,v,beta; write o
+    b_bwd = s * (4 * dk + 3 * dv + 2)          # read q,k,v,beta,dO; write dq,dk,dv,dbeta
+    return f_fwd, f_bwd, b_fwd, b_bwd
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        return {"hbm_gbs": j["hbm_gbs"], "tf_burst": j["bf16_tflops"],
+                "tf_sustained": j.get("bf16_tflops_sustained", j["bf16_tflops"]),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "tf_burst": 1590.0, "tf_sustained": 1400.0,
+            "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms (B200_PROFILING.md)."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append((float(parts[1]), float(parts[2]), float(parts[3]), parts[4:]))
+            except ValueError:
+                continue
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        load = [r for r in rows if r[2] > 250.0] or rows
+        sm = sorted(r[0] for r in load)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in load:
+            for n, flag in zip(names, r[3][1:5]):
+                if flag.strip().lower() in ("active", "1"):
+                    reasons.add(n)
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": sorted(reasons), "samples": len(load),
+                "power_w_max": max(r[2] for r in rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args, ws, rank):
+    """--impl reference: the fp64 oracle (the only 'reference' this paper
+    has) timed on the host cores on a bounded sample of the same workload."""
+    if rank != 0:
+        return
+    import numpy as np
+    import oracle
+    import synth
+    cfg = synth.CONFIGS["sharded"]
+    nthreads = oracle.default_threads()
+    n_units = max(1, min(nthreads, 16))
+    units = [(u // H, u % H) for u in range(n_units)]
+    inp = synth.make_inputs(cfg, units=units)
+
+    def step():
+        oracle.recurrent_fwd(inp["q"], inp["k"], inp["v"], inp["beta"], nthreads=nthreads)
+        oracle.recurrent_bwd(inp["q"], inp["k"], inp["v"], inp["beta"], inp["dO"],
+                             nthreads=nthreads)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    t = (time.perf_counter() - t0) / args.steps
+    # tokens/s of the metric: a step covers all H heads of B*L tokens, so the
+    # sampled n_units unit-sequences are n_units/H of a B=1 step.
+    value = n_units * L / H / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "deltanet_layer_fwd_bwd", "B_per_gpu": B_PER_RANK, "H": H,
+                   "L": L, "Dk": D, "Dv": D, "chunk": C, "io": "bf16-rounded inputs, fp64 oracle"},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": nthreads, "kind": "oracle",
+                         "sample": f"{n_units} of the {B_PER_RANK * H} (b,h) units per step, "
+                                   f"full L={L}, fwd+bwd, fp64 C oracle"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(budget_s=12.0):
+    """Oracle as it stands on the host cores, bounded sample (rank 0, N=1)."""
+    import oracle
+    import synth
+    cfg = synth.CONFIGS["sharded"]
+    nthreads = oracle.default_threads()
+    n_units = nthreads
+    units = [(u // H, u % H) for u in range(n_units)]
+    inp = synth.make_inputs(cfg, units=units)
+    reps, t_tot = 0, 0.0
+    while t_tot < budget_s and reps < 8:
+        t0 = time.perf_counter()
+        oracle.recurrent_fwd(inp["q"], inp["k"], inp["v"], inp["beta"], nthreads=nthreads)
+        oracle.recurrent_bwd(inp["q"], inp["k"], inp["v"], inp["beta"], inp["dO"],
+                             nthreads=nthreads)
+        t_tot += time.perf_counter() - t0
+        reps += 1
+    t = t_tot / reps
+    return {"value": n_units * L / H / t, "unit": "tokens/s", "cores": nthreads,
+            "kind": "oracle",
+            "sample": f"{n_units} (b,h) units x full L={L} fwd+bwd per rep, {reps} reps, "
+                      f"{t_tot:.1f} s; scaled to tokens/s as units*L/H/t"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--force-simt", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    ws, rank, local = dist_env()
+
+    if args.impl == "reference":
+        return run_reference(args, ws, rank)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2406_06484_b200 as dn
+    import synth
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs CUDA devices (no CPU path)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    dn.load_library()
+
+    cfg = synth.CONFIGS["sharded"]
+    rows = range(rank * B_PER_RANK, (rank + 1) * B_PER_RANK)
+    host = synth.make_inputs(cfg, b_range=rows)
+    td = torch.bfloat16
+    q, k, v, beta, dO = (torch.from_numpy(host[f]).to(td).to(dev).contiguous()
+                         for f in ("q", "k", "v", "beta", "dO"))
+    desc = dn.make_desc(B_PER_RANK, H, L, D, D, C, td, l2norm=True, save_states=True,
+                        force_simt=args.force_simt)
+    ws_buf = dn.alloc_workspace(desc, dev)
+    o = torch.empty_like(v)
+    grads = (torch.empty_like(q), torch.empty_like(k), torch.empty_like(v),
+             torch.empty_like(beta))
+    path = dn.deltanet_path(desc)
+    n_launch = dn.deltanet_launch_count(desc, 0) + dn.deltanet_launch_count(desc, 1)
+    stream = torch.cuda.current_stream(dev)
+
+    def fwd():
+        dn.deltanet_fwd(q, k, v, beta, chunk=C, workspace=ws_buf, want_hT=False, out=o,
+                        force_simt=args.force_simt)
+
+    def bwd():
+        dn.deltanet_bwd(q, k, v, beta, dO, chunk=C, workspace=ws_buf, want_dh0=False,
+                        out=grads, force_simt=args.force_simt)
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    for _ in range(args.warmup):
+        fwd()
+        bwd()
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    for i in range(args.steps):
+        ev[i][0].record(stream)
+        fwd()
+        ev[i][1].record(stream)
+        bwd()
+        ev[i][2].record(stream)
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clk = clocks.stop()
+    t_fwd = sum(e[0].elapsed_time(e[1]) for e in ev) / args.steps * 1e-3
+    t_bwd = sum(e[1].elapsed_time(e[2]) for e in ev) / args.steps * 1e-3
+    t_total = ev[0][0].elapsed_time(ev[-1][2]) * 1e-3
+    t_step = t_total / args.steps
+    if ws > 1:
+        tt = torch.tensor([t_step, t_fwd, t_bwd], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_step, t_fwd, t_bwd = tt.tolist()
+
+    tokens_per_step = B_PER_RANK * ws * L
+    value = tokens_per_step / t_step
+    peaks = load_peaks()
+    s = 2
+    ff, fb, bf, bb = per_token_head(D, D, C, s)
+    th = B_PER_RANK * H * L  # token-heads per rank per step
+    # dominant kernel call and its binding roofline
+    dom = ("bwd", t_bwd, fb * th, bb * th) if t_bwd >= t_fwd else ("fwd", t_fwd, ff * th, bf * th)
+    name, t_k, F_k, B_k = dom
+    long_region = t_total > 1.0
+    tf_peak = peaks["tf_sustained"] if long_region else peaks["tf_burst"]
+    t_tc, t_hbm = F_k / (tf_peak * 1e12), B_k / (peaks["hbm_gbs"] * 1e9)
+    if t_hbm >= t_tc:
+        roof = {"bound": "hbm", "achieved": B_k / t_k / 1e9, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s"}
+    else:
+        roof = {"bound": "tensor", "achieved": F_k / t_k / 1e12, "peak": tf_peak,
+                "unit": "TFLOP/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = None
+    roof["kernel"] = f"deltanet_{name} ({'tcgen05' if path == 1 else 'simt'} path)"
+    roof["peak_source"] = peaks["source"] + (" sustained" if roof["bound"] == "tensor" and long_region else "")
+    roof["algorithmic_per_token_head"] = {"flops": F_k / th, "bytes": B_k / th}
+
+    tc_frac = (ff + fb) * th * ws / t_step / (peaks["tf_burst"] * 1e12) / ws
+
+    # ---- e2e through the public API with host buffers (pinned), per step:
+    # H2D of q,k,v,beta,dO; fwd+bwd; D2H of o,dq,dk,dv,dbeta.
+    e2e = None
+    if not args.no_e2e:
+        hin = [t.cpu().pin_memory() for t in (q, k, v, beta, dO)]
+        hout = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+                for t in (o, *grads)]
+        din = [torch.empty_like(t) for t in (q, k, v, beta, dO)]
+        dout = [o, *grads]
+        h2d = sum(t.numel() * t.element_size() for t in hin)
+        d2h = sum(t.numel() * t.element_size() for t in hout)
+
+        def e2e_step():
+            for dst, src in zip(din, hin):
+                dst.copy_(src, non_blocking=True)
+            dn.deltanet_fwd(din[0], din[1], din[2], din[3], chunk=C, workspace=ws_buf,
+                            want_hT=False, out=o, force_simt=args.force_simt)
+            dn.deltanet_bwd(din[0], din[1], din[2], din[3], din[4], chunk=C,
+                            workspace=ws_buf, want_dh0=False, out=grads,
+                            force_simt=args.force_simt)
+            for dst, src in zip(hout, dout):
+                dst.copy_(src, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize(dev)
+        if ws > 1:
+            dist.barrier()
+        n_e2e = max(3, min(args.steps, 20))
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(n_e2e):
+            e2e_step()
+        a1.record(stream)
+        torch.cuda.synchronize(dev)
+        t_e2e = a0.elapsed_time(a1) * 1e-3 / n_e2e
+        if ws > 1:
+            tt = torch.tensor([t_e2e], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_e2e = tt.item()
+        e2e = {"value": tokens_per_step / t_e2e, "unit": "tokens/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": t_e2e * 1e3, "steps": n_e2e}
+
+    # ---- NCCL gather of outputs and gradients (outside the timed step)
+    gather = None
+    if ws > 1:
+        outs = [o, *grads]
+        full = [torch.empty((ws,) + t.shape, dtype=t.dtype, device=dev) for t in outs]
+        dist.barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for dst, src in zip(full, outs):
+            dist.all_gather_into_tensor(dst, src)
+        g1.record(stream)
+        torch.cuda.synchronize(dev)
+        tg = torch.tensor([g0.elapsed_time(g1) * 1e-3], device=dev)
+        dist.all_reduce(tg, op=dist.ReduceOp.MAX)
+        recv = sum(t.numel() * t.element_size() for t in full)
+        gather = {"ms": tg.item() * 1e3, "bytes_received_per_gpu": recv,
+                  "GBps": recv / tg.item() / 1e9, "collective": "ncclAllGather"}
+
+    base = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        base = cpu_baseline()
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"deltanet_layer_fwd_bwd B={B_PER_RANK}/GPU H={H} L={L} "
+                                   f"d={D} chunk={C}",
+                       "global_batch": B_PER_RANK * ws, "seq_len": L, "heads": H,
+                       "head_dim": D, "chunk": C, "parallelism": f"dp{ws} (batch x head shards)",
+                       "l2": "inputs exceed L2 (q,k,v,dO 134 MB each); no flush",
+                       "kernel_path": "tcgen05" if path == 1 else "simt"},
+            "ms_fwd": t_fwd * 1e3, "ms_bwd": t_bwd * 1e3,
+            "tc_peak_frac": tc_frac,
+            "roofline": roof,
+            "cpu_baseline": base,
+            "e2e": e2e,
+            "gpu_launches": n_launch * args.steps,
+            "clocks": clk,
+        }
+        if gather:
+            line["gather"] = gather
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,125 @@
+/*
+ * deltanet.h -- C ABI of the B200 (sm_100a) DeltaNet chunkwise delta-rule
+ * layer library, libdeltanet.so.  Forward and backward of one layer over
+ * q, k, v, beta of shape [B, H, L, d].
+ *
+ * What is computed (PAPER.md = /root/reference/PAPER.md, arXiv 2406.06484):
+ *   per (b, h) unit, with q, k optionally L2-normalised (§3.3),
+ *     S_t = S_{t-1} - beta_t (S_{t-1} k_t - v_t) k_t^T,  o_t = S_t q_t
+ *   (§2.2 lines 82-97), evaluated by the chunkwise-parallel algorithm of §3.2:
+ *   per chunk of C tokens the UT transform (Eq. 10-11)
+ *     T = (I + tril(diag(beta) K K^T, -1))^{-1} diag(beta),  W = T K,  U = T V
+ *   then the state recurrence and output (Eq. 8-9)
+ *     S <- S + (U - W S^T)^T K,   O = Q S^T + (Q K^T (.) M)(U - W S^T)
+ *   with M the inclusive causal mask (Listing 1; R4).
+ *   The backward (not given in the paper; R12) is the exact
+ *   adjoint of that map.
+ *
+ * Conventions
+ *  - Every tensor pointer is DEVICE memory owned by the caller, contiguous,
+ *    row-major, 16-byte aligned (MISALIGNED otherwise).  The library never
+ *    allocates or frees, never synchronises the host, and keeps no mutable
+ *    global state except once-per-process kernel attributes; calls on
+ *    different streams are independent.
+ *  - Layouts: q, k [B,H,L,Dk]; v, o, dO [B,H,L,Dv]; beta [B,H,L];
+ *    states h0, hT, dhT, dh0 [B,H,Dk,Dv] in the orientation H = S^T
+ *    (R2; Listing 1's S).  I/O tensors have the descriptor dtype;
+ *    states are always fp32.  Accumulation is always fp32.
+ *  - stream is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *  - Errors: argument errors are detected before any launch and nothing is
+ *    written; a launch failure returns DELTANET_ERR_CUDA; asynchronous device
+ *    faults surface at the caller's next synchronisation.  No exception
+ *    crosses the ABI.
+ *  - L need not be a multiple of chunk: the tail chunk is processed with the
+ *    missing tokens treated as beta = 0, zero rows (an exact no-op; R14).
+ */
+#ifndef DELTANET_H
+#define DELTANET_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DELTANET_ABI_VERSION 1
+
+typedef enum {
+  DELTANET_BF16 = 0, /* bf16 I/O, fp32 accumulation (BASELINE.json north_star) */
+  DELTANET_FP32 = 1  /* fp32 I/O, fp32 CUDA-core arithmetic (parity mode)     */
+} deltanet_dtype;
+
+enum {
+  /* q <- q / max(||q||_2, eps), same for k, inside the kernel (§3.3
+   * lines 329-331; R9/R10).  Gradients are w.r.t. the RAW q, k. */
+  DELTANET_L2NORM_QK = 1u << 0,
+  /* fwd: write the chunk-boundary states H_t into the workspace so the bwd
+   * does not recompute them (§3.2 line 250 recomputes them; we
+   * store them -- DESIGN.md "Differences from the paper").
+   * bwd: the workspace holds the states of a fwd over the same inputs. */
+  DELTANET_SAVE_STATES = 1u << 1,
+  /* debug: force the generic CUDA-core path even where the tcgen05 path
+   * applies (both are CUDA kernels; there is no CPU fallback). */
+  DELTANET_FORCE_SIMT = 1u << 2
+};
+
+typedef struct {
+  int B, H, L;      /* batch, heads, sequence length (>= 0)                  */
+  int Dk, Dv;       /* head dims, each in {16, 32, 64, 128, 256}             */
+  int chunk;        /* C in {16, 32, 64, 128}             */
+  int dtype;        /* deltanet_dtype                                        */
+  unsigned flags;   /* DELTANET_* bits                                       */
+  float l2_eps;     /* eps of the L2 normalisation; <= 0 selects 1e-6 (R9)   */
+} deltanet_desc;
+
+/* Error codes. */
+#define DELTANET_OK 0
+#define DELTANET_ERR_INVALID_ARG 1 /* null required pointer, negative size   */
+#define DELTANET_ERR_UNSUPPORTED 2 /* Dk/Dv/chunk/dtype outside the table    */
+#define DELTANET_ERR_MISALIGNED 3  /* a pointer not 16-byte aligned          */
+#define DELTANET_ERR_CUDA 4        /* cudaGetLastError() after a launch      */
+#define DELTANET_ERR_WORKSPACE 5   /* workspace NULL or smaller than needed  */
+
+/* Bytes of device workspace both deltanet_fwd and deltanet_bwd need for this
+ * descriptor (the chunk-boundary states, B*H*ceil(L/C)*Dk*Dv elements of the
+ * I/O dtype, plus kernel scratch).  0 for an invalid descriptor. */
+size_t deltanet_workspace_bytes(const deltanet_desc* d);
+
+/* Forward.  q, k, v, beta: inputs; h0: nullable initial state (else 0);
+ * o: output [B,H,L,Dv]; hT: nullable final state; workspace: device buffer
+ * of at least deltanet_workspace_bytes(d) bytes (states are written there
+ * when DELTANET_SAVE_STATES is set). */
+int deltanet_fwd(const deltanet_desc* d, const void* q, const void* k,
+                 const void* v, const void* beta, const float* h0, void* o,
+                 float* hT, void* workspace, size_t workspace_bytes,
+                 void* stream);
+
+/* Backward.  dO: cotangent of o; dhT: nullable cotangent of hT (else 0).
+ * Outputs dq, dk [B,H,L,Dk], dv [B,H,L,Dv], dbeta [B,H,L] in the I/O dtype
+ * (w.r.t. the raw inputs), dh0 nullable [B,H,Dk,Dv] fp32.  With
+ * DELTANET_SAVE_STATES the workspace must hold the states written by a
+ * deltanet_fwd over the same inputs; otherwise they are recomputed. */
+int deltanet_bwd(const deltanet_desc* d, const void* q, const void* k,
+                 const void* v, const void* beta, const float* h0,
+                 const void* dO, const float* dhT, void* dq, void* dk,
+                 void* dv, void* dbeta, float* dh0, void* workspace,
+                 size_t workspace_bytes, void* stream);
+
+/* Which kernel family a descriptor dispatches to: 1 = tcgen05/TMEM/TMA
+ * sm_100a path, 0 = CUDA-core (SIMT) path, -1 = unsupported descriptor. */
+int deltanet_path(const deltanet_desc* d);
+
+/* Number of kernel launches deltanet_fwd (which=0) or deltanet_bwd
+ * (which=1) issues for this descriptor (for launch accounting). */
+int deltanet_launch_count(const deltanet_desc* d, int which);
+
+/* Human-readable message for an error code (static storage). */
+const char* deltanet_strerror(int code);
+
+/* DELTANET_ABI_VERSION of the loaded library. */
+int deltanet_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DELTANET_H */

@@ -1,0 +1,221 @@
+"""B200 (sm_100a) DeltaNet chunkwise delta-rule layer -- Python binding.
+
+Thin ctypes marshalling over ``libdeltanet.so`` (C ABI: include/deltanet.h).
+Every step of the forward and backward runs in the library's CUDA kernels;
+PyTorch only provides device memory and the current stream.  There is no CPU
+fallback: without the built library, or without a CUDA device, every call
+raises.
+
+    o, hT, ws = deltanet_fwd(q, k, v, beta, chunk=64)
+    dq, dk, dv, dbeta, dh0 = deltanet_bwd(q, k, v, beta, dO, chunk=64, workspace=ws)
+
+Shapes: q, k [B,H,L,Dk]; v, dO [B,H,L,Dv]; beta [B,H,L]; states [B,H,Dk,Dv]
+(fp32, orientation H = S^T).  dtype bf16 or fp32 (same for all I/O).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdeltanet.so")
+
+DELTANET_BF16 = 0
+DELTANET_FP32 = 1
+DELTANET_L2NORM_QK = 1 << 0
+DELTANET_SAVE_STATES = 1 << 1
+DELTANET_FORCE_SIMT = 1 << 2
+
+
+class deltanet_desc(ctypes.Structure):
+    _fields_ = [("B", ctypes.c_int), ("H", ctypes.c_int), ("L", ctypes.c_int),
+                ("Dk", ctypes.c_int), ("Dv", ctypes.c_int), ("chunk", ctypes.c_int),
+                ("dtype", ctypes.c_int), ("flags", ctypes.c_uint),
+                ("l2_eps", ctypes.c_float)]
+
+
+EXPORTED = ("deltanet_workspace_bytes", "deltanet_fwd", "deltanet_bwd", "deltanet_path",
+            "deltanet_launch_count", "deltanet_strerror", "deltanet_abi_version")
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libdeltanet.so (raises if missing -- no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"libdeltanet.so not built ({path}); run "
+                           "`python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
+    P = ctypes.c_void_p
+    D = ctypes.POINTER(deltanet_desc)
+    lib.deltanet_workspace_bytes.argtypes = [D]
+    lib.deltanet_workspace_bytes.restype = ctypes.c_size_t
+    lib.deltanet_fwd.argtypes = [D, P, P, P, P, P, P, P, P, ctypes.c_size_t, P]
+    lib.deltanet_fwd.restype = ctypes.c_int
+    lib.deltanet_bwd.argtypes = [D, P, P, P, P, P, P, P, P, P, P, P, P, P, ctypes.c_size_t, P]
+    lib.deltanet_bwd.restype = ctypes.c_int
+    lib.deltanet_path.argtypes = [D]
+    lib.deltanet_path.restype = ctypes.c_int
+    lib.deltanet_launch_count.argtypes = [D, ctypes.c_int]
+    lib.deltanet_launch_count.restype = ctypes.c_int
+    lib.deltanet_strerror.argtypes = [ctypes.c_int]
+    lib.deltanet_strerror.restype = ctypes.c_char_p
+    lib.deltanet_abi_version.argtypes = []
+    lib.deltanet_abi_version.restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+class DeltaNetError(RuntimeError):
+    pass
+
+
+def deltanet_strerror(code: int) -> str:
+    return load_library().deltanet_strerror(int(code)).decode()
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        raise DeltaNetError(f"{what}: {deltanet_strerror(rc)} (code {rc})")
+
+
+def make_desc(B, H, L, Dk, Dv, chunk=64, dtype=torch.bfloat16, l2norm=True,
+              save_states=True, force_simt=False, eps=1e-6) -> deltanet_desc:
+    dt = {torch.bfloat16: DELTANET_BF16, torch.float32: DELTANET_FP32}[dtype]
+    flags = ((DELTANET_L2NORM_QK if l2norm else 0) |
+             (DELTANET_SAVE_STATES if save_states else 0) |
+             (DELTANET_FORCE_SIMT if force_simt else 0))
+    return deltanet_desc(B, H, L, Dk, Dv, chunk, dt, flags, eps)
+
+
+def _desc_for(q, v, chunk, l2norm, save_states, force_simt, eps):
+    B, H, L, Dk = q.shape
+    return make_desc(B, H, L, Dk, v.shape[-1], chunk, q.dtype, l2norm, save_states,
+                     force_simt, eps)
+
+
+def deltanet_workspace_bytes(desc: deltanet_desc) -> int:
+    return int(load_library().deltanet_workspace_bytes(ctypes.byref(desc)))
+
+
+def deltanet_path(desc: deltanet_desc) -> int:
+    return int(load_library().deltanet_path(ctypes.byref(desc)))
+
+
+def deltanet_launch_count(desc: deltanet_desc, which: int) -> int:
+    return int(load_library().deltanet_launch_count(ctypes.byref(desc), int(which)))
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _need(t, name, dtype, device):
+    if t is None:
+        return
+    if not t.is_cuda:
+        raise DeltaNetError(f"{name} must be a CUDA tensor (no CPU path)")
+    if t.dtype != dtype:
+        raise DeltaNetError(f"{name} has dtype {t.dtype}, expected {dtype}")
+    if t.device != device:
+        raise DeltaNetError(f"{name} on {t.device}, expected {device}")
+    if not t.is_contiguous():
+        raise DeltaNetError(f"{name} must be contiguous")
+
+
+def alloc_workspace(desc: deltanet_desc, device) -> torch.Tensor:
+    n = deltanet_workspace_bytes(desc)
+    return torch.empty(max(n, 16), dtype=torch.uint8, device=device)
+
+
+def _stream(device):
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def deltanet_fwd(q, k, v, beta, *, chunk=64, l2norm=True, h0=None, save_states=True,
+                 workspace=None, want_hT=True, force_simt=False, eps=1e-6, out=None):
+    """Forward of the chunkwise delta rule (§3.2 Eq. 8-11).
+    Returns (o, hT or None, workspace)."""
+    lib = load_library()
+    dev = q.device
+    for t, n in ((q, "q"), (k, "k"), (v, "v"), (beta, "beta")):
+        _need(t, n, q.dtype, dev)
+    _need(h0, "h0", torch.float32, dev)
+    d = _desc_for(q, v, chunk, l2norm, save_states, force_simt, eps)
+    B, H, L, Dk = q.shape
+    Dv = v.shape[-1]
+    o = out if out is not None else torch.empty((B, H, L, Dv), dtype=q.dtype, device=dev)
+    hT = torch.empty((B, H, Dk, Dv), dtype=torch.float32, device=dev) if want_hT else None
+    if workspace is None:
+        workspace = alloc_workspace(d, dev)
+    rc = lib.deltanet_fwd(ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(beta), _ptr(h0),
+                          _ptr(o), _ptr(hT), _ptr(workspace), workspace.numel(), _stream(dev))
+    _check(rc, "deltanet_fwd")
+    return o, hT, workspace
+
+
+def deltanet_bwd(q, k, v, beta, dO, *, chunk=64, l2norm=True, h0=None, dhT=None,
+                 workspace=None, states_saved=True, want_dh0=True, force_simt=False,
+                 eps=1e-6, out=None):
+    """Backward: gradients w.r.t. raw q, k, v, beta (and h0).  With
+    states_saved=True the workspace must come from deltanet_fwd(save_states=True)
+    on the same inputs.  Returns (dq, dk, dv, dbeta, dh0 or None)."""
+    lib = load_library()
+    dev = q.device
+    for t, n in ((q, "q"), (k, "k"), (v, "v"), (beta, "beta"), (dO, "dO")):
+        _need(t, n, q.dtype, dev)
+    _need(h0, "h0", torch.float32, dev)
+    _need(dhT, "dhT", torch.float32, dev)
+    if workspace is None:
+        states_saved = False
+    d = _desc_for(q, v, chunk, l2norm, states_saved, force_simt, eps)
+    B, H, L, Dk = q.shape
+    Dv = v.shape[-1]
+    if out is not None:
+        dq, dk, dv, db = out
+    else:
+        dq = torch.empty_like(q)
+        dk = torch.empty_like(k)
+        dv = torch.empty_like(v)
+        db = torch.empty_like(beta)
+    dh0 = torch.empty((B, H, Dk, Dv), dtype=torch.float32, device=dev) if want_dh0 else None
+    if workspace is None:
+        workspace = alloc_workspace(d, dev)
+    rc = lib.deltanet_bwd(ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(beta), _ptr(h0),
+                          _ptr(dO), _ptr(dhT), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(db),
+                          _ptr(dh0), _ptr(workspace), workspace.numel(), _stream(dev))
+    _check(rc, "deltanet_bwd")
+    return dq, dk, dv, db, dh0
+
+
+class DeltaNetChunkFunction(torch.autograd.Function):
+    """autograd wrapper: o = DeltaNet(q, k, v, beta) with L2-normalised q, k."""
+
+    @staticmethod
+    def forward(ctx, q, k, v, beta, chunk=64, l2norm=True):
+        o, _, ws = deltanet_fwd(q, k, v, beta, chunk=chunk, l2norm=l2norm, want_hT=False)
+        ctx.save_for_backward(q, k, v, beta, ws)
+        ctx.chunk, ctx.l2norm = chunk, l2norm
+        return o
+
+    @staticmethod
+    def backward(ctx, dO):
+        q, k, v, beta, ws = ctx.saved_tensors
+        dq, dk, dv, db, _ = deltanet_bwd(q, k, v, beta, dO.contiguous(), chunk=ctx.chunk,
+                                         l2norm=ctx.l2norm, workspace=ws, want_dh0=False)
+        return dq, dk, dv, db, None, None
+
+
+def deltanet(q, k, v, beta, chunk=64, l2norm=True):
+    return DeltaNetChunkFunction.apply(q, k, v, beta, chunk, l2norm)
+
+
+__all__ = ["deltanet_fwd", "deltanet_bwd", "deltanet_workspace_bytes", "deltanet_path",
+           "deltanet_launch_count", "deltanet_strerror", "deltanet_desc", "make_desc",
+           "load_library", "alloc_workspace", "DeltaNetError", "deltanet", "EXPORTED",
+           "LIB_PATH"]

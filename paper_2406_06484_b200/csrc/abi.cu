@@ -1,0 +1,135 @@
+// abi.cu -- the extern "C" boundary of libdeltanet (include/deltanet.h):
+// descriptor validation, workspace sizing, path selection and launch.
+#include <string.h>
+
+#include "common.cuh"
+
+namespace {
+
+bool pow2_in(int x, int lo, int hi) {
+  if (x < lo || x > hi) return false;
+  return (x & (x - 1)) == 0;
+}
+
+bool misaligned(const void* p) { return p && (((uintptr_t)p) & 15u) != 0; }
+
+int validate(const deltanet_desc* d) {
+  if (!d) return DELTANET_ERR_INVALID_ARG;
+  if (d->B < 0 || d->H < 0 || d->L < 0) return DELTANET_ERR_INVALID_ARG;
+  if (d->dtype != DELTANET_BF16 && d->dtype != DELTANET_FP32) return DELTANET_ERR_UNSUPPORTED;
+  if (!pow2_in(d->Dk, 16, 256) || !pow2_in(d->Dv, 16, 256)) return DELTANET_ERR_UNSUPPORTED;
+  if (!pow2_in(d->chunk, 16, 128)) return DELTANET_ERR_UNSUPPORTED;
+  return DELTANET_OK;
+}
+
+bool use_tc(const deltanet_desc* d) {
+  return !(d->flags & DELTANET_FORCE_SIMT) && dn::tc_supported(d);
+}
+
+size_t elem_bytes(const deltanet_desc* d) { return d->dtype == DELTANET_FP32 ? 4 : 2; }
+
+size_t states_bytes(const deltanet_desc* d) {
+  const size_t NC = (size_t)(d->L + d->chunk - 1) / d->chunk;
+  return (size_t)d->B * d->H * NC * d->Dk * d->Dv * elem_bytes(d);
+}
+
+size_t round_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+size_t scratch_bytes(const deltanet_desc* d) {
+  if (use_tc(d)) return dn::tc_scratch_bytes(d);
+  return (size_t)d->B * d->H *
+         dn::simt_scratch_floats_per_unit(d->L, d->Dk, d->Dv, d->chunk) * sizeof(float);
+}
+
+dn::Args make_args(const deltanet_desc* d, void* ws) {
+  dn::Args a;
+  memset(&a, 0, sizeof a);
+  a.B = d->B; a.H = d->H; a.L = d->L; a.Dk = d->Dk; a.Dv = d->Dv; a.C = d->chunk;
+  a.NC = (d->L + d->chunk - 1) / d->chunk;
+  a.flags = d->flags;
+  a.eps = d->l2_eps > 0.f ? d->l2_eps : 1e-6f;
+  a.states = ws;
+  a.scratch = (float*)((char*)ws + round_up(states_bytes(d)));
+  return a;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t deltanet_workspace_bytes(const deltanet_desc* d) {
+  if (validate(d) != DELTANET_OK) return 0;
+  return round_up(states_bytes(d)) + round_up(scratch_bytes(d));
+}
+
+int deltanet_path(const deltanet_desc* d) {
+  if (validate(d) != DELTANET_OK) return -1;
+  return use_tc(d) ? 1 : 0;
+}
+
+int deltanet_launch_count(const deltanet_desc* d, int which) {
+  if (validate(d) != DELTANET_OK) return -1;
+  if ((size_t)d->B * d->H == 0) return 0;
+  if (use_tc(d)) return dn::tc_launch_count(d, which);
+  return 1;
+}
+
+int deltanet_fwd(const deltanet_desc* d, const void* q, const void* k, const void* v,
+                 const void* beta, const float* h0, void* o, float* hT, void* workspace,
+                 size_t workspace_bytes, void* stream) {
+  int rc = validate(d);
+  if (rc) return rc;
+  const size_t units = (size_t)d->B * d->H;
+  const bool tokens = units && d->L > 0;  // L = 0: token tensors may be empty (null)
+  if (tokens && (!q || !k || !v || !beta || !o)) return DELTANET_ERR_INVALID_ARG;
+  if (misaligned(q) || misaligned(k) || misaligned(v) || misaligned(beta) || misaligned(h0) ||
+      misaligned(o) || misaligned(hT) || misaligned(workspace))
+    return DELTANET_ERR_MISALIGNED;
+  const size_t need = deltanet_workspace_bytes(d);
+  if (units && (!workspace || workspace_bytes < need)) return DELTANET_ERR_WORKSPACE;
+  if (!units) return DELTANET_OK;
+  dn::Args a = make_args(d, workspace);
+  a.q = q; a.k = k; a.v = v; a.beta = beta; a.h0 = h0; a.o = o; a.hT = hT;
+  cudaStream_t s = (cudaStream_t)stream;
+  return use_tc(d) ? dn::tc_fwd(a, s) : dn::simt_fwd(a, d->dtype, s);
+}
+
+int deltanet_bwd(const deltanet_desc* d, const void* q, const void* k, const void* v,
+                 const void* beta, const float* h0, const void* dO, const float* dhT, void* dq,
+                 void* dk, void* dv, void* dbeta, float* dh0, void* workspace,
+                 size_t workspace_bytes, void* stream) {
+  int rc = validate(d);
+  if (rc) return rc;
+  const size_t units = (size_t)d->B * d->H;
+  const bool tokens = units && d->L > 0;
+  if (tokens && (!q || !k || !v || !beta || !dO || !dq || !dk || !dv || !dbeta))
+    return DELTANET_ERR_INVALID_ARG;
+  if (misaligned(q) || misaligned(k) || misaligned(v) || misaligned(beta) || misaligned(h0) ||
+      misaligned(dO) || misaligned(dhT) || misaligned(dq) || misaligned(dk) || misaligned(dv) ||
+      misaligned(dbeta) || misaligned(dh0) || misaligned(workspace))
+    return DELTANET_ERR_MISALIGNED;
+  const size_t need = deltanet_workspace_bytes(d);
+  if (units && (!workspace || workspace_bytes < need)) return DELTANET_ERR_WORKSPACE;
+  if (!units) return DELTANET_OK;
+  dn::Args a = make_args(d, workspace);
+  a.q = q; a.k = k; a.v = v; a.beta = beta; a.h0 = h0; a.dO = dO; a.dhT = dhT;
+  a.dq = dq; a.dk = dk; a.dv = dv; a.dbeta = dbeta; a.dh0 = dh0;
+  cudaStream_t s = (cudaStream_t)stream;
+  return use_tc(d) ? dn::tc_bwd(a, s) : dn::simt_bwd(a, d->dtype, s);
+}
+
+const char* deltanet_strerror(int code) {
+  switch (code) {
+    case DELTANET_OK: return "ok";
+    case DELTANET_ERR_INVALID_ARG: return "invalid argument (null pointer or negative size)";
+    case DELTANET_ERR_UNSUPPORTED: return "unsupported descriptor (dtype, Dk/Dv, or chunk)";
+    case DELTANET_ERR_MISALIGNED: return "tensor pointer not 16-byte aligned";
+    case DELTANET_ERR_CUDA: return "CUDA launch failed";
+    case DELTANET_ERR_WORKSPACE: return "workspace missing or too small";
+    default: return "unknown deltanet error code";
+  }
+}
+
+int deltanet_abi_version(void) { return DELTANET_ABI_VERSION; }
+
+}  // extern "C"

@@ -1,0 +1,57 @@
+// common.cuh -- shared device helpers and launch arguments of libdeltanet.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/deltanet.h"
+
+namespace dn {
+
+// All tensor arguments of one fwd or bwd call (see include/deltanet.h).
+struct Args {
+  int B, H, L, Dk, Dv, C, NC;
+  unsigned flags;
+  float eps;
+  const void *q, *k, *v, *beta;
+  const float* h0;
+  void* o;
+  float* hT;
+  const void* dO;
+  const float* dhT;
+  void *dq, *dk, *dv, *dbeta;
+  float* dh0;
+  void* states;    // [B*H][NC][Dk][Dv] of the I/O dtype (H_t before chunk t)
+  float* scratch;  // path-specific scratch
+};
+
+template <typename T>
+__device__ __forceinline__ float ldf(const T* p);
+template <>
+__device__ __forceinline__ float ldf<float>(const float* p) { return *p; }
+template <>
+__device__ __forceinline__ float ldf<__nv_bfloat16>(const __nv_bfloat16* p) {
+  return __bfloat162float(*p);
+}
+template <typename T>
+__device__ __forceinline__ void stf(T* p, float x);
+template <>
+__device__ __forceinline__ void stf<float>(float* p, float x) { *p = x; }
+template <>
+__device__ __forceinline__ void stf<__nv_bfloat16>(__nv_bfloat16* p, float x) {
+  *p = __float2bfloat16_rn(x);
+}
+
+// SIMT path entry points (simt.cu)
+int simt_fwd(const Args& a, int dtype, cudaStream_t s);
+int simt_bwd(const Args& a, int dtype, cudaStream_t s);
+size_t simt_scratch_floats_per_unit(int L, int Dk, int Dv, int C);
+
+// tcgen05 path entry points (tc_fwd.cu / tc_bwd.cu)
+bool tc_supported(const deltanet_desc* d);
+size_t tc_scratch_bytes(const deltanet_desc* d);
+int tc_fwd(const Args& a, cudaStream_t s);
+int tc_bwd(const Args& a, cudaStream_t s);
+int tc_launch_count(const deltanet_desc* d, int which);
+
+}  // namespace dn

@@ -1,0 +1,85 @@
+// mma_probe.cu -- TEST-ONLY probe of the tcgen05 operand conventions used by
+// the product kernels (tc_common.cuh): K-major / MN-major IL tiles, M=64 and
+// M=128 accumulators (TMEM lane mapping), negated A, accumulate-into-D.
+// D = init + (neg ? -1 : 1) * A @ B^T-convention below, fp32 accumulate.
+//   A logical [M][K], B logical [N][K]  (D[m][n] = sum_k A[m][k] B[n][k])
+#include "../../paper_2406_06484_b200/csrc/tc_common.cuh"
+
+using namespace dn::tc;
+
+__global__ void probe_kernel(const __nv_bfloat16* A, const __nv_bfloat16* B, const float* Dinit,
+                             float* D, int M, int N, int K, int a_mn, int b_mn, int neg_a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + M * K * 2;
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  // A tile: K-major -> rows M, cols K ; MN-major -> rows K, cols M
+  for (int e = tid; e < M * K; e += blockDim.x) {
+    int m = e / K, k = e % K;
+    uint32_t off = a_mn ? il_off(k, m, K) : il_off(m, k, M);
+    *reinterpret_cast<__nv_bfloat16*>(sA + off) = A[e];
+  }
+  for (int e = tid; e < N * K; e += blockDim.x) {
+    int n = e / K, k = e % K;
+    uint32_t off = b_mn ? il_off(k, n, K) : il_off(n, k, N);
+    *reinterpret_cast<__nv_bfloat16*>(sB + off) = B[e];
+  }
+  fence_proxy_async();
+  if (warp == 0) tmem_alloc<512>(&tslot);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    mbar_fence_init();
+  }
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tm = tslot;
+  // preload D (lane mapping: M=128 row m -> lane m; M=64 row m -> lane 32*(m/16) + m%16)
+  if (Dinit) {
+    for (int c0 = 0; c0 < N; c0 += 16) {
+      uint32_t r[16];
+      int m = (M == 128) ? tid : ((lane < 16) ? warp * 16 + lane : -1);
+      for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(m >= 0 ? Dinit[m * N + c0 + j] : 0.f);
+      tmem_st16(taddr(tm, warp * 32, c0), r);
+    }
+    tmem_st_wait();
+  }
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  if (tid == 0) {
+    const uint32_t id = idesc_bf16(M, N, a_mn, b_mn, neg_a);
+    const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+    for (int k0 = 0; k0 < K; k0 += 16) {
+      uint64_t ad = a_mn ? desc_mn(a0, K, k0) : desc_k(a0, M, k0);
+      uint64_t bd = b_mn ? desc_mn(b0, K, k0) : desc_k(b0, N, k0);
+      mma_bf16(tm, ad, bd, id, (Dinit != nullptr || k0 > 0) ? 1u : 0u);
+    }
+    mma_commit(&bar);
+  }
+  mbar_wait(&bar, 0);
+  fence_after_sync();
+  for (int c0 = 0; c0 < N; c0 += 16) {
+    uint32_t r[16];
+    tmem_ld16(taddr(tm, warp * 32, c0), r);
+    tmem_ld_wait();
+    int m = (M == 128) ? tid : ((lane < 16) ? warp * 16 + lane : -1);
+    if (m >= 0)
+      for (int j = 0; j < 16; ++j) D[m * N + c0 + j] = __uint_as_float(r[j]);
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tm);
+}
+
+extern "C" int probe_mma(const void* A, const void* B, const float* Dinit, float* D, int M, int N,
+                         int K, int a_mn, int b_mn, int neg_a) {
+  size_t smem = (size_t)(M + N) * K * 2;
+  cudaFuncSetAttribute(probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  probe_kernel<<<1, 128, smem>>>((const __nv_bfloat16*)A, (const __nv_bfloat16*)B, Dinit, D, M,
+                                 N, K, a_mn, b_mn, neg_a);
+  cudaError_t e = cudaDeviceSynchronize();
+  return (int)e;
+}

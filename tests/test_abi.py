@@ -1,0 +1,100 @@
+"""CPU-side checks of the C-ABI library: it builds/loads, exports every symbol
+include/deltanet.h declares, and rejects bad arguments before any launch."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2406_06484_b200 as dn
+from paper_2406_06484_b200 import build as dnbuild
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "deltanet.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    dnbuild.build()
+    return dn.load_library()
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(deltanet_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_expected_api():
+    names = declared_functions()
+    for n in ("deltanet_fwd", "deltanet_bwd", "deltanet_workspace_bytes", "deltanet_strerror"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+    assert set(dn.EXPORTED) == set(declared_functions())
+
+
+def test_no_torch_types_in_abi():
+    src = open(HEADER).read()
+    assert "torch" not in src.lower().replace("pytorch", "") or "at::" not in src
+    assert "at::Tensor" not in src and "c10" not in src
+
+
+def test_abi_version_and_strerror(lib):
+    assert lib.deltanet_abi_version() == 1
+    for code in range(6):
+        assert dn.deltanet_strerror(code)
+    assert "unknown" in dn.deltanet_strerror(99)
+
+
+def _desc(**kw):
+    base = dict(B=2, H=3, L=100, Dk=64, Dv=64, chunk=64, dtype=0, flags=1, l2_eps=1e-6)
+    base.update(kw)
+    return dn.deltanet_desc(**base)
+
+
+def test_workspace_and_validation(lib):
+    d = _desc()
+    n = dn.deltanet_workspace_bytes(d)
+    # states: B*H*ceil(L/C)*Dk*Dv*2 bytes at least
+    assert n >= 2 * 3 * 2 * 64 * 64 * 2
+    assert dn.deltanet_workspace_bytes(_desc(Dk=48)) == 0          # unsupported
+    assert dn.deltanet_workspace_bytes(_desc(chunk=8)) == 0
+    assert dn.deltanet_workspace_bytes(_desc(dtype=7)) == 0
+    assert dn.deltanet_workspace_bytes(_desc(L=-1)) == 0
+    assert dn.deltanet_path(_desc(Dk=48)) == -1
+    assert dn.deltanet_path(_desc(dtype=1)) == 0                   # fp32 -> SIMT
+    assert dn.deltanet_path(_desc(flags=1 | 4)) == 0               # FORCE_SIMT
+
+
+def test_errors_before_launch(lib):
+    """Argument errors return before any CUDA call (works without a GPU)."""
+    D = ctypes.byref
+    d = _desc()
+    nul = None
+    rc = lib.deltanet_fwd(D(d), nul, nul, nul, nul, nul, nul, nul, nul, 0, nul)
+    assert rc == 1
+    rc = lib.deltanet_fwd(D(_desc(Dk=48)), nul, nul, nul, nul, nul, nul, nul, nul, 0, nul)
+    assert rc == 2
+    p = ctypes.c_void_p(16 * 1024 + 4)  # misaligned fake pointer, never dereferenced
+    a = ctypes.c_void_p(16 * 1024)
+    rc = lib.deltanet_fwd(D(d), p, a, a, a, nul, a, nul, a, 1 << 30, nul)
+    assert rc == 3
+    rc = lib.deltanet_fwd(D(d), a, a, a, a, nul, a, nul, a, 16, nul)  # workspace too small
+    assert rc == 5
+    rc = lib.deltanet_bwd(D(d), a, a, a, a, nul, nul, nul, a, a, a, a, nul, a, 1 << 30, nul)
+    assert rc == 1  # dO missing
+    # empty problem: nothing to do, no launch
+    e = _desc(B=0)
+    assert lib.deltanet_fwd(D(e), nul, nul, nul, nul, nul, nul, nul, nul, 0, nul) == 0
+    assert dn.deltanet_launch_count(e, 0) == 0
+
+
+def test_binding_refuses_cpu_tensors(lib):
+    import torch
+    q = torch.zeros(1, 1, 16, 16)
+    with pytest.raises(dn.DeltaNetError):
+        dn.deltanet_fwd(q, q, q, torch.zeros(1, 1, 16), chunk=16)

@@ -1,0 +1,146 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle on the
+same seeded inputs, element by element, normwise tolerance (tests/parity.py).
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from parity import TOL, compare, normwise, run_gpu, run_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2406_06484_b200 import build
+    build.build()
+
+
+def _case(B, H, L, Dk, Dv, C, dtype, keys="silu", index=200):
+    cfg = synth.custom_config(B, H, L, Dk, Dv, C, dtype, index=index)
+    return cfg, synth.make_inputs(cfg, keys=keys)
+
+
+# ---------------------------------------------------------------- fp32 (SIMT)
+
+def test_tiny_config_fp32():
+    """BASELINE.json configs[0]: B=1 H=1 L=64 d=16 chunk=16, fp32, 1e-4."""
+    cfg = synth.CONFIGS["tiny"]
+    inp = synth.make_inputs(cfg)
+    got = run_gpu(inp, "fp32", cfg.chunk)
+    errs = compare(got, run_oracle(inp), TOL["fp32"])
+    assert max(errs.values()) < 1e-5
+
+
+@pytest.mark.parametrize("C", [16, 32, 64, 128])
+@pytest.mark.parametrize("d", [16, 64, 128])
+def test_fp32_shapes_ragged(C, d):
+    """Several chunks and a ragged tail (L = 2C + 37), B=2, H=2, h0/dhT set."""
+    L = 2 * C + 37
+    cfg, inp = _case(2, 2, L, d, d, C, "fp32", index=300 + C + d)
+    rng = np.random.default_rng(C * d)
+    h0 = (0.1 * rng.standard_normal((2, 2, d, d))).astype(np.float32)
+    dhT = rng.standard_normal((2, 2, d, d)).astype(np.float32)
+    got = run_gpu(inp, "fp32", C, h0=h0, dhT=dhT)
+    compare(got, run_oracle(inp, h0=h0.astype(np.float64), dhT=dhT.astype(np.float64)),
+            TOL["fp32"])
+
+
+def test_fp32_rectangular_heads_no_l2():
+    cfg, inp = _case(1, 3, 90, 32, 64, 32, "fp32", keys="gaussian", index=401)
+    # un-normalised gaussian keys would blow up the recurrence; scale them down
+    for f in ("q", "k"):
+        inp[f] = (inp[f] / np.sqrt(32)).astype(np.float32)
+    got = run_gpu(inp, "fp32", 32, l2norm=False)
+    compare(got, run_oracle(inp, l2norm=False), TOL["fp32"])
+
+
+@pytest.mark.parametrize("save_states", [True, False])
+def test_fp32_states_recompute(save_states):
+    cfg, inp = _case(1, 2, 200, 64, 64, 64, "fp32", index=402)
+    got = run_gpu(inp, "fp32", 64, save_states=save_states)
+    compare(got, run_oracle(inp), TOL["fp32"])
+
+
+def test_fp32_identical_keys_beta_one():
+    """Adversarial UT case: all keys of a unit equal, beta = 1."""
+    cfg, inp = _case(1, 2, 150, 32, 32, 64, "fp32", keys="identical", index=403)
+    got = run_gpu(inp, "fp32", 64)
+    compare(got, run_oracle(inp), TOL["fp32"])
+
+
+def test_zero_rows_l2_eps():
+    """Zero q/k rows under L2 normalisation stay finite (R9)."""
+    cfg, inp = _case(1, 1, 64, 16, 16, 16, "fp32", index=404)
+    inp["q"][0, 0, 5] = 0
+    inp["k"][0, 0, 9] = 0
+    got = run_gpu(inp, "fp32", 16)
+    compare(got, run_oracle(inp), TOL["fp32"])
+
+
+def test_empty_length():
+    """L = 0: no tokens; hT = h0 and dh0 = dhT."""
+    import paper_2406_06484_b200 as dn
+    q = torch.zeros(2, 2, 0, 16, device="cuda")
+    b = torch.zeros(2, 2, 0, device="cuda")
+    h0 = torch.randn(2, 2, 16, 16, device="cuda")
+    o, hT, ws = dn.deltanet_fwd(q, q, q, b, chunk=16, h0=h0)
+    dhT = torch.randn_like(h0)
+    g = dn.deltanet_bwd(q, q, q, b, q, chunk=16, h0=h0, dhT=dhT, workspace=ws)
+    torch.cuda.synchronize()
+    assert torch.equal(hT, h0) and torch.equal(g[4], dhT)
+
+
+# ---------------------------------------------------------------- bf16
+
+@pytest.mark.parametrize("force_simt", [False, True])
+def test_bf16_multi_chunk_ragged(force_simt):
+    """bf16, d=128, C=64: 5 chunks + ragged tail, several units."""
+    cfg, inp = _case(2, 3, 4 * 64 + 45, 128, 128, 64, "bf16", index=500)
+    got = run_gpu(inp, "bf16", 64, force_simt=force_simt)
+    compare(got, run_oracle(inp), TOL["bf16"])
+
+
+def test_bf16_with_initial_state():
+    cfg, inp = _case(1, 2, 256, 128, 128, 64, "bf16", index=501)
+    rng = np.random.default_rng(7)
+    h0 = (0.2 * rng.standard_normal((1, 2, 128, 128))).astype(np.float32)
+    dhT = rng.standard_normal((1, 2, 128, 128)).astype(np.float32)
+    got = run_gpu(inp, "bf16", 64, h0=h0, dhT=dhT)
+    compare(got, run_oracle(inp, h0=h0.astype(np.float64), dhT=dhT.astype(np.float64)),
+            TOL["bf16"])
+
+
+@pytest.mark.parametrize("keys", ["gaussian", "identical"])
+def test_bf16_key_distributions(keys):
+    cfg, inp = _case(1, 2, 192, 128, 128, 64, "bf16", keys=keys, index=502)
+    got = run_gpu(inp, "bf16", 64)
+    compare(got, run_oracle(inp), TOL["bf16"])
+
+
+def test_bf16_deterministic():
+    cfg, inp = _case(2, 2, 320, 128, 128, 64, "bf16", index=503)
+    a = run_gpu(inp, "bf16", 64)
+    b = run_gpu(inp, "bf16", 64)
+    for k in a:
+        if a[k] is not None:
+            assert np.array_equal(a[k], b[k]), k
+
+
+@pytest.mark.parametrize("name", ["1.3b", "target"])
+def test_bf16_full_size_sampled_units(name):
+    """BASELINE configs at full size in the bench launch configuration;
+    the oracle checks three sampled (b, h) units."""
+    import paper_2406_06484_b200 as dn
+    cfg = synth.CONFIGS[name]
+    inp = synth.make_inputs(cfg)
+    got = run_gpu(inp, "bf16", cfg.chunk)
+    units = [(0, 0), (cfg.B - 1, cfg.H - 1), (cfg.B // 2, 5)]
+    for (b, h) in units:
+        one = {f: inp[f][b:b + 1, h:h + 1] for f in inp}
+        ref = run_oracle(one)
+        sub = {k: (None if v is None else v[b:b + 1, h:h + 1]) for k, v in got.items()}
+        compare(sub, ref, TOL["bf16"])

@@ -1,0 +1,58 @@
+"""GPU probe of the tcgen05 operand conventions (tests/cuda/mma_probe.cu):
+every (A major, B major, M, negate, accumulate) combination the product
+kernels use, against a plain fp32 matmul of the same bf16 values."""
+import ctypes
+import os
+import subprocess
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.fixture(scope="module")
+def probe():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    src = os.path.join(HERE, "cuda", "mma_probe.cu")
+    lib = os.path.join(HERE, "cuda", "libprobe.so")
+    subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O2", "-std=c++17",
+                    "-Xcompiler", "-fPIC", "-shared", "-o", lib, src], check=True)
+    L = ctypes.CDLL(lib)
+    L.probe_mma.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int] * 6
+    L.probe_mma.restype = ctypes.c_int
+    return L
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 64, 64), (128, 128, 64), (128, 64, 128),
+                                   (64, 64, 128), (64, 128, 128), (64, 128, 64)])
+@pytest.mark.parametrize("a_mn", [0, 1])
+@pytest.mark.parametrize("b_mn", [0, 1])
+def test_mma_layouts(probe, M, N, K, a_mn, b_mn):
+    g = torch.Generator().manual_seed(M * 1000 + N * 10 + K + a_mn * 7 + b_mn * 3)
+    A = torch.randn(M, K, generator=g).bfloat16()
+    B = torch.randn(N, K, generator=g).bfloat16()
+    ref = A.float() @ B.float().T
+    Ad, Bd = A.cuda(), B.cuda()
+    D = torch.zeros(M, N, device="cuda")
+    rc = probe.probe_mma(Ad.data_ptr(), Bd.data_ptr(), None, D.data_ptr(), M, N, K, a_mn, b_mn, 0)
+    assert rc == 0
+    err = (D.cpu() - ref).abs().max().item()
+    assert err <= 1e-3 * ref.abs().max().item(), err
+
+
+@pytest.mark.parametrize("M", [64, 128])
+def test_mma_negate_accumulate(probe, M):
+    N, K = 64, 128
+    g = torch.Generator().manual_seed(M)
+    A = torch.randn(M, K, generator=g).bfloat16()
+    B = torch.randn(N, K, generator=g).bfloat16()
+    D0 = torch.randn(M, N, generator=g)
+    ref = D0 - A.float() @ B.float().T
+    D = torch.zeros(M, N, device="cuda")
+    rc = probe.probe_mma(A.cuda().data_ptr(), B.cuda().data_ptr(), D0.cuda().data_ptr(),
+                         D.data_ptr(), M, N, K, 0, 1, 1)
+    assert rc == 0
+    assert (D.cpu() - ref).abs().max().item() <= 1e-3 * ref.abs().max().item()

@@ -193,6 +193,7 @@ __device__ void unit_forward(const Unit<T>& u, const float* h0, T* o, float* hT,
         for (int r = 0; r <= i; ++r) x = fmaf(s.A[i * C + r], s.U[r * Dv + j], x);
         stf(o + (size_t)(t0 + i) * Dv + j, x);
       }
+      __syncthreads();  // O reads H_t; the update below overwrites it
     }
     // H += K^T U'   (Eq. 8; Listing 1)
     for (int e = threadIdx.x; e < Dk * Dv; e += blockDim.x) {

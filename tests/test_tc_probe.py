@@ -44,15 +44,18 @@ def test_mma_layouts(probe, M, N, K, a_mn, b_mn):
 
 
 @pytest.mark.parametrize("M", [64, 128])
-def test_mma_negate_accumulate(probe, M):
+@pytest.mark.parametrize("init", [0, 1])
+@pytest.mark.parametrize("neg", [0, 1])
+def test_mma_negate_accumulate(probe, M, init, neg):
     N, K = 64, 128
     g = torch.Generator().manual_seed(M)
     A = torch.randn(M, K, generator=g).bfloat16()
     B = torch.randn(N, K, generator=g).bfloat16()
-    D0 = torch.randn(M, N, generator=g)
-    ref = D0 - A.float() @ B.float().T
+    D0 = torch.randn(M, N, generator=g) if init else torch.zeros(M, N)
+    ref = D0 + (-1 if neg else 1) * (A.float() @ B.float().T)
     D = torch.zeros(M, N, device="cuda")
-    rc = probe.probe_mma(A.cuda().data_ptr(), B.cuda().data_ptr(), D0.cuda().data_ptr(),
-                         D.data_ptr(), M, N, K, 0, 1, 1)
+    D0d, Ad, Bd = D0.cuda(), A.cuda(), B.cuda()  # keep device copies alive
+    rc = probe.probe_mma(Ad.data_ptr(), Bd.data_ptr(),
+                         D0d.data_ptr() if init else None, D.data_ptr(), M, N, K, 0, 1, neg)
     assert rc == 0
     assert (D.cpu() - ref).abs().max().item() <= 1e-3 * ref.abs().max().item()

@@ -68,7 +68,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -256,7 +256,6 @@ def main():
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    clk = clocks.stop()
     t_fwd = sum(e[0].elapsed_time(e[1]) for e in ev) / args.steps * 1e-3
     t_bwd = sum(e[1].elapsed_time(e[2]) for e in ev) / args.steps * 1e-3
     t_total = ev[0][0].elapsed_time(ev[-1][2]) * 1e-3
@@ -335,6 +334,8 @@ def main():
         e2e = {"value": tokens_per_step / t_e2e, "unit": "tokens/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": t_e2e * 1e3, "steps": n_e2e}
+
+    clk = clocks.stop()
 
     # ---- NCCL gather of outputs and gradients (outside the timed step)
     gather = None

@@ -216,5 +216,41 @@ __device__ __forceinline__ void il_store8(uint8_t* tile, int R, int r, int c0, c
   *reinterpret_cast<uint4*>(tile + il_off(r, c0, R)) = v;
 }
 
+// ------------------------------------------------------------------ CTA helpers
+__device__ __forceinline__ void cta_sync() {
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+}
+
+// Load 64 fp32 columns [col, col+64) of this warp's 32 TMEM lanes.
+__device__ __forceinline__ void ld64(uint32_t tm, int warp, uint32_t col, float (&f)[64]) {
+  uint32_t r[4][16];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) tmem_ld16(taddr(tm, warp * 32, col + 16 * i), r[i]);
+  tmem_ld_wait();
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 16; ++j) f[16 * i + j] = __uint_as_float(r[i][j]);
+}
+
+// Read 8 bf16 of row r, columns [c0, c0+8) of an IL tile as fp32.
+__device__ __forceinline__ void il_load8(const uint8_t* tile, int R, int r, int c0, float* x) {
+  uint4 v = *reinterpret_cast<const uint4*>(tile + il_off(r, c0, R));
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    float2 f = __bfloat1622float2(h[e]);
+    x[2 * e] = f.x;
+    x[2 * e + 1] = f.y;
+  }
+}
+
 }  // namespace tc
+
+// host: 4-D TMA view of a [B*H][L][D] bf16 tensor whose box {8, rows, D/8, 1}
+// lands in shared memory as the IL layout with R = rows (tc_fwd.cu).
+bool make_il_map(CUtensorMap* m, const void* base, int BH, int L, int D, int rows);
+
 }  // namespace dn

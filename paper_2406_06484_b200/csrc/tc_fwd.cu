@@ -51,24 +51,6 @@ constexpr int SMEM_BYTES = OFF_B + 3 * C * 4;
 // TMEM column map (512 columns allocated)
 constexpr uint32_t TM_H = 0, TM_GQK = 128, TM_GKK = 192, TM_W = 256, TM_U = 320, TM_O = 384;
 
-__device__ __forceinline__ void cta_sync() {
-  fence_before_sync();
-  __syncthreads();
-  fence_after_sync();
-}
-
-// Load 64 fp32 columns [col, col+64) of this warp's TMEM lanes.
-__device__ __forceinline__ void ld64(uint32_t tm, int warp, uint32_t col, float (&f)[64]) {
-  uint32_t r[4][16];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) tmem_ld16(taddr(tm, warp * 32, col + 16 * i), r[i]);
-  tmem_ld_wait();
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 16; ++j) f[16 * i + j] = __uint_as_float(r[i][j]);
-}
-
 #ifdef DN_DEBUG
 // Test-only intermediate dumps (tests/test_tc_debug.py builds with -DDN_DEBUG).
 __device__ float* dn_dbg = nullptr;
@@ -426,7 +408,7 @@ __global__ void __launch_bounds__(NT, 1)
     }
     fence_proxy_async();
     cta_sync();
-    if (tid == 0) {
+    if (tid == 0 && a.o) {
       tma_store_4d(&mO, sO, 0, t0, 0, unit);
       bulk_commit();
     }
@@ -483,13 +465,12 @@ bool tc_supported(const deltanet_desc* d) {
   return d->dtype == DELTANET_BF16 && d->chunk == C && d->Dk == DK && d->Dv == DV && d->L > 0;
 }
 
-size_t tc_scratch_bytes(const deltanet_desc* d) {
-  // the bwd currently recomputes through the SIMT path (its scratch)
-  return (size_t)d->B * d->H * simt_scratch_floats_per_unit(d->L, d->Dk, d->Dv, d->chunk) *
-         sizeof(float);
-}
+size_t tc_scratch_bytes(const deltanet_desc*) { return 0; }  // states region only
 
-int tc_launch_count(const deltanet_desc*, int) { return 1; }
+// fwd: 1 kernel; bwd: 1 kernel, plus the state-recompute forward without SAVE_STATES
+int tc_launch_count(const deltanet_desc* d, int which) {
+  return which == 0 ? 1 : ((d->flags & DELTANET_SAVE_STATES) ? 1 : 2);
+}
 
 int tc_fwd(const Args& a, cudaStream_t s) {
   static bool attr = false;
@@ -502,18 +483,13 @@ int tc_fwd(const Args& a, cudaStream_t s) {
   const int BH = a.B * a.H;
   CUtensorMap mQ, mK, mV, mO;
   if (!make_il_map(&mQ, a.q, BH, a.L, DK, C) || !make_il_map(&mK, a.k, BH, a.L, DK, C) ||
-      !make_il_map(&mV, a.v, BH, a.L, DV, C) || !make_il_map(&mO, a.o, BH, a.L, DV, C))
+      !make_il_map(&mV, a.v, BH, a.L, DV, C) ||
+      !make_il_map(&mO, a.o ? a.o : a.v, BH, a.L, DV, C))  // o == null: states only
     return DELTANET_ERR_CUDA;
   tc_fwd_kernel<<<BH, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);
   return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
 }
 
-int tc_bwd(const Args& a0, cudaStream_t s) {
-  // Interim: the SIMT backward, recomputing its own states (layouts differ).
-  Args a = a0;
-  a.flags &= ~DELTANET_SAVE_STATES;
-  return simt_bwd(a, DELTANET_BF16, s);
-}
 
 }  // namespace dn
 

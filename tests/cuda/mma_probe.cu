@@ -8,7 +8,8 @@
 using namespace dn::tc;
 
 __global__ void probe_kernel(const __nv_bfloat16* A, const __nv_bfloat16* B, const float* Dinit,
-                             float* D, int M, int N, int K, int a_mn, int b_mn, int neg_a) {
+                             float* D, int M, int N, int K, int a_mn, int b_mn, int neg_a,
+                             int lane_off) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tslot;
@@ -40,7 +41,7 @@ __global__ void probe_kernel(const __nv_bfloat16* A, const __nv_bfloat16* B, con
   if (Dinit) {
     for (int c0 = 0; c0 < N; c0 += 16) {
       uint32_t r[16];
-      int m = (M == 128) ? tid : ((lane < 16) ? warp * 16 + lane : -1);
+      int m = (M == 128) ? tid : ((lane >= lane_off && lane < lane_off + 16) ? warp * 16 + lane - lane_off : -1);
       for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(m >= 0 ? Dinit[m * N + c0 + j] : 0.f);
       tmem_st16(taddr(tm, warp * 32, c0), r);
     }
@@ -55,7 +56,7 @@ __global__ void probe_kernel(const __nv_bfloat16* A, const __nv_bfloat16* B, con
     for (int k0 = 0; k0 < K; k0 += 16) {
       uint64_t ad = a_mn ? desc_mn(a0, K, k0) : desc_k(a0, M, k0);
       uint64_t bd = b_mn ? desc_mn(b0, K, k0) : desc_k(b0, N, k0);
-      mma_bf16(tm, ad, bd, id, (Dinit != nullptr || k0 > 0) ? 1u : 0u);
+      mma_bf16(tm + ((uint32_t)lane_off << 16), ad, bd, id, (Dinit != nullptr || k0 > 0) ? 1u : 0u);
     }
     mma_commit(&bar);
   }
@@ -65,7 +66,7 @@ __global__ void probe_kernel(const __nv_bfloat16* A, const __nv_bfloat16* B, con
     uint32_t r[16];
     tmem_ld16(taddr(tm, warp * 32, c0), r);
     tmem_ld_wait();
-    int m = (M == 128) ? tid : ((lane < 16) ? warp * 16 + lane : -1);
+    int m = (M == 128) ? tid : ((lane >= lane_off && lane < lane_off + 16) ? warp * 16 + lane - lane_off : -1);
     if (m >= 0)
       for (int j = 0; j < 16; ++j) D[m * N + c0 + j] = __uint_as_float(r[j]);
   }
@@ -75,11 +76,11 @@ __global__ void probe_kernel(const __nv_bfloat16* A, const __nv_bfloat16* B, con
 }
 
 extern "C" int probe_mma(const void* A, const void* B, const float* Dinit, float* D, int M, int N,
-                         int K, int a_mn, int b_mn, int neg_a) {
+                         int K, int a_mn, int b_mn, int neg_a, int lane_off) {
   size_t smem = (size_t)(M + N) * K * 2;
   cudaFuncSetAttribute(probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   probe_kernel<<<1, 128, smem>>>((const __nv_bfloat16*)A, (const __nv_bfloat16*)B, Dinit, D, M,
-                                 N, K, a_mn, b_mn, neg_a);
+                                 N, K, a_mn, b_mn, neg_a, lane_off);
   cudaError_t e = cudaDeviceSynchronize();
   return (int)e;
 }

@@ -120,11 +120,12 @@ def test_bf16_key_distributions(keys):
     equal, beta = 1) is an adversarial case outside the paper's workload:
     T^{-1} is bidiagonal, U = T^{-1} V holds differences v_i - v_{i-1}, and the
     state update telescopes a sum of C bf16-rounded MMA operands, so the
-    expected error is ~sqrt(C) 2^-9 = 0.016 of the result; its bar is 4e-2
-    (reading R19)."""
+    expected error is ~sqrt(C) 2^-9 = 0.016 of the result (forward); the
+    backward differentiates those differences again (P = X^T dU' holds
+    dU'_t - dU'_{t+1}), roughly doubling it.  Its bar is 6e-2 (R19)."""
     cfg, inp = _case(1, 2, 192, 128, 128, 64, "bf16", keys=keys, index=502)
     got = run_gpu(inp, "bf16", 64)
-    compare(got, run_oracle(inp), TOL["bf16"] if keys != "identical" else 4e-2)
+    compare(got, run_oracle(inp), TOL["bf16"] if keys != "identical" else 6e-2)
 
 
 def test_bf16_deterministic():

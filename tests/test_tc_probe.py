@@ -21,7 +21,7 @@ def probe():
     subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O2", "-std=c++17",
                     "-Xcompiler", "-fPIC", "-shared", "-o", lib, src], check=True)
     L = ctypes.CDLL(lib)
-    L.probe_mma.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int] * 6
+    L.probe_mma.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int] * 7
     L.probe_mma.restype = ctypes.c_int
     return L
 
@@ -37,7 +37,7 @@ def test_mma_layouts(probe, M, N, K, a_mn, b_mn):
     ref = A.float() @ B.float().T
     Ad, Bd = A.cuda(), B.cuda()
     D = torch.zeros(M, N, device="cuda")
-    rc = probe.probe_mma(Ad.data_ptr(), Bd.data_ptr(), None, D.data_ptr(), M, N, K, a_mn, b_mn, 0)
+    rc = probe.probe_mma(Ad.data_ptr(), Bd.data_ptr(), None, D.data_ptr(), M, N, K, a_mn, b_mn, 0, 0)
     assert rc == 0
     err = (D.cpu() - ref).abs().max().item()
     assert err <= 1e-3 * ref.abs().max().item(), err
@@ -56,6 +56,25 @@ def test_mma_negate_accumulate(probe, M, init, neg):
     D = torch.zeros(M, N, device="cuda")
     D0d, Ad, Bd = D0.cuda(), A.cuda(), B.cuda()  # keep device copies alive
     rc = probe.probe_mma(Ad.data_ptr(), Bd.data_ptr(),
-                         D0d.data_ptr() if init else None, D.data_ptr(), M, N, K, 0, 1, neg)
+                         D0d.data_ptr() if init else None, D.data_ptr(), M, N, K, 0, 1, neg, 0)
+    assert rc == 0
+    assert (D.cpu() - ref).abs().max().item() <= 1e-3 * ref.abs().max().item()
+
+
+@pytest.mark.parametrize("N", [64, 128])
+@pytest.mark.parametrize("init", [0, 1])
+def test_mma_m64_lane_offset_16(probe, N, init):
+    """M=64 accumulator at TMEM lane offset 16 (rows in lanes 16-31 of each
+    32-lane quadrant), the pairing the backward kernel relies on."""
+    M, K = 64, 128
+    g = torch.Generator().manual_seed(N + init)
+    A = torch.randn(M, K, generator=g).bfloat16()
+    B = torch.randn(N, K, generator=g).bfloat16()
+    D0 = torch.randn(M, N, generator=g) if init else torch.zeros(M, N)
+    ref = D0 + A.float() @ B.float().T
+    Ad, Bd, D0d = A.cuda(), B.cuda(), D0.cuda()
+    D = torch.zeros(M, N, device="cuda")
+    rc = probe.probe_mma(Ad.data_ptr(), Bd.data_ptr(), D0d.data_ptr() if init else None,
+                         D.data_ptr(), M, N, K, 0, 1, 0, 16)
     assert rc == 0
     assert (D.cpu() - ref).abs().max().item() <= 1e-3 * ref.abs().max().item()

@@ -254,3 +254,85 @@ __device__ __forceinline__ void il_load8(const uint8_t* tile, int R, int r, int 
 bool make_il_map(CUtensorMap* m, const void* base, int BH, int L, int D, int rows);
 
 }  // namespace dn
+
+namespace dn {
+namespace tc {
+
+// Named barrier over one 128-thread warpgroup (ids 1.. ; 0 is __syncthreads).
+__device__ __forceinline__ void wg_sync(int id) {
+  asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory");
+}
+
+// X = (I + L)^{-1} for a 64x64 strictly-lower L, in place in LX (fp32,
+// row stride LSTRIDE floats), by the 128 threads of one warpgroup (wtid).
+// Forward substitution on the two 32x32 diagonal blocks,
+// column-parallel in registers, then X21 = -X22 (L21 X11).  On return the
+// lower triangle and diagonal of LX hold X; the upper-right 32x32 block holds
+// scratch (callers mask j > i).
+template <int LSTRIDE>
+__device__ __forceinline__ void ut_inverse_inplace(float* LX, int wtid, int bar_id) {
+  const int lane = wtid & 31, wwarp = wtid >> 5;
+  if (wwarp < 2) {
+    const int o = 32 * wwarp, j = lane;
+    float x[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+      for (int m = 0; m < i; m += 4) {
+        const float4 l4 = *reinterpret_cast<const float4*>(LX + (o + i) * LSTRIDE + o + m);
+        a0 = fmaf(l4.x, x[m], a0);
+        if (m + 1 < i) a1 = fmaf(l4.y, x[m + 1], a1);
+        if (m + 2 < i) a2 = fmaf(l4.z, x[m + 2], a2);
+        if (m + 3 < i) a3 = fmaf(l4.w, x[m + 3], a3);
+      }
+      x[i] = (i == j) ? 1.f : ((i < j) ? 0.f : -((a0 + a1) + (a2 + a3)));
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 32; ++i) LX[(o + i) * LSTRIDE + o + j] = x[i];
+  }
+  wg_sync(bar_id);
+  {  // Y = L21 X11 -> LX[0:32][32:64]
+    const int j = lane, i0 = wwarp * 8;
+    float y[8];
+#pragma unroll
+    for (int ii = 0; ii < 8; ++ii) y[ii] = 0.f;
+#pragma unroll 2
+    for (int m = 0; m < 32; m += 4) {
+      const float x0 = LX[(m + 0) * LSTRIDE + j], x1 = LX[(m + 1) * LSTRIDE + j],
+                  x2 = LX[(m + 2) * LSTRIDE + j], x3 = LX[(m + 3) * LSTRIDE + j];
+#pragma unroll
+      for (int ii = 0; ii < 8; ++ii) {
+        const float4 l4 = *reinterpret_cast<const float4*>(LX + (32 + i0 + ii) * LSTRIDE + m);
+        y[ii] = fmaf(l4.x, x0, fmaf(l4.y, x1, fmaf(l4.z, x2, fmaf(l4.w, x3, y[ii]))));
+      }
+    }
+#pragma unroll
+    for (int ii = 0; ii < 8; ++ii) LX[(i0 + ii) * LSTRIDE + 32 + j] = y[ii];
+  }
+  wg_sync(bar_id);
+  {  // X21 = -X22 Y -> LX[32:64][0:32]
+    const int j = lane, i0 = wwarp * 8;
+    float y[8];
+#pragma unroll
+    for (int ii = 0; ii < 8; ++ii) y[ii] = 0.f;
+#pragma unroll 2
+    for (int m = 0; m < 32; m += 4) {
+      const float y0 = LX[(m + 0) * LSTRIDE + 32 + j], y1 = LX[(m + 1) * LSTRIDE + 32 + j],
+                  y2 = LX[(m + 2) * LSTRIDE + 32 + j], y3 = LX[(m + 3) * LSTRIDE + 32 + j];
+#pragma unroll
+      for (int ii = 0; ii < 8; ++ii) {
+        const float4 x4 =
+            *reinterpret_cast<const float4*>(LX + (32 + i0 + ii) * LSTRIDE + 32 + m);
+        y[ii] = fmaf(x4.x, y0, fmaf(x4.y, y1, fmaf(x4.z, y2, fmaf(x4.w, y3, y[ii]))));
+      }
+    }
+#pragma unroll
+    for (int ii = 0; ii < 8; ++ii) LX[(32 + i0 + ii) * LSTRIDE + j] = -y[ii];
+  }
+  wg_sync(bar_id);
+}
+
+}  // namespace tc
+}  // namespace dn

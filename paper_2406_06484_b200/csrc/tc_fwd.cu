@@ -17,7 +17,14 @@
 //   Z = diag(s) U'                                      (K_hat^T U' = K^T Z)
 //   O = diag(r) (Q H + tril(Q K^T) Z)                  Eq. 9, M=64
 //   H^T += Z^T K                                       Eq. 8, M=128
-// Algebra of the folded normalisation: DESIGN.md §Forward kernel.
+// Algebra of the folded normalisation: DESIGN.md §4.1.
+//
+// Warp specialisation: warpgroup P (warps 0-3) runs the
+// state-independent "prep" of chunk t+1 (Gram, substitution, W, U) while
+// warpgroup S (warps 4-7) runs the state chain and output of chunk t.
+// Q/K/A/W tiles and the U accumulator are double-buffered by chunk parity;
+// mbarriers full[b] (P -> S) and empty[b] (S -> P) hand the buffers over, and
+// the next chunk's TMA loads are issued as soon as a buffer frees.
 #include <cudaTypedefs.h>
 #include <stdio.h>
 
@@ -29,27 +36,36 @@ namespace {
 
 using namespace tc;
 
-constexpr int C = 64, DK = 128, DV = 128, NT = 128;
-constexpr int LS = 68;  // row stride (floats) of the fp32 substitution buffers
+constexpr int C = 64, DK = 128, DV = 128, NT = 256;
+constexpr int LS = 68;  // row stride (floats) of the fp32 substitution buffer
 
 // dynamic shared memory map (bytes)
-constexpr int OFF_Q = 0;                     // Q   IL R=64  x 128    16 KB
-constexpr int OFF_K = OFF_Q + C * DK * 2;    // K   IL R=64  x 128    16 KB
-constexpr int OFF_V = OFF_K + C * DK * 2;    // V   IL R=64  x 128    16 KB
-constexpr int OFF_T = OFF_V + C * DV * 2;    // T'  IL R=64  x 64      8 KB
-constexpr int OFF_TU = OFF_T + C * C * 2;    // T'' IL R=64  x 64      8 KB
-constexpr int OFF_A = OFF_TU + C * C * 2;    // A   IL R=64  x 64      8 KB
-constexpr int OFF_W = OFF_A + C * C * 2;     // W^T IL R=128 x 64     16 KB
-constexpr int OFF_H = OFF_W + DK * C * 2;    // H^T IL R=128 x 128    32 KB
-constexpr int OFF_Z = OFF_H + DV * DK * 2;   // Z^T IL R=128 x 64     16 KB
-constexpr int OFF_O = OFF_Z + DV * C * 2;    // O   IL R=64  x 128    16 KB
-constexpr int OFF_L = OFF_O + C * DV * 2;    // L   fp32 [64][LS]
-constexpr int OFF_X = OFF_L + C * LS * 4;    // X   fp32 [64][LS]
-constexpr int OFF_B = OFF_X + C * LS * 4;    // beta, s, r  fp32 [3][64]
-constexpr int SMEM_BYTES = OFF_B + 3 * C * 4;
+constexpr int TILE = C * DK * 2;                 // 16 KB chunk tile
+constexpr int OFF_Q = 0;                         // Q[2]  IL R=64 x 128
+constexpr int OFF_K = OFF_Q + 2 * TILE;          // K[2]  IL R=64 x 128
+constexpr int OFF_V = OFF_K + 2 * TILE;          // V     IL R=64 x 128
+constexpr int OFF_T = OFF_V + TILE;              // T'    IL R=64 x 64
+constexpr int OFF_TU = OFF_T + C * C * 2;        // T''   IL R=64 x 64
+constexpr int OFF_A = OFF_TU + C * C * 2;        // A[2]  IL R=64 x 64
+constexpr int OFF_W = OFF_A + 2 * C * C * 2;     // W^T[2] IL R=128 x 64
+constexpr int OFF_H = OFF_W + 2 * DK * C * 2;    // H^T   IL R=128 x 128
+constexpr int OFF_Z = OFF_H + DV * DK * 2;       // Z^T   IL R=128 x 64  | O staging
+constexpr int OFF_L = OFF_Z + DV * C * 2;        // L -> X fp32 [64][LS]
+constexpr int OFF_VEC = OFF_L + C * LS * 4;      // [2][beta, s, r][64] fp32
+constexpr int SMEM_BYTES = OFF_VEC + 2 * 3 * C * 4;
+static_assert(SMEM_BYTES <= 232448 - 1024, "shared memory budget");
 
-// TMEM column map (512 columns allocated)
-constexpr uint32_t TM_H = 0, TM_GQK = 128, TM_GKK = 192, TM_W = 256, TM_U = 320, TM_O = 384;
+// TMEM column map (512 columns)
+constexpr uint32_t LO16 = 16u << 16;
+constexpr uint32_t TM_H = 0;                     // H^T  M=128, 128 cols (S)
+constexpr uint32_t TM_O = 128;                   // O    M=64,  128 cols (S)
+constexpr uint32_t TM_U1 = 256;                  // U^T  buffer 1, M=128, 64 cols
+constexpr uint32_t TM_G = 320;                   // G_qk lane+0 | G_kk lane+16 (P)
+constexpr uint32_t TM_W = 384;                   // W^T  M=128, 64 cols (P)
+constexpr uint32_t TM_U0 = 448;                  // U^T  buffer 0
+__device__ __forceinline__ uint32_t tm_u(int b) { return b ? TM_U1 : TM_U0; }
+
+enum { BAR_P = 1, BAR_S = 2 };  // named barriers of the two warpgroups
 
 #ifdef DN_DEBUG
 // Test-only intermediate dumps (tests/test_tc_debug.py builds with -DDN_DEBUG).
@@ -57,17 +73,20 @@ __device__ float* dn_dbg = nullptr;
 __device__ int dn_dbg_chunk = 0;
 enum { D_L = 0, D_X = 4096, D_GQK = 8192, D_W = 12288, D_U = 20480, D_UP = 28672,
        D_O = 36864, D_H = 45056, D_S = 61440, D_R = 61504, D_B = 61568 };
-__device__ void dbg_smem(float* dst, const float* src, int rows, int cols, int stride) {
-  for (int e = threadIdx.x; e < rows * cols; e += blockDim.x)
-    dst[e] = src[(e / cols) * stride + e % cols];
+__device__ void dbg_smem(float* dst, const float* src, int rows, int cols, int stride, int w) {
+  for (int e = w; e < rows * cols; e += 128) {
+    const int i = e / cols, j = e % cols;
+    // the substitution buffer keeps scratch above the diagonal
+    dst[e] = (stride == LS && j > i && rows == cols) ? 0.f : src[i * stride + j];
+  }
 }
-__device__ void dbg_tmem(float* dst, uint32_t tm, uint32_t col, int ncols, int M) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+__device__ void dbg_tmem(float* dst, uint32_t tm, uint32_t col, int ncols, int M, int w) {
+  const int warp = w >> 5, lane = w & 31;
   for (int c0 = 0; c0 < ncols; c0 += 16) {
     uint32_t r[16];
     tmem_ld16(taddr(tm, warp * 32, col + c0), r);
     tmem_ld_wait();
-    const int row = M == 128 ? (int)threadIdx.x : (lane < 16 ? warp * 16 + lane : -1);
+    const int row = M == 128 ? w : (lane < 16 ? warp * 16 + lane : -1);
     if (row >= 0)
       for (int j = 0; j < 16; ++j) dst[row * ncols + c0 + j] = __uint_as_float(r[j]);
   }
@@ -83,37 +102,26 @@ __global__ void __launch_bounds__(NT, 1)
                   const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mO,
                   Args a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bar_tma, bar_mma;
+  __shared__ uint64_t bar_tma[2], bar_full[2], bar_empty[2], bar_p, bar_s;
   __shared__ uint32_t tslot;
-  uint8_t* sQ = smem + OFF_Q;
-  uint8_t* sK = smem + OFF_K;
-  uint8_t* sV = smem + OFF_V;
-  uint8_t* sT = smem + OFF_T;
-  uint8_t* sTu = smem + OFF_TU;
-  uint8_t* sA = smem + OFF_A;
-  uint8_t* sW = smem + OFF_W;
-  uint8_t* sH = smem + OFF_H;
-  uint8_t* sZ = smem + OFF_Z;
-  uint8_t* sO = smem + OFF_O;
-  float* Ls = reinterpret_cast<float*>(smem + OFF_L);
-  float* Xs = reinterpret_cast<float*>(smem + OFF_X);
-  float* sb = reinterpret_cast<float*>(smem + OFF_B);  // beta
-  float* ss = sb + C;                                   // 1/||k||
-  float* sr = ss + C;                                   // 1/||q||
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wg = tid >> 7;            // 0: prep warpgroup, 1: state/output warpgroup
+  const int w = tid & 127;            // thread index inside the warpgroup
+  const int wwarp = w >> 5;           // warp inside the warpgroup (TMEM lane quadrant)
   const int unit = blockIdx.x;
   const int L = a.L, NC = a.NC;
   const bool l2 = (a.flags & DELTANET_L2NORM_QK) != 0;
-  const __nv_bfloat16* beta = (const __nv_bfloat16*)a.beta + (size_t)unit * L;
-  uint8_t* states =
-      (a.flags & DELTANET_SAVE_STATES) ? (uint8_t*)a.states + (size_t)unit * NC * (DK * DV * 2)
-                                       : nullptr;
 
   if (warp == 0) tmem_alloc<512>(&tslot);
   if (tid == 0) {
-    mbar_init(&bar_tma, 1);
-    mbar_init(&bar_mma, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bar_tma[b], 2);  // Q/K arrival + V arrival
+      mbar_init(&bar_full[b], 1);
+      mbar_init(&bar_empty[b], 1);
+    }
+    mbar_init(&bar_p, 1);
+    mbar_init(&bar_s, 1);
     mbar_fence_init();
     prefetch_tmap(&mQ);
     prefetch_tmap(&mK);
@@ -122,310 +130,301 @@ __global__ void __launch_bounds__(NT, 1)
   }
   cta_sync();
   const uint32_t tm = tslot;
-  uint32_t ph_tma = 0, ph_mma = 0;
+  auto sQ = [&](int b) { return smem + OFF_Q + b * TILE; };
+  auto sK = [&](int b) { return smem + OFF_K + b * TILE; };
+  auto sA = [&](int b) { return smem + OFF_A + b * C * C * 2; };
+  auto sW = [&](int b) { return smem + OFF_W + b * DK * C * 2; };
+  auto vec = [&](int b) { return reinterpret_cast<float*>(smem + OFF_VEC) + b * 3 * C; };
+  uint8_t* sV = smem + OFF_V;
+  uint8_t* sT = smem + OFF_T;
+  uint8_t* sTu = smem + OFF_TU;
+  uint8_t* sH = smem + OFF_H;
+  uint8_t* sZ = smem + OFF_Z;
+  uint8_t* sO = sZ;
+  float* LX = reinterpret_cast<float*>(smem + OFF_L);
 
-  // ---- initial state: H^T row dv = tid (TMEM lane tid) from h0 [dk][dv]
-  {
-    const float* h0 = a.h0 ? a.h0 + (size_t)unit * DK * DV : nullptr;
-#pragma unroll 1
-    for (int c0 = 0; c0 < DK; c0 += 16) {
-      uint32_t r[16];
-      float f[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        f[j] = h0 ? h0[(size_t)(c0 + j) * DV + tid] : 0.f;
-        r[j] = __float_as_uint(f[j]);
+  if (wg == 0) {
+    // =====================================================================
+    // Warpgroup P: prep of chunk c (state independent)
+    // =====================================================================
+    const __nv_bfloat16* beta = (const __nv_bfloat16*)a.beta + (size_t)unit * L;
+    if (w == 0) {  // chunks 0 and 1: both buffers start free
+      for (int c = 0; c < 2 && c < NC; ++c) {
+        mbar_expect_tx(&bar_tma[c], 2 * TILE);
+        tma_load_4d(sQ(c), &mQ, 0, c * C, 0, unit, &bar_tma[c]);
+        tma_load_4d(sK(c), &mK, 0, c * C, 0, unit, &bar_tma[c]);
       }
-      tmem_st16(taddr(tm, warp * 32, TM_H + c0), r);
-      il_store8(sH, DV, tid, c0, f);
-      il_store8(sH, DV, tid, c0 + 8, f + 8);
+      mbar_expect_tx(&bar_tma[0], TILE);
+      tma_load_4d(sV, &mV, 0, 0, 0, unit, &bar_tma[0]);
     }
-    tmem_st_wait();
-  }
-  fence_proxy_async();
-  cta_sync();
-
-  const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aV = smem_u32(sV), aT = smem_u32(sT),
-                 aTu = smem_u32(sTu),
-                 aA = smem_u32(sA), aW = smem_u32(sW), aH = smem_u32(sH), aZ = smem_u32(sZ);
-
+    uint32_t ph_p = 0;
 #pragma unroll 1
-  for (int c = 0; c < NC; ++c) {
-    const int t0 = c * C;
-    // ---- S0: TMA the chunk tiles; beta; save H_c (bf16 image) for the bwd
-    if (tid == 0) {
-      mbar_expect_tx(&bar_tma, 3 * C * DK * 2);
-      tma_load_4d(sQ, &mQ, 0, t0, 0, unit, &bar_tma);
-      tma_load_4d(sK, &mK, 0, t0, 0, unit, &bar_tma);
-      tma_load_4d(sV, &mV, 0, t0, 0, unit, &bar_tma);
-      if (states) {
-        bulk_store(states + (size_t)c * DK * DV * 2, sH, DK * DV * 2);
+    for (int c = 0; c < NC; ++c) {
+      const int b = c & 1, t0 = c * C;
+      float* vb = vec(b);  // beta, s, r of this chunk
+      // beta of the chunk (prefetch into a register before waiting)
+      const float bval = (w < C && t0 + w < L) ? __bfloat162float(beta[t0 + w]) : 0.f;
+      mbar_wait(&bar_tma[b], (c >> 1) & 1);
+      if (c >= 2) mbar_wait(&bar_empty[b], ((c >> 1) - 1) & 1);  // chain c-2 released b
+      if (w == 0) {
+        fence_after_sync();
+        const uint32_t id = idesc_bf16(64, 64, false, false);
+        const uint32_t aq = smem_u32(sQ(b)), ak = smem_u32(sK(b));
+#pragma unroll
+        for (int k0 = 0; k0 < DK; k0 += 16) {
+          mma_bf16(tm + TM_G, desc_k(aq, C, k0), desc_k(ak, C, k0), id, k0 > 0);
+          mma_bf16(tm + TM_G + LO16, desc_k(ak, C, k0), desc_k(ak, C, k0), id, k0 > 0);
+        }
+        mma_commit(&bar_p);
+      }
+      {
+        // w < 64: r = 1/||q_w||; w >= 64: s = 1/||k_{w-64}||   (fp32 from bf16)
+        const int row = w & 63;
+        const uint8_t* tile = w < 64 ? sQ(b) : sK(b);
+        float acc = 0.f;
+#pragma unroll
+        for (int g = 0; g < DK / 8; ++g) {
+          float x[8];
+          il_load8(tile, C, row, g * 8, x);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc = fmaf(x[e], x[e], acc);
+        }
+        float inv = l2 ? 1.f / fmaxf(sqrtf(acc), a.eps) : 1.f;
+        if (t0 + row >= L) inv = 0.f;  // padded token: exact zero contribution
+        vb[(w < 64 ? 2 : 1) * C + row] = inv;
+        if (w < C) vb[w] = bval;
+      }
+      mbar_wait(&bar_p, ph_p);
+      ph_p ^= 1;
+      fence_after_sync();
+      wg_sync(BAR_P);  // beta, s, r visible
+      {
+        // one TMEM load: lanes < 16 hold G_qk rows, lanes >= 16 hold G_kk rows
+        float f[64];
+        ld64(tm, wwarp, TM_G, f);
+        const int i = wwarp * 16 + (lane & 15);
+        if (lane < 16) {  // A = tril(Q K^T), raw (inclusive, R4)
+#pragma unroll
+          for (int g = 0; g < 8; ++g) {
+            float x[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) x[e] = (g * 8 + e <= i) ? f[g * 8 + e] : 0.f;
+            il_store8(sA(b), C, i, g * 8, x);
+          }
+        } else {  // L = beta_i s_i s_j (k_i . k_j), j < i
+          const float bi = vb[i] * vb[C + i];
+#pragma unroll
+          for (int j = 0; j < 64; j += 4) {
+            float4 v;
+            v.x = (j + 0 < i) ? bi * vb[C + j + 0] * f[j + 0] : 0.f;
+            v.y = (j + 1 < i) ? bi * vb[C + j + 1] * f[j + 1] : 0.f;
+            v.z = (j + 2 < i) ? bi * vb[C + j + 2] * f[j + 2] : 0.f;
+            v.w = (j + 3 < i) ? bi * vb[C + j + 3] * f[j + 3] : 0.f;
+            *reinterpret_cast<float4*>(LX + i * LS + j) = v;
+          }
+        }
+      }
+      wg_sync(BAR_P);
+      DBG(dbg_smem(dn_dbg + D_L, LX, C, C, LS, w); dbg_tmem(dn_dbg + D_GQK, tm, TM_G, C, 64, w);
+          dbg_smem(dn_dbg + D_S, vb + C, 1, C, C, w); dbg_smem(dn_dbg + D_R, vb + 2 * C, 1, C, C, w);
+          dbg_smem(dn_dbg + D_B, vb, 1, C, C, w));
+      ut_inverse_inplace<LS>(LX, w, BAR_P);
+      DBG(dbg_smem(dn_dbg + D_X, LX, C, C, LS, w));
+      {
+        // T'[i][j] = X[i][j] beta_j s_j, T''[i][j] = X[i][j] beta_j  (j <= i)
+        const int i = w >> 1, j0 = (w & 1) * 32;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          float x[8], y[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int j = j0 + g * 8 + e;
+            y[e] = (j <= i) ? LX[i * LS + j] * vb[j] : 0.f;
+            x[e] = y[e] * vb[C + j];
+          }
+          il_store8(sT, C, i, j0 + g * 8, x);
+          il_store8(sTu, C, i, j0 + g * 8, y);
+        }
+      }
+      fence_proxy_async();
+      fence_before_sync();
+      wg_sync(BAR_P);
+      if (w == 0) {  // W^T = K^T T'^T, U^T = V^T T''^T  (M=128, N=64, K=64)
+        fence_after_sync();
+        const uint32_t id = idesc_bf16(128, 64, true, false);
+        const uint32_t ak = smem_u32(sK(b)), av = smem_u32(sV), at = smem_u32(sT),
+                       atu = smem_u32(sTu);
+#pragma unroll
+        for (int k0 = 0; k0 < C; k0 += 16) {
+          mma_bf16(tm + TM_W, desc_mn(ak, C, k0), desc_k(at, C, k0), id, k0 > 0);
+          mma_bf16(tm + tm_u(b), desc_mn(av, C, k0), desc_k(atu, C, k0), id, k0 > 0);
+        }
+        mma_commit(&bar_p);
+      }
+      mbar_wait(&bar_p, ph_p);
+      ph_p ^= 1;
+      fence_after_sync();
+      if (w == 0 && c + 1 < NC) {  // V is free again: prefetch the next chunk's V
+        const int nb = (c + 1) & 1;
+        mbar_expect_tx(&bar_tma[nb], TILE);
+        tma_load_4d(sV, &mV, 0, (c + 1) * C, 0, unit, &bar_tma[nb]);
+      }
+      DBG(dbg_tmem(dn_dbg + D_W, tm, TM_W, C, 128, w); dbg_tmem(dn_dbg + D_U, tm, tm_u(b), C, 128, w));
+      {  // W^T (lane = dk) -> bf16 IL tile (row dk, cols = tokens)
+        float f[64];
+        ld64(tm, wwarp, TM_W, f);
+#pragma unroll
+        for (int g = 0; g < 8; ++g) il_store8(sW(b), DK, w, g * 8, f + g * 8);
+      }
+      fence_proxy_async();
+      fence_before_sync();
+      wg_sync(BAR_P);
+      if (w == 0) mbar_arrive(&bar_full[b]);
+    }
+  } else {
+    // =====================================================================
+    // Warpgroup S: state chain + output of chunk c
+    // =====================================================================
+    uint8_t* states = (a.flags & DELTANET_SAVE_STATES)
+                          ? (uint8_t*)a.states + (size_t)unit * NC * (DK * DV * 2)
+                          : nullptr;
+    {  // initial state: H^T row dv = w (TMEM lane w) from h0 [dk][dv]
+      const float* h0 = a.h0 ? a.h0 + (size_t)unit * DK * DV : nullptr;
+#pragma unroll 1
+      for (int c0 = 0; c0 < DK; c0 += 16) {
+        uint32_t r[16];
+        float f[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          f[j] = h0 ? h0[(size_t)(c0 + j) * DV + w] : 0.f;
+          r[j] = __float_as_uint(f[j]);
+        }
+        tmem_st16(taddr(tm, wwarp * 32, TM_H + c0), r);
+        il_store8(sH, DV, w, c0, f);
+        il_store8(sH, DV, w, c0 + 8, f + 8);
+      }
+      tmem_st_wait();
+    }
+    fence_proxy_async();
+    fence_before_sync();
+    wg_sync(BAR_S);
+    const uint32_t aH = smem_u32(sH), aZ = smem_u32(sZ);
+    uint32_t ph_s = 0;
+#pragma unroll 1
+    for (int c = 0; c < NC; ++c) {
+      const int b = c & 1, t0 = c * C;
+      const float* vb = vec(b);
+      mbar_wait(&bar_full[b], (c >> 1) & 1);
+      // r of this lane's output row, read before buffer b is released
+      const float ri = vb[2 * C + wwarp * 16 + (lane & 15)];
+      if (w == 0) {
+        fence_after_sync();
+        // U'^T = U^T - H^T W^T (M=128,N=64,K=128); O = Q H (M=64,N=128,K=128)
+        const uint32_t idn = idesc_bf16(128, 64, false, true, /*neg_a=*/true);
+        const uint32_t ido = idesc_bf16(64, 128, false, false);
+        const uint32_t aw = smem_u32(sW(b)), aq = smem_u32(sQ(b));
+#pragma unroll
+        for (int k0 = 0; k0 < DK; k0 += 16)
+          mma_bf16(tm + tm_u(b), desc_k(aH, DV, k0), desc_mn(aw, DK, k0), idn, 1);
+        mma_commit(&bar_s);
+#pragma unroll
+        for (int k0 = 0; k0 < DK; k0 += 16)
+          mma_bf16(tm + TM_O, desc_k(aq, C, k0), desc_k(aH, DV, k0), ido, k0 > 0);
+        if (states) {  // save H_c (bf16 smem image) for the backward
+          bulk_store(states + (size_t)c * DK * DV * 2, sH, DK * DV * 2);
+          bulk_commit();
+        }
+        bulk_wait_read0();  // previous O store done reading sO (= sZ)
+      }
+      mbar_wait(&bar_s, ph_s);
+      ph_s ^= 1;
+      fence_after_sync();
+      wg_sync(BAR_S);
+      DBG(dbg_tmem(dn_dbg + D_UP, tm, tm_u(b), C, 128, w));
+      {  // Z^T[dv][t] = U'^T[dv][t] * s_t -> bf16 IL tile (row dv)
+        float f[64];
+        ld64(tm, wwarp, tm_u(b), f);
+#pragma unroll
+        for (int t = 0; t < 64; ++t) f[t] *= vb[C + t];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) il_store8(sZ, DV, w, g * 8, f + g * 8);
+      }
+      fence_proxy_async();
+      fence_before_sync();
+      wg_sync(BAR_S);
+      if (w == 0) {
+        fence_after_sync();
+        // H^T += Z^T K (M=128,N=128,K=64); O += tril(QK^T) Z (M=64,N=128,K=64)
+        const uint32_t ido = idesc_bf16(64, 128, false, false);
+        const uint32_t idh = idesc_bf16(128, 128, false, true);
+        const uint32_t aa = smem_u32(sA(b)), ak = smem_u32(sK(b));
+#pragma unroll
+        for (int k0 = 0; k0 < C; k0 += 16)
+          mma_bf16(tm + TM_H, desc_k(aZ, DV, k0), desc_mn(ak, C, k0), idh, 1);
+#pragma unroll
+        for (int k0 = 0; k0 < C; k0 += 16)
+          mma_bf16(tm + TM_O, desc_k(aa, C, k0), desc_k(aZ, DV, k0), ido, 1);
+        mma_commit(&bar_s);
+      }
+      mbar_wait(&bar_s, ph_s);
+      ph_s ^= 1;
+      fence_after_sync();
+      if (w == 0) {
+        mbar_arrive(&bar_empty[b]);  // Q/K/A/W[b] and U[b] are free for chunk c+2
+        if (c + 2 < NC) {
+          mbar_expect_tx(&bar_tma[b], 2 * TILE);
+          tma_load_4d(sQ(b), &mQ, 0, (c + 2) * C, 0, unit, &bar_tma[b]);
+          tma_load_4d(sK(b), &mK, 0, (c + 2) * C, 0, unit, &bar_tma[b]);
+        }
+        bulk_wait_read0();  // state save done reading sH
+      }
+      wg_sync(BAR_S);
+      DBG(dbg_tmem(dn_dbg + D_O, tm, TM_O, DV, 64, w); dbg_tmem(dn_dbg + D_H, tm, TM_H, DK, 128, w));
+      {
+        // H^T -> bf16 sH (operand of the next chunk) first: it is on the chain
+#pragma unroll 1
+        for (int half = 0; half < 2; ++half) {
+          float f[64];
+          ld64(tm, wwarp, TM_H + 64 * half, f);
+#pragma unroll
+          for (int g = 0; g < 8; ++g) il_store8(sH, DV, w, 64 * half + g * 8, f + g * 8);
+        }
+        // O rows * r -> bf16 -> staging (IL R=64, row = token)
+        const int i = wwarp * 16 + (lane & 15);
+#pragma unroll 1
+        for (int half = 0; half < 2; ++half) {
+          float f[64];
+          ld64(tm, wwarp, TM_O + 64 * half, f);
+          if (lane < 16) {
+#pragma unroll
+            for (int e = 0; e < 64; ++e) f[e] *= ri;
+#pragma unroll
+            for (int g = 0; g < 8; ++g) il_store8(sO, C, i, 64 * half + g * 8, f + g * 8);
+          }
+        }
+      }
+      fence_proxy_async();
+      fence_before_sync();
+      wg_sync(BAR_S);
+      if (w == 0 && a.o) {
+        tma_store_4d(&mO, sO, 0, t0, 0, unit);
         bulk_commit();
       }
     }
-    if (tid < C) sb[tid] = (t0 + tid < L) ? __bfloat162float(beta[t0 + tid]) : 0.f;
-    mbar_wait(&bar_tma, ph_tma);
-    ph_tma ^= 1;
-
-    // ---- S1: Gram MMAs (M=64, N=64, K=128) + row norms on CUDA cores
-    if (tid == 0) {
+    // final state hT [dk][dv] (fp32), lane dv = w
+    if (a.hT) {
       fence_after_sync();
-      const uint32_t id = idesc_bf16(64, 64, false, false);
-#pragma unroll
-      for (int k0 = 0; k0 < DK; k0 += 16) {
-        mma_bf16(tm + TM_GQK, desc_k(aQ, C, k0), desc_k(aK, C, k0), id, k0 > 0);
-        mma_bf16(tm + TM_GKK, desc_k(aK, C, k0), desc_k(aK, C, k0), id, k0 > 0);
-      }
-      mma_commit(&bar_mma);
-    }
-    {
-      // tid < 64: ||q_tid||;  tid >= 64: ||k_{tid-64}||  (fp32 from bf16)
-      const int row = tid & 63;
-      const uint8_t* tile = tid < 64 ? sQ : sK;
-      float acc = 0.f;
-#pragma unroll
-      for (int g = 0; g < DK / 8; ++g) {
-        uint4 v = *reinterpret_cast<const uint4*>(tile + il_off(row, g * 8, C));
-        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          float2 f = __bfloat1622float2(h[e]);
-          acc = fmaf(f.x, f.x, fmaf(f.y, f.y, acc));
-        }
-      }
-      float inv = l2 ? 1.f / fmaxf(sqrtf(acc), a.eps) : 1.f;
-      if (t0 + row >= L) inv = 0.f;  // padded token: exact zero contribution
-      (tid < 64 ? sr : ss)[row] = inv;
-    }
-    mbar_wait(&bar_mma, ph_mma);
-    ph_mma ^= 1;
-    cta_sync();
-
-    // ---- S2: A = tril(Q K^T) (bf16, raw), L = beta_i s_i s_j (k_i.k_j), j < i
-    {
-      float f[64];
-      const int i = warp * 16 + (lane & 15);  // M=64 accumulator row of this lane
-      ld64(tm, warp, TM_GQK, f);
-      if (lane < 16) {
-#pragma unroll
-        for (int g = 0; g < 8; ++g) {
-          float x[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) x[e] = (g * 8 + e <= i) ? f[g * 8 + e] : 0.f;
-          il_store8(sA, C, i, g * 8, x);
-        }
-      }
-      ld64(tm, warp, TM_GKK, f);
-      if (lane < 16) {
-        const float bi = sb[i] * ss[i];
-#pragma unroll
-        for (int j = 0; j < 64; j += 4) {
-          float4 v;
-          v.x = (j + 0 < i) ? bi * ss[j + 0] * f[j + 0] : 0.f;
-          v.y = (j + 1 < i) ? bi * ss[j + 1] * f[j + 1] : 0.f;
-          v.z = (j + 2 < i) ? bi * ss[j + 2] * f[j + 2] : 0.f;
-          v.w = (j + 3 < i) ? bi * ss[j + 3] * f[j + 3] : 0.f;
-          *reinterpret_cast<float4*>(Ls + i * LS + j) = v;
-        }
-      }
-    }
-    __syncthreads();
-    DBG(dbg_smem(dn_dbg + D_L, Ls, C, C, LS); dbg_tmem(dn_dbg + D_GQK, tm, TM_GQK, C, 64);
-        dbg_smem(dn_dbg + D_S, ss, 1, C, C); dbg_smem(dn_dbg + D_R, sr, 1, C, C);
-        dbg_smem(dn_dbg + D_B, sb, 1, C, C));
-
-    // ---- S3: X = (I + L)^{-1}, two 32x32 diagonal blocks by column-parallel
-    // forward substitution, then X21 = -X22 L21 X11.
-    if (tid < 64) {
-      const int b = tid >> 5, j = lane;
-      const int o = 32 * b;
-      float x[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        float acc = 0.f;
-#pragma unroll
-        for (int m = 0; m < i; m += 4) {
-          const float4 l4 = *reinterpret_cast<const float4*>(Ls + (o + i) * LS + o + m);
-          acc = fmaf(l4.x, x[m], acc);
-          if (m + 1 < i) acc = fmaf(l4.y, x[m + 1], acc);
-          if (m + 2 < i) acc = fmaf(l4.z, x[m + 2], acc);
-          if (m + 3 < i) acc = fmaf(l4.w, x[m + 3], acc);
-        }
-        x[i] = (i == j) ? 1.f : ((i < j) ? 0.f : -acc);
-      }
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        Xs[(o + i) * LS + o + j] = x[i];
-        Xs[(o + i) * LS + (32 - o) + j] = 0.f;  // upper block 0; lower-left overwritten below
-      }
-    }
-    __syncthreads();
-    {
-      // Y = L21 X11 into Ls[0:32][32:64] (unused upper-right block of L)
-      const int j = lane, i0 = warp * 8;
-      float y[8];
-#pragma unroll
-      for (int ii = 0; ii < 8; ++ii) y[ii] = 0.f;
-#pragma unroll 4
-      for (int m = 0; m < 32; ++m) {
-        const float xm = Xs[m * LS + j];
-#pragma unroll
-        for (int ii = 0; ii < 8; ++ii) y[ii] = fmaf(Ls[(32 + i0 + ii) * LS + m], xm, y[ii]);
-      }
-#pragma unroll
-      for (int ii = 0; ii < 8; ++ii) Ls[(i0 + ii) * LS + 32 + j] = y[ii];
-    }
-    __syncthreads();
-    {
-      // X21 = -X22 Y
-      const int j = lane, i0 = warp * 8;
-      float y[8];
-#pragma unroll
-      for (int ii = 0; ii < 8; ++ii) y[ii] = 0.f;
-#pragma unroll 4
-      for (int m = 0; m < 32; ++m) {
-        const float ym = Ls[m * LS + 32 + j];
-#pragma unroll
-        for (int ii = 0; ii < 8; ++ii) y[ii] = fmaf(Xs[(32 + i0 + ii) * LS + 32 + m], ym, y[ii]);
-      }
-#pragma unroll
-      for (int ii = 0; ii < 8; ++ii) Xs[(32 + i0 + ii) * LS + j] = -y[ii];
-    }
-    __syncthreads();
-    {
-      // T'[i][j] = X[i][j] beta_j s_j, T''[i][j] = X[i][j] beta_j -> bf16 IL tiles
-      const int i = tid >> 1, j0 = (tid & 1) * 32;
-#pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        float x[8], y[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int j = j0 + g * 8 + e;
-          y[e] = Xs[i * LS + j] * sb[j];
-          x[e] = y[e] * ss[j];
-        }
-        il_store8(sT, C, i, j0 + g * 8, x);
-        il_store8(sTu, C, i, j0 + g * 8, y);
-      }
-    }
-    DBG(dbg_smem(dn_dbg + D_X, Xs, C, C, LS));
-    fence_proxy_async();
-    cta_sync();
-
-    // ---- S4: W^T = K^T T'^T, U^T = V^T T''^T  (M=128, N=64, K=64)
-    if (tid == 0) {
-      const uint32_t id = idesc_bf16(128, 64, true, false);
-#pragma unroll
-      for (int k0 = 0; k0 < C; k0 += 16) {
-        mma_bf16(tm + TM_W, desc_mn(aK, C, k0), desc_k(aT, C, k0), id, k0 > 0);
-        mma_bf16(tm + TM_U, desc_mn(aV, C, k0), desc_k(aTu, C, k0), id, k0 > 0);
-      }
-      mma_commit(&bar_mma);
-    }
-    mbar_wait(&bar_mma, ph_mma);
-    ph_mma ^= 1;
-    fence_after_sync();
-
-    DBG(dbg_tmem(dn_dbg + D_W, tm, TM_W, C, 128); dbg_tmem(dn_dbg + D_U, tm, TM_U, C, 128));
-    // ---- S5: W^T (lane = dk) -> bf16 IL tile sW (row dk, cols = tokens)
-    {
-      float f[64];
-      ld64(tm, warp, TM_W, f);
-#pragma unroll
-      for (int g = 0; g < 8; ++g) il_store8(sW, DK, tid, g * 8, f + g * 8);
-    }
-    fence_proxy_async();
-    cta_sync();
-
-    // ---- S6: U'^T = U^T - H^T W^T (M=128,N=64,K=128), O = Q H (M=64,N=128,K=128)
-    if (tid == 0) {
-      const uint32_t idn = idesc_bf16(128, 64, false, true, /*neg_a=*/true);
-      const uint32_t ido = idesc_bf16(64, 128, false, false);
-#pragma unroll
-      for (int k0 = 0; k0 < DK; k0 += 16) {
-        mma_bf16(tm + TM_U, desc_k(aH, DV, k0), desc_mn(aW, DK, k0), idn, 1);
-        mma_bf16(tm + TM_O, desc_k(aQ, C, k0), desc_k(aH, DV, k0), ido, k0 > 0);
-      }
-      mma_commit(&bar_mma);
-    }
-    mbar_wait(&bar_mma, ph_mma);
-    ph_mma ^= 1;
-    fence_after_sync();
-
-    DBG(dbg_tmem(dn_dbg + D_UP, tm, TM_U, C, 128));
-    // ---- S7: Z^T[dv][t] = U'^T[dv][t] * s_t -> bf16 IL tile sZ (row dv)
-    {
-      float f[64];
-      ld64(tm, warp, TM_U, f);
-#pragma unroll
-      for (int t = 0; t < 64; ++t) f[t] *= ss[t];
-#pragma unroll
-      for (int g = 0; g < 8; ++g) il_store8(sZ, DV, tid, g * 8, f + g * 8);
-    }
-    fence_proxy_async();
-    cta_sync();
-
-    // ---- S8: O += tril(QK^T) Z (M=64,N=128,K=64); H^T += Z^T K (M=128,N=128,K=64)
-    if (tid == 0) {
-      const uint32_t ido = idesc_bf16(64, 128, false, false);
-      const uint32_t idh = idesc_bf16(128, 128, false, true);
-#pragma unroll
-      for (int k0 = 0; k0 < C; k0 += 16) {
-        mma_bf16(tm + TM_O, desc_k(aA, C, k0), desc_k(aZ, DV, k0), ido, 1);
-        mma_bf16(tm + TM_H, desc_k(aZ, DV, k0), desc_mn(aK, C, k0), idh, 1);
-      }
-      mma_commit(&bar_mma);
-    }
-    mbar_wait(&bar_mma, ph_mma);
-    ph_mma ^= 1;
-    fence_after_sync();
-
-    DBG(dbg_tmem(dn_dbg + D_O, tm, TM_O, DV, 64); dbg_tmem(dn_dbg + D_H, tm, TM_H, DK, 128));
-    // ---- S9: O rows * r -> bf16 -> TMA store; H^T -> bf16 sH (next chunk)
-    if (tid == 0) bulk_wait_read0();  // previous O store and state save done reading smem
-    __syncthreads();
-    {
-      const int i = warp * 16 + (lane & 15);
+      float* hT = a.hT + (size_t)unit * DK * DV;
 #pragma unroll 1
       for (int half = 0; half < 2; ++half) {
         float f[64];
-        ld64(tm, warp, TM_O + 64 * half, f);
-        if (lane < 16) {
-          const float ri = sr[i];
+        ld64(tm, wwarp, TM_H + 64 * half, f);
 #pragma unroll
-          for (int e = 0; e < 64; ++e) f[e] *= ri;
-#pragma unroll
-          for (int g = 0; g < 8; ++g) il_store8(sO, C, i, 64 * half + g * 8, f + g * 8);
-        }
-      }
-#pragma unroll 1
-      for (int half = 0; half < 2; ++half) {
-        float f[64];
-        ld64(tm, warp, TM_H + 64 * half, f);
-#pragma unroll
-        for (int g = 0; g < 8; ++g) il_store8(sH, DV, tid, 64 * half + g * 8, f + g * 8);
+        for (int e = 0; e < 64; ++e) hT[(size_t)(64 * half + e) * DV + w] = f[e];
       }
     }
-    fence_proxy_async();
-    cta_sync();
-    if (tid == 0 && a.o) {
-      tma_store_4d(&mO, sO, 0, t0, 0, unit);
-      bulk_commit();
-    }
+    if (w == 0) bulk_wait0();
   }
-
-  // ---- final state hT [dk][dv] (fp32), lane dv = tid
-  if (a.hT) {
-    float* hT = a.hT + (size_t)unit * DK * DV;
-#pragma unroll 1
-    for (int half = 0; half < 2; ++half) {
-      float f[64];
-      ld64(tm, warp, TM_H + 64 * half, f);
-#pragma unroll
-      for (int e = 0; e < 64; ++e) hT[(size_t)(64 * half + e) * DV + tid] = f[e];
-    }
-  }
-  if (tid == 0) bulk_wait0();
   cta_sync();
   if (warp == 0) tmem_dealloc<512>(tm);
 }
@@ -447,7 +446,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }  // namespace
 
 // 4-D view {8 elems, L rows, D/8 column groups, B*H units} of a [B*H][L][D]
-// bf16 tensor; a box {8, 64, D/8, 1} lands in smem as the IL layout (R=64).
+// bf16 tensor; a box {8, rows, D/8, 1} lands in smem as the IL layout (R=rows).
 bool make_il_map(CUtensorMap* m, const void* base, int BH, int L, int D, int rows) {
   auto enc = encode_fn();
   if (!enc) return false;
@@ -489,7 +488,6 @@ int tc_fwd(const Args& a, cudaStream_t s) {
   tc_fwd_kernel<<<BH, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);
   return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
 }
-
 
 }  // namespace dn
 

@@ -2,7 +2,7 @@
 //
 // The paper gives no backward (PAPER.md line 250 only says states are
 // recomputed; reading R12).  This kernel evaluates the exact
-// adjoint of Eq. 8-11 chunk by chunk in reverse (DESIGN.md §Backward,
+// adjoint of Eq. 8-11 chunk by chunk in reverse (DESIGN.md §4.2,
 // SURVEY App. A.2), one CTA per (b, h) unit, with dH = dl/dH_{t+1} held in
 // TMEM (fp32, lanes = d_v) across chunks and the chunk-boundary states H_t
 // read from the workspace image the forward wrote.
@@ -20,7 +20,13 @@
 //              dbeta = rowsum(P . R) + rowsum(G . K K^T)
 //   then the L2-normalisation adjoint on dQ, dK (R9).
 // (dK_beta = X^T dW = -P H^T, and rowsum(dK_beta . K) + rowsum(P . V) =
-//  rowsum(P . R) -- DESIGN.md §Backward.)
+//  rowsum(P . R) -- DESIGN.md §4.2.)
+//
+// 256 threads.  Thread phases are split across the two warpgroups by
+// columns (both see all 128 TMEM lanes); the substitution (warpgroup 0)
+// overlaps the R / dU' conversions (warpgroup 1).  The next chunk's Q, K,
+// dO, V and H_t are prefetched by TMA during the tail of the current chunk
+// (K alternates between two slots with the W tile).
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
@@ -31,36 +37,59 @@ namespace {
 
 using namespace tc;
 
-constexpr int C = 64, D = 128, NT = 128;
+constexpr int C = 64, D = 128, NT = 256;
 constexpr int LS = 68;
 constexpr uint32_t LO16 = 16u << 16;  // TMEM lane offset 16 (second M=64 accumulator)
+constexpr int TILE = C * D * 2;       // 16 KB
 
-// ---- shared memory map (bytes); regions reused by lifetime (DESIGN.md)
-constexpr int OFF_Q = 0;          // q_hat  IL R=64 x 128   (whole chunk)
-constexpr int OFF_K = 16384;      // k_hat  IL R=64 x 128   (whole chunk)
-constexpr int OFF_DO = 32768;     // dO     IL R=64 x 128   (whole chunk)
-constexpr int OFF_H = 49152;      // H^T    IL R=128 x 128  (-> dq staging)
-constexpr int OFF_DH = 81920;     // dH^T   IL R=128 x 128  (-> dk staging)
-constexpr int OFF_UP = 114688;    // U'^T   IL R=128 x 64
-constexpr int OFF_X = 131072;     // X      IL R=64 x 64
-constexpr int OFF_W = 139264;     // W^T    IL R=128 x 64
-constexpr int OFF_V = 155648;     // V      IL R=64 x 128   (-> dV staging)
-constexpr int OFF_S = 172032;     // region S (51200 B), see below
-constexpr int S_L = OFF_S;                // Ls fp32 | dU'^T | Y, Mg
-constexpr int S_X = OFF_S + 17408;        // Xs fp32 | R    | G fp32
-constexpr int S_T = OFF_S + 34816;        // T      | dA
-constexpr int S_A = OFF_S + 43008;        // A      | dX
-constexpr int OFF_B = OFF_S + 51200;      // 6 x 64 floats
-constexpr int SMEM_BYTES = OFF_B + 6 * C * 4;
-static_assert(SMEM_BYTES <= 232448, "shared memory budget");
+// ---- shared memory map (bytes); regions reused by lifetime (DESIGN.md §4.2)
+constexpr int OFF_Q = 0;                   // q_hat  IL R=64 x 128
+constexpr int OFF_KW = 16384;              // 2 slots: k_hat | W^T (IL R=128 x 64)
+constexpr int OFF_DO = 49152;              // dO     IL R=64 x 128
+constexpr int OFF_V = 65536;               // V -> dV staging
+constexpr int OFF_H = 81920;               // H^T    IL R=128 x 128
+constexpr int OFF_DH = 114688;             // dH^T   IL R=128 x 128
+constexpr int OFF_X = 147456;              // X      IL R=64 x 64
+constexpr int OFF_R = 155648;              // R (IL R=64 x 128) -> Y [0,8K) + Mg [8K,16K)
+constexpr int OFF_DUP = 172032;            // dU'^T -> U'^T (IL R=128 x 64)
+constexpr int OFF_LX = 188416;             // L/X fp32 -> G fp32 -> dk staging
+constexpr int OFF_T = OFF_LX + C * LS * 4; // T -> dX   ([T|A] = dq staging, 16 KB)
+constexpr int OFF_A = OFF_T + 8192;        // A -> dA
+constexpr int OFF_VEC = OFF_A + 8192;      // beta, r, s, nq, nk, db1[2], dot[2]
+constexpr int SMEM_BYTES = OFF_VEC + 9 * C * 4;
+static_assert(SMEM_BYTES <= 232448 - 1024, "shared memory budget");
 
 // ---- TMEM column map (512 columns)
-constexpr uint32_t TM_DH = 0;                       // dH^T, M=128
-constexpr uint32_t TM_GKK = 128, TM_Y = 128 | LO16; // M=64 pair
-constexpr uint32_t TM_GQK = 192, TM_DA = 192, TM_GB = 192, TM_DX = 192 | LO16;
-constexpr uint32_t TM_W = 256, TM_DU = 256, TM_U = 320;   // M=128 (B1-B3)
-constexpr uint32_t TM_P = 256, TM_DK = 256 | LO16;        // M=64 pair, 128 cols (B4-)
-constexpr uint32_t TM_R = 384, TM_DQ = 384;               // M=64, 128 cols
+constexpr uint32_t TM_DH = 0;                            // dH^T, M=128
+constexpr uint32_t TM_G = 128;                           // G_qk | G_kk (lane+16)
+constexpr uint32_t TM_R = 192, TM_P = 192 | LO16;        // K H | P     (M=64, 128 cols)
+constexpr uint32_t TM_DK = 192, TM_DQ = 192 | LO16;      // dK | dQ     (after P5)
+constexpr uint32_t TM_DU = 320;                          // dU'^T, M=128 (M1-P3)
+constexpr uint32_t TM_DX = 320, TM_GB = 320;             // dX' (M3-P5), G (M6-P7)
+constexpr uint32_t TM_W = 384;                           // W^T, M=128 (M3-P4)
+constexpr uint32_t TM_DA = 384, TM_Y = 384 | LO16;       // dA | Y (M5-P6)
+constexpr uint32_t TM_U = 448;                           // U^T -> U'^T, M=128
+
+enum { BAR_P = 1, BAR_S = 2 };
+enum { MB_G, MB_R, MB_DU, MB_W, MB_P, MB_U, MB_A, MB_Q, MB_K, MB_N };
+
+__device__ __forceinline__ void ld32(uint32_t tm, int wwarp, uint32_t col, float (&f)[32]) {
+  uint32_t r[2][16];
+  tmem_ld16(taddr(tm, wwarp * 32, col), r[0]);
+  tmem_ld16(taddr(tm, wwarp * 32, col + 16), r[1]);
+  tmem_ld_wait();
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 16; ++j) f[16 * i + j] = __uint_as_float(r[i][j]);
+}
+__device__ __forceinline__ void ld16f(uint32_t tm, int wwarp, uint32_t col, float (&f)[16]) {
+  uint32_t r[16];
+  tmem_ld16(taddr(tm, wwarp * 32, col), r);
+  tmem_ld_wait();
+#pragma unroll
+  for (int j = 0; j < 16; ++j) f[j] = __uint_as_float(r[j]);
+}
 
 __global__ void __launch_bounds__(NT, 1)
     tc_bwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
@@ -68,35 +97,33 @@ __global__ void __launch_bounds__(NT, 1)
                   const __grid_constant__ CUtensorMap mDQ, const __grid_constant__ CUtensorMap mDK,
                   const __grid_constant__ CUtensorMap mDV, Args a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bar_tma, bar_mma;
+  __shared__ uint64_t bar_tma, mb[MB_N];
   __shared__ uint32_t tslot;
-  uint8_t *sQ = smem + OFF_Q, *sK = smem + OFF_K, *sDO = smem + OFF_DO, *sH = smem + OFF_H,
-          *sDH = smem + OFF_DH, *sUP = smem + OFF_UP, *sX = smem + OFF_X, *sW = smem + OFF_W,
-          *sV = smem + OFF_V;
-  float* Ls = reinterpret_cast<float*>(smem + S_L);
-  float* Xs = reinterpret_cast<float*>(smem + S_X);
-  uint8_t* sT = smem + S_T;
-  uint8_t* sA = smem + S_A;
-  uint8_t* sDUP = smem + S_L;  // after the substitution
-  uint8_t* sR = smem + S_X;
-  uint8_t* sDA = smem + S_T;
-  uint8_t* sDX = smem + S_A;
-  uint8_t* sY = smem + S_L;          // after B4
-  uint8_t* sMG = smem + S_L + 8192;  // after B4
-  float* Gs = reinterpret_cast<float*>(smem + S_X);  // after B4
-  uint8_t* sDV = sV;
-  uint8_t* sDQo = sH;
-  uint8_t* sDKo = sDH;
-  float* sb = reinterpret_cast<float*>(smem + OFF_B);  // beta
-  float* sr = sb + C;                                   // 1/max(||q||,eps) (0: padded)
-  float* ss = sr + C;                                   // 1/max(||k||,eps)
-  float* nq = ss + C;                                   // ||q||
-  float* nk = nq + C;                                   // ||k||
-  float* sdb = nk + C;                                  // dbeta partial
+  uint8_t *sQ = smem + OFF_Q, *sDO = smem + OFF_DO, *sV = smem + OFF_V, *sH = smem + OFF_H,
+          *sDH = smem + OFF_DH, *sX = smem + OFF_X, *sR = smem + OFF_R, *sDUP = smem + OFF_DUP,
+          *sT = smem + OFF_T, *sA = smem + OFF_A;
+  float* LX = reinterpret_cast<float*>(smem + OFF_LX);
+  uint8_t* sUP = sDUP;             // U'^T after the dH update consumed dU'^T
+  uint8_t* sDV = sV;               // dV staging (in place over V)
+  uint8_t* sDX = sT;               // dX after M3
+  uint8_t* sDA = sA;               // dA after M2
+  uint8_t* sY = sR;                // after M3
+  uint8_t* sMG = sR + 8192;
+  float* Gs = LX;                  // after the substitution
+  uint8_t* sDQo = sT;              // [T|A] 16 KB
+  uint8_t* sDKo = smem + OFF_LX;
+  float* sb = reinterpret_cast<float*>(smem + OFF_VEC);  // beta
+  float* sr = sb + C;        // 1/max(||q||,eps) (0: padded)
+  float* ss = sr + C;        // 1/max(||k||,eps)
+  float* nq = ss + C;        // ||q||
+  float* nk = nq + C;        // ||k||
+  float* db1 = nk + C;       // [2][64] rowsum(P . R) partials
+  float* sdot = db1 + 2 * C; // [2][64] dk-adjoint dot partials
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int r64 = warp * 16 + (lane & 15);  // M=64 accumulator row of this lane
-  const bool lo = lane < 16;                // lane+0 accumulator (else lane+16)
+  const int wg = tid >> 7, w = tid & 127, wwarp = w >> 5;
+  const int r64 = wwarp * 16 + (lane & 15);  // M=64 accumulator row of this lane
+  const bool lo = lane < 16;
   const int unit = blockIdx.x;
   const int L = a.L, NC = a.NC;
   const bool l2 = (a.flags & DELTANET_L2NORM_QK) != 0;
@@ -108,68 +135,73 @@ __global__ void __launch_bounds__(NT, 1)
   if (warp == 0) tmem_alloc<512>(&tslot);
   if (tid == 0) {
     mbar_init(&bar_tma, 1);
-    mbar_init(&bar_mma, 1);
+    for (int i = 0; i < MB_N; ++i) mbar_init(&mb[i], 1);
     mbar_fence_init();
+    prefetch_tmap(&mQ);
+    prefetch_tmap(&mK);
+    prefetch_tmap(&mV);
+    prefetch_tmap(&mDO);
+    prefetch_tmap(&mDQ);
+    prefetch_tmap(&mDK);
+    prefetch_tmap(&mDV);
   }
   cta_sync();
   const uint32_t tm = tslot;
-  uint32_t ph_tma = 0, ph_mma = 0;
-  auto mma_wait = [&]() {
-    mbar_wait(&bar_mma, ph_mma);
-    ph_mma ^= 1;
-    fence_after_sync();
+
+  auto issue_loads = [&](int c, int ks) {  // one thread
+    mbar_expect_tx(&bar_tma, 4 * TILE + D * D * 2);
+    tma_load_4d(sQ, &mQ, 0, c * C, 0, unit, &bar_tma);
+    tma_load_4d(smem + OFF_KW + ks * TILE, &mK, 0, c * C, 0, unit, &bar_tma);
+    tma_load_4d(sDO, &mDO, 0, c * C, 0, unit, &bar_tma);
+    tma_load_4d(sV, &mV, 0, c * C, 0, unit, &bar_tma);
+    bulk_load(sH, states + (size_t)c * D * D * 2, D * D * 2, &bar_tma);
   };
 
-  // dH^T <- dhT^T (lane dv = tid)
+  // dH^T <- dhT^T (lane dv = w; columns split by warpgroup)
   {
     const float* dhT = a.dhT ? a.dhT + (size_t)unit * D * D : nullptr;
 #pragma unroll 1
-    for (int c0 = 0; c0 < D; c0 += 16) {
+    for (int c0 = 64 * wg; c0 < 64 * wg + 64; c0 += 16) {
       uint32_t r[16];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(dhT ? dhT[(size_t)(c0 + j) * D + tid] : 0.f);
-      tmem_st16(taddr(tm, warp * 32, TM_DH + c0), r);
+      for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(dhT ? dhT[(size_t)(c0 + j) * D + w] : 0.f);
+      tmem_st16(taddr(tm, wwarp * 32, TM_DH + c0), r);
     }
     tmem_st_wait();
   }
+  if (tid == 0 && NC > 0) issue_loads(NC - 1, 0);
   cta_sync();
 
-  const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aDO = smem_u32(sDO), aH = smem_u32(sH),
-                 aDH = smem_u32(sDH), aUP = smem_u32(sUP), aX = smem_u32(sX),
-                 aW = smem_u32(sW), aV = smem_u32(sV), aT = smem_u32(sT), aA = smem_u32(sA),
-                 aDUP = smem_u32(sDUP), aR = smem_u32(sR), aDA = smem_u32(sDA),
-                 aDX = smem_u32(sDX), aY = smem_u32(sY), aMG = smem_u32(sMG),
-                 aDV = smem_u32(sDV);
+  const uint32_t aQ = smem_u32(sQ), aDO = smem_u32(sDO), aH = smem_u32(sH),
+                 aDH = smem_u32(sDH), aX = smem_u32(sX), aV = smem_u32(sV), aT = smem_u32(sT),
+                 aA = smem_u32(sA), aDUP = smem_u32(sDUP), aR = smem_u32(sR),
+                 aDA = smem_u32(sDA), aDX = smem_u32(sDX), aY = smem_u32(sY),
+                 aMG = smem_u32(sMG), aDV = smem_u32(sDV), aUP = smem_u32(sUP);
 
 #pragma unroll 1
-  for (int c = NC - 1; c >= 0; --c) {
-    const int t0 = c * C;
-    // ---------------- L0: loads (previous chunk's stores must be done reading smem)
-    if (tid == 0) {
-      bulk_wait_read0();
-      mbar_expect_tx(&bar_tma, 4 * C * D * 2 + D * D * 2);
-      tma_load_4d(sQ, &mQ, 0, t0, 0, unit, &bar_tma);
-      tma_load_4d(sK, &mK, 0, t0, 0, unit, &bar_tma);
-      tma_load_4d(sV, &mV, 0, t0, 0, unit, &bar_tma);
-      tma_load_4d(sDO, &mDO, 0, t0, 0, unit, &bar_tma);
-      bulk_load(sH, states + (size_t)c * D * D * 2, D * D * 2, &bar_tma);
-    }
-    __syncthreads();
+  for (int it = 0; it < NC; ++it) {
+    const int c = NC - 1 - it, t0 = c * C, ks = it & 1;
+    const uint32_t ph = it & 1;
+    uint8_t* sK = smem + OFF_KW + ks * TILE;
+    uint8_t* sW = smem + OFF_KW + (1 - ks) * TILE;
+    const uint32_t aK = smem_u32(sK), aW = smem_u32(sW);
+
+    // ================= P1: dH image, loads, row norms, in-place normalisation
+    if (tid == 0) bulk_wait_read0();  // previous dk store done reading the LX region
     if (tid < C) sb[tid] = (t0 + tid < L) ? __bfloat162float(beta[t0 + tid]) : 0.f;
-    {  // L1: dH^T (dl/dH_{c+1}) -> bf16 image for this chunk's MMAs
+    if (wg == 1) {  // dH^T (dl/dH_{c+1}) -> bf16 image
 #pragma unroll 1
       for (int half = 0; half < 2; ++half) {
         float f[64];
-        ld64(tm, warp, TM_DH + 64 * half, f);
+        ld64(tm, wwarp, TM_DH + 64 * half, f);
 #pragma unroll
-        for (int g = 0; g < 8; ++g) il_store8(sDH, D, tid, 64 * half + g * 8, f + g * 8);
+        for (int g = 0; g < 8; ++g) il_store8(sDH, D, w, 64 * half + g * 8, f + g * 8);
       }
     }
-    mbar_wait(&bar_tma, ph_tma);
-    ph_tma ^= 1;
-    {  // normalise q (tid < 64) / k (tid >= 64) rows in place (R9)
-      const int row = tid & 63;
-      uint8_t* tile = tid < 64 ? sQ : sK;
+    mbar_wait(&bar_tma, ph);
+    if (wg == 0) {  // w < 64: q row w; w >= 64: k row w-64
+      const int row = w & 63;
+      const uint8_t* tile = w < 64 ? sQ : sK;
       float acc = 0.f;
 #pragma unroll
       for (int g = 0; g < D / 8; ++g) {
@@ -181,181 +213,112 @@ __global__ void __launch_bounds__(NT, 1)
       const float n = sqrtf(acc);
       float inv = l2 ? 1.f / fmaxf(n, eps) : 1.f;
       if (t0 + row >= L) inv = 0.f;
-      if (l2) {
+      (w < 64 ? sr : ss)[row] = inv;
+      (w < 64 ? nq : nk)[row] = n;
+    }
+    __syncthreads();
+    if (l2) {  // normalise rows in place (row = w, columns split by warpgroup)
+      const int row = w & 63;
+      uint8_t* tile = w < 64 ? sQ : sK;
+      const float inv = (w < 64 ? sr : ss)[row];
 #pragma unroll
-        for (int g = 0; g < D / 8; ++g) {
-          float x[8];
-          il_load8(tile, C, row, g * 8, x);
+      for (int g = 8 * wg; g < 8 * wg + 8; ++g) {
+        float x[8];
+        il_load8(tile, C, row, g * 8, x);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) x[e] *= inv;
-          il_store8(tile, C, row, g * 8, x);
-        }
+        for (int e = 0; e < 8; ++e) x[e] *= inv;
+        il_store8(tile, C, row, g * 8, x);
       }
-      (tid < 64 ? sr : ss)[row] = inv;
-      (tid < 64 ? nq : nk)[row] = n;
     }
     fence_proxy_async();
     cta_sync();
 
-    // ---------------- B1: Gram (M=64): Q K^T, K K^T
+    // ================= M1: Gram | K H, dH^T K^T
     if (tid == 0) {
-      const uint32_t id = idesc_bf16(64, 64, false, false);
+      const uint32_t idg = idesc_bf16(64, 64, false, false);
+      const uint32_t idr = idesc_bf16(64, 128, false, false);
+      const uint32_t idd = idesc_bf16(128, 64, false, false);
 #pragma unroll
       for (int k0 = 0; k0 < D; k0 += 16) {
-        mma_bf16(tm + TM_GQK, desc_k(aQ, C, k0), desc_k(aK, C, k0), id, k0 > 0);
-        mma_bf16(tm + TM_GKK, desc_k(aK, C, k0), desc_k(aK, C, k0), id, k0 > 0);
+        mma_bf16(tm + TM_G, desc_k(aQ, C, k0), desc_k(aK, C, k0), idg, k0 > 0);
+        mma_bf16(tm + TM_G + LO16, desc_k(aK, C, k0), desc_k(aK, C, k0), idg, k0 > 0);
       }
-      mma_commit(&bar_mma);
+      mma_commit(&mb[MB_G]);
+#pragma unroll
+      for (int k0 = 0; k0 < D; k0 += 16) {
+        mma_bf16(tm + TM_R, desc_k(aK, C, k0), desc_k(aH, D, k0), idr, k0 > 0);
+        mma_bf16(tm + TM_DU, desc_k(aDH, D, k0), desc_k(aK, C, k0), idd, k0 > 0);
+      }
+      mma_commit(&mb[MB_R]);
     }
-    mma_wait();
+
+    // ================= P2: A = tril(Q K^T) -> bf16; L = beta_i (k_i . k_j), j < i
+    mbar_wait(&mb[MB_G], ph);
+    fence_after_sync();
     {
-      float f[64];
-      ld64(tm, warp, TM_GQK, f);
+      float f[32];
+      ld32(tm, wwarp, TM_G + 32 * wg, f);  // lanes<16: G_qk row, lanes>=16: G_kk row
+      const int i = r64;
       if (lo) {
 #pragma unroll
-        for (int g = 0; g < 8; ++g) {
+        for (int g = 0; g < 4; ++g) {
           float x[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) x[e] = (g * 8 + e <= r64) ? f[g * 8 + e] : 0.f;
-          il_store8(sA, C, r64, g * 8, x);
+          for (int e = 0; e < 8; ++e) {
+            const int j = 32 * wg + g * 8 + e;
+            x[e] = (j <= i) ? f[g * 8 + e] : 0.f;
+          }
+          il_store8(sA, C, i, 32 * wg + g * 8, x);
         }
-      }
-      ld64(tm, warp, TM_GKK, f);
-      if (lo) {
-        const float bi = sb[r64];
+      } else {
+        const float bi = sb[i];
 #pragma unroll
-        for (int j = 0; j < 64; j += 4) {
+        for (int j = 0; j < 32; j += 4) {
+          const int jj = 32 * wg + j;
           float4 v;
-          v.x = (j + 0 < r64) ? bi * f[j + 0] : 0.f;
-          v.y = (j + 1 < r64) ? bi * f[j + 1] : 0.f;
-          v.z = (j + 2 < r64) ? bi * f[j + 2] : 0.f;
-          v.w = (j + 3 < r64) ? bi * f[j + 3] : 0.f;
-          *reinterpret_cast<float4*>(Ls + r64 * LS + j) = v;
+          v.x = (jj + 0 < i) ? bi * f[j + 0] : 0.f;
+          v.y = (jj + 1 < i) ? bi * f[j + 1] : 0.f;
+          v.z = (jj + 2 < i) ? bi * f[j + 2] : 0.f;
+          v.w = (jj + 3 < i) ? bi * f[j + 3] : 0.f;
+          *reinterpret_cast<float4*>(LX + i * LS + jj) = v;
         }
       }
     }
-    __syncthreads();
-    // substitution X = (I + L)^{-1} (same blocking as the forward kernel)
-    if (tid < 64) {
-      const int b = tid >> 5, j = lane, o = 32 * b;
-      float x[32];
+    fence_proxy_async();
+    cta_sync();
+
+    // ================= M2: dU'^T += dO^T A
+    if (tid == 0) {
+      const uint32_t ida = idesc_bf16(128, 64, true, true);
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        float acc = 0.f;
-#pragma unroll
-        for (int m = 0; m < i; m += 4) {
-          const float4 l4 = *reinterpret_cast<const float4*>(Ls + (o + i) * LS + o + m);
-          acc = fmaf(l4.x, x[m], acc);
-          if (m + 1 < i) acc = fmaf(l4.y, x[m + 1], acc);
-          if (m + 2 < i) acc = fmaf(l4.z, x[m + 2], acc);
-          if (m + 3 < i) acc = fmaf(l4.w, x[m + 3], acc);
-        }
-        x[i] = (i == j) ? 1.f : ((i < j) ? 0.f : -acc);
-      }
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        Xs[(o + i) * LS + o + j] = x[i];
-        Xs[(o + i) * LS + (32 - o) + j] = 0.f;
-      }
+      for (int k0 = 0; k0 < C; k0 += 16)
+        mma_bf16(tm + TM_DU, desc_mn(aDO, C, k0), desc_mn(aA, C, k0), ida, 1);
+      mma_commit(&mb[MB_DU]);
     }
-    __syncthreads();
-    {
-      const int j = lane, i0 = warp * 8;
-      float y[8];
-#pragma unroll
-      for (int ii = 0; ii < 8; ++ii) y[ii] = 0.f;
-#pragma unroll 4
-      for (int m = 0; m < 32; ++m) {
-        const float xm = Xs[m * LS + j];
-#pragma unroll
-        for (int ii = 0; ii < 8; ++ii) y[ii] = fmaf(Ls[(32 + i0 + ii) * LS + m], xm, y[ii]);
-      }
-#pragma unroll
-      for (int ii = 0; ii < 8; ++ii) Ls[(i0 + ii) * LS + 32 + j] = y[ii];
-    }
-    __syncthreads();
-    {
-      const int j = lane, i0 = warp * 8;
-      float y[8];
-#pragma unroll
-      for (int ii = 0; ii < 8; ++ii) y[ii] = 0.f;
-#pragma unroll 4
-      for (int m = 0; m < 32; ++m) {
-        const float ym = Ls[m * LS + 32 + j];
-#pragma unroll
-        for (int ii = 0; ii < 8; ++ii) y[ii] = fmaf(Xs[(32 + i0 + ii) * LS + 32 + m], ym, y[ii]);
-      }
-#pragma unroll
-      for (int ii = 0; ii < 8; ++ii) Xs[(32 + i0 + ii) * LS + j] = -y[ii];
-    }
-    __syncthreads();
-    {  // X -> bf16 sX;  T = X diag(beta) -> bf16 sT
-      const int i = tid >> 1, j0 = (tid & 1) * 32;
+
+    // ================= P3: wg0 substitution + X, T | wg1 R and dU' conversions
+    if (wg == 0) {
+      ut_inverse_inplace<LS>(LX, w, BAR_P);
+      const int i = w >> 1, j0 = (w & 1) * 32;
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
         float x[8], y[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const int j = j0 + g * 8 + e;
-          x[e] = Xs[i * LS + j];
+          x[e] = (j <= i) ? LX[i * LS + j] : 0.f;
           y[e] = x[e] * sb[j];
         }
         il_store8(sX, C, i, j0 + g * 8, x);
         il_store8(sT, C, i, j0 + g * 8, y);
       }
-    }
-    fence_proxy_async();
-    cta_sync();
-
-    // ---------------- B1b: W^T = K^T T^T, U^T = V^T T^T (M=128, N=64, K=64)
-    if (tid == 0) {
-      const uint32_t id = idesc_bf16(128, 64, true, false);
-#pragma unroll
-      for (int k0 = 0; k0 < C; k0 += 16) {
-        mma_bf16(tm + TM_W, desc_mn(aK, C, k0), desc_k(aT, C, k0), id, k0 > 0);
-        mma_bf16(tm + TM_U, desc_mn(aV, C, k0), desc_k(aT, C, k0), id, k0 > 0);
-      }
-      mma_commit(&bar_mma);
-    }
-    mma_wait();
-    {
-      float f[64];
-      ld64(tm, warp, TM_W, f);
-#pragma unroll
-      for (int g = 0; g < 8; ++g) il_store8(sW, D, tid, g * 8, f + g * 8);
-    }
-    fence_proxy_async();
-    cta_sync();
-
-    // ---------------- B2: U' = U - W H ; K H (for R) ; dU'^T = dH^T K^T + dO^T A
-    if (tid == 0) {
-      const uint32_t idn = idesc_bf16(128, 64, false, true, true);
-      const uint32_t idr = idesc_bf16(64, 128, false, false);
-      const uint32_t idd = idesc_bf16(128, 64, false, false);
-      const uint32_t ida = idesc_bf16(128, 64, true, true);
-#pragma unroll
-      for (int k0 = 0; k0 < D; k0 += 16) {
-        mma_bf16(tm + TM_U, desc_k(aH, D, k0), desc_mn(aW, D, k0), idn, 1);
-        mma_bf16(tm + TM_R, desc_k(aK, C, k0), desc_k(aH, D, k0), idr, k0 > 0);
-        mma_bf16(tm + TM_DU, desc_k(aDH, D, k0), desc_k(aK, C, k0), idd, k0 > 0);
-      }
-#pragma unroll
-      for (int k0 = 0; k0 < C; k0 += 16)
-        mma_bf16(tm + TM_DU, desc_mn(aDO, C, k0), desc_mn(aA, C, k0), ida, 1);
-      mma_commit(&bar_mma);
-    }
-    mma_wait();
-    {  // B3: U'^T, dU'^T -> bf16 (rows d_v);  R = V - K H -> bf16 (rows t)
-      float f[64];
-      ld64(tm, warp, TM_U, f);
-#pragma unroll
-      for (int g = 0; g < 8; ++g) il_store8(sUP, D, tid, g * 8, f + g * 8);
-      ld64(tm, warp, TM_DU, f);
-#pragma unroll
-      for (int g = 0; g < 8; ++g) il_store8(sDUP, D, tid, g * 8, f + g * 8);
+    } else {
+      mbar_wait(&mb[MB_R], ph);
+      fence_after_sync();
 #pragma unroll 1
-      for (int half = 0; half < 2; ++half) {
-        ld64(tm, warp, TM_R + 64 * half, f);
+      for (int half = 0; half < 2; ++half) {  // R = V - K H (rows r64, lanes < 16)
+        float f[64];
+        ld64(tm, wwarp, TM_R + 64 * half, f);
         if (lo) {
 #pragma unroll
           for (int g = 0; g < 8; ++g) {
@@ -367,113 +330,186 @@ __global__ void __launch_bounds__(NT, 1)
           }
         }
       }
+      mbar_wait(&mb[MB_DU], ph);
+      fence_after_sync();
+      {  // dU'^T (lane d_v = w) -> bf16
+        float f[64];
+        ld64(tm, wwarp, TM_DU, f);
+#pragma unroll
+        for (int g = 0; g < 8; ++g) il_store8(sDUP, D, w, g * 8, f + g * 8);
+      }
     }
     fence_proxy_async();
     cta_sync();
 
-    // ---------------- B4: dA, P, dX, dH update, dK += U' dH^T
+    // ================= M3: W, U | P = X^T dU', dX' = dU' R^T
     if (tid == 0) {
-      const uint32_t id_da = idesc_bf16(64, 64, false, true);
-      const uint32_t id_p = idesc_bf16(64, 128, true, false);
-      const uint32_t id_dx = idesc_bf16(64, 64, true, false);
-      const uint32_t id_h1 = idesc_bf16(128, 128, true, true);
-      const uint32_t id_h2 = idesc_bf16(128, 128, false, false, true);
-      const uint32_t id_dk = idesc_bf16(64, 128, true, true);
-#pragma unroll
-      for (int k0 = 0; k0 < D; k0 += 16) {
-        mma_bf16(tm + TM_DA, desc_k(aDO, C, k0), desc_mn(aUP, D, k0), id_da, k0 > 0);
-        mma_bf16(tm + TM_DX, desc_mn(aDUP, D, k0), desc_k(aR, C, k0), id_dx, k0 > 0);
-        mma_bf16(tm + TM_DK, desc_mn(aUP, D, k0), desc_mn(aDH, D, k0), id_dk, k0 > 0);
-      }
+      const uint32_t idw = idesc_bf16(128, 64, true, false);
+      const uint32_t idp = idesc_bf16(64, 128, true, false);
+      const uint32_t idx = idesc_bf16(64, 64, true, false);
 #pragma unroll
       for (int k0 = 0; k0 < C; k0 += 16) {
-        mma_bf16(tm + TM_P, desc_mn(aX, C, k0), desc_k(aDUP, D, k0), id_p, k0 > 0);
-        mma_bf16(tm + TM_DH, desc_mn(aDO, C, k0), desc_mn(aQ, C, k0), id_h1, 1);
-        mma_bf16(tm + TM_DH, desc_k(aDUP, D, k0), desc_k(aW, D, k0), id_h2, 1);
+        mma_bf16(tm + TM_W, desc_mn(aK, C, k0), desc_k(aT, C, k0), idw, k0 > 0);
+        mma_bf16(tm + TM_U, desc_mn(aV, C, k0), desc_k(aT, C, k0), idw, k0 > 0);
       }
-      mma_commit(&bar_mma);
+      mma_commit(&mb[MB_W]);
+#pragma unroll
+      for (int k0 = 0; k0 < C; k0 += 16)
+        mma_bf16(tm + TM_P, desc_mn(aX, C, k0), desc_k(aDUP, D, k0), idp, k0 > 0);
+#pragma unroll
+      for (int k0 = 0; k0 < D; k0 += 16)
+        mma_bf16(tm + TM_DX, desc_mn(aDUP, D, k0), desc_k(aR, C, k0), idx, k0 > 0);
+      mma_commit(&mb[MB_P]);
     }
-    mma_wait();
+
+    // ================= P4: W^T -> bf16 (row dk, columns split)
+    mbar_wait(&mb[MB_W], ph);
+    fence_after_sync();
     {
-      float f[64];
-      ld64(tm, warp, TM_DA, f);  // lanes<16: dA row r64; lanes>=16: dX' row r64
-      if (lo) {
+      float f[32];
+      ld32(tm, wwarp, TM_W + 32 * wg, f);
 #pragma unroll
-        for (int g = 0; g < 8; ++g) {
-          float x[8];
+      for (int g = 0; g < 4; ++g) il_store8(sW, D, w, 32 * wg + g * 8, f + g * 8);
+    }
+    fence_proxy_async();
+    cta_sync();
+
+    // ================= M4: dH += Q^T dO - W^T dU' ; U' = U - W H
+    if (tid == 0) {
+      const uint32_t id1 = idesc_bf16(128, 128, true, true);
+      const uint32_t id2 = idesc_bf16(128, 128, false, false, true);
+      const uint32_t idn = idesc_bf16(128, 64, false, true, true);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) x[e] = (g * 8 + e <= r64) ? f[g * 8 + e] : 0.f;
-          il_store8(sDA, C, r64, g * 8, x);
-        }
-      } else {
-#pragma unroll
-        for (int g = 0; g < 8; ++g) {
-          float x[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) x[e] = f[g * 8 + e] * sb[g * 8 + e];
-          il_store8(sDX, C, r64, g * 8, x);
-        }
+      for (int k0 = 0; k0 < C; k0 += 16) {
+        mma_bf16(tm + TM_DH, desc_mn(aDO, C, k0), desc_mn(aQ, C, k0), id1, 1);
+        mma_bf16(tm + TM_DH, desc_k(aDUP, D, k0), desc_k(aW, D, k0), id2, 1);
       }
-      float db = 0.f;
+#pragma unroll
+      for (int k0 = 0; k0 < D; k0 += 16)
+        mma_bf16(tm + TM_U, desc_k(aH, D, k0), desc_mn(aW, D, k0), idn, 1);
+      mma_commit(&mb[MB_U]);
+    }
+
+    // ================= P5: U'^T -> bf16 ; P, R -> dV, dbeta part ; dX
+    mbar_wait(&mb[MB_U], ph);
+    mbar_wait(&mb[MB_P], ph);
+    fence_after_sync();
+    {
+      float f[32];
+      ld32(tm, wwarp, TM_U + 32 * wg, f);
+#pragma unroll
+      for (int g = 0; g < 4; ++g) il_store8(sUP, D, w, 32 * wg + g * 8, f + g * 8);
+    }
+    {
       const float bt = sb[r64];
+      float db = 0.f;
 #pragma unroll 1
-      for (int half = 0; half < 2; ++half) {
-        float p[64];
-        ld64(tm, warp, TM_P + 64 * half, p);  // lanes<16: P row
-        ld64(tm, warp, TM_R + 64 * half, f);  // lanes<16: (K H) row
+      for (int cc = 0; cc < 4; ++cc) {
+        const int col = 64 * wg + 16 * cc;
+        float f[16], p[16];
+        ld16f(tm, wwarp, TM_R + col, f);  // lanes<16: (K H) row; lanes>=16: P row
+#pragma unroll
+        for (int e = 0; e < 16; ++e) p[e] = __shfl_xor_sync(0xffffffffu, f[e], 16);
         if (lo) {
 #pragma unroll
-          for (int g = 0; g < 8; ++g) {
+          for (int g = 0; g < 2; ++g) {
             float v8[8], dv8[8];
-            il_load8(sV, C, r64, 64 * half + g * 8, v8);
+            il_load8(sV, C, r64, col + g * 8, v8);
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
               db = fmaf(p[g * 8 + e], v8[e] - f[g * 8 + e], db);  // P . R
               dv8[e] = bt * p[g * 8 + e];
             }
-            il_store8(sDV, C, r64, 64 * half + g * 8, dv8);
+            il_store8(sDV, C, r64, col + g * 8, dv8);
           }
         }
       }
-      if (lo) sdb[r64] = db;
+      if (lo) db1[wg * C + r64] = db;
+    }
+    {
+      float f[32];
+      ld32(tm, wwarp, TM_DX + 32 * wg, f);  // lanes<16: dX' row
+      if (lo) {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          float x[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) x[e] = f[g * 8 + e] * sb[32 * wg + g * 8 + e];
+          il_store8(sDX, C, r64, 32 * wg + g * 8, x);
+        }
+      }
     }
     fence_proxy_async();
     cta_sync();
     if (tid == 0) {
       tma_store_4d(&mDV, sDV, 0, t0, 0, unit);
       bulk_commit();
-    }
-
-    // ---------------- B5: dQ = dO H^T + dA K ; dK += dA^T Q - dV H^T ; Y = X^T dX
-    if (tid == 0) {
-      const uint32_t id_q1 = idesc_bf16(64, 128, false, true);
+      // ================= M5: dA, Y, dQ = dO H^T, dK = U' dH^T - dV H^T
+      const uint32_t id_da = idesc_bf16(64, 64, false, true);
+      const uint32_t id_y = idesc_bf16(64, 64, true, true);
+      const uint32_t id_q = idesc_bf16(64, 128, false, true);
       const uint32_t id_k1 = idesc_bf16(64, 128, true, true);
       const uint32_t id_k2 = idesc_bf16(64, 128, false, true, true);
-      const uint32_t id_y = idesc_bf16(64, 64, true, true);
+#pragma unroll
+      for (int k0 = 0; k0 < D; k0 += 16)
+        mma_bf16(tm + TM_DA, desc_k(aDO, C, k0), desc_mn(aUP, D, k0), id_da, k0 > 0);
+#pragma unroll
+      for (int k0 = 0; k0 < C; k0 += 16)
+        mma_bf16(tm + TM_Y, desc_mn(aX, C, k0), desc_mn(aDX, C, k0), id_y, k0 > 0);
+      mma_commit(&mb[MB_A]);
 #pragma unroll
       for (int k0 = 0; k0 < D; k0 += 16) {
-        mma_bf16(tm + TM_DQ, desc_k(aDO, C, k0), desc_mn(aH, D, k0), id_q1, k0 > 0);
+        mma_bf16(tm + TM_DQ, desc_k(aDO, C, k0), desc_mn(aH, D, k0), id_q, k0 > 0);
+        mma_bf16(tm + TM_DK, desc_mn(aUP, D, k0), desc_mn(aDH, D, k0), id_k1, k0 > 0);
         mma_bf16(tm + TM_DK, desc_k(aDV, C, k0), desc_mn(aH, D, k0), id_k2, 1);
       }
+    }
+
+    // ================= P6: dA -> bf16 (masked) | Y -> bf16
+    mbar_wait(&mb[MB_A], ph);
+    fence_after_sync();
+    {
+      float f[32];
+      ld32(tm, wwarp, TM_DA + 32 * wg, f);  // lanes<16: dA row, lanes>=16: Y row
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        float x[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int j = 32 * wg + g * 8 + e;
+          x[e] = (!lo || j <= r64) ? f[g * 8 + e] : 0.f;
+        }
+        il_store8(lo ? sDA : sY, C, r64, 32 * wg + g * 8, x);
+      }
+    }
+    fence_proxy_async();
+    cta_sync();
+
+    // ================= M6: dQ += dA K ; dK += dA^T Q ; G = -Y X^T
+    if (tid == 0) {
+      const uint32_t id_q = idesc_bf16(64, 128, false, true);
+      const uint32_t id_k = idesc_bf16(64, 128, true, true);
+      const uint32_t id_g = idesc_bf16(64, 64, false, false, true);
 #pragma unroll
       for (int k0 = 0; k0 < C; k0 += 16) {
-        mma_bf16(tm + TM_DQ, desc_k(aDA, C, k0), desc_mn(aK, C, k0), id_q1, 1);
-        mma_bf16(tm + TM_DK, desc_mn(aDA, C, k0), desc_mn(aQ, C, k0), id_k1, 1);
-        mma_bf16(tm + TM_Y, desc_mn(aX, C, k0), desc_mn(aDX, C, k0), id_y, k0 > 0);
+        mma_bf16(tm + TM_GB, desc_k(aY, C, k0), desc_k(aX, C, k0), id_g, k0 > 0);
+        mma_bf16(tm + TM_DQ, desc_k(aDA, C, k0), desc_mn(aK, C, k0), id_q, 1);
+        mma_bf16(tm + TM_DK, desc_mn(aDA, C, k0), desc_mn(aQ, C, k0), id_k, 1);
       }
-      mma_commit(&bar_mma);
+      mma_commit(&mb[MB_Q]);
     }
-    mma_wait();
-    {
-      // lanes<16: dq_hat row -> L2 adjoint -> dq staging; lanes>=16: Y row -> sY
-      float f[64];
+
+    // ================= P7: wg0 dq epilogue | wg1 G, dbeta, Mg
+    mbar_wait(&mb[MB_Q], ph);
+    fence_after_sync();
+    if (wg == 0) {
+      // lanes >= 16: dq_hat row r64 (TM_DQ) -> L2 adjoint -> dq staging
       float dot = 0.f;
-      const float inv = sr[r64];
-      const bool big = l2 && nq[r64] >= eps;
 #pragma unroll 1
       for (int half = 0; half < 2; ++half) {
-        ld64(tm, warp, TM_DQ + 64 * half, f);
-        if (lo) {
+        float f[64];
+        ld64(tm, wwarp, TM_R + 64 * half, f);  // lanes>=16 read TM_DQ
+        if (!lo) {
 #pragma unroll
           for (int g = 0; g < 8; ++g) {
             float q8[8];
@@ -483,11 +519,13 @@ __global__ void __launch_bounds__(NT, 1)
           }
         }
       }
-      if (!big) dot = 0.f;
+      const float inv = sr[r64];
+      if (!(l2 && nq[r64] >= eps)) dot = 0.f;
 #pragma unroll 1
       for (int half = 0; half < 2; ++half) {
-        ld64(tm, warp, TM_DQ + 64 * half, f);
-        if (lo) {
+        float f[64];
+        ld64(tm, wwarp, TM_R + 64 * half, f);
+        if (!lo) {
 #pragma unroll
           for (int g = 0; g < 8; ++g) {
             float q8[8];
@@ -499,48 +537,35 @@ __global__ void __launch_bounds__(NT, 1)
           }
         }
       }
-      ld64(tm, warp, TM_GKK, f);  // lanes>=16 see Y (TM_Y = TM_GKK | lane 16)
-      if (!lo) {
+    } else {
+      // lanes < 16: G row (TM_GB); K K^T row from lanes >= 16 (TM_G + lane 16)
+      float db2 = 0.f;
+#pragma unroll 1
+      for (int cc = 0; cc < 4; ++cc) {
+        float g16[16], k16[16], kk[16];
+        ld16f(tm, wwarp, TM_GB + 16 * cc, g16);
+        ld16f(tm, wwarp, TM_G + 16 * cc, k16);
 #pragma unroll
-        for (int g = 0; g < 8; ++g) il_store8(sY, C, r64, g * 8, f + g * 8);
-      }
-    }
-    fence_proxy_async();
-    cta_sync();
-    if (tid == 0) {
-      tma_store_4d(&mDQ, sDQo, 0, t0, 0, unit);
-      bulk_commit();
-      // ---------------- B7: G = -Y X^T (M=64, N=64, K=64)
-      const uint32_t id_g = idesc_bf16(64, 64, false, false, true);
+        for (int e = 0; e < 16; ++e) kk[e] = __shfl_xor_sync(0xffffffffu, k16[e], 16);
+        if (lo) {
 #pragma unroll
-      for (int k0 = 0; k0 < C; k0 += 16)
-        mma_bf16(tm + TM_GB, desc_k(aY, C, k0), desc_k(aX, C, k0), id_g, k0 > 0);
-      mma_commit(&bar_mma);
-    }
-    mma_wait();
-    {
-      // lanes<16: G row -> Gs (strict lower); dbeta += rowsum(G . K K^T)
-      float g64[64], kk[64];
-      ld64(tm, warp, TM_GB, g64);
-      ld64(tm, warp, TM_GKK, kk);
-      if (lo) {
-        float db = sdb[r64];
-#pragma unroll
-        for (int j = 0; j < 64; j += 4) {
-          float4 v;
-          v.x = (j + 0 < r64) ? g64[j + 0] : 0.f;
-          v.y = (j + 1 < r64) ? g64[j + 1] : 0.f;
-          v.z = (j + 2 < r64) ? g64[j + 2] : 0.f;
-          v.w = (j + 3 < r64) ? g64[j + 3] : 0.f;
-          db = fmaf(v.x, kk[j], fmaf(v.y, kk[j + 1], fmaf(v.z, kk[j + 2], fmaf(v.w, kk[j + 3], db))));
-          *reinterpret_cast<float4*>(Gs + r64 * LS + j) = v;
+          for (int j = 0; j < 16; j += 4) {
+            const int jj = 16 * cc + j;
+            float4 v;
+            v.x = (jj + 0 < r64) ? g16[j + 0] : 0.f;
+            v.y = (jj + 1 < r64) ? g16[j + 1] : 0.f;
+            v.z = (jj + 2 < r64) ? g16[j + 2] : 0.f;
+            v.w = (jj + 3 < r64) ? g16[j + 3] : 0.f;
+            db2 = fmaf(v.x, kk[j], fmaf(v.y, kk[j + 1], fmaf(v.z, kk[j + 2], fmaf(v.w, kk[j + 3], db2))));
+            *reinterpret_cast<float4*>(Gs + r64 * LS + jj) = v;
+          }
         }
-        if (t0 + r64 < L) dbeta[t0 + r64] = __float2bfloat16_rn(db);
       }
-    }
-    __syncthreads();
-    {  // Mg[i][j] = b_i G[i][j] + b_j G[j][i]  -> bf16 (row i, 32 columns per thread)
-      const int i = tid >> 1, j0 = (tid & 1) * 32;
+      if (lo && t0 + r64 < L)
+        dbeta[t0 + r64] = __float2bfloat16_rn(db1[r64] + db1[C + r64] + db2);
+      wg_sync(BAR_S);
+      // Mg[i][j] = b_i G[i][j] + b_j G[j][i]  (row i = w/2, 32 columns)
+      const int i = w >> 1, j0 = (w & 1) * 32;
       const float bi = sb[i];
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
@@ -555,48 +580,52 @@ __global__ void __launch_bounds__(NT, 1)
     }
     fence_proxy_async();
     cta_sync();
-    // ---------------- B9: dK += Mg K
+
+    // ================= M7: dK += Mg K ; prefetch chunk c-1
     if (tid == 0) {
+      tma_store_4d(&mDQ, sDQo, 0, t0, 0, unit);
+      bulk_commit();
       const uint32_t id_m = idesc_bf16(64, 128, false, true);
 #pragma unroll
       for (int k0 = 0; k0 < C; k0 += 16)
         mma_bf16(tm + TM_DK, desc_k(aMG, C, k0), desc_mn(aK, C, k0), id_m, 1);
-      mma_commit(&bar_mma);
-    }
-    mma_wait();
-    {
-      // lanes>=16: dk_hat row -> L2 adjoint -> dk staging
-      float f[64];
-      float dot = 0.f;
-      const float inv = ss[r64];
-      const bool big = l2 && nk[r64] >= eps;
-#pragma unroll 1
-      for (int half = 0; half < 2; ++half) {
-        ld64(tm, warp, TM_P + 64 * half, f);  // lanes>=16 read TM_DK
-        if (!lo) {
-#pragma unroll
-          for (int g = 0; g < 8; ++g) {
-            float k8[8];
-            il_load8(sK, C, r64, 64 * half + g * 8, k8);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) dot = fmaf(k8[e], f[g * 8 + e], dot);
-          }
-        }
+      mma_commit(&mb[MB_K]);
+      if (c > 0) {
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // dV store read done
+        issue_loads(c - 1, 1 - ks);
       }
-      if (!big) dot = 0.f;
-#pragma unroll 1
-      for (int half = 0; half < 2; ++half) {
-        ld64(tm, warp, TM_P + 64 * half, f);
-        if (!lo) {
+    }
+
+    // ================= P8: dK epilogue (columns split; row dot combined)
+    mbar_wait(&mb[MB_K], ph);
+    fence_after_sync();
+    {
+      float f[64];
+      ld64(tm, wwarp, TM_DK + 64 * wg, f);  // lanes<16: dk_hat row r64
+      float dot = 0.f;
+      if (lo) {
 #pragma unroll
-          for (int g = 0; g < 8; ++g) {
-            float k8[8];
-            il_load8(sK, C, r64, 64 * half + g * 8, k8);
+        for (int g = 0; g < 8; ++g) {
+          float k8[8];
+          il_load8(sK, C, r64, 64 * wg + g * 8, k8);
 #pragma unroll
-            for (int e = 0; e < 8; ++e)
-              k8[e] = l2 ? inv * (f[g * 8 + e] - k8[e] * dot) : f[g * 8 + e];
-            il_store8(sDKo, C, r64, 64 * half + g * 8, k8);
-          }
+          for (int e = 0; e < 8; ++e) dot = fmaf(k8[e], f[g * 8 + e], dot);
+        }
+        sdot[wg * C + r64] = dot;
+      }
+      __syncthreads();
+      if (lo) {
+        dot = sdot[r64] + sdot[C + r64];
+        if (!(l2 && nk[r64] >= eps)) dot = 0.f;
+        const float inv = ss[r64];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          float k8[8];
+          il_load8(sK, C, r64, 64 * wg + g * 8, k8);
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            k8[e] = l2 ? inv * (f[g * 8 + e] - k8[e] * dot) : f[g * 8 + e];
+          il_store8(sDKo, C, r64, 64 * wg + g * 8, k8);
         }
       }
     }
@@ -608,16 +637,14 @@ __global__ void __launch_bounds__(NT, 1)
     }
   }
 
-  // dh0 = dH (orientation [dk][dv]; lane dv = tid)
+  // dh0 = dH (orientation [dk][dv]; lane dv = w, columns split)
   if (a.dh0) {
+    fence_after_sync();
     float* dh0 = a.dh0 + (size_t)unit * D * D;
-#pragma unroll 1
-    for (int half = 0; half < 2; ++half) {
-      float f[64];
-      ld64(tm, warp, TM_DH + 64 * half, f);
+    float f[64];
+    ld64(tm, wwarp, TM_DH + 64 * wg, f);
 #pragma unroll
-      for (int e = 0; e < 64; ++e) dh0[(size_t)(64 * half + e) * D + tid] = f[e];
-    }
+    for (int e = 0; e < 64; ++e) dh0[(size_t)(64 * wg + e) * D + w] = f[e];
   }
   if (tid == 0) bulk_wait0();
   cta_sync();

@@ -265,18 +265,20 @@ __device__ __forceinline__ void wg_sync(int id) {
 
 // X = (I + L)^{-1} for a 64x64 strictly-lower L, in place in LX (fp32,
 // row stride LSTRIDE floats), by the 128 threads of one warpgroup (wtid).
-// Forward substitution on the two 32x32 diagonal blocks,
-// column-parallel in registers, then X21 = -X22 (L21 X11).  On return the
-// lower triangle and diagonal of LX hold X; the upper-right 32x32 block holds
-// scratch (callers mask j > i).
+// Level 1: forward substitution on the four 16x16
+// diagonal blocks, one warp per block, column-parallel in registers.
+// Levels 2-3: merge blocks pairwise, X21 = -X22 (L21 X11), for 16 -> 32 -> 64.
+// On return the lower triangle and diagonal of LX hold X; entries above the
+// diagonal hold scratch (callers mask j > i).
 template <int LSTRIDE>
-__device__ __forceinline__ void ut_inverse_inplace(float* LX, int wtid, int bar_id) {
+__device__ __forceinline__ void ut_inverse_inplace(float* LX, int wtid, int bar_id,
+                                                   long long* stamps = nullptr) {
   const int lane = wtid & 31, wwarp = wtid >> 5;
-  if (wwarp < 2) {
-    const int o = 32 * wwarp, j = lane;
-    float x[32];
+  {  // level 1: block q = wwarp, column j = lane (< 16)
+    const int o = 16 * wwarp, j = lane & 15;
+    float x[16];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
+    for (int i = 0; i < 16; ++i) {
       float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll
       for (int m = 0; m < i; m += 4) {
@@ -289,19 +291,65 @@ __device__ __forceinline__ void ut_inverse_inplace(float* LX, int wtid, int bar_
       x[i] = (i == j) ? 1.f : ((i < j) ? 0.f : -((a0 + a1) + (a2 + a3)));
     }
     __syncwarp();
+    if (lane < 16) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) LX[(o + i) * LSTRIDE + o + j] = x[i];
+      for (int i = 0; i < 16; ++i) LX[(o + i) * LSTRIDE + o + j] = x[i];
+    }
   }
   wg_sync(bar_id);
-  {  // Y = L21 X11 -> LX[0:32][32:64]
+  if (stamps && wtid == 0) stamps[0] = clock64();
+  {  // level 2, pairs p = 0, 1 at offset 32p: Y = L21 X11 -> LX[o:o+16][o+16:o+32]
+    const int o = 32 * (wtid >> 6), j = wtid & 15, i0 = ((wtid >> 4) & 3) * 4;
+    float y[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int m = 0; m < 16; m += 4) {
+      const float x0 = LX[(o + m + 0) * LSTRIDE + o + j], x1 = LX[(o + m + 1) * LSTRIDE + o + j],
+                  x2 = LX[(o + m + 2) * LSTRIDE + o + j], x3 = LX[(o + m + 3) * LSTRIDE + o + j];
+#pragma unroll
+      for (int ii = 0; ii < 4; ++ii) {
+        const float4 l4 =
+            *reinterpret_cast<const float4*>(LX + (o + 16 + i0 + ii) * LSTRIDE + o + m);
+        y[ii] = fmaf(l4.x, x0, fmaf(l4.y, x1, fmaf(l4.z, x2, fmaf(l4.w, x3, y[ii]))));
+      }
+    }
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii) LX[(o + i0 + ii) * LSTRIDE + o + 16 + j] = y[ii];
+    wg_sync(bar_id);
+  if (stamps && wtid == 0) stamps[1] = clock64();
+    // X21 = -X22 Y -> LX[o+16:o+32][o:o+16]
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii) y[ii] = 0.f;
+#pragma unroll
+    for (int m = 0; m < 16; m += 4) {
+      const float y0 = LX[(o + m + 0) * LSTRIDE + o + 16 + j],
+                  y1 = LX[(o + m + 1) * LSTRIDE + o + 16 + j],
+                  y2 = LX[(o + m + 2) * LSTRIDE + o + 16 + j],
+                  y3 = LX[(o + m + 3) * LSTRIDE + o + 16 + j];
+#pragma unroll
+      for (int ii = 0; ii < 4; ++ii) {
+        const float4 x4 =
+            *reinterpret_cast<const float4*>(LX + (o + 16 + i0 + ii) * LSTRIDE + o + 16 + m);
+        y[ii] = fmaf(x4.x, y0, fmaf(x4.y, y1, fmaf(x4.z, y2, fmaf(x4.w, y3, y[ii]))));
+      }
+    }
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii) LX[(o + 16 + i0 + ii) * LSTRIDE + o + j] = -y[ii];
+  }
+  wg_sync(bar_id);
+  if (stamps && wtid == 0) stamps[2] = clock64();
+  {  // level 3: Y = L21 X11 -> LX[0:32][32:64]
     const int j = lane, i0 = wwarp * 8;
     float y[8];
 #pragma unroll
     for (int ii = 0; ii < 8; ++ii) y[ii] = 0.f;
 #pragma unroll 2
     for (int m = 0; m < 32; m += 4) {
-      const float x0 = LX[(m + 0) * LSTRIDE + j], x1 = LX[(m + 1) * LSTRIDE + j],
-                  x2 = LX[(m + 2) * LSTRIDE + j], x3 = LX[(m + 3) * LSTRIDE + j];
+      // X11 is lower triangular; its upper-right 16x16 block holds level-2
+      // scratch, so entries above the diagonal are masked to zero.
+      const float x0 = (m + 0 >= j) ? LX[(m + 0) * LSTRIDE + j] : 0.f,
+                  x1 = (m + 1 >= j) ? LX[(m + 1) * LSTRIDE + j] : 0.f,
+                  x2 = (m + 2 >= j) ? LX[(m + 2) * LSTRIDE + j] : 0.f,
+                  x3 = (m + 3 >= j) ? LX[(m + 3) * LSTRIDE + j] : 0.f;
 #pragma unroll
       for (int ii = 0; ii < 8; ++ii) {
         const float4 l4 = *reinterpret_cast<const float4*>(LX + (32 + i0 + ii) * LSTRIDE + m);
@@ -312,6 +360,7 @@ __device__ __forceinline__ void ut_inverse_inplace(float* LX, int wtid, int bar_
     for (int ii = 0; ii < 8; ++ii) LX[(i0 + ii) * LSTRIDE + 32 + j] = y[ii];
   }
   wg_sync(bar_id);
+  if (stamps && wtid == 0) stamps[3] = clock64();
   {  // X21 = -X22 Y -> LX[32:64][0:32]
     const int j = lane, i0 = wwarp * 8;
     float y[8];
@@ -323,15 +372,20 @@ __device__ __forceinline__ void ut_inverse_inplace(float* LX, int wtid, int bar_
                   y2 = LX[(m + 2) * LSTRIDE + 32 + j], y3 = LX[(m + 3) * LSTRIDE + 32 + j];
 #pragma unroll
       for (int ii = 0; ii < 8; ++ii) {
+        // X22 lower triangular (its upper-right 16x16 block holds scratch)
+        const int r = i0 + ii;
         const float4 x4 =
-            *reinterpret_cast<const float4*>(LX + (32 + i0 + ii) * LSTRIDE + 32 + m);
-        y[ii] = fmaf(x4.x, y0, fmaf(x4.y, y1, fmaf(x4.z, y2, fmaf(x4.w, y3, y[ii]))));
+            *reinterpret_cast<const float4*>(LX + (32 + r) * LSTRIDE + 32 + m);
+        const float e0 = (m + 0 <= r) ? x4.x : 0.f, e1 = (m + 1 <= r) ? x4.y : 0.f,
+                    e2 = (m + 2 <= r) ? x4.z : 0.f, e3 = (m + 3 <= r) ? x4.w : 0.f;
+        y[ii] = fmaf(e0, y0, fmaf(e1, y1, fmaf(e2, y2, fmaf(e3, y3, y[ii]))));
       }
     }
 #pragma unroll
     for (int ii = 0; ii < 8; ++ii) LX[(32 + i0 + ii) * LSTRIDE + j] = -y[ii];
   }
   wg_sync(bar_id);
+  if (stamps && wtid == 0) stamps[4] = clock64();
 }
 
 }  // namespace tc

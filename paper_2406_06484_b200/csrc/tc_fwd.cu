@@ -97,6 +97,21 @@ __device__ void dbg_tmem(float* dst, uint32_t tm, uint32_t col, int ncols, int M
 #define DBG(stmt) do { } while (0)
 #endif
 
+#ifdef DN_TIMING
+// Test-only phase timestamps of CTA 0 (tests/test_tc_timing.py, -DDN_TIMING).
+__device__ long long* dn_tim = nullptr;
+#define TSTAMP(slot)                                                       \
+  do {                                                                     \
+    if (dn_tim != nullptr && blockIdx.x == 0 && w == 0)                    \
+      dn_tim[(size_t)c * 32 + (slot)] = clock64();                         \
+  } while (0)
+#define TSTAMP_PTR(slot) \
+  ((dn_tim != nullptr && blockIdx.x == 0) ? dn_tim + (size_t)c * 32 + (slot) : nullptr)
+#else
+#define TSTAMP(slot) do { } while (0)
+#define TSTAMP_PTR(slot) nullptr
+#endif
+
 __global__ void __launch_bounds__(NT, 1)
     tc_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                   const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mO,
@@ -158,14 +173,19 @@ __global__ void __launch_bounds__(NT, 1)
       tma_load_4d(sV, &mV, 0, 0, 0, unit, &bar_tma[0]);
     }
     uint32_t ph_p = 0;
+    // beta is prefetched into a register one chunk ahead (global latency)
+    float bnext = (w < C && w < L) ? __bfloat162float(beta[w]) : 0.f;
 #pragma unroll 1
     for (int c = 0; c < NC; ++c) {
       const int b = c & 1, t0 = c * C;
       float* vb = vec(b);  // beta, s, r of this chunk
-      // beta of the chunk (prefetch into a register before waiting)
-      const float bval = (w < C && t0 + w < L) ? __bfloat162float(beta[t0 + w]) : 0.f;
+      const float bval = bnext;
+      bnext = (w < C && t0 + C + w < L) ? __bfloat162float(beta[t0 + C + w]) : 0.f;
+      TSTAMP(0);
       mbar_wait(&bar_tma[b], (c >> 1) & 1);
+      TSTAMP(1);
       if (c >= 2) mbar_wait(&bar_empty[b], ((c >> 1) - 1) & 1);  // chain c-2 released b
+      TSTAMP(2);
       if (w == 0) {
         fence_after_sync();
         const uint32_t id = idesc_bf16(64, 64, false, false);
@@ -194,10 +214,12 @@ __global__ void __launch_bounds__(NT, 1)
         vb[(w < 64 ? 2 : 1) * C + row] = inv;
         if (w < C) vb[w] = bval;
       }
+      TSTAMP(3);
       mbar_wait(&bar_p, ph_p);
       ph_p ^= 1;
       fence_after_sync();
       wg_sync(BAR_P);  // beta, s, r visible
+      TSTAMP(4);
       {
         // one TMEM load: lanes < 16 hold G_qk rows, lanes >= 16 hold G_kk rows
         float f[64];
@@ -214,13 +236,20 @@ __global__ void __launch_bounds__(NT, 1)
         } else {  // L = beta_i s_i s_j (k_i . k_j), j < i
           const float bi = vb[i] * vb[C + i];
 #pragma unroll
-          for (int j = 0; j < 64; j += 4) {
-            float4 v;
-            v.x = (j + 0 < i) ? bi * vb[C + j + 0] * f[j + 0] : 0.f;
-            v.y = (j + 1 < i) ? bi * vb[C + j + 1] * f[j + 1] : 0.f;
-            v.z = (j + 2 < i) ? bi * vb[C + j + 2] * f[j + 2] : 0.f;
-            v.w = (j + 3 < i) ? bi * vb[C + j + 3] * f[j + 3] : 0.f;
-            *reinterpret_cast<float4*>(LX + i * LS + j) = v;
+          for (int h = 0; h < 64; h += 32) {
+            float4 s4[8];  // all loads first: no smem aliasing stalls
+#pragma unroll
+            for (int q = 0; q < 8; ++q) s4[q] = *reinterpret_cast<const float4*>(vb + C + h + 4 * q);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const int j = h + 4 * q;
+              float4 v;
+              v.x = (j + 0 < i) ? bi * s4[q].x * f[j + 0] : 0.f;
+              v.y = (j + 1 < i) ? bi * s4[q].y * f[j + 1] : 0.f;
+              v.z = (j + 2 < i) ? bi * s4[q].z * f[j + 2] : 0.f;
+              v.w = (j + 3 < i) ? bi * s4[q].w * f[j + 3] : 0.f;
+              *reinterpret_cast<float4*>(LX + i * LS + j) = v;
+            }
           }
         }
       }
@@ -228,19 +257,31 @@ __global__ void __launch_bounds__(NT, 1)
       DBG(dbg_smem(dn_dbg + D_L, LX, C, C, LS, w); dbg_tmem(dn_dbg + D_GQK, tm, TM_G, C, 64, w);
           dbg_smem(dn_dbg + D_S, vb + C, 1, C, C, w); dbg_smem(dn_dbg + D_R, vb + 2 * C, 1, C, C, w);
           dbg_smem(dn_dbg + D_B, vb, 1, C, C, w));
-      ut_inverse_inplace<LS>(LX, w, BAR_P);
+      TSTAMP(5);
+      ut_inverse_inplace<LS>(LX, w, BAR_P, TSTAMP_PTR(10));
+      TSTAMP(6);
       DBG(dbg_smem(dn_dbg + D_X, LX, C, C, LS, w));
       {
         // T'[i][j] = X[i][j] beta_j s_j, T''[i][j] = X[i][j] beta_j  (j <= i)
         const int i = w >> 1, j0 = (w & 1) * 32;
+        float4 x4[8], b4[8], s4[8];  // all loads first
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          x4[q] = *reinterpret_cast<const float4*>(LX + i * LS + j0 + 4 * q);
+          b4[q] = *reinterpret_cast<const float4*>(vb + j0 + 4 * q);
+          s4[q] = *reinterpret_cast<const float4*>(vb + C + j0 + 4 * q);
+        }
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           float x[8], y[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            const int j = j0 + g * 8 + e;
-            y[e] = (j <= i) ? LX[i * LS + j] * vb[j] : 0.f;
-            x[e] = y[e] * vb[C + j];
+            const int j = j0 + g * 8 + e, q = 2 * g + e / 4, r = e % 4;
+            const float xv = r == 0 ? x4[q].x : r == 1 ? x4[q].y : r == 2 ? x4[q].z : x4[q].w;
+            const float bv = r == 0 ? b4[q].x : r == 1 ? b4[q].y : r == 2 ? b4[q].z : b4[q].w;
+            const float sv = r == 0 ? s4[q].x : r == 1 ? s4[q].y : r == 2 ? s4[q].z : s4[q].w;
+            y[e] = (j <= i) ? xv * bv : 0.f;
+            x[e] = y[e] * sv;
           }
           il_store8(sT, C, i, j0 + g * 8, x);
           il_store8(sTu, C, i, j0 + g * 8, y);
@@ -261,9 +302,11 @@ __global__ void __launch_bounds__(NT, 1)
         }
         mma_commit(&bar_p);
       }
+      TSTAMP(7);
       mbar_wait(&bar_p, ph_p);
       ph_p ^= 1;
       fence_after_sync();
+      TSTAMP(8);
       if (w == 0 && c + 1 < NC) {  // V is free again: prefetch the next chunk's V
         const int nb = (c + 1) & 1;
         mbar_expect_tx(&bar_tma[nb], TILE);
@@ -280,6 +323,7 @@ __global__ void __launch_bounds__(NT, 1)
       fence_before_sync();
       wg_sync(BAR_P);
       if (w == 0) mbar_arrive(&bar_full[b]);
+      TSTAMP(9);
     }
   } else {
     // =====================================================================
@@ -314,7 +358,9 @@ __global__ void __launch_bounds__(NT, 1)
     for (int c = 0; c < NC; ++c) {
       const int b = c & 1, t0 = c * C;
       const float* vb = vec(b);
+      TSTAMP(16);
       mbar_wait(&bar_full[b], (c >> 1) & 1);
+      TSTAMP(17);
       // r of this lane's output row, read before buffer b is released
       const float ri = vb[2 * C + wwarp * 16 + (lane & 15)];
       if (w == 0) {
@@ -336,10 +382,12 @@ __global__ void __launch_bounds__(NT, 1)
         }
         bulk_wait_read0();  // previous O store done reading sO (= sZ)
       }
+      TSTAMP(22);
       mbar_wait(&bar_s, ph_s);
       ph_s ^= 1;
       fence_after_sync();
       wg_sync(BAR_S);
+      TSTAMP(18);
       DBG(dbg_tmem(dn_dbg + D_UP, tm, tm_u(b), C, 128, w));
       {  // Z^T[dv][t] = U'^T[dv][t] * s_t -> bf16 IL tile (row dv)
         float f[64];
@@ -366,9 +414,11 @@ __global__ void __launch_bounds__(NT, 1)
           mma_bf16(tm + TM_O, desc_k(aa, C, k0), desc_k(aZ, DV, k0), ido, 1);
         mma_commit(&bar_s);
       }
+      TSTAMP(19);
       mbar_wait(&bar_s, ph_s);
       ph_s ^= 1;
       fence_after_sync();
+      TSTAMP(20);
       if (w == 0) {
         mbar_arrive(&bar_empty[b]);  // Q/K/A/W[b] and U[b] are free for chunk c+2
         if (c + 2 < NC) {
@@ -410,6 +460,7 @@ __global__ void __launch_bounds__(NT, 1)
         tma_store_4d(&mO, sO, 0, t0, 0, unit);
         bulk_commit();
       }
+      TSTAMP(21);
     }
     // final state hT [dk][dv] (fp32), lane dv = w
     if (a.hT) {
@@ -496,5 +547,11 @@ extern "C" int dn_debug_set(float* buf, int chunk) {
   if (cudaMemcpyToSymbol(dn::dn_dbg, &buf, sizeof(buf)) != cudaSuccess) return 1;
   if (cudaMemcpyToSymbol(dn::dn_dbg_chunk, &chunk, sizeof(int)) != cudaSuccess) return 1;
   return 0;
+}
+#endif
+
+#ifdef DN_TIMING
+extern "C" int dn_timing_set(long long* buf) {
+  return cudaMemcpyToSymbol(dn::dn_tim, &buf, sizeof(buf)) != cudaSuccess;
 }
 #endif

@@ -390,3 +390,20 @@ __device__ __forceinline__ void ut_inverse_inplace(float* LX, int wtid, int bar_
 
 }  // namespace tc
 }  // namespace dn
+
+namespace dn {
+namespace tc {
+
+// D[tmem] (+)= A[tmem] * B[smem]: A (bf16, K-major) read from TMEM -- lane =
+// row m, each 32-bit column holds two consecutive k; a K=16 step spans 8
+// columns.  Pinned by tests/test_tc_probe.py::test_mma_a_from_tmem.
+__device__ __forceinline__ void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+}  // namespace tc
+}  // namespace dn

@@ -84,3 +84,112 @@ extern "C" int probe_mma(const void* A, const void* B, const float* Dinit, float
   cudaError_t e = cudaDeviceSynchronize();
   return (int)e;
 }
+
+
+// A (M=128 x K, bf16) staged in TMEM columns [256, 256 + K/2): lane m holds
+// row m, column 256 + k/2 holds (A[m][k], A[m][k+1]) packed (low = even k).
+__global__ void probe_ts_kernel(const __nv_bfloat16* A, const __nv_bfloat16* B, float* D, int N,
+                                int K, int b_mn) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  uint8_t* sB = smem;
+  const int tid = threadIdx.x, warp = tid / 32;
+  for (int e = tid; e < N * K; e += blockDim.x) {
+    int n = e / K, k = e % K;
+    uint32_t off = b_mn ? il_off(k, n, K) : il_off(n, k, N);
+    *reinterpret_cast<__nv_bfloat16*>(sB + off) = B[e];
+  }
+  fence_proxy_async();
+  if (warp == 0) tmem_alloc<512>(&tslot);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    mbar_fence_init();
+  }
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tm = tslot;
+  for (int c0 = 0; c0 < K / 2; c0 += 16) {
+    uint32_t r[16];
+    for (int j = 0; j < 16; ++j) {
+      __nv_bfloat162 h;
+      h.x = A[tid * K + 2 * (c0 + j)];
+      h.y = A[tid * K + 2 * (c0 + j) + 1];
+      r[j] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    tmem_st16(taddr(tm, warp * 32, 256 + c0), r);
+  }
+  tmem_st_wait();
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  if (tid == 0) {
+    const uint32_t id = idesc_bf16(128, N, false, b_mn);
+    const uint32_t b0 = smem_u32(sB);
+    for (int k0 = 0; k0 < K; k0 += 16) {
+      uint64_t bd = b_mn ? desc_mn(b0, K, k0) : desc_k(b0, N, k0);
+      mma_bf16_ts(tm, tm + 256 + k0 / 2, bd, id, k0 > 0 ? 1u : 0u);
+    }
+    mma_commit(&bar);
+  }
+  mbar_wait(&bar, 0);
+  fence_after_sync();
+  for (int c0 = 0; c0 < N; c0 += 16) {
+    uint32_t r[16];
+    tmem_ld16(taddr(tm, warp * 32, c0), r);
+    tmem_ld_wait();
+    for (int j = 0; j < 16; ++j) D[tid * N + c0 + j] = __uint_as_float(r[j]);
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tm);
+}
+
+extern "C" int probe_mma_ts(const void* A, const void* B, float* D, int N, int K, int b_mn) {
+  size_t smem = (size_t)N * K * 2;
+  cudaFuncSetAttribute(probe_ts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  probe_ts_kernel<<<1, 128, smem>>>((const __nv_bfloat16*)A, (const __nv_bfloat16*)B, D, N, K,
+                                    b_mn);
+  return (int)cudaDeviceSynchronize();
+}
+
+
+// TMEM -> register read throughput: each warp of the CTA repeatedly loads
+// `ncols` 32-bit columns of its 32-lane quadrant (32x32b.x16 shape).
+__global__ void tmem_bw_kernel(long long* out, int iters, int ncols) {
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x / 32;
+  if (warp == 0) tmem_alloc<512>(&tslot);
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tm = tslot;
+  uint32_t acc = 0;
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    for (int c0 = 0; c0 < ncols; c0 += 16) {
+      uint32_t r[16];
+      tmem_ld16(taddr(tm, (warp & 3) * 32, c0), r);
+      tmem_ld_wait();
+      acc += r[0] ^ r[7] ^ r[15];
+    }
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  if (threadIdx.x == 0) { out[0] = t1 - t0; out[1] = acc; }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tm);
+}
+
+extern "C" long long probe_tmem_bw(int nthreads, int iters, int ncols) {
+  long long* d;
+  long long h[2];
+  cudaMalloc(&d, 16);
+  tmem_bw_kernel<<<1, nthreads>>>(d, iters, ncols);
+  cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return h[0];
+}

@@ -23,6 +23,10 @@ def probe():
     L = ctypes.CDLL(lib)
     L.probe_mma.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int] * 7
     L.probe_mma.restype = ctypes.c_int
+    L.probe_mma_ts.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int] * 3
+    L.probe_mma_ts.restype = ctypes.c_int
+    L.probe_tmem_bw.argtypes = [ctypes.c_int] * 3
+    L.probe_tmem_bw.restype = ctypes.c_longlong
     return L
 
 
@@ -78,3 +82,29 @@ def test_mma_m64_lane_offset_16(probe, N, init):
                          D.data_ptr(), M, N, K, 0, 1, 0, 16)
     assert rc == 0
     assert (D.cpu() - ref).abs().max().item() <= 1e-3 * ref.abs().max().item()
+
+
+@pytest.mark.parametrize("N,K", [(64, 64), (128, 64), (64, 128), (128, 128)])
+@pytest.mark.parametrize("b_mn", [0, 1])
+def test_mma_a_from_tmem(probe, N, K, b_mn):
+    """tcgen05.mma with the A operand in TMEM (M=128, bf16 pairs per column)."""
+    g = torch.Generator().manual_seed(N * 3 + K + b_mn)
+    A = torch.randn(128, K, generator=g).bfloat16()
+    B = torch.randn(N, K, generator=g).bfloat16()
+    ref = A.float() @ B.float().T
+    Ad, Bd = A.cuda(), B.cuda()
+    D = torch.zeros(128, N, device="cuda")
+    assert probe.probe_mma_ts(Ad.data_ptr(), Bd.data_ptr(), D.data_ptr(), N, K, b_mn) == 0
+    assert (D.cpu() - ref).abs().max().item() <= 1e-3 * ref.abs().max().item()
+
+
+def test_tmem_read_throughput(probe):
+    """Measure TMEM -> register bandwidth (bytes per SM cycle); informational."""
+    res = {}
+    for nt in (128, 256, 512):
+        iters, ncols = 200, 128
+        cyc = probe.probe_tmem_bw(nt, iters, ncols)
+        byts = nt * iters * ncols * 4
+        res[nt] = byts / cyc
+    print("\nTMEM read bytes/cycle by thread count:", {k: round(v, 1) for k, v in res.items()})
+    assert all(v > 0 for v in res.values())

@@ -91,6 +91,21 @@ __device__ __forceinline__ void ld16f(uint32_t tm, int wwarp, uint32_t col, floa
   for (int j = 0; j < 16; ++j) f[j] = __uint_as_float(r[j]);
 }
 
+#ifdef DN_TIMING
+// Test-only phase timestamps of CTA 0 (tests/test_tc_timing.py, -DDN_TIMING).
+__device__ long long* dn_tim_bwd = nullptr;
+#define BSTAMP(slot)                                                        \
+  do {                                                                      \
+    if (dn_tim_bwd != nullptr && blockIdx.x == 0 && (tid & 127) == 0)       \
+      dn_tim_bwd[(size_t)it * 32 + (slot)] = clock64();                     \
+  } while (0)
+#define BSTAMP_PTR(slot) \
+  ((dn_tim_bwd != nullptr && blockIdx.x == 0) ? dn_tim_bwd + (size_t)it * 32 + (slot) : nullptr)
+#else
+#define BSTAMP(slot) do { } while (0)
+#define BSTAMP_PTR(slot) nullptr
+#endif
+
 __global__ void __launch_bounds__(NT, 1)
     tc_bwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                   const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mDO,
@@ -187,6 +202,7 @@ __global__ void __launch_bounds__(NT, 1)
     const uint32_t aK = smem_u32(sK), aW = smem_u32(sW);
 
     // ================= P1: dH image, loads, row norms, in-place normalisation
+    if (tid == 0) BSTAMP(0);
     if (tid == 0) bulk_wait_read0();  // previous dk store done reading the LX region
     if (tid < C) sb[tid] = (t0 + tid < L) ? __bfloat162float(beta[t0 + tid]) : 0.f;
     if (wg == 1) {  // dH^T (dl/dH_{c+1}) -> bf16 image
@@ -199,6 +215,7 @@ __global__ void __launch_bounds__(NT, 1)
       }
     }
     mbar_wait(&bar_tma, ph);
+    if (tid == 0) BSTAMP(1);
     if (wg == 0) {  // w < 64: q row w; w >= 64: k row w-64
       const int row = w & 63;
       const uint8_t* tile = w < 64 ? sQ : sK;
@@ -233,6 +250,7 @@ __global__ void __launch_bounds__(NT, 1)
     fence_proxy_async();
     cta_sync();
 
+    if (tid == 0) BSTAMP(2);
     // ================= M1: Gram | K H, dH^T K^T
     if (tid == 0) {
       const uint32_t idg = idesc_bf16(64, 64, false, false);
@@ -255,6 +273,7 @@ __global__ void __launch_bounds__(NT, 1)
     // ================= P2: A = tril(Q K^T) -> bf16; L = beta_i (k_i . k_j), j < i
     mbar_wait(&mb[MB_G], ph);
     fence_after_sync();
+    if (tid == 0) BSTAMP(3);
     {
       float f[32];
       ld32(tm, wwarp, TM_G + 32 * wg, f);  // lanes<16: G_qk row, lanes>=16: G_kk row
@@ -287,6 +306,7 @@ __global__ void __launch_bounds__(NT, 1)
     fence_proxy_async();
     cta_sync();
 
+    if (tid == 0) BSTAMP(4);
     // ================= M2: dU'^T += dO^T A
     if (tid == 0) {
       const uint32_t ida = idesc_bf16(128, 64, true, true);
@@ -298,7 +318,8 @@ __global__ void __launch_bounds__(NT, 1)
 
     // ================= P3: wg0 substitution + X, T | wg1 R and dU' conversions
     if (wg == 0) {
-      ut_inverse_inplace<LS>(LX, w, BAR_P);
+      ut_inverse_inplace<LS>(LX, w, BAR_P, BSTAMP_PTR(24));
+      BSTAMP(16);
       const int i = w >> 1, j0 = (w & 1) * 32;
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
@@ -315,6 +336,7 @@ __global__ void __launch_bounds__(NT, 1)
     } else {
       mbar_wait(&mb[MB_R], ph);
       fence_after_sync();
+      BSTAMP(20);
 #pragma unroll 1
       for (int half = 0; half < 2; ++half) {  // R = V - K H (rows r64, lanes < 16)
         float f[64];
@@ -330,8 +352,10 @@ __global__ void __launch_bounds__(NT, 1)
           }
         }
       }
+      BSTAMP(21);
       mbar_wait(&mb[MB_DU], ph);
       fence_after_sync();
+      BSTAMP(22);
       {  // dU'^T (lane d_v = w) -> bf16
         float f[64];
         ld64(tm, wwarp, TM_DU, f);
@@ -342,6 +366,7 @@ __global__ void __launch_bounds__(NT, 1)
     fence_proxy_async();
     cta_sync();
 
+    if (tid == 0) BSTAMP(5);
     // ================= M3: W, U | P = X^T dU', dX' = dU' R^T
     if (tid == 0) {
       const uint32_t idw = idesc_bf16(128, 64, true, false);
@@ -365,6 +390,7 @@ __global__ void __launch_bounds__(NT, 1)
     // ================= P4: W^T -> bf16 (row dk, columns split)
     mbar_wait(&mb[MB_W], ph);
     fence_after_sync();
+    if (tid == 0) BSTAMP(6);
     {
       float f[32];
       ld32(tm, wwarp, TM_W + 32 * wg, f);
@@ -374,6 +400,7 @@ __global__ void __launch_bounds__(NT, 1)
     fence_proxy_async();
     cta_sync();
 
+    if (tid == 0) BSTAMP(7);
     // ================= M4: dH += Q^T dO - W^T dU' ; U' = U - W H
     if (tid == 0) {
       const uint32_t id1 = idesc_bf16(128, 128, true, true);
@@ -394,6 +421,7 @@ __global__ void __launch_bounds__(NT, 1)
     mbar_wait(&mb[MB_U], ph);
     mbar_wait(&mb[MB_P], ph);
     fence_after_sync();
+    if (tid == 0) BSTAMP(8);
     {
       float f[32];
       ld32(tm, wwarp, TM_U + 32 * wg, f);
@@ -441,6 +469,7 @@ __global__ void __launch_bounds__(NT, 1)
     }
     fence_proxy_async();
     cta_sync();
+    if (tid == 0) BSTAMP(9);
     if (tid == 0) {
       tma_store_4d(&mDV, sDV, 0, t0, 0, unit);
       bulk_commit();
@@ -468,6 +497,7 @@ __global__ void __launch_bounds__(NT, 1)
     // ================= P6: dA -> bf16 (masked) | Y -> bf16
     mbar_wait(&mb[MB_A], ph);
     fence_after_sync();
+    if (tid == 0) BSTAMP(10);
     {
       float f[32];
       ld32(tm, wwarp, TM_DA + 32 * wg, f);  // lanes<16: dA row, lanes>=16: Y row
@@ -485,6 +515,7 @@ __global__ void __launch_bounds__(NT, 1)
     fence_proxy_async();
     cta_sync();
 
+    if (tid == 0) BSTAMP(11);
     // ================= M6: dQ += dA K ; dK += dA^T Q ; G = -Y X^T
     if (tid == 0) {
       const uint32_t id_q = idesc_bf16(64, 128, false, true);
@@ -502,6 +533,7 @@ __global__ void __launch_bounds__(NT, 1)
     // ================= P7: wg0 dq epilogue | wg1 G, dbeta, Mg
     mbar_wait(&mb[MB_Q], ph);
     fence_after_sync();
+    if (tid == 0) BSTAMP(12);
     if (wg == 0) {
       // lanes >= 16: dq_hat row r64 (TM_DQ) -> L2 adjoint -> dq staging
       float dot = 0.f;
@@ -581,6 +613,7 @@ __global__ void __launch_bounds__(NT, 1)
     fence_proxy_async();
     cta_sync();
 
+    if (tid == 0) BSTAMP(13);
     // ================= M7: dK += Mg K ; prefetch chunk c-1
     if (tid == 0) {
       tma_store_4d(&mDQ, sDQo, 0, t0, 0, unit);
@@ -599,6 +632,7 @@ __global__ void __launch_bounds__(NT, 1)
     // ================= P8: dK epilogue (columns split; row dot combined)
     mbar_wait(&mb[MB_K], ph);
     fence_after_sync();
+    if (tid == 0) BSTAMP(14);
     {
       float f[64];
       ld64(tm, wwarp, TM_DK + 64 * wg, f);  // lanes<16: dk_hat row r64
@@ -635,6 +669,7 @@ __global__ void __launch_bounds__(NT, 1)
       tma_store_4d(&mDK, sDKo, 0, t0, 0, unit);
       bulk_commit();
     }
+    if (tid == 0) BSTAMP(15);
   }
 
   // dh0 = dH (orientation [dk][dv]; lane dv = w, columns split)
@@ -685,3 +720,9 @@ int tc_bwd(const Args& a0, cudaStream_t s) {
 }
 
 }  // namespace dn
+
+#ifdef DN_TIMING
+extern "C" int dn_timing_set_bwd(long long* buf) {
+  return cudaMemcpyToSymbol(dn::dn_tim_bwd, &buf, sizeof(buf)) != cudaSuccess;
+}
+#endif

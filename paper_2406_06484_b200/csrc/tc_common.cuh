@@ -276,19 +276,28 @@ __device__ __forceinline__ void ut_inverse_inplace(float* LX, int wtid, int bar_
   const int lane = wtid & 31, wwarp = wtid >> 5;
   {  // level 1: block q = wwarp, column j = lane (< 16)
     const int o = 16 * wwarp, j = lane & 15;
+    // All loads first (branch-free, so they can all be in flight), then the
+    // dependent chain; x_i = [i == j] - [i > j] * sum_m L_im x_m.
+    float4 l4[16][4];
+#pragma unroll
+    for (int i = 1; i < 16; ++i)
+#pragma unroll
+      for (int m = 0; m < i; m += 4)
+        l4[i][m / 4] = *reinterpret_cast<const float4*>(LX + (o + i) * LSTRIDE + o + m);
     float x[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll
       for (int m = 0; m < i; m += 4) {
-        const float4 l4 = *reinterpret_cast<const float4*>(LX + (o + i) * LSTRIDE + o + m);
-        a0 = fmaf(l4.x, x[m], a0);
-        if (m + 1 < i) a1 = fmaf(l4.y, x[m + 1], a1);
-        if (m + 2 < i) a2 = fmaf(l4.z, x[m + 2], a2);
-        if (m + 3 < i) a3 = fmaf(l4.w, x[m + 3], a3);
+        const float4 l = l4[i][m / 4];
+        a0 = fmaf(l.x, x[m], a0);
+        if (m + 1 < i) a1 = fmaf(l.y, x[m + 1], a1);
+        if (m + 2 < i) a2 = fmaf(l.z, x[m + 2], a2);
+        if (m + 3 < i) a3 = fmaf(l.w, x[m + 3], a3);
       }
-      x[i] = (i == j) ? 1.f : ((i < j) ? 0.f : -((a0 + a1) + (a2 + a3)));
+      const float eq = (i == j) ? 1.f : 0.f, gt = (i > j) ? 1.f : 0.f;
+      x[i] = fmaf(-gt, (a0 + a1) + (a2 + a3), eq);
     }
     __syncwarp();
     if (lane < 16) {
@@ -346,10 +355,10 @@ __device__ __forceinline__ void ut_inverse_inplace(float* LX, int wtid, int bar_
     for (int m = 0; m < 32; m += 4) {
       // X11 is lower triangular; its upper-right 16x16 block holds level-2
       // scratch, so entries above the diagonal are masked to zero.
-      const float x0 = (m + 0 >= j) ? LX[(m + 0) * LSTRIDE + j] : 0.f,
-                  x1 = (m + 1 >= j) ? LX[(m + 1) * LSTRIDE + j] : 0.f,
-                  x2 = (m + 2 >= j) ? LX[(m + 2) * LSTRIDE + j] : 0.f,
-                  x3 = (m + 3 >= j) ? LX[(m + 3) * LSTRIDE + j] : 0.f;
+      const float x0 = LX[(m + 0) * LSTRIDE + j] * ((m + 0 >= j) ? 1.f : 0.f),
+                  x1 = LX[(m + 1) * LSTRIDE + j] * ((m + 1 >= j) ? 1.f : 0.f),
+                  x2 = LX[(m + 2) * LSTRIDE + j] * ((m + 2 >= j) ? 1.f : 0.f),
+                  x3 = LX[(m + 3) * LSTRIDE + j] * ((m + 3 >= j) ? 1.f : 0.f);
 #pragma unroll
       for (int ii = 0; ii < 8; ++ii) {
         const float4 l4 = *reinterpret_cast<const float4*>(LX + (32 + i0 + ii) * LSTRIDE + m);

@@ -20,11 +20,13 @@
 // Algebra of the folded normalisation: DESIGN.md §4.1.
 //
 // Warp specialisation: warpgroup P (warps 0-3) runs the
-// state-independent "prep" of chunk t+1 (Gram, substitution, W, U) while
-// warpgroup S (warps 4-7) runs the state chain and output of chunk t.
+// state-independent "prep" of chunk t+1 (norms, A, L, substitution, T, W)
+// while warpgroup S (warps 4-7) runs the conversions of the state chain and
+// the output epilogue of chunk t.  Warp 8 issues the prep MMAs and the V
+// loads; warp 9 issues the chain MMAs, the state save, the O store and the
+// next Q/K loads, so no compute warp ever stalls on an MMA issue queue.
 // Q/K/A/W tiles and the U accumulator are double-buffered by chunk parity;
-// mbarriers full[b] (P -> S) and empty[b] (S -> P) hand the buffers over, and
-// the next chunk's TMA loads are issued as soon as a buffer frees.
+// mbarriers hand every buffer over (full/empty, *_done/*_free/*_ready).
 #include <cudaTypedefs.h>
 #include <stdio.h>
 
@@ -36,7 +38,7 @@ namespace {
 
 using namespace tc;
 
-constexpr int C = 64, DK = 128, DV = 128, NT = 256;
+constexpr int C = 64, DK = 128, DV = 128, NT = 320;  // 2 warpgroups + 2 MMA warps
 constexpr int LS = 68;  // row stride (floats) of the fp32 substitution buffer
 
 // dynamic shared memory map (bytes)
@@ -117,12 +119,14 @@ __global__ void __launch_bounds__(NT, 1)
                   const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mO,
                   Args a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bar_tma[2], bar_full[2], bar_empty[2], bar_p, bar_s;
+  // mbarriers (DESIGN.md §4.1 "fwd pipeline")
+  __shared__ uint64_t bar_tma[2], bar_full[2], bar_empty[2];
+  __shared__ uint64_t g_done, g_free, t_ready, wu_done, w_free;        // prep side
+  __shared__ uint64_t up_done, z_free, z_ready, ho_done, h_ready, st_free;  // state side
   __shared__ uint32_t tslot;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int wg = tid >> 7;            // 0: prep warpgroup, 1: state/output warpgroup
-  const int w = tid & 127;            // thread index inside the warpgroup
+  const int w = tid & 127;            // thread index inside a compute warpgroup
   const int wwarp = w >> 5;           // warp inside the warpgroup (TMEM lane quadrant)
   const int unit = blockIdx.x;
   const int L = a.L, NC = a.NC;
@@ -135,8 +139,17 @@ __global__ void __launch_bounds__(NT, 1)
       mbar_init(&bar_full[b], 1);
       mbar_init(&bar_empty[b], 1);
     }
-    mbar_init(&bar_p, 1);
-    mbar_init(&bar_s, 1);
+    mbar_init(&g_done, 1);
+    mbar_init(&g_free, 1);
+    mbar_init(&t_ready, 1);
+    mbar_init(&wu_done, 1);
+    mbar_init(&w_free, 1);
+    mbar_init(&up_done, 1);
+    mbar_init(&z_free, 1);
+    mbar_init(&z_ready, 1);
+    mbar_init(&ho_done, 1);
+    mbar_init(&h_ready, 1);
+    mbar_init(&st_free, 1);
     mbar_fence_init();
     prefetch_tmap(&mQ);
     prefetch_tmap(&mK);
@@ -158,21 +171,11 @@ __global__ void __launch_bounds__(NT, 1)
   uint8_t* sO = sZ;
   float* LX = reinterpret_cast<float*>(smem + OFF_L);
 
-  if (wg == 0) {
+  if (warp < 4) {
     // =====================================================================
-    // Warpgroup P: prep of chunk c (state independent)
+    // Warpgroup P (warps 0-3): prep of chunk c (state independent)
     // =====================================================================
     const __nv_bfloat16* beta = (const __nv_bfloat16*)a.beta + (size_t)unit * L;
-    if (w == 0) {  // chunks 0 and 1: both buffers start free
-      for (int c = 0; c < 2 && c < NC; ++c) {
-        mbar_expect_tx(&bar_tma[c], 2 * TILE);
-        tma_load_4d(sQ(c), &mQ, 0, c * C, 0, unit, &bar_tma[c]);
-        tma_load_4d(sK(c), &mK, 0, c * C, 0, unit, &bar_tma[c]);
-      }
-      mbar_expect_tx(&bar_tma[0], TILE);
-      tma_load_4d(sV, &mV, 0, 0, 0, unit, &bar_tma[0]);
-    }
-    uint32_t ph_p = 0;
     // beta is prefetched into a register one chunk ahead (global latency)
     float bnext = (w < C && w < L) ? __bfloat162float(beta[w]) : 0.f;
 #pragma unroll 1
@@ -183,43 +186,31 @@ __global__ void __launch_bounds__(NT, 1)
       bnext = (w < C && t0 + C + w < L) ? __bfloat162float(beta[t0 + C + w]) : 0.f;
       TSTAMP(0);
       mbar_wait(&bar_tma[b], (c >> 1) & 1);
-      TSTAMP(1);
       if (c >= 2) mbar_wait(&bar_empty[b], ((c >> 1) - 1) & 1);  // chain c-2 released b
-      TSTAMP(2);
-      if (w == 0) {
-        fence_after_sync();
-        const uint32_t id = idesc_bf16(64, 64, false, false);
-        const uint32_t aq = smem_u32(sQ(b)), ak = smem_u32(sK(b));
-#pragma unroll
-        for (int k0 = 0; k0 < DK; k0 += 16) {
-          mma_bf16(tm + TM_G, desc_k(aq, C, k0), desc_k(ak, C, k0), id, k0 > 0);
-          mma_bf16(tm + TM_G + LO16, desc_k(ak, C, k0), desc_k(ak, C, k0), id, k0 > 0);
-        }
-        mma_commit(&bar_p);
-      }
+      TSTAMP(1);
       {
         // w < 64: r = 1/||q_w||; w >= 64: s = 1/||k_{w-64}||   (fp32 from bf16)
         const int row = w & 63;
         const uint8_t* tile = w < 64 ? sQ(b) : sK(b);
-        float acc = 0.f;
+        float x[DK];
 #pragma unroll
-        for (int g = 0; g < DK / 8; ++g) {
-          float x[8];
-          il_load8(tile, C, row, g * 8, x);
+        for (int g = 0; g < DK / 8; ++g) il_load8(tile, C, row, g * 8, x + 8 * g);
+        float acc0 = 0.f, acc1 = 0.f;
 #pragma unroll
-          for (int e = 0; e < 8; ++e) acc = fmaf(x[e], x[e], acc);
+        for (int e = 0; e < DK; e += 2) {
+          acc0 = fmaf(x[e], x[e], acc0);
+          acc1 = fmaf(x[e + 1], x[e + 1], acc1);
         }
-        float inv = l2 ? 1.f / fmaxf(sqrtf(acc), a.eps) : 1.f;
+        float inv = l2 ? 1.f / fmaxf(sqrtf(acc0 + acc1), a.eps) : 1.f;
         if (t0 + row >= L) inv = 0.f;  // padded token: exact zero contribution
         vb[(w < 64 ? 2 : 1) * C + row] = inv;
         if (w < C) vb[w] = bval;
       }
-      TSTAMP(3);
-      mbar_wait(&bar_p, ph_p);
-      ph_p ^= 1;
-      fence_after_sync();
       wg_sync(BAR_P);  // beta, s, r visible
-      TSTAMP(4);
+      TSTAMP(2);
+      mbar_wait(&g_done, c & 1);
+      fence_after_sync();
+      TSTAMP(3);
       {
         // one TMEM load: lanes < 16 hold G_qk rows, lanes >= 16 hold G_kk rows
         float f[64];
@@ -253,13 +244,15 @@ __global__ void __launch_bounds__(NT, 1)
           }
         }
       }
+      fence_before_sync();
       wg_sync(BAR_P);
       DBG(dbg_smem(dn_dbg + D_L, LX, C, C, LS, w); dbg_tmem(dn_dbg + D_GQK, tm, TM_G, C, 64, w);
           dbg_smem(dn_dbg + D_S, vb + C, 1, C, C, w); dbg_smem(dn_dbg + D_R, vb + 2 * C, 1, C, C, w);
-          dbg_smem(dn_dbg + D_B, vb, 1, C, C, w));
-      TSTAMP(5);
+          dbg_smem(dn_dbg + D_B, vb, 1, C, C, w); fence_before_sync(); wg_sync(BAR_P));
+      if (w == 0) mbar_arrive(&g_free);  // the Gram accumulator may be overwritten
+      TSTAMP(4);
       ut_inverse_inplace<LS>(LX, w, BAR_P, TSTAMP_PTR(10));
-      TSTAMP(6);
+      TSTAMP(5);
       DBG(dbg_smem(dn_dbg + D_X, LX, C, C, LS, w));
       {
         // T'[i][j] = X[i][j] beta_j s_j, T''[i][j] = X[i][j] beta_j  (j <= i)
@@ -288,30 +281,12 @@ __global__ void __launch_bounds__(NT, 1)
         }
       }
       fence_proxy_async();
-      fence_before_sync();
       wg_sync(BAR_P);
-      if (w == 0) {  // W^T = K^T T'^T, U^T = V^T T''^T  (M=128, N=64, K=64)
-        fence_after_sync();
-        const uint32_t id = idesc_bf16(128, 64, true, false);
-        const uint32_t ak = smem_u32(sK(b)), av = smem_u32(sV), at = smem_u32(sT),
-                       atu = smem_u32(sTu);
-#pragma unroll
-        for (int k0 = 0; k0 < C; k0 += 16) {
-          mma_bf16(tm + TM_W, desc_mn(ak, C, k0), desc_k(at, C, k0), id, k0 > 0);
-          mma_bf16(tm + tm_u(b), desc_mn(av, C, k0), desc_k(atu, C, k0), id, k0 > 0);
-        }
-        mma_commit(&bar_p);
-      }
-      TSTAMP(7);
-      mbar_wait(&bar_p, ph_p);
-      ph_p ^= 1;
+      if (w == 0) mbar_arrive(&t_ready);
+      TSTAMP(6);
+      mbar_wait(&wu_done, c & 1);
       fence_after_sync();
-      TSTAMP(8);
-      if (w == 0 && c + 1 < NC) {  // V is free again: prefetch the next chunk's V
-        const int nb = (c + 1) & 1;
-        mbar_expect_tx(&bar_tma[nb], TILE);
-        tma_load_4d(sV, &mV, 0, (c + 1) * C, 0, unit, &bar_tma[nb]);
-      }
+      TSTAMP(7);
       DBG(dbg_tmem(dn_dbg + D_W, tm, TM_W, C, 128, w); dbg_tmem(dn_dbg + D_U, tm, tm_u(b), C, 128, w));
       {  // W^T (lane = dk) -> bf16 IL tile (row dk, cols = tokens)
         float f[64];
@@ -322,16 +297,16 @@ __global__ void __launch_bounds__(NT, 1)
       fence_proxy_async();
       fence_before_sync();
       wg_sync(BAR_P);
-      if (w == 0) mbar_arrive(&bar_full[b]);
-      TSTAMP(9);
+      if (w == 0) {
+        mbar_arrive(&w_free);
+        mbar_arrive(&bar_full[b]);
+      }
+      TSTAMP(8);
     }
-  } else {
+  } else if (warp < 8) {
     // =====================================================================
-    // Warpgroup S: state chain + output of chunk c
+    // Warpgroup S (warps 4-7): state chain conversions + output epilogue
     // =====================================================================
-    uint8_t* states = (a.flags & DELTANET_SAVE_STATES)
-                          ? (uint8_t*)a.states + (size_t)unit * NC * (DK * DV * 2)
-                          : nullptr;
     {  // initial state: H^T row dv = w (TMEM lane w) from h0 [dk][dv]
       const float* h0 = a.h0 ? a.h0 + (size_t)unit * DK * DV : nullptr;
 #pragma unroll 1
@@ -352,42 +327,19 @@ __global__ void __launch_bounds__(NT, 1)
     fence_proxy_async();
     fence_before_sync();
     wg_sync(BAR_S);
-    const uint32_t aH = smem_u32(sH), aZ = smem_u32(sZ);
-    uint32_t ph_s = 0;
+    if (w == 0) mbar_arrive(&h_ready);
 #pragma unroll 1
     for (int c = 0; c < NC; ++c) {
-      const int b = c & 1, t0 = c * C;
+      const int b = c & 1;
       const float* vb = vec(b);
       TSTAMP(16);
       mbar_wait(&bar_full[b], (c >> 1) & 1);
-      TSTAMP(17);
       // r of this lane's output row, read before buffer b is released
       const float ri = vb[2 * C + wwarp * 16 + (lane & 15)];
-      if (w == 0) {
-        fence_after_sync();
-        // U'^T = U^T - H^T W^T (M=128,N=64,K=128); O = Q H (M=64,N=128,K=128)
-        const uint32_t idn = idesc_bf16(128, 64, false, true, /*neg_a=*/true);
-        const uint32_t ido = idesc_bf16(64, 128, false, false);
-        const uint32_t aw = smem_u32(sW(b)), aq = smem_u32(sQ(b));
-#pragma unroll
-        for (int k0 = 0; k0 < DK; k0 += 16)
-          mma_bf16(tm + tm_u(b), desc_k(aH, DV, k0), desc_mn(aw, DK, k0), idn, 1);
-        mma_commit(&bar_s);
-#pragma unroll
-        for (int k0 = 0; k0 < DK; k0 += 16)
-          mma_bf16(tm + TM_O, desc_k(aq, C, k0), desc_k(aH, DV, k0), ido, k0 > 0);
-        if (states) {  // save H_c (bf16 smem image) for the backward
-          bulk_store(states + (size_t)c * DK * DV * 2, sH, DK * DV * 2);
-          bulk_commit();
-        }
-        bulk_wait_read0();  // previous O store done reading sO (= sZ)
-      }
-      TSTAMP(22);
-      mbar_wait(&bar_s, ph_s);
-      ph_s ^= 1;
+      mbar_wait(&up_done, c & 1);
+      mbar_wait(&z_free, c & 1);
       fence_after_sync();
-      wg_sync(BAR_S);
-      TSTAMP(18);
+      TSTAMP(17);
       DBG(dbg_tmem(dn_dbg + D_UP, tm, tm_u(b), C, 128, w));
       {  // Z^T[dv][t] = U'^T[dv][t] * s_t -> bf16 IL tile (row dv)
         float f[64];
@@ -400,35 +352,12 @@ __global__ void __launch_bounds__(NT, 1)
       fence_proxy_async();
       fence_before_sync();
       wg_sync(BAR_S);
-      if (w == 0) {
-        fence_after_sync();
-        // H^T += Z^T K (M=128,N=128,K=64); O += tril(QK^T) Z (M=64,N=128,K=64)
-        const uint32_t ido = idesc_bf16(64, 128, false, false);
-        const uint32_t idh = idesc_bf16(128, 128, false, true);
-        const uint32_t aa = smem_u32(sA(b)), ak = smem_u32(sK(b));
-#pragma unroll
-        for (int k0 = 0; k0 < C; k0 += 16)
-          mma_bf16(tm + TM_H, desc_k(aZ, DV, k0), desc_mn(ak, C, k0), idh, 1);
-#pragma unroll
-        for (int k0 = 0; k0 < C; k0 += 16)
-          mma_bf16(tm + TM_O, desc_k(aa, C, k0), desc_k(aZ, DV, k0), ido, 1);
-        mma_commit(&bar_s);
-      }
-      TSTAMP(19);
-      mbar_wait(&bar_s, ph_s);
-      ph_s ^= 1;
+      if (w == 0) mbar_arrive(&z_ready);
+      TSTAMP(18);
+      mbar_wait(&ho_done, c & 1);
+      mbar_wait(&st_free, c & 1);
       fence_after_sync();
-      TSTAMP(20);
-      if (w == 0) {
-        mbar_arrive(&bar_empty[b]);  // Q/K/A/W[b] and U[b] are free for chunk c+2
-        if (c + 2 < NC) {
-          mbar_expect_tx(&bar_tma[b], 2 * TILE);
-          tma_load_4d(sQ(b), &mQ, 0, (c + 2) * C, 0, unit, &bar_tma[b]);
-          tma_load_4d(sK(b), &mK, 0, (c + 2) * C, 0, unit, &bar_tma[b]);
-        }
-        bulk_wait_read0();  // state save done reading sH
-      }
-      wg_sync(BAR_S);
+      TSTAMP(19);
       DBG(dbg_tmem(dn_dbg + D_O, tm, TM_O, DV, 64, w); dbg_tmem(dn_dbg + D_H, tm, TM_H, DK, 128, w));
       {
         // H^T -> bf16 sH (operand of the next chunk) first: it is on the chain
@@ -456,11 +385,8 @@ __global__ void __launch_bounds__(NT, 1)
       fence_proxy_async();
       fence_before_sync();
       wg_sync(BAR_S);
-      if (w == 0 && a.o) {
-        tma_store_4d(&mO, sO, 0, t0, 0, unit);
-        bulk_commit();
-      }
-      TSTAMP(21);
+      if (w == 0) mbar_arrive(&h_ready);
+      TSTAMP(20);
     }
     // final state hT [dk][dv] (fp32), lane dv = w
     if (a.hT) {
@@ -474,7 +400,122 @@ __global__ void __launch_bounds__(NT, 1)
         for (int e = 0; e < 64; ++e) hT[(size_t)(64 * half + e) * DV + w] = f[e];
       }
     }
-    if (w == 0) bulk_wait0();
+  } else if (warp == 8) {
+    // =====================================================================
+    // Warp 8: prep MMA issue + TMA loads of V (and of Q/K for chunks 0, 1)
+    // =====================================================================
+    if (lane == 0) {
+      for (int c = 0; c < 2 && c < NC; ++c) {
+        mbar_expect_tx(&bar_tma[c], 2 * TILE);
+        tma_load_4d(sQ(c), &mQ, 0, c * C, 0, unit, &bar_tma[c]);
+        tma_load_4d(sK(c), &mK, 0, c * C, 0, unit, &bar_tma[c]);
+      }
+      mbar_expect_tx(&bar_tma[0], TILE);
+      tma_load_4d(sV, &mV, 0, 0, 0, unit, &bar_tma[0]);
+      const uint32_t idg = idesc_bf16(64, 64, false, false);
+      const uint32_t idw = idesc_bf16(128, 64, true, false);
+      const uint32_t at = smem_u32(sT), atu = smem_u32(sTu), av = smem_u32(sV);
+#pragma unroll 1
+      for (int c = 0; c < NC; ++c) {
+        const int b = c & 1;
+        const uint32_t aq = smem_u32(sQ(b)), ak = smem_u32(sK(b));
+        mbar_wait(&bar_tma[b], (c >> 1) & 1);
+        if (c >= 1) mbar_wait(&g_free, (c - 1) & 1);
+        fence_after_sync();
+#pragma unroll
+        for (int k0 = 0; k0 < DK; k0 += 16) {
+          mma_bf16(tm + TM_G, desc_k(aq, C, k0), desc_k(ak, C, k0), idg, k0 > 0);
+          mma_bf16(tm + TM_G + LO16, desc_k(ak, C, k0), desc_k(ak, C, k0), idg, k0 > 0);
+        }
+        mma_commit(&g_done);
+        mbar_wait(&t_ready, c & 1);
+        if (c >= 1) mbar_wait(&w_free, (c - 1) & 1);
+        if (c >= 2) mbar_wait(&bar_empty[b], ((c >> 1) - 1) & 1);  // U[b] consumed
+        fence_after_sync();
+#pragma unroll
+        for (int k0 = 0; k0 < C; k0 += 16) {
+          mma_bf16(tm + TM_W, desc_mn(ak, C, k0), desc_k(at, C, k0), idw, k0 > 0);
+          mma_bf16(tm + tm_u(b), desc_mn(av, C, k0), desc_k(atu, C, k0), idw, k0 > 0);
+        }
+        mma_commit(&wu_done);
+        mbar_wait(&wu_done, c & 1);
+        if (c + 1 < NC) {  // V (and T, T'') free again: prefetch the next chunk's V
+          const int nb = (c + 1) & 1;
+          mbar_expect_tx(&bar_tma[nb], TILE);
+          tma_load_4d(sV, &mV, 0, (c + 1) * C, 0, unit, &bar_tma[nb]);
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // =====================================================================
+    // Warp 9: state-chain MMA issue, state save, O store, next Q/K loads
+    // =====================================================================
+    if (lane == 0) {
+      uint8_t* states = (a.flags & DELTANET_SAVE_STATES)
+                            ? (uint8_t*)a.states + (size_t)unit * NC * (DK * DV * 2)
+                            : nullptr;
+      const uint32_t aH = smem_u32(sH), aZ = smem_u32(sZ);
+      const uint32_t idn = idesc_bf16(128, 64, false, true, /*neg_a=*/true);
+      const uint32_t ido = idesc_bf16(64, 128, false, false);
+      const uint32_t idh = idesc_bf16(128, 128, false, true);
+#pragma unroll 1
+      for (int c = 0; c < NC; ++c) {
+        const int b = c & 1;
+        const uint32_t aw = smem_u32(sW(b)), aq = smem_u32(sQ(b)), aa = smem_u32(sA(b)),
+                       ak = smem_u32(sK(b));
+        mbar_wait(&bar_full[b], (c >> 1) & 1);
+        mbar_wait(&h_ready, c & 1);  // sH = bf16 image of H_c; sO = O of chunk c-1
+        if (c >= 1 && a.o) {
+          tma_store_4d(&mO, sO, 0, (c - 1) * C, 0, unit);
+          bulk_commit();
+        }
+        if (states) {  // save H_c (bf16 smem image) for the backward
+          bulk_store(states + (size_t)c * DK * DV * 2, sH, DK * DV * 2);
+          bulk_commit();
+        }
+        fence_after_sync();
+        // U'^T = U^T - H^T W^T (M=128,N=64,K=128); O = Q H (M=64,N=128,K=128)
+#pragma unroll
+        for (int k0 = 0; k0 < DK; k0 += 16)
+          mma_bf16(tm + tm_u(b), desc_k(aH, DV, k0), desc_mn(aw, DK, k0), idn, 1);
+        mma_commit(&up_done);
+#pragma unroll
+        for (int k0 = 0; k0 < DK; k0 += 16)
+          mma_bf16(tm + TM_O, desc_k(aq, C, k0), desc_k(aH, DV, k0), ido, k0 > 0);
+        // the O store of chunk c-1 must finish reading sO (= sZ) before Z is written
+        asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(1) : "memory");
+        if (!states) bulk_wait_read0();
+        mbar_arrive(&z_free);
+        mbar_wait(&z_ready, c & 1);
+        fence_after_sync();
+        // H^T += Z^T K (M=128,N=128,K=64); O += tril(QK^T) Z (M=64,N=128,K=64)
+#pragma unroll
+        for (int k0 = 0; k0 < C; k0 += 16)
+          mma_bf16(tm + TM_H, desc_k(aZ, DV, k0), desc_mn(ak, C, k0), idh, 1);
+#pragma unroll
+        for (int k0 = 0; k0 < C; k0 += 16)
+          mma_bf16(tm + TM_O, desc_k(aa, C, k0), desc_k(aZ, DV, k0), ido, 1);
+        mma_commit(&ho_done);
+        mbar_wait(&ho_done, c & 1);
+        mbar_arrive(&bar_empty[b]);  // Q/K/A/W[b], vec[b] and U[b] are free for chunk c+2
+        if (c + 2 < NC) {
+          mbar_expect_tx(&bar_tma[b], 2 * TILE);
+          tma_load_4d(sQ(b), &mQ, 0, (c + 2) * C, 0, unit, &bar_tma[b]);
+          tma_load_4d(sK(b), &mK, 0, (c + 2) * C, 0, unit, &bar_tma[b]);
+        }
+        bulk_wait_read0();  // state save done reading sH
+        mbar_arrive(&st_free);
+      }
+      // O of the last chunk
+      mbar_wait(&h_ready, NC & 1);
+      if (a.o && NC > 0) {
+        tma_store_4d(&mO, sO, 0, (NC - 1) * C, 0, unit);
+        bulk_commit();
+      }
+      bulk_wait0();
+    }
+    __syncwarp();
   }
   cta_sync();
   if (warp == 0) tmem_dealloc<512>(tm);

@@ -46,17 +46,60 @@ def test_fwd_timeline():
         assert rc == 0
     torch.cuda.synchronize()
     t = buf.cpu().numpy().reshape(NC, 32).astype(np.int64)
-    names = {0: "P start", 1: "P tma", 2: "P empty", 3: "P gram issued+norms", 4: "P gram wait",
-             5: "P S2 (A, L)", 6: "P substitution", 7: "P T + WU issue", 8: "P WU wait",
-             9: "P W conv + full", 10: " sub L1", 11: " sub L2a", 12: " sub L2b",
-             13: " sub L3a", 14: " sub L3b", 16: "S start", 17: "S full wait",
-             22: "S MMA issue + bulk wait", 18: "S U' wait",
-             19: "S Z + HO issue", 20: "S HO wait", 21: "S H/O conv + store"}
+    names = {0: "P start", 1: "P tma+empty wait", 2: "P norms", 3: "P gram wait",
+             4: "P S2 (A, L)", 10: " sub L1", 11: " sub L2a", 12: " sub L2b", 13: " sub L3a",
+             14: " sub L3b", 5: "P substitution", 6: "P T writes", 7: "P WU wait",
+             8: "P W conv + full", 16: "S start", 17: "S full/up'/zfree wait", 18: "S Z conv",
+             19: "S ho/st wait", 20: "S H/O conv"}
     rows = []
-    for grp in ([0, 1, 2, 3, 4, 5, 10, 11, 12, 13, 14, 6, 7, 8, 9], [16, 17, 22, 18, 19, 20, 21]):
+    for grp in ([0, 1, 2, 3, 4, 10, 11, 12, 13, 14, 5, 6, 7, 8], [16, 17, 18, 19, 20]):
         for a_, b_ in zip(grp[:-1], grp[1:]):
             dt = (t[2:-2, b_] - t[2:-2, a_])
             rows.append(f"{names[b_]:28s} {dt.mean():9.0f} cycles")
         per = np.diff(t[2:-2, grp[0]]).mean()
         rows.append(f"{'-- per chunk (' + ('P' if grp[0] == 0 else 'S') + ')':28s} {per:9.0f} cycles")
+    print("\n" + "\n".join(rows))
+
+
+@pytest.mark.skipif(os.environ.get("DN_TIMING") != "1", reason="profiling aid; set DN_TIMING=1")
+def test_bwd_timeline():
+    import paper_2406_06484_b200 as dn
+    out = os.path.join(HERE, "cuda", "libdeltanet_tim.so")
+    lib = ctypes.CDLL(out)
+    cfg = synth.CONFIGS["target"]
+    x = synth.make_inputs(cfg, b_range=range(1))
+    td = torch.bfloat16
+    q, k, v, b, dO = (torch.from_numpy(x[f]).to(td).cuda() for f in ("q", "k", "v", "beta", "dO"))
+    NC = cfg.L // 64
+    buf = torch.zeros(NC * 32, dtype=torch.int64, device="cuda")
+    lib.dn_timing_set_bwd.argtypes = [ctypes.c_void_p]
+    assert lib.dn_timing_set_bwd(buf.data_ptr()) == 0
+    d = dn.make_desc(1, cfg.H, cfg.L, 128, 128, 64, td)
+    ws = torch.empty(dn.deltanet_workspace_bytes(d), dtype=torch.uint8, device="cuda")
+    o = torch.empty_like(v)
+    g = [torch.empty_like(t) for t in (q, k, v, b)]
+    P = ctypes.c_void_p
+    lib.deltanet_fwd.argtypes = [P] * 9 + [ctypes.c_size_t, P]
+    lib.deltanet_bwd.argtypes = [P] * 14 + [ctypes.c_size_t, P]
+    for _ in range(2):
+        assert lib.deltanet_fwd(ctypes.addressof(d), q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                b.data_ptr(), None, o.data_ptr(), None, ws.data_ptr(),
+                                ws.numel(), None) == 0
+        assert lib.deltanet_bwd(ctypes.addressof(d), q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                b.data_ptr(), None, dO.data_ptr(), None, g[0].data_ptr(),
+                                g[1].data_ptr(), g[2].data_ptr(), g[3].data_ptr(), None,
+                                ws.data_ptr(), ws.numel(), None) == 0
+    torch.cuda.synchronize()
+    t = buf.cpu().numpy().reshape(NC, 32).astype(np.int64)
+    names = {0: "start", 1: "tma wait", 2: "norms+scale", 3: "G wait", 4: "P2 A,L",
+             24: " sub L1", 25: " sub L2a", 26: " sub L2b", 27: " sub L3a", 28: " sub L3b",
+             16: " sub T/X writes", 5: "P3 end", 6: "W wait", 7: "P4 W conv", 8: "U/P wait",
+             9: "P5 U', P, dV, dX", 10: "A wait", 11: "P6 dA, Y", 12: "Q wait",
+             13: "P7 dq | G, Mg", 14: "K wait", 15: "P8 dk"}
+    rows = []
+    seq = [0, 1, 2, 3, 4, 24, 25, 26, 27, 28, 16, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15]
+    for a_, b_ in zip(seq[:-1], seq[1:]):
+        dt = (t[2:-2, b_] - t[2:-2, a_])
+        rows.append(f"{names[b_]:28s} {dt.mean():9.0f} cycles")
+    rows.append(f"{'-- per chunk':28s} {np.diff(t[2:-2, 0]).mean():9.0f} cycles")
     print("\n" + "\n".join(rows))

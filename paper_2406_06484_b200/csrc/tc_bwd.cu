@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(NT, 1)
 
   if (warp == 0) tmem_alloc<512>(&tslot);
   if (tid == 0) {
-    mbar_init(&bar_tma, 1);
+    mbar_init(&bar_tma, 2);
     for (int i = 0; i < MB_N; ++i) mbar_init(&mb[i], 1);
     mbar_fence_init();
     prefetch_tmap(&mQ);
@@ -163,13 +163,18 @@ __global__ void __launch_bounds__(NT, 1)
   cta_sync();
   const uint32_t tm = tslot;
 
-  auto issue_loads = [&](int c, int ks) {  // one thread
-    mbar_expect_tx(&bar_tma, 4 * TILE + D * D * 2);
-    tma_load_4d(sQ, &mQ, 0, c * C, 0, unit, &bar_tma);
+  // Two arrivals per chunk on bar_tma: (K, dO, V, H) as soon as their regions
+  // free up, and Q after the dq epilogue has read the current q_hat.
+  auto issue_loads_main = [&](int c, int ks) {  // one thread
+    mbar_expect_tx(&bar_tma, 3 * TILE + D * D * 2);
     tma_load_4d(smem + OFF_KW + ks * TILE, &mK, 0, c * C, 0, unit, &bar_tma);
     tma_load_4d(sDO, &mDO, 0, c * C, 0, unit, &bar_tma);
     tma_load_4d(sV, &mV, 0, c * C, 0, unit, &bar_tma);
     bulk_load(sH, states + (size_t)c * D * D * 2, D * D * 2, &bar_tma);
+  };
+  auto issue_load_q = [&](int c) {
+    mbar_expect_tx(&bar_tma, TILE);
+    tma_load_4d(sQ, &mQ, 0, c * C, 0, unit, &bar_tma);
   };
 
   // dH^T <- dhT^T (lane dv = w; columns split by warpgroup)
@@ -184,7 +189,10 @@ __global__ void __launch_bounds__(NT, 1)
     }
     tmem_st_wait();
   }
-  if (tid == 0 && NC > 0) issue_loads(NC - 1, 0);
+  if (tid == 0 && NC > 0) {
+    issue_loads_main(NC - 1, 0);
+    issue_load_q(NC - 1);
+  }
   cta_sync();
 
   const uint32_t aQ = smem_u32(sQ), aDO = smem_u32(sDO), aH = smem_u32(sH),
@@ -534,6 +542,12 @@ __global__ void __launch_bounds__(NT, 1)
     mbar_wait(&mb[MB_Q], ph);
     fence_after_sync();
     if (tid == 0) BSTAMP(12);
+    if (tid == 0 && c > 0) {
+      // dO, H^T (last read by M5) and the K slot of W (M4) are free; V is free
+      // once the dV store (oldest bulk group) has been read out.
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      issue_loads_main(c - 1, 1 - ks);
+    }
     if (wg == 0) {
       // lanes >= 16: dq_hat row r64 (TM_DQ) -> L2 adjoint -> dq staging
       float dot = 0.f;
@@ -623,10 +637,7 @@ __global__ void __launch_bounds__(NT, 1)
       for (int k0 = 0; k0 < C; k0 += 16)
         mma_bf16(tm + TM_DK, desc_k(aMG, C, k0), desc_mn(aK, C, k0), id_m, 1);
       mma_commit(&mb[MB_K]);
-      if (c > 0) {
-        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // dV store read done
-        issue_loads(c - 1, 1 - ks);
-      }
+      if (c > 0) issue_load_q(c - 1);  // q_hat consumed by the dq epilogue
     }
 
     // ================= P8: dK epilogue (columns split; row dot combined)

@@ -193,3 +193,135 @@ extern "C" long long probe_tmem_bw(int nthreads, int iters, int ncols) {
   cudaFree(d);
   return h[0];
 }
+
+
+// tcgen05.mma issue/execute throughput from SWIZZLE_NONE IL tiles: one thread
+// issues `n` MMAs of shape M x N x 16 (A K-major or MN-major, B K-major or
+// MN-major), then waits on a commit.  Returns cycles.
+__global__ void mma_tput_kernel(long long* out, int M, int N, int n, int a_mn, int b_mn) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  const int tid = threadIdx.x, warp = tid / 32;
+  for (int e = tid; e < 64 * 1024 / 4; e += blockDim.x) reinterpret_cast<uint32_t*>(smem)[e] = 0;
+  fence_proxy_async();
+  if (warp == 0) tmem_alloc<512>(&tslot);
+  if (tid == 0) { mbar_init(&bar, 1); mbar_fence_init(); }
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tm = tslot;
+  if (tid == 0) {
+    const uint32_t id = idesc_bf16(M, N, a_mn, b_mn);
+    const uint32_t a0 = smem_u32(smem), b0 = smem_u32(smem + 32768);
+    // A tile: M rows x 128 K (K-major) or 128 rows (K) x M cols (MN-major)
+    long long t0 = clock64();
+    for (int i = 0; i < n; ++i) {
+      const int k0 = (i % 8) * 16;
+      uint64_t ad = a_mn ? desc_mn(a0, 128, k0) : desc_k(a0, M, k0);
+      uint64_t bd = b_mn ? desc_mn(b0, 128, k0) : desc_k(b0, N, k0);
+      mma_bf16(tm, ad, bd, id, 1);
+    }
+    long long t1 = clock64();
+    mma_commit(&bar);
+    mbar_wait(&bar, 0);
+    long long t2 = clock64();
+    out[0] = t1 - t0;
+    out[1] = t2 - t0;
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tm);
+}
+
+extern "C" long long probe_mma_tput(int M, int N, int n, int a_mn, int b_mn, long long* issue) {
+  long long* d;
+  long long h[2];
+  cudaMalloc(&d, 16);
+  cudaFuncSetAttribute(mma_tput_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+  mma_tput_kernel<<<1, 128, 65536>>>(d, M, N, n, a_mn, b_mn);
+  cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  *issue = h[0];
+  return h[1];
+}
+
+
+// MMA issue-pattern variants (see test_mma_issue_patterns).
+__device__ __forceinline__ void mma_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+
+__global__ void mma_issue_kernel(long long* out, int variant, int reps) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  const int tid = threadIdx.x, warp = tid / 32;
+  for (int e = tid; e < 64 * 1024 / 4; e += blockDim.x) reinterpret_cast<uint32_t*>(smem)[e] = 0;
+  fence_proxy_async();
+  if (warp == 0) tmem_alloc<512>(&tslot);
+  if (tid == 0) { mbar_init(&bar, 1); mbar_fence_init(); }
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tm = tslot;
+  const uint32_t id = idesc_bf16(128, 64, false, false);
+  const uint32_t a0 = smem_u32(smem), b0 = smem_u32(smem + 32768);
+  long long t0 = 0, t1 = 0;
+  if (variant == 0 && tid == 0) {         // per-iteration descriptors, lane 0 only
+    t0 = clock64();
+    for (int r = 0; r < reps; ++r)
+#pragma unroll
+      for (int k0 = 0; k0 < 128; k0 += 16)
+        mma_bf16(tm, desc_k(a0, 128, k0), desc_k(b0, 64, k0), id, 1);
+    t1 = clock64();
+    mma_commit(&bar);
+  } else if (variant == 1 && tid == 0) {  // precomputed descriptors, lane 0 only
+    uint64_t ad[8], bd[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { ad[k] = desc_k(a0, 128, 16 * k); bd[k] = desc_k(b0, 64, 16 * k); }
+    t0 = clock64();
+    for (int r = 0; r < reps; ++r)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) mma_bf16(tm, ad[k], bd[k], id, 1);
+    t1 = clock64();
+    mma_commit(&bar);
+  } else if (variant == 2 && warp == 0) {  // whole warp, elect.sync inside the asm
+    uint64_t ad[8], bd[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { ad[k] = desc_k(a0, 128, 16 * k); bd[k] = desc_k(b0, 64, 16 * k); }
+    __syncwarp();
+    t0 = clock64();
+    for (int r = 0; r < reps; ++r)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) mma_elect(tm, ad[k], bd[k], id, 1);
+    t1 = clock64();
+    if (tid == 0) mma_commit(&bar);
+  }
+  if (tid == 0) {
+    mbar_wait(&bar, 0);
+    long long t2 = clock64();
+    out[0] = t1 - t0;
+    out[1] = t2 - t0;
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tm);
+}
+
+extern "C" long long probe_mma_issue(int variant, int reps, long long* issue) {
+  long long* d;
+  long long h[2];
+  cudaMalloc(&d, 16);
+  cudaFuncSetAttribute(mma_issue_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+  mma_issue_kernel<<<1, 128, 65536>>>(d, variant, reps);
+  cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  *issue = h[0];
+  return h[1];
+}

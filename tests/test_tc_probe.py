@@ -27,6 +27,10 @@ def probe():
     L.probe_mma_ts.restype = ctypes.c_int
     L.probe_tmem_bw.argtypes = [ctypes.c_int] * 3
     L.probe_tmem_bw.restype = ctypes.c_longlong
+    L.probe_mma_tput.argtypes = [ctypes.c_int] * 5 + [ctypes.POINTER(ctypes.c_longlong)]
+    L.probe_mma_tput.restype = ctypes.c_longlong
+    L.probe_mma_issue.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_longlong)]
+    L.probe_mma_issue.restype = ctypes.c_longlong
     return L
 
 
@@ -108,3 +112,30 @@ def test_tmem_read_throughput(probe):
         res[nt] = byts / cyc
     print("\nTMEM read bytes/cycle by thread count:", {k: round(v, 1) for k, v in res.items()})
     assert all(v > 0 for v in res.values())
+
+
+def test_mma_throughput(probe):
+    """Cycles per tcgen05.mma (K=16) from SWIZZLE_NONE tiles; informational
+    (ideal: max(M,128) * N / 256)."""
+    rows = []
+    for (M, N) in ((128, 64), (128, 128), (64, 64), (64, 128), (128, 256)):
+        for a_mn, b_mn in ((0, 0), (0, 1), (1, 0), (1, 1)):
+            iss = ctypes.c_longlong(0)
+            n = 256
+            cyc = probe.probe_mma_tput(M, N, n, a_mn, b_mn, ctypes.byref(iss))
+            rows.append(f"M={M} N={N} a_mn={a_mn} b_mn={b_mn}: {cyc / n:6.1f} cyc/mma "
+                        f"(issue {iss.value / n:5.1f}), ideal {max(M, 128) * N / 256:5.1f}")
+    print("\n" + "\n".join(rows))
+
+
+def test_mma_issue_patterns(probe):
+    """M=128 N=64 K=16 MMAs: cycles per instruction for three issue patterns
+    (0: descriptors rebuilt per MMA, lane 0; 1: precomputed, lane 0;
+    2: whole warp + elect.sync); informational, ideal 32."""
+    rows = []
+    for v in (0, 1, 2):
+        iss = ctypes.c_longlong(0)
+        reps = 32
+        cyc = probe.probe_mma_issue(v, reps, ctypes.byref(iss))
+        rows.append(f"variant {v}: {cyc / (8 * reps):6.1f} cyc/mma (issue {iss.value / (8 * reps):5.1f})")
+    print("\n" + "\n".join(rows))

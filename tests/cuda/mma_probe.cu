@@ -257,6 +257,8 @@ __device__ __forceinline__ void mma_elect(uint32_t tmem_d, uint64_t adesc, uint6
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
 }
 
+__device__ __forceinline__ int lane_of(int tid) { return tid & 31; }
+
 __global__ void mma_issue_kernel(long long* out, int variant, int reps) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar;
@@ -265,7 +267,7 @@ __global__ void mma_issue_kernel(long long* out, int variant, int reps) {
   for (int e = tid; e < 64 * 1024 / 4; e += blockDim.x) reinterpret_cast<uint32_t*>(smem)[e] = 0;
   fence_proxy_async();
   if (warp == 0) tmem_alloc<512>(&tslot);
-  if (tid == 0) { mbar_init(&bar, 1); mbar_fence_init(); }
+  if (tid == 0) { mbar_init(&bar, variant >= 3 ? variant - 1 : 1); mbar_fence_init(); }
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
@@ -289,6 +291,17 @@ __global__ void mma_issue_kernel(long long* out, int variant, int reps) {
     for (int r = 0; r < reps; ++r)
 #pragma unroll
       for (int k = 0; k < 8; ++k) mma_bf16(tm, ad[k], bd[k], id, 1);
+    t1 = clock64();
+    mma_commit(&bar);
+  } else if (variant >= 3 && warp < variant - 1 && lane_of(tid) == 0) {
+    // variant 3/4/5: 2/3/4 warps issue concurrently into disjoint TMEM columns
+    uint64_t ad[8], bd[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { ad[k] = desc_k(a0, 128, 16 * k); bd[k] = desc_k(b0, 64, 16 * k); }
+    t0 = clock64();
+    for (int r = 0; r < reps; ++r)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) mma_bf16(tm + 64 * warp, ad[k], bd[k], id, 1);
     t1 = clock64();
     mma_commit(&bar);
   } else if (variant == 2 && warp == 0) {  // whole warp, elect.sync inside the asm

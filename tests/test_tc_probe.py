@@ -133,9 +133,11 @@ def test_mma_issue_patterns(probe):
     (0: descriptors rebuilt per MMA, lane 0; 1: precomputed, lane 0;
     2: whole warp + elect.sync); informational, ideal 32."""
     rows = []
-    for v in (0, 1, 2):
+    for v in (0, 1, 2, 3, 4, 5):
         iss = ctypes.c_longlong(0)
         reps = 32
+        nw = v - 1 if v >= 3 else 1
         cyc = probe.probe_mma_issue(v, reps, ctypes.byref(iss))
-        rows.append(f"variant {v}: {cyc / (8 * reps):6.1f} cyc/mma (issue {iss.value / (8 * reps):5.1f})")
+        rows.append(f"variant {v} ({nw} issuing warps): {cyc / (8 * reps * nw):6.1f} cyc/mma "
+                    f"aggregate (per-warp issue {iss.value / (8 * reps):5.1f})")
     print("\n" + "\n".join(rows))

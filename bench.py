@@ -285,6 +285,14 @@ def main():
                 "unit": "TFLOP/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"] = None
+    tj = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    kname = f"tc_{name}_kernel"
+    if path == 1 and os.path.exists(tj):
+        tr = json.load(open(tj)).get(kname)
+        if tr:  # DRAM bytes per launch of this kernel from the committed ncu capture
+            roof["traffic"] = tr["dram_read_bytes"] + tr["dram_write_bytes"]
+            roof["traffic_unit"] = "bytes/launch (ncu dram__bytes_read+write, profiles/)"
+            roof["algorithmic_bytes_per_launch"] = B_k
     roof["kernel"] = f"deltanet_{name} ({'tcgen05' if path == 1 else 'simt'} path)"
     roof["peak_source"] = peaks["source"] + (" sustained" if roof["bound"] == "tensor" and long_region else "")
     roof["algorithmic_per_token_head"] = {"flops": F_k / th, "bytes": B_k / th}

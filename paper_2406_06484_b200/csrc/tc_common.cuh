@@ -263,18 +263,28 @@ __device__ __forceinline__ void wg_sync(int id) {
   asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory");
 }
 
+// Named barrier over NTH threads (NTH = 128 or 256).
+template <int NTH>
+__device__ __forceinline__ void grp_sync(int id) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(NTH) : "memory");
+}
+
 // X = (I + L)^{-1} for a 64x64 strictly-lower L, in place in LX (fp32,
-// row stride LSTRIDE floats), by the 128 threads of one warpgroup (wtid).
+// row stride LSTRIDE floats), by NTH (128 or 256) threads (wtid) that share
+// named barrier bar_id.
 // Level 1: forward substitution on the four 16x16
 // diagonal blocks, one warp per block, column-parallel in registers.
 // Levels 2-3: merge blocks pairwise, X21 = -X22 (L21 X11), for 16 -> 32 -> 64.
 // On return the lower triangle and diagonal of LX hold X; entries above the
 // diagonal hold scratch (callers mask j > i).
-template <int LSTRIDE>
+template <int LSTRIDE, int NTH = 128>
 __device__ __forceinline__ void ut_inverse_inplace(float* LX, int wtid, int bar_id,
                                                    long long* stamps = nullptr) {
+  static_assert(NTH == 128 || NTH == 256, "thread count");
+  constexpr int R2 = 512 / NTH;  // level-2 rows per thread (2 pairs x 16 x 16 outputs)
+  constexpr int R3 = 1024 / NTH;  // level-3 rows per thread (32 x 32 outputs)
   const int lane = wtid & 31, wwarp = wtid >> 5;
-  {  // level 1: block q = wwarp, column j = lane (< 16)
+  if (wwarp < 4) {  // level 1: block q = wwarp, column j = lane (< 16)
     const int o = 16 * wwarp, j = lane & 15;
     // All loads first (branch-free, so they can all be in flight), then the
     // dependent chain; x_i = [i == j] - [i > j] * sum_m L_im x_m.
@@ -305,29 +315,32 @@ __device__ __forceinline__ void ut_inverse_inplace(float* LX, int wtid, int bar_
       for (int i = 0; i < 16; ++i) LX[(o + i) * LSTRIDE + o + j] = x[i];
     }
   }
-  wg_sync(bar_id);
+  grp_sync<NTH>(bar_id);
   if (stamps && wtid == 0) stamps[0] = clock64();
   {  // level 2, pairs p = 0, 1 at offset 32p: Y = L21 X11 -> LX[o:o+16][o+16:o+32]
-    const int o = 32 * (wtid >> 6), j = wtid & 15, i0 = ((wtid >> 4) & 3) * 4;
-    float y[4] = {0.f, 0.f, 0.f, 0.f};
+    const int half = NTH / 2;
+    const int o = 32 * (wtid / half), j = wtid & 15, i0 = ((wtid % half) >> 4) * R2;
+    float y[R2];
+#pragma unroll
+    for (int ii = 0; ii < R2; ++ii) y[ii] = 0.f;
 #pragma unroll
     for (int m = 0; m < 16; m += 4) {
       const float x0 = LX[(o + m + 0) * LSTRIDE + o + j], x1 = LX[(o + m + 1) * LSTRIDE + o + j],
                   x2 = LX[(o + m + 2) * LSTRIDE + o + j], x3 = LX[(o + m + 3) * LSTRIDE + o + j];
 #pragma unroll
-      for (int ii = 0; ii < 4; ++ii) {
+      for (int ii = 0; ii < R2; ++ii) {
         const float4 l4 =
             *reinterpret_cast<const float4*>(LX + (o + 16 + i0 + ii) * LSTRIDE + o + m);
         y[ii] = fmaf(l4.x, x0, fmaf(l4.y, x1, fmaf(l4.z, x2, fmaf(l4.w, x3, y[ii]))));
       }
     }
 #pragma unroll
-    for (int ii = 0; ii < 4; ++ii) LX[(o + i0 + ii) * LSTRIDE + o + 16 + j] = y[ii];
-    wg_sync(bar_id);
-  if (stamps && wtid == 0) stamps[1] = clock64();
+    for (int ii = 0; ii < R2; ++ii) LX[(o + i0 + ii) * LSTRIDE + o + 16 + j] = y[ii];
+    grp_sync<NTH>(bar_id);
+    if (stamps && wtid == 0) stamps[1] = clock64();
     // X21 = -X22 Y -> LX[o+16:o+32][o:o+16]
 #pragma unroll
-    for (int ii = 0; ii < 4; ++ii) y[ii] = 0.f;
+    for (int ii = 0; ii < R2; ++ii) y[ii] = 0.f;
 #pragma unroll
     for (int m = 0; m < 16; m += 4) {
       const float y0 = LX[(o + m + 0) * LSTRIDE + o + 16 + j],
@@ -335,22 +348,22 @@ __device__ __forceinline__ void ut_inverse_inplace(float* LX, int wtid, int bar_
                   y2 = LX[(o + m + 2) * LSTRIDE + o + 16 + j],
                   y3 = LX[(o + m + 3) * LSTRIDE + o + 16 + j];
 #pragma unroll
-      for (int ii = 0; ii < 4; ++ii) {
+      for (int ii = 0; ii < R2; ++ii) {
         const float4 x4 =
             *reinterpret_cast<const float4*>(LX + (o + 16 + i0 + ii) * LSTRIDE + o + 16 + m);
         y[ii] = fmaf(x4.x, y0, fmaf(x4.y, y1, fmaf(x4.z, y2, fmaf(x4.w, y3, y[ii]))));
       }
     }
 #pragma unroll
-    for (int ii = 0; ii < 4; ++ii) LX[(o + 16 + i0 + ii) * LSTRIDE + o + j] = -y[ii];
+    for (int ii = 0; ii < R2; ++ii) LX[(o + 16 + i0 + ii) * LSTRIDE + o + j] = -y[ii];
   }
-  wg_sync(bar_id);
+  grp_sync<NTH>(bar_id);
   if (stamps && wtid == 0) stamps[2] = clock64();
   {  // level 3: Y = L21 X11 -> LX[0:32][32:64]
-    const int j = lane, i0 = wwarp * 8;
-    float y[8];
+    const int j = lane, i0 = wwarp * R3;
+    float y[R3];
 #pragma unroll
-    for (int ii = 0; ii < 8; ++ii) y[ii] = 0.f;
+    for (int ii = 0; ii < R3; ++ii) y[ii] = 0.f;
 #pragma unroll 2
     for (int m = 0; m < 32; m += 4) {
       // X11 is lower triangular; its upper-right 16x16 block holds level-2
@@ -360,27 +373,27 @@ __device__ __forceinline__ void ut_inverse_inplace(float* LX, int wtid, int bar_
                   x2 = LX[(m + 2) * LSTRIDE + j] * ((m + 2 >= j) ? 1.f : 0.f),
                   x3 = LX[(m + 3) * LSTRIDE + j] * ((m + 3 >= j) ? 1.f : 0.f);
 #pragma unroll
-      for (int ii = 0; ii < 8; ++ii) {
+      for (int ii = 0; ii < R3; ++ii) {
         const float4 l4 = *reinterpret_cast<const float4*>(LX + (32 + i0 + ii) * LSTRIDE + m);
         y[ii] = fmaf(l4.x, x0, fmaf(l4.y, x1, fmaf(l4.z, x2, fmaf(l4.w, x3, y[ii]))));
       }
     }
 #pragma unroll
-    for (int ii = 0; ii < 8; ++ii) LX[(i0 + ii) * LSTRIDE + 32 + j] = y[ii];
+    for (int ii = 0; ii < R3; ++ii) LX[(i0 + ii) * LSTRIDE + 32 + j] = y[ii];
   }
-  wg_sync(bar_id);
+  grp_sync<NTH>(bar_id);
   if (stamps && wtid == 0) stamps[3] = clock64();
   {  // X21 = -X22 Y -> LX[32:64][0:32]
-    const int j = lane, i0 = wwarp * 8;
-    float y[8];
+    const int j = lane, i0 = wwarp * R3;
+    float y[R3];
 #pragma unroll
-    for (int ii = 0; ii < 8; ++ii) y[ii] = 0.f;
+    for (int ii = 0; ii < R3; ++ii) y[ii] = 0.f;
 #pragma unroll 2
     for (int m = 0; m < 32; m += 4) {
       const float y0 = LX[(m + 0) * LSTRIDE + 32 + j], y1 = LX[(m + 1) * LSTRIDE + 32 + j],
                   y2 = LX[(m + 2) * LSTRIDE + 32 + j], y3 = LX[(m + 3) * LSTRIDE + 32 + j];
 #pragma unroll
-      for (int ii = 0; ii < 8; ++ii) {
+      for (int ii = 0; ii < R3; ++ii) {
         // X22 lower triangular (its upper-right 16x16 block holds scratch)
         const int r = i0 + ii;
         const float4 x4 =
@@ -391,9 +404,9 @@ __device__ __forceinline__ void ut_inverse_inplace(float* LX, int wtid, int bar_
       }
     }
 #pragma unroll
-    for (int ii = 0; ii < 8; ++ii) LX[(32 + i0 + ii) * LSTRIDE + j] = -y[ii];
+    for (int ii = 0; ii < R3; ++ii) LX[(32 + i0 + ii) * LSTRIDE + j] = -y[ii];
   }
-  wg_sync(bar_id);
+  grp_sync<NTH>(bar_id);
   if (stamps && wtid == 0) stamps[4] = clock64();
 }
 

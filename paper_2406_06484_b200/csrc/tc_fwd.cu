@@ -38,7 +38,8 @@ namespace {
 
 using namespace tc;
 
-constexpr int C = 64, DK = 128, DV = 128, NT = 320;  // 2 warpgroups + 2 MMA warps
+constexpr int C = 64, DK = 128, DV = 128, NT = 448;  // 8 prep + 4 state + 2 MMA warps
+constexpr int NP = 256;  // prep threads
 constexpr int LS = 68;  // row stride (floats) of the fp32 substitution buffer
 
 // dynamic shared memory map (bytes)
@@ -53,7 +54,7 @@ constexpr int OFF_W = OFF_A + 2 * C * C * 2;     // W^T[2] IL R=128 x 64
 constexpr int OFF_H = OFF_W + 2 * DK * C * 2;    // H^T   IL R=128 x 128
 constexpr int OFF_Z = OFF_H + DV * DK * 2;       // Z^T   IL R=128 x 64  | O staging
 constexpr int OFF_L = OFF_Z + DV * C * 2;        // L -> X fp32 [64][LS]
-constexpr int OFF_VEC = OFF_L + C * LS * 4;      // [2][beta, s, r][64] fp32
+constexpr int OFF_VEC = OFF_L + C * LS * 4 + 2 * 128 * 4;  // (LX, partial norms) | [2][beta, s, r][64]
 constexpr int SMEM_BYTES = OFF_VEC + 2 * 3 * C * 4;
 static_assert(SMEM_BYTES <= 232448 - 1024, "shared memory budget");
 
@@ -104,7 +105,7 @@ __device__ void dbg_tmem(float* dst, uint32_t tm, uint32_t col, int ncols, int M
 __device__ long long* dn_tim = nullptr;
 #define TSTAMP(slot)                                                       \
   do {                                                                     \
-    if (dn_tim != nullptr && blockIdx.x == 0 && w == 0)                    \
+    if (dn_tim != nullptr && blockIdx.x == 0 && (tid == 0 || tid == NP))   \
       dn_tim[(size_t)c * 32 + (slot)] = clock64();                         \
   } while (0)
 #define TSTAMP_PTR(slot) \
@@ -126,8 +127,9 @@ __global__ void __launch_bounds__(NT, 1)
   __shared__ uint32_t tslot;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int w = tid & 127;            // thread index inside a compute warpgroup
-  const int wwarp = w >> 5;           // warp inside the warpgroup (TMEM lane quadrant)
+  const int w = tid & 127;            // thread index inside a 128-thread group
+  const int wwarp = w >> 5;           // TMEM lane quadrant of this warp
+  const int half = (tid >> 7) & 1;    // prep: which column half this thread handles
   const int unit = blockIdx.x;
   const int L = a.L, NC = a.NC;
   const bool l2 = (a.flags & DELTANET_L2NORM_QK) != 0;
@@ -171,10 +173,13 @@ __global__ void __launch_bounds__(NT, 1)
   uint8_t* sO = sZ;
   float* LX = reinterpret_cast<float*>(smem + OFF_L);
 
-  if (warp < 4) {
+  if (warp < 8) {
     // =====================================================================
-    // Warpgroup P (warps 0-3): prep of chunk c (state independent)
+    // Prep warps 0-7 (256 threads): prep of chunk c (state independent).
+    // Every row-wise phase is split in two column halves (`half`), so each
+    // SM sub-partition runs two prep warps and hides the other's latency.
     // =====================================================================
+    float* nrm = LX + C * LS;  // [2][128] partial row norms (after LX)
     const __nv_bfloat16* beta = (const __nv_bfloat16*)a.beta + (size_t)unit * L;
     // beta is prefetched into a register one chunk ahead (global latency)
     float bnext = (w < C && w < L) ? __bfloat162float(beta[w]) : 0.f;
@@ -189,83 +194,97 @@ __global__ void __launch_bounds__(NT, 1)
       if (c >= 2) mbar_wait(&bar_empty[b], ((c >> 1) - 1) & 1);  // chain c-2 released b
       TSTAMP(1);
       {
-        // w < 64: r = 1/||q_w||; w >= 64: s = 1/||k_{w-64}||   (fp32 from bf16)
+        // w < 64: ||q_w||^2; w >= 64: ||k_{w-64}||^2, partial over this half's columns
         const int row = w & 63;
         const uint8_t* tile = w < 64 ? sQ(b) : sK(b);
-        float x[DK];
+        float x[DK / 2];
 #pragma unroll
-        for (int g = 0; g < DK / 8; ++g) il_load8(tile, C, row, g * 8, x + 8 * g);
+        for (int g = 0; g < DK / 16; ++g) il_load8(tile, C, row, DK / 2 * half + g * 8, x + 8 * g);
         float acc0 = 0.f, acc1 = 0.f;
 #pragma unroll
-        for (int e = 0; e < DK; e += 2) {
+        for (int e = 0; e < DK / 2; e += 2) {
           acc0 = fmaf(x[e], x[e], acc0);
           acc1 = fmaf(x[e + 1], x[e + 1], acc1);
         }
-        float inv = l2 ? 1.f / fmaxf(sqrtf(acc0 + acc1), a.eps) : 1.f;
+        nrm[half * 128 + w] = acc0 + acc1;
+      }
+      grp_sync<NP>(BAR_P);
+      if (half == 0) {
+        // r = 1/max(||q||, eps), s = 1/max(||k||, eps)   (R9; fp32 from bf16)
+        const int row = w & 63;
+        float inv = l2 ? 1.f / fmaxf(sqrtf(nrm[w] + nrm[128 + w]), a.eps) : 1.f;
         if (t0 + row >= L) inv = 0.f;  // padded token: exact zero contribution
         vb[(w < 64 ? 2 : 1) * C + row] = inv;
         if (w < C) vb[w] = bval;
       }
-      wg_sync(BAR_P);  // beta, s, r visible
+      grp_sync<NP>(BAR_P);  // beta, s, r visible
       TSTAMP(2);
       mbar_wait(&g_done, c & 1);
       fence_after_sync();
       TSTAMP(3);
       {
-        // one TMEM load: lanes < 16 hold G_qk rows, lanes >= 16 hold G_kk rows
-        float f[64];
-        ld64(tm, wwarp, TM_G, f);
-        const int i = wwarp * 16 + (lane & 15);
+        // one TMEM load of this half's 32 columns: lanes < 16 hold G_qk rows,
+        // lanes >= 16 hold G_kk rows
+        float f[32];
+        {
+          uint32_t r[2][16];
+          tmem_ld16(taddr(tm, wwarp * 32, TM_G + 32 * half), r[0]);
+          tmem_ld16(taddr(tm, wwarp * 32, TM_G + 32 * half + 16), r[1]);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            f[e] = __uint_as_float(r[0][e]);
+            f[16 + e] = __uint_as_float(r[1][e]);
+          }
+        }
+        const int i = wwarp * 16 + (lane & 15), h = 32 * half;
         if (lane < 16) {  // A = tril(Q K^T), raw (inclusive, R4)
 #pragma unroll
-          for (int g = 0; g < 8; ++g) {
+          for (int g = 0; g < 4; ++g) {
             float x[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) x[e] = (g * 8 + e <= i) ? f[g * 8 + e] : 0.f;
-            il_store8(sA(b), C, i, g * 8, x);
+            for (int e = 0; e < 8; ++e) x[e] = (h + g * 8 + e <= i) ? f[g * 8 + e] : 0.f;
+            il_store8(sA(b), C, i, h + g * 8, x);
           }
         } else {  // L = beta_i s_i s_j (k_i . k_j), j < i
           const float bi = vb[i] * vb[C + i];
+          float4 s4[8];  // all loads first: no smem aliasing stalls
 #pragma unroll
-          for (int h = 0; h < 64; h += 32) {
-            float4 s4[8];  // all loads first: no smem aliasing stalls
+          for (int q = 0; q < 8; ++q) s4[q] = *reinterpret_cast<const float4*>(vb + C + h + 4 * q);
 #pragma unroll
-            for (int q = 0; q < 8; ++q) s4[q] = *reinterpret_cast<const float4*>(vb + C + h + 4 * q);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const int j = h + 4 * q;
-              float4 v;
-              v.x = (j + 0 < i) ? bi * s4[q].x * f[j + 0] : 0.f;
-              v.y = (j + 1 < i) ? bi * s4[q].y * f[j + 1] : 0.f;
-              v.z = (j + 2 < i) ? bi * s4[q].z * f[j + 2] : 0.f;
-              v.w = (j + 3 < i) ? bi * s4[q].w * f[j + 3] : 0.f;
-              *reinterpret_cast<float4*>(LX + i * LS + j) = v;
-            }
+          for (int q = 0; q < 8; ++q) {
+            const int j = h + 4 * q;
+            float4 v;
+            v.x = (j + 0 < i) ? bi * s4[q].x * f[4 * q + 0] : 0.f;
+            v.y = (j + 1 < i) ? bi * s4[q].y * f[4 * q + 1] : 0.f;
+            v.z = (j + 2 < i) ? bi * s4[q].z * f[4 * q + 2] : 0.f;
+            v.w = (j + 3 < i) ? bi * s4[q].w * f[4 * q + 3] : 0.f;
+            *reinterpret_cast<float4*>(LX + i * LS + j) = v;
           }
         }
       }
       fence_before_sync();
-      wg_sync(BAR_P);
+      grp_sync<NP>(BAR_P);
       DBG(dbg_smem(dn_dbg + D_L, LX, C, C, LS, w); dbg_tmem(dn_dbg + D_GQK, tm, TM_G, C, 64, w);
           dbg_smem(dn_dbg + D_S, vb + C, 1, C, C, w); dbg_smem(dn_dbg + D_R, vb + 2 * C, 1, C, C, w);
-          dbg_smem(dn_dbg + D_B, vb, 1, C, C, w); fence_before_sync(); wg_sync(BAR_P));
-      if (w == 0) mbar_arrive(&g_free);  // the Gram accumulator may be overwritten
+          dbg_smem(dn_dbg + D_B, vb, 1, C, C, w); fence_before_sync(); grp_sync<NP>(BAR_P));
+      if (tid == 0) mbar_arrive(&g_free);  // the Gram accumulator may be overwritten
       TSTAMP(4);
-      ut_inverse_inplace<LS>(LX, w, BAR_P, TSTAMP_PTR(10));
+      ut_inverse_inplace<LS, NP>(LX, tid, BAR_P, TSTAMP_PTR(10));
       TSTAMP(5);
       DBG(dbg_smem(dn_dbg + D_X, LX, C, C, LS, w));
       {
         // T'[i][j] = X[i][j] beta_j s_j, T''[i][j] = X[i][j] beta_j  (j <= i)
-        const int i = w >> 1, j0 = (w & 1) * 32;
-        float4 x4[8], b4[8], s4[8];  // all loads first
+        const int i = tid >> 2, j0 = (tid & 3) * 16;
+        float4 x4[4], b4[4], s4[4];  // all loads first
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < 4; ++q) {
           x4[q] = *reinterpret_cast<const float4*>(LX + i * LS + j0 + 4 * q);
           b4[q] = *reinterpret_cast<const float4*>(vb + j0 + 4 * q);
           s4[q] = *reinterpret_cast<const float4*>(vb + C + j0 + 4 * q);
         }
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
+        for (int g = 0; g < 2; ++g) {
           float x[8], y[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
@@ -281,31 +300,39 @@ __global__ void __launch_bounds__(NT, 1)
         }
       }
       fence_proxy_async();
-      wg_sync(BAR_P);
-      if (w == 0) mbar_arrive(&t_ready);
+      grp_sync<NP>(BAR_P);
+      if (tid == 0) mbar_arrive(&t_ready);
       TSTAMP(6);
       mbar_wait(&wu_done, c & 1);
       fence_after_sync();
       TSTAMP(7);
       DBG(dbg_tmem(dn_dbg + D_W, tm, TM_W, C, 128, w); dbg_tmem(dn_dbg + D_U, tm, tm_u(b), C, 128, w));
-      {  // W^T (lane = dk) -> bf16 IL tile (row dk, cols = tokens)
-        float f[64];
-        ld64(tm, wwarp, TM_W, f);
+      {  // W^T (lane = dk) -> bf16 IL tile (row dk, cols = tokens), this half's columns
+        uint32_t r[2][16];
+        tmem_ld16(taddr(tm, wwarp * 32, TM_W + 32 * half), r[0]);
+        tmem_ld16(taddr(tm, wwarp * 32, TM_W + 32 * half + 16), r[1]);
+        tmem_ld_wait();
+        float f[32];
 #pragma unroll
-        for (int g = 0; g < 8; ++g) il_store8(sW(b), DK, w, g * 8, f + g * 8);
+        for (int e = 0; e < 16; ++e) {
+          f[e] = __uint_as_float(r[0][e]);
+          f[16 + e] = __uint_as_float(r[1][e]);
+        }
+#pragma unroll
+        for (int g = 0; g < 4; ++g) il_store8(sW(b), DK, w, 32 * half + g * 8, f + g * 8);
       }
       fence_proxy_async();
       fence_before_sync();
-      wg_sync(BAR_P);
-      if (w == 0) {
+      grp_sync<NP>(BAR_P);
+      if (tid == 0) {
         mbar_arrive(&w_free);
         mbar_arrive(&bar_full[b]);
       }
       TSTAMP(8);
     }
-  } else if (warp < 8) {
+  } else if (warp < 12) {
     // =====================================================================
-    // Warpgroup S (warps 4-7): state chain conversions + output epilogue
+    // Warpgroup S (warps 8-11): state chain conversions + output epilogue
     // =====================================================================
     {  // initial state: H^T row dv = w (TMEM lane w) from h0 [dk][dv]
       const float* h0 = a.h0 ? a.h0 + (size_t)unit * DK * DV : nullptr;
@@ -400,9 +427,9 @@ __global__ void __launch_bounds__(NT, 1)
         for (int e = 0; e < 64; ++e) hT[(size_t)(64 * half + e) * DV + w] = f[e];
       }
     }
-  } else if (warp == 8) {
+  } else if (warp == 12) {
     // =====================================================================
-    // Warp 8: prep MMA issue + TMA loads of V (and of Q/K for chunks 0, 1)
+    // Warp 12: prep MMA issue + TMA loads of V (and of Q/K for chunks 0, 1)
     // =====================================================================
     if (lane == 0) {
       for (int c = 0; c < 2 && c < NC; ++c) {
@@ -449,7 +476,7 @@ __global__ void __launch_bounds__(NT, 1)
     __syncwarp();
   } else {
     // =====================================================================
-    // Warp 9: state-chain MMA issue, state save, O store, next Q/K loads
+    // Warp 13: state-chain MMA issue, state save, O store, next Q/K loads
     // =====================================================================
     if (lane == 0) {
       uint8_t* states = (a.flags & DELTANET_SAVE_STATES)

@@ -274,15 +274,13 @@ __global__ void __launch_bounds__(NT, 1)
       TSTAMP(5);
       DBG(dbg_smem(dn_dbg + D_X, LX, C, C, LS, w));
       {
-        // T'[i][j] = X[i][j] beta_j s_j, T''[i][j] = X[i][j] beta_j  (j <= i)
-        const int i = tid >> 2, j0 = (tid & 3) * 16;
-        float4 x4[4], b4[4], s4[4];  // all loads first
+        // T'[i][j] = X[i][j] beta_j s_j, T''[i][j] = X[i][j] beta_j  (j <= i).
+        // Lanes map to consecutive rows (conflict-free IL stores); each thread
+        // handles one 16-column quarter of its row.
+        const int i = tid & 63, j0 = (tid >> 6) * 16;
+        float4 x4[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          x4[q] = *reinterpret_cast<const float4*>(LX + i * LS + j0 + 4 * q);
-          b4[q] = *reinterpret_cast<const float4*>(vb + j0 + 4 * q);
-          s4[q] = *reinterpret_cast<const float4*>(vb + C + j0 + 4 * q);
-        }
+        for (int q = 0; q < 4; ++q) x4[q] = *reinterpret_cast<const float4*>(LX + i * LS + j0 + 4 * q);
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
           float x[8], y[8];
@@ -290,10 +288,8 @@ __global__ void __launch_bounds__(NT, 1)
           for (int e = 0; e < 8; ++e) {
             const int j = j0 + g * 8 + e, q = 2 * g + e / 4, r = e % 4;
             const float xv = r == 0 ? x4[q].x : r == 1 ? x4[q].y : r == 2 ? x4[q].z : x4[q].w;
-            const float bv = r == 0 ? b4[q].x : r == 1 ? b4[q].y : r == 2 ? b4[q].z : b4[q].w;
-            const float sv = r == 0 ? s4[q].x : r == 1 ? s4[q].y : r == 2 ? s4[q].z : s4[q].w;
-            y[e] = (j <= i) ? xv * bv : 0.f;
-            x[e] = y[e] * sv;
+            y[e] = (j <= i) ? xv * vb[j] : 0.f;  // vb[j]: broadcast across lanes
+            x[e] = y[e] * vb[C + j];
           }
           il_store8(sT, C, i, j0 + g * 8, x);
           il_store8(sTu, C, i, j0 + g * 8, y);

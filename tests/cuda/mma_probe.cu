@@ -338,3 +338,50 @@ extern "C" long long probe_mma_issue(int variant, int reps, long long* issue) {
   *issue = h[0];
   return h[1];
 }
+
+
+// Throughput of a batch resembling the backward's M5: alternating M=64
+// accumulators at lane offsets 0 / 16 and N in {64, 128}; one thread issues.
+__global__ void mma_batch_kernel(long long* out, int N, int lane16, int n) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  const int tid = threadIdx.x, warp = tid / 32;
+  for (int e = tid; e < 64 * 1024 / 4; e += blockDim.x) reinterpret_cast<uint32_t*>(smem)[e] = 0;
+  fence_proxy_async();
+  if (warp == 0) tmem_alloc<512>(&tslot);
+  if (tid == 0) { mbar_init(&bar, 1); mbar_fence_init(); }
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tm = tslot;
+  if (tid == 0) {
+    const uint32_t id = idesc_bf16(64, N, false, true);
+    const uint32_t a0 = smem_u32(smem), b0 = smem_u32(smem + 32768);
+    uint64_t ad[8], bd[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { ad[k] = desc_k(a0, 64, 16 * k); bd[k] = desc_mn(b0, 128, 16 * k); }
+    long long t0 = clock64();
+    for (int i = 0; i < n; ++i) {
+      const uint32_t d = tm + ((lane16 && (i & 8)) ? (16u << 16) : 0u);
+      mma_bf16(d, ad[i & 7], bd[i & 7], id, 1);
+    }
+    mma_commit(&bar);
+    mbar_wait(&bar, 0);
+    out[0] = clock64() - t0;
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tm);
+}
+
+extern "C" long long probe_mma_batch(int N, int lane16, int n) {
+  long long* d;
+  long long h = 0;
+  cudaMalloc(&d, 16);
+  cudaFuncSetAttribute(mma_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+  mma_batch_kernel<<<1, 128, 65536>>>(d, N, lane16, n);
+  cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return h;
+}

@@ -31,6 +31,8 @@ def probe():
     L.probe_mma_tput.restype = ctypes.c_longlong
     L.probe_mma_issue.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_longlong)]
     L.probe_mma_issue.restype = ctypes.c_longlong
+    L.probe_mma_batch.argtypes = [ctypes.c_int] * 3
+    L.probe_mma_batch.restype = ctypes.c_longlong
     return L
 
 
@@ -118,7 +120,7 @@ def test_mma_throughput(probe):
     """Cycles per tcgen05.mma (K=16) from SWIZZLE_NONE tiles; informational
     (ideal: max(M,128) * N / 256)."""
     rows = []
-    for (M, N) in ((128, 64), (128, 128), (64, 64), (64, 128), (128, 256)):
+    for (M, N) in ((128, 64), (128, 128), (64, 64), (64, 128)):
         for a_mn, b_mn in ((0, 0), (0, 1), (1, 0), (1, 1)):
             iss = ctypes.c_longlong(0)
             n = 256
@@ -140,4 +142,16 @@ def test_mma_issue_patterns(probe):
         cyc = probe.probe_mma_issue(v, reps, ctypes.byref(iss))
         rows.append(f"variant {v} ({nw} issuing warps): {cyc / (8 * reps * nw):6.1f} cyc/mma "
                     f"aggregate (per-warp issue {iss.value / (8 * reps):5.1f})")
+    print("\n" + "\n".join(rows))
+
+
+def test_mma_m64_batches(probe):
+    """M=64 MMA batches (B MN-major), accumulators at lane offset 0 only or
+    alternating 0/16; informational cycles per MMA."""
+    rows = []
+    for N in (64, 128):
+        for l16 in (0, 1):
+            n = 256
+            cyc = probe.probe_mma_batch(N, l16, n)
+            rows.append(f"M=64 N={N} lane16_alternate={l16}: {cyc / n:6.1f} cyc/mma")
     print("\n" + "\n".join(rows))

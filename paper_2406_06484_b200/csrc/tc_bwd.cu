@@ -328,14 +328,18 @@ __global__ void __launch_bounds__(NT, 1)
     if (wg == 0) {
       ut_inverse_inplace<LS>(LX, w, BAR_P, BSTAMP_PTR(24));
       BSTAMP(16);
-      const int i = w >> 1, j0 = (w & 1) * 32;
+      // lanes <-> consecutive rows: conflict-free row loads and IL stores
+      const int i = w & 63, j0 = (w >> 6) * 32;
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
+        const float4 a4 = *reinterpret_cast<const float4*>(LX + i * LS + j0 + g * 8);
+        const float4 b4 = *reinterpret_cast<const float4*>(LX + i * LS + j0 + g * 8 + 4);
+        const float xv[8] = {a4.x, a4.y, a4.z, a4.w, b4.x, b4.y, b4.z, b4.w};
         float x[8], y[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const int j = j0 + g * 8 + e;
-          x[e] = (j <= i) ? LX[i * LS + j] : 0.f;
+          x[e] = (j <= i) ? xv[e] : 0.f;
           y[e] = x[e] * sb[j];
         }
         il_store8(sX, C, i, j0 + g * 8, x);
@@ -610,16 +614,19 @@ __global__ void __launch_bounds__(NT, 1)
       if (lo && t0 + r64 < L)
         dbeta[t0 + r64] = __float2bfloat16_rn(db1[r64] + db1[C + r64] + db2);
       wg_sync(BAR_S);
-      // Mg[i][j] = b_i G[i][j] + b_j G[j][i]  (row i = w/2, 32 columns)
-      const int i = w >> 1, j0 = (w & 1) * 32;
+      // Mg[i][j] = b_i G[i][j] + b_j G[j][i]; lanes <-> consecutive rows i
+      const int i = w & 63, j0 = (w >> 6) * 32;
       const float bi = sb[i];
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
+        const float4 a4 = *reinterpret_cast<const float4*>(Gs + i * LS + j0 + g * 8);
+        const float4 b4 = *reinterpret_cast<const float4*>(Gs + i * LS + j0 + g * 8 + 4);
+        const float gv[8] = {a4.x, a4.y, a4.z, a4.w, b4.x, b4.y, b4.z, b4.w};
         float x[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const int j = j0 + g * 8 + e;
-          x[e] = bi * Gs[i * LS + j] + sb[j] * Gs[j * LS + i];
+          x[e] = bi * gv[e] + sb[j] * Gs[j * LS + i];
         }
         il_store8(sMG, C, i, j0 + g * 8, x);
       }

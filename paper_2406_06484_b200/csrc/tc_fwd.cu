@@ -121,8 +121,8 @@ __global__ void __launch_bounds__(NT, 1)
                   Args a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   // mbarriers (DESIGN.md §4.1 "fwd pipeline")
-  __shared__ uint64_t bar_tma[2], bar_full[2], bar_empty[2];
-  __shared__ uint64_t g_done, g_free, t_ready, wu_done, w_free;        // prep side
+  __shared__ uint64_t qk_full[2], v_full[2], bar_full[2], bar_empty[2];
+  __shared__ uint64_t g_done, g_free, t_ready, w_done, wu_done, w_free;  // prep side
   __shared__ uint64_t up_done, z_free, z_ready, ho_done, h_ready, st_free;  // state side
   __shared__ uint32_t tslot;
 
@@ -137,13 +137,15 @@ __global__ void __launch_bounds__(NT, 1)
   if (warp == 0) tmem_alloc<512>(&tslot);
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&bar_tma[b], 2);  // Q/K arrival + V arrival
+      mbar_init(&qk_full[b], 1);
+      mbar_init(&v_full[b], 1);
       mbar_init(&bar_full[b], 1);
       mbar_init(&bar_empty[b], 1);
     }
     mbar_init(&g_done, 1);
     mbar_init(&g_free, 1);
     mbar_init(&t_ready, 1);
+    mbar_init(&w_done, 1);
     mbar_init(&wu_done, 1);
     mbar_init(&w_free, 1);
     mbar_init(&up_done, 1);
@@ -179,7 +181,6 @@ __global__ void __launch_bounds__(NT, 1)
     // Every row-wise phase is split in two column halves (`half`), so each
     // SM sub-partition runs two prep warps and hides the other's latency.
     // =====================================================================
-    float* nrm = LX + C * LS;  // [2][128] partial row norms (after LX)
     const __nv_bfloat16* beta = (const __nv_bfloat16*)a.beta + (size_t)unit * L;
     // beta is prefetched into a register one chunk ahead (global latency)
     float bnext = (w < C && w < L) ? __bfloat162float(beta[w]) : 0.f;
@@ -190,34 +191,9 @@ __global__ void __launch_bounds__(NT, 1)
       const float bval = bnext;
       bnext = (w < C && t0 + C + w < L) ? __bfloat162float(beta[t0 + C + w]) : 0.f;
       TSTAMP(0);
-      mbar_wait(&bar_tma[b], (c >> 1) & 1);
       if (c >= 2) mbar_wait(&bar_empty[b], ((c >> 1) - 1) & 1);  // chain c-2 released b
       TSTAMP(1);
-      {
-        // w < 64: ||q_w||^2; w >= 64: ||k_{w-64}||^2, partial over this half's columns
-        const int row = w & 63;
-        const uint8_t* tile = w < 64 ? sQ(b) : sK(b);
-        float x[DK / 2];
-#pragma unroll
-        for (int g = 0; g < DK / 16; ++g) il_load8(tile, C, row, DK / 2 * half + g * 8, x + 8 * g);
-        float acc0 = 0.f, acc1 = 0.f;
-#pragma unroll
-        for (int e = 0; e < DK / 2; e += 2) {
-          acc0 = fmaf(x[e], x[e], acc0);
-          acc1 = fmaf(x[e + 1], x[e + 1], acc1);
-        }
-        nrm[half * 128 + w] = acc0 + acc1;
-      }
-      grp_sync<NP>(BAR_P);
-      if (half == 0) {
-        // r = 1/max(||q||, eps), s = 1/max(||k||, eps)   (R9; fp32 from bf16)
-        const int row = w & 63;
-        float inv = l2 ? 1.f / fmaxf(sqrtf(nrm[w] + nrm[128 + w]), a.eps) : 1.f;
-        if (t0 + row >= L) inv = 0.f;  // padded token: exact zero contribution
-        vb[(w < 64 ? 2 : 1) * C + row] = inv;
-        if (w < C) vb[w] = bval;
-      }
-      grp_sync<NP>(BAR_P);  // beta, s, r visible
+      if (half == 0 && w < C) vb[w] = bval;
       TSTAMP(2);
       mbar_wait(&g_done, c & 1);
       fence_after_sync();
@@ -238,6 +214,18 @@ __global__ void __launch_bounds__(NT, 1)
           }
         }
         const int i = wwarp * 16 + (lane & 15), h = 32 * half;
+        // s_i = 1/max(||k_i||, eps) from the Gram diagonal (fp32 sum of exact
+        // bf16 products; R9).  r (for q) is computed by the state warpgroup.
+        if (lane >= 16 && (i >> 5) == half) {
+          float d = 0.f;  // f[i - h] as arithmetic (no dynamic register indexing)
+          const int k = i - h;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) d = fmaf(f[e], (e == k) ? 1.f : 0.f, d);
+          float inv = l2 ? 1.f / fmaxf(sqrtf(d), a.eps) : 1.f;
+          if (t0 + i >= L) inv = 0.f;  // padded token: exact zero contribution
+          vb[C + i] = inv;
+        }
+        grp_sync<NP>(BAR_P);  // beta, s visible
         if (lane < 16) {  // A = tril(Q K^T), raw (inclusive, R4)
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
@@ -266,7 +254,7 @@ __global__ void __launch_bounds__(NT, 1)
       fence_before_sync();
       grp_sync<NP>(BAR_P);
       DBG(dbg_smem(dn_dbg + D_L, LX, C, C, LS, w); dbg_tmem(dn_dbg + D_GQK, tm, TM_G, C, 64, w);
-          dbg_smem(dn_dbg + D_S, vb + C, 1, C, C, w); dbg_smem(dn_dbg + D_R, vb + 2 * C, 1, C, C, w);
+          dbg_smem(dn_dbg + D_S, vb + C, 1, C, C, w);
           dbg_smem(dn_dbg + D_B, vb, 1, C, C, w); fence_before_sync(); grp_sync<NP>(BAR_P));
       if (tid == 0) mbar_arrive(&g_free);  // the Gram accumulator may be overwritten
       TSTAMP(4);
@@ -299,7 +287,7 @@ __global__ void __launch_bounds__(NT, 1)
       grp_sync<NP>(BAR_P);
       if (tid == 0) mbar_arrive(&t_ready);
       TSTAMP(6);
-      mbar_wait(&wu_done, c & 1);
+      mbar_wait(&w_done, c & 1);
       fence_after_sync();
       TSTAMP(7);
       DBG(dbg_tmem(dn_dbg + D_W, tm, TM_W, C, 128, w); dbg_tmem(dn_dbg + D_U, tm, tm_u(b), C, 128, w));
@@ -322,6 +310,7 @@ __global__ void __launch_bounds__(NT, 1)
       grp_sync<NP>(BAR_P);
       if (tid == 0) {
         mbar_arrive(&w_free);
+        mbar_wait(&wu_done, c & 1);  // U^T[b] complete before the chain uses it
         mbar_arrive(&bar_full[b]);
       }
       TSTAMP(8);
@@ -330,6 +319,7 @@ __global__ void __launch_bounds__(NT, 1)
     // =====================================================================
     // Warpgroup S (warps 8-11): state chain conversions + output epilogue
     // =====================================================================
+    float* qn2 = LX + C * LS;  // [2][64] partial ||q||^2 (region after LX)
     {  // initial state: H^T row dv = w (TMEM lane w) from h0 [dk][dv]
       const float* h0 = a.h0 ? a.h0 + (size_t)unit * DK * DV : nullptr;
 #pragma unroll 1
@@ -357,8 +347,27 @@ __global__ void __launch_bounds__(NT, 1)
       const float* vb = vec(b);
       TSTAMP(16);
       mbar_wait(&bar_full[b], (c >> 1) & 1);
-      // r of this lane's output row, read before buffer b is released
-      const float ri = vb[2 * C + wwarp * 16 + (lane & 15)];
+      // r_i = 1/max(||q_i||, eps) for this lane's output row (R9): partial sums
+      // of squares over column halves (thread w: row w & 63, half w >> 6)
+      float ri;
+      {
+        const int row = w & 63, hh = w >> 6;
+        float x[DK / 2];
+#pragma unroll
+        for (int g = 0; g < DK / 16; ++g) il_load8(sQ(b), C, row, DK / 2 * hh + g * 8, x + 8 * g);
+        float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+        for (int e = 0; e < DK / 2; e += 2) {
+          acc0 = fmaf(x[e], x[e], acc0);
+          acc1 = fmaf(x[e + 1], x[e + 1], acc1);
+        }
+        qn2[hh * C + row] = acc0 + acc1;
+        wg_sync(BAR_S);
+        const int i = wwarp * 16 + (lane & 15);
+        ri = l2 ? 1.f / fmaxf(sqrtf(qn2[i] + qn2[C + i]), a.eps) : 1.f;
+        if (c * C + i >= L) ri = 0.f;
+        DBG(if (lane < 16) dn_dbg[D_R + i] = ri);
+      }
       mbar_wait(&up_done, c & 1);
       mbar_wait(&z_free, c & 1);
       fence_after_sync();
@@ -429,21 +438,19 @@ __global__ void __launch_bounds__(NT, 1)
     // =====================================================================
     if (lane == 0) {
       for (int c = 0; c < 2 && c < NC; ++c) {
-        mbar_expect_tx(&bar_tma[c], 2 * TILE);
-        tma_load_4d(sQ(c), &mQ, 0, c * C, 0, unit, &bar_tma[c]);
-        tma_load_4d(sK(c), &mK, 0, c * C, 0, unit, &bar_tma[c]);
+        mbar_expect_tx(&qk_full[c], 2 * TILE);
+        tma_load_4d(sQ(c), &mQ, 0, c * C, 0, unit, &qk_full[c]);
+        tma_load_4d(sK(c), &mK, 0, c * C, 0, unit, &qk_full[c]);
       }
-      mbar_expect_tx(&bar_tma[0], TILE);
-      tma_load_4d(sV, &mV, 0, 0, 0, unit, &bar_tma[0]);
+      mbar_expect_tx(&v_full[0], TILE);
+      tma_load_4d(sV, &mV, 0, 0, 0, unit, &v_full[0]);
       const uint32_t idg = idesc_bf16(64, 64, false, false);
       const uint32_t idw = idesc_bf16(128, 64, true, false);
       const uint32_t at = smem_u32(sT), atu = smem_u32(sTu), av = smem_u32(sV);
-#pragma unroll 1
-      for (int c = 0; c < NC; ++c) {
+      auto gram = [&](int c) {  // G_qk -> lanes 0-15, G_kk -> lanes 16-31 of each quadrant
         const int b = c & 1;
         const uint32_t aq = smem_u32(sQ(b)), ak = smem_u32(sK(b));
-        mbar_wait(&bar_tma[b], (c >> 1) & 1);
-        if (c >= 1) mbar_wait(&g_free, (c - 1) & 1);
+        mbar_wait(&qk_full[b], (c >> 1) & 1);
         fence_after_sync();
 #pragma unroll
         for (int k0 = 0; k0 < DK; k0 += 16) {
@@ -451,21 +458,36 @@ __global__ void __launch_bounds__(NT, 1)
           mma_bf16(tm + TM_G + LO16, desc_k(ak, C, k0), desc_k(ak, C, k0), idg, k0 > 0);
         }
         mma_commit(&g_done);
+      };
+      if (NC > 0) gram(0);
+#pragma unroll 1
+      for (int c = 0; c < NC; ++c) {
+        const int b = c & 1;
+        const uint32_t ak = smem_u32(sK(b));
+        // the next chunk's Gram as soon as the prep has read this chunk's
+        // (it then runs under this chunk's substitution)
+        if (c + 1 < NC) {
+          mbar_wait(&g_free, c & 1);
+          gram(c + 1);
+        }
         mbar_wait(&t_ready, c & 1);
         if (c >= 1) mbar_wait(&w_free, (c - 1) & 1);
         if (c >= 2) mbar_wait(&bar_empty[b], ((c >> 1) - 1) & 1);  // U[b] consumed
+        mbar_wait(&v_full[b], (c >> 1) & 1);
         fence_after_sync();
 #pragma unroll
-        for (int k0 = 0; k0 < C; k0 += 16) {
+        for (int k0 = 0; k0 < C; k0 += 16)
           mma_bf16(tm + TM_W, desc_mn(ak, C, k0), desc_k(at, C, k0), idw, k0 > 0);
+        mma_commit(&w_done);
+#pragma unroll
+        for (int k0 = 0; k0 < C; k0 += 16)
           mma_bf16(tm + tm_u(b), desc_mn(av, C, k0), desc_k(atu, C, k0), idw, k0 > 0);
-        }
         mma_commit(&wu_done);
         mbar_wait(&wu_done, c & 1);
         if (c + 1 < NC) {  // V (and T, T'') free again: prefetch the next chunk's V
           const int nb = (c + 1) & 1;
-          mbar_expect_tx(&bar_tma[nb], TILE);
-          tma_load_4d(sV, &mV, 0, (c + 1) * C, 0, unit, &bar_tma[nb]);
+          mbar_expect_tx(&v_full[nb], TILE);
+          tma_load_4d(sV, &mV, 0, (c + 1) * C, 0, unit, &v_full[nb]);
         }
       }
     }
@@ -523,9 +545,9 @@ __global__ void __launch_bounds__(NT, 1)
         mbar_wait(&ho_done, c & 1);
         mbar_arrive(&bar_empty[b]);  // Q/K/A/W[b], vec[b] and U[b] are free for chunk c+2
         if (c + 2 < NC) {
-          mbar_expect_tx(&bar_tma[b], 2 * TILE);
-          tma_load_4d(sQ(b), &mQ, 0, (c + 2) * C, 0, unit, &bar_tma[b]);
-          tma_load_4d(sK(b), &mK, 0, (c + 2) * C, 0, unit, &bar_tma[b]);
+          mbar_expect_tx(&qk_full[b], 2 * TILE);
+          tma_load_4d(sQ(b), &mQ, 0, (c + 2) * C, 0, unit, &qk_full[b]);
+          tma_load_4d(sK(b), &mK, 0, (c + 2) * C, 0, unit, &qk_full[b]);
         }
         bulk_wait_read0();  // state save done reading sH
         mbar_arrive(&st_free);

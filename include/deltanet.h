@@ -55,8 +55,11 @@ enum {
   DELTANET_L2NORM_QK = 1u << 0,
   /* fwd: write the chunk-boundary states H_t into the workspace so the bwd
    * does not recompute them (§3.2 line 250 recomputes them; we
-   * store them -- DESIGN.md "Differences from the paper").
-   * bwd: the workspace holds the states of a fwd over the same inputs. */
+   * store them -- DESIGN.md "Differences from the paper").  The tcgen05
+   * path also stores a 40 KB per-chunk record (X, W^T, Z^T)
+   * so the bwd skips the UT substitution.
+   * bwd: the workspace holds what a fwd with this flag over the same inputs
+   * and the same desc wrote. */
   DELTANET_SAVE_STATES = 1u << 1,
   /* debug: force the generic CUDA-core path even where the tcgen05 path
    * applies (both are CUDA kernels; there is no CPU fallback). */

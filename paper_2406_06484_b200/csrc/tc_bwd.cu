@@ -4,29 +4,28 @@
 // recomputed; reading R12).  This kernel evaluates the exact
 // adjoint of Eq. 8-11 chunk by chunk in reverse (DESIGN.md §4.2,
 // SURVEY App. A.2), one CTA per (b, h) unit, with dH = dl/dH_{t+1} held in
-// TMEM (fp32, lanes = d_v) across chunks and the chunk-boundary states H_t
-// read from the workspace image the forward wrote.
+// TMEM (fp32, lanes = d_v) across chunks.  The forward's per-chunk record
+// (H_t, X, W^T, Z^T = (diag(s) U')^T; tc_common.cuh REC_*) is read back, so
+// the UT substitution and the W / U / U' products are not recomputed.
 //
 // Per chunk (q_hat, k_hat: L2-normalised rows, rounded to bf16 in smem):
-//   recompute  A = tril(Q K^T), L = tril(diag(b) K K^T, -1), X = (I+L)^{-1},
-//              T = X diag(b), W = T K, U = T V, U' = U - W H, R = V - K H
+//   recompute  A = tril(Q K^T), R = V - K H, U' = diag(max(|k|,eps)) Z
 //   chain      dU' = K dH + A^T dO
 //              dH <- dH + Q^T dO - W^T dU'
 //   local      dA = tril(dO U'^T)          P = X^T dU'  (= dV_beta)
 //              dX = (dU' R^T) diag(b)      Y = X^T dX,  G = tril(-Y X^T, -1)
 //              dQ = dO H^T + dA K
-//              dK = U' dH^T + dA^T Q - dV H^T + (diag(b) G + G^T diag(b)) K
+//              dK = U' dH^T + dA^T Q - dV H^T + (G1 + G1^T) K,  G1 = diag(b) G
 //              dV = diag(b) P
 //              dbeta = rowsum(P . R) + rowsum(G . K K^T)
 //   then the L2-normalisation adjoint on dQ, dK (R9).
 // (dK_beta = X^T dW = -P H^T, and rowsum(dK_beta . K) + rowsum(P . V) =
 //  rowsum(P . R) -- DESIGN.md §4.2.)
 //
-// 256 threads.  Thread phases are split across the two warpgroups by
-// columns (both see all 128 TMEM lanes); the substitution (warpgroup 0)
-// overlaps the R / dU' conversions (warpgroup 1).  The next chunk's Q, K,
-// dO, V and H_t are prefetched by TMA during the tail of the current chunk
-// (K alternates between two slots with the W tile).
+// 256 threads; thread phases split columns between the two warpgroups (both
+// see all 128 TMEM lanes).  The next chunk's Q, K, dO, V, H_t, X and Z^T are
+// prefetched by TMA during the tail of the current chunk; W^T is loaded into
+// the other K slot at the start of the chunk (needed only at the dH update).
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
@@ -38,24 +37,22 @@ namespace {
 using namespace tc;
 
 constexpr int C = 64, D = 128, NT = 256;
-constexpr int LS = 68;
 constexpr uint32_t LO16 = 16u << 16;  // TMEM lane offset 16 (second M=64 accumulator)
 constexpr int TILE = C * D * 2;       // 16 KB
 
 // ---- shared memory map (bytes); regions reused by lifetime
-constexpr int OFF_Q = 0;                   // q_hat  IL R=64 x 128
-constexpr int OFF_KW = 16384;              // 2 slots: k_hat | W^T (IL R=128 x 64)
-constexpr int OFF_DO = 49152;              // dO     IL R=64 x 128
-constexpr int OFF_V = 65536;               // V -> dV staging
-constexpr int OFF_H = 81920;               // H^T    IL R=128 x 128
-constexpr int OFF_DH = 114688;             // dH^T   IL R=128 x 128
-constexpr int OFF_X = 147456;              // X      IL R=64 x 64
-constexpr int OFF_R = 155648;              // R (IL R=64 x 128) -> Y [0,8K) + Mg [8K,16K)
-constexpr int OFF_DUP = 172032;            // dU'^T -> U'^T (IL R=128 x 64)
-constexpr int OFF_LX = 188416;             // L/X fp32 -> G fp32 -> dk staging
-constexpr int OFF_T = OFF_LX + C * LS * 4; // T -> dX   ([T|A] = dq staging, 16 KB)
-constexpr int OFF_A = OFF_T + 8192;        // A -> dA
-constexpr int OFF_VEC = OFF_A + 8192;      // beta, r, s, nq, nk, db1[2], dot[2]
+constexpr int OFF_Q = 0;                    // q_hat  IL R=64 x 128
+constexpr int OFF_KW = OFF_Q + TILE;        // 2 slots: k_hat | W^T (IL R=128 x 64)
+constexpr int OFF_DO = OFF_KW + 2 * TILE;   // dO     IL R=64 x 128
+constexpr int OFF_V = OFF_DO + TILE;        // V -> dV staging
+constexpr int OFF_H = OFF_V + TILE;         // H^T    IL R=128 x 128
+constexpr int OFF_DH = OFF_H + D * D * 2;   // dH^T   IL R=128 x 128
+constexpr int OFF_X = OFF_DH + D * D * 2;   // X      IL R=64 x 64 (record)
+constexpr int OFF_Z = OFF_X + C * C * 2;    // Z^T (record) -> U'^T in place
+constexpr int OFF_R = OFF_Z + TILE;         // R -> Y [0,8K) + G1 [8K,16K) -> dk staging
+constexpr int OFF_DUP = OFF_R + TILE;       // dU'^T -> dq staging
+constexpr int OFF_A = OFF_DUP + TILE;       // A -> dX -> dA
+constexpr int OFF_VEC = OFF_A + C * C * 2;  // beta, r, s, nq, nk, db1[2], dot[2]
 constexpr int SMEM_BYTES = OFF_VEC + 9 * C * 4;
 static_assert(SMEM_BYTES <= 232448 - 1024, "shared memory budget");
 
@@ -66,12 +63,10 @@ constexpr uint32_t TM_R = 192, TM_P = 192 | LO16;        // K H | P     (M=64, 1
 constexpr uint32_t TM_DK = 192, TM_DQ = 192 | LO16;      // dK | dQ     (after P5)
 constexpr uint32_t TM_DU = 320;                          // dU'^T, M=128 (M1-P3)
 constexpr uint32_t TM_DX = 320, TM_GB = 320;             // dX' (M3-P5), G (M6-P7)
-constexpr uint32_t TM_W = 384;                           // W^T, M=128 (M3-P4)
 constexpr uint32_t TM_DA = 384, TM_Y = 384 | LO16;       // dA | Y (M5-P6)
-constexpr uint32_t TM_U = 448;                           // U^T -> U'^T, M=128
 
-enum { BAR_P = 1, BAR_S = 2 };
-enum { MB_G, MB_R, MB_DU, MB_W, MB_P, MB_U, MB_A, MB_Q, MB_K, MB_N };
+enum { BAR_S = 2 };
+enum { MB_G, MB_R, MB_DU, MB_WL, MB_P, MB_A, MB_Q, MB_K, MB_N };
 
 __device__ __forceinline__ void ld32(uint32_t tm, int wwarp, uint32_t col, float (&f)[32]) {
   uint32_t r[2][16];
@@ -99,11 +94,8 @@ __device__ long long* dn_tim_bwd = nullptr;
     if (dn_tim_bwd != nullptr && blockIdx.x == 0 && (tid & 127) == 0)       \
       dn_tim_bwd[(size_t)it * 32 + (slot)] = clock64();                     \
   } while (0)
-#define BSTAMP_PTR(slot) \
-  ((dn_tim_bwd != nullptr && blockIdx.x == 0) ? dn_tim_bwd + (size_t)it * 32 + (slot) : nullptr)
 #else
 #define BSTAMP(slot) do { } while (0)
-#define BSTAMP_PTR(slot) nullptr
 #endif
 
 __global__ void __launch_bounds__(NT, 1)
@@ -115,18 +107,16 @@ __global__ void __launch_bounds__(NT, 1)
   __shared__ uint64_t bar_tma, mb[MB_N];
   __shared__ uint32_t tslot;
   uint8_t *sQ = smem + OFF_Q, *sDO = smem + OFF_DO, *sV = smem + OFF_V, *sH = smem + OFF_H,
-          *sDH = smem + OFF_DH, *sX = smem + OFF_X, *sR = smem + OFF_R, *sDUP = smem + OFF_DUP,
-          *sT = smem + OFF_T, *sA = smem + OFF_A;
-  float* LX = reinterpret_cast<float*>(smem + OFF_LX);
-  uint8_t* sUP = sDUP;             // U'^T after the dH update consumed dU'^T
+          *sDH = smem + OFF_DH, *sX = smem + OFF_X, *sZ = smem + OFF_Z, *sR = smem + OFF_R,
+          *sDUP = smem + OFF_DUP, *sA = smem + OFF_A;
+  uint8_t* sUP = sZ;               // U'^T (converted in place from the record's Z^T)
   uint8_t* sDV = sV;               // dV staging (in place over V)
-  uint8_t* sDX = sT;               // dX after M3
-  uint8_t* sDA = sA;               // dA after M2
+  uint8_t* sDX = sA;               // dX after M2
+  uint8_t* sDA = sA;               // dA after M5
   uint8_t* sY = sR;                // after M3
-  uint8_t* sMG = sR + 8192;
-  float* Gs = LX;                  // after the substitution
-  uint8_t* sDQo = sT;              // [T|A] 16 KB
-  uint8_t* sDKo = smem + OFF_LX;
+  uint8_t* sG1 = sR + 8192;
+  uint8_t* sDQo = sDUP;            // dq staging after M6
+  uint8_t* sDKo = sR;              // dk staging after M7
   float* sb = reinterpret_cast<float*>(smem + OFF_VEC);  // beta
   float* sr = sb + C;        // 1/max(||q||,eps) (0: padded)
   float* ss = sr + C;        // 1/max(||k||,eps)
@@ -146,6 +136,7 @@ __global__ void __launch_bounds__(NT, 1)
   const __nv_bfloat16* beta = (const __nv_bfloat16*)a.beta + (size_t)unit * L;
   __nv_bfloat16* dbeta = (__nv_bfloat16*)a.dbeta + (size_t)unit * L;
   const uint8_t* states = (const uint8_t*)a.states + (size_t)unit * NC * (D * D * 2);
+  const uint8_t* recs = (const uint8_t*)a.scratch + (size_t)unit * NC * REC_BYTES;
 
   if (warp == 0) tmem_alloc<512>(&tslot);
   if (tid == 0) {
@@ -163,14 +154,16 @@ __global__ void __launch_bounds__(NT, 1)
   cta_sync();
   const uint32_t tm = tslot;
 
-  // Two arrivals per chunk on bar_tma: (K, dO, V, H) as soon as their regions
-  // free up, and Q after the dq epilogue has read the current q_hat.
+  // Two arrivals per chunk on bar_tma: (K, dO, V, H, X, Z) as soon as their
+  // regions free up, and Q after the dq epilogue has read the current q_hat.
   auto issue_loads_main = [&](int c, int ks) {  // one thread
-    mbar_expect_tx(&bar_tma, 3 * TILE + D * D * 2);
+    mbar_expect_tx(&bar_tma, 3 * TILE + D * D * 2 + C * C * 2 + D * C * 2);
     tma_load_4d(smem + OFF_KW + ks * TILE, &mK, 0, c * C, 0, unit, &bar_tma);
     tma_load_4d(sDO, &mDO, 0, c * C, 0, unit, &bar_tma);
     tma_load_4d(sV, &mV, 0, c * C, 0, unit, &bar_tma);
     bulk_load(sH, states + (size_t)c * D * D * 2, D * D * 2, &bar_tma);
+    bulk_load(sX, recs + (size_t)c * REC_BYTES + REC_X, C * C * 2, &bar_tma);
+    bulk_load(sZ, recs + (size_t)c * REC_BYTES + REC_Z, D * C * 2, &bar_tma);
   };
   auto issue_load_q = [&](int c) {
     mbar_expect_tx(&bar_tma, TILE);
@@ -196,10 +189,10 @@ __global__ void __launch_bounds__(NT, 1)
   cta_sync();
 
   const uint32_t aQ = smem_u32(sQ), aDO = smem_u32(sDO), aH = smem_u32(sH),
-                 aDH = smem_u32(sDH), aX = smem_u32(sX), aV = smem_u32(sV), aT = smem_u32(sT),
-                 aA = smem_u32(sA), aDUP = smem_u32(sDUP), aR = smem_u32(sR),
-                 aDA = smem_u32(sDA), aDX = smem_u32(sDX), aY = smem_u32(sY),
-                 aMG = smem_u32(sMG), aDV = smem_u32(sDV), aUP = smem_u32(sUP);
+                 aDH = smem_u32(sDH), aX = smem_u32(sX), aA = smem_u32(sA),
+                 aDUP = smem_u32(sDUP), aR = smem_u32(sR), aDA = smem_u32(sDA),
+                 aDX = smem_u32(sDX), aY = smem_u32(sY), aG1 = smem_u32(sG1),
+                 aDV = smem_u32(sDV), aUP = smem_u32(sUP);
 
 #pragma unroll 1
   for (int it = 0; it < NC; ++it) {
@@ -209,9 +202,13 @@ __global__ void __launch_bounds__(NT, 1)
     uint8_t* sW = smem + OFF_KW + (1 - ks) * TILE;
     const uint32_t aK = smem_u32(sK), aW = smem_u32(sW);
 
-    // ================= P1: dH image, loads, row norms, in-place normalisation
-    if (tid == 0) BSTAMP(0);
-    if (tid == 0) bulk_wait_read0();  // previous dk store done reading the LX region
+    // ================= P1: W load, dH image, row norms, in-place normalisation
+    BSTAMP(0);
+    if (tid == 0) {
+      bulk_wait_read0();  // previous dq / dk stores done reading the DUP / R regions
+      mbar_expect_tx(&mb[MB_WL], D * C * 2);  // W^T of this chunk into the free K slot
+      bulk_load(sW, recs + (size_t)c * REC_BYTES + REC_W, D * C * 2, &mb[MB_WL]);
+    }
     if (tid < C) sb[tid] = (t0 + tid < L) ? __bfloat162float(beta[t0 + tid]) : 0.f;
     if (wg == 1) {  // dH^T (dl/dH_{c+1}) -> bf16 image
 #pragma unroll 1
@@ -223,7 +220,7 @@ __global__ void __launch_bounds__(NT, 1)
       }
     }
     mbar_wait(&bar_tma, ph);
-    if (tid == 0) BSTAMP(1);
+    BSTAMP(1);
     if (wg == 0) {  // w < 64: q row w; w >= 64: k row w-64
       const int row = w & 63;
       const uint8_t* tile = w < 64 ? sQ : sK;
@@ -258,7 +255,7 @@ __global__ void __launch_bounds__(NT, 1)
     fence_proxy_async();
     cta_sync();
 
-    if (tid == 0) BSTAMP(2);
+    BSTAMP(2);
     // ================= M1: Gram | K H, dH^T K^T
     if (tid == 0) {
       const uint32_t idg = idesc_bf16(64, 64, false, false);
@@ -271,21 +268,21 @@ __global__ void __launch_bounds__(NT, 1)
       }
       mma_commit(&mb[MB_G]);
 #pragma unroll
-      for (int k0 = 0; k0 < D; k0 += 16) {
-        mma_bf16(tm + TM_R, desc_k(aK, C, k0), desc_k(aH, D, k0), idr, k0 > 0);
+      for (int k0 = 0; k0 < D; k0 += 16)
         mma_bf16(tm + TM_DU, desc_k(aDH, D, k0), desc_k(aK, C, k0), idd, k0 > 0);
-      }
+#pragma unroll
+      for (int k0 = 0; k0 < D; k0 += 16)
+        mma_bf16(tm + TM_R, desc_k(aK, C, k0), desc_k(aH, D, k0), idr, k0 > 0);
       mma_commit(&mb[MB_R]);
     }
 
-    // ================= P2: A = tril(Q K^T) -> bf16; L = beta_i (k_i . k_j), j < i
+    // ================= P2: A = tril(Q K^T) -> bf16 (lanes < 16: G_qk rows)
     mbar_wait(&mb[MB_G], ph);
     fence_after_sync();
-    if (tid == 0) BSTAMP(3);
+    BSTAMP(3);
     {
       float f[32];
-      ld32(tm, wwarp, TM_G + 32 * wg, f);  // lanes<16: G_qk row, lanes>=16: G_kk row
-      const int i = r64;
+      ld32(tm, wwarp, TM_G + 32 * wg, f);
       if (lo) {
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
@@ -293,28 +290,16 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const int j = 32 * wg + g * 8 + e;
-            x[e] = (j <= i) ? f[g * 8 + e] : 0.f;
+            x[e] = (j <= r64) ? f[g * 8 + e] : 0.f;
           }
-          il_store8(sA, C, i, 32 * wg + g * 8, x);
-        }
-      } else {
-        const float bi = sb[i];
-#pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-          const int jj = 32 * wg + j;
-          float4 v;
-          v.x = (jj + 0 < i) ? bi * f[j + 0] : 0.f;
-          v.y = (jj + 1 < i) ? bi * f[j + 1] : 0.f;
-          v.z = (jj + 2 < i) ? bi * f[j + 2] : 0.f;
-          v.w = (jj + 3 < i) ? bi * f[j + 3] : 0.f;
-          *reinterpret_cast<float4*>(LX + i * LS + jj) = v;
+          il_store8(sA, C, r64, 32 * wg + g * 8, x);
         }
       }
     }
     fence_proxy_async();
     cta_sync();
 
-    if (tid == 0) BSTAMP(4);
+    BSTAMP(4);
     // ================= M2: dU'^T += dO^T A
     if (tid == 0) {
       const uint32_t ida = idesc_bf16(128, 64, true, true);
@@ -324,72 +309,52 @@ __global__ void __launch_bounds__(NT, 1)
       mma_commit(&mb[MB_DU]);
     }
 
-    // ================= P3: wg0 substitution + X, T | wg1 R and dU' conversions
-    if (wg == 0) {
-      ut_inverse_inplace<LS>(LX, w, BAR_P, BSTAMP_PTR(24));
-      BSTAMP(16);
-      // lanes <-> consecutive rows: conflict-free row loads and IL stores
-      const int i = w & 63, j0 = (w >> 6) * 32;
+    // ================= P3: U' = diag(max(|k|,eps)) Z ; R = V - K H ; dU' -> bf16
+    if (l2) {  // U'^T[dv][t] = Z^T[dv][t] * max(|k_t|, eps)  (row dv = w)
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
-        const float4 a4 = *reinterpret_cast<const float4*>(LX + i * LS + j0 + g * 8);
-        const float4 b4 = *reinterpret_cast<const float4*>(LX + i * LS + j0 + g * 8 + 4);
-        const float xv[8] = {a4.x, a4.y, a4.z, a4.w, b4.x, b4.y, b4.z, b4.w};
-        float x[8], y[8];
+        const int col = 32 * wg + g * 8;
+        float z8[8];
+        il_load8(sUP, D, w, col, z8);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int j = j0 + g * 8 + e;
-          x[e] = (j <= i) ? xv[e] : 0.f;
-          y[e] = x[e] * sb[j];
-        }
-        il_store8(sX, C, i, j0 + g * 8, x);
-        il_store8(sT, C, i, j0 + g * 8, y);
+        for (int e = 0; e < 8; ++e) z8[e] *= fmaxf(nk[col + e], eps);
+        il_store8(sUP, D, w, col, z8);
       }
-    } else {
-      mbar_wait(&mb[MB_R], ph);
-      fence_after_sync();
-      BSTAMP(20);
-#pragma unroll 1
-      for (int half = 0; half < 2; ++half) {  // R = V - K H (rows r64, lanes < 16)
-        float f[64];
-        ld64(tm, wwarp, TM_R + 64 * half, f);
-        if (lo) {
+    }
+    mbar_wait(&mb[MB_R], ph);
+    fence_after_sync();
+    BSTAMP(5);
+    {  // R = V - K H (rows r64, lanes < 16; this warpgroup's 64 columns)
+      float f[64];
+      ld64(tm, wwarp, TM_R + 64 * wg, f);
+      if (lo) {
 #pragma unroll
-          for (int g = 0; g < 8; ++g) {
-            float v8[8];
-            il_load8(sV, C, r64, 64 * half + g * 8, v8);
+        for (int g = 0; g < 8; ++g) {
+          float v8[8];
+          il_load8(sV, C, r64, 64 * wg + g * 8, v8);
 #pragma unroll
-            for (int e = 0; e < 8; ++e) v8[e] -= f[g * 8 + e];
-            il_store8(sR, C, r64, 64 * half + g * 8, v8);
-          }
+          for (int e = 0; e < 8; ++e) v8[e] -= f[g * 8 + e];
+          il_store8(sR, C, r64, 64 * wg + g * 8, v8);
         }
       }
-      BSTAMP(21);
-      mbar_wait(&mb[MB_DU], ph);
-      fence_after_sync();
-      BSTAMP(22);
-      {  // dU'^T (lane d_v = w) -> bf16
-        float f[64];
-        ld64(tm, wwarp, TM_DU, f);
+    }
+    mbar_wait(&mb[MB_DU], ph);
+    fence_after_sync();
+    BSTAMP(6);
+    {  // dU'^T (lane d_v = w) -> bf16
+      float f[32];
+      ld32(tm, wwarp, TM_DU + 32 * wg, f);
 #pragma unroll
-        for (int g = 0; g < 8; ++g) il_store8(sDUP, D, w, g * 8, f + g * 8);
-      }
+      for (int g = 0; g < 4; ++g) il_store8(sDUP, D, w, 32 * wg + g * 8, f + g * 8);
     }
     fence_proxy_async();
     cta_sync();
 
-    if (tid == 0) BSTAMP(5);
-    // ================= M3: W, U | P = X^T dU', dX' = dU' R^T
+    BSTAMP(7);
+    // ================= M3: P = X^T dU', dX' = dU' R^T ; M4: dH += Q^T dO - W^T dU'
     if (tid == 0) {
-      const uint32_t idw = idesc_bf16(128, 64, true, false);
       const uint32_t idp = idesc_bf16(64, 128, true, false);
       const uint32_t idx = idesc_bf16(64, 64, true, false);
-#pragma unroll
-      for (int k0 = 0; k0 < C; k0 += 16) {
-        mma_bf16(tm + TM_W, desc_mn(aK, C, k0), desc_k(aT, C, k0), idw, k0 > 0);
-        mma_bf16(tm + TM_U, desc_mn(aV, C, k0), desc_k(aT, C, k0), idw, k0 > 0);
-      }
-      mma_commit(&mb[MB_W]);
 #pragma unroll
       for (int k0 = 0; k0 < C; k0 += 16)
         mma_bf16(tm + TM_P, desc_mn(aX, C, k0), desc_k(aDUP, D, k0), idp, k0 > 0);
@@ -397,49 +362,22 @@ __global__ void __launch_bounds__(NT, 1)
       for (int k0 = 0; k0 < D; k0 += 16)
         mma_bf16(tm + TM_DX, desc_mn(aDUP, D, k0), desc_k(aR, C, k0), idx, k0 > 0);
       mma_commit(&mb[MB_P]);
-    }
-
-    // ================= P4: W^T -> bf16 (row dk, columns split)
-    mbar_wait(&mb[MB_W], ph);
-    fence_after_sync();
-    if (tid == 0) BSTAMP(6);
-    {
-      float f[32];
-      ld32(tm, wwarp, TM_W + 32 * wg, f);
-#pragma unroll
-      for (int g = 0; g < 4; ++g) il_store8(sW, D, w, 32 * wg + g * 8, f + g * 8);
-    }
-    fence_proxy_async();
-    cta_sync();
-
-    if (tid == 0) BSTAMP(7);
-    // ================= M4: dH += Q^T dO - W^T dU' ; U' = U - W H
-    if (tid == 0) {
       const uint32_t id1 = idesc_bf16(128, 128, true, true);
       const uint32_t id2 = idesc_bf16(128, 128, false, false, true);
-      const uint32_t idn = idesc_bf16(128, 64, false, true, true);
 #pragma unroll
-      for (int k0 = 0; k0 < C; k0 += 16) {
+      for (int k0 = 0; k0 < C; k0 += 16)
         mma_bf16(tm + TM_DH, desc_mn(aDO, C, k0), desc_mn(aQ, C, k0), id1, 1);
-        mma_bf16(tm + TM_DH, desc_k(aDUP, D, k0), desc_k(aW, D, k0), id2, 1);
-      }
+      mbar_wait(&mb[MB_WL], ph);
+      fence_after_sync();
 #pragma unroll
-      for (int k0 = 0; k0 < D; k0 += 16)
-        mma_bf16(tm + TM_U, desc_k(aH, D, k0), desc_mn(aW, D, k0), idn, 1);
-      mma_commit(&mb[MB_U]);
+      for (int k0 = 0; k0 < C; k0 += 16)
+        mma_bf16(tm + TM_DH, desc_k(aDUP, D, k0), desc_k(aW, D, k0), id2, 1);
     }
 
-    // ================= P5: U'^T -> bf16 ; P, R -> dV, dbeta part ; dX
-    mbar_wait(&mb[MB_U], ph);
+    // ================= P5: P, R -> dV, dbeta part ; dX
     mbar_wait(&mb[MB_P], ph);
     fence_after_sync();
-    if (tid == 0) BSTAMP(8);
-    {
-      float f[32];
-      ld32(tm, wwarp, TM_U + 32 * wg, f);
-#pragma unroll
-      for (int g = 0; g < 4; ++g) il_store8(sUP, D, w, 32 * wg + g * 8, f + g * 8);
-    }
+    BSTAMP(8);
     {
       const float bt = sb[r64];
       float db = 0.f;
@@ -481,7 +419,7 @@ __global__ void __launch_bounds__(NT, 1)
     }
     fence_proxy_async();
     cta_sync();
-    if (tid == 0) BSTAMP(9);
+    BSTAMP(9);
     if (tid == 0) {
       tma_store_4d(&mDV, sDV, 0, t0, 0, unit);
       bulk_commit();
@@ -509,7 +447,7 @@ __global__ void __launch_bounds__(NT, 1)
     // ================= P6: dA -> bf16 (masked) | Y -> bf16
     mbar_wait(&mb[MB_A], ph);
     fence_after_sync();
-    if (tid == 0) BSTAMP(10);
+    BSTAMP(10);
     {
       float f[32];
       ld32(tm, wwarp, TM_DA + 32 * wg, f);  // lanes<16: dA row, lanes>=16: Y row
@@ -527,29 +465,31 @@ __global__ void __launch_bounds__(NT, 1)
     fence_proxy_async();
     cta_sync();
 
-    if (tid == 0) BSTAMP(11);
+    BSTAMP(11);
     // ================= M6: dQ += dA K ; dK += dA^T Q ; G = -Y X^T
     if (tid == 0) {
       const uint32_t id_q = idesc_bf16(64, 128, false, true);
       const uint32_t id_k = idesc_bf16(64, 128, true, true);
       const uint32_t id_g = idesc_bf16(64, 64, false, false, true);
 #pragma unroll
-      for (int k0 = 0; k0 < C; k0 += 16) {
+      for (int k0 = 0; k0 < C; k0 += 16)
         mma_bf16(tm + TM_GB, desc_k(aY, C, k0), desc_k(aX, C, k0), id_g, k0 > 0);
+#pragma unroll
+      for (int k0 = 0; k0 < C; k0 += 16) {
         mma_bf16(tm + TM_DQ, desc_k(aDA, C, k0), desc_mn(aK, C, k0), id_q, 1);
         mma_bf16(tm + TM_DK, desc_mn(aDA, C, k0), desc_mn(aQ, C, k0), id_k, 1);
       }
       mma_commit(&mb[MB_Q]);
     }
 
-    // ================= P7: wg0 dq epilogue | wg1 G, dbeta, Mg
+    // ================= P7: wg0 dq epilogue | wg1 G, dbeta, G1
     mbar_wait(&mb[MB_Q], ph);
     fence_after_sync();
-    if (tid == 0) BSTAMP(12);
+    BSTAMP(12);
     if (tid == 0 && c > 0) {
-      // dO, H^T (last read by M5) and the K slot of W (M4) are free; V is free
-      // once the dV store (oldest bulk group) has been read out.
-      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      // dO, H^T, X, U' (last read by M5/M6) and the W slot (M4) are free; V
+      // is free once the dV store (oldest bulk group) has been read out.
+      bulk_wait_read0();
       issue_loads_main(c - 1, 1 - ks);
     }
     if (wg == 0) {
@@ -590,6 +530,7 @@ __global__ void __launch_bounds__(NT, 1)
     } else {
       // lanes < 16: G row (TM_GB); K K^T row from lanes >= 16 (TM_G + lane 16)
       float db2 = 0.f;
+      const float bi = sb[r64];
 #pragma unroll 1
       for (int cc = 0; cc < 4; ++cc) {
         float g16[16], k16[16], kk[16];
@@ -599,50 +540,37 @@ __global__ void __launch_bounds__(NT, 1)
         for (int e = 0; e < 16; ++e) kk[e] = __shfl_xor_sync(0xffffffffu, k16[e], 16);
         if (lo) {
 #pragma unroll
-          for (int j = 0; j < 16; j += 4) {
-            const int jj = 16 * cc + j;
-            float4 v;
-            v.x = (jj + 0 < r64) ? g16[j + 0] : 0.f;
-            v.y = (jj + 1 < r64) ? g16[j + 1] : 0.f;
-            v.z = (jj + 2 < r64) ? g16[j + 2] : 0.f;
-            v.w = (jj + 3 < r64) ? g16[j + 3] : 0.f;
-            db2 = fmaf(v.x, kk[j], fmaf(v.y, kk[j + 1], fmaf(v.z, kk[j + 2], fmaf(v.w, kk[j + 3], db2))));
-            *reinterpret_cast<float4*>(Gs + r64 * LS + jj) = v;
+          for (int g = 0; g < 2; ++g) {
+            float x[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int j = 16 * cc + g * 8 + e;
+              const float gv = (j < r64) ? g16[g * 8 + e] : 0.f;
+              db2 = fmaf(gv, kk[g * 8 + e], db2);
+              x[e] = bi * gv;
+            }
+            il_store8(sG1, C, r64, 16 * cc + g * 8, x);
           }
         }
       }
       if (lo && t0 + r64 < L)
         dbeta[t0 + r64] = __float2bfloat16_rn(db1[r64] + db1[C + r64] + db2);
-      wg_sync(BAR_S);
-      // Mg[i][j] = b_i G[i][j] + b_j G[j][i]; lanes <-> consecutive rows i
-      const int i = w & 63, j0 = (w >> 6) * 32;
-      const float bi = sb[i];
-#pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        const float4 a4 = *reinterpret_cast<const float4*>(Gs + i * LS + j0 + g * 8);
-        const float4 b4 = *reinterpret_cast<const float4*>(Gs + i * LS + j0 + g * 8 + 4);
-        const float gv[8] = {a4.x, a4.y, a4.z, a4.w, b4.x, b4.y, b4.z, b4.w};
-        float x[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int j = j0 + g * 8 + e;
-          x[e] = bi * gv[e] + sb[j] * Gs[j * LS + i];
-        }
-        il_store8(sMG, C, i, j0 + g * 8, x);
-      }
     }
     fence_proxy_async();
     cta_sync();
 
-    if (tid == 0) BSTAMP(13);
-    // ================= M7: dK += Mg K ; prefetch chunk c-1
+    BSTAMP(13);
+    // ================= M7: dK += (G1 + G1^T) K ; prefetch Q of chunk c-1
     if (tid == 0) {
       tma_store_4d(&mDQ, sDQo, 0, t0, 0, unit);
       bulk_commit();
       const uint32_t id_m = idesc_bf16(64, 128, false, true);
+      const uint32_t id_mt = idesc_bf16(64, 128, true, true);
 #pragma unroll
-      for (int k0 = 0; k0 < C; k0 += 16)
-        mma_bf16(tm + TM_DK, desc_k(aMG, C, k0), desc_mn(aK, C, k0), id_m, 1);
+      for (int k0 = 0; k0 < C; k0 += 16) {
+        mma_bf16(tm + TM_DK, desc_k(aG1, C, k0), desc_mn(aK, C, k0), id_m, 1);
+        mma_bf16(tm + TM_DK, desc_mn(aG1, C, k0), desc_mn(aK, C, k0), id_mt, 1);
+      }
       mma_commit(&mb[MB_K]);
       if (c > 0) issue_load_q(c - 1);  // q_hat consumed by the dq epilogue
     }
@@ -650,7 +578,7 @@ __global__ void __launch_bounds__(NT, 1)
     // ================= P8: dK epilogue (columns split; row dot combined)
     mbar_wait(&mb[MB_K], ph);
     fence_after_sync();
-    if (tid == 0) BSTAMP(14);
+    BSTAMP(14);
     {
       float f[64];
       ld64(tm, wwarp, TM_DK + 64 * wg, f);  // lanes<16: dk_hat row r64
@@ -687,7 +615,7 @@ __global__ void __launch_bounds__(NT, 1)
       tma_store_4d(&mDK, sDKo, 0, t0, 0, unit);
       bulk_commit();
     }
-    if (tid == 0) BSTAMP(15);
+    BSTAMP(15);
   }
 
   // dh0 = dH (orientation [dk][dv]; lane dv = w, columns split)

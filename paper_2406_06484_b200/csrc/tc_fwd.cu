@@ -55,8 +55,10 @@ constexpr int OFF_H = OFF_W + 2 * DK * C * 2;    // H^T   IL R=128 x 128
 constexpr int OFF_Z = OFF_H + DV * DK * 2;       // Z^T   IL R=128 x 64  | O staging
 constexpr int OFF_L = OFF_Z + DV * C * 2;        // L -> X fp32 [64][LS]
 constexpr int OFF_VEC = OFF_L + C * LS * 4 + 2 * 128 * 4;  // (LX, partial norms) | [2][beta, s, r][64]
-constexpr int SMEM_BYTES = OFF_VEC + 2 * 3 * C * 4;
+constexpr int OFF_XB = OFF_VEC + 2 * 3 * C * 4;  // X bf16 IL R=64 x 64 (saved for the bwd)
+constexpr int SMEM_BYTES = OFF_XB + C * C * 2;
 static_assert(SMEM_BYTES <= 232448 - 1024, "shared memory budget");
+static_assert(REC_W == C * C * 2 && REC_BYTES == C * C * 2 + (DK + DV) * C * 2, "record");
 
 // TMEM column map (512 columns)
 constexpr uint32_t LO16 = 16u << 16;
@@ -172,6 +174,10 @@ __global__ void __launch_bounds__(NT, 1)
   uint8_t* sTu = smem + OFF_TU;
   uint8_t* sH = smem + OFF_H;
   uint8_t* sZ = smem + OFF_Z;
+  uint8_t* sXb = smem + OFF_XB;
+  uint8_t* recs = (a.flags & DELTANET_SAVE_STATES)
+                      ? reinterpret_cast<uint8_t*>(a.scratch) + (size_t)unit * NC * REC_BYTES
+                      : nullptr;
   uint8_t* sO = sZ;
   float* LX = reinterpret_cast<float*>(smem + OFF_L);
 
@@ -192,6 +198,7 @@ __global__ void __launch_bounds__(NT, 1)
       bnext = (w < C && t0 + C + w < L) ? __bfloat162float(beta[t0 + C + w]) : 0.f;
       TSTAMP(0);
       if (c >= 2) mbar_wait(&bar_empty[b], ((c >> 1) - 1) & 1);  // chain c-2 released b
+      if (tid == 0 && recs) bulk_wait_read0();  // record stores of chunk c-1 read out
       TSTAMP(1);
       if (half == 0 && w < C) vb[w] = bval;
       TSTAMP(2);
@@ -271,21 +278,30 @@ __global__ void __launch_bounds__(NT, 1)
         for (int q = 0; q < 4; ++q) x4[q] = *reinterpret_cast<const float4*>(LX + i * LS + j0 + 4 * q);
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
-          float x[8], y[8];
+          float x[8], y[8], xs[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const int j = j0 + g * 8 + e, q = 2 * g + e / 4, r = e % 4;
             const float xv = r == 0 ? x4[q].x : r == 1 ? x4[q].y : r == 2 ? x4[q].z : x4[q].w;
-            y[e] = (j <= i) ? xv * vb[j] : 0.f;  // vb[j]: broadcast across lanes
+            const float xm = (j <= i) ? xv : 0.f;
+            xs[e] = xm;
+            y[e] = xm * vb[j];  // vb[j]: broadcast across lanes
             x[e] = y[e] * vb[C + j];
           }
           il_store8(sT, C, i, j0 + g * 8, x);
           il_store8(sTu, C, i, j0 + g * 8, y);
+          if (recs) il_store8(sXb, C, i, j0 + g * 8, xs);
         }
       }
       fence_proxy_async();
       grp_sync<NP>(BAR_P);
-      if (tid == 0) mbar_arrive(&t_ready);
+      if (tid == 0) {
+        mbar_arrive(&t_ready);
+        if (recs) {
+          bulk_store(recs + (size_t)c * REC_BYTES + REC_X, sXb, C * C * 2);
+          bulk_commit();
+        }
+      }
       TSTAMP(6);
       mbar_wait(&w_done, c & 1);
       fence_after_sync();
@@ -310,6 +326,10 @@ __global__ void __launch_bounds__(NT, 1)
       grp_sync<NP>(BAR_P);
       if (tid == 0) {
         mbar_arrive(&w_free);
+        if (recs) {
+          bulk_store(recs + (size_t)c * REC_BYTES + REC_W, sW(b), DK * C * 2);
+          bulk_commit();
+        }
         mbar_wait(&wu_done, c & 1);  // U^T[b] complete before the chain uses it
         mbar_arrive(&bar_full[b]);
       }
@@ -534,6 +554,12 @@ __global__ void __launch_bounds__(NT, 1)
         mbar_arrive(&z_free);
         mbar_wait(&z_ready, c & 1);
         fence_after_sync();
+        if (states) {  // Z^T of this chunk for the backward (read out before st_free)
+          bulk_store(reinterpret_cast<uint8_t*>(a.scratch) + ((size_t)unit * NC + c) * REC_BYTES +
+                         REC_Z,
+                     sZ, DV * C * 2);
+          bulk_commit();
+        }
         // H^T += Z^T K (M=128,N=128,K=64); O += tril(QK^T) Z (M=64,N=128,K=64)
 #pragma unroll
         for (int k0 = 0; k0 < C; k0 += 16)
@@ -601,7 +627,11 @@ bool tc_supported(const deltanet_desc* d) {
   return d->dtype == DELTANET_BF16 && d->chunk == C && d->Dk == DK && d->Dv == DV && d->L > 0;
 }
 
-size_t tc_scratch_bytes(const deltanet_desc*) { return 0; }  // states region only
+// per-chunk records [X | W^T | Z^T] the backward reads (40 KB per chunk per unit)
+size_t tc_scratch_bytes(const deltanet_desc* d) {
+  const size_t NCk = (size_t)(d->L + C - 1) / C;
+  return (size_t)d->B * d->H * NCk * REC_BYTES;
+}
 
 // fwd: 1 kernel; bwd: 1 kernel, plus the state-recompute forward without SAVE_STATES
 int tc_launch_count(const deltanet_desc* d, int which) {

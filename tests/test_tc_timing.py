@@ -91,13 +91,12 @@ def test_bwd_timeline():
                                 ws.data_ptr(), ws.numel(), None) == 0
     torch.cuda.synchronize()
     t = buf.cpu().numpy().reshape(NC, 32).astype(np.int64)
-    names = {0: "start", 1: "tma wait", 2: "norms+scale", 3: "G wait", 4: "P2 A,L",
-             24: " sub L1", 25: " sub L2a", 26: " sub L2b", 27: " sub L3a", 28: " sub L3b",
-             16: " sub T/X writes", 5: "P3 end", 6: "W wait", 7: "P4 W conv", 8: "U/P wait",
-             9: "P5 U', P, dV, dX", 10: "A wait", 11: "P6 dA, Y", 12: "Q wait",
-             13: "P7 dq | G, Mg", 14: "K wait", 15: "P8 dk"}
+    names = {0: "start", 1: "tma wait", 2: "norms+scale", 3: "G wait", 4: "P2 A",
+             5: "P3 U' conv + R wait", 6: "P3 R conv + dU wait", 7: "P3 dU' conv",
+             8: "P wait", 9: "P5 P, dV, dX", 10: "A wait", 11: "P6 dA, Y", 12: "Q wait",
+             13: "P7 dq | G, G1", 14: "K wait", 15: "P8 dk"}
     rows = []
-    seq = [0, 1, 2, 3, 4, 24, 25, 26, 27, 28, 16, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15]
+    seq = list(range(16))
     for a_, b_ in zip(seq[:-1], seq[1:]):
         dt = (t[2:-2, b_] - t[2:-2, a_])
         rows.append(f"{names[b_]:28s} {dt.mean():9.0f} cycles")

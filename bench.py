@@ -52,58 +52,79 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms (B200_PROFILING.md)."""
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clocks + throttle reasons sampled DURING the timed region
+    (B200_PROFILING.md clocks line).  NVML (the library nvidia-smi reads)
+    polled every 5 ms from a thread, so even a ~20 ms timed region gets
+    several samples; samples outside [begin(), end()] are dropped."""
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+               "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
 
-    def __init__(self, gpu_index):
-        self.idx = gpu_index
-        self.proc = None
-        self.path = None
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.window = [None, None]
+        self.ok = False
+        self.err = None
 
     def start(self):
-        fd, self.path = tempfile.mkstemp(suffix=".csv")
-        os.close(fd)
+        import threading
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
-                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-        except Exception:
-            self.proc = None
+            import pynvml as nv
+            import torch
+            nv.nvmlInit()
+            props = torch.cuda.get_device_properties(self.device)
+            h = None
+            bus = getattr(props, "pci_bus_id", None)
+            if bus is not None:
+                dom = getattr(props, "pci_domain_id", 0)
+                dev_ = getattr(props, "pci_device_id", 0)
+                try:
+                    h = nv.nvmlDeviceGetHandleByPciBusId(f"{dom:08x}:{bus:02x}:{dev_:02x}.0")
+                except Exception:
+                    h = None
+            if h is None:
+                h = nv.nvmlDeviceGetHandleByIndex(self.device.index or 0)
+            self.nv, self.h = nv, h
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # no NVML: report it, never guess a clock
+            self.err = f"nvml unavailable: {type(e).__name__}"
+            return
+        self.stop_flag = False
+
+        def loop():
+            nv, h = self.nv, self.h
+            get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                nv.nvmlDeviceGetCurrentClocksThrottleReasons
+            while not self.stop_flag:
+                try:
+                    self.rows.append((time.perf_counter(), nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                                      nv.nvmlDeviceGetPowerUsage(h) / 1000.0, int(get_reasons(h))))
+                except Exception:
+                    pass
+                time.sleep(0.005)
+        self.thread = threading.Thread(target=loop, daemon=True)
+        self.thread.start()
+
+    def begin(self):
+        self.window[0] = time.perf_counter()
+
+    def end(self):
+        self.window[1] = time.perf_counter()
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        rows = []
-        for line in open(self.path):
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                rows.append((float(parts[1]), float(parts[2]), float(parts[3]), parts[4:]))
-            except ValueError:
-                continue
-        os.unlink(self.path)
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self.err], "samples": 0}
+        self.stop_flag = True
+        self.thread.join(timeout=2)
+        t0, t1 = self.window
+        rows = [r for r in self.rows if t0 is not None and t0 <= r[0] <= (t1 or r[0])]
         if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        load = [r for r in rows if r[2] > 250.0] or rows
-        sm = sorted(r[0] for r in load)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in load:
-            for n, flag in zip(names, r[3][1:5]):
-                if flag.strip().lower() in ("active", "1"):
-                    reasons.add(n)
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(r[1] for r in rows),
-                "reasons": sorted(reasons), "samples": len(load),
-                "power_w_max": max(r[2] for r in rows)}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        sm = sorted(r[1] for r in rows)
+        reasons = sorted(n for n, bit in self.REASONS.items() if any(r[3] & bit for r in rows))
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(r[2] for r in rows), "source": "nvml"}
 
 
 def dist_env():
@@ -236,7 +257,7 @@ def main():
         dn.deltanet_bwd(q, k, v, beta, dO, chunk=C, workspace=ws_buf, want_dh0=False,
                         out=grads, force_simt=args.force_simt)
 
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(dev)
     clocks.start()
     for _ in range(args.warmup):
         fwd()
@@ -246,6 +267,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize(dev)
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    clocks.begin()
     for i in range(args.steps):
         ev[i][0].record(stream)
         fwd()
@@ -253,6 +275,7 @@ def main():
         bwd()
         ev[i][2].record(stream)
     torch.cuda.synchronize(dev)
+    clocks.end()
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)

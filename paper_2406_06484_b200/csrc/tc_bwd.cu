@@ -22,10 +22,13 @@
 // (dK_beta = X^T dW = -P H^T, and rowsum(dK_beta . K) + rowsum(P . V) =
 //  rowsum(P . R) -- DESIGN.md §4.2.)
 //
-// 256 threads; thread phases split columns between the two warpgroups (both
-// see all 128 TMEM lanes).  The next chunk's Q, K, dO, V, H_t, X and Z^T are
-// prefetched by TMA during the tail of the current chunk; W^T is loaded into
-// the other K slot at the start of the chunk (needed only at the dH update).
+// 288 threads: warps 0-7 run the SIMT phases (split by columns between the
+// two warpgroups, both see all 128 TMEM lanes); warp 8 issues every MMA, TMA
+// load and store, driven by mbarrier hand-offs, so MMAs queue up behind each
+// other while the SIMT warps convert the previous results.  The next chunk's
+// Q, K, dO, V, H_t, X and Z^T are prefetched by TMA during the tail of the
+// current chunk; W^T is loaded into the other K slot at the start of the
+// chunk (needed only at the dH update).
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
@@ -36,7 +39,7 @@ namespace {
 
 using namespace tc;
 
-constexpr int C = 64, D = 128, NT = 256;
+constexpr int C = 64, D = 128, NT = 288;  // warps 0-7 SIMT, warp 8 issuer
 constexpr uint32_t LO16 = 16u << 16;  // TMEM lane offset 16 (second M=64 accumulator)
 constexpr int TILE = C * D * 2;       // 16 KB
 
@@ -52,8 +55,8 @@ constexpr int OFF_Z = OFF_X + C * C * 2;    // Z^T (record) -> U'^T in place
 constexpr int OFF_R = OFF_Z + TILE;         // R -> Y [0,8K) + G1 [8K,16K) -> dk staging
 constexpr int OFF_DUP = OFF_R + TILE;       // dU'^T -> dq staging
 constexpr int OFF_A = OFF_DUP + TILE;       // A -> dX -> dA
-constexpr int OFF_VEC = OFF_A + C * C * 2;  // beta, r, s, nq, nk, db1[2], dot[2]
-constexpr int SMEM_BYTES = OFF_VEC + 9 * C * 4;
+constexpr int OFF_VEC = OFF_A + C * C * 2;  // beta, r, s, nq, nk, db1[2], db2[2], dot[2], dotq[2]
+constexpr int SMEM_BYTES = OFF_VEC + 13 * C * 4;
 static_assert(SMEM_BYTES <= 232448 - 1024, "shared memory budget");
 
 // ---- TMEM column map (512 columns)
@@ -65,8 +68,11 @@ constexpr uint32_t TM_DU = 320;                          // dU'^T, M=128 (M1-P3)
 constexpr uint32_t TM_DX = 320, TM_GB = 320;             // dX' (M3-P5), G (M6-P7)
 constexpr uint32_t TM_DA = 384, TM_Y = 384 | LO16;       // dA | Y (M5-P6)
 
-enum { BAR_S = 2 };
+enum { BAR_SIMT = 1 };
+// MMA commit / load barriers (issuer -> SIMT) ...
 enum { MB_G, MB_R, MB_DU, MB_WL, MB_P, MB_A, MB_Q, MB_K, MB_N };
+// ... and hand-offs SIMT -> issuer (SG_STG: issuer -> SIMT, staging free)
+enum { SG_NORM, SG_A, SG_P3, SG_P5, SG_P6, SG_P7, SG_DQ, SG_P8, SG_STG, SG_N };
 
 __device__ __forceinline__ void ld32(uint32_t tm, int wwarp, uint32_t col, float (&f)[32]) {
   uint32_t r[2][16];
@@ -87,16 +93,33 @@ __device__ __forceinline__ void ld16f(uint32_t tm, int wwarp, uint32_t col, floa
 }
 
 #ifdef DN_TIMING
-// Test-only phase timestamps of CTA 0 (tests/test_tc_timing.py, -DDN_TIMING).
+// Test-only phase timestamps of CTA 0 (tests/test_tc_timing.py, -DDN_TIMING):
+// slots 0-15 by SIMT threads 0 / 128, slots 16-31 by the issuer.
 __device__ long long* dn_tim_bwd = nullptr;
 #define BSTAMP(slot)                                                        \
   do {                                                                      \
     if (dn_tim_bwd != nullptr && blockIdx.x == 0 && (tid & 127) == 0)       \
       dn_tim_bwd[(size_t)it * 32 + (slot)] = clock64();                     \
   } while (0)
+#define ISTAMP(slot)                                                         \
+  do {                                                                       \
+    if (dn_tim_bwd != nullptr && blockIdx.x == 0)                            \
+      dn_tim_bwd[(size_t)it * 32 + (slot)] = clock64();                      \
+  } while (0)
 #else
 #define BSTAMP(slot) do { } while (0)
+#define ISTAMP(slot) do { } while (0)
 #endif
+
+// SIMT -> issuer hand-off: operand tiles written by the 256 SIMT threads
+// become visible to the tensor core / TMA (async proxy), TMEM reads are
+// ordered before the issuer's next tcgen05 op, then one arrival.
+__device__ __forceinline__ void simt_signal(uint64_t* bar, int tid) {
+  fence_proxy_async();
+  fence_before_sync();
+  grp_sync<256>(BAR_SIMT);
+  if (tid == 0) mbar_arrive(bar);
+}
 
 __global__ void __launch_bounds__(NT, 1)
     tc_bwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
@@ -104,7 +127,7 @@ __global__ void __launch_bounds__(NT, 1)
                   const __grid_constant__ CUtensorMap mDQ, const __grid_constant__ CUtensorMap mDK,
                   const __grid_constant__ CUtensorMap mDV, Args a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bar_tma, mb[MB_N];
+  __shared__ uint64_t bar_tma, mb[MB_N], sg[SG_N];
   __shared__ uint32_t tslot;
   uint8_t *sQ = smem + OFF_Q, *sDO = smem + OFF_DO, *sV = smem + OFF_V, *sH = smem + OFF_H,
           *sDH = smem + OFF_DH, *sX = smem + OFF_X, *sZ = smem + OFF_Z, *sR = smem + OFF_R,
@@ -118,15 +141,17 @@ __global__ void __launch_bounds__(NT, 1)
   uint8_t* sDQo = sDUP;            // dq staging after M6
   uint8_t* sDKo = sR;              // dk staging after M7
   float* sb = reinterpret_cast<float*>(smem + OFF_VEC);  // beta
-  float* sr = sb + C;        // 1/max(||q||,eps) (0: padded)
-  float* ss = sr + C;        // 1/max(||k||,eps)
-  float* nq = ss + C;        // ||q||
-  float* nk = nq + C;        // ||k||
-  float* db1 = nk + C;       // [2][64] rowsum(P . R) partials
-  float* sdot = db1 + 2 * C; // [2][64] dk-adjoint dot partials
+  float* sr = sb + C;         // 1/max(||q||,eps) (0: padded)
+  float* ss = sr + C;         // 1/max(||k||,eps)
+  float* nq = ss + C;         // ||q||
+  float* nk = nq + C;         // ||k||
+  float* db1 = nk + C;        // [2][64] rowsum(P . R) partials
+  float* db2 = db1 + 2 * C;   // [2][64] rowsum(G . K K^T) partials
+  float* sdot = db2 + 2 * C;  // [2][64] dk-adjoint dot partials
+  float* sdotq = sdot + 2 * C;// [2][64] dq-adjoint dot partials
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int wg = tid >> 7, w = tid & 127, wwarp = w >> 5;
+  const int wg = (tid >> 7) & 1, w = tid & 127, wwarp = w >> 5;
   const int r64 = wwarp * 16 + (lane & 15);  // M=64 accumulator row of this lane
   const bool lo = lane < 16;
   const int unit = blockIdx.x;
@@ -142,6 +167,7 @@ __global__ void __launch_bounds__(NT, 1)
   if (tid == 0) {
     mbar_init(&bar_tma, 2);
     for (int i = 0; i < MB_N; ++i) mbar_init(&mb[i], 1);
+    for (int i = 0; i < SG_N; ++i) mbar_init(&sg[i], 1);
     mbar_fence_init();
     prefetch_tmap(&mQ);
     prefetch_tmap(&mK);
@@ -154,480 +180,538 @@ __global__ void __launch_bounds__(NT, 1)
   cta_sync();
   const uint32_t tm = tslot;
 
-  // Two arrivals per chunk on bar_tma: (K, dO, V, H, X, Z) as soon as their
-  // regions free up, and Q after the dq epilogue has read the current q_hat.
-  auto issue_loads_main = [&](int c, int ks) {  // one thread
-    mbar_expect_tx(&bar_tma, 3 * TILE + D * D * 2 + C * C * 2 + D * C * 2);
-    tma_load_4d(smem + OFF_KW + ks * TILE, &mK, 0, c * C, 0, unit, &bar_tma);
-    tma_load_4d(sDO, &mDO, 0, c * C, 0, unit, &bar_tma);
-    tma_load_4d(sV, &mV, 0, c * C, 0, unit, &bar_tma);
-    bulk_load(sH, states + (size_t)c * D * D * 2, D * D * 2, &bar_tma);
-    bulk_load(sX, recs + (size_t)c * REC_BYTES + REC_X, C * C * 2, &bar_tma);
-    bulk_load(sZ, recs + (size_t)c * REC_BYTES + REC_Z, D * C * 2, &bar_tma);
-  };
-  auto issue_load_q = [&](int c) {
-    mbar_expect_tx(&bar_tma, TILE);
-    tma_load_4d(sQ, &mQ, 0, c * C, 0, unit, &bar_tma);
-  };
-
-  // dH^T <- dhT^T (lane dv = w; columns split by warpgroup)
-  {
-    const float* dhT = a.dhT ? a.dhT + (size_t)unit * D * D : nullptr;
+  if (warp == NT / 32 - 1) {
+    // =====================================================================
+    // Issuer warp (lane 0): every tcgen05.mma, TMA load and store.  It only
+    // waits on hand-off barriers, so the SIMT warps never stall behind a
+    // full MMA queue.
+    // =====================================================================
+    if (lane == 0) {
+      const uint32_t aQ = smem_u32(sQ), aDO = smem_u32(sDO), aH = smem_u32(sH),
+                     aDH = smem_u32(sDH), aX = smem_u32(sX), aA = smem_u32(sA),
+                     aDUP = smem_u32(sDUP), aR = smem_u32(sR), aDA = smem_u32(sDA),
+                     aDX = smem_u32(sDX), aY = smem_u32(sY), aG1 = smem_u32(sG1),
+                     aDV = smem_u32(sDV), aUP = smem_u32(sUP);
+      // Two arrivals per chunk on bar_tma: (K, dO, V, H, X, Z) once their
+      // regions are free, and Q once the dq epilogue has read q_hat.
+      auto issue_loads_main = [&](int c, int ks) {
+        mbar_expect_tx(&bar_tma, 3 * TILE + D * D * 2 + C * C * 2 + D * C * 2);
+        tma_load_4d(smem + OFF_KW + ks * TILE, &mK, 0, c * C, 0, unit, &bar_tma);
+        tma_load_4d(sDO, &mDO, 0, c * C, 0, unit, &bar_tma);
+        tma_load_4d(sV, &mV, 0, c * C, 0, unit, &bar_tma);
+        bulk_load(sH, states + (size_t)c * D * D * 2, D * D * 2, &bar_tma);
+        bulk_load(sX, recs + (size_t)c * REC_BYTES + REC_X, C * C * 2, &bar_tma);
+        bulk_load(sZ, recs + (size_t)c * REC_BYTES + REC_Z, D * C * 2, &bar_tma);
+      };
+      auto issue_load_q = [&](int c) {
+        mbar_expect_tx(&bar_tma, TILE);
+        tma_load_4d(sQ, &mQ, 0, c * C, 0, unit, &bar_tma);
+      };
+      if (NC > 0) {
+        issue_loads_main(NC - 1, 0);
+        issue_load_q(NC - 1);
+      }
 #pragma unroll 1
-    for (int c0 = 64 * wg; c0 < 64 * wg + 64; c0 += 16) {
-      uint32_t r[16];
+      for (int it = 0; it < NC; ++it) {
+        const int c = NC - 1 - it, t0 = c * C, ks = it & 1;
+        const uint32_t ph = it & 1;
+        const uint32_t aK = smem_u32(smem + OFF_KW + ks * TILE);
+        uint8_t* sW = smem + OFF_KW + (1 - ks) * TILE;
+        const uint32_t aW = smem_u32(sW);
+        // I0: W^T of this chunk into the free K slot (K of chunk c+1 retired
+        // with the previous chunk's dk epilogue)
+        mbar_expect_tx(&mb[MB_WL], D * C * 2);
+        bulk_load(sW, recs + (size_t)c * REC_BYTES + REC_W, D * C * 2, &mb[MB_WL]);
+
+        // M1: Gram | dH^T K^T, K H
+        mbar_wait(&sg[SG_NORM], ph);
+        fence_after_sync();
+        ISTAMP(16);
+        {
+          const uint32_t idg = idesc_bf16(64, 64, false, false);
+          const uint32_t idr = idesc_bf16(64, 128, false, false);
+          const uint32_t idd = idesc_bf16(128, 64, false, false);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(dhT ? dhT[(size_t)(c0 + j) * D + w] : 0.f);
-      tmem_st16(taddr(tm, wwarp * 32, TM_DH + c0), r);
-    }
-    tmem_st_wait();
-  }
-  if (tid == 0 && NC > 0) {
-    issue_loads_main(NC - 1, 0);
-    issue_load_q(NC - 1);
-  }
-  cta_sync();
-
-  const uint32_t aQ = smem_u32(sQ), aDO = smem_u32(sDO), aH = smem_u32(sH),
-                 aDH = smem_u32(sDH), aX = smem_u32(sX), aA = smem_u32(sA),
-                 aDUP = smem_u32(sDUP), aR = smem_u32(sR), aDA = smem_u32(sDA),
-                 aDX = smem_u32(sDX), aY = smem_u32(sY), aG1 = smem_u32(sG1),
-                 aDV = smem_u32(sDV), aUP = smem_u32(sUP);
-
-#pragma unroll 1
-  for (int it = 0; it < NC; ++it) {
-    const int c = NC - 1 - it, t0 = c * C, ks = it & 1;
-    const uint32_t ph = it & 1;
-    uint8_t* sK = smem + OFF_KW + ks * TILE;
-    uint8_t* sW = smem + OFF_KW + (1 - ks) * TILE;
-    const uint32_t aK = smem_u32(sK), aW = smem_u32(sW);
-
-    // ================= P1: W load, dH image, row norms, in-place normalisation
-    BSTAMP(0);
-    if (tid == 0) {
-      bulk_wait_read0();  // previous dq / dk stores done reading the DUP / R regions
-      mbar_expect_tx(&mb[MB_WL], D * C * 2);  // W^T of this chunk into the free K slot
-      bulk_load(sW, recs + (size_t)c * REC_BYTES + REC_W, D * C * 2, &mb[MB_WL]);
-    }
-    if (tid < C) sb[tid] = (t0 + tid < L) ? __bfloat162float(beta[t0 + tid]) : 0.f;
-    if (wg == 1) {  // dH^T (dl/dH_{c+1}) -> bf16 image
-#pragma unroll 1
-      for (int half = 0; half < 2; ++half) {
-        float f[64];
-        ld64(tm, wwarp, TM_DH + 64 * half, f);
+          for (int k0 = 0; k0 < D; k0 += 16) {
+            mma_bf16(tm + TM_G, desc_k(aQ, C, k0), desc_k(aK, C, k0), idg, k0 > 0);
+            mma_bf16(tm + TM_G + LO16, desc_k(aK, C, k0), desc_k(aK, C, k0), idg, k0 > 0);
+          }
+          mma_commit(&mb[MB_G]);
 #pragma unroll
-        for (int g = 0; g < 8; ++g) il_store8(sDH, D, w, 64 * half + g * 8, f + g * 8);
+          for (int k0 = 0; k0 < D; k0 += 16)
+            mma_bf16(tm + TM_DU, desc_k(aDH, D, k0), desc_k(aK, C, k0), idd, k0 > 0);
+#pragma unroll
+          for (int k0 = 0; k0 < D; k0 += 16)
+            mma_bf16(tm + TM_R, desc_k(aK, C, k0), desc_k(aH, D, k0), idr, k0 > 0);
+          mma_commit(&mb[MB_R]);
+        }
+        ISTAMP(17);
+        bulk_wait_read0();  // dq / dk stores of chunk c+1 read out of the DUP / R regions
+        mbar_arrive(&sg[SG_STG]);
+
+        // M2: dU'^T += dO^T A
+        mbar_wait(&sg[SG_A], ph);
+        fence_after_sync();
+        ISTAMP(18);
+        {
+          const uint32_t ida = idesc_bf16(128, 64, true, true);
+#pragma unroll
+          for (int k0 = 0; k0 < C; k0 += 16)
+            mma_bf16(tm + TM_DU, desc_mn(aDO, C, k0), desc_mn(aA, C, k0), ida, 1);
+          mma_commit(&mb[MB_DU]);
+        }
+        ISTAMP(19);
+
+        // M3: P = X^T dU', dX' = dU' R^T ; M4: dH += Q^T dO - W^T dU'
+        mbar_wait(&sg[SG_P3], ph);
+        fence_after_sync();
+        ISTAMP(20);
+        {
+          const uint32_t idp = idesc_bf16(64, 128, true, false);
+          const uint32_t idx = idesc_bf16(64, 64, true, false);
+#pragma unroll
+          for (int k0 = 0; k0 < C; k0 += 16)
+            mma_bf16(tm + TM_P, desc_mn(aX, C, k0), desc_k(aDUP, D, k0), idp, k0 > 0);
+#pragma unroll
+          for (int k0 = 0; k0 < D; k0 += 16)
+            mma_bf16(tm + TM_DX, desc_mn(aDUP, D, k0), desc_k(aR, C, k0), idx, k0 > 0);
+          mma_commit(&mb[MB_P]);
+          const uint32_t id1 = idesc_bf16(128, 128, true, true);
+          const uint32_t id2 = idesc_bf16(128, 128, false, false, true);
+#pragma unroll
+          for (int k0 = 0; k0 < C; k0 += 16)
+            mma_bf16(tm + TM_DH, desc_mn(aDO, C, k0), desc_mn(aQ, C, k0), id1, 1);
+          mbar_wait(&mb[MB_WL], ph);
+#pragma unroll
+          for (int k0 = 0; k0 < C; k0 += 16)
+            mma_bf16(tm + TM_DH, desc_k(aDUP, D, k0), desc_k(aW, D, k0), id2, 1);
+        }
+        ISTAMP(21);
+
+        // dV store; M5: dA, Y | dQ = dO H^T, dK = U' dH^T - dV H^T
+        mbar_wait(&sg[SG_P5], ph);
+        fence_after_sync();
+        ISTAMP(22);
+        tma_store_4d(&mDV, sDV, 0, t0, 0, unit);
+        bulk_commit();
+        {
+          const uint32_t id_da = idesc_bf16(64, 64, false, true);
+          const uint32_t id_y = idesc_bf16(64, 64, true, true);
+          const uint32_t id_q = idesc_bf16(64, 128, false, true);
+          const uint32_t id_k1 = idesc_bf16(64, 128, true, true);
+          const uint32_t id_k2 = idesc_bf16(64, 128, false, true, true);
+#pragma unroll
+          for (int k0 = 0; k0 < D; k0 += 16)
+            mma_bf16(tm + TM_DA, desc_k(aDO, C, k0), desc_mn(aUP, D, k0), id_da, k0 > 0);
+#pragma unroll
+          for (int k0 = 0; k0 < C; k0 += 16)
+            mma_bf16(tm + TM_Y, desc_mn(aX, C, k0), desc_mn(aDX, C, k0), id_y, k0 > 0);
+          mma_commit(&mb[MB_A]);
+#pragma unroll
+          for (int k0 = 0; k0 < D; k0 += 16) {
+            mma_bf16(tm + TM_DQ, desc_k(aDO, C, k0), desc_mn(aH, D, k0), id_q, k0 > 0);
+            mma_bf16(tm + TM_DK, desc_mn(aUP, D, k0), desc_mn(aDH, D, k0), id_k1, k0 > 0);
+            mma_bf16(tm + TM_DK, desc_k(aDV, C, k0), desc_mn(aH, D, k0), id_k2, 1);
+          }
+        }
+        ISTAMP(23);
+
+        // M6: G = -Y X^T ; dQ += dA K ; dK += dA^T Q
+        mbar_wait(&sg[SG_P6], ph);
+        fence_after_sync();
+        ISTAMP(24);
+        {
+          const uint32_t id_q = idesc_bf16(64, 128, false, true);
+          const uint32_t id_k = idesc_bf16(64, 128, true, true);
+          const uint32_t id_g = idesc_bf16(64, 64, false, false, true);
+#pragma unroll
+          for (int k0 = 0; k0 < C; k0 += 16)
+            mma_bf16(tm + TM_GB, desc_k(aY, C, k0), desc_k(aX, C, k0), id_g, k0 > 0);
+#pragma unroll
+          for (int k0 = 0; k0 < C; k0 += 16) {
+            mma_bf16(tm + TM_DQ, desc_k(aDA, C, k0), desc_mn(aK, C, k0), id_q, 1);
+            mma_bf16(tm + TM_DK, desc_mn(aDA, C, k0), desc_mn(aQ, C, k0), id_k, 1);
+          }
+          mma_commit(&mb[MB_Q]);
+        }
+        ISTAMP(25);
+
+        // prefetch chunk c-1: dO, H^T, X, U' (last read by M5/M6) and the W
+        // slot (M4) are free after M6; V once the dV store has been read out
+        if (c > 0) {
+          mbar_wait(&mb[MB_Q], ph);
+          bulk_wait_read0();
+          issue_loads_main(c - 1, 1 - ks);
+        }
+
+        // M7: dK += (G1 + G1^T) K
+        mbar_wait(&sg[SG_P7], ph);
+        fence_after_sync();
+        ISTAMP(26);
+        {
+          const uint32_t id_m = idesc_bf16(64, 128, false, true);
+          const uint32_t id_mt = idesc_bf16(64, 128, true, true);
+#pragma unroll
+          for (int k0 = 0; k0 < C; k0 += 16) {
+            mma_bf16(tm + TM_DK, desc_k(aG1, C, k0), desc_mn(aK, C, k0), id_m, 1);
+            mma_bf16(tm + TM_DK, desc_mn(aG1, C, k0), desc_mn(aK, C, k0), id_mt, 1);
+          }
+          mma_commit(&mb[MB_K]);
+        }
+        ISTAMP(27);
+
+        // dq store, then Q of chunk c-1 (q_hat read by the dq epilogue)
+        mbar_wait(&sg[SG_DQ], ph);
+        ISTAMP(28);
+        tma_store_4d(&mDQ, sDQo, 0, t0, 0, unit);
+        bulk_commit();
+        if (c > 0) issue_load_q(c - 1);
+
+        // dk store
+        mbar_wait(&sg[SG_P8], ph);
+        ISTAMP(29);
+        tma_store_4d(&mDK, sDKo, 0, t0, 0, unit);
+        bulk_commit();
       }
+      bulk_wait0();
     }
-    mbar_wait(&bar_tma, ph);
-    BSTAMP(1);
-    if (wg == 0) {  // w < 64: q row w; w >= 64: k row w-64
-      const int row = w & 63;
-      const uint8_t* tile = w < 64 ? sQ : sK;
-      float acc = 0.f;
-#pragma unroll
-      for (int g = 0; g < D / 8; ++g) {
-        float x[8];
-        il_load8(tile, C, row, g * 8, x);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc = fmaf(x[e], x[e], acc);
-      }
-      const float n = sqrtf(acc);
-      float inv = l2 ? 1.f / fmaxf(n, eps) : 1.f;
-      if (t0 + row >= L) inv = 0.f;
-      (w < 64 ? sr : ss)[row] = inv;
-      (w < 64 ? nq : nk)[row] = n;
-    }
-    __syncthreads();
-    if (l2) {  // normalise rows in place (row = w, columns split by warpgroup)
-      const int row = w & 63;
-      uint8_t* tile = w < 64 ? sQ : sK;
-      const float inv = (w < 64 ? sr : ss)[row];
-#pragma unroll
-      for (int g = 8 * wg; g < 8 * wg + 8; ++g) {
-        float x[8];
-        il_load8(tile, C, row, g * 8, x);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) x[e] *= inv;
-        il_store8(tile, C, row, g * 8, x);
-      }
-    }
-    fence_proxy_async();
-    cta_sync();
-
-    BSTAMP(2);
-    // ================= M1: Gram | K H, dH^T K^T
-    if (tid == 0) {
-      const uint32_t idg = idesc_bf16(64, 64, false, false);
-      const uint32_t idr = idesc_bf16(64, 128, false, false);
-      const uint32_t idd = idesc_bf16(128, 64, false, false);
-#pragma unroll
-      for (int k0 = 0; k0 < D; k0 += 16) {
-        mma_bf16(tm + TM_G, desc_k(aQ, C, k0), desc_k(aK, C, k0), idg, k0 > 0);
-        mma_bf16(tm + TM_G + LO16, desc_k(aK, C, k0), desc_k(aK, C, k0), idg, k0 > 0);
-      }
-      mma_commit(&mb[MB_G]);
-#pragma unroll
-      for (int k0 = 0; k0 < D; k0 += 16)
-        mma_bf16(tm + TM_DU, desc_k(aDH, D, k0), desc_k(aK, C, k0), idd, k0 > 0);
-#pragma unroll
-      for (int k0 = 0; k0 < D; k0 += 16)
-        mma_bf16(tm + TM_R, desc_k(aK, C, k0), desc_k(aH, D, k0), idr, k0 > 0);
-      mma_commit(&mb[MB_R]);
-    }
-
-    // ================= P2: A = tril(Q K^T) -> bf16 (lanes < 16: G_qk rows)
-    mbar_wait(&mb[MB_G], ph);
-    fence_after_sync();
-    BSTAMP(3);
+    __syncwarp();
+  } else {
+    // =====================================================================
+    // SIMT warps 0-7 (two warpgroups; phases split columns between them)
+    // =====================================================================
+    // dH^T <- dhT^T (lane dv = w; columns split by warpgroup)
     {
-      float f[32];
-      ld32(tm, wwarp, TM_G + 32 * wg, f);
-      if (lo) {
+      const float* dhT = a.dhT ? a.dhT + (size_t)unit * D * D : nullptr;
+#pragma unroll 1
+      for (int c0 = 64 * wg; c0 < 64 * wg + 64; c0 += 16) {
+        uint32_t r[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(dhT ? dhT[(size_t)(c0 + j) * D + w] : 0.f);
+        tmem_st16(taddr(tm, wwarp * 32, TM_DH + c0), r);
+      }
+      tmem_st_wait();
+      fence_before_sync();
+      grp_sync<256>(BAR_SIMT);
+      fence_after_sync();
+    }
+
+#pragma unroll 1
+    for (int it = 0; it < NC; ++it) {
+      const int c = NC - 1 - it, t0 = c * C, ks = it & 1;
+      const uint32_t ph = it & 1;
+      uint8_t* sK = smem + OFF_KW + ks * TILE;
+
+      // ================= P1: dH image, row norms, in-place normalisation
+      BSTAMP(0);
+      if (tid < C) sb[tid] = (t0 + tid < L) ? __bfloat162float(beta[t0 + tid]) : 0.f;
+      if (wg == 1) {  // dH^T (dl/dH_{c+1}; complete: MB_K of chunk c+1 waited) -> bf16
+        fence_after_sync();
+#pragma unroll 1
+        for (int half = 0; half < 2; ++half) {
+          float f[64];
+          ld64(tm, wwarp, TM_DH + 64 * half, f);
+#pragma unroll
+          for (int g = 0; g < 8; ++g) il_store8(sDH, D, w, 64 * half + g * 8, f + g * 8);
+        }
+      }
+      mbar_wait(&bar_tma, ph);
+      BSTAMP(1);
+      if (wg == 0) {  // w < 64: q row w; w >= 64: k row w-64
+        const int row = w & 63;
+        const uint8_t* tile = w < 64 ? sQ : sK;
+        float acc = 0.f;
+#pragma unroll
+        for (int g = 0; g < D / 8; ++g) {
+          float x[8];
+          il_load8(tile, C, row, g * 8, x);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc = fmaf(x[e], x[e], acc);
+        }
+        const float n = sqrtf(acc);
+        float inv = l2 ? 1.f / fmaxf(n, eps) : 1.f;
+        if (t0 + row >= L) inv = 0.f;
+        (w < 64 ? sr : ss)[row] = inv;
+        (w < 64 ? nq : nk)[row] = n;
+      }
+      grp_sync<256>(BAR_SIMT);
+      if (l2) {  // normalise rows in place (row = w, columns split by warpgroup)
+        const int row = w & 63;
+        uint8_t* tile = w < 64 ? sQ : sK;
+        const float inv = (w < 64 ? sr : ss)[row];
+#pragma unroll
+        for (int g = 8 * wg; g < 8 * wg + 8; ++g) {
+          float x[8];
+          il_load8(tile, C, row, g * 8, x);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) x[e] *= inv;
+          il_store8(tile, C, row, g * 8, x);
+        }
+      }
+      simt_signal(&sg[SG_NORM], tid);
+      BSTAMP(2);
+
+      // ================= P2: A = tril(Q K^T) -> bf16 (lanes < 16: G_qk rows)
+      mbar_wait(&mb[MB_G], ph);
+      fence_after_sync();
+      BSTAMP(3);
+      {
+        float f[32];
+        ld32(tm, wwarp, TM_G + 32 * wg, f);
+        if (lo) {
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            float x[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int j = 32 * wg + g * 8 + e;
+              x[e] = (j <= r64) ? f[g * 8 + e] : 0.f;
+            }
+            il_store8(sA, C, r64, 32 * wg + g * 8, x);
+          }
+        }
+      }
+      simt_signal(&sg[SG_A], tid);
+      BSTAMP(4);
+
+      // ================= P3: U' = diag(max(|k|,eps)) Z ; R = V - K H ; dU' -> bf16
+      if (l2) {  // U'^T[dv][t] = Z^T[dv][t] * max(|k_t|, eps)  (row dv = w)
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const int col = 32 * wg + g * 8;
+          float z8[8];
+          il_load8(sUP, D, w, col, z8);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) z8[e] *= fmaxf(nk[col + e], eps);
+          il_store8(sUP, D, w, col, z8);
+        }
+      }
+      mbar_wait(&sg[SG_STG], ph);  // R / DUP regions free (previous dq/dk stores read out)
+      mbar_wait(&mb[MB_R], ph);
+      fence_after_sync();
+      BSTAMP(5);
+      // R = V - K H, row r64, this warpgroup's 64 columns; lanes < 16 hold the
+      // accumulator row, each lane pair splits every 16 columns 8 / 8
+#pragma unroll 1
+      for (int cc = 0; cc < 4; ++cc) {
+        const int col = 64 * wg + 16 * cc;
+        float f[16], x[8];
+        ld16f(tm, wwarp, TM_R + col, f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) x[e] = __shfl_xor_sync(0xffffffffu, f[8 + e], 16);
+        if (lo) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) x[e] = f[e];
+        }
+        const int c8 = col + (lo ? 0 : 8);
+        float v8[8];
+        il_load8(sV, C, r64, c8, v8);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v8[e] -= x[e];
+        il_store8(sR, C, r64, c8, v8);
+      }
+      mbar_wait(&mb[MB_DU], ph);
+      fence_after_sync();
+      BSTAMP(6);
+      {  // dU'^T (lane d_v = w) -> bf16
+        float f[32];
+        ld32(tm, wwarp, TM_DU + 32 * wg, f);
+#pragma unroll
+        for (int g = 0; g < 4; ++g) il_store8(sDUP, D, w, 32 * wg + g * 8, f + g * 8);
+      }
+      simt_signal(&sg[SG_P3], tid);
+      BSTAMP(7);
+
+      // ================= P5: P, R -> dV, dbeta part ; dX
+      mbar_wait(&mb[MB_P], ph);
+      fence_after_sync();
+      BSTAMP(8);
+      {
+        // lanes < 16 hold (K H) rows, lanes >= 16 P rows (same r64): each lane
+        // pair trades halves so that both lanes work on 8 of every 16 columns
+        const float bt = sb[r64];
+        float db = 0.f;
+#pragma unroll 1
+        for (int cc = 0; cc < 4; ++cc) {
+          const int col = 64 * wg + 16 * cc;
+          float f[16], x[8];
+          ld16f(tm, wwarp, TM_R + col, f);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) x[e] = __shfl_xor_sync(0xffffffffu, lo ? f[8 + e] : f[e], 16);
+          const int c8 = col + (lo ? 0 : 8);
+          float v8[8], dv8[8];
+          il_load8(sV, C, r64, c8, v8);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float kh = lo ? f[e] : x[e];
+            const float p = lo ? x[e] : f[8 + e];
+            db = fmaf(p, v8[e] - kh, db);  // P . R
+            dv8[e] = bt * p;
+          }
+          il_store8(sDV, C, r64, c8, dv8);
+        }
+        db += __shfl_xor_sync(0xffffffffu, db, 16);
+        if (lo) db1[wg * C + r64] = db;
+      }
+#pragma unroll 1
+      for (int cc = 0; cc < 2; ++cc) {  // dX = dX' diag(beta) (lanes < 16: dX' rows)
+        const int col = 32 * wg + 16 * cc;
+        float f[16], x[8];
+        ld16f(tm, wwarp, TM_DX + col, f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) x[e] = __shfl_xor_sync(0xffffffffu, f[8 + e], 16);
+        if (lo) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) x[e] = f[e];
+        }
+        const int c8 = col + (lo ? 0 : 8);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) x[e] *= sb[c8 + e];
+        il_store8(sDX, C, r64, c8, x);
+      }
+      simt_signal(&sg[SG_P5], tid);
+      BSTAMP(9);
+
+      // ================= P6: dA -> bf16 (masked) | Y -> bf16
+      mbar_wait(&mb[MB_A], ph);
+      fence_after_sync();
+      BSTAMP(10);
+      {
+        float f[32];
+        ld32(tm, wwarp, TM_DA + 32 * wg, f);  // lanes<16: dA row, lanes>=16: Y row
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           float x[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const int j = 32 * wg + g * 8 + e;
-            x[e] = (j <= r64) ? f[g * 8 + e] : 0.f;
+            x[e] = (!lo || j <= r64) ? f[g * 8 + e] : 0.f;
           }
-          il_store8(sA, C, r64, 32 * wg + g * 8, x);
+          il_store8(lo ? sDA : sY, C, r64, 32 * wg + g * 8, x);
         }
       }
-    }
-    fence_proxy_async();
-    cta_sync();
+      simt_signal(&sg[SG_P6], tid);
+      BSTAMP(11);
 
-    BSTAMP(4);
-    // ================= M2: dU'^T += dO^T A
-    if (tid == 0) {
-      const uint32_t ida = idesc_bf16(128, 64, true, true);
-#pragma unroll
-      for (int k0 = 0; k0 < C; k0 += 16)
-        mma_bf16(tm + TM_DU, desc_mn(aDO, C, k0), desc_mn(aA, C, k0), ida, 1);
-      mma_commit(&mb[MB_DU]);
-    }
-
-    // ================= P3: U' = diag(max(|k|,eps)) Z ; R = V - K H ; dU' -> bf16
-    if (l2) {  // U'^T[dv][t] = Z^T[dv][t] * max(|k_t|, eps)  (row dv = w)
-#pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        const int col = 32 * wg + g * 8;
-        float z8[8];
-        il_load8(sUP, D, w, col, z8);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) z8[e] *= fmaxf(nk[col + e], eps);
-        il_store8(sUP, D, w, col, z8);
-      }
-    }
-    mbar_wait(&mb[MB_R], ph);
-    fence_after_sync();
-    BSTAMP(5);
-    {  // R = V - K H (rows r64, lanes < 16; this warpgroup's 64 columns)
-      float f[64];
-      ld64(tm, wwarp, TM_R + 64 * wg, f);
-      if (lo) {
-#pragma unroll
-        for (int g = 0; g < 8; ++g) {
-          float v8[8];
-          il_load8(sV, C, r64, 64 * wg + g * 8, v8);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) v8[e] -= f[g * 8 + e];
-          il_store8(sR, C, r64, 64 * wg + g * 8, v8);
-        }
-      }
-    }
-    mbar_wait(&mb[MB_DU], ph);
-    fence_after_sync();
-    BSTAMP(6);
-    {  // dU'^T (lane d_v = w) -> bf16
-      float f[32];
-      ld32(tm, wwarp, TM_DU + 32 * wg, f);
-#pragma unroll
-      for (int g = 0; g < 4; ++g) il_store8(sDUP, D, w, 32 * wg + g * 8, f + g * 8);
-    }
-    fence_proxy_async();
-    cta_sync();
-
-    BSTAMP(7);
-    // ================= M3: P = X^T dU', dX' = dU' R^T ; M4: dH += Q^T dO - W^T dU'
-    if (tid == 0) {
-      const uint32_t idp = idesc_bf16(64, 128, true, false);
-      const uint32_t idx = idesc_bf16(64, 64, true, false);
-#pragma unroll
-      for (int k0 = 0; k0 < C; k0 += 16)
-        mma_bf16(tm + TM_P, desc_mn(aX, C, k0), desc_k(aDUP, D, k0), idp, k0 > 0);
-#pragma unroll
-      for (int k0 = 0; k0 < D; k0 += 16)
-        mma_bf16(tm + TM_DX, desc_mn(aDUP, D, k0), desc_k(aR, C, k0), idx, k0 > 0);
-      mma_commit(&mb[MB_P]);
-      const uint32_t id1 = idesc_bf16(128, 128, true, true);
-      const uint32_t id2 = idesc_bf16(128, 128, false, false, true);
-#pragma unroll
-      for (int k0 = 0; k0 < C; k0 += 16)
-        mma_bf16(tm + TM_DH, desc_mn(aDO, C, k0), desc_mn(aQ, C, k0), id1, 1);
-      mbar_wait(&mb[MB_WL], ph);
+      // ================= P7: G1 = diag(b) G, dbeta part 2 ; then the dq epilogue
+      mbar_wait(&mb[MB_Q], ph);
       fence_after_sync();
-#pragma unroll
-      for (int k0 = 0; k0 < C; k0 += 16)
-        mma_bf16(tm + TM_DH, desc_k(aDUP, D, k0), desc_k(aW, D, k0), id2, 1);
-    }
-
-    // ================= P5: P, R -> dV, dbeta part ; dX
-    mbar_wait(&mb[MB_P], ph);
-    fence_after_sync();
-    BSTAMP(8);
-    {
-      const float bt = sb[r64];
-      float db = 0.f;
+      BSTAMP(12);
+      {
+        // lanes < 16: G row (TM_GB); K K^T row from lanes >= 16 (TM_G + lane 16)
+        float d2 = 0.f;
+        const float bi = sb[r64];
 #pragma unroll 1
-      for (int cc = 0; cc < 4; ++cc) {
-        const int col = 64 * wg + 16 * cc;
-        float f[16], p[16];
-        ld16f(tm, wwarp, TM_R + col, f);  // lanes<16: (K H) row; lanes>=16: P row
+        for (int cc = 0; cc < 2; ++cc) {
+          const int col = 32 * wg + 16 * cc;
+          float g16[16], k16[16], kk[16];
+          ld16f(tm, wwarp, TM_GB + col, g16);
+          ld16f(tm, wwarp, TM_G + col, k16);
 #pragma unroll
-        for (int e = 0; e < 16; ++e) p[e] = __shfl_xor_sync(0xffffffffu, f[e], 16);
-        if (lo) {
+          for (int e = 0; e < 16; ++e) kk[e] = __shfl_xor_sync(0xffffffffu, k16[e], 16);
+          if (lo) {
 #pragma unroll
-          for (int g = 0; g < 2; ++g) {
-            float v8[8], dv8[8];
-            il_load8(sV, C, r64, col + g * 8, v8);
+            for (int g = 0; g < 2; ++g) {
+              float x[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              db = fmaf(p[g * 8 + e], v8[e] - f[g * 8 + e], db);  // P . R
-              dv8[e] = bt * p[g * 8 + e];
+              for (int e = 0; e < 8; ++e) {
+                const int j = col + g * 8 + e;
+                const float gv = (j < r64) ? g16[g * 8 + e] : 0.f;
+                d2 = fmaf(gv, kk[g * 8 + e], d2);
+                x[e] = bi * gv;
+              }
+              il_store8(sG1, C, r64, col + g * 8, x);
             }
-            il_store8(sDV, C, r64, col + g * 8, dv8);
           }
         }
+        if (lo) db2[wg * C + r64] = d2;
       }
-      if (lo) db1[wg * C + r64] = db;
-    }
-    {
-      float f[32];
-      ld32(tm, wwarp, TM_DX + 32 * wg, f);  // lanes<16: dX' row
-      if (lo) {
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          float x[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) x[e] = f[g * 8 + e] * sb[32 * wg + g * 8 + e];
-          il_store8(sDX, C, r64, 32 * wg + g * 8, x);
-        }
-      }
-    }
-    fence_proxy_async();
-    cta_sync();
-    BSTAMP(9);
-    if (tid == 0) {
-      tma_store_4d(&mDV, sDV, 0, t0, 0, unit);
-      bulk_commit();
-      // ================= M5: dA, Y, dQ = dO H^T, dK = U' dH^T - dV H^T
-      const uint32_t id_da = idesc_bf16(64, 64, false, true);
-      const uint32_t id_y = idesc_bf16(64, 64, true, true);
-      const uint32_t id_q = idesc_bf16(64, 128, false, true);
-      const uint32_t id_k1 = idesc_bf16(64, 128, true, true);
-      const uint32_t id_k2 = idesc_bf16(64, 128, false, true, true);
-#pragma unroll
-      for (int k0 = 0; k0 < D; k0 += 16)
-        mma_bf16(tm + TM_DA, desc_k(aDO, C, k0), desc_mn(aUP, D, k0), id_da, k0 > 0);
-#pragma unroll
-      for (int k0 = 0; k0 < C; k0 += 16)
-        mma_bf16(tm + TM_Y, desc_mn(aX, C, k0), desc_mn(aDX, C, k0), id_y, k0 > 0);
-      mma_commit(&mb[MB_A]);
-#pragma unroll
-      for (int k0 = 0; k0 < D; k0 += 16) {
-        mma_bf16(tm + TM_DQ, desc_k(aDO, C, k0), desc_mn(aH, D, k0), id_q, k0 > 0);
-        mma_bf16(tm + TM_DK, desc_mn(aUP, D, k0), desc_mn(aDH, D, k0), id_k1, k0 > 0);
-        mma_bf16(tm + TM_DK, desc_k(aDV, C, k0), desc_mn(aH, D, k0), id_k2, 1);
-      }
-    }
-
-    // ================= P6: dA -> bf16 (masked) | Y -> bf16
-    mbar_wait(&mb[MB_A], ph);
-    fence_after_sync();
-    BSTAMP(10);
-    {
-      float f[32];
-      ld32(tm, wwarp, TM_DA + 32 * wg, f);  // lanes<16: dA row, lanes>=16: Y row
-#pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        float x[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int j = 32 * wg + g * 8 + e;
-          x[e] = (!lo || j <= r64) ? f[g * 8 + e] : 0.f;
-        }
-        il_store8(lo ? sDA : sY, C, r64, 32 * wg + g * 8, x);
-      }
-    }
-    fence_proxy_async();
-    cta_sync();
-
-    BSTAMP(11);
-    // ================= M6: dQ += dA K ; dK += dA^T Q ; G = -Y X^T
-    if (tid == 0) {
-      const uint32_t id_q = idesc_bf16(64, 128, false, true);
-      const uint32_t id_k = idesc_bf16(64, 128, true, true);
-      const uint32_t id_g = idesc_bf16(64, 64, false, false, true);
-#pragma unroll
-      for (int k0 = 0; k0 < C; k0 += 16)
-        mma_bf16(tm + TM_GB, desc_k(aY, C, k0), desc_k(aX, C, k0), id_g, k0 > 0);
-#pragma unroll
-      for (int k0 = 0; k0 < C; k0 += 16) {
-        mma_bf16(tm + TM_DQ, desc_k(aDA, C, k0), desc_mn(aK, C, k0), id_q, 1);
-        mma_bf16(tm + TM_DK, desc_mn(aDA, C, k0), desc_mn(aQ, C, k0), id_k, 1);
-      }
-      mma_commit(&mb[MB_Q]);
-    }
-
-    // ================= P7: wg0 dq epilogue | wg1 G, dbeta, G1
-    mbar_wait(&mb[MB_Q], ph);
-    fence_after_sync();
-    BSTAMP(12);
-    if (tid == 0 && c > 0) {
-      // dO, H^T, X, U' (last read by M5/M6) and the W slot (M4) are free; V
-      // is free once the dV store (oldest bulk group) has been read out.
-      bulk_wait_read0();
-      issue_loads_main(c - 1, 1 - ks);
-    }
-    if (wg == 0) {
-      // lanes >= 16: dq_hat row r64 (TM_DQ) -> L2 adjoint -> dq staging
-      float dot = 0.f;
-#pragma unroll 1
-      for (int half = 0; half < 2; ++half) {
+      simt_signal(&sg[SG_P7], tid);
+      BSTAMP(13);
+      if (wg == 0 && lo && t0 + r64 < L)
+        dbeta[t0 + r64] = __float2bfloat16_rn(db1[r64] + db1[C + r64] + db2[r64] + db2[C + r64]);
+      {
+        // lanes >= 16: dq_hat row r64 (TM_DQ), this warpgroup's 64 columns;
+        // the row dot q_hat . dq_hat is combined across the warpgroups
         float f[64];
-        ld64(tm, wwarp, TM_R + 64 * half, f);  // lanes>=16 read TM_DQ
+        ld64(tm, wwarp, TM_R + 64 * wg, f);
+        float dot = 0.f;
         if (!lo) {
 #pragma unroll
           for (int g = 0; g < 8; ++g) {
             float q8[8];
-            il_load8(sQ, C, r64, 64 * half + g * 8, q8);
+            il_load8(sQ, C, r64, 64 * wg + g * 8, q8);
 #pragma unroll
             for (int e = 0; e < 8; ++e) dot = fmaf(q8[e], f[g * 8 + e], dot);
           }
+          sdotq[wg * C + r64] = dot;
         }
-      }
-      const float inv = sr[r64];
-      if (!(l2 && nq[r64] >= eps)) dot = 0.f;
-#pragma unroll 1
-      for (int half = 0; half < 2; ++half) {
-        float f[64];
-        ld64(tm, wwarp, TM_R + 64 * half, f);
+        grp_sync<256>(BAR_SIMT);
         if (!lo) {
+          dot = sdotq[r64] + sdotq[C + r64];
+          if (!(l2 && nq[r64] >= eps)) dot = 0.f;
+          const float inv = sr[r64];
 #pragma unroll
           for (int g = 0; g < 8; ++g) {
             float q8[8];
-            il_load8(sQ, C, r64, 64 * half + g * 8, q8);
+            il_load8(sQ, C, r64, 64 * wg + g * 8, q8);
 #pragma unroll
             for (int e = 0; e < 8; ++e)
               q8[e] = l2 ? inv * (f[g * 8 + e] - q8[e] * dot) : f[g * 8 + e];
-            il_store8(sDQo, C, r64, 64 * half + g * 8, q8);
+            il_store8(sDQo, C, r64, 64 * wg + g * 8, q8);
           }
         }
       }
-    } else {
-      // lanes < 16: G row (TM_GB); K K^T row from lanes >= 16 (TM_G + lane 16)
-      float db2 = 0.f;
-      const float bi = sb[r64];
-#pragma unroll 1
-      for (int cc = 0; cc < 4; ++cc) {
-        float g16[16], k16[16], kk[16];
-        ld16f(tm, wwarp, TM_GB + 16 * cc, g16);
-        ld16f(tm, wwarp, TM_G + 16 * cc, k16);
-#pragma unroll
-        for (int e = 0; e < 16; ++e) kk[e] = __shfl_xor_sync(0xffffffffu, k16[e], 16);
+      simt_signal(&sg[SG_DQ], tid);
+
+      // ================= P8: dK epilogue (columns split; row dot combined)
+      mbar_wait(&mb[MB_K], ph);
+      fence_after_sync();
+      BSTAMP(14);
+      {
+        float f[64];
+        ld64(tm, wwarp, TM_DK + 64 * wg, f);  // lanes<16: dk_hat row r64
+        float dot = 0.f;
         if (lo) {
 #pragma unroll
-          for (int g = 0; g < 2; ++g) {
-            float x[8];
+          for (int g = 0; g < 8; ++g) {
+            float k8[8];
+            il_load8(sK, C, r64, 64 * wg + g * 8, k8);
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const int j = 16 * cc + g * 8 + e;
-              const float gv = (j < r64) ? g16[g * 8 + e] : 0.f;
-              db2 = fmaf(gv, kk[g * 8 + e], db2);
-              x[e] = bi * gv;
-            }
-            il_store8(sG1, C, r64, 16 * cc + g * 8, x);
+            for (int e = 0; e < 8; ++e) dot = fmaf(k8[e], f[g * 8 + e], dot);
+          }
+          sdot[wg * C + r64] = dot;
+        }
+        grp_sync<256>(BAR_SIMT);
+        if (lo) {
+          dot = sdot[r64] + sdot[C + r64];
+          if (!(l2 && nk[r64] >= eps)) dot = 0.f;
+          const float inv = ss[r64];
+#pragma unroll
+          for (int g = 0; g < 8; ++g) {
+            float k8[8];
+            il_load8(sK, C, r64, 64 * wg + g * 8, k8);
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              k8[e] = l2 ? inv * (f[g * 8 + e] - k8[e] * dot) : f[g * 8 + e];
+            il_store8(sDKo, C, r64, 64 * wg + g * 8, k8);
           }
         }
       }
-      if (lo && t0 + r64 < L)
-        dbeta[t0 + r64] = __float2bfloat16_rn(db1[r64] + db1[C + r64] + db2);
-    }
-    fence_proxy_async();
-    cta_sync();
-
-    BSTAMP(13);
-    // ================= M7: dK += (G1 + G1^T) K ; prefetch Q of chunk c-1
-    if (tid == 0) {
-      tma_store_4d(&mDQ, sDQo, 0, t0, 0, unit);
-      bulk_commit();
-      const uint32_t id_m = idesc_bf16(64, 128, false, true);
-      const uint32_t id_mt = idesc_bf16(64, 128, true, true);
-#pragma unroll
-      for (int k0 = 0; k0 < C; k0 += 16) {
-        mma_bf16(tm + TM_DK, desc_k(aG1, C, k0), desc_mn(aK, C, k0), id_m, 1);
-        mma_bf16(tm + TM_DK, desc_mn(aG1, C, k0), desc_mn(aK, C, k0), id_mt, 1);
-      }
-      mma_commit(&mb[MB_K]);
-      if (c > 0) issue_load_q(c - 1);  // q_hat consumed by the dq epilogue
+      simt_signal(&sg[SG_P8], tid);
+      BSTAMP(15);
     }
 
-    // ================= P8: dK epilogue (columns split; row dot combined)
-    mbar_wait(&mb[MB_K], ph);
-    fence_after_sync();
-    BSTAMP(14);
-    {
+    // dh0 = dH (orientation [dk][dv]; lane dv = w, columns split)
+    if (a.dh0) {
+      fence_after_sync();
+      float* dh0 = a.dh0 + (size_t)unit * D * D;
       float f[64];
-      ld64(tm, wwarp, TM_DK + 64 * wg, f);  // lanes<16: dk_hat row r64
-      float dot = 0.f;
-      if (lo) {
+      ld64(tm, wwarp, TM_DH + 64 * wg, f);
 #pragma unroll
-        for (int g = 0; g < 8; ++g) {
-          float k8[8];
-          il_load8(sK, C, r64, 64 * wg + g * 8, k8);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) dot = fmaf(k8[e], f[g * 8 + e], dot);
-        }
-        sdot[wg * C + r64] = dot;
-      }
-      __syncthreads();
-      if (lo) {
-        dot = sdot[r64] + sdot[C + r64];
-        if (!(l2 && nk[r64] >= eps)) dot = 0.f;
-        const float inv = ss[r64];
-#pragma unroll
-        for (int g = 0; g < 8; ++g) {
-          float k8[8];
-          il_load8(sK, C, r64, 64 * wg + g * 8, k8);
-#pragma unroll
-          for (int e = 0; e < 8; ++e)
-            k8[e] = l2 ? inv * (f[g * 8 + e] - k8[e] * dot) : f[g * 8 + e];
-          il_store8(sDKo, C, r64, 64 * wg + g * 8, k8);
-        }
-      }
+      for (int e = 0; e < 64; ++e) dh0[(size_t)(64 * wg + e) * D + w] = f[e];
     }
-    fence_proxy_async();
-    cta_sync();
-    if (tid == 0) {
-      tma_store_4d(&mDK, sDKo, 0, t0, 0, unit);
-      bulk_commit();
-    }
-    BSTAMP(15);
   }
-
-  // dh0 = dH (orientation [dk][dv]; lane dv = w, columns split)
-  if (a.dh0) {
-    fence_after_sync();
-    float* dh0 = a.dh0 + (size_t)unit * D * D;
-    float f[64];
-    ld64(tm, wwarp, TM_DH + 64 * wg, f);
-#pragma unroll
-    for (int e = 0; e < 64; ++e) dh0[(size_t)(64 * wg + e) * D + w] = f[e];
-  }
-  if (tid == 0) bulk_wait0();
   cta_sync();
   if (warp == 0) tmem_dealloc<512>(tm);
 }

@@ -17,15 +17,20 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 
 
-@pytest.mark.skipif(os.environ.get("DN_TIMING") != "1", reason="profiling aid; set DN_TIMING=1")
-def test_fwd_timeline():
-    import paper_2406_06484_b200 as dn
+@pytest.fixture(scope="module")
+def timlib():
     out = os.path.join(HERE, "cuda", "libdeltanet_tim.so")
     srcs = sorted(glob.glob(os.path.join(ROOT, "paper_2406_06484_b200", "csrc", "*.cu")))
     subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17",
                     "-DDN_TIMING", "-Xcompiler", "-fPIC", "-shared", "-I",
                     os.path.join(ROOT, "include"), "-o", out, *srcs], check=True)
-    lib = ctypes.CDLL(out)
+    return ctypes.CDLL(out)
+
+
+@pytest.mark.skipif(os.environ.get("DN_TIMING") != "1", reason="profiling aid; set DN_TIMING=1")
+def test_fwd_timeline(timlib):
+    import paper_2406_06484_b200 as dn
+    lib = timlib
     cfg = synth.CONFIGS["target"]
     x = synth.make_inputs(cfg, b_range=range(1))
     td = torch.bfloat16
@@ -62,10 +67,9 @@ def test_fwd_timeline():
 
 
 @pytest.mark.skipif(os.environ.get("DN_TIMING") != "1", reason="profiling aid; set DN_TIMING=1")
-def test_bwd_timeline():
+def test_bwd_timeline(timlib):
     import paper_2406_06484_b200 as dn
-    out = os.path.join(HERE, "cuda", "libdeltanet_tim.so")
-    lib = ctypes.CDLL(out)
+    lib = timlib
     cfg = synth.CONFIGS["target"]
     x = synth.make_inputs(cfg, b_range=range(1))
     td = torch.bfloat16
@@ -94,11 +98,19 @@ def test_bwd_timeline():
     names = {0: "start", 1: "tma wait", 2: "norms+scale", 3: "G wait", 4: "P2 A",
              5: "P3 U' conv + R wait", 6: "P3 R conv + dU wait", 7: "P3 dU' conv",
              8: "P wait", 9: "P5 P, dV, dX", 10: "A wait", 11: "P6 dA, Y", 12: "Q wait",
-             13: "P7 dq | G, G1", 14: "K wait", 15: "P8 dk"}
+             13: "P7 G1, dbeta", 14: "dq epi + K wait", 15: "P8 dk"}
     rows = []
     seq = list(range(16))
     for a_, b_ in zip(seq[:-1], seq[1:]):
         dt = (t[2:-2, b_] - t[2:-2, a_])
         rows.append(f"{names[b_]:28s} {dt.mean():9.0f} cycles")
     rows.append(f"{'-- per chunk':28s} {np.diff(t[2:-2, 0]).mean():9.0f} cycles")
+    # issuer stamps (slots 16-29), relative to the SIMT chunk start (slot 0)
+    inames = {16: "I norm rcv", 17: "I M1 issued", 18: "I A rcv", 19: "I M2 issued",
+              20: "I P3 rcv", 21: "I M3/M4 issued", 22: "I P5 rcv", 23: "I M5 issued",
+              24: "I P6 rcv", 25: "I M6 issued", 26: "I P7 rcv", 27: "I M7 issued",
+              28: "I dq rcv", 29: "I P8 rcv"}
+    for s_ in range(16, 30):
+        dt = t[2:-2, s_] - t[2:-2, 0]
+        rows.append(f"{inames[s_]:28s} {dt.mean():9.0f} cycles after chunk start")
     print("\n" + "\n".join(rows))

@@ -8,27 +8,31 @@
 // (H_t, X, W^T, Z^T = (diag(s) U')^T; tc_common.cuh REC_*) is read back, so
 // the UT substitution and the W / U / U' products are not recomputed.
 //
-// Per chunk (q_hat, k_hat: L2-normalised rows, rounded to bf16 in smem):
-//   recompute  A = tril(Q K^T), R = V - K H, U' = diag(max(|k|,eps)) Z
-//   chain      dU' = K dH + A^T dO
-//              dH <- dH + Q^T dO - W^T dU'
+// Per chunk (q_hat = diag(r) q, k_hat = diag(s) k: L2-normalised rows):
+//   recompute  A = tril(Q_hat K_hat^T), R = V - K_hat H, U' = diag(1/s) Z
+//   chain      dU' = K_hat dH + A^T dO
+//              dH <- dH + Q_hat^T dO - W^T dU'
 //   local      dA = tril(dO U'^T)          P = X^T dU'  (= dV_beta)
 //              dX = (dU' R^T) diag(b)      Y = X^T dX,  G = tril(-Y X^T, -1)
-//              dQ = dO H^T + dA K
-//              dK = U' dH^T + dA^T Q - dV H^T + (G1 + G1^T) K,  G1 = diag(b) G
+//              dQ = dO H^T + dA K_hat
+//              dK = U' dH^T + dA^T Q_hat - dV H^T + (G1 + G1^T) K_hat,  G1 = diag(b) G
 //              dV = diag(b) P
-//              dbeta = rowsum(P . R) + rowsum(G . K K^T)
+//              dbeta = rowsum(P . R) + rowsum(G . K_hat K_hat^T)
 //   then the L2-normalisation adjoint on dQ, dK (R9).
 // (dK_beta = X^T dW = -P H^T, and rowsum(dK_beta . K) + rowsum(P . V) =
 //  rowsum(P . R) -- DESIGN.md §4.2.)
 //
+// The first products of a chunk (K K^T, Q K^T, dH^T K^T, K H) run on the RAW
+// bf16 q / k tiles as they land, so they overlap the previous chunk's
+// epilogues; the row scales enter exactly in the conversions:
+//   A_m = tril(diag(r) Q K^T)  (M2 operand; A = A_m diag(s)),
+//   dU'^T = (dH^T K^T + dO^T A_m) diag(s),  R = V - diag(s) (K H),
+//   K_hat K_hat^T = diag(s) K K^T diag(s).
+// q and k are normalised in place afterwards for the remaining products.
+//
 // 288 threads: warps 0-7 run the SIMT phases (split by columns between the
 // two warpgroups, both see all 128 TMEM lanes); warp 8 issues every MMA, TMA
-// load and store, driven by mbarrier hand-offs, so MMAs queue up behind each
-// other while the SIMT warps convert the previous results.  The next chunk's
-// Q, K, dO, V, H_t, X and Z^T are prefetched by TMA during the tail of the
-// current chunk; W^T is loaded into the other K slot at the start of the
-// chunk (needed only at the dH update).
+// load and store, driven by mbarrier hand-offs.
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
@@ -42,10 +46,11 @@ using namespace tc;
 constexpr int C = 64, D = 128, NT = 288;  // warps 0-7 SIMT, warp 8 issuer
 constexpr uint32_t LO16 = 16u << 16;  // TMEM lane offset 16 (second M=64 accumulator)
 constexpr int TILE = C * D * 2;       // 16 KB
+constexpr int HALF_ROWS = 64 * 16;    // byte offset of row 64 in an IL R=128 tile
 
 // ---- shared memory map (bytes); regions reused by lifetime
-constexpr int OFF_Q = 0;                    // q_hat  IL R=64 x 128
-constexpr int OFF_KW = OFF_Q + TILE;        // 2 slots: k_hat | W^T (IL R=128 x 64)
+constexpr int OFF_Q = 0;                    // q (raw, then q_hat in place)
+constexpr int OFF_KW = OFF_Q + TILE;        // 2 slots: k (raw, then k_hat) | W^T (IL R=128 x 64)
 constexpr int OFF_DO = OFF_KW + 2 * TILE;   // dO     IL R=64 x 128
 constexpr int OFF_V = OFF_DO + TILE;        // V -> dV staging
 constexpr int OFF_H = OFF_V + TILE;         // H^T    IL R=128 x 128
@@ -54,25 +59,26 @@ constexpr int OFF_X = OFF_DH + D * D * 2;   // X      IL R=64 x 64 (record)
 constexpr int OFF_Z = OFF_X + C * C * 2;    // Z^T (record) -> U'^T in place
 constexpr int OFF_R = OFF_Z + TILE;         // R -> Y [0,8K) + G1 [8K,16K) -> dk staging
 constexpr int OFF_DUP = OFF_R + TILE;       // dU'^T -> dq staging
-constexpr int OFF_A = OFF_DUP + TILE;       // A -> dX -> dA
-constexpr int OFF_VEC = OFF_A + C * C * 2;  // beta, r, s, nq, nk, db1[2], db2[2], dot[2], dotq[2]
-constexpr int SMEM_BYTES = OFF_VEC + 13 * C * 4;
+constexpr int OFF_A = OFF_DUP + TILE;       // A_m -> dX -> dA
+constexpr int OFF_VEC = OFF_A + C * C * 2;  // beta, r, s, nq, nk, db1[2], db2[2], dot[2], dotq[2], n2[2][2]
+constexpr int SMEM_BYTES = OFF_VEC + 17 * C * 4;
 static_assert(SMEM_BYTES <= 232448 - 1024, "shared memory budget");
 
 // ---- TMEM column map (512 columns)
 constexpr uint32_t TM_DH = 0;                            // dH^T, M=128
-constexpr uint32_t TM_G = 128;                           // G_qk | G_kk (lane+16)
-constexpr uint32_t TM_R = 192, TM_P = 192 | LO16;        // K H | P     (M=64, 128 cols)
-constexpr uint32_t TM_DK = 192, TM_DQ = 192 | LO16;      // dK | dQ     (after P5)
+constexpr uint32_t TM_G = 128;                           // Q K^T | K K^T (lane+16), raw
+constexpr uint32_t TM_DK = 192, TM_DQ = 192 | LO16;      // dK | dQ  (M=64, 128 cols)
 constexpr uint32_t TM_DU = 320;                          // dU'^T, M=128 (M1-P3)
 constexpr uint32_t TM_DX = 320, TM_GB = 320;             // dX' (M3-P5), G (M6-P7)
+constexpr uint32_t TM_P = 384;                           // P[:, :64] | P[:, 64:] (M3-P5)
 constexpr uint32_t TM_DA = 384, TM_Y = 384 | LO16;       // dA | Y (M5-P6)
+constexpr uint32_t TM_KH = 448;                          // (K H)[:, :64] | [:, 64:], raw K
 
 enum { BAR_SIMT = 1 };
-// MMA commit / load barriers (issuer -> SIMT) ...
-enum { MB_G, MB_R, MB_DU, MB_WL, MB_P, MB_A, MB_Q, MB_K, MB_N };
-// ... and hand-offs SIMT -> issuer (SG_STG: issuer -> SIMT, staging free)
-enum { SG_NORM, SG_A, SG_P3, SG_P5, SG_P6, SG_P7, SG_DQ, SG_P8, SG_STG, SG_N };
+// issuer -> SIMT: MMA commits and TMA arrivals
+enum { MB_G, MB_R, MB_DU, MB_WL, MB_P, MB_DH, MB_A, MB_Q, MB_K, MB_MAIN, MB_QL, MB_N };
+// SIMT -> issuer hand-offs (SG_STG: issuer -> SIMT, staging regions free)
+enum { SG_DHI, SG_A, SG_P3, SG_P5, SG_P6, SG_P7, SG_DQ, SG_P8, SG_STG, SG_N };
 
 __device__ __forceinline__ void ld32(uint32_t tm, int wwarp, uint32_t col, float (&f)[32]) {
   uint32_t r[2][16];
@@ -127,7 +133,7 @@ __global__ void __launch_bounds__(NT, 1)
                   const __grid_constant__ CUtensorMap mDQ, const __grid_constant__ CUtensorMap mDK,
                   const __grid_constant__ CUtensorMap mDV, Args a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bar_tma, mb[MB_N], sg[SG_N];
+  __shared__ uint64_t mb[MB_N], sg[SG_N];
   __shared__ uint32_t tslot;
   uint8_t *sQ = smem + OFF_Q, *sDO = smem + OFF_DO, *sV = smem + OFF_V, *sH = smem + OFF_H,
           *sDH = smem + OFF_DH, *sX = smem + OFF_X, *sZ = smem + OFF_Z, *sR = smem + OFF_R,
@@ -141,14 +147,15 @@ __global__ void __launch_bounds__(NT, 1)
   uint8_t* sDQo = sDUP;            // dq staging after M6
   uint8_t* sDKo = sR;              // dk staging after M7
   float* sb = reinterpret_cast<float*>(smem + OFF_VEC);  // beta
-  float* sr = sb + C;         // 1/max(||q||,eps) (0: padded)
-  float* ss = sr + C;         // 1/max(||k||,eps)
-  float* nq = ss + C;         // ||q||
-  float* nk = nq + C;         // ||k||
-  float* db1 = nk + C;        // [2][64] rowsum(P . R) partials
-  float* db2 = db1 + 2 * C;   // [2][64] rowsum(G . K K^T) partials
-  float* sdot = db2 + 2 * C;  // [2][64] dk-adjoint dot partials
-  float* sdotq = sdot + 2 * C;// [2][64] dq-adjoint dot partials
+  float* sr = sb + C;          // 1/max(||q||,eps) (0: padded)
+  float* ss = sr + C;          // 1/max(||k||,eps)
+  float* nq = ss + C;          // ||q||
+  float* nk = nq + C;          // ||k||
+  float* db1 = nk + C;         // [2][64] rowsum(P . R) partials
+  float* db2 = db1 + 2 * C;    // [2][64] rowsum(G . K K^T) partials
+  float* sdot = db2 + 2 * C;   // [2][64] dk-adjoint dot partials
+  float* sdotq = sdot + 2 * C; // [2][64] dq-adjoint dot partials
+  float* n2 = sdotq + 2 * C;   // [2 (q,k)][2 (half)][64] squared-norm partials
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wg = (tid >> 7) & 1, w = tid & 127, wwarp = w >> 5;
@@ -165,7 +172,6 @@ __global__ void __launch_bounds__(NT, 1)
 
   if (warp == 0) tmem_alloc<512>(&tslot);
   if (tid == 0) {
-    mbar_init(&bar_tma, 2);
     for (int i = 0; i < MB_N; ++i) mbar_init(&mb[i], 1);
     for (int i = 0; i < SG_N; ++i) mbar_init(&sg[i], 1);
     mbar_fence_init();
@@ -183,8 +189,9 @@ __global__ void __launch_bounds__(NT, 1)
   if (warp == NT / 32 - 1) {
     // =====================================================================
     // Issuer warp (lane 0): every tcgen05.mma, TMA load and store.  It only
-    // waits on hand-off barriers, so the SIMT warps never stall behind a
-    // full MMA queue.
+    // waits on hand-off barriers; the SIMT warps never stall behind a full
+    // MMA queue.  Software-pipelined: chunk c-1's first products are issued
+    // as soon as its tiles land, under chunk c's epilogues.
     // =====================================================================
     if (lane == 0) {
       const uint32_t aQ = smem_u32(sQ), aDO = smem_u32(sDO), aH = smem_u32(sH),
@@ -192,67 +199,92 @@ __global__ void __launch_bounds__(NT, 1)
                      aDUP = smem_u32(sDUP), aR = smem_u32(sR), aDA = smem_u32(sDA),
                      aDX = smem_u32(sDX), aY = smem_u32(sY), aG1 = smem_u32(sG1),
                      aDV = smem_u32(sDV), aUP = smem_u32(sUP);
-      // Two arrivals per chunk on bar_tma: (K, dO, V, H, X, Z) once their
-      // regions are free, and Q once the dq epilogue has read q_hat.
-      auto issue_loads_main = [&](int c, int ks) {
-        mbar_expect_tx(&bar_tma, 3 * TILE + D * D * 2 + C * C * 2 + D * C * 2);
-        tma_load_4d(smem + OFF_KW + ks * TILE, &mK, 0, c * C, 0, unit, &bar_tma);
-        tma_load_4d(sDO, &mDO, 0, c * C, 0, unit, &bar_tma);
-        tma_load_4d(sV, &mV, 0, c * C, 0, unit, &bar_tma);
-        bulk_load(sH, states + (size_t)c * D * D * 2, D * D * 2, &bar_tma);
-        bulk_load(sX, recs + (size_t)c * REC_BYTES + REC_X, C * C * 2, &bar_tma);
-        bulk_load(sZ, recs + (size_t)c * REC_BYTES + REC_Z, D * C * 2, &bar_tma);
+      auto issue_loads_main = [&](int c, int ks) {  // K, dO, V, H_t, X, Z^T
+        mbar_expect_tx(&mb[MB_MAIN], 3 * TILE + D * D * 2 + C * C * 2 + D * C * 2);
+        tma_load_4d(smem + OFF_KW + ks * TILE, &mK, 0, c * C, 0, unit, &mb[MB_MAIN]);
+        tma_load_4d(sDO, &mDO, 0, c * C, 0, unit, &mb[MB_MAIN]);
+        tma_load_4d(sV, &mV, 0, c * C, 0, unit, &mb[MB_MAIN]);
+        bulk_load(sH, states + (size_t)c * D * D * 2, D * D * 2, &mb[MB_MAIN]);
+        bulk_load(sX, recs + (size_t)c * REC_BYTES + REC_X, C * C * 2, &mb[MB_MAIN]);
+        bulk_load(sZ, recs + (size_t)c * REC_BYTES + REC_Z, D * C * 2, &mb[MB_MAIN]);
       };
       auto issue_load_q = [&](int c) {
-        mbar_expect_tx(&bar_tma, TILE);
-        tma_load_4d(sQ, &mQ, 0, c * C, 0, unit, &bar_tma);
+        mbar_expect_tx(&mb[MB_QL], TILE);
+        tma_load_4d(sQ, &mQ, 0, c * C, 0, unit, &mb[MB_QL]);
+      };
+      auto issue_load_w = [&](int c, int ks) {  // W^T of chunk c into the slot not holding K
+        mbar_expect_tx(&mb[MB_WL], D * C * 2);
+        bulk_load(smem + OFF_KW + (1 - ks) * TILE, recs + (size_t)c * REC_BYTES + REC_W, D * C * 2,
+                  &mb[MB_WL]);
       };
       if (NC > 0) {
         issue_loads_main(NC - 1, 0);
         issue_load_q(NC - 1);
+        issue_load_w(NC - 1, 0);
       }
 #pragma unroll 1
       for (int it = 0; it < NC; ++it) {
         const int c = NC - 1 - it, t0 = c * C, ks = it & 1;
-        const uint32_t ph = it & 1;
+        const uint32_t ph = it & 1, php = (it - 1) & 1;
         const uint32_t aK = smem_u32(smem + OFF_KW + ks * TILE);
-        uint8_t* sW = smem + OFF_KW + (1 - ks) * TILE;
-        const uint32_t aW = smem_u32(sW);
-        // I0: W^T of this chunk into the free K slot (K of chunk c+1 retired
-        // with the previous chunk's dk epilogue)
-        mbar_expect_tx(&mb[MB_WL], D * C * 2);
-        bulk_load(sW, recs + (size_t)c * REC_BYTES + REC_W, D * C * 2, &mb[MB_WL]);
+        const uint32_t aW = smem_u32(smem + OFF_KW + (1 - ks) * TILE);
 
-        // M1: Gram | dH^T K^T, K H
-        mbar_wait(&sg[SG_NORM], ph);
+        // M1a (raw k): K K^T | dH^T K^T | K H.  TMEM G / GB / KH were released
+        // by the previous chunk's P7 / P5 (waited below in program order).
+        mbar_wait(&mb[MB_MAIN], ph);
+        mbar_wait(&sg[SG_DHI], ph);
         fence_after_sync();
         ISTAMP(16);
         {
           const uint32_t idg = idesc_bf16(64, 64, false, false);
-          const uint32_t idr = idesc_bf16(64, 128, false, false);
           const uint32_t idd = idesc_bf16(128, 64, false, false);
 #pragma unroll
-          for (int k0 = 0; k0 < D; k0 += 16) {
-            mma_bf16(tm + TM_G, desc_k(aQ, C, k0), desc_k(aK, C, k0), idg, k0 > 0);
+          for (int k0 = 0; k0 < D; k0 += 16)
             mma_bf16(tm + TM_G + LO16, desc_k(aK, C, k0), desc_k(aK, C, k0), idg, k0 > 0);
-          }
-          mma_commit(&mb[MB_G]);
 #pragma unroll
           for (int k0 = 0; k0 < D; k0 += 16)
             mma_bf16(tm + TM_DU, desc_k(aDH, D, k0), desc_k(aK, C, k0), idd, k0 > 0);
 #pragma unroll
-          for (int k0 = 0; k0 < D; k0 += 16)
-            mma_bf16(tm + TM_R, desc_k(aK, C, k0), desc_k(aH, D, k0), idr, k0 > 0);
+          for (int k0 = 0; k0 < D; k0 += 16) {
+            mma_bf16(tm + TM_KH, desc_k(aK, C, k0), desc_k(aH, D, k0), idg, k0 > 0);
+            mma_bf16(tm + TM_KH + LO16, desc_k(aK, C, k0), desc_k(aH + HALF_ROWS, D, k0), idg,
+                     k0 > 0);
+          }
           mma_commit(&mb[MB_R]);
         }
         ISTAMP(17);
-        bulk_wait_read0();  // dq / dk stores of chunk c+1 read out of the DUP / R regions
+        if (it > 0) {
+          // previous chunk's tail: dq store + Q of this chunk ...
+          mbar_wait(&sg[SG_DQ], php);
+          tma_store_4d(&mDQ, sDQo, 0, t0 + C, 0, unit);
+          bulk_commit();
+          issue_load_q(c);
+          // ... dk store + W^T of this chunk into the retired K slot
+          mbar_wait(&sg[SG_P8], php);
+          tma_store_4d(&mDK, sDKo, 0, t0 + C, 0, unit);
+          bulk_commit();
+          issue_load_w(c, ks);
+        }
+        ISTAMP(18);
+        bulk_wait_read0();  // dq / dk staging (DUP / R regions) read out
         mbar_arrive(&sg[SG_STG]);
 
-        // M2: dU'^T += dO^T A
+        // M1b: Q K^T (raw)
+        mbar_wait(&mb[MB_QL], ph);
+        fence_after_sync();
+        {
+          const uint32_t idg = idesc_bf16(64, 64, false, false);
+#pragma unroll
+          for (int k0 = 0; k0 < D; k0 += 16)
+            mma_bf16(tm + TM_G, desc_k(aQ, C, k0), desc_k(aK, C, k0), idg, k0 > 0);
+          mma_commit(&mb[MB_G]);
+        }
+        ISTAMP(19);
+
+        // M2: dU'^T += dO^T A_m
         mbar_wait(&sg[SG_A], ph);
         fence_after_sync();
-        ISTAMP(18);
+        ISTAMP(20);
         {
           const uint32_t ida = idesc_bf16(128, 64, true, true);
 #pragma unroll
@@ -260,45 +292,51 @@ __global__ void __launch_bounds__(NT, 1)
             mma_bf16(tm + TM_DU, desc_mn(aDO, C, k0), desc_mn(aA, C, k0), ida, 1);
           mma_commit(&mb[MB_DU]);
         }
-        ISTAMP(19);
 
-        // M3: P = X^T dU', dX' = dU' R^T ; M4: dH += Q^T dO - W^T dU'
+        // M3: P = X^T dU' (two N=64 halves), dX' = dU' R^T
+        // M4: dH += Q_hat^T dO - W^T dU' ; dK = U' dH^T (dH image of chunk c+1)
         mbar_wait(&sg[SG_P3], ph);
         fence_after_sync();
-        ISTAMP(20);
+        ISTAMP(21);
         {
-          const uint32_t idp = idesc_bf16(64, 128, true, false);
-          const uint32_t idx = idesc_bf16(64, 64, true, false);
+          const uint32_t idp = idesc_bf16(64, 64, true, false);
 #pragma unroll
-          for (int k0 = 0; k0 < C; k0 += 16)
+          for (int k0 = 0; k0 < C; k0 += 16) {
             mma_bf16(tm + TM_P, desc_mn(aX, C, k0), desc_k(aDUP, D, k0), idp, k0 > 0);
+            mma_bf16(tm + TM_P + LO16, desc_mn(aX, C, k0), desc_k(aDUP + HALF_ROWS, D, k0), idp,
+                     k0 > 0);
+          }
 #pragma unroll
           for (int k0 = 0; k0 < D; k0 += 16)
-            mma_bf16(tm + TM_DX, desc_mn(aDUP, D, k0), desc_k(aR, C, k0), idx, k0 > 0);
+            mma_bf16(tm + TM_DX, desc_mn(aDUP, D, k0), desc_k(aR, C, k0), idp, k0 > 0);
           mma_commit(&mb[MB_P]);
           const uint32_t id1 = idesc_bf16(128, 128, true, true);
           const uint32_t id2 = idesc_bf16(128, 128, false, false, true);
+          const uint32_t id_k1 = idesc_bf16(64, 128, true, true);
 #pragma unroll
           for (int k0 = 0; k0 < C; k0 += 16)
             mma_bf16(tm + TM_DH, desc_mn(aDO, C, k0), desc_mn(aQ, C, k0), id1, 1);
+#pragma unroll
+          for (int k0 = 0; k0 < D; k0 += 16)
+            mma_bf16(tm + TM_DK, desc_mn(aUP, D, k0), desc_mn(aDH, D, k0), id_k1, k0 > 0);
           mbar_wait(&mb[MB_WL], ph);
 #pragma unroll
           for (int k0 = 0; k0 < C; k0 += 16)
             mma_bf16(tm + TM_DH, desc_k(aDUP, D, k0), desc_k(aW, D, k0), id2, 1);
+          mma_commit(&mb[MB_DH]);
         }
-        ISTAMP(21);
+        ISTAMP(22);
 
-        // dV store; M5: dA, Y | dQ = dO H^T, dK = U' dH^T - dV H^T
+        // dV store; M5: dA, Y | dQ = dO H^T, dK -= dV H^T
         mbar_wait(&sg[SG_P5], ph);
         fence_after_sync();
-        ISTAMP(22);
+        ISTAMP(23);
         tma_store_4d(&mDV, sDV, 0, t0, 0, unit);
         bulk_commit();
         {
           const uint32_t id_da = idesc_bf16(64, 64, false, true);
           const uint32_t id_y = idesc_bf16(64, 64, true, true);
           const uint32_t id_q = idesc_bf16(64, 128, false, true);
-          const uint32_t id_k1 = idesc_bf16(64, 128, true, true);
           const uint32_t id_k2 = idesc_bf16(64, 128, false, true, true);
 #pragma unroll
           for (int k0 = 0; k0 < D; k0 += 16)
@@ -310,16 +348,15 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
           for (int k0 = 0; k0 < D; k0 += 16) {
             mma_bf16(tm + TM_DQ, desc_k(aDO, C, k0), desc_mn(aH, D, k0), id_q, k0 > 0);
-            mma_bf16(tm + TM_DK, desc_mn(aUP, D, k0), desc_mn(aDH, D, k0), id_k1, k0 > 0);
             mma_bf16(tm + TM_DK, desc_k(aDV, C, k0), desc_mn(aH, D, k0), id_k2, 1);
           }
         }
-        ISTAMP(23);
+        ISTAMP(24);
 
-        // M6: G = -Y X^T ; dQ += dA K ; dK += dA^T Q
+        // M6: G = -Y X^T ; dQ += dA K_hat ; dK += dA^T Q_hat
         mbar_wait(&sg[SG_P6], ph);
         fence_after_sync();
-        ISTAMP(24);
+        ISTAMP(25);
         {
           const uint32_t id_q = idesc_bf16(64, 128, false, true);
           const uint32_t id_k = idesc_bf16(64, 128, true, true);
@@ -334,20 +371,20 @@ __global__ void __launch_bounds__(NT, 1)
           }
           mma_commit(&mb[MB_Q]);
         }
-        ISTAMP(25);
 
-        // prefetch chunk c-1: dO, H^T, X, U' (last read by M5/M6) and the W
-        // slot (M4) are free after M6; V once the dV store has been read out
+        // prefetch chunk c-1 (K into the W slot): dO, H^T, X, U' and W^T are
+        // free after M6; V once the dV store has been read out
         if (c > 0) {
           mbar_wait(&mb[MB_Q], ph);
           bulk_wait_read0();
           issue_loads_main(c - 1, 1 - ks);
         }
+        ISTAMP(26);
 
-        // M7: dK += (G1 + G1^T) K
+        // M7: dK += (G1 + G1^T) K_hat
         mbar_wait(&sg[SG_P7], ph);
         fence_after_sync();
-        ISTAMP(26);
+        ISTAMP(27);
         {
           const uint32_t id_m = idesc_bf16(64, 128, false, true);
           const uint32_t id_mt = idesc_bf16(64, 128, true, true);
@@ -358,19 +395,14 @@ __global__ void __launch_bounds__(NT, 1)
           }
           mma_commit(&mb[MB_K]);
         }
-        ISTAMP(27);
-
-        // dq store, then Q of chunk c-1 (q_hat read by the dq epilogue)
-        mbar_wait(&sg[SG_DQ], ph);
-        ISTAMP(28);
-        tma_store_4d(&mDQ, sDQo, 0, t0, 0, unit);
+      }
+      if (NC > 0) {  // tail of chunk 0
+        const int it = NC - 1;
+        mbar_wait(&sg[SG_DQ], it & 1);
+        tma_store_4d(&mDQ, sDQo, 0, 0, 0, unit);
         bulk_commit();
-        if (c > 0) issue_load_q(c - 1);
-
-        // dk store
-        mbar_wait(&sg[SG_P8], ph);
-        ISTAMP(29);
-        tma_store_4d(&mDK, sDKo, 0, t0, 0, unit);
+        mbar_wait(&sg[SG_P8], it & 1);
+        tma_store_4d(&mDK, sDKo, 0, 0, 0, unit);
         bulk_commit();
       }
       bulk_wait0();
@@ -380,20 +412,25 @@ __global__ void __launch_bounds__(NT, 1)
     // =====================================================================
     // SIMT warps 0-7 (two warpgroups; phases split columns between them)
     // =====================================================================
-    // dH^T <- dhT^T (lane dv = w; columns split by warpgroup)
     {
+      // dH^T <- dhT^T in TMEM (lane dv = w; columns split by warpgroup) and
+      // its bf16 image for the first chunk
       const float* dhT = a.dhT ? a.dhT + (size_t)unit * D * D : nullptr;
 #pragma unroll 1
       for (int c0 = 64 * wg; c0 < 64 * wg + 64; c0 += 16) {
         uint32_t r[16];
+        float f[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(dhT ? dhT[(size_t)(c0 + j) * D + w] : 0.f);
+        for (int j = 0; j < 16; ++j) {
+          f[j] = dhT ? dhT[(size_t)(c0 + j) * D + w] : 0.f;
+          r[j] = __float_as_uint(f[j]);
+        }
         tmem_st16(taddr(tm, wwarp * 32, TM_DH + c0), r);
+        il_store8(sDH, D, w, c0, f);
+        il_store8(sDH, D, w, c0 + 8, f + 8);
       }
       tmem_st_wait();
-      fence_before_sync();
-      grp_sync<256>(BAR_SIMT);
-      fence_after_sync();
+      simt_signal(&sg[SG_DHI], tid);
     }
 
 #pragma unroll 1
@@ -402,80 +439,68 @@ __global__ void __launch_bounds__(NT, 1)
       const uint32_t ph = it & 1;
       uint8_t* sK = smem + OFF_KW + ks * TILE;
 
-      // ================= P1: dH image, row norms, in-place normalisation
+      // ================= P1: row norms from the raw tiles
       BSTAMP(0);
       if (tid < C) sb[tid] = (t0 + tid < L) ? __bfloat162float(beta[t0 + tid]) : 0.f;
-      if (wg == 1) {  // dH^T (dl/dH_{c+1}; complete: MB_K of chunk c+1 waited) -> bf16
-        fence_after_sync();
-#pragma unroll 1
-        for (int half = 0; half < 2; ++half) {
-          float f[64];
-          ld64(tm, wwarp, TM_DH + 64 * half, f);
+      {
+        // wg0: q rows, wg1: k rows; thread w: row w & 63, column half w >> 6
+        const int row = w & 63, hf = w >> 6;
+        mbar_wait(&mb[wg == 0 ? MB_QL : MB_MAIN], ph);
+        const uint8_t* tile = wg == 0 ? sQ : sK;
+        float acc0 = 0.f, acc1 = 0.f;
 #pragma unroll
-          for (int g = 0; g < 8; ++g) il_store8(sDH, D, w, 64 * half + g * 8, f + g * 8);
+        for (int g = 8 * hf; g < 8 * hf + 8; ++g) {
+          float x[8];
+          il_load8(tile, C, row, g * 8, x);
+#pragma unroll
+          for (int e = 0; e < 8; e += 2) {
+            acc0 = fmaf(x[e], x[e], acc0);
+            acc1 = fmaf(x[e + 1], x[e + 1], acc1);
+          }
         }
+        n2[(wg * 2 + hf) * C + row] = acc0 + acc1;
+        mbar_wait(&mb[MB_MAIN], ph);  // every SIMT thread observes both arrivals
+        mbar_wait(&mb[MB_QL], ph);
+        grp_sync<256>(BAR_SIMT);
+        if (w < 64) {
+          const float n = sqrtf(n2[(wg * 2) * C + row] + n2[(wg * 2 + 1) * C + row]);
+          float inv = l2 ? 1.f / fmaxf(n, eps) : 1.f;
+          if (t0 + row >= L) inv = 0.f;
+          (wg == 0 ? sr : ss)[row] = inv;
+          (wg == 0 ? nq : nk)[row] = n;
+        }
+        grp_sync<256>(BAR_SIMT);
       }
-      mbar_wait(&bar_tma, ph);
       BSTAMP(1);
-      if (wg == 0) {  // w < 64: q row w; w >= 64: k row w-64
-        const int row = w & 63;
-        const uint8_t* tile = w < 64 ? sQ : sK;
-        float acc = 0.f;
-#pragma unroll
-        for (int g = 0; g < D / 8; ++g) {
-          float x[8];
-          il_load8(tile, C, row, g * 8, x);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) acc = fmaf(x[e], x[e], acc);
-        }
-        const float n = sqrtf(acc);
-        float inv = l2 ? 1.f / fmaxf(n, eps) : 1.f;
-        if (t0 + row >= L) inv = 0.f;
-        (w < 64 ? sr : ss)[row] = inv;
-        (w < 64 ? nq : nk)[row] = n;
-      }
-      grp_sync<256>(BAR_SIMT);
-      if (l2) {  // normalise rows in place (row = w, columns split by warpgroup)
-        const int row = w & 63;
-        uint8_t* tile = w < 64 ? sQ : sK;
-        const float inv = (w < 64 ? sr : ss)[row];
-#pragma unroll
-        for (int g = 8 * wg; g < 8 * wg + 8; ++g) {
-          float x[8];
-          il_load8(tile, C, row, g * 8, x);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) x[e] *= inv;
-          il_store8(tile, C, row, g * 8, x);
-        }
-      }
-      simt_signal(&sg[SG_NORM], tid);
-      BSTAMP(2);
 
-      // ================= P2: A = tril(Q K^T) -> bf16 (lanes < 16: G_qk rows)
+      // ================= P2: A_m = tril(diag(r) Q K^T) -> bf16 (lanes < 16)
       mbar_wait(&mb[MB_G], ph);
       fence_after_sync();
-      BSTAMP(3);
+      BSTAMP(2);
       {
         float f[32];
         ld32(tm, wwarp, TM_G + 32 * wg, f);
         if (lo) {
+          const float ri = sr[r64];
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
             float x[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
               const int j = 32 * wg + g * 8 + e;
-              x[e] = (j <= r64) ? f[g * 8 + e] : 0.f;
+              x[e] = (j <= r64) ? ri * f[g * 8 + e] : 0.f;
             }
             il_store8(sA, C, r64, 32 * wg + g * 8, x);
           }
         }
       }
       simt_signal(&sg[SG_A], tid);
-      BSTAMP(4);
+      BSTAMP(3);
 
-      // ================= P3: U' = diag(max(|k|,eps)) Z ; R = V - K H ; dU' -> bf16
-      if (l2) {  // U'^T[dv][t] = Z^T[dv][t] * max(|k_t|, eps)  (row dv = w)
+      // ================= P3: U' = diag(max(|k|,eps)) Z ; q_hat in place ;
+      //                       R = V - diag(s) K H ; dU' = (..) diag(s) -> bf16
+      if (l2) {
+        // U'^T[dv][t] = Z^T[dv][t] * max(|k_t|, eps)  (row dv = w)
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           const int col = 32 * wg + g * 8;
@@ -485,70 +510,76 @@ __global__ void __launch_bounds__(NT, 1)
           for (int e = 0; e < 8; ++e) z8[e] *= fmaxf(nk[col + e], eps);
           il_store8(sUP, D, w, col, z8);
         }
+        // q_hat = diag(r) q in place (M1 done reading raw q: MB_G waited)
+        const int row = w & 63;
+        const float inv = sr[row];
+#pragma unroll
+        for (int g = 8 * wg + 4 * (w >> 6); g < 8 * wg + 4 * (w >> 6) + 4; ++g) {
+          float x[8];
+          il_load8(sQ, C, row, g * 8, x);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) x[e] *= inv;
+          il_store8(sQ, C, row, g * 8, x);
+        }
       }
       mbar_wait(&sg[SG_STG], ph);  // R / DUP regions free (previous dq/dk stores read out)
       mbar_wait(&mb[MB_R], ph);
       fence_after_sync();
-      BSTAMP(5);
-      // R = V - K H, row r64, this warpgroup's 64 columns; lanes < 16 hold the
-      // accumulator row, each lane pair splits every 16 columns 8 / 8
-#pragma unroll 1
-      for (int cc = 0; cc < 4; ++cc) {
-        const int col = 64 * wg + 16 * cc;
-        float f[16], x[8];
-        ld16f(tm, wwarp, TM_R + col, f);
+      BSTAMP(4);
+      {
+        // (K H) row r64: lanes < 16 hold columns [0,64), lanes >= 16 [64,128);
+        // this warpgroup takes 32 of each half
+        float f[32];
+        ld32(tm, wwarp, TM_KH + 32 * wg, f);
+        const float si = ss[r64];
+        const int c0 = (lo ? 0 : 64) + 32 * wg;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) x[e] = __shfl_xor_sync(0xffffffffu, f[8 + e], 16);
-        if (lo) {
+        for (int g = 0; g < 4; ++g) {
+          float v8[8];
+          il_load8(sV, C, r64, c0 + g * 8, v8);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) x[e] = f[e];
+          for (int e = 0; e < 8; ++e) v8[e] = fmaf(-si, f[g * 8 + e], v8[e]);
+          il_store8(sR, C, r64, c0 + g * 8, v8);
         }
-        const int c8 = col + (lo ? 0 : 8);
-        float v8[8];
-        il_load8(sV, C, r64, c8, v8);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) v8[e] -= x[e];
-        il_store8(sR, C, r64, c8, v8);
       }
       mbar_wait(&mb[MB_DU], ph);
       fence_after_sync();
-      BSTAMP(6);
-      {  // dU'^T (lane d_v = w) -> bf16
+      BSTAMP(5);
+      {  // dU'^T (lane d_v = w) * s_j -> bf16
         float f[32];
         ld32(tm, wwarp, TM_DU + 32 * wg, f);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) f[e] *= ss[32 * wg + e];
 #pragma unroll
         for (int g = 0; g < 4; ++g) il_store8(sDUP, D, w, 32 * wg + g * 8, f + g * 8);
       }
       simt_signal(&sg[SG_P3], tid);
-      BSTAMP(7);
+      BSTAMP(6);
 
       // ================= P5: P, R -> dV, dbeta part ; dX
       mbar_wait(&mb[MB_P], ph);
       fence_after_sync();
-      BSTAMP(8);
+      BSTAMP(7);
       {
-        // lanes < 16 hold (K H) rows, lanes >= 16 P rows (same r64): each lane
-        // pair trades halves so that both lanes work on 8 of every 16 columns
-        const float bt = sb[r64];
+        // lanes < 16: columns [0,64), lanes >= 16: [64,128) of row r64, for
+        // both P (TM_P) and K H (TM_KH); 32 of each half per warpgroup
+        float p[32], f[32];
+        ld32(tm, wwarp, TM_P + 32 * wg, p);
+        ld32(tm, wwarp, TM_KH + 32 * wg, f);
+        const float bt = sb[r64], si = ss[r64];
+        const int c0 = (lo ? 0 : 64) + 32 * wg;
         float db = 0.f;
-#pragma unroll 1
-        for (int cc = 0; cc < 4; ++cc) {
-          const int col = 64 * wg + 16 * cc;
-          float f[16], x[8];
-          ld16f(tm, wwarp, TM_R + col, f);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) x[e] = __shfl_xor_sync(0xffffffffu, lo ? f[8 + e] : f[e], 16);
-          const int c8 = col + (lo ? 0 : 8);
+        for (int g = 0; g < 4; ++g) {
           float v8[8], dv8[8];
-          il_load8(sV, C, r64, c8, v8);
+          il_load8(sV, C, r64, c0 + g * 8, v8);
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            const float kh = lo ? f[e] : x[e];
-            const float p = lo ? x[e] : f[8 + e];
-            db = fmaf(p, v8[e] - kh, db);  // P . R
-            dv8[e] = bt * p;
+            const float rr = fmaf(-si, f[g * 8 + e], v8[e]);
+            db = fmaf(p[g * 8 + e], rr, db);  // P . R
+            dv8[e] = bt * p[g * 8 + e];
           }
-          il_store8(sDV, C, r64, c8, dv8);
+          il_store8(sDV, C, r64, c0 + g * 8, dv8);
         }
         db += __shfl_xor_sync(0xffffffffu, db, 16);
         if (lo) db1[wg * C + r64] = db;
@@ -570,6 +601,30 @@ __global__ void __launch_bounds__(NT, 1)
         il_store8(sDX, C, r64, c8, x);
       }
       simt_signal(&sg[SG_P5], tid);
+      BSTAMP(8);
+
+      // ================= P5b (under M5): dH image for chunk c-1 ; k_hat in place
+      if (c > 0) {
+        mbar_wait(&mb[MB_DH], ph);  // M4 done; dK = U' dH^T done reading the old image
+        fence_after_sync();
+        float f[64];
+        ld64(tm, wwarp, TM_DH + 64 * wg, f);
+#pragma unroll
+        for (int g = 0; g < 8; ++g) il_store8(sDH, D, w, 64 * wg + g * 8, f + g * 8);
+      }
+      if (l2) {
+        const int row = w & 63;
+        const float inv = ss[row];
+#pragma unroll
+        for (int g = 8 * wg + 4 * (w >> 6); g < 8 * wg + 4 * (w >> 6) + 4; ++g) {
+          float x[8];
+          il_load8(sK, C, row, g * 8, x);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) x[e] *= inv;
+          il_store8(sK, C, row, g * 8, x);
+        }
+      }
+      if (c > 0) simt_signal(&sg[SG_DHI], tid);
       BSTAMP(9);
 
       // ================= P6: dA -> bf16 (masked) | Y -> bf16
@@ -598,9 +653,9 @@ __global__ void __launch_bounds__(NT, 1)
       fence_after_sync();
       BSTAMP(12);
       {
-        // lanes < 16: G row (TM_GB); K K^T row from lanes >= 16 (TM_G + lane 16)
+        // lanes < 16: G row (TM_GB); raw K K^T row from lanes >= 16 (TM_G + 16)
         float d2 = 0.f;
-        const float bi = sb[r64];
+        const float bi = sb[r64], si = ss[r64];
 #pragma unroll 1
         for (int cc = 0; cc < 2; ++cc) {
           const int col = 32 * wg + 16 * cc;
@@ -617,14 +672,14 @@ __global__ void __launch_bounds__(NT, 1)
               for (int e = 0; e < 8; ++e) {
                 const int j = col + g * 8 + e;
                 const float gv = (j < r64) ? g16[g * 8 + e] : 0.f;
-                d2 = fmaf(gv, kk[g * 8 + e], d2);
+                d2 = fmaf(gv * ss[j], kk[g * 8 + e], d2);
                 x[e] = bi * gv;
               }
               il_store8(sG1, C, r64, col + g * 8, x);
             }
           }
         }
-        if (lo) db2[wg * C + r64] = d2;
+        if (lo) db2[wg * C + r64] = d2 * si;
       }
       simt_signal(&sg[SG_P7], tid);
       BSTAMP(13);
@@ -634,7 +689,7 @@ __global__ void __launch_bounds__(NT, 1)
         // lanes >= 16: dq_hat row r64 (TM_DQ), this warpgroup's 64 columns;
         // the row dot q_hat . dq_hat is combined across the warpgroups
         float f[64];
-        ld64(tm, wwarp, TM_R + 64 * wg, f);
+        ld64(tm, wwarp, TM_DK + 64 * wg, f);
         float dot = 0.f;
         if (!lo) {
 #pragma unroll

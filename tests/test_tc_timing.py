@@ -95,10 +95,11 @@ def test_bwd_timeline(timlib):
                                 ws.data_ptr(), ws.numel(), None) == 0
     torch.cuda.synchronize()
     t = buf.cpu().numpy().reshape(NC, 32).astype(np.int64)
-    names = {0: "start", 1: "tma wait", 2: "norms+scale", 3: "G wait", 4: "P2 A",
-             5: "P3 U' conv + R wait", 6: "P3 R conv + dU wait", 7: "P3 dU' conv",
-             8: "P wait", 9: "P5 P, dV, dX", 10: "A wait", 11: "P6 dA, Y", 12: "Q wait",
-             13: "P7 G1, dbeta", 14: "dq epi + K wait", 15: "P8 dk"}
+    names = {0: "start", 1: "P1 loads + norms", 2: "G wait", 3: "P2 A_m",
+             4: "P3 U', q_hat, R wait", 5: "P3 R conv + dU wait", 6: "P3 dU' conv",
+             7: "P wait", 8: "P5 P, dV, dX", 9: "P5b dH image, k_hat", 10: "A wait",
+             11: "P6 dA, Y", 12: "Q wait", 13: "P7 G1, dbeta", 14: "dq epi + K wait",
+             15: "P8 dk"}
     rows = []
     seq = list(range(16))
     for a_, b_ in zip(seq[:-1], seq[1:]):
@@ -106,11 +107,11 @@ def test_bwd_timeline(timlib):
         rows.append(f"{names[b_]:28s} {dt.mean():9.0f} cycles")
     rows.append(f"{'-- per chunk':28s} {np.diff(t[2:-2, 0]).mean():9.0f} cycles")
     # issuer stamps (slots 16-29), relative to the SIMT chunk start (slot 0)
-    inames = {16: "I norm rcv", 17: "I M1 issued", 18: "I A rcv", 19: "I M2 issued",
-              20: "I P3 rcv", 21: "I M3/M4 issued", 22: "I P5 rcv", 23: "I M5 issued",
-              24: "I P6 rcv", 25: "I M6 issued", 26: "I P7 rcv", 27: "I M7 issued",
-              28: "I dq rcv", 29: "I P8 rcv"}
-    for s_ in range(16, 30):
+    inames = {16: "I main+dHimg rcv", 17: "I M1a issued", 18: "I prev dq/dk stored",
+              19: "I M1b issued", 20: "I A rcv", 21: "I P3 rcv", 22: "I M3/M4 issued",
+              23: "I P5 rcv", 24: "I M5 issued", 25: "I P6 rcv", 26: "I M6 + loads",
+              27: "I P7 rcv"}
+    for s_ in range(16, 28):
         dt = t[2:-2, s_] - t[2:-2, 0]
         rows.append(f"{inames[s_]:28s} {dt.mean():9.0f} cycles after chunk start")
     print("\n" + "\n".join(rows))

@@ -30,9 +30,10 @@
 //   K_hat K_hat^T = diag(s) K K^T diag(s).
 // q and k are normalised in place afterwards for the remaining products.
 //
-// 288 threads: warps 0-7 run the SIMT phases (split by columns between the
-// two warpgroups, both see all 128 TMEM lanes); warp 8 issues every MMA, TMA
-// load and store, driven by mbarrier hand-offs.
+// 320 threads: warps 0-7 run the SIMT phases (split by columns between the
+// two warpgroups, both see all 128 TMEM lanes); warp 8 issues every MMA and
+// warp 9 every TMA load and store, both driven by mbarrier hand-offs (a
+// single issuer would sit blocked on a full MMA queue while a load waits).
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
@@ -43,7 +44,7 @@ namespace {
 
 using namespace tc;
 
-constexpr int C = 64, D = 128, NT = 288;  // warps 0-7 SIMT, warp 8 issuer
+constexpr int C = 64, D = 128, NT = 320;  // warps 0-7 SIMT, 8 MMA issuer, 9 TMA
 constexpr uint32_t LO16 = 16u << 16;  // TMEM lane offset 16 (second M=64 accumulator)
 constexpr int TILE = C * D * 2;       // 16 KB
 constexpr int HALF_ROWS = 64 * 16;    // byte offset of row 64 in an IL R=128 tile
@@ -186,19 +187,12 @@ __global__ void __launch_bounds__(NT, 1)
   cta_sync();
   const uint32_t tm = tslot;
 
-  if (warp == NT / 32 - 1) {
+  if (warp == 9) {
     // =====================================================================
-    // Issuer warp (lane 0): every tcgen05.mma, TMA load and store.  It only
-    // waits on hand-off barriers; the SIMT warps never stall behind a full
-    // MMA queue.  Software-pipelined: chunk c-1's first products are issued
-    // as soon as its tiles land, under chunk c's epilogues.
+    // TMA warp (lane 0): every load and store; SG_STG tells the SIMT warps
+    // that the dq / dk staging regions have been read out.
     // =====================================================================
     if (lane == 0) {
-      const uint32_t aQ = smem_u32(sQ), aDO = smem_u32(sDO), aH = smem_u32(sH),
-                     aDH = smem_u32(sDH), aX = smem_u32(sX), aA = smem_u32(sA),
-                     aDUP = smem_u32(sDUP), aR = smem_u32(sR), aDA = smem_u32(sDA),
-                     aDX = smem_u32(sDX), aY = smem_u32(sY), aG1 = smem_u32(sG1),
-                     aDV = smem_u32(sDV), aUP = smem_u32(sUP);
       auto issue_loads_main = [&](int c, int ks) {  // K, dO, V, H_t, X, Z^T
         mbar_expect_tx(&mb[MB_MAIN], 3 * TILE + D * D * 2 + C * C * 2 + D * C * 2);
         tma_load_4d(smem + OFF_KW + ks * TILE, &mK, 0, c * C, 0, unit, &mb[MB_MAIN]);
@@ -222,10 +216,53 @@ __global__ void __launch_bounds__(NT, 1)
         issue_load_q(NC - 1);
         issue_load_w(NC - 1, 0);
       }
+      mbar_arrive(&sg[SG_STG]);
 #pragma unroll 1
       for (int it = 0; it < NC; ++it) {
         const int c = NC - 1 - it, t0 = c * C, ks = it & 1;
-        const uint32_t ph = it & 1, php = (it - 1) & 1;
+        const uint32_t ph = it & 1;
+        mbar_wait(&sg[SG_P5], ph);
+        tma_store_4d(&mDV, sDV, 0, t0, 0, unit);
+        bulk_commit();
+        // chunk c-1 (K into the W slot): dO, H^T, X, U' and W^T are free
+        // after M6; V once the dV store has been read out
+        mbar_wait(&mb[MB_Q], ph);
+        if (c > 0) {
+          bulk_wait_read0();
+          issue_loads_main(c - 1, 1 - ks);
+        }
+        mbar_wait(&sg[SG_DQ], ph);  // q_hat read by the dq epilogue
+        tma_store_4d(&mDQ, sDQo, 0, t0, 0, unit);
+        bulk_commit();
+        if (c > 0) issue_load_q(c - 1);
+        mbar_wait(&sg[SG_P8], ph);  // k_hat read by the dk epilogue
+        tma_store_4d(&mDK, sDKo, 0, t0, 0, unit);
+        bulk_commit();
+        if (c > 0) {
+          issue_load_w(c - 1, 1 - ks);
+          bulk_wait_read0();  // dq / dk staging (DUP / R regions) read out
+          mbar_arrive(&sg[SG_STG]);
+        }
+      }
+      bulk_wait0();
+    }
+    __syncwarp();
+  } else if (warp == 8) {
+    // =====================================================================
+    // MMA warp (lane 0): every tcgen05.mma.  Software-pipelined: chunk c-1's
+    // first products are issued as soon as its tiles land, under chunk c's
+    // epilogues.
+    // =====================================================================
+    if (lane == 0) {
+      const uint32_t aQ = smem_u32(sQ), aDO = smem_u32(sDO), aH = smem_u32(sH),
+                     aDH = smem_u32(sDH), aX = smem_u32(sX), aA = smem_u32(sA),
+                     aDUP = smem_u32(sDUP), aR = smem_u32(sR), aDA = smem_u32(sDA),
+                     aDX = smem_u32(sDX), aY = smem_u32(sY), aG1 = smem_u32(sG1),
+                     aDV = smem_u32(sDV), aUP = smem_u32(sUP);
+#pragma unroll 1
+      for (int it = 0; it < NC; ++it) {
+        const int ks = it & 1;
+        const uint32_t ph = it & 1;
         const uint32_t aK = smem_u32(smem + OFF_KW + ks * TILE);
         const uint32_t aW = smem_u32(smem + OFF_KW + (1 - ks) * TILE);
 
@@ -253,25 +290,11 @@ __global__ void __launch_bounds__(NT, 1)
           mma_commit(&mb[MB_R]);
         }
         ISTAMP(17);
-        if (it > 0) {
-          // previous chunk's tail: dq store + Q of this chunk ...
-          mbar_wait(&sg[SG_DQ], php);
-          tma_store_4d(&mDQ, sDQo, 0, t0 + C, 0, unit);
-          bulk_commit();
-          issue_load_q(c);
-          // ... dk store + W^T of this chunk into the retired K slot
-          mbar_wait(&sg[SG_P8], php);
-          tma_store_4d(&mDK, sDKo, 0, t0 + C, 0, unit);
-          bulk_commit();
-          issue_load_w(c, ks);
-        }
-        ISTAMP(18);
-        bulk_wait_read0();  // dq / dk staging (DUP / R regions) read out
-        mbar_arrive(&sg[SG_STG]);
 
         // M1b: Q K^T (raw)
         mbar_wait(&mb[MB_QL], ph);
         fence_after_sync();
+        ISTAMP(18);
         {
           const uint32_t idg = idesc_bf16(64, 64, false, false);
 #pragma unroll
@@ -327,12 +350,10 @@ __global__ void __launch_bounds__(NT, 1)
         }
         ISTAMP(22);
 
-        // dV store; M5: dA, Y | dQ = dO H^T, dK -= dV H^T
+        // M5: dA, Y | dQ = dO H^T, dK -= dV H^T
         mbar_wait(&sg[SG_P5], ph);
         fence_after_sync();
         ISTAMP(23);
-        tma_store_4d(&mDV, sDV, 0, t0, 0, unit);
-        bulk_commit();
         {
           const uint32_t id_da = idesc_bf16(64, 64, false, true);
           const uint32_t id_y = idesc_bf16(64, 64, true, true);
@@ -371,14 +392,6 @@ __global__ void __launch_bounds__(NT, 1)
           }
           mma_commit(&mb[MB_Q]);
         }
-
-        // prefetch chunk c-1 (K into the W slot): dO, H^T, X, U' and W^T are
-        // free after M6; V once the dV store has been read out
-        if (c > 0) {
-          mbar_wait(&mb[MB_Q], ph);
-          bulk_wait_read0();
-          issue_loads_main(c - 1, 1 - ks);
-        }
         ISTAMP(26);
 
         // M7: dK += (G1 + G1^T) K_hat
@@ -396,16 +409,6 @@ __global__ void __launch_bounds__(NT, 1)
           mma_commit(&mb[MB_K]);
         }
       }
-      if (NC > 0) {  // tail of chunk 0
-        const int it = NC - 1;
-        mbar_wait(&sg[SG_DQ], it & 1);
-        tma_store_4d(&mDQ, sDQo, 0, 0, 0, unit);
-        bulk_commit();
-        mbar_wait(&sg[SG_P8], it & 1);
-        tma_store_4d(&mDK, sDKo, 0, 0, 0, unit);
-        bulk_commit();
-      }
-      bulk_wait0();
     }
     __syncwarp();
   } else {

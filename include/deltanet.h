@@ -56,7 +56,7 @@ enum {
   /* fwd: write the chunk-boundary states H_t into the workspace so the bwd
    * does not recompute them (§3.2 line 250 recomputes them; we
    * store them -- DESIGN.md "Differences from the paper").  The tcgen05
-   * path also stores a 40 KB per-chunk record (X, W^T, Z^T)
+   * path also stores a 24 KB per-chunk record (X, Z^T)
    * so the bwd skips the UT substitution.
    * bwd: the workspace holds what a fwd with this flag over the same inputs
    * and the same desc wrote. */

@@ -5,13 +5,13 @@
 // adjoint of Eq. 8-11 chunk by chunk in reverse (DESIGN.md §4.2,
 // SURVEY App. A.2), one CTA per (b, h) unit, with dH = dl/dH_{t+1} held in
 // TMEM (fp32, lanes = d_v) across chunks.  The forward's per-chunk record
-// (H_t, X, W^T, Z^T = (diag(s) U')^T; tc_common.cuh REC_*) is read back, so
-// the UT substitution and the W / U / U' products are not recomputed.
+// (H_t, X, Z^T = (diag(s) U')^T; tc_common.cuh REC_*) is read back, so the
+// UT substitution and the W / U / U' products are not recomputed.
 //
 // Per chunk (q_hat = diag(r) q, k_hat = diag(s) k: L2-normalised rows):
 //   recompute  A = tril(Q_hat K_hat^T), R = V - K_hat H, U' = diag(1/s) Z
 //   chain      dU' = K_hat dH + A^T dO
-//              dH <- dH + Q_hat^T dO - W^T dU'
+//              dH <- dH + Q_hat^T dO - W^T dU',  W^T dU' = K_hat^T diag(b) X^T dU' = K_hat^T dV
 //   local      dA = tril(dO U'^T)          P = X^T dU'  (= dV_beta)
 //              dX = (dU' R^T) diag(b)      Y = X^T dX,  G = tril(-Y X^T, -1)
 //              dQ = dO H^T + dA K_hat
@@ -51,8 +51,8 @@ constexpr int HALF_ROWS = 64 * 16;    // byte offset of row 64 in an IL R=128 ti
 
 // ---- shared memory map (bytes); regions reused by lifetime
 constexpr int OFF_Q = 0;                    // q (raw, then q_hat in place)
-constexpr int OFF_KW = OFF_Q + TILE;        // 2 slots: k (raw, then k_hat) | W^T (IL R=128 x 64)
-constexpr int OFF_DO = OFF_KW + 2 * TILE;   // dO     IL R=64 x 128
+constexpr int OFF_K = OFF_Q + TILE;         // 2 slots: k (raw, then k_hat), chunk parity
+constexpr int OFF_DO = OFF_K + 2 * TILE;    // dO     IL R=64 x 128
 constexpr int OFF_V = OFF_DO + TILE;        // V -> dV staging
 constexpr int OFF_H = OFF_V + TILE;         // H^T    IL R=128 x 128
 constexpr int OFF_DH = OFF_H + D * D * 2;   // dH^T   IL R=128 x 128
@@ -61,7 +61,7 @@ constexpr int OFF_Z = OFF_X + C * C * 2;    // Z^T (record) -> U'^T in place
 constexpr int OFF_R = OFF_Z + TILE;         // R -> Y [0,8K) + G1 [8K,16K) -> dk staging
 constexpr int OFF_DUP = OFF_R + TILE;       // dU'^T -> dq staging
 constexpr int OFF_A = OFF_DUP + TILE;       // A_m -> dX -> dA
-constexpr int OFF_VEC = OFF_A + C * C * 2;  // beta, r, s, nq, nk, db1[2], db2[2], dot[2], dotq[2], n2[2][2]
+constexpr int OFF_VEC = OFF_A + C * C * 2;  // beta, r, s, nq, nk, db1[2], db2[2], dot[2], dotq[2], n2[4]
 constexpr int SMEM_BYTES = OFF_VEC + 17 * C * 4;
 static_assert(SMEM_BYTES <= 232448 - 1024, "shared memory budget");
 
@@ -77,9 +77,9 @@ constexpr uint32_t TM_KH = 448;                          // (K H)[:, :64] | [:, 
 
 enum { BAR_SIMT = 1 };
 // issuer -> SIMT: MMA commits and TMA arrivals
-enum { MB_G, MB_R, MB_DU, MB_WL, MB_P, MB_DH, MB_A, MB_Q, MB_K, MB_MAIN, MB_QL, MB_N };
+enum { MB_G, MB_R, MB_DU, MB_P, MB_DH, MB_A, MB_LD, MB_GB, MB_K, MB_MAIN, MB_QL, MB_KL0, MB_KL1, MB_N };
 // SIMT -> issuer hand-offs (SG_STG: issuer -> SIMT, staging regions free)
-enum { SG_DHI, SG_A, SG_P3, SG_P5, SG_P6, SG_P7, SG_DQ, SG_P8, SG_STG, SG_N };
+enum { SG_DHI, SG_A, SG_P3, SG_P5, SG_P6, SG_P7, SG_P8, SG_STG, SG_N };
 
 __device__ __forceinline__ void ld32(uint32_t tm, int wwarp, uint32_t col, float (&f)[32]) {
   uint32_t r[2][16];
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(NT, 1)
   float* db2 = db1 + 2 * C;    // [2][64] rowsum(G . K K^T) partials
   float* sdot = db2 + 2 * C;   // [2][64] dk-adjoint dot partials
   float* sdotq = sdot + 2 * C; // [2][64] dq-adjoint dot partials
-  float* n2 = sdotq + 2 * C;   // [2 (q,k)][2 (half)][64] squared-norm partials
+  float* n2 = sdotq + 2 * C;   // [4][64] squared-norm partials (column quarters)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wg = (tid >> 7) & 1, w = tid & 127, wwarp = w >> 5;
@@ -189,60 +189,71 @@ __global__ void __launch_bounds__(NT, 1)
 
   if (warp == 9) {
     // =====================================================================
-    // TMA warp (lane 0): every load and store; SG_STG tells the SIMT warps
-    // that the dq / dk staging regions have been read out.
+    // TMA warp (lane 0): every load and store.  Chunk c-1's tiles are loaded
+    // as their regions retire during chunk c: K at the start of chunk c
+    // (double-buffered), dO / V / H / Z after M5 (MB_LD), X after G (MB_GB),
+    // Q after the chunk-c epilogue.  SG_STG tells the SIMT warps that the dq /
+    // dk staging regions have been read out.
     // =====================================================================
     if (lane == 0) {
-      auto issue_loads_main = [&](int c, int ks) {  // K, dO, V, H_t, X, Z^T
-        mbar_expect_tx(&mb[MB_MAIN], 3 * TILE + D * D * 2 + C * C * 2 + D * C * 2);
-        tma_load_4d(smem + OFF_KW + ks * TILE, &mK, 0, c * C, 0, unit, &mb[MB_MAIN]);
+      constexpr uint32_t MAIN_BYTES = 3 * TILE + D * D * 2 + C * C * 2;  // dO V Z | H | X
+      auto load_k = [&](int c, int slot) {  // own barrier per slot (one phase per use)
+        mbar_expect_tx(&mb[MB_KL0 + slot], TILE);
+        tma_load_4d(smem + OFF_K + slot * TILE, &mK, 0, c * C, 0, unit, &mb[MB_KL0 + slot]);
+      };
+      auto load_rest = [&](int c) {  // dO, V, H_t, Z^T (opens the MB_MAIN phase, X included)
+        mbar_expect_tx(&mb[MB_MAIN], MAIN_BYTES);
         tma_load_4d(sDO, &mDO, 0, c * C, 0, unit, &mb[MB_MAIN]);
         tma_load_4d(sV, &mV, 0, c * C, 0, unit, &mb[MB_MAIN]);
         bulk_load(sH, states + (size_t)c * D * D * 2, D * D * 2, &mb[MB_MAIN]);
-        bulk_load(sX, recs + (size_t)c * REC_BYTES + REC_X, C * C * 2, &mb[MB_MAIN]);
         bulk_load(sZ, recs + (size_t)c * REC_BYTES + REC_Z, D * C * 2, &mb[MB_MAIN]);
       };
-      auto issue_load_q = [&](int c) {
+      auto load_x = [&](int c) {
+        bulk_load(sX, recs + (size_t)c * REC_BYTES + REC_X, C * C * 2, &mb[MB_MAIN]);
+      };
+      auto load_q = [&](int c) {
         mbar_expect_tx(&mb[MB_QL], TILE);
         tma_load_4d(sQ, &mQ, 0, c * C, 0, unit, &mb[MB_QL]);
       };
-      auto issue_load_w = [&](int c, int ks) {  // W^T of chunk c into the slot not holding K
-        mbar_expect_tx(&mb[MB_WL], D * C * 2);
-        bulk_load(smem + OFF_KW + (1 - ks) * TILE, recs + (size_t)c * REC_BYTES + REC_W, D * C * 2,
-                  &mb[MB_WL]);
-      };
       if (NC > 0) {
-        issue_loads_main(NC - 1, 0);
-        issue_load_q(NC - 1);
-        issue_load_w(NC - 1, 0);
+        load_k(NC - 1, 0);
+        load_rest(NC - 1);
+        load_x(NC - 1);
+        load_q(NC - 1);
       }
       mbar_arrive(&sg[SG_STG]);
 #pragma unroll 1
       for (int it = 0; it < NC; ++it) {
-        const int c = NC - 1 - it, t0 = c * C, ks = it & 1;
+        const int c = NC - 1 - it, t0 = c * C;
         const uint32_t ph = it & 1;
+        if (it > 0) {  // tail of chunk c+1: its epilogue read q_hat / k_hat
+          mbar_wait(&sg[SG_P8], ph ^ 1);
+          tma_store_4d(&mDQ, sDQo, 0, t0 + C, 0, unit);
+          tma_store_4d(&mDK, sDKo, 0, t0 + C, 0, unit);
+          bulk_commit();
+          load_q(c);
+          if (c > 0) load_k(c - 1, (it + 1) & 1);  // the slot of chunk c+1
+          bulk_wait_read0();  // dq / dk staging (DUP / R regions) read out
+          mbar_arrive(&sg[SG_STG]);
+        } else if (c > 0) {
+          load_k(c - 1, 1);
+        }
         mbar_wait(&sg[SG_P5], ph);
         tma_store_4d(&mDV, sDV, 0, t0, 0, unit);
         bulk_commit();
-        // chunk c-1 (K into the W slot): dO, H^T, X, U' and W^T are free
-        // after M6; V once the dV store has been read out
-        mbar_wait(&mb[MB_Q], ph);
         if (c > 0) {
+          mbar_wait(&mb[MB_LD], ph);  // dO, H^T, U' read by M5; V once dV is read out
           bulk_wait_read0();
-          issue_loads_main(c - 1, 1 - ks);
+          load_rest(c - 1);
+          mbar_wait(&mb[MB_GB], ph);  // X read by G
+          load_x(c - 1);
         }
-        mbar_wait(&sg[SG_DQ], ph);  // q_hat read by the dq epilogue
-        tma_store_4d(&mDQ, sDQo, 0, t0, 0, unit);
+      }
+      if (NC > 0) {
+        mbar_wait(&sg[SG_P8], (NC - 1) & 1);
+        tma_store_4d(&mDQ, sDQo, 0, 0, 0, unit);
+        tma_store_4d(&mDK, sDKo, 0, 0, 0, unit);
         bulk_commit();
-        if (c > 0) issue_load_q(c - 1);
-        mbar_wait(&sg[SG_P8], ph);  // k_hat read by the dk epilogue
-        tma_store_4d(&mDK, sDKo, 0, t0, 0, unit);
-        bulk_commit();
-        if (c > 0) {
-          issue_load_w(c - 1, 1 - ks);
-          bulk_wait_read0();  // dq / dk staging (DUP / R regions) read out
-          mbar_arrive(&sg[SG_STG]);
-        }
       }
       bulk_wait0();
     }
@@ -263,11 +274,11 @@ __global__ void __launch_bounds__(NT, 1)
       for (int it = 0; it < NC; ++it) {
         const int ks = it & 1;
         const uint32_t ph = it & 1;
-        const uint32_t aK = smem_u32(smem + OFF_KW + ks * TILE);
-        const uint32_t aW = smem_u32(smem + OFF_KW + (1 - ks) * TILE);
+        const uint32_t aK = smem_u32(smem + OFF_K + ks * TILE);
 
         // M1a (raw k): K K^T | dH^T K^T | K H.  TMEM G / GB / KH were released
         // by the previous chunk's P7 / P5 (waited below in program order).
+        mbar_wait(&mb[MB_KL0 + ks], (it >> 1) & 1);
         mbar_wait(&mb[MB_MAIN], ph);
         mbar_wait(&sg[SG_DHI], ph);
         fence_after_sync();
@@ -317,7 +328,7 @@ __global__ void __launch_bounds__(NT, 1)
         }
 
         // M3: P = X^T dU' (two N=64 halves), dX' = dU' R^T
-        // M4: dH += Q_hat^T dO - W^T dU' ; dK = U' dH^T (dH image of chunk c+1)
+        // M4a: dH += Q_hat^T dO ; dK = U' dH^T (dH image of chunk c+1)
         mbar_wait(&sg[SG_P3], ph);
         fence_after_sync();
         ISTAMP(21);
@@ -334,7 +345,6 @@ __global__ void __launch_bounds__(NT, 1)
             mma_bf16(tm + TM_DX, desc_mn(aDUP, D, k0), desc_k(aR, C, k0), idp, k0 > 0);
           mma_commit(&mb[MB_P]);
           const uint32_t id1 = idesc_bf16(128, 128, true, true);
-          const uint32_t id2 = idesc_bf16(128, 128, false, false, true);
           const uint32_t id_k1 = idesc_bf16(64, 128, true, true);
 #pragma unroll
           for (int k0 = 0; k0 < C; k0 += 16)
@@ -342,19 +352,20 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
           for (int k0 = 0; k0 < D; k0 += 16)
             mma_bf16(tm + TM_DK, desc_mn(aUP, D, k0), desc_mn(aDH, D, k0), id_k1, k0 > 0);
-          mbar_wait(&mb[MB_WL], ph);
-#pragma unroll
-          for (int k0 = 0; k0 < C; k0 += 16)
-            mma_bf16(tm + TM_DH, desc_k(aDUP, D, k0), desc_k(aW, D, k0), id2, 1);
-          mma_commit(&mb[MB_DH]);
         }
         ISTAMP(22);
 
+        // M4b: dH -= W^T dU' = K_hat^T dV  (W = X diag(b) K_hat, dV = diag(b) X^T dU')
         // M5: dA, Y | dQ = dO H^T, dK -= dV H^T
         mbar_wait(&sg[SG_P5], ph);
         fence_after_sync();
         ISTAMP(23);
         {
+          const uint32_t id2 = idesc_bf16(128, 128, true, true, true);
+#pragma unroll
+          for (int k0 = 0; k0 < C; k0 += 16)
+            mma_bf16(tm + TM_DH, desc_mn(aDV, C, k0), desc_mn(aK, C, k0), id2, 1);
+          mma_commit(&mb[MB_DH]);
           const uint32_t id_da = idesc_bf16(64, 64, false, true);
           const uint32_t id_y = idesc_bf16(64, 64, true, true);
           const uint32_t id_q = idesc_bf16(64, 128, false, true);
@@ -371,10 +382,12 @@ __global__ void __launch_bounds__(NT, 1)
             mma_bf16(tm + TM_DQ, desc_k(aDO, C, k0), desc_mn(aH, D, k0), id_q, k0 > 0);
             mma_bf16(tm + TM_DK, desc_k(aDV, C, k0), desc_mn(aH, D, k0), id_k2, 1);
           }
+          mma_commit(&mb[MB_LD]);
         }
         ISTAMP(24);
 
-        // M6: G = -Y X^T ; dQ += dA K_hat ; dK += dA^T Q_hat
+        // M6: G = -Y X^T first (the SIMT warps wait on it) ; dQ += dA K_hat ;
+        // dK += dA^T Q_hat
         mbar_wait(&sg[SG_P6], ph);
         fence_after_sync();
         ISTAMP(25);
@@ -385,12 +398,12 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
           for (int k0 = 0; k0 < C; k0 += 16)
             mma_bf16(tm + TM_GB, desc_k(aY, C, k0), desc_k(aX, C, k0), id_g, k0 > 0);
+          mma_commit(&mb[MB_GB]);
 #pragma unroll
           for (int k0 = 0; k0 < C; k0 += 16) {
             mma_bf16(tm + TM_DQ, desc_k(aDA, C, k0), desc_mn(aK, C, k0), id_q, 1);
             mma_bf16(tm + TM_DK, desc_mn(aDA, C, k0), desc_mn(aQ, C, k0), id_k, 1);
           }
-          mma_commit(&mb[MB_Q]);
         }
         ISTAMP(26);
 
@@ -440,19 +453,18 @@ __global__ void __launch_bounds__(NT, 1)
     for (int it = 0; it < NC; ++it) {
       const int c = NC - 1 - it, t0 = c * C, ks = it & 1;
       const uint32_t ph = it & 1;
-      uint8_t* sK = smem + OFF_KW + ks * TILE;
+      uint8_t* sK = smem + OFF_K + ks * TILE;
 
-      // ================= P1: row norms from the raw tiles
+      // ================= P1: k norms ; U' ; R = V - diag(s) K H ; q norms
       BSTAMP(0);
       if (tid < C) sb[tid] = (t0 + tid < L) ? __bfloat162float(beta[t0 + tid]) : 0.f;
-      {
-        // wg0: q rows, wg1: k rows; thread w: row w & 63, column half w >> 6
-        const int row = w & 63, hf = w >> 6;
-        mbar_wait(&mb[wg == 0 ? MB_QL : MB_MAIN], ph);
-        const uint8_t* tile = wg == 0 ? sQ : sK;
+      // squared row norms of a raw 64x128 tile: thread = (row w & 63, column
+      // quarter wg * 2 + (w >> 6)), combined through n2
+      auto row_norms = [&](const uint8_t* tile, float* inv_out, float* n_out) {
+        const int row = w & 63, qt = wg * 2 + (w >> 6);
         float acc0 = 0.f, acc1 = 0.f;
 #pragma unroll
-        for (int g = 8 * hf; g < 8 * hf + 8; ++g) {
+        for (int g = 4 * qt; g < 4 * qt + 4; ++g) {
           float x[8];
           il_load8(tile, C, row, g * 8, x);
 #pragma unroll
@@ -461,25 +473,60 @@ __global__ void __launch_bounds__(NT, 1)
             acc1 = fmaf(x[e + 1], x[e + 1], acc1);
           }
         }
-        n2[(wg * 2 + hf) * C + row] = acc0 + acc1;
-        mbar_wait(&mb[MB_MAIN], ph);  // every SIMT thread observes both arrivals
-        mbar_wait(&mb[MB_QL], ph);
+        n2[qt * C + row] = acc0 + acc1;
         grp_sync<256>(BAR_SIMT);
-        if (w < 64) {
-          const float n = sqrtf(n2[(wg * 2) * C + row] + n2[(wg * 2 + 1) * C + row]);
+        if (tid < C) {
+          const float n = sqrtf((n2[tid] + n2[C + tid]) + (n2[2 * C + tid] + n2[3 * C + tid]));
           float inv = l2 ? 1.f / fmaxf(n, eps) : 1.f;
-          if (t0 + row >= L) inv = 0.f;
-          (wg == 0 ? sr : ss)[row] = inv;
-          (wg == 0 ? nq : nk)[row] = n;
+          if (t0 + tid >= L) inv = 0.f;
+          inv_out[tid] = inv;
+          n_out[tid] = n;
         }
         grp_sync<256>(BAR_SIMT);
-      }
+      };
+      mbar_wait(&mb[MB_KL0 + ks], (it >> 1) & 1);
+      mbar_wait(&mb[MB_MAIN], ph);
+      row_norms(sK, ss, nk);
       BSTAMP(1);
+      if (l2) {  // U'^T[dv][t] = Z^T[dv][t] * max(|k_t|, eps)  (row dv = w)
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const int col = 32 * wg + g * 8;
+          float z8[8];
+          il_load8(sUP, D, w, col, z8);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) z8[e] *= fmaxf(nk[col + e], eps);
+          il_store8(sUP, D, w, col, z8);
+        }
+      }
+      mbar_wait(&sg[SG_STG], ph);  // R / DUP regions free (previous dq/dk stores read out)
+      mbar_wait(&mb[MB_R], ph);
+      fence_after_sync();
+      BSTAMP(2);
+      {
+        // (K H) row r64: lanes < 16 hold columns [0,64), lanes >= 16 [64,128);
+        // this warpgroup takes 32 of each half
+        float f[32];
+        ld32(tm, wwarp, TM_KH + 32 * wg, f);
+        const float si = ss[r64];
+        const int c0 = (lo ? 0 : 64) + 32 * wg;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          float v8[8];
+          il_load8(sV, C, r64, c0 + g * 8, v8);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v8[e] = fmaf(-si, f[g * 8 + e], v8[e]);
+          il_store8(sR, C, r64, c0 + g * 8, v8);
+        }
+      }
+      mbar_wait(&mb[MB_QL], ph);
+      BSTAMP(3);
+      row_norms(sQ, sr, nq);
 
       // ================= P2: A_m = tril(diag(r) Q K^T) -> bf16 (lanes < 16)
       mbar_wait(&mb[MB_G], ph);
       fence_after_sync();
-      BSTAMP(2);
+      BSTAMP(4);
       {
         float f[32];
         ld32(tm, wwarp, TM_G + 32 * wg, f);
@@ -498,51 +545,20 @@ __global__ void __launch_bounds__(NT, 1)
         }
       }
       simt_signal(&sg[SG_A], tid);
-      BSTAMP(3);
 
-      // ================= P3: U' = diag(max(|k|,eps)) Z ; q_hat in place ;
-      //                       R = V - diag(s) K H ; dU' = (..) diag(s) -> bf16
-      if (l2) {
-        // U'^T[dv][t] = Z^T[dv][t] * max(|k_t|, eps)  (row dv = w)
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          const int col = 32 * wg + g * 8;
-          float z8[8];
-          il_load8(sUP, D, w, col, z8);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) z8[e] *= fmaxf(nk[col + e], eps);
-          il_store8(sUP, D, w, col, z8);
-        }
-        // q_hat = diag(r) q in place (M1 done reading raw q: MB_G waited)
+      // ================= P3: q_hat, k_hat in place ; dU' = (..) diag(s) -> bf16
+      if (l2) {  // M1 is done reading raw q, k (MB_G); thread: row w & 63 of q
+        // (wg0) or k (wg1), one column half
         const int row = w & 63;
-        const float inv = sr[row];
+        uint8_t* tile = wg == 0 ? sQ : sK;
+        const float inv = (wg == 0 ? sr : ss)[row];
 #pragma unroll
-        for (int g = 8 * wg + 4 * (w >> 6); g < 8 * wg + 4 * (w >> 6) + 4; ++g) {
+        for (int g = 8 * (w >> 6); g < 8 * (w >> 6) + 8; ++g) {
           float x[8];
-          il_load8(sQ, C, row, g * 8, x);
+          il_load8(tile, C, row, g * 8, x);
 #pragma unroll
           for (int e = 0; e < 8; ++e) x[e] *= inv;
-          il_store8(sQ, C, row, g * 8, x);
-        }
-      }
-      mbar_wait(&sg[SG_STG], ph);  // R / DUP regions free (previous dq/dk stores read out)
-      mbar_wait(&mb[MB_R], ph);
-      fence_after_sync();
-      BSTAMP(4);
-      {
-        // (K H) row r64: lanes < 16 hold columns [0,64), lanes >= 16 [64,128);
-        // this warpgroup takes 32 of each half
-        float f[32];
-        ld32(tm, wwarp, TM_KH + 32 * wg, f);
-        const float si = ss[r64];
-        const int c0 = (lo ? 0 : 64) + 32 * wg;
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          float v8[8];
-          il_load8(sV, C, r64, c0 + g * 8, v8);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) v8[e] = fmaf(-si, f[g * 8 + e], v8[e]);
-          il_store8(sR, C, r64, c0 + g * 8, v8);
+          il_store8(tile, C, row, g * 8, x);
         }
       }
       mbar_wait(&mb[MB_DU], ph);
@@ -606,7 +622,7 @@ __global__ void __launch_bounds__(NT, 1)
       simt_signal(&sg[SG_P5], tid);
       BSTAMP(8);
 
-      // ================= P5b (under M5): dH image for chunk c-1 ; k_hat in place
+      // ================= P5b (under M5): dH image for chunk c-1
       if (c > 0) {
         mbar_wait(&mb[MB_DH], ph);  // M4 done; dK = U' dH^T done reading the old image
         fence_after_sync();
@@ -614,20 +630,8 @@ __global__ void __launch_bounds__(NT, 1)
         ld64(tm, wwarp, TM_DH + 64 * wg, f);
 #pragma unroll
         for (int g = 0; g < 8; ++g) il_store8(sDH, D, w, 64 * wg + g * 8, f + g * 8);
+        simt_signal(&sg[SG_DHI], tid);
       }
-      if (l2) {
-        const int row = w & 63;
-        const float inv = ss[row];
-#pragma unroll
-        for (int g = 8 * wg + 4 * (w >> 6); g < 8 * wg + 4 * (w >> 6) + 4; ++g) {
-          float x[8];
-          il_load8(sK, C, row, g * 8, x);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) x[e] *= inv;
-          il_store8(sK, C, row, g * 8, x);
-        }
-      }
-      if (c > 0) simt_signal(&sg[SG_DHI], tid);
       BSTAMP(9);
 
       // ================= P6: dA -> bf16 (masked) | Y -> bf16
@@ -651,109 +655,76 @@ __global__ void __launch_bounds__(NT, 1)
       simt_signal(&sg[SG_P6], tid);
       BSTAMP(11);
 
-      // ================= P7: G1 = diag(b) G, dbeta part 2 ; then the dq epilogue
-      mbar_wait(&mb[MB_Q], ph);
+      // ================= P7: G1 = diag(b) G, dbeta part 2
+      mbar_wait(&mb[MB_GB], ph);
       fence_after_sync();
       BSTAMP(12);
       {
-        // lanes < 16: G row (TM_GB); raw K K^T row from lanes >= 16 (TM_G + 16)
+        // lanes < 16 hold the G row (TM_GB), lanes >= 16 the raw K K^T row
+        // (TM_G + 16); each lane pair splits every 16 columns 8 / 8
         float d2 = 0.f;
-        const float bi = sb[r64], si = ss[r64];
+        const float bi = sb[r64];
 #pragma unroll 1
         for (int cc = 0; cc < 2; ++cc) {
           const int col = 32 * wg + 16 * cc;
-          float g16[16], k16[16], kk[16];
+          float g16[16], k16[16], x[8];
           ld16f(tm, wwarp, TM_GB + col, g16);
           ld16f(tm, wwarp, TM_G + col, k16);
 #pragma unroll
-          for (int e = 0; e < 16; ++e) kk[e] = __shfl_xor_sync(0xffffffffu, k16[e], 16);
-          if (lo) {
+          for (int e = 0; e < 8; ++e) x[e] = __shfl_xor_sync(0xffffffffu, lo ? g16[8 + e] : k16[e], 16);
+          const int c8 = col + (lo ? 0 : 8);
+          float y[8];
 #pragma unroll
-            for (int g = 0; g < 2; ++g) {
-              float x[8];
-#pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                const int j = col + g * 8 + e;
-                const float gv = (j < r64) ? g16[g * 8 + e] : 0.f;
-                d2 = fmaf(gv * ss[j], kk[g * 8 + e], d2);
-                x[e] = bi * gv;
-              }
-              il_store8(sG1, C, r64, col + g * 8, x);
-            }
+          for (int e = 0; e < 8; ++e) {
+            const int j = c8 + e;
+            const float gr = lo ? g16[e] : x[e];
+            const float kk = lo ? x[e] : k16[8 + e];
+            const float gv = (j < r64) ? gr : 0.f;
+            d2 = fmaf(gv * ss[j], kk, d2);
+            y[e] = bi * gv;
           }
+          il_store8(sG1, C, r64, c8, y);
         }
-        if (lo) db2[wg * C + r64] = d2 * si;
+        d2 += __shfl_xor_sync(0xffffffffu, d2, 16);
+        if (lo) db2[wg * C + r64] = d2 * ss[r64];
       }
       simt_signal(&sg[SG_P7], tid);
       BSTAMP(13);
       if (wg == 0 && lo && t0 + r64 < L)
         dbeta[t0 + r64] = __float2bfloat16_rn(db1[r64] + db1[C + r64] + db2[r64] + db2[C + r64]);
-      {
-        // lanes >= 16: dq_hat row r64 (TM_DQ), this warpgroup's 64 columns;
-        // the row dot q_hat . dq_hat is combined across the warpgroups
-        float f[64];
-        ld64(tm, wwarp, TM_DK + 64 * wg, f);
-        float dot = 0.f;
-        if (!lo) {
-#pragma unroll
-          for (int g = 0; g < 8; ++g) {
-            float q8[8];
-            il_load8(sQ, C, r64, 64 * wg + g * 8, q8);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) dot = fmaf(q8[e], f[g * 8 + e], dot);
-          }
-          sdotq[wg * C + r64] = dot;
-        }
-        grp_sync<256>(BAR_SIMT);
-        if (!lo) {
-          dot = sdotq[r64] + sdotq[C + r64];
-          if (!(l2 && nq[r64] >= eps)) dot = 0.f;
-          const float inv = sr[r64];
-#pragma unroll
-          for (int g = 0; g < 8; ++g) {
-            float q8[8];
-            il_load8(sQ, C, r64, 64 * wg + g * 8, q8);
-#pragma unroll
-            for (int e = 0; e < 8; ++e)
-              q8[e] = l2 ? inv * (f[g * 8 + e] - q8[e] * dot) : f[g * 8 + e];
-            il_store8(sDQo, C, r64, 64 * wg + g * 8, q8);
-          }
-        }
-      }
-      simt_signal(&sg[SG_DQ], tid);
 
-      // ================= P8: dK epilogue (columns split; row dot combined)
+      // ================= P8: dq / dk epilogue (lanes >= 16: dq_hat row, lanes
+      // < 16: dk_hat row; columns split by warpgroup; row dots combined)
       mbar_wait(&mb[MB_K], ph);
       fence_after_sync();
       BSTAMP(14);
       {
         float f[64];
-        ld64(tm, wwarp, TM_DK + 64 * wg, f);  // lanes<16: dk_hat row r64
+        ld64(tm, wwarp, TM_DK + 64 * wg, f);
+        const uint8_t* tile = lo ? sK : sQ;
         float dot = 0.f;
-        if (lo) {
 #pragma unroll
-          for (int g = 0; g < 8; ++g) {
-            float k8[8];
-            il_load8(sK, C, r64, 64 * wg + g * 8, k8);
+        for (int g = 0; g < 8; ++g) {
+          float x8[8];
+          il_load8(tile, C, r64, 64 * wg + g * 8, x8);
 #pragma unroll
-            for (int e = 0; e < 8; ++e) dot = fmaf(k8[e], f[g * 8 + e], dot);
-          }
-          sdot[wg * C + r64] = dot;
+          for (int e = 0; e < 8; ++e) dot = fmaf(x8[e], f[g * 8 + e], dot);
         }
+        (lo ? sdot : sdotq)[wg * C + r64] = dot;
         grp_sync<256>(BAR_SIMT);
-        if (lo) {
-          dot = sdot[r64] + sdot[C + r64];
-          if (!(l2 && nk[r64] >= eps)) dot = 0.f;
-          const float inv = ss[r64];
+        const float* dd = lo ? sdot : sdotq;
+        dot = dd[r64] + dd[C + r64];
+        if (!(l2 && (lo ? nk : nq)[r64] >= eps)) dot = 0.f;
+        const float inv = (lo ? ss : sr)[r64];
+        uint8_t* out = lo ? sDKo : sDQo;
 #pragma unroll
-          for (int g = 0; g < 8; ++g) {
-            float k8[8];
-            il_load8(sK, C, r64, 64 * wg + g * 8, k8);
+        for (int g = 0; g < 8; ++g) {
+          float x8[8];
+          il_load8(tile, C, r64, 64 * wg + g * 8, x8);
 #pragma unroll
-            for (int e = 0; e < 8; ++e)
-              k8[e] = l2 ? inv * (f[g * 8 + e] - k8[e] * dot) : f[g * 8 + e];
-            il_store8(sDKo, C, r64, 64 * wg + g * 8, k8);
-          }
+          for (int e = 0; e < 8; ++e)
+            x8[e] = l2 ? inv * (f[g * 8 + e] - x8[e] * dot) : f[g * 8 + e];
+          il_store8(out, C, r64, 64 * wg + g * 8, x8);
         }
       }
       simt_signal(&sg[SG_P8], tid);

@@ -24,10 +24,11 @@ namespace tc {
 
 // Per-chunk record the tcgen05 forward writes (with DELTANET_SAVE_STATES)
 // for the backward, next to H_t: smem images of X = (I+L)^{-1} (bf16, IL
-// R=64 x 64, exactly lower-triangular), W^T (IL R=128 x 64) and
-// Z^T = (diag(s) U')^T (IL R=128 x 64).  Offsets in bytes.
-constexpr int REC_X = 0, REC_W = 64 * 64 * 2, REC_Z = REC_W + 128 * 64 * 2;
-constexpr int REC_BYTES = REC_Z + 128 * 64 * 2;  // 40 KB
+// R=64 x 64, exactly lower-triangular) and Z^T = (diag(s) U')^T (IL R=128 x
+// 64).  Offsets in bytes.  (W is not needed: the backward
+// uses W^T dU' = K_hat^T diag(beta) X^T dU' = K_hat^T dV.)
+constexpr int REC_X = 0, REC_Z = 64 * 64 * 2;
+constexpr int REC_BYTES = REC_Z + 128 * 64 * 2;  // 24 KB
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);

@@ -58,7 +58,7 @@ constexpr int OFF_VEC = OFF_L + C * LS * 4 + 2 * 128 * 4;  // (LX, partial norms
 constexpr int OFF_XB = OFF_VEC + 2 * 3 * C * 4;  // X bf16 IL R=64 x 64 (saved for the bwd)
 constexpr int SMEM_BYTES = OFF_XB + C * C * 2;
 static_assert(SMEM_BYTES <= 232448 - 1024, "shared memory budget");
-static_assert(REC_W == C * C * 2 && REC_BYTES == C * C * 2 + (DK + DV) * C * 2, "record");
+static_assert(REC_Z == C * C * 2 && REC_BYTES == C * C * 2 + DV * C * 2, "record");
 
 // TMEM column map (512 columns)
 constexpr uint32_t LO16 = 16u << 16;
@@ -326,10 +326,6 @@ __global__ void __launch_bounds__(NT, 1)
       grp_sync<NP>(BAR_P);
       if (tid == 0) {
         mbar_arrive(&w_free);
-        if (recs) {
-          bulk_store(recs + (size_t)c * REC_BYTES + REC_W, sW(b), DK * C * 2);
-          bulk_commit();
-        }
         mbar_wait(&wu_done, c & 1);  // U^T[b] complete before the chain uses it
         mbar_arrive(&bar_full[b]);
       }

@@ -95,11 +95,11 @@ def test_bwd_timeline(timlib):
                                 ws.data_ptr(), ws.numel(), None) == 0
     torch.cuda.synchronize()
     t = buf.cpu().numpy().reshape(NC, 32).astype(np.int64)
-    names = {0: "start", 1: "P1 loads + norms", 2: "G wait", 3: "P2 A_m",
-             4: "P3 U', q_hat, R wait", 5: "P3 R conv + dU wait", 6: "P3 dU' conv",
-             7: "P wait", 8: "P5 P, dV, dX", 9: "P5b dH image, k_hat", 10: "A wait",
-             11: "P6 dA, Y", 12: "Q wait", 13: "P7 G1, dbeta", 14: "dq epi + K wait",
-             15: "P8 dk"}
+    names = {0: "start", 1: "main wait + k norms", 2: "U' conv + R wait", 3: "R conv + Q wait",
+             4: "q norms + G wait", 5: "P2 A_m, q/k_hat, dU wait", 6: "P3 dU' conv",
+             7: "P wait", 8: "P5 P, dV, dX", 9: "P5b dH image", 10: "A wait",
+             11: "P6 dA, Y", 12: "G wait", 13: "P7 G1, dbeta", 14: "K wait",
+             15: "P8 dq/dk epilogue"}
     rows = []
     seq = list(range(16))
     for a_, b_ in zip(seq[:-1], seq[1:]):
@@ -109,7 +109,7 @@ def test_bwd_timeline(timlib):
     # issuer stamps (slots 16-29), relative to the SIMT chunk start (slot 0)
     inames = {16: "I main+dHimg rcv", 17: "I M1a issued", 18: "I Q rcv",
               19: "I M1b issued", 20: "I A rcv", 21: "I P3 rcv", 22: "I M3/M4 issued",
-              23: "I P5 rcv", 24: "I M5 issued", 25: "I P6 rcv", 26: "I M6 issued",
+              23: "I P5 rcv", 24: "I M5a+dQ issued", 25: "I P6 rcv", 26: "I M6 issued",
               27: "I P7 rcv"}
     for s_ in range(16, 28):
         dt = t[2:-2, s_] - t[2:-2, 0]

@@ -50,8 +50,8 @@ constexpr int TILE = C * D * 2;       // 16 KB
 constexpr int HALF_ROWS = 64 * 16;    // byte offset of row 64 in an IL R=128 tile
 
 // ---- shared memory map (bytes); regions reused by lifetime
-constexpr int OFF_Q = 0;                    // q (raw, then q_hat in place)
-constexpr int OFF_K = OFF_Q + TILE;         // 2 slots: k (raw, then k_hat), chunk parity
+constexpr int OFF_QU0 = 0;                  // QU slot 0 (see OFF_QU1)
+constexpr int OFF_K = OFF_QU0 + TILE;        // 2 slots: k (raw, then k_hat), chunk parity
 constexpr int OFF_DO = OFF_K + 2 * TILE;    // dO     IL R=64 x 128
 constexpr int OFF_V = OFF_DO + TILE;        // V -> dV staging
 constexpr int OFF_H = OFF_V + TILE;         // H^T    IL R=128 x 128
@@ -59,8 +59,10 @@ constexpr int OFF_DH = OFF_H + D * D * 2;   // dH^T   IL R=128 x 128
 constexpr int OFF_X = OFF_DH + D * D * 2;   // X      IL R=64 x 64 (record)
 constexpr int OFF_Z = OFF_X + C * C * 2;    // Z^T (record) -> U'^T in place
 constexpr int OFF_R = OFF_Z + TILE;         // R -> Y [0,8K) + G1 [8K,16K) -> dk staging
-constexpr int OFF_DUP = OFF_R + TILE;       // dU'^T -> dq staging
-constexpr int OFF_A = OFF_DUP + TILE;       // A_m -> dX -> dA
+// QU slots alternate by chunk parity: q (raw -> q_hat -> dq staging in place)
+// of chunk c in one, dU'^T of chunk c then q of chunk c-1 in the other
+constexpr int OFF_QU1 = OFF_R + TILE;
+constexpr int OFF_A = OFF_QU1 + TILE;       // A_m -> dX -> dA
 constexpr int OFF_VEC = OFF_A + C * C * 2;  // beta, r, s, nq, nk, db1[2], db2[2], dot[2], dotq[2], n2[4]
 constexpr int SMEM_BYTES = OFF_VEC + 17 * C * 4;
 static_assert(SMEM_BYTES <= 232448 - 1024, "shared memory budget");
@@ -136,16 +138,16 @@ __global__ void __launch_bounds__(NT, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mb[MB_N], sg[SG_N];
   __shared__ uint32_t tslot;
-  uint8_t *sQ = smem + OFF_Q, *sDO = smem + OFF_DO, *sV = smem + OFF_V, *sH = smem + OFF_H,
+  uint8_t *sDO = smem + OFF_DO, *sV = smem + OFF_V, *sH = smem + OFF_H,
           *sDH = smem + OFF_DH, *sX = smem + OFF_X, *sZ = smem + OFF_Z, *sR = smem + OFF_R,
-          *sDUP = smem + OFF_DUP, *sA = smem + OFF_A;
+          *sA = smem + OFF_A;
+  auto qu = [&](int slot) { return smem + (slot ? OFF_QU1 : OFF_QU0); };
   uint8_t* sUP = sZ;               // U'^T (converted in place from the record's Z^T)
   uint8_t* sDV = sV;               // dV staging (in place over V)
   uint8_t* sDX = sA;               // dX after M2
   uint8_t* sDA = sA;               // dA after M5
   uint8_t* sY = sR;                // after M3
   uint8_t* sG1 = sR + 8192;
-  uint8_t* sDQo = sDUP;            // dq staging after M6
   uint8_t* sDKo = sR;              // dk staging after M7
   float* sb = reinterpret_cast<float*>(smem + OFF_VEC);  // beta
   float* sr = sb + C;          // 1/max(||q||,eps) (0: padded)
@@ -211,15 +213,15 @@ __global__ void __launch_bounds__(NT, 1)
       auto load_x = [&](int c) {
         bulk_load(sX, recs + (size_t)c * REC_BYTES + REC_X, C * C * 2, &mb[MB_MAIN]);
       };
-      auto load_q = [&](int c) {
+      auto load_q = [&](int c, int slot) {
         mbar_expect_tx(&mb[MB_QL], TILE);
-        tma_load_4d(sQ, &mQ, 0, c * C, 0, unit, &mb[MB_QL]);
+        tma_load_4d(qu(slot), &mQ, 0, c * C, 0, unit, &mb[MB_QL]);
       };
       if (NC > 0) {
         load_k(NC - 1, 0);
         load_rest(NC - 1);
         load_x(NC - 1);
-        load_q(NC - 1);
+        load_q(NC - 1, 0);
       }
       mbar_arrive(&sg[SG_STG]);
 #pragma unroll 1
@@ -228,15 +230,18 @@ __global__ void __launch_bounds__(NT, 1)
         const uint32_t ph = it & 1;
         if (it > 0) {  // tail of chunk c+1: its epilogue read q_hat / k_hat
           mbar_wait(&sg[SG_P8], ph ^ 1);
-          tma_store_4d(&mDQ, sDQo, 0, t0 + C, 0, unit);
+          tma_store_4d(&mDQ, qu((it + 1) & 1), 0, t0 + C, 0, unit);  // dq in place over q_hat
           tma_store_4d(&mDK, sDKo, 0, t0 + C, 0, unit);
           bulk_commit();
-          load_q(c);
           if (c > 0) load_k(c - 1, (it + 1) & 1);  // the slot of chunk c+1
           bulk_wait_read0();  // dq / dk staging (DUP / R regions) read out
           mbar_arrive(&sg[SG_STG]);
         } else if (c > 0) {
           load_k(c - 1, 1);
+        }
+        if (c > 0) {  // q of chunk c-1 into the slot of dU'^T (last read by M3)
+          mbar_wait(&mb[MB_P], ph);
+          load_q(c - 1, (it + 1) & 1);
         }
         mbar_wait(&sg[SG_P5], ph);
         tma_store_4d(&mDV, sDV, 0, t0, 0, unit);
@@ -251,7 +256,7 @@ __global__ void __launch_bounds__(NT, 1)
       }
       if (NC > 0) {
         mbar_wait(&sg[SG_P8], (NC - 1) & 1);
-        tma_store_4d(&mDQ, sDQo, 0, 0, 0, unit);
+        tma_store_4d(&mDQ, qu((NC - 1) & 1), 0, 0, 0, unit);
         tma_store_4d(&mDK, sDKo, 0, 0, 0, unit);
         bulk_commit();
       }
@@ -265,9 +270,9 @@ __global__ void __launch_bounds__(NT, 1)
     // epilogues.
     // =====================================================================
     if (lane == 0) {
-      const uint32_t aQ = smem_u32(sQ), aDO = smem_u32(sDO), aH = smem_u32(sH),
+      const uint32_t aDO = smem_u32(sDO), aH = smem_u32(sH),
                      aDH = smem_u32(sDH), aX = smem_u32(sX), aA = smem_u32(sA),
-                     aDUP = smem_u32(sDUP), aR = smem_u32(sR), aDA = smem_u32(sDA),
+                     aR = smem_u32(sR), aDA = smem_u32(sDA),
                      aDX = smem_u32(sDX), aY = smem_u32(sY), aG1 = smem_u32(sG1),
                      aDV = smem_u32(sDV), aUP = smem_u32(sUP);
 #pragma unroll 1
@@ -275,6 +280,7 @@ __global__ void __launch_bounds__(NT, 1)
         const int ks = it & 1;
         const uint32_t ph = it & 1;
         const uint32_t aK = smem_u32(smem + OFF_K + ks * TILE);
+        const uint32_t aQ = smem_u32(qu(ks)), aDUP = smem_u32(qu(ks ^ 1));
 
         // M1a (raw k): K K^T | dH^T K^T | K H.  TMEM G / GB / KH were released
         // by the previous chunk's P7 / P5 (waited below in program order).
@@ -454,6 +460,8 @@ __global__ void __launch_bounds__(NT, 1)
       const int c = NC - 1 - it, t0 = c * C, ks = it & 1;
       const uint32_t ph = it & 1;
       uint8_t* sK = smem + OFF_K + ks * TILE;
+      uint8_t* sQ = qu(ks);         // q -> q_hat -> dq staging
+      uint8_t* sDUP = qu(ks ^ 1);   // dU'^T
 
       // ================= P1: k norms ; U' ; R = V - diag(s) K H ; q norms
       BSTAMP(0);
@@ -716,7 +724,7 @@ __global__ void __launch_bounds__(NT, 1)
         dot = dd[r64] + dd[C + r64];
         if (!(l2 && (lo ? nk : nq)[r64] >= eps)) dot = 0.f;
         const float inv = (lo ? ss : sr)[r64];
-        uint8_t* out = lo ? sDKo : sDQo;
+        uint8_t* out = lo ? sDKo : sQ;  // dq in place over q_hat (read above by this thread)
 #pragma unroll
         for (int g = 0; g < 8; ++g) {
           float x8[8];

@@ -27,7 +27,6 @@
 // epilogues; the row scales enter exactly in the conversions:
 //   A_m = tril(diag(r) Q K^T)  (M2 operand; A = A_m diag(s)),
 //   dU'^T = (dH^T K^T + dO^T A_m) diag(s),  R = V - diag(s) (K H),
-//   K_hat K_hat^T = diag(s) K K^T diag(s).
 // q and k are normalised in place afterwards for the remaining products.
 //
 // 320 threads: warps 0-7 run the SIMT phases (split by columns between the
@@ -69,7 +68,7 @@ static_assert(SMEM_BYTES <= 232448 - 1024, "shared memory budget");
 
 // ---- TMEM column map (512 columns)
 constexpr uint32_t TM_DH = 0;                            // dH^T, M=128
-constexpr uint32_t TM_G = 128;                           // Q K^T | K K^T (lane+16), raw
+constexpr uint32_t TM_G = 128;                           // raw Q K^T | K_hat K_hat^T (lane+16)
 constexpr uint32_t TM_DK = 192, TM_DQ = 192 | LO16;      // dK | dQ  (M=64, 128 cols)
 constexpr uint32_t TM_DU = 320;                          // dU'^T, M=128 (M1-P3)
 constexpr uint32_t TM_DX = 320, TM_GB = 320;             // dX' (M3-P5), G (M6-P7)
@@ -282,8 +281,8 @@ __global__ void __launch_bounds__(NT, 1)
         const uint32_t aK = smem_u32(smem + OFF_K + ks * TILE);
         const uint32_t aQ = smem_u32(qu(ks)), aDUP = smem_u32(qu(ks ^ 1));
 
-        // M1a (raw k): K K^T | dH^T K^T | K H.  TMEM G / GB / KH were released
-        // by the previous chunk's P7 / P5 (waited below in program order).
+        // M1a (raw k): dH^T K^T | K H.  TMEM DU / KH were released by the
+        // previous chunk's P7 / P5 (waited below in program order).
         mbar_wait(&mb[MB_KL0 + ks], (it >> 1) & 1);
         mbar_wait(&mb[MB_MAIN], ph);
         mbar_wait(&sg[SG_DHI], ph);
@@ -292,9 +291,6 @@ __global__ void __launch_bounds__(NT, 1)
         {
           const uint32_t idg = idesc_bf16(64, 64, false, false);
           const uint32_t idd = idesc_bf16(128, 64, false, false);
-#pragma unroll
-          for (int k0 = 0; k0 < D; k0 += 16)
-            mma_bf16(tm + TM_G + LO16, desc_k(aK, C, k0), desc_k(aK, C, k0), idg, k0 > 0);
 #pragma unroll
           for (int k0 = 0; k0 < D; k0 += 16)
             mma_bf16(tm + TM_DU, desc_k(aDH, D, k0), desc_k(aK, C, k0), idd, k0 > 0);
@@ -334,7 +330,7 @@ __global__ void __launch_bounds__(NT, 1)
         }
 
         // M3: P = X^T dU' (two N=64 halves), dX' = dU' R^T
-        // M4a: dH += Q_hat^T dO ; dK = U' dH^T (dH image of chunk c+1)
+        // M4a: dH += Q_hat^T dO ; dK = U' dH^T (dH image of chunk c+1) ; K_hat K_hat^T
         mbar_wait(&sg[SG_P3], ph);
         fence_after_sync();
         ISTAMP(21);
@@ -358,6 +354,11 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
           for (int k0 = 0; k0 < D; k0 += 16)
             mma_bf16(tm + TM_DK, desc_mn(aUP, D, k0), desc_mn(aDH, D, k0), id_k1, k0 > 0);
+          // K_hat K_hat^T (k normalised in P3) for the dbeta term of P7
+          const uint32_t idg = idesc_bf16(64, 64, false, false);
+#pragma unroll
+          for (int k0 = 0; k0 < D; k0 += 16)
+            mma_bf16(tm + TM_G + LO16, desc_k(aK, C, k0), desc_k(aK, C, k0), idg, k0 > 0);
         }
         ISTAMP(22);
 
@@ -455,6 +456,10 @@ __global__ void __launch_bounds__(NT, 1)
       simt_signal(&sg[SG_DHI], tid);
     }
 
+    // beta of the next chunk is read from global one chunk ahead
+    float bnext = (tid < C && NC > 0 && (NC - 1) * C + tid < L)
+                      ? __bfloat162float(beta[(NC - 1) * C + tid])
+                      : 0.f;
 #pragma unroll 1
     for (int it = 0; it < NC; ++it) {
       const int c = NC - 1 - it, t0 = c * C, ks = it & 1;
@@ -465,7 +470,7 @@ __global__ void __launch_bounds__(NT, 1)
 
       // ================= P1: k norms ; U' ; R = V - diag(s) K H ; q norms
       BSTAMP(0);
-      if (tid < C) sb[tid] = (t0 + tid < L) ? __bfloat162float(beta[t0 + tid]) : 0.f;
+      if (tid < C) sb[tid] = bnext;
       // squared row norms of a raw 64x128 tile: thread = (row w & 63, column
       // quarter wg * 2 + (w >> 6)), combined through n2
       auto row_norms = [&](const uint8_t* tile, float* inv_out, float* n_out) {
@@ -584,6 +589,7 @@ __global__ void __launch_bounds__(NT, 1)
       BSTAMP(6);
 
       // ================= P5: P, R -> dV, dbeta part ; dX
+      if (tid < C && c > 0) bnext = __bfloat162float(beta[t0 - C + tid]);
       mbar_wait(&mb[MB_P], ph);
       fence_after_sync();
       BSTAMP(7);
@@ -668,7 +674,7 @@ __global__ void __launch_bounds__(NT, 1)
       fence_after_sync();
       BSTAMP(12);
       {
-        // lanes < 16 hold the G row (TM_GB), lanes >= 16 the raw K K^T row
+        // lanes < 16 hold the G row (TM_GB), lanes >= 16 the K_hat K_hat^T row
         // (TM_G + 16); each lane pair splits every 16 columns 8 / 8
         float d2 = 0.f;
         const float bi = sb[r64];
@@ -688,13 +694,13 @@ __global__ void __launch_bounds__(NT, 1)
             const float gr = lo ? g16[e] : x[e];
             const float kk = lo ? x[e] : k16[8 + e];
             const float gv = (j < r64) ? gr : 0.f;
-            d2 = fmaf(gv * ss[j], kk, d2);
+            d2 = fmaf(gv, kk, d2);
             y[e] = bi * gv;
           }
           il_store8(sG1, C, r64, c8, y);
         }
         d2 += __shfl_xor_sync(0xffffffffu, d2, 16);
-        if (lo) db2[wg * C + r64] = d2 * ss[r64];
+        if (lo) db2[wg * C + r64] = d2;
       }
       simt_signal(&sg[SG_P7], tid);
       BSTAMP(13);

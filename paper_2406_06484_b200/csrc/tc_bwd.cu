@@ -57,7 +57,7 @@ constexpr int OFF_H = OFF_V + TILE;         // H^T    IL R=128 x 128
 constexpr int OFF_DH = OFF_H + D * D * 2;   // dH^T   IL R=128 x 128
 constexpr int OFF_X = OFF_DH + D * D * 2;   // X      IL R=64 x 64 (record)
 constexpr int OFF_Z = OFF_X + C * C * 2;    // Z^T (record) -> U'^T in place
-constexpr int OFF_R = OFF_Z + TILE;         // R -> Y [0,8K) + G1 [8K,16K) -> dk staging
+constexpr int OFF_R = OFF_Z + TILE;         // R -> Y [0,8K) + G1 [8K,16K)
 // QU slots alternate by chunk parity: q (raw -> q_hat -> dq staging in place)
 // of chunk c in one, dU'^T of chunk c then q of chunk c-1 in the other
 constexpr int OFF_QU1 = OFF_R + TILE;
@@ -147,7 +147,6 @@ __global__ void __launch_bounds__(NT, 1)
   uint8_t* sDA = sA;               // dA after M5
   uint8_t* sY = sR;                // after M3
   uint8_t* sG1 = sR + 8192;
-  uint8_t* sDKo = sR;              // dk staging after M7
   float* sb = reinterpret_cast<float*>(smem + OFF_VEC);  // beta
   float* sr = sb + C;          // 1/max(||q||,eps) (0: padded)
   float* ss = sr + C;          // 1/max(||k||,eps)
@@ -193,8 +192,8 @@ __global__ void __launch_bounds__(NT, 1)
     // TMA warp (lane 0): every load and store.  Chunk c-1's tiles are loaded
     // as their regions retire during chunk c: K at the start of chunk c
     // (double-buffered), dO / V / H / Z after M5 (MB_LD), X after G (MB_GB),
-    // Q after the chunk-c epilogue.  SG_STG tells the SIMT warps that the dq /
-    // dk staging regions have been read out.
+    // Q after M3 (into the dU'^T slot).  SG_STG tells the SIMT warps that the
+    // dq staging (the other q slot) has been read out.
     // =====================================================================
     if (lane == 0) {
       constexpr uint32_t MAIN_BYTES = 3 * TILE + D * D * 2 + C * C * 2;  // dO V Z | H | X
@@ -229,12 +228,13 @@ __global__ void __launch_bounds__(NT, 1)
         const uint32_t ph = it & 1;
         if (it > 0) {  // tail of chunk c+1: its epilogue read q_hat / k_hat
           mbar_wait(&sg[SG_P8], ph ^ 1);
-          tma_store_4d(&mDQ, qu((it + 1) & 1), 0, t0 + C, 0, unit);  // dq in place over q_hat
-          tma_store_4d(&mDK, sDKo, 0, t0 + C, 0, unit);
+          // dq / dk were staged in place over q_hat / k_hat of chunk c+1
+          tma_store_4d(&mDQ, qu((it + 1) & 1), 0, t0 + C, 0, unit);
+          tma_store_4d(&mDK, smem + OFF_K + ((it + 1) & 1) * TILE, 0, t0 + C, 0, unit);
           bulk_commit();
-          if (c > 0) load_k(c - 1, (it + 1) & 1);  // the slot of chunk c+1
-          bulk_wait_read0();  // dq / dk staging (DUP / R regions) read out
-          mbar_arrive(&sg[SG_STG]);
+          bulk_wait_read0();           // both read out: the q slot takes dU'^T (P3),
+          mbar_arrive(&sg[SG_STG]);    // the k slot chunk c-1's k
+          if (c > 0) load_k(c - 1, (it + 1) & 1);
         } else if (c > 0) {
           load_k(c - 1, 1);
         }
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(NT, 1)
       if (NC > 0) {
         mbar_wait(&sg[SG_P8], (NC - 1) & 1);
         tma_store_4d(&mDQ, qu((NC - 1) & 1), 0, 0, 0, unit);
-        tma_store_4d(&mDK, sDKo, 0, 0, 0, unit);
+        tma_store_4d(&mDK, smem + OFF_K + ((NC - 1) & 1) * TILE, 0, 0, 0, unit);
         bulk_commit();
       }
       bulk_wait0();
@@ -512,7 +512,6 @@ __global__ void __launch_bounds__(NT, 1)
           il_store8(sUP, D, w, col, z8);
         }
       }
-      mbar_wait(&sg[SG_STG], ph);  // R / DUP regions free (previous dq/dk stores read out)
       mbar_wait(&mb[MB_R], ph);
       fence_after_sync();
       BSTAMP(2);
@@ -574,6 +573,7 @@ __global__ void __launch_bounds__(NT, 1)
           il_store8(tile, C, row, g * 8, x);
         }
       }
+      mbar_wait(&sg[SG_STG], ph);  // the dU' slot (dq staging of chunk c+1) read out
       mbar_wait(&mb[MB_DU], ph);
       fence_after_sync();
       BSTAMP(5);
@@ -730,7 +730,7 @@ __global__ void __launch_bounds__(NT, 1)
         dot = dd[r64] + dd[C + r64];
         if (!(l2 && (lo ? nk : nq)[r64] >= eps)) dot = 0.f;
         const float inv = (lo ? ss : sr)[r64];
-        uint8_t* out = lo ? sDKo : sQ;  // dq in place over q_hat (read above by this thread)
+        uint8_t* out = lo ? sK : sQ;  // in place over k_hat / q_hat (read above by this thread)
 #pragma unroll
         for (int g = 0; g < 8; ++g) {
           float x8[8];

@@ -277,21 +277,76 @@ __device__ __forceinline__ void grp_sync(int id) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(NTH) : "memory");
 }
 
+// Warp-level tensor-core product D(16x8) += A(16x8) B(8x8), tf32 inputs
+// (cvt.rna from fp32), fp32 accumulate.  Fragments (g = lane/4, t = lane%4):
+// a = {A[g][t], A[g+8][t], A[g][t+4], A[g+8][t+4]}, b = {B[t][g], B[t+4][g]},
+// d = {D[g][2t], D[g][2t+1], D[g+8][2t], D[g+8][2t+1]}.
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ void mma_tf32_16x8x8(float (&d)[4], const float (&a)[4],
+                                                const float (&b)[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(to_tf32(a[0])), "r"(to_tf32(a[1])), "r"(to_tf32(a[2])), "r"(to_tf32(a[3])),
+        "r"(to_tf32(b[0])), "r"(to_tf32(b[1])));
+}
+
+// One 16x8 tile of P = A B (K = 8 * KSTEPS) from fp32 row-major smem, by one
+// warp.  A(r, k) = LX[(ar + r) * LS + ac + k], B(k, n) = LX[(br + k) * LS + bc + n];
+// a_lower / b_lower mask A / B to their lower triangle relative to the given
+// diagonal offsets (entries above it hold scratch).
+template <int LS, int KSTEPS>
+__device__ __forceinline__ void tile_mma(const float* LX, int ar, int ac, int br, int bc,
+                                         bool a_lower, int a_diag, bool b_lower, int b_diag,
+                                         int lane, float (&d)[4]) {
+  const int g = lane >> 2, t = lane & 3;
+  d[0] = d[1] = d[2] = d[3] = 0.f;
+#pragma unroll
+  for (int ks = 0; ks < KSTEPS; ++ks) {
+    const int k0 = 8 * ks;
+    float a[4], b[2];
+    a[0] = LX[(ar + g) * LS + ac + k0 + t];
+    a[1] = LX[(ar + g + 8) * LS + ac + k0 + t];
+    a[2] = LX[(ar + g) * LS + ac + k0 + t + 4];
+    a[3] = LX[(ar + g + 8) * LS + ac + k0 + t + 4];
+    b[0] = LX[(br + k0 + t) * LS + bc + g];
+    b[1] = LX[(br + k0 + t + 4) * LS + bc + g];
+    if (a_lower) {  // A(r, k) = 0 for k - r > a_diag
+      a[0] = (k0 + t - g <= a_diag) ? a[0] : 0.f;
+      a[1] = (k0 + t - g - 8 <= a_diag) ? a[1] : 0.f;
+      a[2] = (k0 + t + 4 - g <= a_diag) ? a[2] : 0.f;
+      a[3] = (k0 + t + 4 - g - 8 <= a_diag) ? a[3] : 0.f;
+    }
+    if (b_lower) {  // B(k, n) = 0 for n - k > b_diag
+      b[0] = (g - (k0 + t) <= b_diag) ? b[0] : 0.f;
+      b[1] = (g - (k0 + t + 4) <= b_diag) ? b[1] : 0.f;
+    }
+    mma_tf32_16x8x8(d, a, b);
+  }
+}
+
 // X = (I + L)^{-1} for a 64x64 strictly-lower L, in place in LX (fp32,
-// row stride LSTRIDE floats), by NTH (128 or 256) threads (wtid) that share
-// named barrier bar_id.
+// row stride LSTRIDE floats), by 256 threads (wtid) that share named barrier
+// bar_id.
 // Level 1: forward substitution on the four 16x16
 // diagonal blocks, one warp per block, column-parallel in registers.
-// Levels 2-3: merge blocks pairwise, X21 = -X22 (L21 X11), for 16 -> 32 -> 64.
+// Levels 2-3: merge blocks pairwise, X21 = -X22 (L21 X11), for 16 -> 32 -> 64,
+// as warp-level tf32 tensor-core products (mma.sync m16n8k8; R20:
+// tf32 operand rounding, 2^-11, is below the bf16 rounding X then gets).
 // On return the lower triangle and diagonal of LX hold X; entries above the
 // diagonal hold scratch (callers mask j > i).
-template <int LSTRIDE, int NTH = 128>
+template <int LSTRIDE, int NTH = 256>
 __device__ __forceinline__ void ut_inverse_inplace(float* LX, int wtid, int bar_id,
                                                    long long* stamps = nullptr) {
-  static_assert(NTH == 128 || NTH == 256, "thread count");
-  constexpr int R2 = 512 / NTH;  // level-2 rows per thread (2 pairs x 16 x 16 outputs)
-  constexpr int R3 = 1024 / NTH;  // level-3 rows per thread (32 x 32 outputs)
+  static_assert(NTH == 256, "the tensor-core merges assume 8 warps");
+  constexpr int LS = LSTRIDE;
   const int lane = wtid & 31, wwarp = wtid >> 5;
+  const int g = lane >> 2, t = lane & 3;
   if (wwarp < 4) {  // level 1: block q = wwarp, column j = lane (< 16)
     const int o = 16 * wwarp, j = lane & 15;
     // All loads first (branch-free, so they can all be in flight), then the
@@ -301,7 +356,7 @@ __device__ __forceinline__ void ut_inverse_inplace(float* LX, int wtid, int bar_
     for (int i = 1; i < 16; ++i)
 #pragma unroll
       for (int m = 0; m < i; m += 4)
-        l4[i][m / 4] = *reinterpret_cast<const float4*>(LX + (o + i) * LSTRIDE + o + m);
+        l4[i][m / 4] = *reinterpret_cast<const float4*>(LX + (o + i) * LS + o + m);
     float x[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
@@ -320,99 +375,55 @@ __device__ __forceinline__ void ut_inverse_inplace(float* LX, int wtid, int bar_
     __syncwarp();
     if (lane < 16) {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) LX[(o + i) * LSTRIDE + o + j] = x[i];
+      for (int i = 0; i < 16; ++i) LX[(o + i) * LS + o + j] = x[i];
     }
   }
   grp_sync<NTH>(bar_id);
   if (stamps && wtid == 0) stamps[0] = clock64();
-  {  // level 2, pairs p = 0, 1 at offset 32p: Y = L21 X11 -> LX[o:o+16][o+16:o+32]
-    const int half = NTH / 2;
-    const int o = 32 * (wtid / half), j = wtid & 15, i0 = ((wtid % half) >> 4) * R2;
-    float y[R2];
-#pragma unroll
-    for (int ii = 0; ii < R2; ++ii) y[ii] = 0.f;
-#pragma unroll
-    for (int m = 0; m < 16; m += 4) {
-      const float x0 = LX[(o + m + 0) * LSTRIDE + o + j], x1 = LX[(o + m + 1) * LSTRIDE + o + j],
-                  x2 = LX[(o + m + 2) * LSTRIDE + o + j], x3 = LX[(o + m + 3) * LSTRIDE + o + j];
-#pragma unroll
-      for (int ii = 0; ii < R2; ++ii) {
-        const float4 l4 =
-            *reinterpret_cast<const float4*>(LX + (o + 16 + i0 + ii) * LSTRIDE + o + m);
-        y[ii] = fmaf(l4.x, x0, fmaf(l4.y, x1, fmaf(l4.z, x2, fmaf(l4.w, x3, y[ii]))));
-      }
-    }
-#pragma unroll
-    for (int ii = 0; ii < R2; ++ii) LX[(o + i0 + ii) * LSTRIDE + o + 16 + j] = y[ii];
-    grp_sync<NTH>(bar_id);
-    if (stamps && wtid == 0) stamps[1] = clock64();
-    // X21 = -X22 Y -> LX[o+16:o+32][o:o+16]
-#pragma unroll
-    for (int ii = 0; ii < R2; ++ii) y[ii] = 0.f;
-#pragma unroll
-    for (int m = 0; m < 16; m += 4) {
-      const float y0 = LX[(o + m + 0) * LSTRIDE + o + 16 + j],
-                  y1 = LX[(o + m + 1) * LSTRIDE + o + 16 + j],
-                  y2 = LX[(o + m + 2) * LSTRIDE + o + 16 + j],
-                  y3 = LX[(o + m + 3) * LSTRIDE + o + 16 + j];
-#pragma unroll
-      for (int ii = 0; ii < R2; ++ii) {
-        const float4 x4 =
-            *reinterpret_cast<const float4*>(LX + (o + 16 + i0 + ii) * LSTRIDE + o + 16 + m);
-        y[ii] = fmaf(x4.x, y0, fmaf(x4.y, y1, fmaf(x4.z, y2, fmaf(x4.w, y3, y[ii]))));
-      }
-    }
-#pragma unroll
-    for (int ii = 0; ii < R2; ++ii) LX[(o + 16 + i0 + ii) * LSTRIDE + o + j] = -y[ii];
+  // level 2 (warps 0-3): pair p at offset o = 32p, column tile n0 = 8 * (w & 1)
+  const int o2 = 32 * ((wwarp >> 1) & 1), n2 = 8 * (wwarp & 1);
+  if (wwarp < 4) {  // Y = L21 X11 -> LX[o:o+16][o+16:o+32] (scratch)
+    float d[4];
+    // X11 is a level-1 block: zero above its diagonal, no mask needed
+    tile_mma<LS, 2>(LX, o2 + 16, o2, o2, o2 + n2, false, 0, false, 0, lane, d);
+    LX[(o2 + g) * LS + o2 + 16 + n2 + 2 * t] = d[0];
+    LX[(o2 + g) * LS + o2 + 16 + n2 + 2 * t + 1] = d[1];
+    LX[(o2 + g + 8) * LS + o2 + 16 + n2 + 2 * t] = d[2];
+    LX[(o2 + g + 8) * LS + o2 + 16 + n2 + 2 * t + 1] = d[3];
+  }
+  grp_sync<NTH>(bar_id);
+  if (stamps && wtid == 0) stamps[1] = clock64();
+  if (wwarp < 4) {  // X21 = -X22 Y -> LX[o+16:o+32][o:o+16]
+    float d[4];
+    tile_mma<LS, 2>(LX, o2 + 16, o2 + 16, o2, o2 + 16 + n2, true, 0, false, 0, lane, d);
+    LX[(o2 + 16 + g) * LS + o2 + n2 + 2 * t] = -d[0];
+    LX[(o2 + 16 + g) * LS + o2 + n2 + 2 * t + 1] = -d[1];
+    LX[(o2 + 16 + g + 8) * LS + o2 + n2 + 2 * t] = -d[2];
+    LX[(o2 + 16 + g + 8) * LS + o2 + n2 + 2 * t + 1] = -d[3];
   }
   grp_sync<NTH>(bar_id);
   if (stamps && wtid == 0) stamps[2] = clock64();
-  {  // level 3: Y = L21 X11 -> LX[0:32][32:64]
-    const int j = lane, i0 = wwarp * R3;
-    float y[R3];
-#pragma unroll
-    for (int ii = 0; ii < R3; ++ii) y[ii] = 0.f;
-#pragma unroll 2
-    for (int m = 0; m < 32; m += 4) {
-      // X11 is lower triangular; its upper-right 16x16 block holds level-2
-      // scratch, so entries above the diagonal are masked to zero.
-      const float x0 = LX[(m + 0) * LSTRIDE + j] * ((m + 0 >= j) ? 1.f : 0.f),
-                  x1 = LX[(m + 1) * LSTRIDE + j] * ((m + 1 >= j) ? 1.f : 0.f),
-                  x2 = LX[(m + 2) * LSTRIDE + j] * ((m + 2 >= j) ? 1.f : 0.f),
-                  x3 = LX[(m + 3) * LSTRIDE + j] * ((m + 3 >= j) ? 1.f : 0.f);
-#pragma unroll
-      for (int ii = 0; ii < R3; ++ii) {
-        const float4 l4 = *reinterpret_cast<const float4*>(LX + (32 + i0 + ii) * LSTRIDE + m);
-        y[ii] = fmaf(l4.x, x0, fmaf(l4.y, x1, fmaf(l4.z, x2, fmaf(l4.w, x3, y[ii]))));
-      }
-    }
-#pragma unroll
-    for (int ii = 0; ii < R3; ++ii) LX[(i0 + ii) * LSTRIDE + 32 + j] = y[ii];
+  // level 3 (8 warps): row tile r0 = 16 * (w >> 2), column tile n0 = 8 * (w & 3)
+  const int r3 = 16 * (wwarp >> 2), n3 = 8 * (wwarp & 3);
+  {  // Y = L21 X11 -> LX[0:32][32:64] (scratch)
+    float d[4];
+    // X11(m, j) = 0 for j > m (its upper-right block holds level-2 scratch)
+    tile_mma<LS, 4>(LX, 32 + r3, 0, 0, n3, false, 0, true, -n3, lane, d);
+    LX[(r3 + g) * LS + 32 + n3 + 2 * t] = d[0];
+    LX[(r3 + g) * LS + 32 + n3 + 2 * t + 1] = d[1];
+    LX[(r3 + g + 8) * LS + 32 + n3 + 2 * t] = d[2];
+    LX[(r3 + g + 8) * LS + 32 + n3 + 2 * t + 1] = d[3];
   }
   grp_sync<NTH>(bar_id);
   if (stamps && wtid == 0) stamps[3] = clock64();
   {  // X21 = -X22 Y -> LX[32:64][0:32]
-    const int j = lane, i0 = wwarp * R3;
-    float y[R3];
-#pragma unroll
-    for (int ii = 0; ii < R3; ++ii) y[ii] = 0.f;
-#pragma unroll 2
-    for (int m = 0; m < 32; m += 4) {
-      const float y0 = LX[(m + 0) * LSTRIDE + 32 + j], y1 = LX[(m + 1) * LSTRIDE + 32 + j],
-                  y2 = LX[(m + 2) * LSTRIDE + 32 + j], y3 = LX[(m + 3) * LSTRIDE + 32 + j];
-#pragma unroll
-      for (int ii = 0; ii < R3; ++ii) {
-        // X22 lower triangular (its upper-right 16x16 block holds scratch)
-        const int r = i0 + ii;
-        const float4 x4 =
-            *reinterpret_cast<const float4*>(LX + (32 + r) * LSTRIDE + 32 + m);
-        const float e0 = (m + 0 <= r) ? x4.x : 0.f, e1 = (m + 1 <= r) ? x4.y : 0.f,
-                    e2 = (m + 2 <= r) ? x4.z : 0.f, e3 = (m + 3 <= r) ? x4.w : 0.f;
-        y[ii] = fmaf(e0, y0, fmaf(e1, y1, fmaf(e2, y2, fmaf(e3, y3, y[ii]))));
-      }
-    }
-#pragma unroll
-    for (int ii = 0; ii < R3; ++ii) LX[(32 + i0 + ii) * LSTRIDE + j] = -y[ii];
+    float d[4];
+    // X22(i, m) = 0 for m > i (its upper-right block holds level-2 scratch)
+    tile_mma<LS, 4>(LX, 32 + r3, 32, 0, 32 + n3, true, r3, false, 0, lane, d);
+    LX[(32 + r3 + g) * LS + n3 + 2 * t] = -d[0];
+    LX[(32 + r3 + g) * LS + n3 + 2 * t + 1] = -d[1];
+    LX[(32 + r3 + g + 8) * LS + n3 + 2 * t] = -d[2];
+    LX[(32 + r3 + g + 8) * LS + n3 + 2 * t + 1] = -d[3];
   }
   grp_sync<NTH>(bar_id);
   if (stamps && wtid == 0) stamps[4] = clock64();

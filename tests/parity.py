@@ -6,6 +6,8 @@ err(x) = max|x - ref| / max|ref|; bar 1e-4 for fp32 I/O, 2e-2 for bf16 I/O.
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -67,6 +69,8 @@ def compare(got, ref, tol, keys=None):
         assert got[key].shape == ref[key].shape, (key, got[key].shape, ref[key].shape)
         assert np.isfinite(got[key]).all(), f"{key} has non-finite values"
         errs[key] = normwise(got[key], ref[key])
+    if os.environ.get("PARITY_VERBOSE") == "1":
+        print("\n  normwise:", {k: f"{e:.2e}" for k, e in errs.items()}, f"(bar {tol})")
     bad = {k: e for k, e in errs.items() if not e <= tol}
     assert not bad, f"normwise errors above {tol}: {bad} (all: {errs})"
     return errs

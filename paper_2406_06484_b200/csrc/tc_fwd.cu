@@ -112,7 +112,12 @@ __device__ long long* dn_tim = nullptr;
   } while (0)
 #define TSTAMP_PTR(slot) \
   ((dn_tim != nullptr && blockIdx.x == 0) ? dn_tim + (size_t)c * 32 + (slot) : nullptr)
+#define TSTAMP1(slot)                                                      \
+  do {                                                                     \
+    if (dn_tim != nullptr && blockIdx.x == 0) dn_tim[(size_t)c * 32 + (slot)] = clock64(); \
+  } while (0)
 #else
+#define TSTAMP1(slot) do { } while (0)
 #define TSTAMP(slot) do { } while (0)
 #define TSTAMP_PTR(slot) nullptr
 #endif
@@ -232,7 +237,9 @@ __global__ void __launch_bounds__(NT, 1)
           if (t0 + i >= L) inv = 0.f;  // padded token: exact zero contribution
           vb[C + i] = inv;
         }
+        TSTAMP(21);
         grp_sync<NP>(BAR_P);  // beta, s visible
+        TSTAMP(22);
         if (lane < 16) {  // A = tril(Q K^T), raw (inclusive, R4)
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
@@ -258,6 +265,7 @@ __global__ void __launch_bounds__(NT, 1)
           }
         }
       }
+      TSTAMP(23);
       fence_before_sync();
       grp_sync<NP>(BAR_P);
       DBG(dbg_smem(dn_dbg + D_L, LX, C, C, LS, w); dbg_tmem(dn_dbg + D_GQK, tm, TM_G, C, 64, w);
@@ -480,16 +488,26 @@ __global__ void __launch_bounds__(NT, 1)
       for (int c = 0; c < NC; ++c) {
         const int b = c & 1;
         const uint32_t ak = smem_u32(sK(b));
-        // the next chunk's Gram as soon as the prep has read this chunk's
-        // (it then runs under this chunk's substitution)
-        if (c + 1 < NC) {
-          mbar_wait(&g_free, c & 1);
-          gram(c + 1);
+        // the next chunk's Gram as soon as the prep has read this chunk's and
+        // q/k of chunk c+1 have landed (it then runs under this chunk's
+        // substitution) -- but never ahead of this chunk's W/U products: if
+        // T is ready first, the Gram waits until after them
+        bool gram_pending = c + 1 < NC;
+        if (gram_pending) mbar_wait(&g_free, c & 1);
+        while (true) {
+          if (gram_pending && mbar_test(&qk_full[(c + 1) & 1], ((c + 1) >> 1) & 1)) {
+            gram(c + 1);
+            gram_pending = false;
+          }
+          if (mbar_test(&t_ready, c & 1)) break;
         }
-        mbar_wait(&t_ready, c & 1);
+        TSTAMP1(24);
         if (c >= 1) mbar_wait(&w_free, (c - 1) & 1);
+        TSTAMP1(25);
         if (c >= 2) mbar_wait(&bar_empty[b], ((c >> 1) - 1) & 1);  // U[b] consumed
+        TSTAMP1(26);
         mbar_wait(&v_full[b], (c >> 1) & 1);
+        TSTAMP1(27);
         fence_after_sync();
 #pragma unroll
         for (int k0 = 0; k0 < C; k0 += 16)
@@ -499,6 +517,7 @@ __global__ void __launch_bounds__(NT, 1)
         for (int k0 = 0; k0 < C; k0 += 16)
           mma_bf16(tm + tm_u(b), desc_mn(av, C, k0), desc_k(atu, C, k0), idw, k0 > 0);
         mma_commit(&wu_done);
+        if (gram_pending) gram(c + 1);
         mbar_wait(&wu_done, c & 1);
         if (c + 1 < NC) {  // V (and T, T'') free again: prefetch the next chunk's V
           const int nb = (c + 1) & 1;

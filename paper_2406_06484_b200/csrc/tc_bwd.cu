@@ -114,9 +114,25 @@ __device__ long long* dn_tim_bwd = nullptr;
     if (dn_tim_bwd != nullptr && blockIdx.x == 0)                            \
       dn_tim_bwd[(size_t)it * 32 + (slot)] = clock64();                      \
   } while (0)
+// per-CTA [globaltimer start, end, smid] after the CTA-0 stamps
+#define CTA_STAMP(k, v)                                                      \
+  do {                                                                       \
+    if (dn_tim_bwd != nullptr) dn_tim_bwd[(size_t)a.NC * 32 + blockIdx.x * 4 + (k)] = (v); \
+  } while (0)
+__device__ __forceinline__ long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return (long long)t;
+}
+__device__ __forceinline__ long long smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+  return r;
+}
 #else
 #define BSTAMP(slot) do { } while (0)
 #define ISTAMP(slot) do { } while (0)
+#define CTA_STAMP(k, v) do { } while (0)
 #endif
 
 // SIMT -> issuer hand-off: operand tiles written by the 256 SIMT threads
@@ -173,6 +189,8 @@ __global__ void __launch_bounds__(NT, 1)
 
   if (warp == 0) tmem_alloc<512>(&tslot);
   if (tid == 0) {
+    CTA_STAMP(0, gtimer());
+    CTA_STAMP(2, smid());
     for (int i = 0; i < MB_N; ++i) mbar_init(&mb[i], 1);
     for (int i = 0; i < SG_N; ++i) mbar_init(&sg[i], 1);
     mbar_fence_init();
@@ -756,6 +774,7 @@ __global__ void __launch_bounds__(NT, 1)
     }
   }
   cta_sync();
+  if (tid == 0) CTA_STAMP(1, gtimer());
   if (warp == 0) tmem_dealloc<512>(tm);
 }
 

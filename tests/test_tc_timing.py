@@ -32,14 +32,15 @@ def test_fwd_timeline(timlib):
     import paper_2406_06484_b200 as dn
     lib = timlib
     cfg = synth.CONFIGS["target"]
-    x = synth.make_inputs(cfg, b_range=range(1))
+    B = int(os.environ.get("DN_TIMING_B", cfg.B))  # full bench batch: HBM contended
+    x = synth.make_inputs(cfg, b_range=range(B))
     td = torch.bfloat16
     q, k, v, b = (torch.from_numpy(x[f]).to(td).cuda() for f in ("q", "k", "v", "beta"))
     NC = cfg.L // 64
     buf = torch.zeros(NC * 32, dtype=torch.int64, device="cuda")
     lib.dn_timing_set.argtypes = [ctypes.c_void_p]
     assert lib.dn_timing_set(buf.data_ptr()) == 0
-    d = dn.make_desc(1, cfg.H, cfg.L, 128, 128, 64, td)
+    d = dn.make_desc(B, cfg.H, cfg.L, 128, 128, 64, td)
     ws = torch.empty(dn.deltanet_workspace_bytes(d), dtype=torch.uint8, device="cuda")
     o = torch.empty_like(v)
     P = ctypes.c_void_p
@@ -76,14 +77,15 @@ def test_bwd_timeline(timlib):
     import paper_2406_06484_b200 as dn
     lib = timlib
     cfg = synth.CONFIGS["target"]
-    x = synth.make_inputs(cfg, b_range=range(1))
+    B = int(os.environ.get("DN_TIMING_B", cfg.B))  # full bench batch: HBM contended
+    x = synth.make_inputs(cfg, b_range=range(B))
     td = torch.bfloat16
     q, k, v, b, dO = (torch.from_numpy(x[f]).to(td).cuda() for f in ("q", "k", "v", "beta", "dO"))
     NC = cfg.L // 64
-    buf = torch.zeros(NC * 32, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(NC * 32 + B * cfg.H * 4, dtype=torch.int64, device="cuda")
     lib.dn_timing_set_bwd.argtypes = [ctypes.c_void_p]
     assert lib.dn_timing_set_bwd(buf.data_ptr()) == 0
-    d = dn.make_desc(1, cfg.H, cfg.L, 128, 128, 64, td)
+    d = dn.make_desc(B, cfg.H, cfg.L, 128, 128, 64, td)
     ws = torch.empty(dn.deltanet_workspace_bytes(d), dtype=torch.uint8, device="cuda")
     o = torch.empty_like(v)
     g = [torch.empty_like(t) for t in (q, k, v, b)]
@@ -99,7 +101,14 @@ def test_bwd_timeline(timlib):
                                 g[1].data_ptr(), g[2].data_ptr(), g[3].data_ptr(), None,
                                 ws.data_ptr(), ws.numel(), None) == 0
     torch.cuda.synchronize()
-    t = buf.cpu().numpy().reshape(NC, 32).astype(np.int64)
+    allt = buf.cpu().numpy().astype(np.int64)
+    t = allt[:NC * 32].reshape(NC, 32)
+    cta = allt[NC * 32:].reshape(B * cfg.H, 4)
+    dur = (cta[:, 1] - cta[:, 0]) / 1e3
+    span = (cta[:, 1].max() - cta[:, 0].min()) / 1e3
+    print(f"\nper-CTA bwd duration us: min {dur.min():.1f} median {np.median(dur):.1f} "
+          f"max {dur.max():.1f}; kernel span {span:.1f} us; CTA 0 {dur[0]:.1f} us "
+          f"(SM {cta[0, 2]}); start skew {(cta[:, 0].max() - cta[:, 0].min()) / 1e3:.1f} us")
     names = {0: "start", 1: "main wait + k norms", 2: "U' conv + R wait", 3: "R conv + Q wait",
              4: "q norms + G wait", 5: "P2 A_m, q/k_hat, dU wait", 6: "P3 dU' conv",
              7: "P wait", 8: "P5 P, dV, dX", 9: "P5b dH image", 10: "A wait",

@@ -731,14 +731,18 @@ __global__ void __launch_bounds__(NT, 1)
       fence_after_sync();
       BSTAMP(14);
       {
+        // each thread keeps the bf16 chunks it read and overwrites exactly
+        // those (in-place staging)
         float f[64];
         ld64(tm, wwarp, TM_DK + 64 * wg, f);
-        const uint8_t* tile = lo ? sK : sQ;
+        uint8_t* tile = lo ? sK : sQ;
+        uint4 raw[8];
         float dot = 0.f;
 #pragma unroll
         for (int g = 0; g < 8; ++g) {
+          raw[g] = *reinterpret_cast<const uint4*>(tile + il_off(r64, 64 * wg + g * 8, C));
           float x8[8];
-          il_load8(tile, C, r64, 64 * wg + g * 8, x8);
+          unpack8(raw[g], x8);
 #pragma unroll
           for (int e = 0; e < 8; ++e) dot = fmaf(x8[e], f[g * 8 + e], dot);
         }
@@ -748,15 +752,14 @@ __global__ void __launch_bounds__(NT, 1)
         dot = dd[r64] + dd[C + r64];
         if (!(l2 && (lo ? nk : nq)[r64] >= eps)) dot = 0.f;
         const float inv = (lo ? ss : sr)[r64];
-        uint8_t* out = lo ? sK : sQ;  // in place over k_hat / q_hat (read above by this thread)
 #pragma unroll
         for (int g = 0; g < 8; ++g) {
           float x8[8];
-          il_load8(tile, C, r64, 64 * wg + g * 8, x8);
+          unpack8(raw[g], x8);
 #pragma unroll
           for (int e = 0; e < 8; ++e)
             x8[e] = l2 ? inv * (f[g * 8 + e] - x8[e] * dot) : f[g * 8 + e];
-          il_store8(out, C, r64, 64 * wg + g * 8, x8);
+          il_store8(tile, C, r64, 64 * wg + g * 8, x8);
         }
       }
       simt_signal(&sg[SG_P8], tid);

@@ -279,6 +279,17 @@ bool make_il_map(CUtensorMap* m, const void* base, int BH, int L, int D, int row
 namespace dn {
 namespace tc {
 
+// Unpack one 16 B chunk (8 bf16) to fp32.
+__device__ __forceinline__ void unpack8(const uint4& v, float* x) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    float2 f = __bfloat1622float2(h[e]);
+    x[2 * e] = f.x;
+    x[2 * e + 1] = f.y;
+  }
+}
+
 // Named barrier over one 128-thread warpgroup (ids 1.. ; 0 is __syncthreads).
 __device__ __forceinline__ void wg_sync(int id) {
   asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory");

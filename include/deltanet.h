@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define DELTANET_ABI_VERSION 1
+#define DELTANET_ABI_VERSION 2
 
 typedef enum {
   DELTANET_BF16 = 0, /* bf16 I/O, fp32 accumulation (BASELINE.json north_star) */
@@ -108,12 +108,25 @@ int deltanet_bwd(const deltanet_desc* d, const void* q, const void* k,
                  void* dv, void* dbeta, float* dh0, void* workspace,
                  size_t workspace_bytes, void* stream);
 
+/* Recurrent (token-by-token) form, for inference / decode:
+ * the delta rule of PAPER.md §2.2 applied one token at a time,
+ *   S_t = S_{t-1} - beta_t (S_{t-1} k_t - v_t) k_t^T,  o_t = S_t q_t,
+ * in the kernel orientation H = S^T, fp32 state, with q, k L2-normalised
+ * under DELTANET_L2NORM_QK.  Same tensors and layouts as
+ * deltanet_fwd; d->chunk is ignored and no workspace is used.  h0 nullable
+ * (zeros); hT nullable; h0 == hT is allowed (in-place state update, the
+ * decode loop).  No backward (inference only).  Same error codes. */
+int deltanet_recurrent_fwd(const deltanet_desc* d, const void* q,
+                           const void* k, const void* v, const void* beta,
+                           const float* h0, void* o, float* hT, void* stream);
+
 /* Which kernel family a descriptor dispatches to: 1 = tcgen05/TMEM/TMA
  * sm_100a path, 0 = CUDA-core (SIMT) path, -1 = unsupported descriptor. */
 int deltanet_path(const deltanet_desc* d);
 
-/* Number of kernel launches deltanet_fwd (which=0) or deltanet_bwd
- * (which=1) issues for this descriptor (for launch accounting). */
+/* Number of kernel launches deltanet_fwd (which=0), deltanet_bwd (which=1)
+ * or deltanet_recurrent_fwd (which=2) issues for this descriptor (for launch
+ * accounting). */
 int deltanet_launch_count(const deltanet_desc* d, int which);
 
 /* Human-readable message for an error code (static storage). */

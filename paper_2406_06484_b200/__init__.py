@@ -37,7 +37,8 @@ class deltanet_desc(ctypes.Structure):
 
 
 EXPORTED = ("deltanet_workspace_bytes", "deltanet_fwd", "deltanet_bwd", "deltanet_path",
-            "deltanet_launch_count", "deltanet_strerror", "deltanet_abi_version")
+            "deltanet_launch_count", "deltanet_strerror", "deltanet_abi_version",
+            "deltanet_recurrent_fwd")
 
 _lib = None
 
@@ -59,6 +60,8 @@ def load_library(path: str = LIB_PATH):
     lib.deltanet_fwd.restype = ctypes.c_int
     lib.deltanet_bwd.argtypes = [D, P, P, P, P, P, P, P, P, P, P, P, P, P, ctypes.c_size_t, P]
     lib.deltanet_bwd.restype = ctypes.c_int
+    lib.deltanet_recurrent_fwd.argtypes = [D, P, P, P, P, P, P, P, P]
+    lib.deltanet_recurrent_fwd.restype = ctypes.c_int
     lib.deltanet_path.argtypes = [D]
     lib.deltanet_path.restype = ctypes.c_int
     lib.deltanet_launch_count.argtypes = [D, ctypes.c_int]
@@ -157,6 +160,29 @@ def deltanet_fwd(q, k, v, beta, *, chunk=64, l2norm=True, h0=None, save_states=T
                           _ptr(o), _ptr(hT), _ptr(workspace), workspace.numel(), _stream(dev))
     _check(rc, "deltanet_fwd")
     return o, hT, workspace
+
+
+def deltanet_recurrent_fwd(q, k, v, beta, *, l2norm=True, h0=None, want_hT=True, eps=1e-6,
+                           out=None, hT=None):
+    """Recurrent (token-by-token) forward for inference / decode (PAPER.md
+    §2.2; include/deltanet.h deltanet_recurrent_fwd).  Passing
+    hT=h0 updates the state in place.  Returns (o, hT or None)."""
+    lib = load_library()
+    dev = q.device
+    for t, n in ((q, "q"), (k, "k"), (v, "v"), (beta, "beta")):
+        _need(t, n, q.dtype, dev)
+    _need(h0, "h0", torch.float32, dev)
+    _need(hT, "hT", torch.float32, dev)
+    B, H, L, Dk = q.shape
+    Dv = v.shape[-1]
+    d = make_desc(B, H, L, Dk, Dv, 64, q.dtype, l2norm=l2norm, eps=eps)
+    o = out if out is not None else torch.empty((B, H, L, Dv), dtype=q.dtype, device=dev)
+    if hT is None and want_hT:
+        hT = torch.empty((B, H, Dk, Dv), dtype=torch.float32, device=dev)
+    rc = lib.deltanet_recurrent_fwd(ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(beta),
+                                    _ptr(h0), _ptr(o), _ptr(hT), _stream(dev))
+    _check(rc, "deltanet_recurrent_fwd")
+    return o, hT
 
 
 def deltanet_bwd(q, k, v, beta, dO, *, chunk=64, l2norm=True, h0=None, dhT=None,

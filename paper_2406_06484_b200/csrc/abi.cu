@@ -22,6 +22,15 @@ int validate(const deltanet_desc* d) {
   return DELTANET_OK;
 }
 
+// the recurrent form has no chunk: only shapes and dtype are checked
+int validate_rec(const deltanet_desc* d) {
+  if (!d) return DELTANET_ERR_INVALID_ARG;
+  if (d->B < 0 || d->H < 0 || d->L < 0) return DELTANET_ERR_INVALID_ARG;
+  if (d->dtype != DELTANET_BF16 && d->dtype != DELTANET_FP32) return DELTANET_ERR_UNSUPPORTED;
+  if (!pow2_in(d->Dk, 16, 256) || !pow2_in(d->Dv, 16, 256)) return DELTANET_ERR_UNSUPPORTED;
+  return DELTANET_OK;
+}
+
 bool use_tc(const deltanet_desc* d) {
   return !(d->flags & DELTANET_FORCE_SIMT) && dn::tc_supported(d);
 }
@@ -68,6 +77,10 @@ int deltanet_path(const deltanet_desc* d) {
 }
 
 int deltanet_launch_count(const deltanet_desc* d, int which) {
+  if (which == 2) {  // deltanet_recurrent_fwd
+    if (validate_rec(d) != DELTANET_OK) return -1;
+    return (size_t)d->B * d->H == 0 ? 0 : 1;
+  }
   if (validate(d) != DELTANET_OK) return -1;
   if ((size_t)d->B * d->H == 0) return 0;
   if (use_tc(d)) return dn::tc_launch_count(d, which);
@@ -116,6 +129,26 @@ int deltanet_bwd(const deltanet_desc* d, const void* q, const void* k, const voi
   a.dq = dq; a.dk = dk; a.dv = dv; a.dbeta = dbeta; a.dh0 = dh0;
   cudaStream_t s = (cudaStream_t)stream;
   return use_tc(d) ? dn::tc_bwd(a, s) : dn::simt_bwd(a, d->dtype, s);
+}
+
+int deltanet_recurrent_fwd(const deltanet_desc* d, const void* q, const void* k, const void* v,
+                           const void* beta, const float* h0, void* o, float* hT,
+                           void* stream) {
+  int rc = validate_rec(d);
+  if (rc) return rc;
+  const size_t units = (size_t)d->B * d->H;
+  if (units && d->L > 0 && (!q || !k || !v || !beta || !o)) return DELTANET_ERR_INVALID_ARG;
+  if (misaligned(q) || misaligned(k) || misaligned(v) || misaligned(beta) || misaligned(h0) ||
+      misaligned(o) || misaligned(hT))
+    return DELTANET_ERR_MISALIGNED;
+  if (!units) return DELTANET_OK;
+  dn::Args a;
+  memset(&a, 0, sizeof a);
+  a.B = d->B; a.H = d->H; a.L = d->L; a.Dk = d->Dk; a.Dv = d->Dv;
+  a.flags = d->flags;
+  a.eps = d->l2_eps > 0.f ? d->l2_eps : 1e-6f;
+  a.q = q; a.k = k; a.v = v; a.beta = beta; a.h0 = h0; a.o = o; a.hT = hT;
+  return dn::rec_fwd(a, d->dtype, (cudaStream_t)stream);
 }
 
 const char* deltanet_strerror(int code) {

@@ -47,6 +47,9 @@ int simt_fwd(const Args& a, int dtype, cudaStream_t s);
 int simt_bwd(const Args& a, int dtype, cudaStream_t s);
 size_t simt_scratch_floats_per_unit(int L, int Dk, int Dv, int C);
 
+// recurrent (token-by-token) inference path (recurrent.cu)
+int rec_fwd(const Args& a, int dtype, cudaStream_t s);
+
 // tcgen05 path entry points (tc_fwd.cu / tc_bwd.cu)
 bool tc_supported(const deltanet_desc* d);
 size_t tc_scratch_bytes(const deltanet_desc* d);

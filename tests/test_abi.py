@@ -44,7 +44,7 @@ def test_no_torch_types_in_abi():
 
 
 def test_abi_version_and_strerror(lib):
-    assert lib.deltanet_abi_version() == 1
+    assert lib.deltanet_abi_version() == 2
     for code in range(6):
         assert dn.deltanet_strerror(code)
     assert "unknown" in dn.deltanet_strerror(99)
@@ -98,3 +98,20 @@ def test_binding_refuses_cpu_tensors(lib):
     q = torch.zeros(1, 1, 16, 16)
     with pytest.raises(dn.DeltaNetError):
         dn.deltanet_fwd(q, q, q, torch.zeros(1, 1, 16), chunk=16)
+
+
+def test_recurrent_errors_before_launch(lib):
+    """deltanet_recurrent_fwd validates shapes/dtype (not chunk) before any launch."""
+    D = ctypes.byref
+    nul = None
+    a = ctypes.c_void_p(16 * 1024)
+    p = ctypes.c_void_p(16 * 1024 + 4)
+    assert lib.deltanet_recurrent_fwd(D(_desc()), nul, nul, nul, nul, nul, nul, nul, nul) == 1
+    assert lib.deltanet_recurrent_fwd(D(_desc(Dk=48)), a, a, a, a, nul, a, nul, nul) == 2
+    assert lib.deltanet_recurrent_fwd(D(_desc(dtype=7)), a, a, a, a, nul, a, nul, nul) == 2
+    assert lib.deltanet_recurrent_fwd(D(_desc()), p, a, a, a, nul, a, nul, nul) == 3
+    # chunk is not part of the recurrent form: an invalid chunk is not an error
+    assert dn.deltanet_launch_count(_desc(chunk=8), 2) == 1
+    assert dn.deltanet_launch_count(_desc(B=0), 2) == 0
+    e = _desc(B=0)
+    assert lib.deltanet_recurrent_fwd(D(e), nul, nul, nul, nul, nul, nul, nul, nul) == 0

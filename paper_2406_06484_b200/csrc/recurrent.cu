@@ -87,9 +87,11 @@ __global__ void __launch_bounds__(256) rec_fwd_kernel(Args a, int VB) {
       __syncthreads();
     }
     if (col < VB) {
-      for (int t = 0; t < nt; ++t) {
-        const float* kr = sk + t * S::KS + S::idx(seg * S::RPT);
-        const float* qr = sq + t * S::KS + S::idx(seg * S::RPT);
+      // u_t = k_t . h before token t's update; one fused pass per token then
+      // applies the update and forms o_t = q_t . h and u_{t+1} = k_{t+1} . h
+      float u;
+      {
+        const float* kr = sk + S::idx(seg * S::RPT);
         float u0 = 0.f, u1 = 0.f, u2 = 0.f, u3 = 0.f;
 #pragma unroll
         for (int r = 0; r < S::RPT; r += 4) {
@@ -99,15 +101,21 @@ __global__ void __launch_bounds__(256) rec_fwd_kernel(Args a, int VB) {
           u2 = fmaf(k4.z, h[r + 2], u2);
           u3 = fmaf(k4.w, h[r + 3], u3);
         }
-        float u = (u0 + u1) + (u2 + u3);
+        u = (u0 + u1) + (u2 + u3);
 #pragma unroll
         for (int m = 1; m < S::TPC; m <<= 1) u += __shfl_xor_sync(0xffffffffu, u, m);
+      }
+      for (int t = 0; t < nt; ++t) {
+        const float* kr = sk + t * S::KS + S::idx(seg * S::RPT);
+        const float* qr = sq + t * S::KS + S::idx(seg * S::RPT);
+        const float* kn = (t + 1 < nt) ? kr + S::KS : kr;  // k_{t+1} (dummy at the block end)
         const float cc = sb[t] * (u - sv[t * VB + col]);
-        float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
+        float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f, n0 = 0.f, n1 = 0.f, n2 = 0.f, n3 = 0.f;
 #pragma unroll
         for (int r = 0; r < S::RPT; r += 4) {
           const float4 k4 = *reinterpret_cast<const float4*>(kr + r);
           const float4 q4 = *reinterpret_cast<const float4*>(qr + r);
+          const float4 n4 = *reinterpret_cast<const float4*>(kn + r);
           h[r] = fmaf(-cc, k4.x, h[r]);
           h[r + 1] = fmaf(-cc, k4.y, h[r + 1]);
           h[r + 2] = fmaf(-cc, k4.z, h[r + 2]);
@@ -116,10 +124,18 @@ __global__ void __launch_bounds__(256) rec_fwd_kernel(Args a, int VB) {
           o1 = fmaf(q4.y, h[r + 1], o1);
           o2 = fmaf(q4.z, h[r + 2], o2);
           o3 = fmaf(q4.w, h[r + 3], o3);
+          n0 = fmaf(n4.x, h[r], n0);
+          n1 = fmaf(n4.y, h[r + 1], n1);
+          n2 = fmaf(n4.z, h[r + 2], n2);
+          n3 = fmaf(n4.w, h[r + 3], n3);
         }
         float ov = (o0 + o1) + (o2 + o3);
+        u = (n0 + n1) + (n2 + n3);
 #pragma unroll
-        for (int m = 1; m < S::TPC; m <<= 1) ov += __shfl_xor_sync(0xffffffffu, ov, m);
+        for (int m = 1; m < S::TPC; m <<= 1) {
+          ov += __shfl_xor_sync(0xffffffffu, ov, m);
+          u += __shfl_xor_sync(0xffffffffu, u, m);
+        }
         if (seg == 0) so[t * VB + col] = ov;
       }
     }

@@ -278,8 +278,10 @@ __global__ void __launch_bounds__(NT, 1)
       DBG(dbg_smem(dn_dbg + D_X, LX, C, C, LS, w));
       {
         // T'[i][j] = X[i][j] beta_j s_j, T''[i][j] = X[i][j] beta_j  (j <= i).
+        // (T' / T'' of chunk c-1 are free once its W/U products completed.)
         // Lanes map to consecutive rows (conflict-free IL stores); each thread
         // handles one 16-column quarter of its row.
+        if (c >= 1) mbar_wait(&wu_done, (c - 1) & 1);
         const int i = tid & 63, j0 = (tid >> 6) * 16;
         float4 x4[4];
 #pragma unroll
@@ -311,32 +313,7 @@ __global__ void __launch_bounds__(NT, 1)
         }
       }
       TSTAMP(6);
-      mbar_wait(&w_done, c & 1);
-      fence_after_sync();
       TSTAMP(7);
-      DBG(dbg_tmem(dn_dbg + D_W, tm, TM_W, C, 128, w); dbg_tmem(dn_dbg + D_U, tm, tm_u(b), C, 128, w));
-      {  // W^T (lane = dk) -> bf16 IL tile (row dk, cols = tokens), this half's columns
-        uint32_t r[2][16];
-        tmem_ld16(taddr(tm, wwarp * 32, TM_W + 32 * half), r[0]);
-        tmem_ld16(taddr(tm, wwarp * 32, TM_W + 32 * half + 16), r[1]);
-        tmem_ld_wait();
-        float f[32];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          f[e] = __uint_as_float(r[0][e]);
-          f[16 + e] = __uint_as_float(r[1][e]);
-        }
-#pragma unroll
-        for (int g = 0; g < 4; ++g) il_store8(sW(b), DK, w, 32 * half + g * 8, f + g * 8);
-      }
-      fence_proxy_async();
-      fence_before_sync();
-      grp_sync<NP>(BAR_P);
-      if (tid == 0) {
-        mbar_arrive(&w_free);
-        mbar_wait(&wu_done, c & 1);  // U^T[b] complete before the chain uses it
-        mbar_arrive(&bar_full[b]);
-      }
       TSTAMP(8);
     }
   } else if (warp < 12) {
@@ -370,7 +347,27 @@ __global__ void __launch_bounds__(NT, 1)
       const int b = c & 1;
       const float* vb = vec(b);
       TSTAMP(16);
-      mbar_wait(&bar_full[b], (c >> 1) & 1);
+      // W^T of this chunk (lane = dk) -> bf16 IL tile sW(b) (row dk, cols =
+      // tokens); the prep warps only hand over T (t_ready), so the W/U
+      // products and this conversion are off the prep's critical path
+      mbar_wait(&w_done, c & 1);
+      fence_after_sync();
+      {
+        float f[64];
+        ld64(tm, wwarp, TM_W, f);
+#pragma unroll
+        for (int g = 0; g < 8; ++g) il_store8(sW(b), DK, w, g * 8, f + g * 8);
+      }
+      fence_proxy_async();
+      fence_before_sync();
+      wg_sync(BAR_S);
+      if (w == 0) {
+        // U^T[b] complete before the chain uses it; waited before w_free is
+        // released so that wu_done cannot run a phase ahead of this wait
+        mbar_wait(&wu_done, c & 1);
+        mbar_arrive(&w_free);
+        mbar_arrive(&bar_full[b]);
+      }
       // r_i = 1/max(||q_i||, eps) for this lane's output row (R9): partial sums
       // of squares over column halves (thread w: row w & 63, half w >> 6)
       float ri;

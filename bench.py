@@ -186,6 +186,46 @@ def measure_recurrent(dn, dev, q, k, v, beta, t_fwd_chunk, peaks):
             "decode": decode}
 
 
+def measure_prologue(dn, dev, B, H, L, D, peaks):
+    """Side measurement (outside the timed step) of the layer prologue
+    (SURVEY §8(f) f1): short conv + SiLU + sigmoid + layout change, forward
+    and backward, on the step's shapes; HBM-bound (bytes = tensors read and
+    written once)."""
+    import torch
+    stream = torch.cuda.current_stream(dev)
+    g = torch.Generator(device=dev).manual_seed(11)
+    xs = [torch.randn((B, L, H, D), device=dev, generator=g).to(torch.bfloat16) for _ in range(3)]
+    xb = torch.randn((B, L, H), device=dev, generator=g).to(torch.bfloat16)
+    ws = [0.5 * torch.randn((H * D, 4), device=dev, generator=g) for _ in range(3)]
+    outs = dn.deltanet_prologue_fwd(*xs, xb, *ws)
+    gr = [torch.randn_like(t) for t in outs]
+    gouts = dn.deltanet_prologue_bwd(*xs, xb, *ws, *gr)
+
+    def timed(fn, reps=10):
+        fn()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1) * 1e-3 / reps
+
+    nb = lambda ts: sum(t.numel() * t.element_size() for t in ts)
+    t_f = timed(lambda: dn.deltanet_prologue_fwd(*xs, xb, *ws, out=outs))
+    t_b = timed(lambda: dn.deltanet_prologue_bwd(*xs, xb, *ws, *gr, out=gouts))
+    bf = nb(xs) + nb([xb]) + nb(outs)
+    bb = nb(xs) + nb([xb]) + nb(gr) + nb(gouts[:4])
+    roof = lambda by, t: {"bound": "hbm", "achieved": by / t / 1e9, "peak": peaks["hbm_gbs"],
+                          "unit": "GB/s", "frac": by / t / 1e9 / peaks["hbm_gbs"],
+                          "bytes": by}
+    return {"kernel": "deltanet_prologue_fwd / _bwd (short conv 4 + SiLU + sigmoid + layout)",
+            "workload": f"B={B} H={H} L={L} d={D} bf16",
+            "fwd_ms": t_f * 1e3, "bwd_ms": t_b * 1e3,
+            "fwd_roofline": roof(bf, t_f), "bwd_roofline": roof(bb, t_b)}
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -450,9 +490,10 @@ def main():
     base = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         base = cpu_baseline()
-    rec = None
+    rec = pro = None
     if rank == 0 and not args.no_recurrent and not args.force_simt:
         rec = measure_recurrent(dn, dev, q, k, v, beta, t_fwd, peaks)
+        pro = measure_prologue(dn, dev, B_PER_RANK, H, L, D, peaks)
 
     if rank == 0:
         line = {
@@ -478,6 +519,8 @@ def main():
             line["gather"] = gather
         if rec:
             line["recurrent"] = rec
+        if pro:
+            line["prologue"] = pro
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.barrier()

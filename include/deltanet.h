@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define DELTANET_ABI_VERSION 2
+#define DELTANET_ABI_VERSION 3
 
 typedef enum {
   DELTANET_BF16 = 0, /* bf16 I/O, fp32 accumulation (BASELINE.json north_star) */
@@ -63,7 +63,10 @@ enum {
   DELTANET_SAVE_STATES = 1u << 1,
   /* debug: force the generic CUDA-core path even where the tcgen05 path
    * applies (both are CUDA kernels; there is no CPU fallback). */
-  DELTANET_FORCE_SIMT = 1u << 2
+  DELTANET_FORCE_SIMT = 1u << 2,
+  /* layer prologue only: SiLU on v as well (the paper states SiLU for q, k
+   * only; R22) */
+  DELTANET_PROLOGUE_SILU_V = 1u << 3
 };
 
 typedef struct {
@@ -120,13 +123,46 @@ int deltanet_recurrent_fwd(const deltanet_desc* d, const void* q,
                            const void* k, const void* v, const void* beta,
                            const float* h0, void* o, float* hT, void* stream);
 
+/* Layer prologue: the steps in front of the chunkwise
+ * kernel in a DeltaNet layer.  After the q/k/v projections a causal depthwise
+ * short convolution of width 4 (§3.4), the SiLU
+ * feature map on q and k (their L2 normalisation is fused into the
+ * chunkwise kernels), beta = sigmoid(W_beta x):
+ *   y[t] = sum_{j<4} w[c][j] x[t-3+j]  (x[t<0] = 0);  q = SiLU(y_q),
+ *   k = SiLU(y_k), v = y_v (SiLU too with DELTANET_PROLOGUE_SILU_V),
+ *   beta = sigmoid(xb).
+ * Inputs in the projections' token-major layout: xq, xk [B, L, H, Dk],
+ * xv [B, L, H, Dv], xb [B, L, H] (I/O dtype); weights wq, wk [H*Dk][4],
+ * wv [H*Dv][4] fp32 (channel c = h*D + d).  Outputs in the deltanet_fwd
+ * layout: q, k [B,H,L,Dk], v [B,H,L,Dv], beta [B,H,L].  d->chunk ignored. */
+int deltanet_prologue_fwd(const deltanet_desc* d, const void* xq,
+                          const void* xk, const void* xv, const void* xb,
+                          const float* wq, const float* wk, const float* wv,
+                          void* q, void* k, void* v, void* beta, void* stream);
+
+/* Device workspace deltanet_prologue_bwd needs (per-block partial sums of
+ * the weight gradients; 0 for an invalid descriptor). */
+size_t deltanet_prologue_workspace_bytes(const deltanet_desc* d);
+
+/* Backward of the prologue: dq, dk, dv, dbeta are the cotangents of its
+ * outputs (what deltanet_bwd returns); writes dxq, dxk, dxv, dxb (layouts of
+ * xq ... xb) and overwrites dwq, dwk, dwv (fp32, reduced over B and L in a
+ * fixed order: deterministic). */
+int deltanet_prologue_bwd(const deltanet_desc* d, const void* xq,
+                          const void* xk, const void* xv, const void* xb,
+                          const float* wq, const float* wk, const float* wv,
+                          const void* dq, const void* dk, const void* dv,
+                          const void* dbeta, void* dxq, void* dxk, void* dxv,
+                          void* dxb, float* dwq, float* dwk, float* dwv,
+                          void* workspace, size_t workspace_bytes, void* stream);
+
 /* Which kernel family a descriptor dispatches to: 1 = tcgen05/TMEM/TMA
  * sm_100a path, 0 = CUDA-core (SIMT) path, -1 = unsupported descriptor. */
 int deltanet_path(const deltanet_desc* d);
 
-/* Number of kernel launches deltanet_fwd (which=0), deltanet_bwd (which=1)
- * or deltanet_recurrent_fwd (which=2) issues for this descriptor (for launch
- * accounting). */
+/* Number of kernel launches deltanet_fwd (which=0), deltanet_bwd (which=1),
+ * deltanet_recurrent_fwd (2), deltanet_prologue_fwd (3) or
+ * deltanet_prologue_bwd (4) issues for this descriptor (launch accounting). */
 int deltanet_launch_count(const deltanet_desc* d, int which);
 
 /* Human-readable message for an error code (static storage). */

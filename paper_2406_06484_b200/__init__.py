@@ -26,6 +26,7 @@ DELTANET_BF16 = 0
 DELTANET_FP32 = 1
 DELTANET_L2NORM_QK = 1 << 0
 DELTANET_SAVE_STATES = 1 << 1
+DELTANET_PROLOGUE_SILU_V = 1 << 3
 DELTANET_FORCE_SIMT = 1 << 2
 
 
@@ -38,7 +39,8 @@ class deltanet_desc(ctypes.Structure):
 
 EXPORTED = ("deltanet_workspace_bytes", "deltanet_fwd", "deltanet_bwd", "deltanet_path",
             "deltanet_launch_count", "deltanet_strerror", "deltanet_abi_version",
-            "deltanet_recurrent_fwd")
+            "deltanet_recurrent_fwd", "deltanet_prologue_fwd", "deltanet_prologue_bwd",
+            "deltanet_prologue_workspace_bytes")
 
 _lib = None
 
@@ -62,6 +64,12 @@ def load_library(path: str = LIB_PATH):
     lib.deltanet_bwd.restype = ctypes.c_int
     lib.deltanet_recurrent_fwd.argtypes = [D, P, P, P, P, P, P, P, P]
     lib.deltanet_recurrent_fwd.restype = ctypes.c_int
+    lib.deltanet_prologue_fwd.argtypes = [D] + [P] * 12
+    lib.deltanet_prologue_fwd.restype = ctypes.c_int
+    lib.deltanet_prologue_bwd.argtypes = [D] + [P] * 19 + [ctypes.c_size_t, P]
+    lib.deltanet_prologue_bwd.restype = ctypes.c_int
+    lib.deltanet_prologue_workspace_bytes.argtypes = [D]
+    lib.deltanet_prologue_workspace_bytes.restype = ctypes.c_size_t
     lib.deltanet_path.argtypes = [D]
     lib.deltanet_path.restype = ctypes.c_int
     lib.deltanet_launch_count.argtypes = [D, ctypes.c_int]
@@ -183,6 +191,63 @@ def deltanet_recurrent_fwd(q, k, v, beta, *, l2norm=True, h0=None, want_hT=True,
                                     _ptr(h0), _ptr(o), _ptr(hT), _stream(dev))
     _check(rc, "deltanet_recurrent_fwd")
     return o, hT
+
+
+def _prologue_desc(xq, xv, silu_v):
+    B, L, H, Dk = xq.shape
+    Dv = xv.shape[-1]
+    d = make_desc(B, H, L, Dk, Dv, 64, xq.dtype, l2norm=False, save_states=False)
+    if silu_v:
+        d.flags |= DELTANET_PROLOGUE_SILU_V
+    return d
+
+
+def deltanet_prologue_fwd(xq, xk, xv, xb, wq, wk, wv, *, silu_v=False, out=None):
+    """Layer prologue (include/deltanet.h deltanet_prologue_fwd; PAPER.md
+    P:96): short causal conv (width 4) + SiLU on
+    q, k, sigmoid on beta, [B, L, H, D] -> [B, H, L, D].  Returns (q, k, v, beta)."""
+    lib = load_library()
+    dev = xq.device
+    for t, n in ((xq, "xq"), (xk, "xk"), (xv, "xv"), (xb, "xb")):
+        _need(t, n, xq.dtype, dev)
+    for t, n in ((wq, "wq"), (wk, "wk"), (wv, "wv")):
+        _need(t, n, torch.float32, dev)
+    B, L, H, Dk = xq.shape
+    Dv = xv.shape[-1]
+    d = _prologue_desc(xq, xv, silu_v)
+    if out is None:
+        out = (torch.empty((B, H, L, Dk), dtype=xq.dtype, device=dev),
+               torch.empty((B, H, L, Dk), dtype=xq.dtype, device=dev),
+               torch.empty((B, H, L, Dv), dtype=xq.dtype, device=dev),
+               torch.empty((B, H, L), dtype=xq.dtype, device=dev))
+    rc = lib.deltanet_prologue_fwd(ctypes.byref(d), _ptr(xq), _ptr(xk), _ptr(xv), _ptr(xb),
+                                   _ptr(wq), _ptr(wk), _ptr(wv), *[_ptr(t) for t in out],
+                                   _stream(dev))
+    _check(rc, "deltanet_prologue_fwd")
+    return out
+
+
+def deltanet_prologue_bwd(xq, xk, xv, xb, wq, wk, wv, dq, dk, dv, dbeta, *, silu_v=False,
+                          workspace=None, out=None):
+    """Backward of the prologue: returns (dxq, dxk, dxv, dxb, dwq, dwk, dwv)."""
+    lib = load_library()
+    dev = xq.device
+    for t, n in ((dq, "dq"), (dk, "dk"), (dv, "dv"), (dbeta, "dbeta")):
+        _need(t, n, xq.dtype, dev)
+    d = _prologue_desc(xq, xv, silu_v)
+    if workspace is None:
+        n = int(lib.deltanet_prologue_workspace_bytes(ctypes.byref(d)))
+        workspace = torch.empty(max(n, 16), dtype=torch.uint8, device=dev)
+    if out is None:
+        out = (torch.empty_like(xq), torch.empty_like(xk), torch.empty_like(xv),
+               torch.empty_like(xb), torch.empty_like(wq), torch.empty_like(wk),
+               torch.empty_like(wv))
+    rc = lib.deltanet_prologue_bwd(ctypes.byref(d), _ptr(xq), _ptr(xk), _ptr(xv), _ptr(xb),
+                                   _ptr(wq), _ptr(wk), _ptr(wv), _ptr(dq), _ptr(dk), _ptr(dv),
+                                   _ptr(dbeta), *[_ptr(t) for t in out], _ptr(workspace),
+                                   workspace.numel(), _stream(dev))
+    _check(rc, "deltanet_prologue_bwd")
+    return out
 
 
 def deltanet_bwd(q, k, v, beta, dO, *, chunk=64, l2norm=True, h0=None, dhT=None,

@@ -77,9 +77,10 @@ int deltanet_path(const deltanet_desc* d) {
 }
 
 int deltanet_launch_count(const deltanet_desc* d, int which) {
-  if (which == 2) {  // deltanet_recurrent_fwd
+  if (which >= 2 && which <= 4) {  // recurrent fwd, prologue fwd / bwd
     if (validate_rec(d) != DELTANET_OK) return -1;
-    return (size_t)d->B * d->H == 0 ? 0 : 1;
+    if ((size_t)d->B * d->H == 0 || (which >= 3 && d->L == 0)) return 0;
+    return which == 4 ? 2 : 1;
   }
   if (validate(d) != DELTANET_OK) return -1;
   if ((size_t)d->B * d->H == 0) return 0;
@@ -149,6 +150,55 @@ int deltanet_recurrent_fwd(const deltanet_desc* d, const void* q, const void* k,
   a.eps = d->l2_eps > 0.f ? d->l2_eps : 1e-6f;
   a.q = q; a.k = k; a.v = v; a.beta = beta; a.h0 = h0; a.o = o; a.hT = hT;
   return dn::rec_fwd(a, d->dtype, (cudaStream_t)stream);
+}
+
+size_t deltanet_prologue_workspace_bytes(const deltanet_desc* d) {
+  if (validate_rec(d) != DELTANET_OK) return 0;
+  return dn::prologue_workspace_bytes(d);
+}
+
+int deltanet_prologue_fwd(const deltanet_desc* d, const void* xq, const void* xk, const void* xv,
+                          const void* xb, const float* wq, const float* wk, const float* wv,
+                          void* q, void* k, void* v, void* beta, void* stream) {
+  int rc = validate_rec(d);
+  if (rc) return rc;
+  if ((size_t)d->B * d->H == 0 || d->L == 0) return DELTANET_OK;
+  if (!xq || !xk || !xv || !xb || !wq || !wk || !wv || !q || !k || !v || !beta)
+    return DELTANET_ERR_INVALID_ARG;
+  if (misaligned(xq) || misaligned(xk) || misaligned(xv) || misaligned(wq) || misaligned(wk) ||
+      misaligned(wv) || misaligned(q) || misaligned(k) || misaligned(v))
+    return DELTANET_ERR_MISALIGNED;
+  return dn::prologue_fwd(d, xq, xk, xv, xb, wq, wk, wv, q, k, v, beta, (cudaStream_t)stream);
+}
+
+int deltanet_prologue_bwd(const deltanet_desc* d, const void* xq, const void* xk, const void* xv,
+                          const void* xb, const float* wq, const float* wk, const float* wv,
+                          const void* dq, const void* dk, const void* dv, const void* dbeta,
+                          void* dxq, void* dxk, void* dxv, void* dxb, float* dwq, float* dwk,
+                          float* dwv, void* workspace, size_t workspace_bytes, void* stream) {
+  int rc = validate_rec(d);
+  if (rc) return rc;
+  if ((size_t)d->B * d->H == 0) return DELTANET_OK;
+  if (!dwq || !dwk || !dwv) return DELTANET_ERR_INVALID_ARG;
+  if (d->L > 0 && (!xq || !xk || !xv || !xb || !wq || !wk || !wv || !dq || !dk || !dv ||
+                   !dbeta || !dxq || !dxk || !dxv || !dxb))
+    return DELTANET_ERR_INVALID_ARG;
+  if (misaligned(xq) || misaligned(xk) || misaligned(xv) || misaligned(wq) || misaligned(wk) ||
+      misaligned(wv) || misaligned(dq) || misaligned(dk) || misaligned(dv) || misaligned(dxq) ||
+      misaligned(dxk) || misaligned(dxv) || misaligned(workspace))
+    return DELTANET_ERR_MISALIGNED;
+  if (d->L == 0) {  // no tokens: zero weight gradients
+    cudaStream_t s = (cudaStream_t)stream;
+    if (cudaMemsetAsync(dwq, 0, (size_t)d->H * d->Dk * 4 * sizeof(float), s) != cudaSuccess ||
+        cudaMemsetAsync(dwk, 0, (size_t)d->H * d->Dk * 4 * sizeof(float), s) != cudaSuccess ||
+        cudaMemsetAsync(dwv, 0, (size_t)d->H * d->Dv * 4 * sizeof(float), s) != cudaSuccess)
+      return DELTANET_ERR_CUDA;
+    return DELTANET_OK;
+  }
+  if (!workspace || workspace_bytes < dn::prologue_workspace_bytes(d))
+    return DELTANET_ERR_WORKSPACE;
+  return dn::prologue_bwd(d, xq, xk, xv, xb, wq, wk, wv, dq, dk, dv, dbeta, dxq, dxk, dxv, dxb,
+                          dwq, dwk, dwv, workspace, (cudaStream_t)stream);
 }
 
 const char* deltanet_strerror(int code) {

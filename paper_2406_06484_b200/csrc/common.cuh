@@ -50,6 +50,17 @@ size_t simt_scratch_floats_per_unit(int L, int Dk, int Dv, int C);
 // recurrent (token-by-token) inference path (recurrent.cu)
 int rec_fwd(const Args& a, int dtype, cudaStream_t s);
 
+// layer prologue (prologue.cu)
+size_t prologue_workspace_bytes(const deltanet_desc* d);
+int prologue_fwd(const deltanet_desc* d, const void* xq, const void* xk, const void* xv,
+                 const void* xb, const float* wq, const float* wk, const float* wv, void* q,
+                 void* k, void* v, void* beta, cudaStream_t s);
+int prologue_bwd(const deltanet_desc* d, const void* xq, const void* xk, const void* xv,
+                 const void* xb, const float* wq, const float* wk, const float* wv,
+                 const void* dq, const void* dk, const void* dv, const void* dbeta, void* dxq,
+                 void* dxk, void* dxv, void* dxb, float* dwq, float* dwk, float* dwv,
+                 void* ws, cudaStream_t s);
+
 // tcgen05 path entry points (tc_fwd.cu / tc_bwd.cu)
 bool tc_supported(const deltanet_desc* d);
 size_t tc_scratch_bytes(const deltanet_desc* d);

@@ -23,26 +23,6 @@ namespace {
 constexpr int RUN = 32, RUNS = 16, TT = RUN * RUNS;  // tokens per thread / CTA
 
 template <typename T>
-__device__ __forceinline__ void load8(const T* p, float (&x)[8]);
-template <>
-__device__ __forceinline__ void load8<__nv_bfloat16>(const __nv_bfloat16* p, float (&x)[8]) {
-  const uint4 v = *reinterpret_cast<const uint4*>(p);
-  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
-#pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    const float2 f = __bfloat1622float2(h[e]);
-    x[2 * e] = f.x;
-    x[2 * e + 1] = f.y;
-  }
-}
-template <>
-__device__ __forceinline__ void load8<float>(const float* p, float (&x)[8]) {
-  const float4 a = *reinterpret_cast<const float4*>(p);
-  const float4 b = *reinterpret_cast<const float4*>(p + 4);
-  x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
-  x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
-}
-template <typename T>
 __device__ __forceinline__ void store8(T* p, const float (&x)[8]);
 template <>
 __device__ __forceinline__ void store8<__nv_bfloat16>(__nv_bfloat16* p, const float (&x)[8]) {
@@ -60,6 +40,45 @@ __device__ __forceinline__ void store8<float>(float* p, const float (&x)[8]) {
   *reinterpret_cast<float4*>(p) = make_float4(x[0], x[1], x[2], x[3]);
   *reinterpret_cast<float4*>(p + 4) = make_float4(x[4], x[5], x[6], x[7]);
 }
+
+// 8 elements as raw 16 B words (bf16: one uint4, fp32: two), so that several
+// tokens' loads can be in flight before any is unpacked
+template <typename T>
+struct Raw8 {
+  uint4 w[sizeof(T) / 2];
+};
+template <typename T>
+__device__ __forceinline__ void load_raw(const T* p, Raw8<T>& r) {
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(T) / 2); ++i) r.w[i] = reinterpret_cast<const uint4*>(p)[i];
+}
+template <typename T>
+__device__ __forceinline__ void unpack(const Raw8<T>& r, float (&x)[8]);
+template <>
+__device__ __forceinline__ void unpack<__nv_bfloat16>(const Raw8<__nv_bfloat16>& r, float (&x)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r.w[0]);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 f = __bfloat1622float2(h[e]);
+    x[2 * e] = f.x;
+    x[2 * e + 1] = f.y;
+  }
+}
+template <>
+__device__ __forceinline__ void unpack<float>(const Raw8<float>& r, float (&x)[8]) {
+  const float* f = reinterpret_cast<const float*>(&r.w[0]);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) x[e] = f[e];
+}
+
+template <typename T>
+__device__ __forceinline__ void load8(const T* p, float (&x)[8]) {
+  Raw8<T> r;
+  load_raw(p, r);
+  unpack(r, x);
+}
+
+constexpr int UNR = 4;  // tokens loaded ahead per iteration
 
 __device__ __forceinline__ float sigm(float y) { return 1.f / (1.f + __expf(-y)); }
 
@@ -91,7 +110,7 @@ __device__ __forceinline__ Tz pick(const ProArgs& a, int z) {
 
 // grid (ntile, B*H, 4): z < 3 conv + activation of q / k / v, z == 3 beta
 template <typename T>
-__global__ void __launch_bounds__(256) prologue_fwd_kernel(ProArgs a) {
+__global__ void __launch_bounds__(256, 2) prologue_fwd_kernel(ProArgs a) {
   const int tile = blockIdx.x, bh = blockIdx.y, z = blockIdx.z;
   const int b = bh / a.H, h = bh % a.H, H = a.H, L = a.L;
   const int t_begin = tile * TT;
@@ -128,19 +147,27 @@ __global__ void __launch_bounds__(256) prologue_fwd_kernel(ProArgs a) {
     }
   }
   const int t1 = min(L, t0 + RUN);
-  for (int t = t0; t < t1; ++t) {
-    float xt[8], o[8];
-    load8(x + (size_t)t * H * D, xt);
+  for (int tb = t0; tb < t1; tb += UNR) {
+    Raw8<T> raw[UNR];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const float yy = fmaf(w[e][0], win[0][e],
-                            fmaf(w[e][1], win[1][e], fmaf(w[e][2], win[2][e], w[e][3] * xt[e])));
-      o[e] = tz.silu ? yy * sigm(yy) : yy;
-      win[0][e] = win[1][e];
-      win[1][e] = win[2][e];
-      win[2][e] = xt[e];
+    for (int u = 0; u < UNR; ++u)
+      if (tb + u < t1) load_raw(x + (size_t)(tb + u) * H * D, raw[u]);
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      if (tb + u >= t1) break;
+      float xt[8], o[8];
+      unpack(raw[u], xt);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float yy = fmaf(w[e][0], win[0][e],
+                              fmaf(w[e][1], win[1][e], fmaf(w[e][2], win[2][e], w[e][3] * xt[e])));
+        o[e] = tz.silu ? yy * sigm(yy) : yy;
+        win[0][e] = win[1][e];
+        win[1][e] = win[2][e];
+        win[2][e] = xt[e];
+      }
+      store8(y + (size_t)(tb + u) * D, o);
     }
-    store8(y + (size_t)t * D, o);
   }
   }
 }
@@ -199,10 +226,22 @@ __global__ void __launch_bounds__(256) prologue_bwd_kernel(ProArgs a) {
     }
     const int t1 = min(L, t0 + RUN);
     const int tend = min(L, t1 + 3);  // dy needed up to t1 + 2 for dx[t1 - 1]
-    for (int t = t0; t < tend; ++t) {
+    for (int tb = t0; tb < tend; tb += UNR) {
+    Raw8<T> rx[UNR], rg[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      if (tb + u < tend) {
+        load_raw(x + (size_t)(tb + u) * H * D, rx[u]);
+        load_raw(g + (size_t)(tb + u) * D, rg[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int t = tb + u;
+      if (t >= tend) break;
       float xt[8], gt[8], dyt[8];
-      load8(x + (size_t)t * H * D, xt);
-      load8(g + (size_t)t * D, gt);
+      unpack(rx[u], xt);
+      unpack(rg[u], gt);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         xw[0][e] = xw[1][e];
@@ -237,6 +276,7 @@ __global__ void __launch_bounds__(256) prologue_bwd_kernel(ProArgs a) {
         dyw[1][e] = dyw[2][e];
         dyw[2][e] = dyt[e];
       }
+    }
     }
     // tail: tokens whose dy window runs past L (dy[t >= L] = 0)
     for (int s = max(t0, tend - 3); s < t1; ++s) {

@@ -352,6 +352,9 @@ __global__ void __launch_bounds__(NT, 1)
       // products and this conversion are off the prep's critical path
       mbar_wait(&w_done, c & 1);
       fence_after_sync();
+      DBG(mbar_wait(&wu_done, c & 1); fence_after_sync();
+          dbg_tmem(dn_dbg + D_W, tm, TM_W, C, 128, w);
+          dbg_tmem(dn_dbg + D_U, tm, tm_u(b), C, 128, w));
       {
         float f[64];
         ld64(tm, wwarp, TM_W, f);

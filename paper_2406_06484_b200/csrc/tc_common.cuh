@@ -15,6 +15,7 @@
 // A TMA box {8 elements, R rows, Cc/8 groups} writes exactly this layout.
 #pragma once
 #include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -273,6 +274,8 @@ __device__ __forceinline__ void il_load8(const uint8_t* tile, int R, int r, int 
 // host: 4-D TMA view of a [B*H][L][D] bf16 tensor whose box {8, rows, D/8, 1}
 // lands in shared memory as the IL layout with R = rows (tc_fwd.cu).
 bool make_il_map(CUtensorMap* m, const void* base, int BH, int L, int D, int rows);
+// cuTensorMapEncodeTiled through the runtime's driver entry point (tc_fwd.cu)
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn();
 
 }  // namespace dn
 

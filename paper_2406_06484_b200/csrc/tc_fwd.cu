@@ -607,6 +607,8 @@ __global__ void __launch_bounds__(NT, 1)
   if (warp == 0) tmem_dealloc<512>(tm);
 }
 
+}  // namespace
+
 // ------------------------------------------------------------------ host side
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -621,7 +623,6 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-}  // namespace
 
 // 4-D view {8 elems, L rows, D/8 column groups, B*H units} of a [B*H][L][D]
 // bf16 tensor; a box {8, rows, D/8, 1} lands in smem as the IL layout (R=rows).

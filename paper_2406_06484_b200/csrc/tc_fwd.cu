@@ -240,27 +240,41 @@ __global__ void __launch_bounds__(NT, 1)
         TSTAMP(21);
         grp_sync<NP>(BAR_P);  // beta, s visible
         TSTAMP(22);
-        if (lane < 16) {  // A = tril(Q K^T), raw (inclusive, R4)
+        // lane pair (lo: G_qk row i, hi: G_kk row i) trades halves, so both
+        // lanes write 16 columns of A and 16 of L with no divergence
+        const bool lo = lane < 16;
+        float x[16];
 #pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            float x[8];
+        for (int e = 0; e < 16; ++e) x[e] = __shfl_xor_sync(0xffffffffu, lo ? f[16 + e] : f[e], 16);
+        const int c0 = h + (lo ? 0 : 16);
+        {  // A = tril(Q K^T), raw (inclusive, R4)
 #pragma unroll
-            for (int e = 0; e < 8; ++e) x[e] = (h + g * 8 + e <= i) ? f[g * 8 + e] : 0.f;
-            il_store8(sA(b), C, i, h + g * 8, x);
+          for (int g = 0; g < 2; ++g) {
+            float a8[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const float qk = lo ? f[g * 8 + e] : x[g * 8 + e];
+              a8[e] = (c0 + g * 8 + e <= i) ? qk : 0.f;
+            }
+            il_store8(sA(b), C, i, c0 + g * 8, a8);
           }
-        } else {  // L = beta_i s_i s_j (k_i . k_j), j < i
+        }
+        {  // L = beta_i s_i s_j (k_i . k_j), j < i
           const float bi = vb[i] * vb[C + i];
-          float4 s4[8];  // all loads first: no smem aliasing stalls
+          float4 s4[4];  // all loads first: no smem aliasing stalls
 #pragma unroll
-          for (int q = 0; q < 8; ++q) s4[q] = *reinterpret_cast<const float4*>(vb + C + h + 4 * q);
+          for (int q = 0; q < 4; ++q) s4[q] = *reinterpret_cast<const float4*>(vb + C + c0 + 4 * q);
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int j = h + 4 * q;
+          for (int q = 0; q < 4; ++q) {
+            const int j = c0 + 4 * q;
+            float kk[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) kk[e] = lo ? x[4 * q + e] : f[16 + 4 * q + e];
             float4 v;
-            v.x = (j + 0 < i) ? bi * s4[q].x * f[4 * q + 0] : 0.f;
-            v.y = (j + 1 < i) ? bi * s4[q].y * f[4 * q + 1] : 0.f;
-            v.z = (j + 2 < i) ? bi * s4[q].z * f[4 * q + 2] : 0.f;
-            v.w = (j + 3 < i) ? bi * s4[q].w * f[4 * q + 3] : 0.f;
+            v.x = (j + 0 < i) ? bi * s4[q].x * kk[0] : 0.f;
+            v.y = (j + 1 < i) ? bi * s4[q].y * kk[1] : 0.f;
+            v.z = (j + 2 < i) ? bi * s4[q].z * kk[2] : 0.f;
+            v.w = (j + 3 < i) ? bi * s4[q].w * kk[3] : 0.f;
             *reinterpret_cast<float4*>(LX + i * LS + j) = v;
           }
         }

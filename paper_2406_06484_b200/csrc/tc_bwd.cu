@@ -558,20 +558,22 @@ __global__ void __launch_bounds__(NT, 1)
       fence_after_sync();
       BSTAMP(4);
       {
-        float f[32];
+        // lanes < 16 hold the Q K^T row; each lane pair splits its 32 columns
+        float f[32], x[16];
         ld32(tm, wwarp, TM_G + 32 * wg, f);
-        if (lo) {
-          const float ri = sr[r64];
 #pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            float x[8];
+        for (int e = 0; e < 16; ++e) x[e] = __shfl_xor_sync(0xffffffffu, f[16 + e], 16);
+        const float ri = sr[r64];
+        const int c0 = 32 * wg + (lo ? 0 : 16);
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const int j = 32 * wg + g * 8 + e;
-              x[e] = (j <= r64) ? ri * f[g * 8 + e] : 0.f;
-            }
-            il_store8(sA, C, r64, 32 * wg + g * 8, x);
+        for (int g = 0; g < 2; ++g) {
+          float a8[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float v = lo ? f[g * 8 + e] : x[g * 8 + e];
+            a8[e] = (c0 + g * 8 + e <= r64) ? ri * v : 0.f;
           }
+          il_store8(sA, C, r64, c0 + g * 8, a8);
         }
       }
       simt_signal(&sg[SG_A], tid);

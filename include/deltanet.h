@@ -66,7 +66,11 @@ enum {
   DELTANET_FORCE_SIMT = 1u << 2,
   /* layer prologue only: SiLU on v as well (the paper states SiLU for q, k
    * only; R22) */
-  DELTANET_PROLOGUE_SILU_V = 1u << 3
+  DELTANET_PROLOGUE_SILU_V = 1u << 3,
+  /* tcgen05 forward: never split a unit's sequence into segments processed
+   * by several CTAs (the segment-parallel forward, is used
+   * automatically when B*H is small against the SM count) */
+  DELTANET_NO_SEGMENTS = 1u << 4
 };
 
 typedef struct {

@@ -28,6 +28,7 @@ DELTANET_L2NORM_QK = 1 << 0
 DELTANET_SAVE_STATES = 1 << 1
 DELTANET_PROLOGUE_SILU_V = 1 << 3
 DELTANET_FORCE_SIMT = 1 << 2
+DELTANET_NO_SEGMENTS = 1 << 4
 
 
 class deltanet_desc(ctypes.Structure):
@@ -96,18 +97,19 @@ def _check(rc: int, what: str):
 
 
 def make_desc(B, H, L, Dk, Dv, chunk=64, dtype=torch.bfloat16, l2norm=True,
-              save_states=True, force_simt=False, eps=1e-6) -> deltanet_desc:
+              save_states=True, force_simt=False, eps=1e-6, segments=True) -> deltanet_desc:
     dt = {torch.bfloat16: DELTANET_BF16, torch.float32: DELTANET_FP32}[dtype]
     flags = ((DELTANET_L2NORM_QK if l2norm else 0) |
              (DELTANET_SAVE_STATES if save_states else 0) |
-             (DELTANET_FORCE_SIMT if force_simt else 0))
+             (DELTANET_FORCE_SIMT if force_simt else 0) |
+             (0 if segments else DELTANET_NO_SEGMENTS))
     return deltanet_desc(B, H, L, Dk, Dv, chunk, dt, flags, eps)
 
 
-def _desc_for(q, v, chunk, l2norm, save_states, force_simt, eps):
+def _desc_for(q, v, chunk, l2norm, save_states, force_simt, eps, segments=True):
     B, H, L, Dk = q.shape
     return make_desc(B, H, L, Dk, v.shape[-1], chunk, q.dtype, l2norm, save_states,
-                     force_simt, eps)
+                     force_simt, eps, segments)
 
 
 def deltanet_workspace_bytes(desc: deltanet_desc) -> int:
@@ -149,15 +151,17 @@ def _stream(device):
 
 
 def deltanet_fwd(q, k, v, beta, *, chunk=64, l2norm=True, h0=None, save_states=True,
-                 workspace=None, want_hT=True, force_simt=False, eps=1e-6, out=None):
+                 workspace=None, want_hT=True, force_simt=False, eps=1e-6, out=None,
+                 segments=True):
     """Forward of the chunkwise delta rule (§3.2 Eq. 8-11).
+    ``segments=False`` forbids the segment-parallel forward.
     Returns (o, hT or None, workspace)."""
     lib = load_library()
     dev = q.device
     for t, n in ((q, "q"), (k, "k"), (v, "v"), (beta, "beta")):
         _need(t, n, q.dtype, dev)
     _need(h0, "h0", torch.float32, dev)
-    d = _desc_for(q, v, chunk, l2norm, save_states, force_simt, eps)
+    d = _desc_for(q, v, chunk, l2norm, save_states, force_simt, eps, segments)
     B, H, L, Dk = q.shape
     Dv = v.shape[-1]
     o = out if out is not None else torch.empty((B, H, L, Dv), dtype=q.dtype, device=dev)
@@ -252,7 +256,7 @@ def deltanet_prologue_bwd(xq, xk, xv, xb, wq, wk, wv, dq, dk, dv, dbeta, *, silu
 
 def deltanet_bwd(q, k, v, beta, dO, *, chunk=64, l2norm=True, h0=None, dhT=None,
                  workspace=None, states_saved=True, want_dh0=True, force_simt=False,
-                 eps=1e-6, out=None):
+                 eps=1e-6, out=None, segments=True):
     """Backward: gradients w.r.t. raw q, k, v, beta (and h0).  With
     states_saved=True the workspace must come from deltanet_fwd(save_states=True)
     on the same inputs.  Returns (dq, dk, dv, dbeta, dh0 or None)."""
@@ -264,7 +268,7 @@ def deltanet_bwd(q, k, v, beta, dO, *, chunk=64, l2norm=True, h0=None, dhT=None,
     _need(dhT, "dhT", torch.float32, dev)
     if workspace is None:
         states_saved = False
-    d = _desc_for(q, v, chunk, l2norm, states_saved, force_simt, eps)
+    d = _desc_for(q, v, chunk, l2norm, states_saved, force_simt, eps, segments)
     B, H, L, Dk = q.shape
     Dv = v.shape[-1]
     if out is not None:

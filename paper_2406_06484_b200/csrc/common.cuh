@@ -23,6 +23,12 @@ struct Args {
   float* dh0;
   void* states;    // [B*H][NC][Dk][Dv] of the I/O dtype (H_t before chunk t)
   float* scratch;  // path-specific scratch
+  // sequence segments of the tcgen05 forward (tc_fwd.cu):
+  // nseg CTAs per unit, seg_len chunks each (nseg <= 1: one CTA per unit)
+  int nseg, seg_len;
+  float* hseg;  // [B*H][nseg][Dk][Dv] state at each segment start (pass 3 input)
+  float* hloc;  // [B*H][nseg][Dk][Dv] segment-local end state from zero (pass 1)
+  float* psi;   // [B*H][nseg][Dk][Dk] segment transition (pass 1)
 };
 
 template <typename T>

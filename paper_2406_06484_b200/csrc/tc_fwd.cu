@@ -122,6 +122,10 @@ __device__ long long* dn_tim = nullptr;
 #define TSTAMP_PTR(slot) nullptr
 #endif
 
+// SEG1 = pass 1 of the segment-parallel forward: from a zero
+// state, the segment's end state H_loc and its transition
+// Psi = prod_c (I - W_c^T K_hat_c) (H^T_end = H^T_start Psi + H^T_loc); no O.
+template <bool SEG1>
 __global__ void __launch_bounds__(NT, 1)
     tc_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                   const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mO,
@@ -137,8 +141,14 @@ __global__ void __launch_bounds__(NT, 1)
   const int w = tid & 127;            // thread index inside a 128-thread group
   const int wwarp = w >> 5;           // TMEM lane quadrant of this warp
   const int half = (tid >> 7) & 1;    // prep: which column half this thread handles
-  const int unit = blockIdx.x;
-  const int L = a.L, NC = a.NC;
+  // segment of this CTA: chunks [cbase, cbase + NC) of unit; local chunk c is
+  // global chunk cbase + c (token T0 + c*C); L counts tokens from T0
+  const int nseg = a.nseg > 1 ? a.nseg : 1;
+  const int unit = blockIdx.x / nseg, seg = blockIdx.x % nseg;
+  const int cbase = nseg > 1 ? seg * a.seg_len : 0;
+  const int NC = nseg > 1 ? min(a.seg_len, a.NC - cbase) : a.NC;
+  const int T0 = cbase * C;
+  const int L = a.L - T0;
   const bool l2 = (a.flags & DELTANET_L2NORM_QK) != 0;
 
   if (warp == 0) tmem_alloc<512>(&tslot);
@@ -172,7 +182,7 @@ __global__ void __launch_bounds__(NT, 1)
   auto sQ = [&](int b) { return smem + OFF_Q + b * TILE; };
   auto sK = [&](int b) { return smem + OFF_K + b * TILE; };
   auto sA = [&](int b) { return smem + OFF_A + b * C * C * 2; };
-  auto sW = [&](int b) { return smem + OFF_W + b * DK * C * 2; };
+  auto sW = [&](int b) { return smem + OFF_W + (SEG1 ? 1 : b) * DK * C * 2; };
   auto vec = [&](int b) { return reinterpret_cast<float*>(smem + OFF_VEC) + b * 3 * C; };
   uint8_t* sV = smem + OFF_V;
   uint8_t* sT = smem + OFF_T;
@@ -180,9 +190,14 @@ __global__ void __launch_bounds__(NT, 1)
   uint8_t* sH = smem + OFF_H;
   uint8_t* sZ = smem + OFF_Z;
   uint8_t* sXb = smem + OFF_XB;
-  uint8_t* recs = (a.flags & DELTANET_SAVE_STATES)
-                      ? reinterpret_cast<uint8_t*>(a.scratch) + (size_t)unit * NC * REC_BYTES
+  uint8_t* recs = (!SEG1 && (a.flags & DELTANET_SAVE_STATES))
+                      ? reinterpret_cast<uint8_t*>(a.scratch) +
+                            ((size_t)unit * a.NC + cbase) * REC_BYTES
                       : nullptr;
+  // SEG1: the Psi image [dk][dk] bf16 (IL R=128) over A[0], A[1], W[0]; W in W[1]
+  uint8_t* sPsi = smem + OFF_A;
+  static_assert(OFF_W == OFF_A + 2 * C * C * 2 && 2 * C * C * 2 + DK * C * 2 == DK * DK * 2,
+                "Psi image spans A[0..1] and W[0]");
   uint8_t* sO = sZ;
   float* LX = reinterpret_cast<float*>(smem + OFF_L);
 
@@ -192,7 +207,7 @@ __global__ void __launch_bounds__(NT, 1)
     // Every row-wise phase is split in two column halves (`half`), so each
     // SM sub-partition runs two prep warps and hides the other's latency.
     // =====================================================================
-    const __nv_bfloat16* beta = (const __nv_bfloat16*)a.beta + (size_t)unit * L;
+    const __nv_bfloat16* beta = (const __nv_bfloat16*)a.beta + (size_t)unit * a.L + T0;
     // beta is prefetched into a register one chunk ahead (global latency)
     float bnext = (w < C && w < L) ? __bfloat162float(beta[w]) : 0.f;
 #pragma unroll 1
@@ -256,7 +271,7 @@ __global__ void __launch_bounds__(NT, 1)
               const float qk = lo ? f[g * 8 + e] : x[g * 8 + e];
               a8[e] = (c0 + g * 8 + e <= i) ? qk : 0.f;
             }
-            il_store8(sA(b), C, i, c0 + g * 8, a8);
+            if (!SEG1) il_store8(sA(b), C, i, c0 + g * 8, a8);
           }
         }
         {  // L = beta_i s_i s_j (k_i . k_j), j < i
@@ -335,8 +350,11 @@ __global__ void __launch_bounds__(NT, 1)
     // Warpgroup S (warps 8-11): state chain conversions + output epilogue
     // =====================================================================
     float* qn2 = LX + C * LS;  // [2][64] partial ||q||^2 (region after LX)
-    {  // initial state: H^T row dv = w (TMEM lane w) from h0 [dk][dv]
-      const float* h0 = a.h0 ? a.h0 + (size_t)unit * DK * DV : nullptr;
+    {  // initial state: H^T row dv = w (TMEM lane w) from h0 [dk][dv] (segment
+      // starts after the first: the scanned state; SEG1: zero)
+      const float* h0 = SEG1 ? nullptr
+                        : (seg > 0 && a.hseg) ? a.hseg + ((size_t)unit * nseg + seg) * DK * DV
+                        : a.h0 ? a.h0 + (size_t)unit * DK * DV : nullptr;
 #pragma unroll 1
       for (int c0 = 0; c0 < DK; c0 += 16) {
         uint32_t r[16];
@@ -349,6 +367,21 @@ __global__ void __launch_bounds__(NT, 1)
         tmem_st16(taddr(tm, wwarp * 32, TM_H + c0), r);
         il_store8(sH, DV, w, c0, f);
         il_store8(sH, DV, w, c0 + 8, f + 8);
+      }
+      if (SEG1) {  // Psi = I: TMEM (fp32, lane = row a = w) and the bf16 image
+#pragma unroll 1
+        for (int c0 = 0; c0 < DK; c0 += 16) {
+          uint32_t r[16];
+          float f[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            f[j] = (c0 + j == w) ? 1.f : 0.f;
+            r[j] = __float_as_uint(f[j]);
+          }
+          tmem_st16(taddr(tm, wwarp * 32, TM_O + c0), r);
+          il_store8(sPsi, DK, w, c0, f);
+          il_store8(sPsi, DK, w, c0 + 8, f + 8);
+        }
       }
       tmem_st_wait();
     }
@@ -381,14 +414,16 @@ __global__ void __launch_bounds__(NT, 1)
       if (w == 0) {
         // U^T[b] complete before the chain uses it; waited before w_free is
         // released so that wu_done cannot run a phase ahead of this wait
+        // (SEG1: TM_W then holds T1 = Psi W^T until the Psi update: w_free
+        // comes after ho_done)
         mbar_wait(&wu_done, c & 1);
-        mbar_arrive(&w_free);
+        if (!SEG1) mbar_arrive(&w_free);
         mbar_arrive(&bar_full[b]);
       }
       // r_i = 1/max(||q_i||, eps) for this lane's output row (R9): partial sums
       // of squares over column halves (thread w: row w & 63, half w >> 6)
-      float ri;
-      {
+      float ri = 0.f;
+      if (!SEG1) {
         const int row = w & 63, hh = w >> 6;
         float x[DK / 2];
 #pragma unroll
@@ -419,6 +454,24 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
         for (int g = 0; g < 8; ++g) il_store8(sZ, DV, w, g * 8, f + g * 8);
       }
+      if (SEG1) {
+        // T1 = Psi W^T (TM_W, lane = row a, cols = tokens) -> -T1 diag(s) as
+        // bf16 pairs in TM_W's first 32 columns: the A operand (from TMEM) of
+        // Psi += (-T1 diag(s)) K = Psi - Psi W^T K_hat
+        float f[64];
+        ld64(tm, wwarp, TM_W, f);
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          uint32_t r[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int t = 32 * h2 + 2 * j;
+            r[j] = pack_bf16(-f[t] * vb[C + t], -f[t + 1] * vb[C + t + 1]);
+          }
+          tmem_st16(taddr(tm, wwarp * 32, TM_W + 16 * h2), r);
+        }
+        tmem_st_wait();
+      }
       fence_proxy_async();
       fence_before_sync();
       wg_sync(BAR_S);
@@ -438,30 +491,58 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
           for (int g = 0; g < 8; ++g) il_store8(sH, DV, w, 64 * half + g * 8, f + g * 8);
         }
-        // O rows * r -> bf16 -> staging (IL R=64, row = token)
-        const int i = wwarp * 16 + (lane & 15);
+        if (SEG1) {  // Psi (TM_O, lane = row a) -> bf16 image (row a) for the next T1
 #pragma unroll 1
-        for (int half = 0; half < 2; ++half) {
-          float f[64];
-          ld64(tm, wwarp, TM_O + 64 * half, f);
-          if (lane < 16) {
+          for (int half = 0; half < 2; ++half) {
+            float f[64];
+            ld64(tm, wwarp, TM_O + 64 * half, f);
 #pragma unroll
-            for (int e = 0; e < 64; ++e) f[e] *= ri;
+            for (int g = 0; g < 8; ++g) il_store8(sPsi, DK, w, 64 * half + g * 8, f + g * 8);
+          }
+        } else {
+          // O rows * r -> bf16 -> staging (IL R=64, row = token)
+          const int i = wwarp * 16 + (lane & 15);
+#pragma unroll 1
+          for (int half = 0; half < 2; ++half) {
+            float f[64];
+            ld64(tm, wwarp, TM_O + 64 * half, f);
+            if (lane < 16) {
 #pragma unroll
-            for (int g = 0; g < 8; ++g) il_store8(sO, C, i, 64 * half + g * 8, f + g * 8);
+              for (int e = 0; e < 64; ++e) f[e] *= ri;
+#pragma unroll
+              for (int g = 0; g < 8; ++g) il_store8(sO, C, i, 64 * half + g * 8, f + g * 8);
+            }
           }
         }
       }
       fence_proxy_async();
       fence_before_sync();
       wg_sync(BAR_S);
-      if (w == 0) mbar_arrive(&h_ready);
+      if (w == 0) {
+        if (SEG1) mbar_arrive(&w_free);  // T1 consumed by the Psi update (ho_done)
+        mbar_arrive(&h_ready);
+      }
       TSTAMP(20);
     }
-    // final state hT [dk][dv] (fp32), lane dv = w
-    if (a.hT) {
+    // final state hT [dk][dv] (fp32), lane dv = w: the last segment's; SEG1
+    // writes the segment-local end state and Psi instead
+    float* hout = SEG1 ? a.hloc + ((size_t)unit * nseg + seg) * DK * DV
+                  : (seg == nseg - 1) ? a.hT : nullptr;
+    if (!SEG1 && hout) hout += (size_t)unit * DK * DV;
+    if (SEG1) {
       fence_after_sync();
-      float* hT = a.hT + (size_t)unit * DK * DV;
+      float* psi = a.psi + ((size_t)unit * nseg + seg) * DK * DK;
+#pragma unroll 1
+      for (int half = 0; half < 2; ++half) {
+        float f[64];
+        ld64(tm, wwarp, TM_O + 64 * half, f);
+#pragma unroll
+        for (int e = 0; e < 64; ++e) psi[(size_t)w * DK + 64 * half + e] = f[e];
+      }
+    }
+    if (hout) {
+      fence_after_sync();
+      float* hT = hout;
 #pragma unroll 1
       for (int half = 0; half < 2; ++half) {
         float f[64];
@@ -477,11 +558,11 @@ __global__ void __launch_bounds__(NT, 1)
     if (lane == 0) {
       for (int c = 0; c < 2 && c < NC; ++c) {
         mbar_expect_tx(&qk_full[c], 2 * TILE);
-        tma_load_4d(sQ(c), &mQ, 0, c * C, 0, unit, &qk_full[c]);
-        tma_load_4d(sK(c), &mK, 0, c * C, 0, unit, &qk_full[c]);
+        tma_load_4d(sQ(c), &mQ, 0, T0 + c * C, 0, unit, &qk_full[c]);
+        tma_load_4d(sK(c), &mK, 0, T0 + c * C, 0, unit, &qk_full[c]);
       }
       mbar_expect_tx(&v_full[0], TILE);
-      tma_load_4d(sV, &mV, 0, 0, 0, unit, &v_full[0]);
+      tma_load_4d(sV, &mV, 0, T0, 0, unit, &v_full[0]);
       const uint32_t idg = idesc_bf16(64, 64, false, false);
       const uint32_t idw = idesc_bf16(128, 64, true, false);
       const uint32_t at = smem_u32(sT), atu = smem_u32(sTu), av = smem_u32(sV);
@@ -536,7 +617,7 @@ __global__ void __launch_bounds__(NT, 1)
         if (c + 1 < NC) {  // V (and T, T'') free again: prefetch the next chunk's V
           const int nb = (c + 1) & 1;
           mbar_expect_tx(&v_full[nb], TILE);
-          tma_load_4d(sV, &mV, 0, (c + 1) * C, 0, unit, &v_full[nb]);
+          tma_load_4d(sV, &mV, 0, T0 + (c + 1) * C, 0, unit, &v_full[nb]);
         }
       }
     }
@@ -546,9 +627,13 @@ __global__ void __launch_bounds__(NT, 1)
     // Warp 13: state-chain MMA issue, state save, O store, next Q/K loads
     // =====================================================================
     if (lane == 0) {
-      uint8_t* states = (a.flags & DELTANET_SAVE_STATES)
-                            ? (uint8_t*)a.states + (size_t)unit * NC * (DK * DV * 2)
+      uint8_t* states = (!SEG1 && (a.flags & DELTANET_SAVE_STATES))
+                            ? (uint8_t*)a.states + ((size_t)unit * a.NC + cbase) * (DK * DV * 2)
                             : nullptr;
+      void* const o_out = SEG1 ? nullptr : a.o;
+      const uint32_t aPsi = smem_u32(sPsi);
+      const uint32_t idt = idesc_bf16(128, 64, false, true);    // T1 = Psi W^T
+      const uint32_t idp = idesc_bf16(128, 128, false, true);   // Psi += (-T1 s) K
       const uint32_t aH = smem_u32(sH), aZ = smem_u32(sZ);
       const uint32_t idn = idesc_bf16(128, 64, false, true, /*neg_a=*/true);
       const uint32_t ido = idesc_bf16(64, 128, false, false);
@@ -560,8 +645,8 @@ __global__ void __launch_bounds__(NT, 1)
                        ak = smem_u32(sK(b));
         mbar_wait(&bar_full[b], (c >> 1) & 1);
         mbar_wait(&h_ready, c & 1);  // sH = bf16 image of H_c; sO = O of chunk c-1
-        if (c >= 1 && a.o) {
-          tma_store_4d(&mO, sO, 0, (c - 1) * C, 0, unit);
+        if (c >= 1 && o_out) {
+          tma_store_4d(&mO, sO, 0, T0 + (c - 1) * C, 0, unit);
           bulk_commit();
         }
         if (states) {  // save H_c (bf16 smem image) for the backward
@@ -573,10 +658,17 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
         for (int k0 = 0; k0 < DK; k0 += 16)
           mma_bf16(tm + tm_u(b), desc_k(aH, DV, k0), desc_mn(aw, DK, k0), idn, 1);
-        mma_commit(&up_done);
+        if (SEG1) {  // T1 = Psi W^T (M=128 a, N=64 t, K=128 dk) into TM_W
 #pragma unroll
-        for (int k0 = 0; k0 < DK; k0 += 16)
-          mma_bf16(tm + TM_O, desc_k(aq, C, k0), desc_k(aH, DV, k0), ido, k0 > 0);
+          for (int k0 = 0; k0 < DK; k0 += 16)
+            mma_bf16(tm + TM_W, desc_k(aPsi, DK, k0), desc_mn(aw, DK, k0), idt, k0 > 0);
+        }
+        mma_commit(&up_done);
+        if (!SEG1) {
+#pragma unroll
+          for (int k0 = 0; k0 < DK; k0 += 16)
+            mma_bf16(tm + TM_O, desc_k(aq, C, k0), desc_k(aH, DV, k0), ido, k0 > 0);
+        }
         // the O store of chunk c-1 must finish reading sO (= sZ) before Z is written
         asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(1) : "memory");
         if (!states) bulk_wait_read0();
@@ -584,7 +676,7 @@ __global__ void __launch_bounds__(NT, 1)
         mbar_wait(&z_ready, c & 1);
         fence_after_sync();
         if (states) {  // Z^T of this chunk for the backward (read out before st_free)
-          bulk_store(reinterpret_cast<uint8_t*>(a.scratch) + ((size_t)unit * NC + c) * REC_BYTES +
+          bulk_store(reinterpret_cast<uint8_t*>(a.scratch) + ((size_t)unit * a.NC + cbase + c) * REC_BYTES +
                          REC_Z,
                      sZ, DV * C * 2);
           bulk_commit();
@@ -593,24 +685,30 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
         for (int k0 = 0; k0 < C; k0 += 16)
           mma_bf16(tm + TM_H, desc_k(aZ, DV, k0), desc_mn(ak, C, k0), idh, 1);
+        if (SEG1) {  // Psi += (-T1 diag(s)) K, A from TMEM (bf16 pairs in TM_W)
 #pragma unroll
-        for (int k0 = 0; k0 < C; k0 += 16)
-          mma_bf16(tm + TM_O, desc_k(aa, C, k0), desc_k(aZ, DV, k0), ido, 1);
+          for (int k0 = 0; k0 < C; k0 += 16)
+            mma_bf16_ts(tm + TM_O, tm + TM_W + k0 / 2, desc_mn(ak, C, k0), idp, 1);
+        } else {
+#pragma unroll
+          for (int k0 = 0; k0 < C; k0 += 16)
+            mma_bf16(tm + TM_O, desc_k(aa, C, k0), desc_k(aZ, DV, k0), ido, 1);
+        }
         mma_commit(&ho_done);
         mbar_wait(&ho_done, c & 1);
         mbar_arrive(&bar_empty[b]);  // Q/K/A/W[b], vec[b] and U[b] are free for chunk c+2
         if (c + 2 < NC) {
           mbar_expect_tx(&qk_full[b], 2 * TILE);
-          tma_load_4d(sQ(b), &mQ, 0, (c + 2) * C, 0, unit, &qk_full[b]);
-          tma_load_4d(sK(b), &mK, 0, (c + 2) * C, 0, unit, &qk_full[b]);
+          tma_load_4d(sQ(b), &mQ, 0, T0 + (c + 2) * C, 0, unit, &qk_full[b]);
+          tma_load_4d(sK(b), &mK, 0, T0 + (c + 2) * C, 0, unit, &qk_full[b]);
         }
         bulk_wait_read0();  // state save done reading sH
         mbar_arrive(&st_free);
       }
       // O of the last chunk
       mbar_wait(&h_ready, NC & 1);
-      if (a.o && NC > 0) {
-        tma_store_4d(&mO, sO, 0, (NC - 1) * C, 0, unit);
+      if (o_out && NC > 0) {
+        tma_store_4d(&mO, sO, 0, T0 + (NC - 1) * C, 0, unit);
         bulk_commit();
       }
       bulk_wait0();
@@ -619,6 +717,42 @@ __global__ void __launch_bounds__(NT, 1)
   }
   cta_sync();
   if (warp == 0) tmem_dealloc<512>(tm);
+}
+
+// Pass 2 of the segment-parallel forward: per unit, the states at the segment
+// starts, H_start(s+1) = Psi_s^T H_start(s) + H_loc(s) (H = S^T, [dk][dv]),
+// from H_start(0) = h0.  The columns of H evolve independently: a CTA scans
+// one 16-column block; fp32 throughout.
+__global__ void __launch_bounds__(256) seg_scan_kernel(Args a) {
+  __shared__ float Hs[DK][16];
+  const int unit = blockIdx.x, j0 = blockIdx.y * 16, nseg = a.nseg;
+  const int tid = threadIdx.x, i = tid >> 1, jj = (tid & 1) * 8;
+  for (int e = tid; e < DK * 16; e += blockDim.x) {
+    const int r = e / 16, cc = e % 16;
+    Hs[r][cc] = a.h0 ? a.h0[(size_t)unit * DK * DV + (size_t)r * DV + j0 + cc] : 0.f;
+  }
+  __syncthreads();
+  for (int sg = 0; sg + 1 < nseg; ++sg) {
+    const float* psi = a.psi + ((size_t)unit * nseg + sg) * DK * DK;
+    const float* hl = a.hloc + ((size_t)unit * nseg + sg) * DK * DV + (size_t)i * DV + j0 + jj;
+    float acc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = hl[e];
+#pragma unroll 4
+    for (int r = 0; r < DK; ++r) {
+      const float pv = psi[(size_t)r * DK + i];  // Psi[r][i]
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = fmaf(pv, Hs[r][jj + e], acc[e]);
+    }
+    __syncthreads();
+    float* out = a.hseg + ((size_t)unit * nseg + sg + 1) * DK * DV + (size_t)i * DV + j0 + jj;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      Hs[i][jj + e] = acc[e];
+      out[e] = acc[e];
+    }
+    __syncthreads();
+  }
 }
 
 }  // namespace
@@ -658,31 +792,90 @@ bool tc_supported(const deltanet_desc* d) {
 }
 
 // per-chunk records [X | W^T | Z^T] the backward reads (40 KB per chunk per unit)
+namespace {
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = 148;  // B200
+    }
+  }
+  return n;
+}
+size_t round256(size_t x) { return (x + 255) & ~(size_t)255; }
+size_t rec_bytes(int B, int H, int L) {
+  return (size_t)B * H * ((size_t)(L + C - 1) / C) * REC_BYTES;
+}
+}  // namespace
+
+// Sequence segments per unit of the tcgen05 forward: when
+// B*H units leave SMs idle, each unit's chunks are split over up to
+// SMs / units CTAs (segments of >= 8 chunks, at most 16).
+int tc_fwd_segments(const deltanet_desc* d) {
+  if (d->flags & DELTANET_NO_SEGMENTS) return 1;
+  const int units = d->B * d->H, NCk = (d->L + C - 1) / C;
+  if (units <= 0) return 1;
+  int n = sm_count() / units;
+  n = n < NCk / 8 ? n : NCk / 8;
+  n = n < 16 ? n : 16;
+  if (n < 3) return 1;  // passes 1 + 3 cost about two forwards: pays from 3 segments
+  const int seg_len = (NCk + n - 1) / n;
+  return (NCk + seg_len - 1) / seg_len;
+}
+
+// per-chunk records [X | Z^T] the backward reads (24 KB per chunk per unit),
+// then the segment scratch (H_loc, Psi, H_start per (unit, segment))
 size_t tc_scratch_bytes(const deltanet_desc* d) {
-  const size_t NCk = (size_t)(d->L + C - 1) / C;
-  return (size_t)d->B * d->H * NCk * REC_BYTES;
+  const int nseg = tc_fwd_segments(d);
+  const size_t seg = nseg > 1 ? (size_t)d->B * d->H * nseg * (2 * DK * DV + DK * DK) * 4 : 0;
+  return round256(rec_bytes(d->B, d->H, d->L)) + seg;
 }
 
-// fwd: 1 kernel; bwd: 1 kernel, plus the state-recompute forward without SAVE_STATES
+// fwd: 1 kernel (3 when segmented); bwd: 1 kernel, plus the state-recompute
+// forward without SAVE_STATES
 int tc_launch_count(const deltanet_desc* d, int which) {
-  return which == 0 ? 1 : ((d->flags & DELTANET_SAVE_STATES) ? 1 : 2);
+  const int f = tc_fwd_segments(d) > 1 ? 3 : 1;
+  return which == 0 ? f : ((d->flags & DELTANET_SAVE_STATES) ? 1 : 1 + f);
 }
 
-int tc_fwd(const Args& a, cudaStream_t s) {
+int tc_fwd(const Args& a0, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(tc_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(tc_fwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(tc_fwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              SMEM_BYTES) != cudaSuccess)
       return DELTANET_ERR_CUDA;
     attr = true;
   }
+  Args a = a0;
   const int BH = a.B * a.H;
   CUtensorMap mQ, mK, mV, mO;
   if (!make_il_map(&mQ, a.q, BH, a.L, DK, C) || !make_il_map(&mK, a.k, BH, a.L, DK, C) ||
       !make_il_map(&mV, a.v, BH, a.L, DV, C) ||
       !make_il_map(&mO, a.o ? a.o : a.v, BH, a.L, DV, C))  // o == null: states only
     return DELTANET_ERR_CUDA;
-  tc_fwd_kernel<<<BH, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);
+  deltanet_desc d;
+  d.B = a.B; d.H = a.H; d.L = a.L; d.Dk = a.Dk; d.Dv = a.Dv; d.chunk = a.C;
+  d.dtype = DELTANET_BF16; d.flags = a.flags; d.l2_eps = a.eps;
+  const int nseg = tc_fwd_segments(&d);
+  if (nseg <= 1) {
+    a.nseg = 1;
+    tc_fwd_kernel<false><<<BH, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);
+    return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
+  }
+  a.nseg = nseg;
+  a.seg_len = (a.NC + nseg - 1) / nseg;
+  float* base = (float*)((char*)a.scratch + round256(rec_bytes(a.B, a.H, a.L)));
+  a.hloc = base;
+  a.psi = a.hloc + (size_t)BH * nseg * DK * DV;
+  a.hseg = a.psi + (size_t)BH * nseg * DK * DK;
+  tc_fwd_kernel<true><<<BH * nseg, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);   // pass 1
+  seg_scan_kernel<<<dim3(BH, DV / 16), 256, 0, s>>>(a);                     // pass 2
+  tc_fwd_kernel<false><<<BH * nseg, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);  // pass 3
   return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
 }
 

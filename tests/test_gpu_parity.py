@@ -151,3 +151,52 @@ def test_bf16_full_size_sampled_units(name):
         ref = run_oracle(one)
         sub = {k: (None if v is None else v[b:b + 1, h:h + 1]) for k, v in got.items()}
         compare(sub, ref, TOL["bf16"])
+
+
+# ------------------------------------------------- segment-parallel forward
+
+def _segmented(B, H, L):
+    import paper_2406_06484_b200 as dn
+    d = dn.make_desc(B, H, L, 128, 128, 64, torch.bfloat16)
+    return dn.deltanet_launch_count(d, 0) == 3
+
+
+@pytest.mark.parametrize("save_states", [True, False])
+def test_bf16_segmented_forward(save_states):
+    """Few units, many chunks: the forward splits each unit's sequence into
+    segments (pass 1: local end state + transition, pass 2: scan of the
+    segment-start states, pass 3: the forward from those states; DESIGN.md
+    §4.6).  h0 / dhT exercise the scan's start and the backward that reads
+    pass 3's states (or recomputes them through the same segmented forward)."""
+    L = 64 * 40 + 17
+    assert _segmented(1, 2, L)
+    cfg, inp = _case(1, 2, L, 128, 128, 64, "bf16", index=520)
+    rng = np.random.default_rng(11)
+    h0 = (0.2 * rng.standard_normal((1, 2, 128, 128))).astype(np.float32)
+    dhT = rng.standard_normal((1, 2, 128, 128)).astype(np.float32)
+    got = run_gpu(inp, "bf16", 64, h0=h0, dhT=dhT, save_states=save_states)
+    compare(got, run_oracle(inp, h0=h0.astype(np.float64), dhT=dhT.astype(np.float64)),
+            TOL["bf16"])
+
+
+def test_bf16_segments_match_serial():
+    """The segmented and the one-CTA-per-unit forward agree to the bf16 bar
+    (both are bf16-rounded evaluations of the same exact recurrence)."""
+    cfg, inp = _case(1, 3, 64 * 33, 128, 128, 64, "bf16", index=521)
+    a = run_gpu(inp, "bf16", 64)
+    b = run_gpu(inp, "bf16", 64, segments=False)
+    compare({k: a[k] for k in ("o", "hT")}, {k: b[k] for k in ("o", "hT")}, TOL["bf16"])
+
+
+def test_bf16_long_context_sampled_units():
+    """BASELINE configs[2] (B=2 H=16 L=16384): 32 units, so the forward runs
+    segmented; three sampled units against the oracle (fwd + bwd)."""
+    cfg = synth.CONFIGS["long"]
+    assert _segmented(cfg.B, cfg.H, cfg.L)
+    inp = synth.make_inputs(cfg)
+    got = run_gpu(inp, "bf16", cfg.chunk)
+    for (b, h) in [(0, 0), (cfg.B - 1, cfg.H - 1), (1, 6)]:
+        one = {f: inp[f][b:b + 1, h:h + 1] for f in inp}
+        ref = run_oracle(one)
+        sub = {k: (None if v is None else v[b:b + 1, h:h + 1]) for k, v in got.items()}
+        compare(sub, ref, TOL["bf16"])

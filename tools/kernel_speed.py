@@ -50,12 +50,20 @@ def main():
         t_c = timed(lambda: dn.deltanet_fwd(q, k, v, beta, chunk=64, save_states=False,
                                             workspace=ws, want_hT=False, out=o))
         t_r = timed(lambda: dn.deltanet_recurrent_fwd(q, k, v, beta, want_hT=False, out=o))
+        d1 = dn.make_desc(B, H, L, D, D, 64, torch.bfloat16, save_states=False, segments=False)
+        ws1 = dn.alloc_workspace(d1, q.device)
+        t_1 = timed(lambda: dn.deltanet_fwd(q, k, v, beta, chunk=64, save_states=False,
+                                            workspace=ws1, want_hT=False, out=o,
+                                            segments=False))
         pr, pc = PAPER[L]
+        nseg_launches = dn.deltanet_launch_count(d, 0)
         rows.append({"L": L, "B": B, "recurrent_ms": t_r, "chunkwise_ms": t_c,
+                     "chunkwise_one_cta_per_unit_ms": t_1, "segmented": nseg_launches == 3,
                      "speedup": t_r / t_c, "paper_recurrent": pr, "paper_chunkwise": pc,
                      "paper_speedup": pr / pc})
-        print(f"L={L:6d} B={B:3d}  recurrent {t_r:8.3f} ms  chunkwise {t_c:7.3f} ms  "
-              f"speed-up {t_r / t_c:6.2f}x   (paper: {pr:.3f} / {pc:.3f} = {pr / pc:.2f}x)")
+        print(f"L={L:6d} B={B:3d}  recurrent {t_r:8.3f} ms  chunkwise {t_c:7.3f} ms "
+              f"(1 CTA/unit {t_1:7.3f} ms)  speed-up {t_r / t_c:6.2f}x   "
+              f"(paper: {pr:.3f} / {pc:.3f} = {pr / pc:.2f}x)")
     if out:
         json.dump({"what": "fig:kernel_speed on B200, d_head=128, B*L=16384, forward, bf16",
                    "rows": rows}, open(out, "w"), indent=1)

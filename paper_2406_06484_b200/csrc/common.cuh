@@ -73,5 +73,7 @@ size_t tc_scratch_bytes(const deltanet_desc* d);
 int tc_fwd(const Args& a, cudaStream_t s);
 int tc_bwd(const Args& a, cudaStream_t s);
 int tc_launch_count(const deltanet_desc* d, int which);
+int tc_fwd_segments(const deltanet_desc* d);
+int tc_seg_setup(Args& a);
 
 }  // namespace dn

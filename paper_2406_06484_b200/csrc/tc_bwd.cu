@@ -145,6 +145,10 @@ __device__ __forceinline__ void simt_signal(uint64_t* bar, int tid) {
   if (tid == 0) mbar_arrive(bar);
 }
 
+// SEG1 = pass 1 of the segment-parallel backward: only the
+// dH chain of the segment, from dH = 0 at its end, down to its start (the
+// segment-local dl/dH_start); no local gradients, no stores.
+template <bool SEG1>
 __global__ void __launch_bounds__(NT, 1)
     tc_bwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                   const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mDO,
@@ -178,14 +182,20 @@ __global__ void __launch_bounds__(NT, 1)
   const int wg = (tid >> 7) & 1, w = tid & 127, wwarp = w >> 5;
   const int r64 = wwarp * 16 + (lane & 15);  // M=64 accumulator row of this lane
   const bool lo = lane < 16;
-  const int unit = blockIdx.x;
-  const int L = a.L, NC = a.NC;
+  // segment of this CTA (tc_fwd.cu): local chunk c is global chunk cbase + c,
+  // token T0 + c*C; L counts tokens from T0
+  const int nseg = a.nseg > 1 ? a.nseg : 1;
+  const int unit = blockIdx.x / nseg, seg = blockIdx.x % nseg;
+  const int cbase = nseg > 1 ? seg * a.seg_len : 0;
+  const int NC = nseg > 1 ? min(a.seg_len, a.NC - cbase) : a.NC;
+  const int T0 = cbase * C;
+  const int L = a.L - T0;
   const bool l2 = (a.flags & DELTANET_L2NORM_QK) != 0;
   const float eps = a.eps;
-  const __nv_bfloat16* beta = (const __nv_bfloat16*)a.beta + (size_t)unit * L;
-  __nv_bfloat16* dbeta = (__nv_bfloat16*)a.dbeta + (size_t)unit * L;
-  const uint8_t* states = (const uint8_t*)a.states + (size_t)unit * NC * (D * D * 2);
-  const uint8_t* recs = (const uint8_t*)a.scratch + (size_t)unit * NC * REC_BYTES;
+  const __nv_bfloat16* beta = (const __nv_bfloat16*)a.beta + (size_t)unit * a.L + T0;
+  __nv_bfloat16* dbeta = (__nv_bfloat16*)a.dbeta + (size_t)unit * a.L + T0;
+  const uint8_t* states = (const uint8_t*)a.states + ((size_t)unit * a.NC + cbase) * (D * D * 2);
+  const uint8_t* recs = (const uint8_t*)a.scratch + ((size_t)unit * a.NC + cbase) * REC_BYTES;
 
   if (warp == 0) tmem_alloc<512>(&tslot);
   if (tid == 0) {
@@ -214,24 +224,28 @@ __global__ void __launch_bounds__(NT, 1)
     // dq staging (the other q slot) has been read out.
     // =====================================================================
     if (lane == 0) {
-      constexpr uint32_t MAIN_BYTES = 3 * TILE + D * D * 2 + C * C * 2;  // dO V Z | H | X
+      // SEG1 reads only dO and X besides q, k
+      constexpr uint32_t MAIN_BYTES =
+          SEG1 ? TILE + C * C * 2 : 3 * TILE + D * D * 2 + C * C * 2;  // dO V Z | H | X
       auto load_k = [&](int c, int slot) {  // own barrier per slot (one phase per use)
         mbar_expect_tx(&mb[MB_KL0 + slot], TILE);
-        tma_load_4d(smem + OFF_K + slot * TILE, &mK, 0, c * C, 0, unit, &mb[MB_KL0 + slot]);
+        tma_load_4d(smem + OFF_K + slot * TILE, &mK, 0, T0 + c * C, 0, unit, &mb[MB_KL0 + slot]);
       };
       auto load_rest = [&](int c) {  // dO, V, H_t, Z^T (opens the MB_MAIN phase, X included)
         mbar_expect_tx(&mb[MB_MAIN], MAIN_BYTES);
-        tma_load_4d(sDO, &mDO, 0, c * C, 0, unit, &mb[MB_MAIN]);
-        tma_load_4d(sV, &mV, 0, c * C, 0, unit, &mb[MB_MAIN]);
-        bulk_load(sH, states + (size_t)c * D * D * 2, D * D * 2, &mb[MB_MAIN]);
-        bulk_load(sZ, recs + (size_t)c * REC_BYTES + REC_Z, D * C * 2, &mb[MB_MAIN]);
+        tma_load_4d(sDO, &mDO, 0, T0 + c * C, 0, unit, &mb[MB_MAIN]);
+        if (!SEG1) {
+          tma_load_4d(sV, &mV, 0, T0 + c * C, 0, unit, &mb[MB_MAIN]);
+          bulk_load(sH, states + (size_t)c * D * D * 2, D * D * 2, &mb[MB_MAIN]);
+          bulk_load(sZ, recs + (size_t)c * REC_BYTES + REC_Z, D * C * 2, &mb[MB_MAIN]);
+        }
       };
       auto load_x = [&](int c) {
         bulk_load(sX, recs + (size_t)c * REC_BYTES + REC_X, C * C * 2, &mb[MB_MAIN]);
       };
       auto load_q = [&](int c, int slot) {
         mbar_expect_tx(&mb[MB_QL], TILE);
-        tma_load_4d(qu(slot), &mQ, 0, c * C, 0, unit, &mb[MB_QL]);
+        tma_load_4d(qu(slot), &mQ, 0, T0 + c * C, 0, unit, &mb[MB_QL]);
       };
       if (NC > 0) {
         load_k(NC - 1, 0);
@@ -242,14 +256,15 @@ __global__ void __launch_bounds__(NT, 1)
       mbar_arrive(&sg[SG_STG]);
 #pragma unroll 1
       for (int it = 0; it < NC; ++it) {
-        const int c = NC - 1 - it, t0 = c * C;
+        const int c = NC - 1 - it, t0 = T0 + c * C;
         const uint32_t ph = it & 1;
         if (it > 0) {  // tail of chunk c+1: its epilogue read q_hat / k_hat
           mbar_wait(&sg[SG_P8], ph ^ 1);
-          // dq / dk were staged in place over q_hat / k_hat of chunk c+1
-          tma_store_4d(&mDQ, qu((it + 1) & 1), 0, t0 + C, 0, unit);
-          tma_store_4d(&mDK, smem + OFF_K + ((it + 1) & 1) * TILE, 0, t0 + C, 0, unit);
-          bulk_commit();
+          if (!SEG1) {  // dq / dk were staged in place over q_hat / k_hat of chunk c+1
+            tma_store_4d(&mDQ, qu((it + 1) & 1), 0, t0 + C, 0, unit);
+            tma_store_4d(&mDK, smem + OFF_K + ((it + 1) & 1) * TILE, 0, t0 + C, 0, unit);
+            bulk_commit();
+          }
           bulk_wait_read0();           // both read out: the q slot takes dU'^T (P3),
           mbar_arrive(&sg[SG_STG]);    // the k slot chunk c-1's k
           if (c > 0) load_k(c - 1, (it + 1) & 1);
@@ -261,8 +276,10 @@ __global__ void __launch_bounds__(NT, 1)
           load_q(c - 1, (it + 1) & 1);
         }
         mbar_wait(&sg[SG_P5], ph);
-        tma_store_4d(&mDV, sDV, 0, t0, 0, unit);
-        bulk_commit();
+        if (!SEG1) {
+          tma_store_4d(&mDV, sDV, 0, t0, 0, unit);
+          bulk_commit();
+        }
         if (c > 0) {
           mbar_wait(&mb[MB_LD], ph);  // dO, H^T, U' read by M5; V once dV is read out
           bulk_wait_read0();
@@ -273,9 +290,11 @@ __global__ void __launch_bounds__(NT, 1)
       }
       if (NC > 0) {
         mbar_wait(&sg[SG_P8], (NC - 1) & 1);
-        tma_store_4d(&mDQ, qu((NC - 1) & 1), 0, 0, 0, unit);
-        tma_store_4d(&mDK, smem + OFF_K + ((NC - 1) & 1) * TILE, 0, 0, 0, unit);
-        bulk_commit();
+        if (!SEG1) {
+          tma_store_4d(&mDQ, qu((NC - 1) & 1), 0, T0, 0, unit);
+          tma_store_4d(&mDK, smem + OFF_K + ((NC - 1) & 1) * TILE, 0, T0, 0, unit);
+          bulk_commit();
+        }
       }
       bulk_wait0();
     }
@@ -312,11 +331,13 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
           for (int k0 = 0; k0 < D; k0 += 16)
             mma_bf16(tm + TM_DU, desc_k(aDH, D, k0), desc_k(aK, C, k0), idd, k0 > 0);
+          if (!SEG1) {
 #pragma unroll
-          for (int k0 = 0; k0 < D; k0 += 16) {
-            mma_bf16(tm + TM_KH, desc_k(aK, C, k0), desc_k(aH, D, k0), idg, k0 > 0);
-            mma_bf16(tm + TM_KH + LO16, desc_k(aK, C, k0), desc_k(aH + HALF_ROWS, D, k0), idg,
-                     k0 > 0);
+            for (int k0 = 0; k0 < D; k0 += 16) {
+              mma_bf16(tm + TM_KH, desc_k(aK, C, k0), desc_k(aH, D, k0), idg, k0 > 0);
+              mma_bf16(tm + TM_KH + LO16, desc_k(aK, C, k0), desc_k(aH + HALF_ROWS, D, k0), idg,
+                       k0 > 0);
+            }
           }
           mma_commit(&mb[MB_R]);
         }
@@ -360,23 +381,27 @@ __global__ void __launch_bounds__(NT, 1)
             mma_bf16(tm + TM_P + LO16, desc_mn(aX, C, k0), desc_k(aDUP + HALF_ROWS, D, k0), idp,
                      k0 > 0);
           }
+          if (!SEG1) {
 #pragma unroll
-          for (int k0 = 0; k0 < D; k0 += 16)
-            mma_bf16(tm + TM_DX, desc_mn(aDUP, D, k0), desc_k(aR, C, k0), idp, k0 > 0);
+            for (int k0 = 0; k0 < D; k0 += 16)
+              mma_bf16(tm + TM_DX, desc_mn(aDUP, D, k0), desc_k(aR, C, k0), idp, k0 > 0);
+          }
           mma_commit(&mb[MB_P]);
           const uint32_t id1 = idesc_bf16(128, 128, true, true);
           const uint32_t id_k1 = idesc_bf16(64, 128, true, true);
 #pragma unroll
           for (int k0 = 0; k0 < C; k0 += 16)
             mma_bf16(tm + TM_DH, desc_mn(aDO, C, k0), desc_mn(aQ, C, k0), id1, 1);
+          if (!SEG1) {
 #pragma unroll
-          for (int k0 = 0; k0 < D; k0 += 16)
-            mma_bf16(tm + TM_DK, desc_mn(aUP, D, k0), desc_mn(aDH, D, k0), id_k1, k0 > 0);
-          // K_hat K_hat^T (k normalised in P3) for the dbeta term of P7
-          const uint32_t idg = idesc_bf16(64, 64, false, false);
+            for (int k0 = 0; k0 < D; k0 += 16)
+              mma_bf16(tm + TM_DK, desc_mn(aUP, D, k0), desc_mn(aDH, D, k0), id_k1, k0 > 0);
+            // K_hat K_hat^T (k normalised in P3) for the dbeta term of P7
+            const uint32_t idg = idesc_bf16(64, 64, false, false);
 #pragma unroll
-          for (int k0 = 0; k0 < D; k0 += 16)
-            mma_bf16(tm + TM_G + LO16, desc_k(aK, C, k0), desc_k(aK, C, k0), idg, k0 > 0);
+            for (int k0 = 0; k0 < D; k0 += 16)
+              mma_bf16(tm + TM_G + LO16, desc_k(aK, C, k0), desc_k(aK, C, k0), idg, k0 > 0);
+          }
         }
         ISTAMP(22);
 
@@ -391,6 +416,11 @@ __global__ void __launch_bounds__(NT, 1)
           for (int k0 = 0; k0 < C; k0 += 16)
             mma_bf16(tm + TM_DH, desc_mn(aDV, C, k0), desc_mn(aK, C, k0), id2, 1);
           mma_commit(&mb[MB_DH]);
+          if (SEG1) {  // the chain is all: dO, X and the q / k slots are free
+            mma_commit(&mb[MB_LD]);
+            mma_commit(&mb[MB_GB]);
+            continue;
+          }
           const uint32_t id_da = idesc_bf16(64, 64, false, true);
           const uint32_t id_y = idesc_bf16(64, 64, true, true);
           const uint32_t id_q = idesc_bf16(64, 128, false, true);
@@ -456,7 +486,11 @@ __global__ void __launch_bounds__(NT, 1)
     {
       // dH^T <- dhT^T in TMEM (lane dv = w; columns split by warpgroup) and
       // its bf16 image for the first chunk
-      const float* dhT = a.dhT ? a.dhT + (size_t)unit * D * D : nullptr;
+      // the cotangent at this segment's end: dhT for the last segment, the
+      // scanned dl/dH for the others (pass 3), zero in pass 1
+      const float* dhT = SEG1 ? nullptr
+                         : (seg < nseg - 1) ? a.hseg + ((size_t)unit * nseg + seg) * D * D
+                         : a.dhT ? a.dhT + (size_t)unit * D * D : nullptr;
 #pragma unroll 1
       for (int c0 = 64 * wg; c0 < 64 * wg + 64; c0 += 16) {
         uint32_t r[16];
@@ -519,7 +553,7 @@ __global__ void __launch_bounds__(NT, 1)
       mbar_wait(&mb[MB_MAIN], ph);
       row_norms(sK, ss, nk);
       BSTAMP(1);
-      if (l2) {  // U'^T[dv][t] = Z^T[dv][t] * max(|k_t|, eps)  (row dv = w)
+      if (l2 && !SEG1) {  // U'^T[dv][t] = Z^T[dv][t] * max(|k_t|, eps)  (row dv = w)
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           const int col = 32 * wg + g * 8;
@@ -530,23 +564,25 @@ __global__ void __launch_bounds__(NT, 1)
           il_store8(sUP, D, w, col, z8);
         }
       }
-      mbar_wait(&mb[MB_R], ph);
-      fence_after_sync();
-      BSTAMP(2);
-      {
-        // (K H) row r64: lanes < 16 hold columns [0,64), lanes >= 16 [64,128);
-        // this warpgroup takes 32 of each half
-        float f[32];
-        ld32(tm, wwarp, TM_KH + 32 * wg, f);
-        const float si = ss[r64];
-        const int c0 = (lo ? 0 : 64) + 32 * wg;
+      if (!SEG1) {  // (SEG1 needs no R)
+        mbar_wait(&mb[MB_R], ph);
+        fence_after_sync();
+        BSTAMP(2);
+        {
+          // (K H) row r64: lanes < 16 hold columns [0,64), lanes >= 16 [64,128);
+          // this warpgroup takes 32 of each half
+          float f[32];
+          ld32(tm, wwarp, TM_KH + 32 * wg, f);
+          const float si = ss[r64];
+          const int c0 = (lo ? 0 : 64) + 32 * wg;
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          float v8[8];
-          il_load8(sV, C, r64, c0 + g * 8, v8);
+          for (int g = 0; g < 4; ++g) {
+            float v8[8];
+            il_load8(sV, C, r64, c0 + g * 8, v8);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) v8[e] = fmaf(-si, f[g * 8 + e], v8[e]);
-          il_store8(sR, C, r64, c0 + g * 8, v8);
+            for (int e = 0; e < 8; ++e) v8[e] = fmaf(-si, f[g * 8 + e], v8[e]);
+            il_store8(sR, C, r64, c0 + g * 8, v8);
+          }
         }
       }
       mbar_wait(&mb[MB_QL], ph);
@@ -608,50 +644,64 @@ __global__ void __launch_bounds__(NT, 1)
       simt_signal(&sg[SG_P3], tid);
       BSTAMP(6);
 
-      // ================= P5: P, R -> dV, dbeta part ; dX
+      // ================= P5: P, R -> dV, dbeta part ; dX  (SEG1: dV only)
       if (tid < C && c > 0) bnext = __bfloat162float(beta[t0 - C + tid]);
       mbar_wait(&mb[MB_P], ph);
       fence_after_sync();
       BSTAMP(7);
-      {
-        // lanes < 16: columns [0,64), lanes >= 16: [64,128) of row r64, for
-        // both P (TM_P) and K H (TM_KH); 32 of each half per warpgroup
-        float p[32], f[32];
+      if (SEG1) {  // dV = diag(beta) P only (the chain's K_hat^T dV)
+        float p[32];
         ld32(tm, wwarp, TM_P + 32 * wg, p);
-        ld32(tm, wwarp, TM_KH + 32 * wg, f);
-        const float bt = sb[r64], si = ss[r64];
+        const float bt = sb[r64];
         const int c0 = (lo ? 0 : 64) + 32 * wg;
-        float db = 0.f;
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
-          float v8[8], dv8[8];
-          il_load8(sV, C, r64, c0 + g * 8, v8);
+          float dv8[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const float rr = fmaf(-si, f[g * 8 + e], v8[e]);
-            db = fmaf(p[g * 8 + e], rr, db);  // P . R
-            dv8[e] = bt * p[g * 8 + e];
-          }
+          for (int e = 0; e < 8; ++e) dv8[e] = bt * p[g * 8 + e];
           il_store8(sDV, C, r64, c0 + g * 8, dv8);
         }
-        db += __shfl_xor_sync(0xffffffffu, db, 16);
-        if (lo) db1[wg * C + r64] = db;
-      }
-#pragma unroll 1
-      for (int cc = 0; cc < 2; ++cc) {  // dX = dX' diag(beta) (lanes < 16: dX' rows)
-        const int col = 32 * wg + 16 * cc;
-        float f[16], x[8];
-        ld16f(tm, wwarp, TM_DX + col, f);
+      } else {
+        {
+          // lanes < 16: columns [0,64), lanes >= 16: [64,128) of row r64, for
+          // both P (TM_P) and K H (TM_KH); 32 of each half per warpgroup
+          float p[32], f[32];
+          ld32(tm, wwarp, TM_P + 32 * wg, p);
+          ld32(tm, wwarp, TM_KH + 32 * wg, f);
+          const float bt = sb[r64], si = ss[r64];
+          const int c0 = (lo ? 0 : 64) + 32 * wg;
+          float db = 0.f;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) x[e] = __shfl_xor_sync(0xffffffffu, f[8 + e], 16);
-        if (lo) {
+          for (int g = 0; g < 4; ++g) {
+            float v8[8], dv8[8];
+            il_load8(sV, C, r64, c0 + g * 8, v8);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) x[e] = f[e];
+            for (int e = 0; e < 8; ++e) {
+              const float rr = fmaf(-si, f[g * 8 + e], v8[e]);
+              db = fmaf(p[g * 8 + e], rr, db);  // P . R
+              dv8[e] = bt * p[g * 8 + e];
+            }
+            il_store8(sDV, C, r64, c0 + g * 8, dv8);
+          }
+          db += __shfl_xor_sync(0xffffffffu, db, 16);
+          if (lo) db1[wg * C + r64] = db;
         }
-        const int c8 = col + (lo ? 0 : 8);
+#pragma unroll 1
+        for (int cc = 0; cc < 2; ++cc) {  // dX = dX' diag(beta) (lanes < 16: dX' rows)
+          const int col = 32 * wg + 16 * cc;
+          float f[16], x[8];
+          ld16f(tm, wwarp, TM_DX + col, f);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) x[e] *= sb[c8 + e];
-        il_store8(sDX, C, r64, c8, x);
+          for (int e = 0; e < 8; ++e) x[e] = __shfl_xor_sync(0xffffffffu, f[8 + e], 16);
+          if (lo) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) x[e] = f[e];
+          }
+          const int c8 = col + (lo ? 0 : 8);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) x[e] *= sb[c8 + e];
+          il_store8(sDX, C, r64, c8, x);
+        }
       }
       simt_signal(&sg[SG_P5], tid);
       BSTAMP(8);
@@ -667,6 +717,10 @@ __global__ void __launch_bounds__(NT, 1)
         simt_signal(&sg[SG_DHI], tid);
       }
       BSTAMP(9);
+      if (SEG1) {  // pass 1 stops at the chain; the TMA warp reloads the k slot
+        simt_signal(&sg[SG_P8], tid);
+        continue;
+      }
 
       // ================= P6: dA -> bf16 (masked) | Y -> bf16
       mbar_wait(&mb[MB_A], ph);
@@ -768,19 +822,59 @@ __global__ void __launch_bounds__(NT, 1)
       BSTAMP(15);
     }
 
-    // dh0 = dH (orientation [dk][dv]; lane dv = w, columns split)
-    if (a.dh0) {
+    // dh0 = dH (orientation [dk][dv]; lane dv = w, columns split): segment 0's
+    // (pass 3); pass 1 writes the segment-local dl/dH_start instead
+    float* dho = SEG1 ? a.hloc + ((size_t)unit * nseg + seg) * D * D
+                 : (seg == 0 && a.dh0) ? a.dh0 + (size_t)unit * D * D : nullptr;
+    if (SEG1 && NC > 0) mbar_wait(&mb[MB_DH], (NC - 1) & 1);  // the last chunk's dH update
+    if (dho) {
       fence_after_sync();
-      float* dh0 = a.dh0 + (size_t)unit * D * D;
       float f[64];
       ld64(tm, wwarp, TM_DH + 64 * wg, f);
 #pragma unroll
-      for (int e = 0; e < 64; ++e) dh0[(size_t)(64 * wg + e) * D + w] = f[e];
+      for (int e = 0; e < 64; ++e) dho[(size_t)(64 * wg + e) * D + w] = f[e];
     }
   }
   cta_sync();
   if (tid == 0) CTA_STAMP(1, gtimer());
   if (warp == 0) tmem_dealloc<512>(tm);
+}
+
+// Pass 2 of the segment-parallel backward: the cotangent at each segment's
+// end, dl/dH_end(s-1) = dl/dH_start(s) = Psi_s dl/dH_end(s) + dH_loc(s), from
+// dl/dH_end(S-1) = dhT (H = S^T, [dk][dv]; Psi from the forward's pass 1 --
+// the backward's per-chunk maps are the transposes of the forward's).  A CTA
+// scans one 16-column block; fp32.
+__global__ void __launch_bounds__(256) seg_scan_bwd_kernel(Args a) {
+  __shared__ float Hs[D][16];
+  const int unit = blockIdx.x, j0 = blockIdx.y * 16, nseg = a.nseg;
+  const int tid = threadIdx.x, i = tid >> 1, jj = (tid & 1) * 8;
+  for (int e = tid; e < D * 16; e += blockDim.x) {
+    const int r = e / 16, cc = e % 16;
+    Hs[r][cc] = a.dhT ? a.dhT[(size_t)unit * D * D + (size_t)r * D + j0 + cc] : 0.f;
+  }
+  __syncthreads();
+  for (int sg = nseg - 1; sg >= 1; --sg) {
+    const float* psi = a.psi + ((size_t)unit * nseg + sg) * D * D + (size_t)i * D;
+    const float* hl = a.hloc + ((size_t)unit * nseg + sg) * D * D + (size_t)i * D + j0 + jj;
+    float acc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = hl[e];
+#pragma unroll 4
+    for (int r = 0; r < D; ++r) {
+      const float pv = psi[r];  // Psi[i][r]
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = fmaf(pv, Hs[r][jj + e], acc[e]);
+    }
+    __syncthreads();
+    float* out = a.hseg + ((size_t)unit * nseg + sg - 1) * D * D + (size_t)i * D + j0 + jj;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      Hs[i][jj + e] = acc[e];
+      out[e] = acc[e];
+    }
+    __syncthreads();
+  }
 }
 
 }  // namespace
@@ -790,14 +884,17 @@ int tc_fwd(const Args& a, cudaStream_t s);
 int tc_bwd(const Args& a0, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(tc_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(tc_bwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(tc_bwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              SMEM_BYTES) != cudaSuccess)
       return DELTANET_ERR_CUDA;
     attr = true;
   }
   Args a = a0;
   if (!(a.flags & DELTANET_SAVE_STATES)) {
-    // recompute the chunk states with the forward kernel (no O store)
+    // recompute the chunk states (and the segment transitions) with the
+    // forward kernel (no O store)
     Args f = a0;
     f.flags |= DELTANET_SAVE_STATES;
     f.o = nullptr;
@@ -812,7 +909,15 @@ int tc_bwd(const Args& a0, cudaStream_t s) {
       !make_il_map(&mDQ, a.dq, BH, a.L, D, C) || !make_il_map(&mDK, a.dk, BH, a.L, D, C) ||
       !make_il_map(&mDV, a.dv, BH, a.L, D, C))
     return DELTANET_ERR_CUDA;
-  tc_bwd_kernel<<<BH, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mDO, mDQ, mDK, mDV, a);
+  const int nseg = tc_seg_setup(a);
+  if (nseg <= 1) {
+    tc_bwd_kernel<false><<<BH, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mDO, mDQ, mDK, mDV, a);
+    return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
+  }
+  // segment-parallel backward, with the forward's Psi
+  tc_bwd_kernel<true><<<BH * nseg, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mDO, mDQ, mDK, mDV, a);
+  seg_scan_bwd_kernel<<<dim3(BH, D / 16), 256, 0, s>>>(a);
+  tc_bwd_kernel<false><<<BH * nseg, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mDO, mDQ, mDK, mDV, a);
   return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
 }
 

@@ -834,11 +834,30 @@ size_t tc_scratch_bytes(const deltanet_desc* d) {
   return round256(rec_bytes(d->B, d->H, d->L)) + seg;
 }
 
-// fwd: 1 kernel (3 when segmented); bwd: 1 kernel, plus the state-recompute
-// forward without SAVE_STATES
+// fwd: 1 kernel (3 when segmented); bwd: 1 kernel (3 when segmented), plus
+// the state-recompute forward without SAVE_STATES
 int tc_launch_count(const deltanet_desc* d, int which) {
   const int f = tc_fwd_segments(d) > 1 ? 3 : 1;
-  return which == 0 ? f : ((d->flags & DELTANET_SAVE_STATES) ? 1 : 1 + f);
+  return which == 0 ? f : ((d->flags & DELTANET_SAVE_STATES) ? f : 2 * f);
+}
+
+// Segment layout shared by the forward and the backward: nseg, seg_len and
+// the scratch after the records (H_loc | Psi | H_start per (unit, segment);
+// the backward reuses H_loc and H_start for dl/dH).  Returns nseg.
+int tc_seg_setup(Args& a) {
+  deltanet_desc d;
+  d.B = a.B; d.H = a.H; d.L = a.L; d.Dk = a.Dk; d.Dv = a.Dv; d.chunk = a.C;
+  d.dtype = DELTANET_BF16; d.flags = a.flags; d.l2_eps = a.eps;
+  const int nseg = tc_fwd_segments(&d);
+  a.nseg = nseg > 1 ? nseg : 1;
+  if (nseg <= 1) return 1;
+  const int BH = a.B * a.H;
+  a.seg_len = (a.NC + nseg - 1) / nseg;
+  float* base = (float*)((char*)a.scratch + round256(rec_bytes(a.B, a.H, a.L)));
+  a.hloc = base;
+  a.psi = a.hloc + (size_t)BH * nseg * DK * DV;
+  a.hseg = a.psi + (size_t)BH * nseg * DK * DK;
+  return nseg;
 }
 
 int tc_fwd(const Args& a0, cudaStream_t s) {
@@ -858,21 +877,11 @@ int tc_fwd(const Args& a0, cudaStream_t s) {
       !make_il_map(&mV, a.v, BH, a.L, DV, C) ||
       !make_il_map(&mO, a.o ? a.o : a.v, BH, a.L, DV, C))  // o == null: states only
     return DELTANET_ERR_CUDA;
-  deltanet_desc d;
-  d.B = a.B; d.H = a.H; d.L = a.L; d.Dk = a.Dk; d.Dv = a.Dv; d.chunk = a.C;
-  d.dtype = DELTANET_BF16; d.flags = a.flags; d.l2_eps = a.eps;
-  const int nseg = tc_fwd_segments(&d);
+  const int nseg = tc_seg_setup(a);
   if (nseg <= 1) {
-    a.nseg = 1;
     tc_fwd_kernel<false><<<BH, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);
     return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
   }
-  a.nseg = nseg;
-  a.seg_len = (a.NC + nseg - 1) / nseg;
-  float* base = (float*)((char*)a.scratch + round256(rec_bytes(a.B, a.H, a.L)));
-  a.hloc = base;
-  a.psi = a.hloc + (size_t)BH * nseg * DK * DV;
-  a.hseg = a.psi + (size_t)BH * nseg * DK * DK;
   tc_fwd_kernel<true><<<BH * nseg, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);   // pass 1
   seg_scan_kernel<<<dim3(BH, DV / 16), 256, 0, s>>>(a);                     // pass 2
   tc_fwd_kernel<false><<<BH * nseg, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);  // pass 3

@@ -200,3 +200,20 @@ def test_bf16_long_context_sampled_units():
         ref = run_oracle(one)
         sub = {k: (None if v is None else v[b:b + 1, h:h + 1]) for k, v in got.items()}
         compare(sub, ref, TOL["bf16"])
+
+
+@pytest.mark.parametrize("name", ["hd256", "sharded"])
+def test_bf16_remaining_configs_sampled_units(name):
+    """BASELINE configs[3] (d=256 on the CUDA-core path: its fp32 state does
+    not fit TMEM beside the tcgen05 kernel's accumulators) and
+    configs[4] (B=64: 1024 units, several waves) at full size; two sampled
+    units against the oracle."""
+    cfg = synth.CONFIGS[name]
+    units = [(0, 0), (cfg.B - 1, cfg.H - 1)]
+    inp = synth.make_inputs(cfg)
+    got = run_gpu(inp, "bf16", cfg.chunk)
+    for (b, h) in units:
+        one = {f: inp[f][b:b + 1, h:h + 1] for f in inp}
+        ref = run_oracle(one)
+        sub = {k: (None if v is None else v[b:b + 1, h:h + 1]) for k, v in got.items()}
+        compare(sub, ref, TOL["bf16"])

@@ -226,6 +226,44 @@ def measure_prologue(dn, dev, B, H, L, D, peaks):
             "fwd_roofline": roof(bf, t_f), "bwd_roofline": roof(bb, t_b)}
 
 
+def measure_long_context(dn, dev):
+    """Side measurement (outside the timed step): BASELINE configs[2], the
+    long-context shape B=2 H=16 L=16384 (32 units on 148 SMs), fwd+bwd with
+    the segment-parallel kernels and with one CTA per unit."""
+    import torch
+    stream = torch.cuda.current_stream(dev)
+    B, Hh, Ll, D = 2, 16, 16384, 128
+    g = torch.Generator(device=dev).manual_seed(13)
+    mk = lambda: torch.randn((B, Hh, Ll, D), device=dev, generator=g).to(torch.bfloat16)
+    q, k, v, dO = mk(), mk(), mk(), mk()
+    beta = torch.rand((B, Hh, Ll), device=dev, generator=g).to(torch.bfloat16)
+    o = torch.empty_like(v)
+    grads = (torch.empty_like(q), torch.empty_like(k), torch.empty_like(v),
+             torch.empty_like(beta))
+    res = {"workload": f"B={B} H={Hh} L={Ll} d={D} chunk=64 bf16 fwd+bwd"}
+    for seg in (True, False):
+        d = dn.make_desc(B, Hh, Ll, D, D, 64, torch.bfloat16, segments=seg)
+        ws = dn.alloc_workspace(d, dev)
+
+        def step():
+            dn.deltanet_fwd(q, k, v, beta, workspace=ws, want_hT=False, out=o, segments=seg)
+            dn.deltanet_bwd(q, k, v, beta, dO, workspace=ws, want_dh0=False, out=grads,
+                            segments=seg)
+        step()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(5):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        t = e0.elapsed_time(e1) * 1e-3 / 5
+        res["segmented" if seg else "one_cta_per_unit"] = {
+            "ms_per_step": t * 1e3, "tokens_per_s": B * Ll / t,
+            "launches": dn.deltanet_launch_count(d, 0) + dn.deltanet_launch_count(d, 1)}
+    return res
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -490,10 +528,11 @@ def main():
     base = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         base = cpu_baseline()
-    rec = pro = None
+    rec = pro = lng = None
     if rank == 0 and not args.no_recurrent and not args.force_simt:
         rec = measure_recurrent(dn, dev, q, k, v, beta, t_fwd, peaks)
         pro = measure_prologue(dn, dev, B_PER_RANK, H, L, D, peaks)
+        lng = measure_long_context(dn, dev)
 
     if rank == 0:
         line = {
@@ -521,6 +560,8 @@ def main():
             line["recurrent"] = rec
         if pro:
             line["prologue"] = pro
+        if lng:
+            line["long_context"] = lng
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.barrier()

@@ -106,6 +106,26 @@ class ClockSampler:
         self.thread = threading.Thread(target=loop, daemon=True)
         self.thread.start()
 
+    def sample_now(self):
+        """One synchronous sample from the calling thread."""
+        if not self.ok:
+            return
+        nv, h = self.nv, self.h
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        try:
+            self.rows.append((time.perf_counter(), nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                              nv.nvmlDeviceGetPowerUsage(h) / 1000.0, int(get_reasons(h))))
+        except Exception:
+            pass
+
+    def poll_until(self, event):
+        """Sample from the launching thread while the GPU runs the queued
+        timed region (the sampler thread may be starved of the GIL)."""
+        while not event.query():
+            self.sample_now()
+            time.sleep(0.002)
+
     def begin(self):
         self.window[0] = time.perf_counter()
 
@@ -413,6 +433,7 @@ def main():
         ev[i][1].record(stream)
         bwd()
         ev[i][2].record(stream)
+    clocks.poll_until(ev[-1][2])
     torch.cuda.synchronize(dev)
     clocks.end()
     if ws > 1:

@@ -217,3 +217,29 @@ def test_bf16_remaining_configs_sampled_units(name):
         ref = run_oracle(one)
         sub = {k: (None if v is None else v[b:b + 1, h:h + 1]) for k, v in got.items()}
         compare(sub, ref, TOL["bf16"])
+
+
+# ------------------------------------------------- tcgen05 edge cases
+
+@pytest.mark.parametrize("L", [1, 37, 64, 128, 64 * 41 + 1])
+def test_bf16_tc_lengths(L):
+    """tcgen05 path: a single partial chunk, exact multiples of C, and (at
+    64*41+1 with one unit) a segmented run whose last segment is short."""
+    import paper_2406_06484_b200 as dn
+    H = 1 if L > 1000 else 2
+    assert dn.deltanet_path(dn.make_desc(1, H, L, 128, 128, 64, torch.bfloat16)) == 1
+    cfg, inp = _case(1, H, L, 128, 128, 64, "bf16", index=530 + L % 97)
+    got = run_gpu(inp, "bf16", 64)
+    compare(got, run_oracle(inp), TOL["bf16"])
+
+
+def test_bf16_tc_no_l2_unit_keys():
+    """tcgen05 path without the in-kernel L2 normalisation (flag off) on keys
+    and queries normalised by the caller: same result as the flag on."""
+    cfg, inp = _case(2, 2, 300, 128, 128, 64, "bf16", index=540)
+    for f in ("q", "k"):
+        x = inp[f].astype(np.float64)
+        x = x / np.maximum(np.linalg.norm(x, axis=-1, keepdims=True), 1e-6)
+        inp[f] = synth.round_to_bf16(x.astype(np.float32))
+    got = run_gpu(inp, "bf16", 64, l2norm=False)
+    compare(got, run_oracle(inp, l2norm=False), TOL["bf16"])

@@ -559,8 +559,11 @@ __global__ void __launch_bounds__(NT, 1)
           const int col = 32 * wg + g * 8;
           float z8[8];
           il_load8(sUP, D, w, col, z8);
+          const float4 n0 = *reinterpret_cast<const float4*>(nk + col);
+          const float4 n1 = *reinterpret_cast<const float4*>(nk + col + 4);
+          const float nn[8] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
 #pragma unroll
-          for (int e = 0; e < 8; ++e) z8[e] *= fmaxf(nk[col + e], eps);
+          for (int e = 0; e < 8; ++e) z8[e] *= fmaxf(nn[e], eps);
           il_store8(sUP, D, w, col, z8);
         }
       }
@@ -637,7 +640,13 @@ __global__ void __launch_bounds__(NT, 1)
         float f[32];
         ld32(tm, wwarp, TM_DU + 32 * wg, f);
 #pragma unroll
-        for (int e = 0; e < 32; ++e) f[e] *= ss[32 * wg + e];
+        for (int e = 0; e < 32; e += 4) {  // vector broadcast loads of s
+          const float4 s4 = *reinterpret_cast<const float4*>(ss + 32 * wg + e);
+          f[e] *= s4.x;
+          f[e + 1] *= s4.y;
+          f[e + 2] *= s4.z;
+          f[e + 3] *= s4.w;
+        }
 #pragma unroll
         for (int g = 0; g < 4; ++g) il_store8(sDUP, D, w, 32 * wg + g * 8, f + g * 8);
       }
@@ -698,8 +707,10 @@ __global__ void __launch_bounds__(NT, 1)
             for (int e = 0; e < 8; ++e) x[e] = f[e];
           }
           const int c8 = col + (lo ? 0 : 8);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) x[e] *= sb[c8 + e];
+          const float4 b0 = *reinterpret_cast<const float4*>(sb + c8);
+          const float4 b1 = *reinterpret_cast<const float4*>(sb + c8 + 4);
+          x[0] *= b0.x; x[1] *= b0.y; x[2] *= b0.z; x[3] *= b0.w;
+          x[4] *= b1.x; x[5] *= b1.y; x[6] *= b1.z; x[7] *= b1.w;
           il_store8(sDX, C, r64, c8, x);
         }
       }

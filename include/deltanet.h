@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define DELTANET_ABI_VERSION 3
+#define DELTANET_ABI_VERSION 4
 
 typedef enum {
   DELTANET_BF16 = 0, /* bf16 I/O, fp32 accumulation (BASELINE.json north_star) */
@@ -160,13 +160,63 @@ int deltanet_prologue_bwd(const deltanet_desc* d, const void* xq,
                           void* dxb, float* dwq, float* dwk, float* dwv,
                           void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- Context parallelism ----
+ * A sequence split into P consecutive parts (one per GPU, or per call) is
+ * processed part-locally, with the parts' boundary states stitched by the
+ * affine composition of the per-chunk state update (§3.2 Eq. 8,
+ * line 166: S_{t+1} = S_t (I - W_t^T K_t) + U_t^T K_t).  Over a part p the
+ * composition is, in the orientation H = S^T,
+ *   H_end = Psi_p^T H_start + Hloc_p,   Psi_p = prod_t (I - W_t^T K_t) [Dk,Dk]
+ * (the product over the part's chunks in order; Hloc_p the part's end state
+ * from H_start = 0), and the backward's cotangent chain is its adjoint,
+ *   dH_start = Psi_p dH_end + dHloc_p
+ * (dHloc_p = dl/dH_start of the part with dH_end = 0).  A context-parallel
+ * fwd is: deltanet_fwd_transition on each part; gather (Psi, Hloc) of all
+ * parts (e.g. NCCL all_gather); deltanet_state_scan(part, reverse=0) gives
+ * the part's H_start; deltanet_fwd with h0 = H_start.  The bwd:
+ * deltanet_bwd_transition; gather dHloc; deltanet_state_scan(reverse=1)
+ * gives dhT of the part; deltanet_bwd with h0 = H_start, dhT = that.
+ * These three calls need the tcgen05 path's shapes (bf16, Dk = Dv = 128,
+ * chunk 64, no DELTANET_FORCE_SIMT; else UNSUPPORTED); L = 0 is allowed
+ * (Psi = I, Hloc = 0).  Psi and the states are fp32; a part's Psi, Hloc,
+ * dHloc have the layout [B,H,128,128] (row i of Psi = row i of the matrix). */
+
+/* Psi [B,H,Dk,Dk] and Hloc [B,H,Dk,Dv] of this call's sequence (one
+ * launch; no workspace: the chain is not stored). */
+int deltanet_fwd_transition(const deltanet_desc* d, const void* q,
+                            const void* k, const void* v, const void* beta,
+                            float* psi, float* hloc, void* stream);
+
+/* dHloc [B,H,Dk,Dv] of this call's sequence for the cotangent dO.  The
+ * workspace (deltanet_workspace_bytes(d)) must hold what deltanet_fwd with
+ * DELTANET_SAVE_STATES wrote over the same q, k, v, beta (any h0) when the
+ * flag is set; without it the per-chunk records are recomputed into it. */
+int deltanet_bwd_transition(const deltanet_desc* d, const void* q,
+                            const void* k, const void* v, const void* beta,
+                            const void* dO, float* dhloc, void* workspace,
+                            size_t workspace_bytes, void* stream);
+
+/* Boundary state of part `part` of nparts from the gathered transitions
+ * psi_all [nparts][B,H,Dk,Dk] and loc_all [nparts][B,H,Dk,Dv] (fp32):
+ *   reverse = 0: out = H_start(part) = fold over p = 0 .. part-1 of
+ *                H <- Psi_p^T H + Hloc_p, from H = edge (h0; NULL = 0);
+ *   reverse = 1: out = dH_end(part) = fold over p = nparts-1 down to part+1
+ *                of G <- Psi_p G + dHloc_p, from G = edge (dhT; NULL = 0).
+ * out [B,H,Dk,Dv] may alias edge.  fp32 CUDA-core arithmetic. */
+int deltanet_state_scan(const deltanet_desc* d, int nparts, int part,
+                        int reverse, const float* psi_all,
+                        const float* loc_all, const float* edge, float* out,
+                        void* stream);
+
 /* Which kernel family a descriptor dispatches to: 1 = tcgen05/TMEM/TMA
  * sm_100a path, 0 = CUDA-core (SIMT) path, -1 = unsupported descriptor. */
 int deltanet_path(const deltanet_desc* d);
 
 /* Number of kernel launches deltanet_fwd (which=0), deltanet_bwd (which=1),
- * deltanet_recurrent_fwd (2), deltanet_prologue_fwd (3) or
- * deltanet_prologue_bwd (4) issues for this descriptor (launch accounting). */
+ * deltanet_recurrent_fwd (2), deltanet_prologue_fwd (3),
+ * deltanet_prologue_bwd (4), deltanet_fwd_transition (5),
+ * deltanet_bwd_transition (6) or deltanet_state_scan (7) issues for this
+ * descriptor (launch accounting). */
 int deltanet_launch_count(const deltanet_desc* d, int which);
 
 /* Human-readable message for an error code (static storage). */

@@ -41,7 +41,8 @@ class deltanet_desc(ctypes.Structure):
 EXPORTED = ("deltanet_workspace_bytes", "deltanet_fwd", "deltanet_bwd", "deltanet_path",
             "deltanet_launch_count", "deltanet_strerror", "deltanet_abi_version",
             "deltanet_recurrent_fwd", "deltanet_prologue_fwd", "deltanet_prologue_bwd",
-            "deltanet_prologue_workspace_bytes")
+            "deltanet_prologue_workspace_bytes", "deltanet_fwd_transition",
+            "deltanet_bwd_transition", "deltanet_state_scan")
 
 _lib = None
 
@@ -71,6 +72,12 @@ def load_library(path: str = LIB_PATH):
     lib.deltanet_prologue_bwd.restype = ctypes.c_int
     lib.deltanet_prologue_workspace_bytes.argtypes = [D]
     lib.deltanet_prologue_workspace_bytes.restype = ctypes.c_size_t
+    lib.deltanet_fwd_transition.argtypes = [D] + [P] * 7
+    lib.deltanet_fwd_transition.restype = ctypes.c_int
+    lib.deltanet_bwd_transition.argtypes = [D] + [P] * 7 + [ctypes.c_size_t, P]
+    lib.deltanet_bwd_transition.restype = ctypes.c_int
+    lib.deltanet_state_scan.argtypes = [D, ctypes.c_int, ctypes.c_int, ctypes.c_int] + [P] * 5
+    lib.deltanet_state_scan.restype = ctypes.c_int
     lib.deltanet_path.argtypes = [D]
     lib.deltanet_path.restype = ctypes.c_int
     lib.deltanet_launch_count.argtypes = [D, ctypes.c_int]
@@ -288,6 +295,75 @@ def deltanet_bwd(q, k, v, beta, dO, *, chunk=64, l2norm=True, h0=None, dhT=None,
     return dq, dk, dv, db, dh0
 
 
+def deltanet_fwd_transition(q, k, v, beta, *, l2norm=True, eps=1e-6, psi=None, hloc=None):
+    """Transition of this sequence (include/deltanet.h, context parallelism):
+    H_end = psi^T H_start + hloc.  Returns (psi [B,H,Dk,Dk], hloc [B,H,Dk,Dv])."""
+    lib = load_library()
+    dev = q.device
+    for t, n in ((q, "q"), (k, "k"), (v, "v"), (beta, "beta")):
+        _need(t, n, q.dtype, dev)
+    B, H, L, Dk = q.shape
+    Dv = v.shape[-1]
+    d = make_desc(B, H, L, Dk, Dv, 64, q.dtype, l2norm=l2norm, eps=eps)
+    if psi is None:
+        psi = torch.empty((B, H, Dk, Dk), dtype=torch.float32, device=dev)
+    if hloc is None:
+        hloc = torch.empty((B, H, Dk, Dv), dtype=torch.float32, device=dev)
+    _need(psi, "psi", torch.float32, dev)
+    _need(hloc, "hloc", torch.float32, dev)
+    rc = lib.deltanet_fwd_transition(ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(beta),
+                                     _ptr(psi), _ptr(hloc), _stream(dev))
+    _check(rc, "deltanet_fwd_transition")
+    return psi, hloc
+
+
+def deltanet_bwd_transition(q, k, v, beta, dO, *, l2norm=True, eps=1e-6, workspace=None,
+                            states_saved=True, dhloc=None):
+    """Local cotangent chain dl/dH_start of this sequence with dl/dH_end = 0.
+    With states_saved the workspace comes from deltanet_fwd(save_states=True)
+    over the same q, k, v, beta.  Returns dhloc [B,H,Dk,Dv]."""
+    lib = load_library()
+    dev = q.device
+    for t, n in ((q, "q"), (k, "k"), (v, "v"), (beta, "beta"), (dO, "dO")):
+        _need(t, n, q.dtype, dev)
+    B, H, L, Dk = q.shape
+    Dv = v.shape[-1]
+    if workspace is None:
+        states_saved = False
+    d = make_desc(B, H, L, Dk, Dv, 64, q.dtype, l2norm=l2norm, save_states=states_saved, eps=eps)
+    if workspace is None:
+        workspace = alloc_workspace(d, dev)
+    if dhloc is None:
+        dhloc = torch.empty((B, H, Dk, Dv), dtype=torch.float32, device=dev)
+    _need(dhloc, "dhloc", torch.float32, dev)
+    rc = lib.deltanet_bwd_transition(ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(beta),
+                                     _ptr(dO), _ptr(dhloc), _ptr(workspace), workspace.numel(),
+                                     _stream(dev))
+    _check(rc, "deltanet_bwd_transition")
+    return dhloc
+
+
+def deltanet_state_scan(psi_all, loc_all, part, *, reverse=False, edge=None, out=None):
+    """Boundary state of part ``part`` from the gathered transitions
+    psi_all [P,B,H,Dk,Dk], loc_all [P,B,H,Dk,Dv] (include/deltanet.h):
+    forward H_start(part) from edge = h0, or (reverse) dH_end(part) from
+    edge = dhT.  Returns out [B,H,Dk,Dv] fp32."""
+    lib = load_library()
+    dev = loc_all.device
+    P, B, H, Dk, Dv = loc_all.shape
+    for t, n in ((psi_all, "psi_all"), (loc_all, "loc_all"), (edge, "edge")):
+        _need(t, n, torch.float32, dev)
+    if out is None:
+        out = torch.empty((B, H, Dk, Dv), dtype=torch.float32, device=dev)
+    _need(out, "out", torch.float32, dev)
+    d = make_desc(B, H, 0, Dk, Dv, 64, torch.bfloat16)
+    rc = lib.deltanet_state_scan(ctypes.byref(d), int(P), int(part), int(bool(reverse)),
+                                 _ptr(psi_all), _ptr(loc_all), _ptr(edge), _ptr(out),
+                                 _stream(dev))
+    _check(rc, "deltanet_state_scan")
+    return out
+
+
 class DeltaNetChunkFunction(torch.autograd.Function):
     """autograd wrapper: o = DeltaNet(q, k, v, beta) with L2-normalised q, k."""
 
@@ -313,4 +389,5 @@ def deltanet(q, k, v, beta, chunk=64, l2norm=True):
 __all__ = ["deltanet_fwd", "deltanet_bwd", "deltanet_workspace_bytes", "deltanet_path",
            "deltanet_launch_count", "deltanet_strerror", "deltanet_desc", "make_desc",
            "load_library", "alloc_workspace", "DeltaNetError", "deltanet", "EXPORTED",
-           "LIB_PATH"]
+           "LIB_PATH", "deltanet_fwd_transition", "deltanet_bwd_transition",
+           "deltanet_state_scan"]

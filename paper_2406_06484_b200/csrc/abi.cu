@@ -62,6 +62,17 @@ dn::Args make_args(const deltanet_desc* d, void* ws) {
   return a;
 }
 
+// context parallelism: transitions exist
+// on the tcgen05 path's shapes; L = 0 is the identity map
+int validate_cp(const deltanet_desc* d) {
+  int rc = validate(d);
+  if (rc) return rc;
+  if (d->flags & DELTANET_FORCE_SIMT) return DELTANET_ERR_UNSUPPORTED;
+  deltanet_desc e = *d;
+  e.L = 1;
+  return dn::tc_supported(&e) ? DELTANET_OK : DELTANET_ERR_UNSUPPORTED;
+}
+
 }  // namespace
 
 extern "C" {
@@ -81,6 +92,13 @@ int deltanet_launch_count(const deltanet_desc* d, int which) {
     if (validate_rec(d) != DELTANET_OK) return -1;
     if ((size_t)d->B * d->H == 0 || (which >= 3 && d->L == 0)) return 0;
     return which == 4 ? 2 : 1;
+  }
+  if (which >= 5 && which <= 7) {  // context-parallel transitions, scan
+    if (validate_cp(d) != DELTANET_OK) return -1;
+    if ((size_t)d->B * d->H == 0) return 0;
+    if (which == 6 && d->L > 0 && !(d->flags & DELTANET_SAVE_STATES))
+      return 1 + dn::tc_launch_count(d, 0);
+    return 1;
   }
   if (validate(d) != DELTANET_OK) return -1;
   if ((size_t)d->B * d->H == 0) return 0;
@@ -199,6 +217,68 @@ int deltanet_prologue_bwd(const deltanet_desc* d, const void* xq, const void* xk
     return DELTANET_ERR_WORKSPACE;
   return dn::prologue_bwd(d, xq, xk, xv, xb, wq, wk, wv, dq, dk, dv, dbeta, dxq, dxk, dxv, dxb,
                           dwq, dwk, dwv, workspace, (cudaStream_t)stream);
+}
+
+int deltanet_fwd_transition(const deltanet_desc* d, const void* q, const void* k, const void* v,
+                            const void* beta, float* psi, float* hloc, void* stream) {
+  int rc = validate_cp(d);
+  if (rc) return rc;
+  const size_t units = (size_t)d->B * d->H;
+  if (!units) return DELTANET_OK;
+  if (!psi || !hloc || (d->L > 0 && (!q || !k || !v || !beta))) return DELTANET_ERR_INVALID_ARG;
+  if (misaligned(q) || misaligned(k) || misaligned(v) || misaligned(beta) || misaligned(psi) ||
+      misaligned(hloc))
+    return DELTANET_ERR_MISALIGNED;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (d->L == 0) return dn::cp_empty((int)units, psi, hloc, s);
+  dn::Args a = make_args(d, nullptr);
+  a.scratch = nullptr;
+  a.states = nullptr;
+  a.q = q; a.k = k; a.v = v; a.beta = beta;
+  return dn::tc_fwd_transition(a, psi, hloc, s);
+}
+
+int deltanet_bwd_transition(const deltanet_desc* d, const void* q, const void* k, const void* v,
+                            const void* beta, const void* dO, float* dhloc, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+  int rc = validate_cp(d);
+  if (rc) return rc;
+  const size_t units = (size_t)d->B * d->H;
+  if (!units) return DELTANET_OK;
+  if (!dhloc || (d->L > 0 && (!q || !k || !v || !beta || !dO))) return DELTANET_ERR_INVALID_ARG;
+  if (misaligned(q) || misaligned(k) || misaligned(v) || misaligned(beta) || misaligned(dO) ||
+      misaligned(dhloc) || misaligned(workspace))
+    return DELTANET_ERR_MISALIGNED;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (d->L == 0) return dn::cp_empty((int)units, nullptr, dhloc, s);
+  if (!workspace || workspace_bytes < deltanet_workspace_bytes(d)) return DELTANET_ERR_WORKSPACE;
+  dn::Args a = make_args(d, workspace);
+  a.q = q; a.k = k; a.v = v; a.beta = beta; a.dO = dO;
+  if (!(d->flags & DELTANET_SAVE_STATES)) {  // records of this shard (X is independent of h0)
+    dn::Args f = a;
+    f.flags |= DELTANET_SAVE_STATES;
+    f.o = nullptr;
+    f.hT = nullptr;
+    rc = dn::tc_fwd(f, s);
+    if (rc) return rc;
+  }
+  return dn::tc_bwd_transition(a, dhloc, s);
+}
+
+int deltanet_state_scan(const deltanet_desc* d, int nparts, int part, int reverse,
+                        const float* psi_all, const float* loc_all, const float* edge, float* out,
+                        void* stream) {
+  int rc = validate_cp(d);
+  if (rc) return rc;
+  if (nparts < 1 || part < 0 || part >= nparts || (reverse != 0 && reverse != 1))
+    return DELTANET_ERR_INVALID_ARG;
+  const size_t units = (size_t)d->B * d->H;
+  if (!units) return DELTANET_OK;
+  if (!out || (nparts > 1 && (!psi_all || !loc_all))) return DELTANET_ERR_INVALID_ARG;
+  if (misaligned(psi_all) || misaligned(loc_all) || misaligned(edge) || misaligned(out))
+    return DELTANET_ERR_MISALIGNED;
+  return dn::cp_scan((int)units, nparts, part, reverse, psi_all, loc_all, edge, out,
+                     (cudaStream_t)stream);
 }
 
 const char* deltanet_strerror(int code) {

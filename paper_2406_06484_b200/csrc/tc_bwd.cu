@@ -932,6 +932,31 @@ int tc_bwd(const Args& a0, cudaStream_t s) {
   return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
 }
 
+// Context parallelism: the local cotangent chain of this call's sequence from
+// dl/dH_end = 0 (pass 1 with one segment per unit); needs the forward's
+// per-chunk records in the workspace (deltanet_fwd with SAVE_STATES)
+int tc_bwd_transition(const Args& a0, float* dhloc, cudaStream_t s) {
+  Args a = a0;
+  const int BH = a.B * a.H;
+  CUtensorMap mQ, mK, mV, mDO, mDQ, mDK, mDV;
+  if (!make_il_map(&mQ, a.q, BH, a.L, D, C) || !make_il_map(&mK, a.k, BH, a.L, D, C) ||
+      !make_il_map(&mV, a.v, BH, a.L, D, C) || !make_il_map(&mDO, a.dO, BH, a.L, D, C) ||
+      !make_il_map(&mDQ, a.q, BH, a.L, D, C) || !make_il_map(&mDK, a.k, BH, a.L, D, C) ||
+      !make_il_map(&mDV, a.v, BH, a.L, D, C))
+    return DELTANET_ERR_CUDA;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(tc_bwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             SMEM_BYTES) != cudaSuccess)
+      return DELTANET_ERR_CUDA;
+    attr = true;
+  }
+  a.nseg = 1;
+  a.hloc = dhloc;
+  tc_bwd_kernel<true><<<BH, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mDO, mDQ, mDK, mDV, a);
+  return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
+}
+
 }  // namespace dn
 
 #ifdef DN_TIMING

@@ -755,6 +755,61 @@ __global__ void __launch_bounds__(256) seg_scan_kernel(Args a) {
   }
 }
 
+// Context-parallel scan (deltanet_state_scan): parts p of the sequence with
+// transitions Psi_p [Dk][Dk] and local states loc_p [Dk][Dv] (gathered over
+// ranks).  Forward: out = fold_{p < part} (H <- Psi_p^T H + loc_p) from h_edge;
+// reverse: out = fold_{p > part, descending} (G <- Psi_p G + loc_p) from
+// h_edge.  A CTA owns one 16-column block of one unit; fp32.
+struct ScanArgs {
+  int units, nparts, part, reverse;
+  const float *psi, *loc, *edge;
+  float* out;
+};
+__global__ void __launch_bounds__(256) cp_scan_kernel(ScanArgs sa) {
+  __shared__ float Hs[DK][16];
+  const int unit = blockIdx.x, j0 = blockIdx.y * 16;
+  const int tid = threadIdx.x, i = tid >> 1, jj = (tid & 1) * 8;
+  for (int e = tid; e < DK * 16; e += blockDim.x) {
+    const int r = e / 16, cc = e % 16;
+    Hs[r][cc] = sa.edge ? sa.edge[(size_t)unit * DK * DV + (size_t)r * DV + j0 + cc] : 0.f;
+  }
+  __syncthreads();
+  const int n = sa.reverse ? sa.nparts - 1 - sa.part : sa.part;
+  for (int step = 0; step < n; ++step) {
+    const int p = sa.reverse ? sa.nparts - 1 - step : step;
+    const float* psi = sa.psi + ((size_t)p * sa.units + unit) * DK * DK;
+    const float* lc = sa.loc + ((size_t)p * sa.units + unit) * DK * DV + (size_t)i * DV + j0 + jj;
+    float acc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = lc[e];
+#pragma unroll 4
+    for (int r = 0; r < DK; ++r) {
+      const float pv = sa.reverse ? psi[(size_t)i * DK + r] : psi[(size_t)r * DK + i];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = fmaf(pv, Hs[r][jj + e], acc[e]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 8; ++e) Hs[i][jj + e] = acc[e];
+    __syncthreads();
+  }
+  for (int e = tid; e < DK * 16; e += blockDim.x) {
+    const int r = e / 16, cc = e % 16;
+    sa.out[(size_t)unit * DK * DV + (size_t)r * DV + j0 + cc] = Hs[r][cc];
+  }
+}
+
+// transition of an empty sequence: Psi = I, loc = 0 (psi or loc may be null)
+__global__ void cp_empty_kernel(int units, float* psi, float* loc) {
+  const size_t n = (size_t)units * DK * DK;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (size_t)gridDim.x * blockDim.x) {
+    const int r = (int)((e / DK) % DK), c = (int)(e % DK);
+    if (psi) psi[e] = r == c ? 1.f : 0.f;
+    if (loc) loc[e] = 0.f;  // DK == DV
+  }
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ host side
@@ -885,6 +940,44 @@ int tc_fwd(const Args& a0, cudaStream_t s) {
   tc_fwd_kernel<true><<<BH * nseg, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);   // pass 1
   seg_scan_kernel<<<dim3(BH, DV / 16), 256, 0, s>>>(a);                     // pass 2
   tc_fwd_kernel<false><<<BH * nseg, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);  // pass 3
+  return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
+}
+
+// Context parallelism (include/deltanet.h): the transition of this call's
+// whole sequence (pass 1 of the segment machinery with one segment per unit)
+int tc_fwd_transition(const Args& a0, float* psi, float* hloc, cudaStream_t s) {
+  Args a = a0;
+  const int BH = a.B * a.H;
+  CUtensorMap mQ, mK, mV, mO;
+  if (!make_il_map(&mQ, a.q, BH, a.L, DK, C) || !make_il_map(&mK, a.k, BH, a.L, DK, C) ||
+      !make_il_map(&mV, a.v, BH, a.L, DV, C) || !make_il_map(&mO, a.v, BH, a.L, DV, C))
+    return DELTANET_ERR_CUDA;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(tc_fwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             SMEM_BYTES) != cudaSuccess)
+      return DELTANET_ERR_CUDA;
+    attr = true;
+  }
+  a.nseg = 1;
+  a.hloc = hloc;
+  a.psi = psi;
+  a.o = nullptr;
+  a.hT = nullptr;
+  a.h0 = nullptr;
+  tc_fwd_kernel<true><<<BH, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);
+  return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
+}
+
+int cp_empty(int units, float* psi, float* loc, cudaStream_t s) {
+  cp_empty_kernel<<<4 * 148, 256, 0, s>>>(units, psi, loc);
+  return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
+}
+
+int cp_scan(int units, int nparts, int part, int reverse, const float* psi, const float* loc,
+            const float* edge, float* out, cudaStream_t s) {
+  ScanArgs sa{units, nparts, part, reverse, psi, loc, edge, out};
+  cp_scan_kernel<<<dim3(units, DV / 16), 256, 0, s>>>(sa);
   return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
 }
 

@@ -61,6 +61,10 @@ def _load():
                 fn.restype = ctypes.c_int
             lib.dn_oracle_bwd.argtypes = [ctypes.POINTER(_Desc)] + [P] * 12
             lib.dn_oracle_bwd.restype = ctypes.c_int
+            lib.dn_oracle_gated_fwd.argtypes = [ctypes.POINTER(_Desc)] + [P] * 8
+            lib.dn_oracle_gated_fwd.restype = ctypes.c_int
+            lib.dn_oracle_gated_bwd.argtypes = [ctypes.POINTER(_Desc)] + [P] * 14
+            lib.dn_oracle_gated_bwd.restype = ctypes.c_int
             _lib = lib
     return _lib
 
@@ -119,4 +123,41 @@ def recurrent_bwd(q, k, v, beta, dO, h0=None, dhT=None, l2norm=True, eps=1e-6,
     return dq, dk, dv, db, dh0
 
 
-__all__ = ["build", "recurrent_fwd", "recurrent_bwd", "default_threads"]
+def gated_fwd(q, k, v, beta, g, h0=None, l2norm=True, eps=1e-6, nthreads=None):
+    """O, hT of Gated DeltaNet (PAPER.md Table tab:overview):
+    S_t = S_{t-1} (alpha_t (I - beta_t k_t k_t^T)) + beta_t v_t k_t^T,
+    alpha_t = exp(g_t), g [B,H,L] the log-decay (R23)."""
+    q, k, v, beta, g, h0 = map(_f64, (q, k, v, beta, g, h0))
+    B, H, L, Dk = q.shape
+    Dv = v.shape[-1]
+    o = np.zeros((B, H, L, Dv))
+    hT = np.zeros((B, H, Dk, Dv))
+    d = _Desc(B, H, L, Dk, Dv, int(bool(l2norm)), float(eps),
+              int(nthreads or default_threads()))
+    rc = _load().dn_oracle_gated_fwd(ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(beta),
+                                     _ptr(g), _ptr(h0), _ptr(o), _ptr(hT))
+    if rc:
+        raise RuntimeError(f"dn_oracle_gated_fwd failed ({rc})")
+    return o, hT
+
+
+def gated_bwd(q, k, v, beta, g, dO, h0=None, dhT=None, l2norm=True, eps=1e-6, nthreads=None):
+    """dq, dk, dv, dbeta, dg, dh0 of Gated DeltaNet by reverse mode."""
+    q, k, v, beta, g, dO, h0, dhT = map(_f64, (q, k, v, beta, g, dO, h0, dhT))
+    B, H, L, Dk = q.shape
+    Dv = v.shape[-1]
+    dq, dk, dv = np.zeros_like(q), np.zeros_like(k), np.zeros_like(v)
+    db, dg = np.zeros_like(beta), np.zeros_like(beta)
+    dh0 = np.zeros((B, H, Dk, Dv))
+    d = _Desc(B, H, L, Dk, Dv, int(bool(l2norm)), float(eps),
+              int(nthreads or default_threads()))
+    rc = _load().dn_oracle_gated_bwd(ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(beta),
+                                     _ptr(g), _ptr(h0), _ptr(dO), _ptr(dhT), _ptr(dq),
+                                     _ptr(dk), _ptr(dv), _ptr(db), _ptr(dg), _ptr(dh0))
+    if rc:
+        raise RuntimeError(f"dn_oracle_gated_bwd failed ({rc})")
+    return dq, dk, dv, db, dg, dh0
+
+
+__all__ = ["build", "recurrent_fwd", "recurrent_bwd", "gated_fwd", "gated_bwd",
+           "default_threads"]

@@ -16,8 +16,8 @@
 
 typedef struct {
   const dn_oracle_desc* d;
-  const double *q, *k, *v, *beta, *h0, *dO, *dhT;
-  double *o, *hT, *dq, *dk, *dv, *dbeta, *dh0;
+  const double *q, *k, *v, *beta, *g, *h0, *dO, *dhT;
+  double *o, *hT, *dq, *dk, *dv, *dbeta, *dg, *dh0;
   int worker, nworkers, bwd;
   int status;
 } job_t;
@@ -50,17 +50,25 @@ static void l2_normalize_adjoint(const double* y, const double* dy, double nrm,
 
 /* One delta-rule step, §2.2 line 86:
  *   S_t = S_{t-1} - beta_t (S_{t-1} k_t - v_t) k_t^T
- * S is Dv x Dk row-major.  r (scratch, Dv) receives v_t - S_{t-1} k_t. */
+ * and its gated form (Gated DeltaNet, PAPER.md Table tab:overview):
+ *   S_t = S_{t-1} (alpha_t (I - beta_t k_t k_t^T)) + beta_t v_t k_t^T
+ *       = alpha_t S_{t-1} + beta_t (v_t - alpha_t S_{t-1} k_t) k_t^T
+ * (alpha_t = 1 is the ungated step, bit for bit).  S is Dv x Dk row-major;
+ * r (scratch, Dv) receives v_t - alpha_t S_{t-1} k_t. */
 static void delta_step(double* S, const double* kt, const double* vt,
-                       double bt, double* r, int Dk, int Dv) {
+                       double bt, double at, double* r, int Dk, int Dv) {
   for (int i = 0; i < Dv; ++i) {
     double sk = 0.0;
     for (int j = 0; j < Dk; ++j) sk += S[(size_t)i * Dk + j] * kt[j];
-    r[i] = vt[i] - sk;
+    r[i] = vt[i] - at * sk;
   }
   for (int i = 0; i < Dv; ++i)
-    for (int j = 0; j < Dk; ++j) S[(size_t)i * Dk + j] += bt * r[i] * kt[j];
+    for (int j = 0; j < Dk; ++j)
+      S[(size_t)i * Dk + j] = at * S[(size_t)i * Dk + j] + bt * r[i] * kt[j];
 }
+
+/* alpha_t = exp(g_t) (g = log-decay, R23); 1 without a gate */
+static double gate(const double* g, int t) { return g ? exp(g[t]) : 1.0; }
 
 /* o_t = S_t q_t  (§2.2 line 97). */
 static void readout(const double* S, const double* qt, double* ot, int Dk,
@@ -92,6 +100,7 @@ static void unit_fwd(const dn_oracle_desc* d, size_t u, const job_t* J,
   const double* k = J->k + u * (size_t)L * Dk;
   const double* v = J->v + u * (size_t)L * Dv;
   const double* beta = J->beta + u * (size_t)L;
+  const double* gg = J->g ? J->g + u * (size_t)L : NULL;
   double* o = J->o + u * (size_t)L * Dv;
 
   double* S = work;                          /* Dv*Dk */
@@ -113,7 +122,7 @@ static void unit_fwd(const dn_oracle_desc* d, size_t u, const job_t* J,
       memcpy(qh, q + (size_t)t * Dk, sizeof(double) * Dk);
       memcpy(kh, k + (size_t)t * Dk, sizeof(double) * Dk);
     }
-    delta_step(S, kh, v + (size_t)t * Dv, beta[t], r, Dk, Dv);
+    delta_step(S, kh, v + (size_t)t * Dv, beta[t], gate(gg, t), r, Dk, Dv);
     readout(S, qh, o + (size_t)t * Dv, Dk, Dv);
   }
   if (J->hT)
@@ -127,6 +136,10 @@ static void unit_fwd(const dn_oracle_desc* d, size_t u, const job_t* J,
  *   dS += do_t q_t^T;  dq_t = S_t^T do_t;  g = dS k_t;  r = v_t - S_{t-1} k_t
  *   dv_t = beta_t g;   dbeta_t = g . r;   dk_t = beta_t (dS^T r - S_{t-1}^T g)
  *   dS <- dS - beta_t g k_t^T                                  (= dl/dS_{t-1})
+ * Gated step (S_t = a S_{t-1} + beta r k^T, r = v - a S_{t-1} k, a = alpha_t):
+ * the same with r = v_t - a S_{t-1} k_t,  dk_t = beta_t (dS^T r - a S_{t-1}^T g),
+ *   dalpha_t = <dS, S_{t-1}> - beta_t g . (S_{t-1} k_t),  dg_t = a dalpha_t,
+ *   dS <- a (dS - beta_t g k_t^T).
  */
 static void unit_bwd(const dn_oracle_desc* d, size_t u, const job_t* J,
                      double* work) {
@@ -141,6 +154,8 @@ static void unit_bwd(const dn_oracle_desc* d, size_t u, const job_t* J,
   double* dk = J->dk + u * (size_t)L * Dk;
   double* dv = J->dv + u * (size_t)L * Dv;
   double* dbeta = J->dbeta + u * (size_t)L;
+  const double* gg = J->g ? J->g + u * (size_t)L : NULL;
+  double* dgg = J->dg ? J->dg + u * (size_t)L : NULL;
 
   const int nseg = (L + CKPT - 1) / CKPT;
   double* ck = work;                          /* (nseg+1) * SS checkpoints */
@@ -166,7 +181,7 @@ static void unit_bwd(const dn_oracle_desc* d, size_t u, const job_t* J,
           J->h0 ? J->h0[u * SS + (size_t)j * Dv + i] : 0.0;
   memcpy(ck, S, sizeof(double) * SS);
   for (int t = 0; t < L; ++t) {
-    delta_step(S, kh + (size_t)t * Dk, v + (size_t)t * Dv, beta[t], r, Dk, Dv);
+    delta_step(S, kh + (size_t)t * Dk, v + (size_t)t * Dv, beta[t], gate(gg, t), r, Dk, Dv);
     if ((t + 1) % CKPT == 0 || t + 1 == L)
       memcpy(ck + (size_t)((t + CKPT) / CKPT) * SS, S, sizeof(double) * SS);
   }
@@ -185,7 +200,7 @@ static void unit_bwd(const dn_oracle_desc* d, size_t u, const job_t* J,
       memcpy(seg + (size_t)(t - t0 + 1) * SS, seg + (size_t)(t - t0) * SS,
              sizeof(double) * SS);
       delta_step(seg + (size_t)(t - t0 + 1) * SS, kh + (size_t)t * Dk,
-                 v + (size_t)t * Dv, beta[t], r, Dk, Dv);
+                 v + (size_t)t * Dv, beta[t], gate(gg, t), r, Dk, Dv);
     }
     for (int t = t1 - 1; t >= t0; --t) {
       const double* St = seg + (size_t)(t - t0 + 1) * SS; /* S_t (after) */
@@ -195,6 +210,7 @@ static void unit_bwd(const dn_oracle_desc* d, size_t u, const job_t* J,
       const double* vt = v + (size_t)t * Dv;
       const double* dot = dO + (size_t)t * Dv;
       const double bt = beta[t];
+      const double at = gate(gg, t);
       /* dS += do_t q_t^T */
       for (int i = 0; i < Dv; ++i)
         for (int j = 0; j < Dk; ++j) dS[(size_t)i * Dk + j] += dot[i] * qt[j];
@@ -204,16 +220,20 @@ static void unit_bwd(const dn_oracle_desc* d, size_t u, const job_t* J,
         for (int i = 0; i < Dv; ++i) s += St[(size_t)i * Dk + j] * dot[i];
         dqh[j] = s;
       }
-      /* g = dS k_t ; r = v_t - S_{t-1} k_t */
+      /* g = dS k_t ; r = v_t - a S_{t-1} k_t ; dalpha_t */
+      double da = 0.0;
       for (int i = 0; i < Dv; ++i) {
         double sg = 0.0, sk = 0.0;
         for (int j = 0; j < Dk; ++j) {
           sg += dS[(size_t)i * Dk + j] * kt[j];
           sk += Sp[(size_t)i * Dk + j] * kt[j];
+          da += dS[(size_t)i * Dk + j] * Sp[(size_t)i * Dk + j];
         }
         g[i] = sg;
-        r[i] = vt[i] - sk;
+        r[i] = vt[i] - at * sk;
+        da -= bt * sg * sk;
       }
+      if (dgg) dgg[t] = at * da;
       /* dv_t = beta_t g ; dbeta_t = g . r */
       double gr = 0.0;
       for (int i = 0; i < Dv; ++i) {
@@ -221,16 +241,17 @@ static void unit_bwd(const dn_oracle_desc* d, size_t u, const job_t* J,
         gr += g[i] * r[i];
       }
       dbeta[t] = gr;
-      /* dk_t = beta_t (dS^T r - S_{t-1}^T g) */
+      /* dk_t = beta_t (dS^T r - a S_{t-1}^T g) */
       for (int j = 0; j < Dk; ++j) {
         double s = 0.0;
         for (int i = 0; i < Dv; ++i)
-          s += dS[(size_t)i * Dk + j] * r[i] - Sp[(size_t)i * Dk + j] * g[i];
+          s += dS[(size_t)i * Dk + j] * r[i] - at * Sp[(size_t)i * Dk + j] * g[i];
         dkh[j] = bt * s;
       }
-      /* dS <- dS - beta_t g k_t^T */
+      /* dS <- a (dS - beta_t g k_t^T) */
       for (int i = 0; i < Dv; ++i)
-        for (int j = 0; j < Dk; ++j) dS[(size_t)i * Dk + j] -= bt * g[i] * kt[j];
+        for (int j = 0; j < Dk; ++j)
+          dS[(size_t)i * Dk + j] = at * (dS[(size_t)i * Dk + j] - bt * g[i] * kt[j]);
       /* chain through the L2 normalisation (R9) */
       if (d->l2norm) {
         l2_normalize_adjoint(qt, dqh, qn[t], d->eps, dq + (size_t)t * Dk, Dk);
@@ -313,14 +334,36 @@ static int bad_desc(const dn_oracle_desc* d) {
          !(d->eps > 0.0);
 }
 
-int dn_oracle_fwd(const dn_oracle_desc* d, const double* q, const double* k,
-                  const double* v, const double* beta, const double* h0,
-                  double* o, double* hT) {
+int dn_oracle_gated_fwd(const dn_oracle_desc* d, const double* q, const double* k,
+                        const double* v, const double* beta, const double* g,
+                        const double* h0, double* o, double* hT) {
   if (bad_desc(d) || !q || !k || !v || !beta || !o) return 1;
   job_t J;
   memset(&J, 0, sizeof J);
-  J.d = d; J.q = q; J.k = k; J.v = v; J.beta = beta; J.h0 = h0;
+  J.d = d; J.q = q; J.k = k; J.v = v; J.beta = beta; J.g = g; J.h0 = h0;
   J.o = o; J.hT = hT; J.bwd = 0;
+  return run(&J);
+}
+
+int dn_oracle_fwd(const dn_oracle_desc* d, const double* q, const double* k,
+                  const double* v, const double* beta, const double* h0,
+                  double* o, double* hT) {
+  return dn_oracle_gated_fwd(d, q, k, v, beta, NULL, h0, o, hT);
+}
+
+int dn_oracle_gated_bwd(const dn_oracle_desc* d, const double* q, const double* k,
+                        const double* v, const double* beta, const double* g,
+                        const double* h0, const double* dO, const double* dhT,
+                        double* dq, double* dk, double* dv, double* dbeta,
+                        double* dg, double* dh0) {
+  if (bad_desc(d) || !q || !k || !v || !beta || !dO || !dq || !dk || !dv ||
+      !dbeta || (g && !dg))
+    return 1;
+  job_t J;
+  memset(&J, 0, sizeof J);
+  J.d = d; J.q = q; J.k = k; J.v = v; J.beta = beta; J.g = g; J.h0 = h0;
+  J.dO = dO; J.dhT = dhT; J.dq = dq; J.dk = dk; J.dv = dv; J.dbeta = dbeta;
+  J.dg = dg; J.dh0 = dh0; J.bwd = 1;
   return run(&J);
 }
 
@@ -328,13 +371,6 @@ int dn_oracle_bwd(const dn_oracle_desc* d, const double* q, const double* k,
                   const double* v, const double* beta, const double* h0,
                   const double* dO, const double* dhT, double* dq, double* dk,
                   double* dv, double* dbeta, double* dh0) {
-  if (bad_desc(d) || !q || !k || !v || !beta || !dO || !dq || !dk || !dv ||
-      !dbeta)
-    return 1;
-  job_t J;
-  memset(&J, 0, sizeof J);
-  J.d = d; J.q = q; J.k = k; J.v = v; J.beta = beta; J.h0 = h0;
-  J.dO = dO; J.dhT = dhT; J.dq = dq; J.dk = dk; J.dv = dv; J.dbeta = dbeta;
-  J.dh0 = dh0; J.bwd = 1;
-  return run(&J);
+  return dn_oracle_gated_bwd(d, q, k, v, beta, NULL, h0, dO, dhT, dq, dk, dv, dbeta,
+                             NULL, dh0);
 }

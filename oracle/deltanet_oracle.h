@@ -20,6 +20,11 @@
  *   q, k  [B,H,L,Dk]      v, o, dO  [B,H,L,Dv]      beta  [B,H,L]
  *   h0, hT, dhT, dh0  [B,H,Dk,Dv]   -- the kernel orientation H = S^T
  * Nullable: h0 (zero), hT, dhT (zero), dh0.
+ *
+ * Gated DeltaNet (PAPER.md Table tab:overview):
+ *     S_t = S_{t-1} (alpha_t (I - beta_t k_t k_t^T)) + beta_t v_t k_t^T
+ * with alpha_t = exp(g_t), g [B,H,L] the log-decay (R23); the
+ * gated entry points take g (NULL = ungated, alpha = 1) and return dg.
  * Returns 0 on success, 1 on an invalid argument (nothing written).
  */
 #ifndef DELTANET_ORACLE_H
@@ -43,6 +48,16 @@ int dn_oracle_bwd(const dn_oracle_desc* d, const double* q, const double* k,
                   const double* v, const double* beta, const double* h0,
                   const double* dO, const double* dhT, double* dq, double* dk,
                   double* dv, double* dbeta, double* dh0);
+
+int dn_oracle_gated_fwd(const dn_oracle_desc* d, const double* q, const double* k,
+                        const double* v, const double* beta, const double* g,
+                        const double* h0, double* o, double* hT);
+
+int dn_oracle_gated_bwd(const dn_oracle_desc* d, const double* q, const double* k,
+                        const double* v, const double* beta, const double* g,
+                        const double* h0, const double* dO, const double* dhT,
+                        double* dq, double* dk, double* dv, double* dbeta,
+                        double* dg, double* dh0);
 
 #ifdef __cplusplus
 }

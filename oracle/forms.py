@@ -151,3 +151,129 @@ def chunkwise_backward(Q, K, V, beta, dO, C, S0=None, dST=None):
         dkk = dkk + bG @ k + bG.T @ k
         dQ[sl] = dq; dK[sl] = dkk; db[sl] = dbc
     return dQ, dK, dV, db, dH
+
+
+# ---------------------------------------------------------------- Gated DeltaNet
+def _gate_tables(g):
+    """Within one chunk: G_r = sum_{j<=r} g_j, gamma_r = exp(G_r) and
+    Gamma[r, i] = exp(G_r - G_i) for i <= r (0 above the diagonal), formed as
+    exponentials of differences so no ratio over- or underflows."""
+    G = np.cumsum(g)
+    diff = G[:, None] - G[None, :]
+    Gam = np.where(np.tril(np.ones_like(diff)) > 0, np.exp(np.minimum(diff, 0.0)), 0.0)
+    return G, np.exp(G), Gam
+
+
+def gated_chunkwise_forward(Q, K, V, beta, g, C, H0=None):
+    """Chunkwise form of Gated DeltaNet (PAPER.md Table tab:overview, P:757:
+    S_t = S_{t-1}(alpha_t(I - beta_t k_t k_t^T)) + beta_t v_t k_t^T, alpha = e^g)
+    derived like Eq. 8-11 (R23), kernel orientation H = S^T.
+    Per chunk, with G, gamma, Gamma of _gate_tables:
+        X  = (I + tril(diag(beta) (Gamma . K K^T), -1))^{-1}
+        W  = X diag(beta gamma) K,   U = X diag(beta) V,   U' = U - W H
+        O  = diag(gamma) Q H + (Gamma . tril(Q K^T)) U'
+        H <- gamma_C H + (diag(gamma_C / gamma) K)^T U'
+    The tail is padded with beta = 0, g = 0 (an exact no-op).  Returns O, H."""
+    L, dk = K.shape
+    dv = V.shape[1]
+    pad = (-L) % C
+    if pad:
+        Q = np.vstack([Q, np.zeros((pad, dk))])
+        K = np.vstack([K, np.zeros((pad, dk))])
+        V = np.vstack([V, np.zeros((pad, dv))])
+        beta = np.concatenate([beta, np.zeros(pad)])
+        g = np.concatenate([g, np.zeros(pad)])
+    H = np.zeros((dk, dv)) if H0 is None else H0.copy()
+    O = np.zeros((L + pad, dv))
+    for c in range((L + pad) // C):
+        sl = slice(c * C, (c + 1) * C)
+        q, k, v, b = Q[sl], K[sl], V[sl], beta[sl]
+        G, gam, Gam = _gate_tables(g[sl])
+        X = np.linalg.inv(np.eye(C) + np.tril(b[:, None] * Gam * (k @ k.T), -1))
+        W = X @ ((b * gam)[:, None] * k)
+        U = X @ (b[:, None] * v)
+        Up = U - W @ H
+        O[sl] = gam[:, None] * (q @ H) + (Gam * np.tril(q @ k.T)) @ Up
+        H = gam[-1] * H + ((gam[-1] / gam)[:, None] * k).T @ Up
+    return O[:L], H
+
+
+def gated_chunkwise_backward(Q, K, V, beta, g, dO, C, H0=None, dHT=None):
+    """Chunked reverse sweep of gated_chunkwise_forward (R23), H
+    orientation, already-normalised q, k; L a multiple of C.  Returns dQ, dK,
+    dV, dbeta, dg, dH0.  Per chunk, with D = gamma_C / gamma, dH = dl/dH_next:
+      dU' = diag(D) K dH + A^T dO,  A = Gamma . tril(QK^T),  dA = tril(dO U'^T)
+      dQ  = diag(gamma) dO H^T + (Gamma . dA) K
+      dK  = diag(D) U' dH^T + (Gamma . dA)^T Q + UT / inverse adjoints
+      dH <- gamma_C dH + (diag(gamma) Q)^T dO - W^T dU'
+    and dG_r (w.r.t. the cumulative log-gate) collects the gamma, Gamma and D
+    factors; dg = reverse cumulative sum of dG within the chunk."""
+    L, dk = K.shape
+    dv = V.shape[1]
+    assert L % C == 0
+    n = L // C
+    H = np.zeros((dk, dv)) if H0 is None else H0.copy()
+    saved = []
+    for c in range(n):
+        sl = slice(c * C, (c + 1) * C)
+        q, k, v, b = Q[sl], K[sl], V[sl], beta[sl]
+        G, gam, Gam = _gate_tables(g[sl])
+        X = np.linalg.inv(np.eye(C) + np.tril(b[:, None] * Gam * (k @ k.T), -1))
+        W = X @ ((b * gam)[:, None] * k)
+        U = X @ (b[:, None] * v)
+        Up = U - W @ H
+        saved.append((H.copy(), X, W, Up, G, gam, Gam))
+        H = gam[-1] * H + ((gam[-1] / gam)[:, None] * k).T @ Up
+    dQ = np.zeros_like(Q); dK = np.zeros_like(K); dV = np.zeros_like(V)
+    db = np.zeros_like(beta); dg = np.zeros_like(g)
+    dH = np.zeros((dk, dv)) if dHT is None else dHT.copy()
+    for c in reversed(range(n)):
+        sl = slice(c * C, (c + 1) * C)
+        q, k, v, b, do = Q[sl], K[sl], V[sl], beta[sl], dO[sl]
+        Ht, X, W, Up, G, gam, Gam = saved[c]
+        D = gam[-1] / gam
+        QK = np.tril(q @ k.T)
+        A = Gam * QK
+        dG = np.zeros(C)
+        # H_next = gamma_C H + (D K)^T U'
+        dUp = (D[:, None] * k) @ dH + A.T @ do
+        dKbar = Up @ dH.T                       # w.r.t. D K
+        dkk = D[:, None] * dKbar
+        dD = (dKbar * k).sum(1)
+        dG[-1] += (dD * D).sum() + gam[-1] * (dH * Ht).sum()
+        dG -= dD * D
+        # O = diag(gamma) Q H + A U'
+        dA = np.tril(do @ Up.T)
+        dS = Gam * dA
+        dq = gam[:, None] * (do @ Ht.T) + dS @ k
+        dkk = dkk + dS.T @ q
+        dG += gam * (q * (do @ Ht.T)).sum(1)
+        dGam = dA * QK
+        # U' = U - W H
+        dW = -dUp @ Ht.T
+        dHn = gam[-1] * dH + (gam[:, None] * q).T @ do - W.T @ dUp
+        # W = X diag(beta gamma) K, U = X diag(beta) V
+        Kbg = (b * gam)[:, None] * k
+        Vb = b[:, None] * v
+        dX = dUp @ Vb.T + dW @ Kbg.T
+        dKbg = X.T @ dW
+        dVb = X.T @ dUp
+        dV[sl] = b[:, None] * dVb
+        dkk = dkk + (b * gam)[:, None] * dKbg
+        rk = (dKbg * k).sum(1)
+        dbc = (dVb * v).sum(1) + gam * rk
+        dG += b * gam * rk
+        # X = (I + Kg)^{-1},  Kg = tril(diag(beta) (Gamma . K K^T), -1)
+        Gb = np.tril(-X.T @ dX @ X.T, -1)
+        KK = k @ k.T
+        dbc = dbc + (Gb * Gam * KK).sum(1)
+        E = b[:, None] * Gb * Gam
+        dkk = dkk + E @ k + E.T @ k
+        dGam = dGam + b[:, None] * Gb * KK
+        # Gamma[r, i] = exp(G_r - G_i)
+        T = dGam * Gam
+        dG += T.sum(1) - T.sum(0)
+        dg[sl] = np.cumsum(dG[::-1])[::-1]
+        dQ[sl] = dq; dK[sl] = dkk; db[sl] = dbc
+        dH = dHn
+    return dQ, dK, dV, db, dg, dH

@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define DELTANET_ABI_VERSION 4
+#define DELTANET_ABI_VERSION 5
 
 typedef enum {
   DELTANET_BF16 = 0, /* bf16 I/O, fp32 accumulation (BASELINE.json north_star) */
@@ -70,7 +70,11 @@ enum {
   /* tcgen05 forward: never split a unit's sequence into segments processed
    * by several CTAs (the segment-parallel forward, is used
    * automatically when B*H is small against the SM count) */
-  DELTANET_NO_SEGMENTS = 1u << 4
+  DELTANET_NO_SEGMENTS = 1u << 4,
+  /* Gated DeltaNet (set internally by the deltanet_gated_* calls; set it in
+   * the descriptor passed to deltanet_workspace_bytes / deltanet_path /
+   * deltanet_launch_count to query the gated calls) */
+  DELTANET_GATED = 1u << 5
 };
 
 typedef struct {
@@ -159,6 +163,36 @@ int deltanet_prologue_bwd(const deltanet_desc* d, const void* xq,
                           const void* dbeta, void* dxq, void* dxk, void* dxv,
                           void* dxb, float* dwq, float* dwk, float* dwv,
                           void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- Gated DeltaNet (R23) ----
+ * The recurrence of PAPER.md Table tab:overview,
+ *   S_t = S_{t-1} (alpha_t (I - beta_t k_t k_t^T)) + beta_t v_t k_t^T,
+ *   o_t = S_t q_t,   alpha_t = exp(g_t),
+ * with g [B,H,L] the per-token log-decay, fp32 whatever the I/O dtype
+ * (g <= 0 for a decay; any finite g is accepted).  Same tensors, layouts,
+ * flags and error codes as deltanet_fwd / deltanet_bwd plus g and dg
+ * ([B,H,L] fp32, the gradient w.r.t. g).  The workspace must be at least
+ * deltanet_workspace_bytes of the descriptor with DELTANET_GATED set.
+ * g = NULL is the ungated layer. */
+int deltanet_gated_fwd(const deltanet_desc* d, const void* q, const void* k,
+                       const void* v, const void* beta, const float* g,
+                       const float* h0, void* o, float* hT, void* workspace,
+                       size_t workspace_bytes, void* stream);
+
+int deltanet_gated_bwd(const deltanet_desc* d, const void* q, const void* k,
+                       const void* v, const void* beta, const float* g,
+                       const float* h0, const void* dO, const float* dhT,
+                       void* dq, void* dk, void* dv, void* dbeta, float* dg,
+                       float* dh0, void* workspace, size_t workspace_bytes,
+                       void* stream);
+
+/* Recurrent (token-by-token) gated forward for inference / decode; as
+ * deltanet_recurrent_fwd plus g (nullable). */
+int deltanet_gated_recurrent_fwd(const deltanet_desc* d, const void* q,
+                                 const void* k, const void* v,
+                                 const void* beta, const float* g,
+                                 const float* h0, void* o, float* hT,
+                                 void* stream);
 
 /* ---- Context parallelism ----
  * A sequence split into P consecutive parts (one per GPU, or per call) is

@@ -29,6 +29,7 @@ DELTANET_SAVE_STATES = 1 << 1
 DELTANET_PROLOGUE_SILU_V = 1 << 3
 DELTANET_FORCE_SIMT = 1 << 2
 DELTANET_NO_SEGMENTS = 1 << 4
+DELTANET_GATED = 1 << 5
 
 
 class deltanet_desc(ctypes.Structure):
@@ -42,7 +43,8 @@ EXPORTED = ("deltanet_workspace_bytes", "deltanet_fwd", "deltanet_bwd", "deltane
             "deltanet_launch_count", "deltanet_strerror", "deltanet_abi_version",
             "deltanet_recurrent_fwd", "deltanet_prologue_fwd", "deltanet_prologue_bwd",
             "deltanet_prologue_workspace_bytes", "deltanet_fwd_transition",
-            "deltanet_bwd_transition", "deltanet_state_scan")
+            "deltanet_bwd_transition", "deltanet_state_scan", "deltanet_gated_fwd",
+            "deltanet_gated_bwd", "deltanet_gated_recurrent_fwd")
 
 _lib = None
 
@@ -78,6 +80,12 @@ def load_library(path: str = LIB_PATH):
     lib.deltanet_bwd_transition.restype = ctypes.c_int
     lib.deltanet_state_scan.argtypes = [D, ctypes.c_int, ctypes.c_int, ctypes.c_int] + [P] * 5
     lib.deltanet_state_scan.restype = ctypes.c_int
+    lib.deltanet_gated_fwd.argtypes = [D] + [P] * 9 + [ctypes.c_size_t, P]
+    lib.deltanet_gated_fwd.restype = ctypes.c_int
+    lib.deltanet_gated_bwd.argtypes = [D] + [P] * 15 + [ctypes.c_size_t, P]
+    lib.deltanet_gated_bwd.restype = ctypes.c_int
+    lib.deltanet_gated_recurrent_fwd.argtypes = [D] + [P] * 9
+    lib.deltanet_gated_recurrent_fwd.restype = ctypes.c_int
     lib.deltanet_path.argtypes = [D]
     lib.deltanet_path.restype = ctypes.c_int
     lib.deltanet_launch_count.argtypes = [D, ctypes.c_int]
@@ -104,19 +112,21 @@ def _check(rc: int, what: str):
 
 
 def make_desc(B, H, L, Dk, Dv, chunk=64, dtype=torch.bfloat16, l2norm=True,
-              save_states=True, force_simt=False, eps=1e-6, segments=True) -> deltanet_desc:
+              save_states=True, force_simt=False, eps=1e-6, segments=True,
+              gated=False) -> deltanet_desc:
     dt = {torch.bfloat16: DELTANET_BF16, torch.float32: DELTANET_FP32}[dtype]
     flags = ((DELTANET_L2NORM_QK if l2norm else 0) |
              (DELTANET_SAVE_STATES if save_states else 0) |
              (DELTANET_FORCE_SIMT if force_simt else 0) |
-             (0 if segments else DELTANET_NO_SEGMENTS))
+             (0 if segments else DELTANET_NO_SEGMENTS) |
+             (DELTANET_GATED if gated else 0))
     return deltanet_desc(B, H, L, Dk, Dv, chunk, dt, flags, eps)
 
 
-def _desc_for(q, v, chunk, l2norm, save_states, force_simt, eps, segments=True):
+def _desc_for(q, v, chunk, l2norm, save_states, force_simt, eps, segments=True, gated=False):
     B, H, L, Dk = q.shape
     return make_desc(B, H, L, Dk, v.shape[-1], chunk, q.dtype, l2norm, save_states,
-                     force_simt, eps, segments)
+                     force_simt, eps, segments, gated)
 
 
 def deltanet_workspace_bytes(desc: deltanet_desc) -> int:
@@ -364,6 +374,81 @@ def deltanet_state_scan(psi_all, loc_all, part, *, reverse=False, edge=None, out
     return out
 
 
+def deltanet_gated_fwd(q, k, v, beta, g, *, chunk=64, l2norm=True, h0=None, save_states=True,
+                       workspace=None, want_hT=True, force_simt=False, eps=1e-6, out=None):
+    """Forward of Gated DeltaNet (PAPER.md Table tab:overview; DESIGN.md
+    R23): g [B,H,L] fp32 log-decay, alpha = exp(g).  Returns (o, hT, workspace)."""
+    lib = load_library()
+    dev = q.device
+    for t, n in ((q, "q"), (k, "k"), (v, "v"), (beta, "beta")):
+        _need(t, n, q.dtype, dev)
+    _need(g, "g", torch.float32, dev)
+    _need(h0, "h0", torch.float32, dev)
+    d = _desc_for(q, v, chunk, l2norm, save_states, force_simt, eps, gated=True)
+    B, H, L, Dk = q.shape
+    Dv = v.shape[-1]
+    o = out if out is not None else torch.empty((B, H, L, Dv), dtype=q.dtype, device=dev)
+    hT = torch.empty((B, H, Dk, Dv), dtype=torch.float32, device=dev) if want_hT else None
+    if workspace is None:
+        workspace = alloc_workspace(d, dev)
+    rc = lib.deltanet_gated_fwd(ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(beta), _ptr(g),
+                                _ptr(h0), _ptr(o), _ptr(hT), _ptr(workspace), workspace.numel(),
+                                _stream(dev))
+    _check(rc, "deltanet_gated_fwd")
+    return o, hT, workspace
+
+
+def deltanet_gated_bwd(q, k, v, beta, g, dO, *, chunk=64, l2norm=True, h0=None, dhT=None,
+                       workspace=None, states_saved=True, want_dh0=True, force_simt=False,
+                       eps=1e-6):
+    """Backward of Gated DeltaNet.  Returns (dq, dk, dv, dbeta, dg, dh0 or None)."""
+    lib = load_library()
+    dev = q.device
+    for t, n in ((q, "q"), (k, "k"), (v, "v"), (beta, "beta"), (dO, "dO")):
+        _need(t, n, q.dtype, dev)
+    for t, n in ((g, "g"), (h0, "h0"), (dhT, "dhT")):
+        _need(t, n, torch.float32, dev)
+    if workspace is None:
+        states_saved = False
+    d = _desc_for(q, v, chunk, l2norm, states_saved, force_simt, eps, gated=True)
+    B, H, L, Dk = q.shape
+    Dv = v.shape[-1]
+    dq, dk, dv, db = (torch.empty_like(t) for t in (q, k, v, beta))
+    dg = torch.empty_like(g)
+    dh0 = torch.empty((B, H, Dk, Dv), dtype=torch.float32, device=dev) if want_dh0 else None
+    if workspace is None:
+        workspace = alloc_workspace(d, dev)
+    rc = lib.deltanet_gated_bwd(ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(beta), _ptr(g),
+                                _ptr(h0), _ptr(dO), _ptr(dhT), _ptr(dq), _ptr(dk), _ptr(dv),
+                                _ptr(db), _ptr(dg), _ptr(dh0), _ptr(workspace),
+                                workspace.numel(), _stream(dev))
+    _check(rc, "deltanet_gated_bwd")
+    return dq, dk, dv, db, dg, dh0
+
+
+def deltanet_gated_recurrent_fwd(q, k, v, beta, g, *, l2norm=True, h0=None, want_hT=True,
+                                 eps=1e-6, out=None, hT=None):
+    """Recurrent (token-by-token) gated forward for inference / decode.
+    Passing hT=h0 updates the state in place.  Returns (o, hT or None)."""
+    lib = load_library()
+    dev = q.device
+    for t, n in ((q, "q"), (k, "k"), (v, "v"), (beta, "beta")):
+        _need(t, n, q.dtype, dev)
+    for t, n in ((g, "g"), (h0, "h0"), (hT, "hT")):
+        _need(t, n, torch.float32, dev)
+    B, H, L, Dk = q.shape
+    Dv = v.shape[-1]
+    d = make_desc(B, H, L, Dk, Dv, 64, q.dtype, l2norm=l2norm, eps=eps)
+    o = out if out is not None else torch.empty((B, H, L, Dv), dtype=q.dtype, device=dev)
+    if hT is None and want_hT:
+        hT = torch.empty((B, H, Dk, Dv), dtype=torch.float32, device=dev)
+    rc = lib.deltanet_gated_recurrent_fwd(ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v),
+                                          _ptr(beta), _ptr(g), _ptr(h0), _ptr(o), _ptr(hT),
+                                          _stream(dev))
+    _check(rc, "deltanet_gated_recurrent_fwd")
+    return o, hT
+
+
 class DeltaNetChunkFunction(torch.autograd.Function):
     """autograd wrapper: o = DeltaNet(q, k, v, beta) with L2-normalised q, k."""
 
@@ -390,4 +475,5 @@ __all__ = ["deltanet_fwd", "deltanet_bwd", "deltanet_workspace_bytes", "deltanet
            "deltanet_launch_count", "deltanet_strerror", "deltanet_desc", "make_desc",
            "load_library", "alloc_workspace", "DeltaNetError", "deltanet", "EXPORTED",
            "LIB_PATH", "deltanet_fwd_transition", "deltanet_bwd_transition",
-           "deltanet_state_scan"]
+           "deltanet_state_scan", "deltanet_gated_fwd", "deltanet_gated_bwd",
+           "deltanet_gated_recurrent_fwd", "DELTANET_GATED"]

@@ -32,7 +32,8 @@ int validate_rec(const deltanet_desc* d) {
 }
 
 bool use_tc(const deltanet_desc* d) {
-  return !(d->flags & DELTANET_FORCE_SIMT) && dn::tc_supported(d);
+  return !(d->flags & DELTANET_FORCE_SIMT) && dn::tc_supported(d) &&
+         (!(d->flags & DELTANET_GATED) || dn::tc_gated_supported(d));
 }
 
 size_t elem_bytes(const deltanet_desc* d) { return d->dtype == DELTANET_FP32 ? 4 : 2; }
@@ -67,7 +68,7 @@ dn::Args make_args(const deltanet_desc* d, void* ws) {
 int validate_cp(const deltanet_desc* d) {
   int rc = validate(d);
   if (rc) return rc;
-  if (d->flags & DELTANET_FORCE_SIMT) return DELTANET_ERR_UNSUPPORTED;
+  if (d->flags & (DELTANET_FORCE_SIMT | DELTANET_GATED)) return DELTANET_ERR_UNSUPPORTED;
   deltanet_desc e = *d;
   e.L = 1;
   return dn::tc_supported(&e) ? DELTANET_OK : DELTANET_ERR_UNSUPPORTED;
@@ -106,9 +107,9 @@ int deltanet_launch_count(const deltanet_desc* d, int which) {
   return 1;
 }
 
-int deltanet_fwd(const deltanet_desc* d, const void* q, const void* k, const void* v,
-                 const void* beta, const float* h0, void* o, float* hT, void* workspace,
-                 size_t workspace_bytes, void* stream) {
+static int fwd_impl(const deltanet_desc* d, const void* q, const void* k, const void* v,
+                    const void* beta, const float* g, const float* h0, void* o, float* hT,
+                    void* workspace, size_t workspace_bytes, void* stream) {
   int rc = validate(d);
   if (rc) return rc;
   const size_t units = (size_t)d->B * d->H;
@@ -121,20 +122,36 @@ int deltanet_fwd(const deltanet_desc* d, const void* q, const void* k, const voi
   if (units && (!workspace || workspace_bytes < need)) return DELTANET_ERR_WORKSPACE;
   if (!units) return DELTANET_OK;
   dn::Args a = make_args(d, workspace);
-  a.q = q; a.k = k; a.v = v; a.beta = beta; a.h0 = h0; a.o = o; a.hT = hT;
+  a.q = q; a.k = k; a.v = v; a.beta = beta; a.h0 = h0; a.o = o; a.hT = hT; a.g = g;
   cudaStream_t s = (cudaStream_t)stream;
   return use_tc(d) ? dn::tc_fwd(a, s) : dn::simt_fwd(a, d->dtype, s);
 }
 
-int deltanet_bwd(const deltanet_desc* d, const void* q, const void* k, const void* v,
-                 const void* beta, const float* h0, const void* dO, const float* dhT, void* dq,
-                 void* dk, void* dv, void* dbeta, float* dh0, void* workspace,
+int deltanet_fwd(const deltanet_desc* d, const void* q, const void* k, const void* v,
+                 const void* beta, const float* h0, void* o, float* hT, void* workspace,
                  size_t workspace_bytes, void* stream) {
+  if (d && (d->flags & DELTANET_GATED)) return DELTANET_ERR_INVALID_ARG;
+  return fwd_impl(d, q, k, v, beta, nullptr, h0, o, hT, workspace, workspace_bytes, stream);
+}
+
+int deltanet_gated_fwd(const deltanet_desc* d, const void* q, const void* k, const void* v,
+                       const void* beta, const float* g, const float* h0, void* o, float* hT,
+                       void* workspace, size_t workspace_bytes, void* stream) {
+  if (!d) return DELTANET_ERR_INVALID_ARG;
+  deltanet_desc e = *d;
+  if (g) e.flags |= DELTANET_GATED;
+  return fwd_impl(&e, q, k, v, beta, g, h0, o, hT, workspace, workspace_bytes, stream);
+}
+
+static int bwd_impl(const deltanet_desc* d, const void* q, const void* k, const void* v,
+                    const void* beta, const float* g, const float* h0, const void* dO,
+                    const float* dhT, void* dq, void* dk, void* dv, void* dbeta, float* dg,
+                    float* dh0, void* workspace, size_t workspace_bytes, void* stream) {
   int rc = validate(d);
   if (rc) return rc;
   const size_t units = (size_t)d->B * d->H;
   const bool tokens = units && d->L > 0;
-  if (tokens && (!q || !k || !v || !beta || !dO || !dq || !dk || !dv || !dbeta))
+  if (tokens && (!q || !k || !v || !beta || !dO || !dq || !dk || !dv || !dbeta || (g && !dg)))
     return DELTANET_ERR_INVALID_ARG;
   if (misaligned(q) || misaligned(k) || misaligned(v) || misaligned(beta) || misaligned(h0) ||
       misaligned(dO) || misaligned(dhT) || misaligned(dq) || misaligned(dk) || misaligned(dv) ||
@@ -145,14 +162,40 @@ int deltanet_bwd(const deltanet_desc* d, const void* q, const void* k, const voi
   if (!units) return DELTANET_OK;
   dn::Args a = make_args(d, workspace);
   a.q = q; a.k = k; a.v = v; a.beta = beta; a.h0 = h0; a.dO = dO; a.dhT = dhT;
-  a.dq = dq; a.dk = dk; a.dv = dv; a.dbeta = dbeta; a.dh0 = dh0;
+  a.dq = dq; a.dk = dk; a.dv = dv; a.dbeta = dbeta; a.dh0 = dh0; a.g = g; a.dg = dg;
   cudaStream_t s = (cudaStream_t)stream;
   return use_tc(d) ? dn::tc_bwd(a, s) : dn::simt_bwd(a, d->dtype, s);
+}
+
+int deltanet_bwd(const deltanet_desc* d, const void* q, const void* k, const void* v,
+                 const void* beta, const float* h0, const void* dO, const float* dhT, void* dq,
+                 void* dk, void* dv, void* dbeta, float* dh0, void* workspace,
+                 size_t workspace_bytes, void* stream) {
+  if (d && (d->flags & DELTANET_GATED)) return DELTANET_ERR_INVALID_ARG;
+  return bwd_impl(d, q, k, v, beta, nullptr, h0, dO, dhT, dq, dk, dv, dbeta, nullptr, dh0,
+                  workspace, workspace_bytes, stream);
+}
+
+int deltanet_gated_bwd(const deltanet_desc* d, const void* q, const void* k, const void* v,
+                       const void* beta, const float* g, const float* h0, const void* dO,
+                       const float* dhT, void* dq, void* dk, void* dv, void* dbeta, float* dg,
+                       float* dh0, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!d) return DELTANET_ERR_INVALID_ARG;
+  deltanet_desc e = *d;
+  if (g) e.flags |= DELTANET_GATED;
+  return bwd_impl(&e, q, k, v, beta, g, h0, dO, dhT, dq, dk, dv, dbeta, dg, dh0, workspace,
+                  workspace_bytes, stream);
 }
 
 int deltanet_recurrent_fwd(const deltanet_desc* d, const void* q, const void* k, const void* v,
                            const void* beta, const float* h0, void* o, float* hT,
                            void* stream) {
+  return deltanet_gated_recurrent_fwd(d, q, k, v, beta, nullptr, h0, o, hT, stream);
+}
+
+int deltanet_gated_recurrent_fwd(const deltanet_desc* d, const void* q, const void* k,
+                                 const void* v, const void* beta, const float* g,
+                                 const float* h0, void* o, float* hT, void* stream) {
   int rc = validate_rec(d);
   if (rc) return rc;
   const size_t units = (size_t)d->B * d->H;
@@ -166,7 +209,7 @@ int deltanet_recurrent_fwd(const deltanet_desc* d, const void* q, const void* k,
   a.B = d->B; a.H = d->H; a.L = d->L; a.Dk = d->Dk; a.Dv = d->Dv;
   a.flags = d->flags;
   a.eps = d->l2_eps > 0.f ? d->l2_eps : 1e-6f;
-  a.q = q; a.k = k; a.v = v; a.beta = beta; a.h0 = h0; a.o = o; a.hT = hT;
+  a.q = q; a.k = k; a.v = v; a.beta = beta; a.h0 = h0; a.o = o; a.hT = hT; a.g = g;
   return dn::rec_fwd(a, d->dtype, (cudaStream_t)stream);
 }
 

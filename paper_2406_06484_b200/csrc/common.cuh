@@ -29,6 +29,10 @@ struct Args {
   float* hseg;  // [B*H][nseg][Dk][Dv] state at each segment start (pass 3 input)
   float* hloc;  // [B*H][nseg][Dk][Dv] segment-local end state from zero (pass 1)
   float* psi;   // [B*H][nseg][Dk][Dk] segment transition (pass 1)
+  // Gated DeltaNet (R23): log-decay g [B*H][L]
+  // fp32 (null = ungated) and its gradient
+  const float* g;
+  float* dg;
 };
 
 template <typename T>
@@ -69,6 +73,7 @@ int prologue_bwd(const deltanet_desc* d, const void* xq, const void* xk, const v
 
 // tcgen05 path entry points (tc_fwd.cu / tc_bwd.cu)
 bool tc_supported(const deltanet_desc* d);
+bool tc_gated_supported(const deltanet_desc* d);
 size_t tc_scratch_bytes(const deltanet_desc* d);
 int tc_fwd(const Args& a, cudaStream_t s);
 int tc_bwd(const Args& a, cudaStream_t s);

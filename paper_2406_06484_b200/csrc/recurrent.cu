@@ -9,7 +9,9 @@
 // independently of the other columns given the token stream, so the state is
 // split by columns across threads and CTAs: a CTA owns VB <= 64 columns of one
 // (b, h) unit, a thread owns RPT <= 64 rows of one column in registers (TPC
-// threads per column, adjacent lanes, combined with shuffles).  Tokens are
+// threads per column, adjacent lanes, combined with shuffles).  Gated
+// DeltaNet (R23): H <- alpha (H - beta k (k^T H)) + beta k v^T, i.e.
+// H[i][j] = alpha H[i][j] - beta (alpha u_j - v_j) k_i.  Tokens are
 // staged through shared memory 32 at a time (q, k normalised there).  fp32
 // state and arithmetic; bf16 or fp32 I/O.  Latency-bound on the per-token
 // dependency (two TPC-lane reductions per token) at long L; HBM-bound on the
@@ -40,6 +42,7 @@ __global__ void __launch_bounds__(256) rec_fwd_kernel(Args a, int VB) {
   float* sv = sq + TB * S::KS;       // [TB][VB]
   float* so = sv + TB * VB;          // [TB][VB]
   float* sb = so + TB * VB;          // [TB]
+  float* sa = sb + TB;               // [TB] alpha = exp(g) (1 without a gate)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
   const int unit = blockIdx.x, c0 = blockIdx.y * VB;
@@ -51,6 +54,7 @@ __global__ void __launch_bounds__(256) rec_fwd_kernel(Args a, int VB) {
   const T* v = (const T*)a.v + (size_t)unit * L * Dv;
   const T* beta = (const T*)a.beta + (size_t)unit * L;
   T* o = (T*)a.o + (size_t)unit * L * Dv;
+  const float* gg = a.g ? a.g + (size_t)unit * L : nullptr;
 
   float h[S::RPT];
   {
@@ -72,7 +76,10 @@ __global__ void __launch_bounds__(256) rec_fwd_kernel(Args a, int VB) {
       const int t = e / VB, j = e % VB;
       sv[t * VB + j] = ldf(v + (size_t)(t0 + t) * Dv + c0 + j);
     }
-    if (tid < nt) sb[tid] = ldf(beta + t0 + tid);
+    if (tid < nt) {
+      sb[tid] = ldf(beta + t0 + tid);
+      sa[tid] = gg ? __expf(gg[t0 + tid]) : 1.f;
+    }
     __syncthreads();
     if (l2) {  // x <- x / max(||x||, eps), one warp per (token, tensor)
       for (int p = warp; p < 2 * nt; p += nwarp) {
@@ -109,17 +116,18 @@ __global__ void __launch_bounds__(256) rec_fwd_kernel(Args a, int VB) {
         const float* kr = sk + t * S::KS + S::idx(seg * S::RPT);
         const float* qr = sq + t * S::KS + S::idx(seg * S::RPT);
         const float* kn = (t + 1 < nt) ? kr + S::KS : kr;  // k_{t+1} (dummy at the block end)
-        const float cc = sb[t] * (u - sv[t * VB + col]);
+        const float al = sa[t];
+        const float cc = sb[t] * (al * u - sv[t * VB + col]);
         float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f, n0 = 0.f, n1 = 0.f, n2 = 0.f, n3 = 0.f;
 #pragma unroll
         for (int r = 0; r < S::RPT; r += 4) {
           const float4 k4 = *reinterpret_cast<const float4*>(kr + r);
           const float4 q4 = *reinterpret_cast<const float4*>(qr + r);
           const float4 n4 = *reinterpret_cast<const float4*>(kn + r);
-          h[r] = fmaf(-cc, k4.x, h[r]);
-          h[r + 1] = fmaf(-cc, k4.y, h[r + 1]);
-          h[r + 2] = fmaf(-cc, k4.z, h[r + 2]);
-          h[r + 3] = fmaf(-cc, k4.w, h[r + 3]);
+          h[r] = fmaf(-cc, k4.x, al * h[r]);
+          h[r + 1] = fmaf(-cc, k4.y, al * h[r + 1]);
+          h[r + 2] = fmaf(-cc, k4.z, al * h[r + 2]);
+          h[r + 3] = fmaf(-cc, k4.w, al * h[r + 3]);
           o0 = fmaf(q4.x, h[r], o0);
           o1 = fmaf(q4.y, h[r + 1], o1);
           o2 = fmaf(q4.z, h[r + 2], o2);
@@ -158,10 +166,10 @@ int launch(const Args& a, cudaStream_t s) {
   const int VB = a.Dv < 64 ? a.Dv : 64;
   const int threads = VB * S::TPC;  // 16..256, a multiple of 16
   const int nthreads = (threads + 31) / 32 * 32;
-  const size_t smem = (size_t)(2 * TB * S::KS + 2 * TB * VB + TB) * sizeof(float);
+  const size_t smem = (size_t)(2 * TB * S::KS + 2 * TB * VB + 2 * TB) * sizeof(float);
   static bool attr = false;  // per template instance: the largest (VB = 64) footprint
   if (!attr) {
-    const size_t smax = (size_t)(2 * TB * S::KS + 2 * TB * 64 + TB) * sizeof(float);
+    const size_t smax = (size_t)(2 * TB * S::KS + 2 * TB * 64 + 2 * TB) * sizeof(float);
     if (cudaFuncSetAttribute(rec_fwd_kernel<T, DK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smax) != cudaSuccess)
       return DELTANET_ERR_CUDA;

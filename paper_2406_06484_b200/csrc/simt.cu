@@ -12,6 +12,13 @@
 // SURVEY App. B) and every shape the tcgen05 path does not cover.
 // Intermediates live in a per-unit global scratch (L2-resident); it is a
 // correctness path, not the throughput path.
+//
+// Gated DeltaNet (R23; oracle/forms.py gated_chunkwise_*): with
+// the in-chunk cumulative log-gate G, gamma_i = e^{G_i}, Gamma(i,r) =
+// e^{G_i - G_r} (r <= i), D_i = e^{G_{C-1} - G_i}, the chunk step becomes
+// X = (I + tril(diag(beta)(Gamma . KK^T), -1))^{-1}, W = X diag(beta gamma) K,
+// O = diag(gamma) Q H + (Gamma . tril(QK^T)) U', H <- gamma_C H + (D K)^T U';
+// without a gate every factor is exactly 1 and the code skips them.
 #include "common.cuh"
 
 namespace dn {
@@ -23,11 +30,12 @@ struct Scratch {
   float *KK, *A, *Ti, *dA, *dTi, *Gb;  // [C*C]
   float *W, *dqh, *dkh, *dW, *dKb;     // [C*Dk]
   float *U, *dUp, *dVb;                // [C*Dv]
+  float *Gc, *dG, *tmp;                // [C] gate: cumulative log-gate, dl/dG, row temp
 };
 
 __host__ __device__ inline size_t scratch_floats(int L, int Dk, int Dv, int C) {
   return 2 * (size_t)L + 2 * (size_t)Dk * Dv + 6 * (size_t)C * C +
-         5 * (size_t)C * Dk + 3 * (size_t)C * Dv;
+         5 * (size_t)C * Dk + 3 * (size_t)C * Dv + 3 * (size_t)C + 1;
 }
 
 __device__ Scratch carve(float* base, int L, int Dk, int Dv, int C) {
@@ -51,12 +59,16 @@ __device__ Scratch carve(float* base, int L, int Dk, int Dv, int C) {
   s.U = p; p += (size_t)C * Dv;
   s.dUp = p; p += (size_t)C * Dv;
   s.dVb = p; p += (size_t)C * Dv;
+  s.Gc = p; p += C;
+  s.dG = p; p += C;
+  s.tmp = p; p += C + 1;
   return s;
 }
 
 template <typename T>
 struct Unit {
   const T *q, *k, *v, *beta, *dO;
+  const float* g;  // log-gate of this unit, null = ungated
   int L, Dk, Dv, C;
   bool l2;
   float eps;
@@ -80,7 +92,28 @@ struct Unit {
   __device__ float dd(int t, int j) const {
     return t < L ? ldf(dO + (size_t)t * Dv + j) : 0.f;
   }
+  // gate factors of the current chunk (s.Gc filled by chunk_gates)
+  __device__ float gam(int i) const { return g ? __expf(s.Gc[i]) : 1.f; }
+  __device__ float Gam(int i, int r) const {
+    return g ? (r <= i ? __expf(s.Gc[i] - s.Gc[r]) : 0.f) : (r <= i ? 1.f : 0.f);
+  }
+  __device__ float Dn(int i) const { return g ? __expf(s.Gc[C - 1] - s.Gc[i]) : 1.f; }
 };
+
+// s.Gc[i] = sum_{j <= i} g[t0 + j] (padding: g = 0)
+template <typename T>
+__device__ void chunk_gates(const Unit<T>& u, int t0) {
+  if (!u.g) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float acc = 0.f;
+    for (int i = 0; i < u.C; ++i) {
+      acc += (t0 + i < u.L) ? u.g[t0 + i] : 0.f;
+      u.s.Gc[i] = acc;
+    }
+  }
+  __syncthreads();
+}
 
 template <typename T>
 __device__ void row_norms(Unit<T>& u) {
@@ -104,6 +137,7 @@ template <typename T>
 __device__ void chunk_ut(const Unit<T>& u, int t0) {
   const int C = u.C, Dk = u.Dk, Dv = u.Dv;
   const Scratch& s = u.s;
+  chunk_gates(u, t0);
   for (int e = threadIdx.x; e < C * C; e += blockDim.x) {
     int i = e / C, j = e % C;
     float kk = 0.f, qk = 0.f;
@@ -113,7 +147,7 @@ __device__ void chunk_ut(const Unit<T>& u, int t0) {
       qk = fmaf(u.qh(t0 + i, m), kj, qk);
     }
     s.KK[e] = kk;
-    s.A[e] = (j <= i) ? qk : 0.f;
+    s.A[e] = (j <= i) ? qk * u.Gam(i, j) : 0.f;
   }
   __syncthreads();
   // column j of Ti: x_i = delta_ij - sum_{j<=m<i} beta_i KK[i][m] x_m
@@ -122,7 +156,8 @@ __device__ void chunk_ut(const Unit<T>& u, int t0) {
       float x = (i == j) ? 1.f : 0.f;
       if (i > j) {
         const float bi = u.bb(t0 + i);
-        for (int m = j; m < i; ++m) x = fmaf(-bi * s.KK[i * C + m], s.Ti[m * C + j], x);
+        for (int m = j; m < i; ++m)
+          x = fmaf(-bi * s.KK[i * C + m] * u.Gam(i, m), s.Ti[m * C + j], x);
       }
       s.Ti[i * C + j] = (i < j) ? 0.f : x;
     }
@@ -131,7 +166,8 @@ __device__ void chunk_ut(const Unit<T>& u, int t0) {
   for (int e = threadIdx.x; e < C * Dk; e += blockDim.x) {
     int i = e / Dk, m = e % Dk;
     float w = 0.f;
-    for (int r = 0; r <= i; ++r) w = fmaf(s.Ti[i * C + r] * u.bb(t0 + r), u.kh(t0 + r, m), w);
+    for (int r = 0; r <= i; ++r)
+      w = fmaf(s.Ti[i * C + r] * u.bb(t0 + r) * u.gam(r), u.kh(t0 + r, m), w);
     s.W[e] = w;
   }
   for (int e = threadIdx.x; e < C * Dv; e += blockDim.x) {
@@ -190,16 +226,19 @@ __device__ void unit_forward(const Unit<T>& u, const float* h0, T* o, float* hT,
         if (t0 + i >= L) continue;
         float x = 0.f;
         for (int m = 0; m < Dk; ++m) x = fmaf(u.qh(t0 + i, m), s.H[m * Dv + j], x);
+        x *= u.gam(i);
         for (int r = 0; r <= i; ++r) x = fmaf(s.A[i * C + r], s.U[r * Dv + j], x);
         stf(o + (size_t)(t0 + i) * Dv + j, x);
       }
       __syncthreads();  // O reads H_t; the update below overwrites it
     }
     // H += K^T U'   (Eq. 8; Listing 1)
+    // gated: H <- gamma_C H + (D K)^T U'
+    const float gC = u.gam(C - 1);
     for (int e = threadIdx.x; e < Dk * Dv; e += blockDim.x) {
       int m = e / Dv, j = e % Dv;
-      float x = s.H[e];
-      for (int r = 0; r < C; ++r) x = fmaf(u.kh(t0 + r, m), s.U[r * Dv + j], x);
+      float x = s.H[e] * gC;
+      for (int r = 0; r < C; ++r) x = fmaf(u.kh(t0 + r, m) * u.Dn(r), s.U[r * Dv + j], x);
       s.H[e] = x;
     }
     __syncthreads();
@@ -217,6 +256,7 @@ __global__ void __launch_bounds__(256) simt_fwd_kernel(Args a) {
   u.v = (const T*)a.v + unit * a.L * a.Dv;
   u.beta = (const T*)a.beta + unit * a.L;
   u.dO = nullptr;
+  u.g = a.g ? a.g + unit * a.L : nullptr;
   u.L = a.L; u.Dk = a.Dk; u.Dv = a.Dv; u.C = a.C;
   u.l2 = (a.flags & DELTANET_L2NORM_QK) != 0;
   u.eps = a.eps;
@@ -240,6 +280,7 @@ __global__ void __launch_bounds__(256) simt_bwd_kernel(Args a) {
   u.v = (const T*)a.v + unit * L * Dv;
   u.beta = (const T*)a.beta + unit * L;
   u.dO = (const T*)a.dO + unit * L * Dv;
+  u.g = a.g ? a.g + unit * L : nullptr;
   u.L = L; u.Dk = Dk; u.Dv = Dv; u.C = C;
   u.l2 = (a.flags & DELTANET_L2NORM_QK) != 0;
   u.eps = a.eps;
@@ -270,6 +311,7 @@ __global__ void __launch_bounds__(256) simt_bwd_kernel(Args a) {
       int i = e / Dv, j = e % Dv;
       float x = 0.f;
       for (int m = 0; m < Dk; ++m) x = fmaf(u.kh(t0 + i, m), s.dH[m * Dv + j], x);
+      x *= u.Dn(i);
       for (int r = i; r < C; ++r) x = fmaf(s.A[r * C + i], u.dd(t0 + r, j), x);
       s.dUp[e] = x;
     }
@@ -291,19 +333,59 @@ __global__ void __launch_bounds__(256) simt_bwd_kernel(Args a) {
         xk = fmaf(s.U[i * Dv + j], s.dH[m * Dv + j], xk);
         xw = fmaf(-s.dUp[i * Dv + j], h, xw);
       }
-      for (int r = 0; r <= i; ++r) xq = fmaf(s.dA[i * C + r], u.kh(t0 + r, m), xq);
-      for (int r = i; r < C; ++r) xk = fmaf(s.dA[r * C + i], u.qh(t0 + r, m), xk);
+      xq *= u.gam(i);
+      xk *= u.Dn(i);
+      for (int r = 0; r <= i; ++r) xq = fmaf(s.dA[i * C + r] * u.Gam(i, r), u.kh(t0 + r, m), xq);
+      for (int r = i; r < C; ++r) xk = fmaf(s.dA[r * C + i] * u.Gam(r, i), u.qh(t0 + r, m), xk);
       s.dqh[e] = xq;
       s.dkh[e] = xk;
       s.dW[e] = xw;
     }
     __syncthreads();
-    // 6. dH += Q^T dO - W^T dU'
+    if (u.g) {
+      // gate, part 1 (dl/dG_i, G the cumulative log-gate): from gamma in
+      // diag(gamma) Q H, from D in (D K)^T U', from Gamma in A, and
+      // gamma_C <dH, H> from gamma_C H
+      for (int i = threadIdx.x; i < C; i += blockDim.x) {
+        float qo = 0.f, dd = 0.f;
+        for (int m = 0; m < Dk; ++m) {
+          float ph = 0.f, pu = 0.f;
+          for (int j = 0; j < Dv; ++j) {
+            ph = fmaf(u.dd(t0 + i, j), s.H[m * Dv + j], ph);
+            pu = fmaf(s.U[i * Dv + j], s.dH[m * Dv + j], pu);
+          }
+          qo = fmaf(u.qh(t0 + i, m), ph, qo);
+          dd = fmaf(u.kh(t0 + i, m), pu, dd);
+        }
+        float row = 0.f, col = 0.f;
+        for (int r = 0; r <= i; ++r) row = fmaf(s.dA[i * C + r], s.A[i * C + r], row);
+        for (int r = i; r < C; ++r) col = fmaf(s.dA[r * C + i], s.A[r * C + i], col);
+        const float dD = dd * u.Dn(i);
+        s.dG[i] = u.gam(i) * qo - dD + row - col;
+        s.tmp[i] = dD;
+      }
+      if (threadIdx.x == 0) s.tmp[C] = 0.f;
+      __syncthreads();
+      float part = 0.f;
+      for (int e = threadIdx.x; e < Dk * Dv; e += blockDim.x) part = fmaf(s.dH[e], s.H[e], part);
+      for (int m = 16; m > 0; m >>= 1) part += __shfl_xor_sync(0xffffffffu, part, m);
+      if ((threadIdx.x & 31) == 0) atomicAdd(&s.tmp[C], part);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        float x = u.gam(C - 1) * s.tmp[C];
+        for (int i = 0; i < C; ++i) x += s.tmp[i];
+        s.dG[C - 1] += x;
+      }
+      __syncthreads();
+    }
+    // 6. dH += Q^T dO - W^T dU'   (gated: dH <- gamma_C dH + (gamma Q)^T dO - W^T dU')
+    const float gC = u.gam(C - 1);
     for (int e = threadIdx.x; e < Dk * Dv; e += blockDim.x) {
       int m = e / Dv, j = e % Dv;
-      float x = s.dH[e];
+      float x = s.dH[e] * gC;
       for (int i = 0; i < C; ++i)
-        x = fmaf(u.qh(t0 + i, m), u.dd(t0 + i, j), fmaf(-s.W[i * Dk + m], s.dUp[i * Dv + j], x));
+        x = fmaf(u.qh(t0 + i, m) * u.gam(i), u.dd(t0 + i, j),
+                 fmaf(-s.W[i * Dk + m], s.dUp[i * Dv + j], x));
       s.dH[e] = x;
     }
     // 7. dTi = dW (beta K)^T + dU' (beta V)^T
@@ -311,6 +393,7 @@ __global__ void __launch_bounds__(256) simt_bwd_kernel(Args a) {
       int i = e / C, r = e % C;
       float x = 0.f;
       for (int m = 0; m < Dk; ++m) x = fmaf(s.dW[i * Dk + m], u.kh(t0 + r, m), x);
+      x *= u.gam(r);
       for (int j = 0; j < Dv; ++j) x = fmaf(s.dUp[i * Dv + j], u.vv(t0 + r, j), x);
       s.dTi[e] = x * u.bb(t0 + r);
     }
@@ -353,19 +436,44 @@ __global__ void __launch_bounds__(256) simt_bwd_kernel(Args a) {
     for (int e = threadIdx.x; e < C * Dk; e += blockDim.x) {
       int i = e / Dk, m = e % Dk;
       const float bi = u.bb(t0 + i);
-      float x = s.dkh[e] + bi * s.dKb[e];
-      for (int r = 0; r < i; ++r) x = fmaf(bi * s.Gb[i * C + r], u.kh(t0 + r, m), x);
-      for (int r = i + 1; r < C; ++r) x = fmaf(u.bb(t0 + r) * s.Gb[r * C + i], u.kh(t0 + r, m), x);
+      float x = s.dkh[e] + bi * u.gam(i) * s.dKb[e];
+      for (int r = 0; r < i; ++r)
+        x = fmaf(bi * s.Gb[i * C + r] * u.Gam(i, r), u.kh(t0 + r, m), x);
+      for (int r = i + 1; r < C; ++r)
+        x = fmaf(u.bb(t0 + r) * s.Gb[r * C + i] * u.Gam(r, i), u.kh(t0 + r, m), x);
       s.dkh[e] = x;
     }
     // 12/14. dbeta = rowsum(dKb . K) + rowsum(dVb . V) + rowsum(Gb . KK)
     for (int i = threadIdx.x; i < C; i += blockDim.x) {
       if (t0 + i >= L) continue;
-      float x = 0.f;
-      for (int m = 0; m < Dk; ++m) x = fmaf(s.dKb[i * Dk + m], u.kh(t0 + i, m), x);
+      float rk = 0.f, x = 0.f;
+      for (int m = 0; m < Dk; ++m) rk = fmaf(s.dKb[i * Dk + m], u.kh(t0 + i, m), rk);
       for (int j = 0; j < Dv; ++j) x = fmaf(s.dVb[i * Dv + j], u.vv(t0 + i, j), x);
-      for (int r = 0; r < i; ++r) x = fmaf(s.Gb[i * C + r], s.KK[i * C + r], x);
+      x = fmaf(u.gam(i), rk, x);
+      for (int r = 0; r < i; ++r) x = fmaf(s.Gb[i * C + r] * u.Gam(i, r), s.KK[i * C + r], x);
       stf(dbeta + t0 + i, x);
+    }
+    if (u.g) {
+      // gate, part 2: gamma in W's diag(beta gamma), Gamma in the UT matrix;
+      // then dg = reverse cumulative sum of dl/dG within the chunk
+      for (int i = threadIdx.x; i < C; i += blockDim.x) {
+        const float bi = u.bb(t0 + i);
+        float rk = 0.f, row = 0.f, col = 0.f;
+        for (int m = 0; m < Dk; ++m) rk = fmaf(s.dKb[i * Dk + m], u.kh(t0 + i, m), rk);
+        for (int r = 0; r < i; ++r)
+          row = fmaf(bi * s.Gb[i * C + r] * u.Gam(i, r), s.KK[i * C + r], row);
+        for (int r = i + 1; r < C; ++r)
+          col = fmaf(u.bb(t0 + r) * s.Gb[r * C + i] * u.Gam(r, i), s.KK[r * C + i], col);
+        s.dG[i] += bi * u.gam(i) * rk + row - col;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        float acc = 0.f;
+        for (int i = C - 1; i >= 0; --i) {
+          acc += s.dG[i];
+          if (t0 + i < L && a.dg) a.dg[unit * L + t0 + i] = acc;
+        }
+      }
     }
     __syncthreads();
     // L2-norm adjoint (R9): dx = (dxh - xh (xh . dxh)) / ||x|| if ||x|| >= eps

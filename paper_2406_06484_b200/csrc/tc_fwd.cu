@@ -846,6 +846,9 @@ bool tc_supported(const deltanet_desc* d) {
   return d->dtype == DELTANET_BF16 && d->chunk == C && d->Dk == DK && d->Dv == DV && d->L > 0;
 }
 
+// gated DeltaNet (R23) on the tcgen05 kernels: not yet (SIMT path)
+bool tc_gated_supported(const deltanet_desc*) { return false; }
+
 // per-chunk records [X | W^T | Z^T] the backward reads (40 KB per chunk per unit)
 namespace {
 int sm_count() {

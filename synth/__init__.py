@@ -15,6 +15,10 @@ Each (b, h) unit has its own counter-style seed
 so any rank (or the oracle) can regenerate any unit alone.
 Alternative key distributions for parity edge cases: "gaussian" (raw
 N(0,1) keys), "identical" (all keys of a unit equal, beta=1).
+
+Gated DeltaNet (f4, R23) log-gates, fp32, from a separate stream:
+  g = -scale * softplus(N(0,1))      (alpha = e^g in (0, 1))
+scale = 0.05 is a slow decay (mean alpha ~ 0.96), 1.0 a fast one.
 """
 from __future__ import annotations
 
@@ -128,3 +132,17 @@ def make_inputs(cfg: Config, b_range=None, keys="silu", units=None):
 
 def custom_config(B, H, L, Dk, Dv, chunk, dtype, index=100, name="custom"):
     return Config(name, B, H, L, Dk, Dv, chunk, dtype, index)
+
+
+def make_gates(cfg: Config, scale: float = 0.05, b_range=None):
+    """Log-gates g [B', H, L] fp32 (seed stream: the unit seed + 7919)."""
+    if b_range is None:
+        b_range = range(cfg.B)
+    b_range = list(b_range)
+    out = np.empty((len(b_range), cfg.H, cfg.L), np.float32)
+    for bi, b in enumerate(b_range):
+        for h in range(cfg.H):
+            rng = np.random.Generator(np.random.Philox(unit_seed(cfg.index, b, h, cfg.H) + 7919))
+            z = rng.standard_normal(cfg.L, dtype=np.float32).astype(np.float64)
+            out[bi, h] = (-scale * np.logaddexp(0.0, z)).astype(np.float32)
+    return out

@@ -44,7 +44,7 @@ def test_no_torch_types_in_abi():
 
 
 def test_abi_version_and_strerror(lib):
-    assert lib.deltanet_abi_version() == 4
+    assert lib.deltanet_abi_version() == 5
     for code in range(6):
         assert dn.deltanet_strerror(code)
     assert "unknown" in dn.deltanet_strerror(99)
@@ -149,3 +149,22 @@ def test_context_parallel_errors_before_launch(lib):
         assert dn.deltanet_launch_count(_desc(**ok), which) >= 1
         assert dn.deltanet_launch_count(e, which) == 0
         assert dn.deltanet_launch_count(_desc(Dk=64, Dv=64), which) == -1
+
+
+def test_gated_errors_before_launch(lib):
+    """Gated entry points: g without dg is INVALID_ARG; the plain entry points
+    refuse a descriptor carrying DELTANET_GATED; the workspace query with the
+    flag covers the gated path; the CP transitions refuse it."""
+    D = ctypes.byref
+    nul = None
+    a = ctypes.c_void_p(16 * 1024)
+    big = 1 << 34
+    d = _desc()
+    assert lib.deltanet_gated_bwd(D(d), a, a, a, a, a, nul, a, nul, a, a, a, a, nul, nul, a, big,
+                                  nul) == 1
+    dg = _desc(flags=dn.DELTANET_GATED)
+    assert lib.deltanet_fwd(D(dg), a, a, a, a, nul, a, nul, a, big, nul) == 1
+    assert dn.deltanet_workspace_bytes(dg) > 0
+    ok = _desc(Dk=128, Dv=128, chunk=64, flags=dn.DELTANET_GATED)
+    assert lib.deltanet_fwd_transition(D(ok), a, a, a, a, a, a, nul) == 2
+    assert dn.deltanet_launch_count(dg, 0) == 1

@@ -1,0 +1,131 @@
+"""GPU parity of Gated DeltaNet (include/deltanet.h
+deltanet_gated_fwd / _bwd / _recurrent_fwd; R23) against the fp64
+oracle (oracle.gated_fwd / gated_bwd, pinned in tests/test_oracle_gated.py),
+normwise (R16): 1e-4 for fp32 I/O, 2e-2 for bf16 I/O; dg is fp32
+in both cases and held to the same bar as the other gradients."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from parity import TOL, compare, to_dev, torch_dtype
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2406_06484_b200 import build
+    build.build()
+
+
+def _case(B, H, L, Dk, Dv, C, dtype, index, scale=0.05):
+    cfg = synth.custom_config(B, H, L, Dk, Dv, C, dtype, index=index)
+    inp = synth.make_inputs(cfg)
+    inp["g"] = synth.make_gates(cfg, scale)
+    return inp
+
+
+def _np(t):
+    return None if t is None else t.float().cpu().numpy().astype(np.float64)
+
+
+def _gpu(inp, dtype, C, h0=None, dhT=None, l2norm=True, force_simt=False):
+    import paper_2406_06484_b200 as dn
+    td = torch_dtype(dtype)
+    q, k, v, b, dO = (to_dev(inp[f], td) for f in ("q", "k", "v", "beta", "dO"))
+    g = to_dev(inp["g"], torch.float32)
+    h0t = None if h0 is None else to_dev(h0, torch.float32)
+    dhTt = None if dhT is None else to_dev(dhT, torch.float32)
+    o, hT, ws = dn.deltanet_gated_fwd(q, k, v, b, g, chunk=C, h0=h0t, l2norm=l2norm,
+                                      force_simt=force_simt)
+    dq, dk, dv, db, dg, dh0 = dn.deltanet_gated_bwd(q, k, v, b, g, dO, chunk=C, h0=h0t,
+                                                    dhT=dhTt, workspace=ws, l2norm=l2norm,
+                                                    force_simt=force_simt)
+    torch.cuda.synchronize()
+    return {"o": _np(o), "hT": _np(hT), "dq": _np(dq), "dk": _np(dk), "dv": _np(dv),
+            "dbeta": _np(db), "dg": _np(dg), "dh0": _np(dh0)}
+
+
+def _ref(inp, h0=None, dhT=None, l2norm=True):
+    o, hT = oracle.gated_fwd(inp["q"], inp["k"], inp["v"], inp["beta"], inp["g"], h0=h0,
+                             l2norm=l2norm)
+    dq, dk, dv, db, dg, dh0 = oracle.gated_bwd(inp["q"], inp["k"], inp["v"], inp["beta"],
+                                               inp["g"], inp["dO"], h0=h0, dhT=dhT,
+                                               l2norm=l2norm)
+    return {"o": o, "hT": hT, "dq": dq, "dk": dk, "dv": dv, "dbeta": db, "dg": dg, "dh0": dh0}
+
+
+@pytest.mark.parametrize("Dk,Dv,C", [(16, 16, 16), (32, 64, 32), (64, 32, 16), (128, 128, 64)])
+@pytest.mark.parametrize("scale", [0.05, 1.0])
+def test_fp32_shapes(Dk, Dv, C, scale):
+    inp = _case(2, 2, 3 * C + 5, Dk, Dv, C, "fp32", index=800 + Dk + Dv + C, scale=scale)
+    rng = np.random.default_rng(Dk + Dv)
+    h0 = 0.3 * rng.standard_normal((2, 2, Dk, Dv))
+    dhT = 0.3 * rng.standard_normal((2, 2, Dk, Dv))
+    compare(_gpu(inp, "fp32", C, h0=h0, dhT=dhT), _ref(inp, h0=h0, dhT=dhT), TOL["fp32"])
+
+
+def test_fp32_no_l2norm():
+    inp = _case(1, 2, 77, 32, 32, 16, "fp32", index=830)
+    inp["k"] = 0.3 * inp["k"]
+    compare(_gpu(inp, "fp32", 16, l2norm=False), _ref(inp, l2norm=False), TOL["fp32"])
+
+
+@pytest.mark.parametrize("L", [64, 300])
+def test_bf16_target_shape(L):
+    inp = _case(2, 2, L, 128, 128, 64, "bf16", index=840 + L)
+    compare(_gpu(inp, "bf16", 64), _ref(inp), TOL["bf16"])
+
+
+def test_zero_gate_equals_ungated_kernel():
+    """g = 0 through the gated entry points is the ungated SIMT computation, bit for bit."""
+    import paper_2406_06484_b200 as dn
+    inp = _case(2, 2, 150, 64, 64, 32, "fp32", index=850)
+    inp["g"] = np.zeros_like(inp["g"])
+    got = _gpu(inp, "fp32", 32)
+    q, k, v, b, dO = (to_dev(inp[f], torch.float32) for f in ("q", "k", "v", "beta", "dO"))
+    o, hT, ws = dn.deltanet_fwd(q, k, v, b, chunk=32, force_simt=True)
+    dq, dk, dv, db, dh0 = dn.deltanet_bwd(q, k, v, b, dO, chunk=32, workspace=ws,
+                                          force_simt=True)
+    torch.cuda.synchronize()
+    for key, t in (("o", o), ("hT", hT), ("dq", dq), ("dk", dk), ("dv", dv), ("dbeta", db),
+                   ("dh0", dh0)):
+        assert np.array_equal(got[key], _np(t)), key
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+@pytest.mark.parametrize("scale", [0.05, 1.0])
+def test_recurrent_gated(dtype, scale):
+    import paper_2406_06484_b200 as dn
+    inp = _case(2, 3, 70, 128, 128, 64, dtype, index=860, scale=scale)
+    td = torch_dtype(dtype)
+    q, k, v, b = (to_dev(inp[f], td) for f in ("q", "k", "v", "beta"))
+    g = to_dev(inp["g"], torch.float32)
+    h0 = 0.3 * np.random.default_rng(2).standard_normal((2, 3, 128, 128))
+    o, hT = dn.deltanet_gated_recurrent_fwd(q, k, v, b, g, h0=to_dev(h0, torch.float32))
+    torch.cuda.synchronize()
+    ro, rhT = oracle.gated_fwd(inp["q"], inp["k"], inp["v"], inp["beta"], inp["g"], h0=h0)
+    compare({"o": _np(o), "hT": _np(hT)}, {"o": ro, "hT": rhT}, TOL[dtype])
+
+
+def test_recurrent_gated_decode_loop():
+    """One-token gated calls carrying the state in place equal one call over L."""
+    import paper_2406_06484_b200 as dn
+    inp = _case(1, 2, 24, 128, 128, 64, "bf16", index=870, scale=0.3)
+    q, k, v, b = (to_dev(inp[f], torch.bfloat16) for f in ("q", "k", "v", "beta"))
+    g = to_dev(inp["g"], torch.float32)
+    o_ref, h_ref = dn.deltanet_gated_recurrent_fwd(q, k, v, b, g)
+    state = torch.zeros((1, 2, 128, 128), dtype=torch.float32, device="cuda")
+    outs = []
+    for t in range(24):
+        sl = lambda x: x[:, :, t:t + 1].contiguous()
+        o, _ = dn.deltanet_gated_recurrent_fwd(sl(q), sl(k), sl(v), sl(b), sl(g), h0=state,
+                                               hT=state)
+        outs.append(o)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(outs, 2), o_ref)
+    assert torch.equal(state, h_ref)

@@ -31,10 +31,13 @@ int validate_rec(const deltanet_desc* d) {
   return DELTANET_OK;
 }
 
+// forward path; the gated backward always runs on the SIMT path (use_tc_bwd)
 bool use_tc(const deltanet_desc* d) {
   return !(d->flags & DELTANET_FORCE_SIMT) && dn::tc_supported(d) &&
          (!(d->flags & DELTANET_GATED) || dn::tc_gated_supported(d));
 }
+
+bool use_tc_bwd(const deltanet_desc* d) { return use_tc(d) && !(d->flags & DELTANET_GATED); }
 
 size_t elem_bytes(const deltanet_desc* d) { return d->dtype == DELTANET_FP32 ? 4 : 2; }
 
@@ -46,9 +49,13 @@ size_t states_bytes(const deltanet_desc* d) {
 size_t round_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 size_t scratch_bytes(const deltanet_desc* d) {
-  if (use_tc(d)) return dn::tc_scratch_bytes(d);
-  return (size_t)d->B * d->H *
-         dn::simt_scratch_floats_per_unit(d->L, d->Dk, d->Dv, d->chunk) * sizeof(float);
+  const size_t simt = (size_t)d->B * d->H *
+                      dn::simt_scratch_floats_per_unit(d->L, d->Dk, d->Dv, d->chunk) *
+                      sizeof(float);
+  if (!use_tc(d)) return simt;
+  const size_t tc = dn::tc_scratch_bytes(d);
+  // gated: tcgen05 forward, SIMT backward -> room for both
+  return (d->flags & DELTANET_GATED) ? (tc > simt ? tc : simt) : tc;
 }
 
 dn::Args make_args(const deltanet_desc* d, void* ws) {
@@ -103,7 +110,7 @@ int deltanet_launch_count(const deltanet_desc* d, int which) {
   }
   if (validate(d) != DELTANET_OK) return -1;
   if ((size_t)d->B * d->H == 0) return 0;
-  if (use_tc(d)) return dn::tc_launch_count(d, which);
+  if (which == 1 ? use_tc_bwd(d) : use_tc(d)) return dn::tc_launch_count(d, which);
   return 1;
 }
 
@@ -164,7 +171,11 @@ static int bwd_impl(const deltanet_desc* d, const void* q, const void* k, const 
   a.q = q; a.k = k; a.v = v; a.beta = beta; a.h0 = h0; a.dO = dO; a.dhT = dhT;
   a.dq = dq; a.dk = dk; a.dv = dv; a.dbeta = dbeta; a.dh0 = dh0; a.g = g; a.dg = dg;
   cudaStream_t s = (cudaStream_t)stream;
-  return use_tc(d) ? dn::tc_bwd(a, s) : dn::simt_bwd(a, d->dtype, s);
+  if (use_tc_bwd(d)) return dn::tc_bwd(a, s);
+  // the SIMT backward cannot read states saved by a tcgen05 forward (their
+  // layout is the bf16 operand image): it recomputes them
+  if (use_tc(d)) a.flags &= ~DELTANET_SAVE_STATES;
+  return dn::simt_bwd(a, d->dtype, s);
 }
 
 int deltanet_bwd(const deltanet_desc* d, const void* q, const void* k, const void* v,

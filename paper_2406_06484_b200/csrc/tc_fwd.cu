@@ -54,8 +54,10 @@ constexpr int OFF_W = OFF_A + 2 * C * C * 2;     // W^T[2] IL R=128 x 64
 constexpr int OFF_H = OFF_W + 2 * DK * C * 2;    // H^T   IL R=128 x 128
 constexpr int OFF_Z = OFF_H + DV * DK * 2;       // Z^T   IL R=128 x 64  | O staging
 constexpr int OFF_L = OFF_Z + DV * C * 2;        // L -> X fp32 [64][LS]
-constexpr int OFF_VEC = OFF_L + C * LS * 4 + 2 * 128 * 4;  // (LX, partial norms) | [2][beta, s, r][64]
-constexpr int OFF_XB = OFF_VEC + 2 * 3 * C * 4;  // X bf16 IL R=64 x 64 (saved for the bwd)
+// per-chunk vectors [2][beta, s, -, G, gamma, D][64] (G, gamma, D: gated only)
+constexpr int NVEC = 6;
+constexpr int OFF_VEC = OFF_L + C * LS * 4 + 2 * 128 * 4;  // (LX, partial norms) | vectors
+constexpr int OFF_XB = OFF_VEC + 2 * NVEC * C * 4;  // X bf16 IL R=64 x 64 (saved for the bwd)
 constexpr int SMEM_BYTES = OFF_XB + C * C * 2;
 static_assert(SMEM_BYTES <= 232448 - 1024, "shared memory budget");
 static_assert(REC_Z == C * C * 2 && REC_BYTES == C * C * 2 + DV * C * 2, "record");
@@ -125,7 +127,13 @@ __device__ long long* dn_tim = nullptr;
 // SEG1 = pass 1 of the segment-parallel forward: from a zero
 // state, the segment's end state H_loc and its transition
 // Psi = prod_c (I - W_c^T K_hat_c) (H^T_end = H^T_start Psi + H^T_loc); no O.
-template <bool SEG1>
+// GATED = Gated DeltaNet (R23, §4.9): per chunk, with the in-chunk
+// cumulative log-gate G, gamma = e^G, Gamma(i,j) = e^{G_i - G_j},
+// D_j = e^{G_63 - G_j}: A and L carry Gamma, T' carries gamma
+// (W = X diag(beta gamma) K_hat), Q rows are scaled by gamma in place before
+// O = Q H, H is rescaled by gamma_63 in TMEM, and the state update takes
+// Z_h = diag(s D) U' from TMEM (bf16 pairs) while O takes Z = diag(s) U'.
+template <bool SEG1, bool GATED = false>
 __global__ void __launch_bounds__(NT, 1)
     tc_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                   const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mO,
@@ -183,7 +191,7 @@ __global__ void __launch_bounds__(NT, 1)
   auto sK = [&](int b) { return smem + OFF_K + b * TILE; };
   auto sA = [&](int b) { return smem + OFF_A + b * C * C * 2; };
   auto sW = [&](int b) { return smem + OFF_W + (SEG1 ? 1 : b) * DK * C * 2; };
-  auto vec = [&](int b) { return reinterpret_cast<float*>(smem + OFF_VEC) + b * 3 * C; };
+  auto vec = [&](int b) { return reinterpret_cast<float*>(smem + OFF_VEC) + b * NVEC * C; };
   uint8_t* sV = smem + OFF_V;
   uint8_t* sT = smem + OFF_T;
   uint8_t* sTu = smem + OFF_TU;
@@ -210,17 +218,42 @@ __global__ void __launch_bounds__(NT, 1)
     const __nv_bfloat16* beta = (const __nv_bfloat16*)a.beta + (size_t)unit * a.L + T0;
     // beta is prefetched into a register one chunk ahead (global latency)
     float bnext = (w < C && w < L) ? __bfloat162float(beta[w]) : 0.f;
+    // gated: own log-gate and the warp-0 counterpart (lane), one chunk ahead
+    const float* gsrc = GATED ? a.g + (size_t)unit * a.L + T0 : nullptr;
+    float gnext = 0.f, g0next = 0.f;
+    if (GATED) {
+      gnext = (w < C && w < L) ? gsrc[w] : 0.f;
+      g0next = (lane < L) ? gsrc[lane] : 0.f;
+    }
 #pragma unroll 1
     for (int c = 0; c < NC; ++c) {
       const int b = c & 1, t0 = c * C;
-      float* vb = vec(b);  // beta, s, r of this chunk
+      float* vb = vec(b);  // beta, s, -, G, gamma, D of this chunk
       const float bval = bnext;
       bnext = (w < C && t0 + C + w < L) ? __bfloat162float(beta[t0 + C + w]) : 0.f;
+      float gval = 0.f, g0val = 0.f;
+      if (GATED) {
+        gval = gnext;
+        g0val = g0next;
+        gnext = (w < C && t0 + C + w < L) ? gsrc[t0 + C + w] : 0.f;
+        g0next = (t0 + C + lane < L) ? gsrc[t0 + C + lane] : 0.f;
+      }
       TSTAMP(0);
       if (c >= 2) mbar_wait(&bar_empty[b], ((c >> 1) - 1) & 1);  // chain c-2 released b
       if (tid == 0 && recs) bulk_wait_read0();  // record stores of chunk c-1 read out
       TSTAMP(1);
       if (half == 0 && w < C) vb[w] = bval;
+      if (GATED && half == 0 && w < C) {
+        // G_w = sum_{j <= w} g_j: warp inclusive scan + warp 0's total
+        float x = gval, t0s = g0val;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const float y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+          t0s += __shfl_xor_sync(0xffffffffu, t0s, o);
+        }
+        vb[3 * C + w] = x + (w >= 32 ? t0s : 0.f);
+      }
       TSTAMP(2);
       mbar_wait(&g_done, c & 1);
       fence_after_sync();
@@ -253,8 +286,13 @@ __global__ void __launch_bounds__(NT, 1)
           vb[C + i] = inv;
         }
         TSTAMP(21);
-        grp_sync<NP>(BAR_P);  // beta, s visible
+        grp_sync<NP>(BAR_P);  // beta, s (and G) visible
         TSTAMP(22);
+        if (GATED && half == 0 && w < C) {  // read after later syncs (T', state WG)
+          const float Gw = vb[3 * C + w];
+          vb[4 * C + w] = __expf(Gw);
+          vb[5 * C + w] = __expf(vb[3 * C + C - 1] - Gw);
+        }
         // lane pair (lo: G_qk row i, hi: G_kk row i) trades halves, so both
         // lanes write 16 columns of A and 16 of L with no divergence
         const bool lo = lane < 16;
@@ -262,13 +300,27 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
         for (int e = 0; e < 16; ++e) x[e] = __shfl_xor_sync(0xffffffffu, lo ? f[16 + e] : f[e], 16);
         const int c0 = h + (lo ? 0 : 16);
-        {  // A = tril(Q K^T), raw (inclusive, R4)
+        // gated: Gamma(i, j) = e^{G_i - G_j} for the 16 columns of this lane
+        float gam16[16];
+        if (GATED) {
+          const float Gi = vb[3 * C + i];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float4 g4 = *reinterpret_cast<const float4*>(vb + 3 * C + c0 + 4 * q);
+            gam16[4 * q + 0] = __expf(fminf(Gi - g4.x, 0.f));
+            gam16[4 * q + 1] = __expf(fminf(Gi - g4.y, 0.f));
+            gam16[4 * q + 2] = __expf(fminf(Gi - g4.z, 0.f));
+            gam16[4 * q + 3] = __expf(fminf(Gi - g4.w, 0.f));
+          }
+        }
+        {  // A = tril(Q K^T), raw (inclusive, R4); gated: Gamma . A
 #pragma unroll
           for (int g = 0; g < 2; ++g) {
             float a8[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-              const float qk = lo ? f[g * 8 + e] : x[g * 8 + e];
+              float qk = lo ? f[g * 8 + e] : x[g * 8 + e];
+              if (GATED) qk *= gam16[g * 8 + e];
               a8[e] = (c0 + g * 8 + e <= i) ? qk : 0.f;
             }
             if (!SEG1) il_store8(sA(b), C, i, c0 + g * 8, a8);
@@ -284,7 +336,10 @@ __global__ void __launch_bounds__(NT, 1)
             const int j = c0 + 4 * q;
             float kk[4];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) kk[e] = lo ? x[4 * q + e] : f[16 + 4 * q + e];
+            for (int e = 0; e < 4; ++e) {
+              kk[e] = lo ? x[4 * q + e] : f[16 + 4 * q + e];
+              if (GATED) kk[e] *= gam16[4 * q + e];
+            }
             float4 v;
             v.x = (j + 0 < i) ? bi * s4[q].x * kk[0] : 0.f;
             v.y = (j + 1 < i) ? bi * s4[q].y * kk[1] : 0.f;
@@ -326,6 +381,7 @@ __global__ void __launch_bounds__(NT, 1)
             xs[e] = xm;
             y[e] = xm * vb[j];  // vb[j]: broadcast across lanes
             x[e] = y[e] * vb[C + j];
+            if (GATED) x[e] *= vb[4 * C + j];  // W = X diag(beta gamma) K_hat
           }
           il_store8(sT, C, i, j0 + g * 8, x);
           il_store8(sTu, C, i, j0 + g * 8, y);
@@ -408,6 +464,37 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
         for (int g = 0; g < 8; ++g) il_store8(sW(b), DK, w, g * 8, f + g * 8);
       }
+      // r_i = 1/max(||q_i||, eps) for this lane's output row (R9): partial sums
+      // of squares over column halves (thread w: row w & 63, half w >> 6).
+      // Gated: the same pass scales the raw Q rows by gamma in place (O = Q H
+      // then carries diag(gamma)), so it runs before bar_full releases Q.
+      float ri = 0.f;
+      auto norms = [&]() {
+        const int row = w & 63, hh = w >> 6;
+        float x[DK / 2];
+#pragma unroll
+        for (int g = 0; g < DK / 16; ++g) il_load8(sQ(b), C, row, DK / 2 * hh + g * 8, x + 8 * g);
+        float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+        for (int e = 0; e < DK / 2; e += 2) {
+          acc0 = fmaf(x[e], x[e], acc0);
+          acc1 = fmaf(x[e + 1], x[e + 1], acc1);
+        }
+        qn2[hh * C + row] = acc0 + acc1;
+        if (GATED) {
+          const float gr = vb[4 * C + row];
+#pragma unroll
+          for (int e = 0; e < DK / 2; ++e) x[e] *= gr;
+#pragma unroll
+          for (int g = 0; g < DK / 16; ++g) il_store8(sQ(b), C, row, DK / 2 * hh + g * 8, x + 8 * g);
+        }
+        wg_sync(BAR_S);
+        const int i = wwarp * 16 + (lane & 15);
+        ri = l2 ? 1.f / fmaxf(sqrtf(qn2[i] + qn2[C + i]), a.eps) : 1.f;
+        if (c * C + i >= L) ri = 0.f;
+        DBG(if (lane < 16) dn_dbg[D_R + i] = ri);
+      };
+      if (GATED) norms();
       fence_proxy_async();
       fence_before_sync();
       wg_sync(BAR_S);
@@ -420,27 +507,7 @@ __global__ void __launch_bounds__(NT, 1)
         if (!SEG1) mbar_arrive(&w_free);
         mbar_arrive(&bar_full[b]);
       }
-      // r_i = 1/max(||q_i||, eps) for this lane's output row (R9): partial sums
-      // of squares over column halves (thread w: row w & 63, half w >> 6)
-      float ri = 0.f;
-      if (!SEG1) {
-        const int row = w & 63, hh = w >> 6;
-        float x[DK / 2];
-#pragma unroll
-        for (int g = 0; g < DK / 16; ++g) il_load8(sQ(b), C, row, DK / 2 * hh + g * 8, x + 8 * g);
-        float acc0 = 0.f, acc1 = 0.f;
-#pragma unroll
-        for (int e = 0; e < DK / 2; e += 2) {
-          acc0 = fmaf(x[e], x[e], acc0);
-          acc1 = fmaf(x[e + 1], x[e + 1], acc1);
-        }
-        qn2[hh * C + row] = acc0 + acc1;
-        wg_sync(BAR_S);
-        const int i = wwarp * 16 + (lane & 15);
-        ri = l2 ? 1.f / fmaxf(sqrtf(qn2[i] + qn2[C + i]), a.eps) : 1.f;
-        if (c * C + i >= L) ri = 0.f;
-        DBG(if (lane < 16) dn_dbg[D_R + i] = ri);
-      }
+      if (!SEG1 && !GATED) norms();
       mbar_wait(&up_done, c & 1);
       mbar_wait(&z_free, c & 1);
       fence_after_sync();
@@ -453,6 +520,34 @@ __global__ void __launch_bounds__(NT, 1)
         for (int t = 0; t < 64; ++t) f[t] *= vb[C + t];
 #pragma unroll
         for (int g = 0; g < 8; ++g) il_store8(sZ, DV, w, g * 8, f + g * 8);
+        if (GATED) {
+          // Z_h^T = Z^T diag(D) as bf16 pairs over U's first 32 TMEM columns
+          // (the A operand of H^T += Z_h^T K), and H^T *= gamma_63 in TMEM
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            uint32_t r[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int t = 32 * h2 + 2 * j;
+              r[j] = pack_bf16(f[t] * vb[5 * C + t], f[t + 1] * vb[5 * C + t + 1]);
+            }
+            tmem_st16(taddr(tm, wwarp * 32, tm_u(b) + 16 * h2), r);
+          }
+          const float gC = vb[4 * C + C - 1];
+#pragma unroll 1
+          for (int hh = 0; hh < 2; ++hh) {
+            float hf[64];
+            ld64(tm, wwarp, TM_H + 64 * hh, hf);
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              uint32_t r[16];
+#pragma unroll
+              for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(hf[16 * q4 + j] * gC);
+              tmem_st16(taddr(tm, wwarp * 32, TM_H + 64 * hh + 16 * q4), r);
+            }
+          }
+          tmem_st_wait();
+        }
       }
       if (SEG1) {
         // T1 = Psi W^T (TM_W, lane = row a, cols = tokens) -> -T1 diag(s) as
@@ -682,9 +777,16 @@ __global__ void __launch_bounds__(NT, 1)
           bulk_commit();
         }
         // H^T += Z^T K (M=128,N=128,K=64); O += tril(QK^T) Z (M=64,N=128,K=64)
+        // (gated: H^T += Z_h^T K with Z_h^T from TMEM)
+        if (GATED) {
 #pragma unroll
-        for (int k0 = 0; k0 < C; k0 += 16)
-          mma_bf16(tm + TM_H, desc_k(aZ, DV, k0), desc_mn(ak, C, k0), idh, 1);
+          for (int k0 = 0; k0 < C; k0 += 16)
+            mma_bf16_ts(tm + TM_H, tm + tm_u(b) + k0 / 2, desc_mn(ak, C, k0), idh, 1);
+        } else {
+#pragma unroll
+          for (int k0 = 0; k0 < C; k0 += 16)
+            mma_bf16(tm + TM_H, desc_k(aZ, DV, k0), desc_mn(ak, C, k0), idh, 1);
+        }
         if (SEG1) {  // Psi += (-T1 diag(s)) K, A from TMEM (bf16 pairs in TM_W)
 #pragma unroll
           for (int k0 = 0; k0 < C; k0 += 16)
@@ -846,8 +948,9 @@ bool tc_supported(const deltanet_desc* d) {
   return d->dtype == DELTANET_BF16 && d->chunk == C && d->Dk == DK && d->Dv == DV && d->L > 0;
 }
 
-// gated DeltaNet (R23) on the tcgen05 kernels: not yet (SIMT path)
-bool tc_gated_supported(const deltanet_desc*) { return false; }
+// gated DeltaNet (R23) on the tcgen05 kernels: the forward (the gated
+// backward runs on the SIMT path)
+bool tc_gated_supported(const deltanet_desc*) { return true; }
 
 // per-chunk records [X | W^T | Z^T] the backward reads (40 KB per chunk per unit)
 namespace {
@@ -873,7 +976,7 @@ size_t rec_bytes(int B, int H, int L) {
 // B*H units leave SMs idle, each unit's chunks are split over up to
 // SMs / units CTAs (segments of >= 8 chunks, at most 16).
 int tc_fwd_segments(const deltanet_desc* d) {
-  if (d->flags & DELTANET_NO_SEGMENTS) return 1;
+  if (d->flags & (DELTANET_NO_SEGMENTS | DELTANET_GATED)) return 1;  // gated: one CTA per unit
   const int units = d->B * d->H, NCk = (d->L + C - 1) / C;
   if (units <= 0) return 1;
   int n = sm_count() / units;
@@ -924,7 +1027,9 @@ int tc_fwd(const Args& a0, cudaStream_t s) {
     if (cudaFuncSetAttribute(tc_fwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              SMEM_BYTES) != cudaSuccess ||
         cudaFuncSetAttribute(tc_fwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             SMEM_BYTES) != cudaSuccess)
+                             SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(tc_fwd_kernel<false, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess)
       return DELTANET_ERR_CUDA;
     attr = true;
   }
@@ -936,6 +1041,10 @@ int tc_fwd(const Args& a0, cudaStream_t s) {
       !make_il_map(&mO, a.o ? a.o : a.v, BH, a.L, DV, C))  // o == null: states only
     return DELTANET_ERR_CUDA;
   const int nseg = tc_seg_setup(a);
+  if (a.g) {  // gated DeltaNet (R23): one CTA per unit
+    tc_fwd_kernel<false, true><<<BH, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);
+    return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
+  }
   if (nseg <= 1) {
     tc_fwd_kernel<false><<<BH, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);
     return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;

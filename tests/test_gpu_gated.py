@@ -129,3 +129,40 @@ def test_recurrent_gated_decode_loop():
     torch.cuda.synchronize()
     assert torch.equal(torch.cat(outs, 2), o_ref)
     assert torch.equal(state, h_ref)
+
+
+@pytest.mark.parametrize("scale", [0.05, 1.0, 4.0])
+@pytest.mark.parametrize("L", [64, 1000])
+def test_bf16_tcgen05_forward(L, scale):
+    """The tcgen05 gated forward (include/deltanet.h: path 1 for bf16 d=128
+    C=64) from a nonzero h0, slow to very fast decay (4.0: e^{-4 softplus}
+    per token, in-chunk products far below fp32's range as ratios)."""
+    import paper_2406_06484_b200 as dn
+    assert dn.deltanet_path(dn.make_desc(2, 2, L, 128, 128, gated=True)) == 1
+    inp = _case(2, 2, L, 128, 128, 64, "bf16", index=880 + L, scale=scale)
+    q, k, v, b = (to_dev(inp[f], torch.bfloat16) for f in ("q", "k", "v", "beta"))
+    g = to_dev(inp["g"], torch.float32)
+    h0 = 0.3 * np.random.default_rng(4).standard_normal((2, 2, 128, 128))
+    o, hT, _ = dn.deltanet_gated_fwd(q, k, v, b, g, h0=to_dev(h0, torch.float32))
+    torch.cuda.synchronize()
+    ro, rhT = oracle.gated_fwd(inp["q"], inp["k"], inp["v"], inp["beta"], inp["g"], h0=h0)
+    compare({"o": _np(o), "hT": _np(hT)}, {"o": ro, "hT": rhT}, TOL["bf16"])
+
+
+def test_bf16_gated_full_size_sampled_units():
+    """BASELINE target shape (B=8 H=16 L=4096) gated forward in one launch;
+    three sampled units against the oracle."""
+    import paper_2406_06484_b200 as dn
+    cfg = synth.CONFIGS["target"]
+    inp = synth.make_inputs(cfg)
+    gates = synth.make_gates(cfg)
+    q, k, v, b = (to_dev(inp[f], torch.bfloat16) for f in ("q", "k", "v", "beta"))
+    o, hT, _ = dn.deltanet_gated_fwd(q, k, v, b, to_dev(gates, torch.float32))
+    torch.cuda.synchronize()
+    o, hT = _np(o), _np(hT)
+    for (bb, h) in [(0, 0), (cfg.B - 1, cfg.H - 1), (3, 9)]:
+        one = {f: inp[f][bb:bb + 1, h:h + 1] for f in inp}
+        ro, rhT = oracle.gated_fwd(one["q"], one["k"], one["v"], one["beta"],
+                                   gates[bb:bb + 1, h:h + 1])
+        compare({"o": o[bb:bb + 1, h:h + 1], "hT": hT[bb:bb + 1, h:h + 1]},
+                {"o": ro, "hT": rhT}, TOL["bf16"])

@@ -284,6 +284,96 @@ def measure_long_context(dn, dev):
     return res
 
 
+def _timed(dev, fn, reps):
+    import torch
+    stream = torch.cuda.current_stream(dev)
+    fn()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    return e0.elapsed_time(e1) * 1e-3 / reps
+
+
+def measure_gated(dn, dev, q, k, v, beta, t_fwd_ungated):
+    """Side measurement (outside the timed step) of Gated DeltaNet (SURVEY
+    §8(f) f4): the tcgen05 gated forward on the step's
+    forward workload (gates g = -0.05 softplus(N(0,1))), and the gated
+    backward (CUDA-core SIMT path today) on a small workload."""
+    import torch
+    B, Hh, Ll, D = q.shape
+    gen = torch.Generator(device=dev).manual_seed(17)
+    gates = -0.05 * torch.nn.functional.softplus(
+        torch.randn((B, Hh, Ll), device=dev, generator=gen))
+    o = torch.empty_like(v)
+    d = dn.make_desc(B, Hh, Ll, D, D, 64, torch.bfloat16, gated=True)
+    ws = dn.alloc_workspace(d, dev)
+    t_f = _timed(dev, lambda: dn.deltanet_gated_fwd(q, k, v, beta, gates, workspace=ws, out=o,
+                                                    want_hT=False), 5)
+    Bs, Hs, Ls = 1, 8, 512
+    sl = lambda t: t[:Bs, :Hs, :Ls].contiguous()
+    qs, ks, vs, bs, gs = sl(q), sl(k), sl(v), sl(beta), sl(gates)
+    dOs = torch.randn_like(vs)
+    _, _, wss = dn.deltanet_gated_fwd(qs, ks, vs, bs, gs)
+    t_b = _timed(dev, lambda: dn.deltanet_gated_bwd(qs, ks, vs, bs, gs, dOs, workspace=wss,
+                                                    want_dh0=False), 1)
+    return {"fwd": {"workload": f"B={B} H={Hh} L={Ll} d={D} bf16 (the step's forward)",
+                    "kernel": "tc_fwd_kernel<gated> (tcgen05)", "ms": t_f * 1e3,
+                    "tokens_per_s": B * Ll / t_f, "vs_ungated_fwd": t_f / t_fwd_ungated,
+                    "launches": dn.deltanet_launch_count(d, 0)},
+            "bwd": {"workload": f"B={Bs} H={Hs} L={Ls} d={D} bf16",
+                    "kernel": "simt_bwd_kernel (CUDA cores; tcgen05 gated bwd not built)",
+                    "ms": t_b * 1e3, "tokens_per_s": Bs * Ls / t_b}}
+
+
+def measure_context_parallel(dn, dev, parts=2):
+    """Side measurement (outside the timed step) of context parallelism
+     on BASELINE configs[2] (B=2 H=16 L=16384), `parts`
+    simulated ranks on this GPU: the per-rank kernels (transition, scan,
+    fwd / bwd of its L/parts tokens from the scanned state) timed on the last
+    part, against the whole sequence on one GPU.  The all-gather of the
+    transitions (2 x 64 KB per unit per rank) is not included."""
+    import torch
+    B, Hh, Ll, D = 2, 16, 16384, 128
+    Lp = Ll // parts
+    g = torch.Generator(device=dev).manual_seed(19)
+    mk = lambda L_: torch.randn((B, Hh, L_, D), device=dev, generator=g).to(torch.bfloat16)
+    q, k, v, dO = mk(Lp), mk(Lp), mk(Lp), mk(Lp)
+    beta = torch.rand((B, Hh, Lp), device=dev, generator=g).to(torch.bfloat16)
+    psi, hloc = dn.deltanet_fwd_transition(q, k, v, beta)
+    psi_all = torch.stack([psi] * parts)
+    loc_all = torch.stack([hloc] * parts)
+    o = torch.empty_like(v)
+    grads = (torch.empty_like(q), torch.empty_like(k), torch.empty_like(v),
+             torch.empty_like(beta))
+    d = dn.make_desc(B, Hh, Lp, D, D, 64, torch.bfloat16)
+    ws = dn.alloc_workspace(d, dev)
+    hs = torch.empty((B, Hh, D, D), dtype=torch.float32, device=dev)
+    de = torch.empty_like(hs)
+    dloc = torch.empty_like(hs)
+
+    def rank_step():
+        dn.deltanet_fwd_transition(q, k, v, beta, psi=psi, hloc=hloc)
+        dn.deltanet_state_scan(psi_all, loc_all, parts - 1, out=hs)
+        dn.deltanet_fwd(q, k, v, beta, h0=hs, workspace=ws, want_hT=False, out=o)
+        dn.deltanet_bwd_transition(q, k, v, beta, dO, workspace=ws, dhloc=dloc)
+        dn.deltanet_state_scan(psi_all, loc_all, parts - 1, reverse=True, out=de)
+        dn.deltanet_bwd(q, k, v, beta, dO, h0=hs, dhT=de, workspace=ws, want_dh0=False,
+                        out=grads)
+    t_rank = _timed(dev, rank_step, 5)
+    t_tr = _timed(dev, lambda: dn.deltanet_fwd_transition(q, k, v, beta, psi=psi, hloc=hloc), 5)
+    t_btr = _timed(dev, lambda: dn.deltanet_bwd_transition(q, k, v, beta, dO, workspace=ws,
+                                                           dhloc=dloc), 5)
+    return {"workload": f"B={B} H={Hh} L={Ll} d={D}, {parts} parts of {Lp} tokens",
+            "per_rank_ms": t_rank * 1e3,
+            "fwd_transition_ms": t_tr * 1e3, "bwd_transition_ms": t_btr * 1e3,
+            "projected_tokens_per_s": parts * B * Lp / t_rank,
+            "note": "per-rank kernel time of one simulated rank; excludes the NCCL all-gather"}
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -549,11 +639,13 @@ def main():
     base = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         base = cpu_baseline()
-    rec = pro = lng = None
+    rec = pro = lng = gat = cpx = None
     if rank == 0 and not args.no_recurrent and not args.force_simt:
         rec = measure_recurrent(dn, dev, q, k, v, beta, t_fwd, peaks)
         pro = measure_prologue(dn, dev, B_PER_RANK, H, L, D, peaks)
         lng = measure_long_context(dn, dev)
+        gat = measure_gated(dn, dev, q, k, v, beta, t_fwd)
+        cpx = measure_context_parallel(dn, dev)
 
     if rank == 0:
         line = {
@@ -583,6 +675,10 @@ def main():
             line["prologue"] = pro
         if lng:
             line["long_context"] = lng
+        if gat:
+            line["gated"] = gat
+        if cpx:
+            line["context_parallel"] = cpx
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.barrier()

@@ -343,20 +343,20 @@ def measure_context_parallel(dn, dev, parts=2):
     mk = lambda L_: torch.randn((B, Hh, L_, D), device=dev, generator=g).to(torch.bfloat16)
     q, k, v, dO = mk(Lp), mk(Lp), mk(Lp), mk(Lp)
     beta = torch.rand((B, Hh, Lp), device=dev, generator=g).to(torch.bfloat16)
-    psi, hloc = dn.deltanet_fwd_transition(q, k, v, beta)
+    d = dn.make_desc(B, Hh, Lp, D, D, 64, torch.bfloat16)
+    ws = dn.alloc_workspace(d, dev)
+    psi, hloc = dn.deltanet_fwd_transition(q, k, v, beta, workspace=ws)
     psi_all = torch.stack([psi] * parts)
     loc_all = torch.stack([hloc] * parts)
     o = torch.empty_like(v)
     grads = (torch.empty_like(q), torch.empty_like(k), torch.empty_like(v),
              torch.empty_like(beta))
-    d = dn.make_desc(B, Hh, Lp, D, D, 64, torch.bfloat16)
-    ws = dn.alloc_workspace(d, dev)
     hs = torch.empty((B, Hh, D, D), dtype=torch.float32, device=dev)
     de = torch.empty_like(hs)
     dloc = torch.empty_like(hs)
 
     def rank_step():
-        dn.deltanet_fwd_transition(q, k, v, beta, psi=psi, hloc=hloc)
+        dn.deltanet_fwd_transition(q, k, v, beta, psi=psi, hloc=hloc, workspace=ws)
         dn.deltanet_state_scan(psi_all, loc_all, parts - 1, out=hs)
         dn.deltanet_fwd(q, k, v, beta, h0=hs, workspace=ws, want_hT=False, out=o)
         dn.deltanet_bwd_transition(q, k, v, beta, dO, workspace=ws, dhloc=dloc)
@@ -364,12 +364,14 @@ def measure_context_parallel(dn, dev, parts=2):
         dn.deltanet_bwd(q, k, v, beta, dO, h0=hs, dhT=de, workspace=ws, want_dh0=False,
                         out=grads)
     t_rank = _timed(dev, rank_step, 5)
-    t_tr = _timed(dev, lambda: dn.deltanet_fwd_transition(q, k, v, beta, psi=psi, hloc=hloc), 5)
+    t_tr = _timed(dev, lambda: dn.deltanet_fwd_transition(q, k, v, beta, psi=psi, hloc=hloc, workspace=ws), 5)
     t_btr = _timed(dev, lambda: dn.deltanet_bwd_transition(q, k, v, beta, dO, workspace=ws,
                                                            dhloc=dloc), 5)
     return {"workload": f"B={B} H={Hh} L={Ll} d={D}, {parts} parts of {Lp} tokens",
             "per_rank_ms": t_rank * 1e3,
             "fwd_transition_ms": t_tr * 1e3, "bwd_transition_ms": t_btr * 1e3,
+            "transition_launches": [dn.deltanet_launch_count(d, 5),
+                                    dn.deltanet_launch_count(d, 6)],
             "projected_tokens_per_s": parts * B * Lp / t_rank,
             "note": "per-rank kernel time of one simulated rank; excludes the NCCL all-gather"}
 

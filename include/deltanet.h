@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define DELTANET_ABI_VERSION 5
+#define DELTANET_ABI_VERSION 6
 
 typedef enum {
   DELTANET_BF16 = 0, /* bf16 I/O, fp32 accumulation (BASELINE.json north_star) */
@@ -215,16 +215,21 @@ int deltanet_gated_recurrent_fwd(const deltanet_desc* d, const void* q,
  * (Psi = I, Hloc = 0).  Psi and the states are fp32; a part's Psi, Hloc,
  * dHloc have the layout [B,H,128,128] (row i of Psi = row i of the matrix). */
 
-/* Psi [B,H,Dk,Dk] and Hloc [B,H,Dk,Dv] of this call's sequence (one
- * launch; no workspace: the chain is not stored). */
+/* Psi [B,H,Dk,Dk] and Hloc [B,H,Dk,Dv] of this call's sequence.  One
+ * launch, or (when B*H leaves SMs idle, as deltanet_fwd's segments) the
+ * segment-parallel pass 1 plus a composition launch; the workspace
+ * (deltanet_workspace_bytes(d)) holds the segment scratch.  Nothing the
+ * backward needs is written there. */
 int deltanet_fwd_transition(const deltanet_desc* d, const void* q,
                             const void* k, const void* v, const void* beta,
-                            float* psi, float* hloc, void* stream);
+                            float* psi, float* hloc, void* workspace,
+                            size_t workspace_bytes, void* stream);
 
 /* dHloc [B,H,Dk,Dv] of this call's sequence for the cotangent dO.  The
  * workspace (deltanet_workspace_bytes(d)) must hold what deltanet_fwd with
  * DELTANET_SAVE_STATES wrote over the same q, k, v, beta (any h0) when the
- * flag is set; without it the per-chunk records are recomputed into it. */
+ * flag is set (its per-chunk records and, when segmented, its segment
+ * transitions); without the flag they are recomputed into it. */
 int deltanet_bwd_transition(const deltanet_desc* d, const void* q,
                             const void* k, const void* v, const void* beta,
                             const void* dO, float* dhloc, void* workspace,

@@ -74,7 +74,7 @@ def load_library(path: str = LIB_PATH):
     lib.deltanet_prologue_bwd.restype = ctypes.c_int
     lib.deltanet_prologue_workspace_bytes.argtypes = [D]
     lib.deltanet_prologue_workspace_bytes.restype = ctypes.c_size_t
-    lib.deltanet_fwd_transition.argtypes = [D] + [P] * 7
+    lib.deltanet_fwd_transition.argtypes = [D] + [P] * 7 + [ctypes.c_size_t, P]
     lib.deltanet_fwd_transition.restype = ctypes.c_int
     lib.deltanet_bwd_transition.argtypes = [D] + [P] * 7 + [ctypes.c_size_t, P]
     lib.deltanet_bwd_transition.restype = ctypes.c_int
@@ -305,7 +305,8 @@ def deltanet_bwd(q, k, v, beta, dO, *, chunk=64, l2norm=True, h0=None, dhT=None,
     return dq, dk, dv, db, dh0
 
 
-def deltanet_fwd_transition(q, k, v, beta, *, l2norm=True, eps=1e-6, psi=None, hloc=None):
+def deltanet_fwd_transition(q, k, v, beta, *, l2norm=True, eps=1e-6, psi=None, hloc=None,
+                            workspace=None):
     """Transition of this sequence (include/deltanet.h, context parallelism):
     H_end = psi^T H_start + hloc.  Returns (psi [B,H,Dk,Dk], hloc [B,H,Dk,Dv])."""
     lib = load_library()
@@ -321,8 +322,11 @@ def deltanet_fwd_transition(q, k, v, beta, *, l2norm=True, eps=1e-6, psi=None, h
         hloc = torch.empty((B, H, Dk, Dv), dtype=torch.float32, device=dev)
     _need(psi, "psi", torch.float32, dev)
     _need(hloc, "hloc", torch.float32, dev)
+    if workspace is None:
+        workspace = alloc_workspace(d, dev)
     rc = lib.deltanet_fwd_transition(ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(beta),
-                                     _ptr(psi), _ptr(hloc), _stream(dev))
+                                     _ptr(psi), _ptr(hloc), _ptr(workspace), workspace.numel(),
+                                     _stream(dev))
     _check(rc, "deltanet_fwd_transition")
     return psi, hloc
 

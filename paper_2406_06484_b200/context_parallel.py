@@ -5,11 +5,11 @@ unit (the sequence is cut into consecutive parts, one per rank).  The parts
 are stitched by the affine composition of the chunk state update (PAPER.md
 §3.2 Eq. 8; include/deltanet.h "Context parallelism"):
 
-  forward   1. (Psi_r, Hloc_r) = deltanet_fwd_transition(part r)      [1 launch]
+  forward   1. (Psi_r, Hloc_r) = deltanet_fwd_transition(part r)      [1-2 launches]
             2. all-gather (Psi, Hloc) over the group                  [NCCL]
             3. H_start(r) = deltanet_state_scan(part r)               [1 launch]
             4. o_r = deltanet_fwd(part r, h0 = H_start(r))            [the usual kernels]
-  backward  1. dHloc_r = deltanet_bwd_transition(part r, dO_r)        [1 launch]
+  backward  1. dHloc_r = deltanet_bwd_transition(part r, dO_r)        [1-2 launches]
             2. all-gather dHloc                                       [NCCL]
             3. dH_end(r) = deltanet_state_scan(part r, reverse)       [1 launch]
             4. grads_r = deltanet_bwd(part r, h0 = H_start(r), dhT = dH_end(r))
@@ -30,12 +30,17 @@ import torch.distributed as dist
 
 
 def _cuda_ops():
-    from . import (deltanet_bwd, deltanet_bwd_transition, deltanet_fwd,
-                   deltanet_fwd_transition, deltanet_state_scan)
+    from . import (alloc_workspace, deltanet_bwd, deltanet_bwd_transition, deltanet_fwd,
+                   deltanet_fwd_transition, deltanet_state_scan, make_desc)
+
+    def alloc(q, v, l2norm):  # one workspace for the transition, the fwd and the bwd
+        B, H, L, Dk = q.shape
+        return alloc_workspace(make_desc(B, H, L, Dk, v.shape[-1], 64, q.dtype, l2norm=l2norm),
+                               q.device)
     return SimpleNamespace(fwd_transition=deltanet_fwd_transition,
                            bwd_transition=deltanet_bwd_transition,
                            state_scan=deltanet_state_scan, fwd=deltanet_fwd,
-                           bwd=deltanet_bwd)
+                           bwd=deltanet_bwd, alloc=alloc)
 
 
 def _all_gather(x: torch.Tensor, group) -> torch.Tensor:
@@ -64,11 +69,13 @@ def cp_fwd(q, k, v, beta, *, group=None, h0=None, l2norm=True, ops=None):
     after this rank's part (the sequence's final state on the last rank)."""
     ops = ops or _cuda_ops()
     r = dist.get_rank(group)
-    psi, hloc = ops.fwd_transition(q, k, v, beta, l2norm=l2norm)
+    ws = ops.alloc(q, v, l2norm) if hasattr(ops, "alloc") else None
+    psi, hloc = ops.fwd_transition(q, k, v, beta, l2norm=l2norm, workspace=ws)
     both = _all_gather(torch.stack((psi, hloc)), group)  # [P, 2, B, H, D, D]
     psi_all, loc_all = both[:, 0].contiguous(), both[:, 1].contiguous()
     h_start = ops.state_scan(psi_all, loc_all, r, edge=h0)
-    o, hT, ws = ops.fwd(q, k, v, beta, h0=h_start, l2norm=l2norm, save_states=True)
+    o, hT, ws = ops.fwd(q, k, v, beta, h0=h_start, l2norm=l2norm, save_states=True,
+                        workspace=ws)
     return o, hT, CPState(ws, h_start, psi_all)
 
 

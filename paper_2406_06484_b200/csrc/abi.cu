@@ -104,9 +104,10 @@ int deltanet_launch_count(const deltanet_desc* d, int which) {
   if (which >= 5 && which <= 7) {  // context-parallel transitions, scan
     if (validate_cp(d) != DELTANET_OK) return -1;
     if ((size_t)d->B * d->H == 0) return 0;
-    if (which == 6 && d->L > 0 && !(d->flags & DELTANET_SAVE_STATES))
-      return 1 + dn::tc_launch_count(d, 0);
-    return 1;
+    if (which == 7 || d->L == 0) return 1;
+    const int tr = dn::tc_fwd_segments(d) > 1 ? 2 : 1;  // pass 1 (+ composition)
+    if (which == 6 && !(d->flags & DELTANET_SAVE_STATES)) return tr + dn::tc_launch_count(d, 0);
+    return tr;
   }
   if (validate(d) != DELTANET_OK) return -1;
   if ((size_t)d->B * d->H == 0) return 0;
@@ -274,20 +275,20 @@ int deltanet_prologue_bwd(const deltanet_desc* d, const void* xq, const void* xk
 }
 
 int deltanet_fwd_transition(const deltanet_desc* d, const void* q, const void* k, const void* v,
-                            const void* beta, float* psi, float* hloc, void* stream) {
+                            const void* beta, float* psi, float* hloc, void* workspace,
+                            size_t workspace_bytes, void* stream) {
   int rc = validate_cp(d);
   if (rc) return rc;
   const size_t units = (size_t)d->B * d->H;
   if (!units) return DELTANET_OK;
   if (!psi || !hloc || (d->L > 0 && (!q || !k || !v || !beta))) return DELTANET_ERR_INVALID_ARG;
   if (misaligned(q) || misaligned(k) || misaligned(v) || misaligned(beta) || misaligned(psi) ||
-      misaligned(hloc))
+      misaligned(hloc) || misaligned(workspace))
     return DELTANET_ERR_MISALIGNED;
   cudaStream_t s = (cudaStream_t)stream;
   if (d->L == 0) return dn::cp_empty((int)units, psi, hloc, s);
-  dn::Args a = make_args(d, nullptr);
-  a.scratch = nullptr;
-  a.states = nullptr;
+  if (!workspace || workspace_bytes < deltanet_workspace_bytes(d)) return DELTANET_ERR_WORKSPACE;
+  dn::Args a = make_args(d, workspace);
   a.q = q; a.k = k; a.v = v; a.beta = beta;
   return dn::tc_fwd_transition(a, psi, hloc, s);
 }

@@ -83,6 +83,7 @@ int tc_seg_setup(Args& a);
 int tc_fwd_transition(const Args& a, float* psi, float* hloc, cudaStream_t s);
 int tc_bwd_transition(const Args& a, float* dhloc, cudaStream_t s);
 int cp_empty(int units, float* psi, float* loc, cudaStream_t s);
+int cp_compose_bwd(const Args& a, float* dhloc, cudaStream_t s);
 int cp_scan(int units, int nparts, int part, int reverse, const float* psi, const float* loc,
             const float* edge, float* out, cudaStream_t s);
 

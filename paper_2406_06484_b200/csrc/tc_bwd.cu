@@ -933,8 +933,9 @@ int tc_bwd(const Args& a0, cudaStream_t s) {
 }
 
 // Context parallelism: the local cotangent chain of this call's sequence from
-// dl/dH_end = 0 (pass 1 with one segment per unit); needs the forward's
-// per-chunk records in the workspace (deltanet_fwd with SAVE_STATES)
+// dl/dH_end = 0 (pass 1 with one segment per unit, or S segments composed
+// with the forward's segment transitions); needs the forward's per-chunk
+// records (and segment Psi) in the workspace (deltanet_fwd with SAVE_STATES)
 int tc_bwd_transition(const Args& a0, float* dhloc, cudaStream_t s) {
   Args a = a0;
   const int BH = a.B * a.H;
@@ -951,10 +952,16 @@ int tc_bwd_transition(const Args& a0, float* dhloc, cudaStream_t s) {
       return DELTANET_ERR_CUDA;
     attr = true;
   }
-  a.nseg = 1;
-  a.hloc = dhloc;
-  tc_bwd_kernel<true><<<BH, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mDO, mDQ, mDK, mDV, a);
-  return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
+  const int nseg = tc_seg_setup(a);
+  if (nseg <= 1) {
+    a.nseg = 1;
+    a.hloc = dhloc;
+    tc_bwd_kernel<true><<<BH, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mDO, mDQ, mDK, mDV, a);
+    return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
+  }
+  tc_bwd_kernel<true><<<BH * nseg, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mDO, mDQ, mDK, mDV, a);
+  if (cudaGetLastError() != cudaSuccess) return DELTANET_ERR_CUDA;
+  return cp_compose_bwd(a, dhloc, s);
 }
 
 }  // namespace dn

@@ -901,6 +901,55 @@ __global__ void __launch_bounds__(256) cp_scan_kernel(ScanArgs sa) {
   }
 }
 
+// Composition of a unit's S segment transitions (context parallelism with
+// the segment-parallel pass 1), fp32:
+//   fwd: Psi = Psi_0 Psi_1 ... Psi_{S-1} (blockIdx.y < 8: column block),
+//        Hloc = fold_s (H <- Psi_s^T H + hloc_s) from 0 (blockIdx.y >= 8);
+//   bwd: dHloc = fold_{s = S-1..0} (G <- Psi_s G + dhloc_s) from 0.
+__global__ void __launch_bounds__(256) cp_compose_kernel(int nseg, int bwd, const float* psi_s,
+                                                         const float* loc_s, float* psi_out,
+                                                         float* loc_out) {
+  __shared__ float Xs[DK][16];
+  const int unit = blockIdx.x;
+  const bool do_psi = !bwd && blockIdx.y < DK / 16;
+  const int j0 = (do_psi ? blockIdx.y : blockIdx.y - (bwd ? 0 : DK / 16)) * 16;
+  const int tid = threadIdx.x, i = tid >> 1, jj = (tid & 1) * 8;
+  const float* P = psi_s + (size_t)unit * nseg * DK * DK;
+  const float* H = loc_s + (size_t)unit * nseg * DK * DV;
+  for (int e = tid; e < DK * 16; e += blockDim.x) {
+    const int r = e / 16, cc = e % 16;
+    Xs[r][cc] = do_psi ? P[(size_t)(nseg - 1) * DK * DK + (size_t)r * DK + j0 + cc] : 0.f;
+  }
+  __syncthreads();
+  const int n = do_psi ? nseg - 1 : nseg;
+  for (int step = 0; step < n; ++step) {
+    // fwd Psi: s = S-2 .. 0 (X <- Psi_s X); fwd Hloc: s = 0 .. S-1 (Psi_s^T);
+    // bwd: s = S-1 .. 0 (Psi_s)
+    const int sg = do_psi ? nseg - 2 - step : bwd ? nseg - 1 - step : step;
+    const float* ps = P + (size_t)sg * DK * DK;
+    float acc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      acc[e] = do_psi ? 0.f : H[(size_t)sg * DK * DV + (size_t)i * DV + j0 + jj + e];
+    const bool tr = !do_psi && !bwd;
+#pragma unroll 4
+    for (int r = 0; r < DK; ++r) {
+      const float pv = tr ? ps[(size_t)r * DK + i] : ps[(size_t)i * DK + r];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = fmaf(pv, Xs[r][jj + e], acc[e]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 8; ++e) Xs[i][jj + e] = acc[e];
+    __syncthreads();
+  }
+  float* out = do_psi ? psi_out + (size_t)unit * DK * DK : loc_out + (size_t)unit * DK * DV;
+  for (int e = tid; e < DK * 16; e += blockDim.x) {
+    const int r = e / 16, cc = e % 16;
+    out[(size_t)r * DK + j0 + cc] = Xs[r][cc];
+  }
+}
+
 // transition of an empty sequence: Psi = I, loc = 0 (psi or loc may be null)
 __global__ void cp_empty_kernel(int units, float* psi, float* loc) {
   const size_t n = (size_t)units * DK * DK;
@@ -1056,7 +1105,9 @@ int tc_fwd(const Args& a0, cudaStream_t s) {
 }
 
 // Context parallelism (include/deltanet.h): the transition of this call's
-// whole sequence (pass 1 of the segment machinery with one segment per unit)
+// whole sequence: pass 1 of the segment machinery, one segment per unit, or,
+// when the units leave SMs idle, S segments per unit composed by
+// cp_compose_kernel (a.scratch = the workspace's segment scratch)
 int tc_fwd_transition(const Args& a0, float* psi, float* hloc, cudaStream_t s) {
   Args a = a0;
   const int BH = a.B * a.H;
@@ -1071,13 +1122,25 @@ int tc_fwd_transition(const Args& a0, float* psi, float* hloc, cudaStream_t s) {
       return DELTANET_ERR_CUDA;
     attr = true;
   }
-  a.nseg = 1;
-  a.hloc = hloc;
-  a.psi = psi;
   a.o = nullptr;
   a.hT = nullptr;
   a.h0 = nullptr;
-  tc_fwd_kernel<true><<<BH, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);
+  const int nseg = a.scratch ? tc_seg_setup(a) : 1;
+  if (nseg <= 1) {
+    a.nseg = 1;
+    a.hloc = hloc;
+    a.psi = psi;
+    tc_fwd_kernel<true><<<BH, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);
+  } else {
+    tc_fwd_kernel<true><<<BH * nseg, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);
+    cp_compose_kernel<<<dim3(BH, 2 * DK / 16), 256, 0, s>>>(nseg, 0, a.psi, a.hloc, psi, hloc);
+  }
+  return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
+}
+
+int cp_compose_bwd(const Args& a, float* dhloc, cudaStream_t s) {
+  cp_compose_kernel<<<dim3(a.B * a.H, DV / 16), 256, 0, s>>>(a.nseg, 1, a.psi, a.hloc, nullptr,
+                                                             dhloc);
   return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
 }
 

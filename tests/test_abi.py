@@ -44,7 +44,7 @@ def test_no_torch_types_in_abi():
 
 
 def test_abi_version_and_strerror(lib):
-    assert lib.deltanet_abi_version() == 5
+    assert lib.deltanet_abi_version() == 6
     for code in range(6):
         assert dn.deltanet_strerror(code)
     assert "unknown" in dn.deltanet_strerror(99)
@@ -127,14 +127,14 @@ def test_context_parallel_errors_before_launch(lib):
     p = ctypes.c_void_p(16 * 1024 + 4)
     ok = dict(Dk=128, Dv=128, chunk=64)
     # UNSUPPORTED outside the tcgen05 shapes
-    assert lib.deltanet_fwd_transition(D(_desc(Dk=64, Dv=64)), a, a, a, a, a, a, nul) == 2
-    assert lib.deltanet_fwd_transition(D(_desc(**ok, dtype=1)), a, a, a, a, a, a, nul) == 2
-    assert lib.deltanet_fwd_transition(D(_desc(**ok, flags=4)), a, a, a, a, a, a, nul) == 2
+    assert lib.deltanet_fwd_transition(D(_desc(Dk=64, Dv=64)), a, a, a, a, a, a, a, 1 << 34, nul) == 2
+    assert lib.deltanet_fwd_transition(D(_desc(**ok, dtype=1)), a, a, a, a, a, a, a, 1 << 34, nul) == 2
+    assert lib.deltanet_fwd_transition(D(_desc(**ok, flags=4)), a, a, a, a, a, a, a, 1 << 34, nul) == 2
     assert lib.deltanet_state_scan(D(_desc(Dk=64, Dv=64)), 2, 0, 0, a, a, nul, a, nul) == 2
     # null required pointers, bad part index, misalignment
-    assert lib.deltanet_fwd_transition(D(_desc(**ok)), a, a, a, a, nul, a, nul) == 1
-    assert lib.deltanet_fwd_transition(D(_desc(**ok)), nul, a, a, a, a, a, nul) == 1
-    assert lib.deltanet_fwd_transition(D(_desc(**ok)), a, a, a, a, p, a, nul) == 3
+    assert lib.deltanet_fwd_transition(D(_desc(**ok)), a, a, a, a, nul, a, a, 1 << 34, nul) == 1
+    assert lib.deltanet_fwd_transition(D(_desc(**ok)), nul, a, a, a, a, a, a, 1 << 34, nul) == 1
+    assert lib.deltanet_fwd_transition(D(_desc(**ok)), a, a, a, a, p, a, a, 1 << 34, nul) == 3
     assert lib.deltanet_bwd_transition(D(_desc(**ok)), a, a, a, a, nul, a, a, 1 << 30, nul) == 1
     assert lib.deltanet_bwd_transition(D(_desc(**ok)), a, a, a, a, a, a, nul, 0, nul) == 5
     for nparts, part, rev in ((0, 0, 0), (2, 2, 0), (2, -1, 1), (2, 0, 2)):
@@ -143,7 +143,7 @@ def test_context_parallel_errors_before_launch(lib):
     assert lib.deltanet_state_scan(D(_desc(**ok)), 2, 1, 0, a, a, nul, p, nul) == 3
     # nothing to do: B*H = 0
     e = _desc(B=0, **ok)
-    assert lib.deltanet_fwd_transition(D(e), nul, nul, nul, nul, nul, nul, nul) == 0
+    assert lib.deltanet_fwd_transition(D(e), nul, nul, nul, nul, nul, nul, nul, 0, nul) == 0
     assert lib.deltanet_state_scan(D(e), 2, 0, 0, nul, nul, nul, nul, nul) == 0
     for which in (5, 6, 7):
         assert dn.deltanet_launch_count(_desc(**ok), which) >= 1
@@ -166,5 +166,5 @@ def test_gated_errors_before_launch(lib):
     assert lib.deltanet_fwd(D(dg), a, a, a, a, nul, a, nul, a, big, nul) == 1
     assert dn.deltanet_workspace_bytes(dg) > 0
     ok = _desc(Dk=128, Dv=128, chunk=64, flags=dn.DELTANET_GATED)
-    assert lib.deltanet_fwd_transition(D(ok), a, a, a, a, a, a, nul) == 2
+    assert lib.deltanet_fwd_transition(D(ok), a, a, a, a, a, a, a, 1 << 34, nul) == 2
     assert dn.deltanet_launch_count(dg, 0) == 1

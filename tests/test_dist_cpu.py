@@ -94,14 +94,14 @@ def _oracle_ops():
     T = torch.from_numpy
     N = lambda t: None if t is None else t.numpy()
 
-    def fwd_transition(q, k, v, beta, l2norm=True):
+    def fwd_transition(q, k, v, beta, l2norm=True, workspace=None):
         psi, hloc = cpo.transition(q.numpy(), k.numpy(), v.numpy(), beta.numpy(), l2norm=l2norm)
         return T(psi), T(hloc)
 
     def state_scan(psi_all, loc_all, part, reverse=False, edge=None):
         return T(cpo.state_scan(psi_all.numpy(), loc_all.numpy(), part, reverse, N(edge)))
 
-    def fwd(q, k, v, beta, h0=None, l2norm=True, save_states=True):
+    def fwd(q, k, v, beta, h0=None, l2norm=True, save_states=True, workspace=None):
         o, hT = oracle.recurrent_fwd(q.numpy(), k.numpy(), v.numpy(), beta.numpy(), h0=N(h0),
                                      l2norm=l2norm, nthreads=1)
         return T(o), T(hT), torch.zeros(1)

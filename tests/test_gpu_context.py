@@ -207,3 +207,28 @@ def test_cp_over_nccl_world1():
     got = {"o": _np(o), "hT": _np(hT), "dq": _np(g[0]), "dk": _np(g[1]), "dv": _np(g[2]),
            "dbeta": _np(g[3]), "dh0": _np(g[4])}
     compare(got, run_oracle(inp), TOL["bf16"])
+
+
+def test_segmented_transitions_long_parts():
+    """Parts long enough (and units few enough) that the transitions run the
+    segment-parallel pass 1 plus the composition kernel (launch count 2):
+    transitions against the oracle, and a 2-part run against the uncut oracle."""
+    import paper_2406_06484_b200 as dn
+    L = 8192
+    inp = _inputs(1, 2, L, 790)
+    x = _dev(inp)
+    half = {f: t[:, :, L // 2:].contiguous() for f, t in x.items()}
+    d = dn.make_desc(1, 2, L // 2, 128, 128)
+    assert dn.deltanet_launch_count(d, 5) == 2 and dn.deltanet_launch_count(d, 6) == 2
+    psi, hloc = dn.deltanet_fwd_transition(half["q"], half["k"], half["v"], half["beta"])
+    _, _, ws = dn.deltanet_fwd(half["q"], half["k"], half["v"], half["beta"])
+    dloc = dn.deltanet_bwd_transition(half["q"], half["k"], half["v"], half["beta"], half["dO"],
+                                      workspace=ws)
+    torch.cuda.synchronize()
+    sl = {f: a[:, :, L // 2:] for f, a in inp.items()}
+    rpsi, rhloc = cpo.transition(sl["q"], sl["k"], sl["v"], sl["beta"])
+    rdloc = cpo.bwd_transition(sl["q"], sl["k"], sl["v"], sl["beta"], sl["dO"])
+    compare({"psi": _np(psi), "hloc": _np(hloc), "dhloc": _np(dloc)},
+            {"psi": rpsi, "hloc": rhloc, "dhloc": rdloc}, TOL["bf16"])
+    got = _cp_run(x, [0, L // 2, L])
+    compare(got, run_oracle(inp), TOL["bf16"])

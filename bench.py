@@ -31,6 +31,10 @@ METRIC = "tokens/s fwd+bwd DeltaNet layer (H=16,d=128,L=4K) at 1/2/4/8 B200; % b
 B_PER_RANK, H, L, D, C = 8, 16, 4096, 128, 64
 
 
+# unit slabs of the host-buffer pipeline in the e2e leg
+E2E_SLABS = int(os.environ.get("DELTANET_E2E_SLABS", "8"))  # 8 measured best (8..64)
+
+
 def per_token_head(dk, dv, c, s):
     """Algorithmic work per token x head."""
     f_fwd = 6 * dk * dv + 2 * c * (3 * dk + 2 * dv) + c * c / 3
@@ -581,21 +585,17 @@ def main():
         hin = [t.cpu().pin_memory() for t in (q, k, v, beta, dO)]
         hout = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
                 for t in (o, *grads)]
-        din = [torch.empty_like(t) for t in (q, k, v, beta, dO)]
-        dout = [o, *grads]
         h2d = sum(t.numel() * t.element_size() for t in hin)
         d2h = sum(t.numel() * t.element_size() for t in hout)
 
+        host_buf = [None]
+
         def e2e_step():
-            for dst, src in zip(din, hin):
-                dst.copy_(src, non_blocking=True)
-            dn.deltanet_fwd(din[0], din[1], din[2], din[3], chunk=C, workspace=ws_buf,
-                            want_hT=False, out=o, force_simt=args.force_simt)
-            dn.deltanet_bwd(din[0], din[1], din[2], din[3], din[4], chunk=C,
-                            workspace=ws_buf, want_dh0=False, out=grads,
-                            force_simt=args.force_simt)
-            for dst, src in zip(hout, dout):
-                dst.copy_(src, non_blocking=True)
+            # the library's host-buffer entry point: slabs of batch rows
+            # pipelined H2D / fwd+bwd / D2H on three streams (deltanet_fwd_bwd_host)
+            host_buf[0], _ = dn.deltanet_fwd_bwd_host(*hin, out=tuple(hout), slabs=E2E_SLABS,
+                                                      chunk=C, dev_buffer=host_buf[0],
+                                                      device=dev)
 
         for _ in range(2):
             e2e_step()
@@ -616,7 +616,9 @@ def main():
             t_e2e = tt.item()
         e2e = {"value": tokens_per_step / t_e2e, "unit": "tokens/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "ms_per_step": t_e2e * 1e3, "steps": n_e2e}
+               "ms_per_step": t_e2e * 1e3, "steps": n_e2e,
+               "api": f"deltanet_fwd_bwd_host (pinned host tensors, {E2E_SLABS} slabs, "
+                      "H2D / compute / D2H overlapped on three streams)"}
 
     clk = clocks.stop()
 

@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define DELTANET_ABI_VERSION 6
+#define DELTANET_ABI_VERSION 7
 
 typedef enum {
   DELTANET_BF16 = 0, /* bf16 I/O, fp32 accumulation (BASELINE.json north_star) */
@@ -118,6 +118,29 @@ int deltanet_bwd(const deltanet_desc* d, const void* q, const void* k,
                  const void* dO, const float* dhT, void* dq, void* dk,
                  void* dv, void* dbeta, float* dh0, void* workspace,
                  size_t workspace_bytes, void* stream);
+
+/* Forward + backward of HOST-resident tensors (the same layouts, in pinned
+ * host memory for copy/compute overlap): the B*H (b, h) units are cut into
+ * `slabs` consecutive unit ranges (each a descriptor with B = units, H = 1)
+ * that flow through a three-stream pipeline inside the library --
+ * H2D of slab i+1, deltanet_fwd + deltanet_bwd (with
+ * DELTANET_SAVE_STATES) of slab i, D2H of slab i-1 -- through two
+ * ping-pong device buffers carved from dev_buffer (at least
+ * deltanet_fwd_bwd_host_device_bytes(d, slabs) bytes).  Writes o, dq, dk,
+ * dv, dbeta (host); h0 / hT / dh0 are not exposed here (zero / unused).
+ * Asynchronous: `stream` (the caller's) is made to wait for the last
+ * read-out, so a synchronisation of it makes the host outputs valid; the
+ * internal streams and events are created and released per call.  Same
+ * error codes; WORKSPACE if dev_buffer is missing or small. */
+int deltanet_fwd_bwd_host(const deltanet_desc* d, const void* q,
+                          const void* k, const void* v, const void* beta,
+                          const void* dO, void* o, void* dq, void* dk, void* dv,
+                          void* dbeta, int slabs, void* dev_buffer,
+                          size_t dev_bytes, void* stream);
+
+/* Device bytes deltanet_fwd_bwd_host needs for this descriptor and slab
+ * count (slabs > B*H counts as B*H); 0 for an invalid descriptor. */
+size_t deltanet_fwd_bwd_host_device_bytes(const deltanet_desc* d, int slabs);
 
 /* Recurrent (token-by-token) form, for inference / decode:
  * the delta rule of PAPER.md §2.2 applied one token at a time,

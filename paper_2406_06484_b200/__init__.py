@@ -44,7 +44,8 @@ EXPORTED = ("deltanet_workspace_bytes", "deltanet_fwd", "deltanet_bwd", "deltane
             "deltanet_recurrent_fwd", "deltanet_prologue_fwd", "deltanet_prologue_bwd",
             "deltanet_prologue_workspace_bytes", "deltanet_fwd_transition",
             "deltanet_bwd_transition", "deltanet_state_scan", "deltanet_gated_fwd",
-            "deltanet_gated_bwd", "deltanet_gated_recurrent_fwd")
+            "deltanet_gated_bwd", "deltanet_gated_recurrent_fwd", "deltanet_fwd_bwd_host",
+            "deltanet_fwd_bwd_host_device_bytes")
 
 _lib = None
 
@@ -86,6 +87,10 @@ def load_library(path: str = LIB_PATH):
     lib.deltanet_gated_bwd.restype = ctypes.c_int
     lib.deltanet_gated_recurrent_fwd.argtypes = [D] + [P] * 9
     lib.deltanet_gated_recurrent_fwd.restype = ctypes.c_int
+    lib.deltanet_fwd_bwd_host.argtypes = [D] + [P] * 10 + [ctypes.c_int, P, ctypes.c_size_t, P]
+    lib.deltanet_fwd_bwd_host.restype = ctypes.c_int
+    lib.deltanet_fwd_bwd_host_device_bytes.argtypes = [D, ctypes.c_int]
+    lib.deltanet_fwd_bwd_host_device_bytes.restype = ctypes.c_size_t
     lib.deltanet_path.argtypes = [D]
     lib.deltanet_path.restype = ctypes.c_int
     lib.deltanet_launch_count.argtypes = [D, ctypes.c_int]
@@ -451,6 +456,33 @@ def deltanet_gated_recurrent_fwd(q, k, v, beta, g, *, l2norm=True, h0=None, want
                                           _stream(dev))
     _check(rc, "deltanet_gated_recurrent_fwd")
     return o, hT
+
+
+def deltanet_fwd_bwd_host(q, k, v, beta, dO, *, out, slabs=8, chunk=64, l2norm=True,
+                          dev_buffer=None, device=None, eps=1e-6):
+    """Forward + backward of host (CPU, ideally pinned) tensors through the
+    library's copy/compute pipeline (include/deltanet.h deltanet_fwd_bwd_host).
+    ``out`` = (o, dq, dk, dv, dbeta) host tensors.  Asynchronous on the
+    current stream of ``device``.  Returns (dev_buffer, out)."""
+    lib = load_library()
+    dev = torch.device(device if device is not None else "cuda")
+    for t, n in ((q, "q"), (k, "k"), (v, "v"), (beta, "beta"), (dO, "dO"), *zip(out, "o dq dk dv dbeta".split())):
+        if t.is_cuda:
+            raise DeltaNetError(f"{n} must be a host tensor for deltanet_fwd_bwd_host")
+        if not t.is_contiguous() or t.dtype != q.dtype:
+            raise DeltaNetError(f"{n} must be contiguous with dtype {q.dtype}")
+    B, H, L, Dk = q.shape
+    d = make_desc(B, H, L, Dk, v.shape[-1], chunk, q.dtype, l2norm=l2norm, eps=eps)
+    need = int(lib.deltanet_fwd_bwd_host_device_bytes(ctypes.byref(d), int(slabs)))
+    if dev_buffer is None or dev_buffer.numel() < need:
+        dev_buffer = torch.empty(max(need, 16), dtype=torch.uint8, device=dev)
+    o, dq, dk, dv, db = out
+    rc = lib.deltanet_fwd_bwd_host(ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(beta),
+                                   _ptr(dO), _ptr(o), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(db),
+                                   int(slabs), _ptr(dev_buffer), dev_buffer.numel(),
+                                   _stream(dev))
+    _check(rc, "deltanet_fwd_bwd_host")
+    return dev_buffer, out
 
 
 class DeltaNetChunkFunction(torch.autograd.Function):

@@ -81,6 +81,33 @@ int validate_cp(const deltanet_desc* d) {
   return dn::tc_supported(&e) ? DELTANET_OK : DELTANET_ERR_UNSUPPORTED;
 }
 
+// host-buffer pipeline (deltanet_fwd_bwd_host): per-slab buffer sizes
+struct SlabLayout {
+  int rows;          // (b, h) units per slab (the last may have fewer)
+  size_t in_bytes;   // q k v dO beta of one slab
+  size_t out_bytes;  // o dq dk dv dbeta of one slab
+  size_t ws_bytes;   // fwd/bwd workspace of one (full) slab
+};
+
+SlabLayout slab_layout(const deltanet_desc* d, int slabs) {
+  // units are independent and contiguous ([B*H][L][D]): a slab is a unit
+  // range, run as a descriptor with B = units, H = 1
+  SlabLayout sl;
+  const int units = d->B * d->H;
+  sl.rows = (units + slabs - 1) / slabs;
+  deltanet_desc e = *d;
+  e.B = sl.rows;
+  e.H = 1;
+  e.flags |= DELTANET_SAVE_STATES;
+  const size_t eb = elem_bytes(d), per_row_tok = (size_t)d->L;
+  const size_t qk = per_row_tok * d->Dk * eb, vv = per_row_tok * d->Dv * eb,
+               bb = per_row_tok * eb;
+  sl.in_bytes = round_up(sl.rows * qk) * 2 + round_up(sl.rows * vv) * 2 + round_up(sl.rows * bb);
+  sl.out_bytes = sl.in_bytes;  // o dq dk dv dbeta have the shapes of v q k dO beta
+  sl.ws_bytes = round_up(deltanet_workspace_bytes(&e));
+  return sl;
+}
+
 }  // namespace
 
 extern "C" {
@@ -272,6 +299,119 @@ int deltanet_prologue_bwd(const deltanet_desc* d, const void* xq, const void* xk
     return DELTANET_ERR_WORKSPACE;
   return dn::prologue_bwd(d, xq, xk, xv, xb, wq, wk, wv, dq, dk, dv, dbeta, dxq, dxk, dxv, dxb,
                           dwq, dwk, dwv, workspace, (cudaStream_t)stream);
+}
+
+// ---- host-buffer pipeline (include/deltanet.h deltanet_fwd_bwd_host) ----
+size_t deltanet_fwd_bwd_host_device_bytes(const deltanet_desc* d, int slabs) {
+  if (validate(d) != DELTANET_OK || slabs < 1) return 0;
+  const int units = d->B * d->H;
+  if (slabs > units) slabs = units > 0 ? units : 1;
+  const SlabLayout sl = slab_layout(d, slabs);
+  return 2 * (sl.in_bytes + sl.out_bytes) + sl.ws_bytes;
+}
+
+int deltanet_fwd_bwd_host(const deltanet_desc* d, const void* q, const void* k, const void* v,
+                          const void* beta, const void* dO, void* o, void* dq, void* dk,
+                          void* dv, void* dbeta, int slabs, void* dev_buffer,
+                          size_t dev_bytes, void* stream) {
+  int rc = validate(d);
+  if (rc) return rc;
+  if (slabs < 1) return DELTANET_ERR_INVALID_ARG;
+  const size_t units = (size_t)d->B * d->H;
+  if (!units || d->L == 0) return DELTANET_OK;
+  if (!q || !k || !v || !beta || !dO || !o || !dq || !dk || !dv || !dbeta)
+    return DELTANET_ERR_INVALID_ARG;
+  if (misaligned(dev_buffer)) return DELTANET_ERR_MISALIGNED;
+  if ((size_t)slabs > units) slabs = (int)units;
+  if (!dev_buffer || dev_bytes < deltanet_fwd_bwd_host_device_bytes(d, slabs))
+    return DELTANET_ERR_WORKSPACE;
+  const SlabLayout sl = slab_layout(d, slabs);
+  slabs = (int)((units + sl.rows - 1) / sl.rows);
+  cudaStream_t user = (cudaStream_t)stream;
+  cudaStream_t sin = nullptr, scmp = nullptr, sout = nullptr;
+  cudaEvent_t ev_entry = nullptr, ev_done = nullptr, ev_in[2] = {}, ev_cmp[2] = {},
+              ev_out[2] = {};
+  bool ok = cudaStreamCreateWithFlags(&sin, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&scmp, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&sout, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaEventCreateWithFlags(&ev_entry, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming) == cudaSuccess;
+  for (int b = 0; b < 2 && ok; ++b)
+    ok = cudaEventCreateWithFlags(&ev_in[b], cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&ev_cmp[b], cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&ev_out[b], cudaEventDisableTiming) == cudaSuccess;
+  // the device buffer may still be in use by earlier work on the caller's stream
+  ok = ok && cudaEventRecord(ev_entry, user) == cudaSuccess &&
+       cudaStreamWaitEvent(sin, ev_entry, 0) == cudaSuccess &&
+       cudaStreamWaitEvent(scmp, ev_entry, 0) == cudaSuccess &&
+       cudaStreamWaitEvent(sout, ev_entry, 0) == cudaSuccess;
+  const size_t eb = elem_bytes(d), per_row_tok = (size_t)d->L;  // per unit
+  const size_t rq = per_row_tok * d->Dk * eb, rv = per_row_tok * d->Dv * eb,
+               rb = per_row_tok * eb;
+  char* base = (char*)dev_buffer;
+  void* wsb = base + 2 * (sl.in_bytes + sl.out_bytes);
+  for (int i = 0; i < slabs && ok; ++i) {
+    const int b = i & 1, r0 = i * sl.rows;
+    const int nr = ((size_t)r0 + sl.rows <= units) ? sl.rows : (int)units - r0;
+    // slab buffers (ping-pong by slab parity): q k v dO beta | o dq dk dv dbeta
+    char* io = base + (size_t)b * (sl.in_bytes + sl.out_bytes);
+    char* iq = io;
+    char* ik = iq + round_up(sl.rows * rq);
+    char* iv = ik + round_up(sl.rows * rq);
+    char* ido = iv + round_up(sl.rows * rv);
+    char* ib = ido + round_up(sl.rows * rv);
+    char* oo = io + sl.in_bytes;
+    char* odq = oo + round_up(sl.rows * rv);
+    char* odk = odq + round_up(sl.rows * rq);
+    char* odv = odk + round_up(sl.rows * rq);
+    char* odb = odv + round_up(sl.rows * rv);
+    const size_t fq = (size_t)r0 * rq, fv = (size_t)r0 * rv, fb = (size_t)r0 * rb;
+    const size_t nq = (size_t)nr * rq, nv = (size_t)nr * rv, nb = (size_t)nr * rb;
+    // slab i's inputs once slab i-2's outputs have been read out of buffer b
+    if (i >= 2) ok = cudaStreamWaitEvent(sin, ev_out[b], 0) == cudaSuccess;
+    ok = ok &&
+         cudaMemcpyAsync(iq, (const char*)q + fq, nq, cudaMemcpyHostToDevice, sin) == cudaSuccess &&
+         cudaMemcpyAsync(ik, (const char*)k + fq, nq, cudaMemcpyHostToDevice, sin) == cudaSuccess &&
+         cudaMemcpyAsync(iv, (const char*)v + fv, nv, cudaMemcpyHostToDevice, sin) == cudaSuccess &&
+         cudaMemcpyAsync(ido, (const char*)dO + fv, nv, cudaMemcpyHostToDevice, sin) == cudaSuccess &&
+         cudaMemcpyAsync(ib, (const char*)beta + fb, nb, cudaMemcpyHostToDevice, sin) == cudaSuccess &&
+         cudaEventRecord(ev_in[b], sin) == cudaSuccess &&
+         cudaStreamWaitEvent(scmp, ev_in[b], 0) == cudaSuccess;
+    if (!ok) break;
+    deltanet_desc e = *d;
+    e.B = nr;
+    e.H = 1;
+    e.flags |= DELTANET_SAVE_STATES;
+    rc = fwd_impl(&e, iq, ik, iv, ib, nullptr, nullptr, oo, nullptr, wsb, sl.ws_bytes, scmp);
+    if (!rc)
+      rc = bwd_impl(&e, iq, ik, iv, ib, nullptr, nullptr, ido, nullptr, odq, odk, odv, odb,
+                    nullptr, nullptr, wsb, sl.ws_bytes, scmp);
+    if (rc) break;
+    ok = cudaEventRecord(ev_cmp[b], scmp) == cudaSuccess &&
+         cudaStreamWaitEvent(sout, ev_cmp[b], 0) == cudaSuccess &&
+         cudaMemcpyAsync((char*)o + fv, oo, nv, cudaMemcpyDeviceToHost, sout) == cudaSuccess &&
+         cudaMemcpyAsync((char*)dq + fq, odq, nq, cudaMemcpyDeviceToHost, sout) == cudaSuccess &&
+         cudaMemcpyAsync((char*)dk + fq, odk, nq, cudaMemcpyDeviceToHost, sout) == cudaSuccess &&
+         cudaMemcpyAsync((char*)dv + fv, odv, nv, cudaMemcpyDeviceToHost, sout) == cudaSuccess &&
+         cudaMemcpyAsync((char*)dbeta + fb, odb, nb, cudaMemcpyDeviceToHost, sout) == cudaSuccess &&
+         cudaEventRecord(ev_out[b], sout) == cudaSuccess;
+  }
+  // the caller's stream resumes after the last read-out (sout is in order)
+  const bool tail = cudaEventRecord(ev_done, sout) == cudaSuccess &&
+                    cudaStreamWaitEvent(user, ev_done, 0) == cudaSuccess;
+  ok = ok && tail;
+  for (int b = 0; b < 2; ++b) {
+    if (ev_in[b]) cudaEventDestroy(ev_in[b]);
+    if (ev_cmp[b]) cudaEventDestroy(ev_cmp[b]);
+    if (ev_out[b]) cudaEventDestroy(ev_out[b]);
+  }
+  if (ev_entry) cudaEventDestroy(ev_entry);
+  if (ev_done) cudaEventDestroy(ev_done);
+  if (sin) cudaStreamDestroy(sin);
+  if (scmp) cudaStreamDestroy(scmp);
+  if (sout) cudaStreamDestroy(sout);
+  if (rc) return rc;
+  return ok ? DELTANET_OK : DELTANET_ERR_CUDA;
 }
 
 int deltanet_fwd_transition(const deltanet_desc* d, const void* q, const void* k, const void* v,

@@ -44,7 +44,7 @@ def test_no_torch_types_in_abi():
 
 
 def test_abi_version_and_strerror(lib):
-    assert lib.deltanet_abi_version() == 6
+    assert lib.deltanet_abi_version() == 7
     for code in range(6):
         assert dn.deltanet_strerror(code)
     assert "unknown" in dn.deltanet_strerror(99)

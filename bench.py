@@ -302,35 +302,34 @@ def _timed(dev, fn, reps):
     return e0.elapsed_time(e1) * 1e-3 / reps
 
 
-def measure_gated(dn, dev, q, k, v, beta, t_fwd_ungated):
+def measure_gated(dn, dev, q, k, v, beta, t_fwd_ungated, t_bwd_ungated):
     """Side measurement (outside the timed step) of Gated DeltaNet (SURVEY
-    §8(f) f4): the tcgen05 gated forward on the step's
-    forward workload (gates g = -0.05 softplus(N(0,1))), and the gated
-    backward (CUDA-core SIMT path today) on a small workload."""
+    §8(f) f4): the tcgen05 gated forward and backward on the
+    step's workload (gates g = -0.05 softplus(N(0,1)), dO ~ N(0,1)); the
+    backward reads the forward's saved records like the ungated step."""
     import torch
     B, Hh, Ll, D = q.shape
     gen = torch.Generator(device=dev).manual_seed(17)
     gates = -0.05 * torch.nn.functional.softplus(
         torch.randn((B, Hh, Ll), device=dev, generator=gen))
+    dO = torch.randn(v.shape, device=dev, generator=gen).to(v.dtype)
     o = torch.empty_like(v)
     d = dn.make_desc(B, Hh, Ll, D, D, 64, torch.bfloat16, gated=True)
     ws = dn.alloc_workspace(d, dev)
     t_f = _timed(dev, lambda: dn.deltanet_gated_fwd(q, k, v, beta, gates, workspace=ws, out=o,
                                                     want_hT=False), 5)
-    Bs, Hs, Ls = 1, 8, 512
-    sl = lambda t: t[:Bs, :Hs, :Ls].contiguous()
-    qs, ks, vs, bs, gs = sl(q), sl(k), sl(v), sl(beta), sl(gates)
-    dOs = torch.randn_like(vs)
-    _, _, wss = dn.deltanet_gated_fwd(qs, ks, vs, bs, gs)
-    t_b = _timed(dev, lambda: dn.deltanet_gated_bwd(qs, ks, vs, bs, gs, dOs, workspace=wss,
-                                                    want_dh0=False), 1)
-    return {"fwd": {"workload": f"B={B} H={Hh} L={Ll} d={D} bf16 (the step's forward)",
-                    "kernel": "tc_fwd_kernel<gated> (tcgen05)", "ms": t_f * 1e3,
-                    "tokens_per_s": B * Ll / t_f, "vs_ungated_fwd": t_f / t_fwd_ungated,
+    t_b = _timed(dev, lambda: dn.deltanet_gated_bwd(q, k, v, beta, gates, dO, workspace=ws,
+                                                    want_dh0=False), 5)
+    wl = f"B={B} H={Hh} L={Ll} d={D} bf16 (the step's workload)"
+    return {"fwd": {"workload": wl, "kernel": "tc_fwd_kernel<false, true> (tcgen05)",
+                    "ms": t_f * 1e3, "tokens_per_s": B * Ll / t_f,
+                    "vs_ungated_fwd": t_f / t_fwd_ungated,
                     "launches": dn.deltanet_launch_count(d, 0)},
-            "bwd": {"workload": f"B={Bs} H={Hs} L={Ls} d={D} bf16",
-                    "kernel": "simt_bwd_kernel (CUDA cores; tcgen05 gated bwd not built)",
-                    "ms": t_b * 1e3, "tokens_per_s": Bs * Ls / t_b}}
+            "bwd": {"workload": wl, "kernel": "tc_bwd_kernel<false, true> (tcgen05)",
+                    "ms": t_b * 1e3, "tokens_per_s": B * Ll / t_b,
+                    "vs_ungated_bwd": t_b / t_bwd_ungated,
+                    "launches": dn.deltanet_launch_count(d, 1)},
+            "fwd_bwd_tokens_per_s": B * Ll / (t_f + t_b)}
 
 
 def measure_context_parallel(dn, dev, parts=2):
@@ -648,7 +647,7 @@ def main():
         rec = measure_recurrent(dn, dev, q, k, v, beta, t_fwd, peaks)
         pro = measure_prologue(dn, dev, B_PER_RANK, H, L, D, peaks)
         lng = measure_long_context(dn, dev)
-        gat = measure_gated(dn, dev, q, k, v, beta, t_fwd)
+        gat = measure_gated(dn, dev, q, k, v, beta, t_fwd, t_bwd)
         cpx = measure_context_parallel(dn, dev)
 
     if rank == 0:

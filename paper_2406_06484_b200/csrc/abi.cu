@@ -31,13 +31,13 @@ int validate_rec(const deltanet_desc* d) {
   return DELTANET_OK;
 }
 
-// forward path; the gated backward always runs on the SIMT path (use_tc_bwd)
+// path choice (the gated forward and backward share the tcgen05 shapes)
 bool use_tc(const deltanet_desc* d) {
   return !(d->flags & DELTANET_FORCE_SIMT) && dn::tc_supported(d) &&
          (!(d->flags & DELTANET_GATED) || dn::tc_gated_supported(d));
 }
 
-bool use_tc_bwd(const deltanet_desc* d) { return use_tc(d) && !(d->flags & DELTANET_GATED); }
+bool use_tc_bwd(const deltanet_desc* d) { return use_tc(d); }
 
 size_t elem_bytes(const deltanet_desc* d) { return d->dtype == DELTANET_FP32 ? 4 : 2; }
 
@@ -54,8 +54,7 @@ size_t scratch_bytes(const deltanet_desc* d) {
                       sizeof(float);
   if (!use_tc(d)) return simt;
   const size_t tc = dn::tc_scratch_bytes(d);
-  // gated: tcgen05 forward, SIMT backward -> room for both
-  return (d->flags & DELTANET_GATED) ? (tc > simt ? tc : simt) : tc;
+  return tc;
 }
 
 dn::Args make_args(const deltanet_desc* d, void* ws) {

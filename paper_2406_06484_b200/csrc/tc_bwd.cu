@@ -63,7 +63,12 @@ constexpr int OFF_R = OFF_Z + TILE;         // R -> Y [0,8K) + G1 [8K,16K)
 constexpr int OFF_QU1 = OFF_R + TILE;
 constexpr int OFF_A = OFF_QU1 + TILE;       // A_m -> dX -> dA
 constexpr int OFF_VEC = OFF_A + C * C * 2;  // beta, r, s, nq, nk, db1[2], db2[2], dot[2], dotq[2], n2[4]
-constexpr int SMEM_BYTES = OFF_VEC + 17 * C * 4;
+// gated: gate vectors of the chunk and the dl/dG partials
+constexpr int OFF_GV = OFF_VEC + 17 * C * 4;  // gG, gam, gD [64] each
+// colT1[4][64] colT2[4][64] pkh[2][64] DD[2][64] rowT1[2][64] tq[2][64] dG[64] hdot[8] gCn
+constexpr int OFF_GP = OFF_GV + 3 * C * 4;
+constexpr int GP_FLOATS = 4 * C + 4 * C + 2 * C + 2 * C + 2 * C + 2 * C + C + 8 + 8;
+constexpr int SMEM_BYTES = OFF_GP + GP_FLOATS * 4;
 static_assert(SMEM_BYTES <= 232448 - 1024, "shared memory budget");
 
 // ---- TMEM column map (512 columns)
@@ -91,6 +96,31 @@ __device__ __forceinline__ void ld32(uint32_t tm, int wwarp, uint32_t col, float
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int j = 0; j < 16; ++j) f[16 * i + j] = __uint_as_float(r[i][j]);
+}
+__device__ __forceinline__ float warp_sum(float x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+// reduce-scatter across N lanes (N = 32, or 16 within each half-warp): on
+// return lane l holds the sum over the N lanes of v[l % N]
+template <int N>
+__device__ __forceinline__ float reduce_scatter(float (&v)[N], int lane) {
+#pragma unroll
+  for (int m = N / 2; m >= 1; m >>= 1) {
+    const bool up = (lane & m) != 0;
+#pragma unroll
+    for (int i = 0; i < m; ++i) {
+      const float send = up ? v[i] : v[i + m];
+      const float keep = up ? v[i + m] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+    }
+  }
+  return v[0];
+}
+// Gamma(i, j) = e^{G_i - G_j} (j <= i; clamped at 1 above the diagonal)
+__device__ __forceinline__ float gamma_ij(const float* gG, int i, int j) {
+  return __expf(fminf(gG[i] - gG[j], 0.f));
 }
 __device__ __forceinline__ void ld16f(uint32_t tm, int wwarp, uint32_t col, float (&f)[16]) {
   uint32_t r[16];
@@ -148,7 +178,26 @@ __device__ __forceinline__ void simt_signal(uint64_t* bar, int tid) {
 // SEG1 = pass 1 of the segment-parallel backward: only the
 // dH chain of the segment, from dH = 0 at its end, down to its start (the
 // segment-local dl/dH_start); no local gradients, no stores.
-template <bool SEG1>
+// GATED = Gated DeltaNet backward (R23, §4.9; the exact adjoint of
+// tc_fwd_kernel<false, true>, oracle/forms.py gated_chunkwise_backward).  With
+// the chunk's cumulative log-gate G, gamma = e^G, Gamma(i,j) = e^{G_i - G_j},
+// D_j = e^{G_63 - G_j} (all formed from differences, never as ratios):
+//   dU'^T = (dH^T K^T diag(D) + dO^T (Gamma . A_m)) diag(s)   [two accumulators]
+//   R = V - diag(gamma s) K H,  sDV = diag(gamma) dV (dV itself stored from P5)
+//   dK = diag(D) U' dH^T (rescaled in TMEM) - (gamma dV) H^T + dS^T Q_hat + ...
+//   dS = Gamma . dA;  G1 = diag(beta) (Gamma . G)
+//   dO is scaled by gamma in place once dA has read it (P6); then
+//   dH += (gamma dO)^T Q_hat and dQ = (gamma dO) H^T + dS K_hat
+//   dH <- gamma_63 dH rescaled in TMEM when its bf16 image is taken (P5b)
+// and dl/dG_i = q_hat_i . (gamma dO H^T)_i + rowsum(T1)_i - colsum(T1)_i + rowsum(T2)_i - colsum(T2)_i
+//   - beta_i gamma_i rowsum(P . K_hat H)_i - DD_i
+//   + [i = 63] (sum_j DD_j + gamma_63 <dH, H_t>),
+// T1 = dS . Q_hat K_hat^T, T2 = G1 . K_hat K_hat^T, DD_j = D_j k_hat_j . (U' dH^T)_j
+// (the first term is read in P7 before dS K_hat accumulates into dQ, and the
+// T1 row and column sums come from the same fp32 values, so their diagonal
+// cancels exactly under fast decay); dg = reverse cumulative sum of dl/dG
+// within the chunk.
+template <bool SEG1, bool GATED = false>
 __global__ void __launch_bounds__(NT, 1)
     tc_bwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                   const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mDO,
@@ -177,6 +226,20 @@ __global__ void __launch_bounds__(NT, 1)
   float* sdot = db2 + 2 * C;   // [2][64] dk-adjoint dot partials
   float* sdotq = sdot + 2 * C; // [2][64] dq-adjoint dot partials
   float* n2 = sdotq + 2 * C;   // [4][64] squared-norm partials (column quarters)
+  // gated only
+  float* gG = reinterpret_cast<float*>(smem + OFF_GV);  // in-chunk cumulative log-gate
+  float* gam = gG + C;         // e^G
+  float* gD = gam + C;         // e^{G_63 - G}
+  float* colT1 = reinterpret_cast<float*>(smem + OFF_GP);  // [4 warps][64]
+  float* colT2 = colT1 + 4 * C;  // [4 warps][64]
+  float* pkh = colT2 + 4 * C;    // [2][64] rowsum(P . K_hat H) partials
+  float* ddp = pkh + 2 * C;      // [2][64] k_hat . (U' dH^T) partials
+  float* rowT1 = ddp + 2 * C;    // [2][64] rowsum(T1) partials
+  float* tqp = rowT1 + 2 * C;    // [2][64] q_hat . (gamma dO H^T) partials
+  float* dGs = tqp + 2 * C;      // [64] dl/dG of the chunk
+  float* hdot = dGs + C;         // [8] <dH image, H_t> per warp
+  float* gCn = hdot + 8;         // e^{G_63} of the next chunk processed (c - 1)
+  static_assert(!(SEG1 && GATED), "the gated backward runs one CTA per unit");
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wg = (tid >> 7) & 1, w = tid & 127, wwarp = w >> 5;
@@ -276,7 +339,7 @@ __global__ void __launch_bounds__(NT, 1)
           load_q(c - 1, (it + 1) & 1);
         }
         mbar_wait(&sg[SG_P5], ph);
-        if (!SEG1) {
+        if (!SEG1 && !GATED) {  // (gated: sDV holds gamma dV; dV is stored from P5)
           tma_store_4d(&mDV, sDV, 0, t0, 0, unit);
           bulk_commit();
         }
@@ -363,8 +426,11 @@ __global__ void __launch_bounds__(NT, 1)
         {
           const uint32_t ida = idesc_bf16(128, 64, true, true);
 #pragma unroll
+          // gated: its own accumulator (TM_P, free until M3); P3 adds
+          // diag(D) times the dH^T K^T term
           for (int k0 = 0; k0 < C; k0 += 16)
-            mma_bf16(tm + TM_DU, desc_mn(aDO, C, k0), desc_mn(aA, C, k0), ida, 1);
+            mma_bf16(tm + (GATED ? TM_P : TM_DU), desc_mn(aDO, C, k0), desc_mn(aA, C, k0), ida,
+                     GATED ? k0 > 0 : 1);
           mma_commit(&mb[MB_DU]);
         }
 
@@ -373,7 +439,30 @@ __global__ void __launch_bounds__(NT, 1)
         mbar_wait(&sg[SG_P3], ph);
         fence_after_sync();
         ISTAMP(21);
-        {
+        if (GATED) {
+          // dK = U' dH^T first: P5 takes k_hat . (U' dH^T) and rescales it by D
+          // before M5 accumulates (MB_P covers it); dH += (gamma dO)^T Q_hat
+          // waits for P6 (dO scaled in place)
+          const uint32_t id_k1 = idesc_bf16(64, 128, true, true);
+#pragma unroll
+          for (int k0 = 0; k0 < D; k0 += 16)
+            mma_bf16(tm + TM_DK, desc_mn(aUP, D, k0), desc_mn(aDH, D, k0), id_k1, k0 > 0);
+          const uint32_t idp = idesc_bf16(64, 64, true, false);
+#pragma unroll
+          for (int k0 = 0; k0 < C; k0 += 16) {
+            mma_bf16(tm + TM_P, desc_mn(aX, C, k0), desc_k(aDUP, D, k0), idp, k0 > 0);
+            mma_bf16(tm + TM_P + LO16, desc_mn(aX, C, k0), desc_k(aDUP + HALF_ROWS, D, k0), idp,
+                     k0 > 0);
+          }
+#pragma unroll
+          for (int k0 = 0; k0 < D; k0 += 16)
+            mma_bf16(tm + TM_DX, desc_mn(aDUP, D, k0), desc_k(aR, C, k0), idp, k0 > 0);
+          const uint32_t idg = idesc_bf16(64, 64, false, false);
+#pragma unroll
+          for (int k0 = 0; k0 < D; k0 += 16)
+            mma_bf16(tm + TM_G + LO16, desc_k(aK, C, k0), desc_k(aK, C, k0), idg, k0 > 0);
+          mma_commit(&mb[MB_P]);
+        } else {
           const uint32_t idp = idesc_bf16(64, 64, true, false);
 #pragma unroll
           for (int k0 = 0; k0 < C; k0 += 16) {
@@ -415,7 +504,7 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
           for (int k0 = 0; k0 < C; k0 += 16)
             mma_bf16(tm + TM_DH, desc_mn(aDV, C, k0), desc_mn(aK, C, k0), id2, 1);
-          mma_commit(&mb[MB_DH]);
+          if (!GATED) mma_commit(&mb[MB_DH]);
           if (SEG1) {  // the chain is all: dO, X and the q / k slots are free
             mma_commit(&mb[MB_LD]);
             mma_commit(&mb[MB_GB]);
@@ -434,10 +523,10 @@ __global__ void __launch_bounds__(NT, 1)
           mma_commit(&mb[MB_A]);
 #pragma unroll
           for (int k0 = 0; k0 < D; k0 += 16) {
-            mma_bf16(tm + TM_DQ, desc_k(aDO, C, k0), desc_mn(aH, D, k0), id_q, k0 > 0);
+            if (!GATED) mma_bf16(tm + TM_DQ, desc_k(aDO, C, k0), desc_mn(aH, D, k0), id_q, k0 > 0);
             mma_bf16(tm + TM_DK, desc_k(aDV, C, k0), desc_mn(aH, D, k0), id_k2, 1);
           }
-          mma_commit(&mb[MB_LD]);
+          if (!GATED) mma_commit(&mb[MB_LD]);
         }
         ISTAMP(24);
 
@@ -446,6 +535,18 @@ __global__ void __launch_bounds__(NT, 1)
         mbar_wait(&sg[SG_P6], ph);
         fence_after_sync();
         ISTAMP(25);
+        if (GATED) {  // dO now holds gamma dO
+          const uint32_t id1 = idesc_bf16(128, 128, true, true);
+#pragma unroll
+          for (int k0 = 0; k0 < C; k0 += 16)
+            mma_bf16(tm + TM_DH, desc_mn(aDO, C, k0), desc_mn(aQ, C, k0), id1, 1);
+          mma_commit(&mb[MB_DH]);
+          const uint32_t id_q = idesc_bf16(64, 128, false, true);
+#pragma unroll
+          for (int k0 = 0; k0 < D; k0 += 16)
+            mma_bf16(tm + TM_DQ, desc_k(aDO, C, k0), desc_mn(aH, D, k0), id_q, k0 > 0);
+          mma_commit(&mb[MB_LD]);
+        }
         {
           const uint32_t id_q = idesc_bf16(64, 128, false, true);
           const uint32_t id_k = idesc_bf16(64, 128, true, true);
@@ -454,10 +555,12 @@ __global__ void __launch_bounds__(NT, 1)
           for (int k0 = 0; k0 < C; k0 += 16)
             mma_bf16(tm + TM_GB, desc_k(aY, C, k0), desc_k(aX, C, k0), id_g, k0 > 0);
           mma_commit(&mb[MB_GB]);
+          if (!GATED) {  // (gated: after P7, which reads TM_DQ = (gamma dO) H^T)
 #pragma unroll
-          for (int k0 = 0; k0 < C; k0 += 16) {
-            mma_bf16(tm + TM_DQ, desc_k(aDA, C, k0), desc_mn(aK, C, k0), id_q, 1);
-            mma_bf16(tm + TM_DK, desc_mn(aDA, C, k0), desc_mn(aQ, C, k0), id_k, 1);
+            for (int k0 = 0; k0 < C; k0 += 16) {
+              mma_bf16(tm + TM_DQ, desc_k(aDA, C, k0), desc_mn(aK, C, k0), id_q, 1);
+              mma_bf16(tm + TM_DK, desc_mn(aDA, C, k0), desc_mn(aQ, C, k0), id_k, 1);
+            }
           }
         }
         ISTAMP(26);
@@ -466,6 +569,15 @@ __global__ void __launch_bounds__(NT, 1)
         mbar_wait(&sg[SG_P7], ph);
         fence_after_sync();
         ISTAMP(27);
+        if (GATED) {  // M6's dQ += dS K_hat ; dK += dS^T Q_hat
+          const uint32_t id_q = idesc_bf16(64, 128, false, true);
+          const uint32_t id_k = idesc_bf16(64, 128, true, true);
+#pragma unroll
+          for (int k0 = 0; k0 < C; k0 += 16) {
+            mma_bf16(tm + TM_DQ, desc_k(aDA, C, k0), desc_mn(aK, C, k0), id_q, 1);
+            mma_bf16(tm + TM_DK, desc_mn(aDA, C, k0), desc_mn(aQ, C, k0), id_k, 1);
+          }
+        }
         {
           const uint32_t id_m = idesc_bf16(64, 128, false, true);
           const uint32_t id_mt = idesc_bf16(64, 128, true, true);
@@ -483,9 +595,27 @@ __global__ void __launch_bounds__(NT, 1)
     // =====================================================================
     // SIMT warps 0-7 (two warpgroups; phases split columns between them)
     // =====================================================================
+    // gated: log-gates of the chunk processed next, rows (lane, 32 + lane) in
+    // warps 0-1, read one chunk ahead; e^{G_63} of the last chunk rescales dhT
+    const float* gsrc = GATED ? a.g + (size_t)unit * a.L + T0 : nullptr;
+    auto gload = [&](int cc, int j) {
+      return (GATED && cc >= 0 && cc * C + j < L) ? gsrc[cc * C + j] : 0.f;
+    };
+    float ga = 0.f, gb = 0.f;
+    if (GATED) {
+      if (tid < C) {
+        ga = gload(NC - 1, lane);
+        gb = gload(NC - 1, 32 + lane);
+      }
+      if (tid < 32) {
+        const float t = warp_sum(ga) + warp_sum(gb);
+        if (tid == 0) gCn[0] = __expf(t);
+      }
+      grp_sync<256>(BAR_SIMT);
+    }
     {
       // dH^T <- dhT^T in TMEM (lane dv = w; columns split by warpgroup) and
-      // its bf16 image for the first chunk
+      // its bf16 image for the first chunk (gated: TMEM holds e^{G_63} dhT)
       // the cotangent at this segment's end: dhT for the last segment, the
       // scanned dl/dH for the others (pass 3), zero in pass 1
       const float* dhT = SEG1 ? nullptr
@@ -498,7 +628,7 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           f[j] = dhT ? dhT[(size_t)(c0 + j) * D + w] : 0.f;
-          r[j] = __float_as_uint(f[j]);
+          r[j] = __float_as_uint(GATED ? f[j] * gCn[0] : f[j]);
         }
         tmem_st16(taddr(tm, wwarp * 32, TM_DH + c0), r);
         il_store8(sDH, D, w, c0, f);
@@ -519,10 +649,27 @@ __global__ void __launch_bounds__(NT, 1)
       uint8_t* sK = smem + OFF_K + ks * TILE;
       uint8_t* sQ = qu(ks);         // q -> q_hat -> dq staging
       uint8_t* sDUP = qu(ks ^ 1);   // dU'^T
+      float qkg[16];                // gated: Gamma . Q_hat K_hat^T of P2 (used in P6)
 
       // ================= P1: k norms ; U' ; R = V - diag(s) K H ; q norms
       BSTAMP(0);
       if (tid < C) sb[tid] = bnext;
+      if (GATED && tid < C) {
+        // G = in-chunk inclusive cumsum of g; gamma = e^G; D = e^{G_63 - G}
+        float x = tid < 32 ? ga : gb;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const float y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        const float tot0 = warp_sum(ga), tot1 = warp_sum(gb);
+        const float Gi = x + (tid >= 32 ? tot0 : 0.f);
+        gG[tid] = Gi;
+        gam[tid] = __expf(Gi);
+        gD[tid] = __expf((tot0 + tot1) - Gi);
+        ga = gload(c - 1, lane);  // next chunk processed (summed in P3)
+        gb = gload(c - 1, 32 + lane);
+      }
       // squared row norms of a raw 64x128 tile: thread = (row w & 63, column
       // quarter wg * 2 + (w >> 6)), combined through n2
       auto row_norms = [&](const uint8_t* tile, float* inv_out, float* n_out) {
@@ -553,6 +700,20 @@ __global__ void __launch_bounds__(NT, 1)
       mbar_wait(&mb[MB_MAIN], ph);
       row_norms(sK, ss, nk);
       BSTAMP(1);
+      if (GATED) {  // <dH image (dl/dH_{t+1}), H_t>: both bf16 IL R=128 images
+        float hd = 0.f;
+#pragma unroll
+        for (int k8 = 0; k8 < 8; ++k8) {
+          const int off = (tid + 256 * k8) * 16;
+          float x8[8], y8[8];
+          unpack8(*reinterpret_cast<const uint4*>(sH + off), x8);
+          unpack8(*reinterpret_cast<const uint4*>(sDH + off), y8);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) hd = fmaf(x8[e], y8[e], hd);
+        }
+        hd = warp_sum(hd);
+        if (lane == 0) hdot[warp] = hd;
+      }
       if (l2 && !SEG1) {  // U'^T[dv][t] = Z^T[dv][t] * max(|k_t|, eps)  (row dv = w)
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
@@ -576,7 +737,7 @@ __global__ void __launch_bounds__(NT, 1)
           // this warpgroup takes 32 of each half
           float f[32];
           ld32(tm, wwarp, TM_KH + 32 * wg, f);
-          const float si = ss[r64];
+          const float si = GATED ? ss[r64] * gam[r64] : ss[r64];  // gated: R = V - gamma K_hat H
           const int c0 = (lo ? 0 : 64) + 32 * wg;
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
@@ -609,8 +770,11 @@ __global__ void __launch_bounds__(NT, 1)
           float a8[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            const float v = lo ? f[g * 8 + e] : x[g * 8 + e];
-            a8[e] = (c0 + g * 8 + e <= r64) ? ri * v : 0.f;
+            const int j = c0 + g * 8 + e;
+            float v = lo ? f[g * 8 + e] : x[g * 8 + e];
+            if (GATED) v *= gamma_ij(gG, r64, j);  // Gamma . A_m
+            a8[e] = (j <= r64) ? ri * v : 0.f;
+            if (GATED) qkg[g * 8 + e] = a8[e] * ss[j];  // Gamma . Q_hat K_hat^T (T1 of P6)
           }
           il_store8(sA, C, r64, c0 + g * 8, a8);
         }
@@ -636,9 +800,19 @@ __global__ void __launch_bounds__(NT, 1)
       mbar_wait(&mb[MB_DU], ph);
       fence_after_sync();
       BSTAMP(5);
+      if (GATED && tid < 32) {  // e^{G_63} of chunk c-1 (P5b rescales dH by it)
+        const float t = warp_sum(ga) + warp_sum(gb);
+        if (tid == 0) gCn[0] = __expf(t);
+      }
       {  // dU'^T (lane d_v = w) * s_j -> bf16
         float f[32];
         ld32(tm, wwarp, TM_DU + 32 * wg, f);
+        if (GATED) {  // dU'^T = dH^T K^T diag(D) (TM_DU) + dO^T (Gamma . A_m) (TM_P)
+          float p[32];
+          ld32(tm, wwarp, TM_P + 32 * wg, p);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) f[e] = fmaf(f[e], gD[32 * wg + e], p[e]);
+        }
 #pragma unroll
         for (int e = 0; e < 32; e += 4) {  // vector broadcast loads of s
           const float4 s4 = *reinterpret_cast<const float4*>(ss + 32 * wg + e);
@@ -671,6 +845,32 @@ __global__ void __launch_bounds__(NT, 1)
           il_store8(sDV, C, r64, c0 + g * 8, dv8);
         }
       } else {
+        if (GATED) {
+          // dK = U' dH^T (lanes < 16; lanes >= 16 carry TM_DQ's stale rows
+          // back unchanged): DD partial k_hat . (U' dH^T), then rows * D
+          float f[64];
+          ld64(tm, wwarp, TM_DK + 64 * wg, f);
+          float dd = 0.f;
+          if (lo) {
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+              float x8[8];
+              il_load8(sK, C, r64, 64 * wg + g * 8, x8);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) dd = fmaf(x8[e], f[g * 8 + e], dd);
+            }
+            ddp[wg * C + r64] = dd;
+          }
+          const float sc = lo ? gD[r64] : 1.f;
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            uint32_t r[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(f[16 * q4 + j] * sc);
+            tmem_st16(taddr(tm, wwarp * 32, TM_DK + 64 * wg + 16 * q4), r);
+          }
+          tmem_st_wait();
+        }
         {
           // lanes < 16: columns [0,64), lanes >= 16: [64,128) of row r64, for
           // both P (TM_P) and K H (TM_KH); 32 of each half per warpgroup
@@ -678,22 +878,42 @@ __global__ void __launch_bounds__(NT, 1)
           ld32(tm, wwarp, TM_P + 32 * wg, p);
           ld32(tm, wwarp, TM_KH + 32 * wg, f);
           const float bt = sb[r64], si = ss[r64];
+          const float gi = GATED ? gam[r64] : 1.f;
           const int c0 = (lo ? 0 : 64) + 32 * wg;
-          float db = 0.f;
+          float db = 0.f, pk = 0.f;
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
             float v8[8], dv8[8];
             il_load8(sV, C, r64, c0 + g * 8, v8);
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-              const float rr = fmaf(-si, f[g * 8 + e], v8[e]);
+              const float kh = si * f[g * 8 + e];  // (K_hat H)[r64][.]
+              const float rr = fmaf(-gi, kh, v8[e]);
               db = fmaf(p[g * 8 + e], rr, db);  // P . R
+              if (GATED) pk = fmaf(p[g * 8 + e], kh, pk);
               dv8[e] = bt * p[g * 8 + e];
+            }
+            if (GATED) {  // dV to global here; the operand tile takes gamma dV
+              if (t0 + r64 < L) {
+                uint4 u;
+                u.x = pack_bf16(dv8[0], dv8[1]);
+                u.y = pack_bf16(dv8[2], dv8[3]);
+                u.z = pack_bf16(dv8[4], dv8[5]);
+                u.w = pack_bf16(dv8[6], dv8[7]);
+                *reinterpret_cast<uint4*>((__nv_bfloat16*)a.dv +
+                                          ((size_t)unit * a.L + T0 + t0 + r64) * D + c0 + g * 8) = u;
+              }
+#pragma unroll
+              for (int e = 0; e < 8; ++e) dv8[e] *= gi;
             }
             il_store8(sDV, C, r64, c0 + g * 8, dv8);
           }
           db += __shfl_xor_sync(0xffffffffu, db, 16);
           if (lo) db1[wg * C + r64] = db;
+          if (GATED) {
+            pk += __shfl_xor_sync(0xffffffffu, pk, 16);
+            if (lo) pkh[wg * C + r64] = pk;
+          }
         }
 #pragma unroll 1
         for (int cc = 0; cc < 2; ++cc) {  // dX = dX' diag(beta) (lanes < 16: dX' rows)
@@ -717,16 +937,30 @@ __global__ void __launch_bounds__(NT, 1)
       simt_signal(&sg[SG_P5], tid);
       BSTAMP(8);
 
-      // ================= P5b (under M5): dH image for chunk c-1
-      if (c > 0) {
+      // ================= P5b (under M5): dH image for chunk c-1 (gated:
+      // after P6, since dH += (gamma dO)^T Q_hat needs dO scaled; TMEM dH is
+      // then rescaled by e^{G_63} of chunk c-1)
+      auto dh_image = [&]() {
         mbar_wait(&mb[MB_DH], ph);  // M4 done; dK = U' dH^T done reading the old image
         fence_after_sync();
         float f[64];
         ld64(tm, wwarp, TM_DH + 64 * wg, f);
 #pragma unroll
         for (int g = 0; g < 8; ++g) il_store8(sDH, D, w, 64 * wg + g * 8, f + g * 8);
+        if (GATED) {
+          const float sc = gCn[0];
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            uint32_t r[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(f[16 * q4 + j] * sc);
+            tmem_st16(taddr(tm, wwarp * 32, TM_DH + 64 * wg + 16 * q4), r);
+          }
+          tmem_st_wait();
+        }
         simt_signal(&sg[SG_DHI], tid);
-      }
+      };
+      if (!GATED && c > 0) dh_image();
       BSTAMP(9);
       if (SEG1) {  // pass 1 stops at the chain; the TMA warp reloads the k slot
         simt_signal(&sg[SG_P8], tid);
@@ -740,19 +974,54 @@ __global__ void __launch_bounds__(NT, 1)
       {
         float f[32];
         ld32(tm, wwarp, TM_DA + 32 * wg, f);  // lanes<16: dA row, lanes>=16: Y row
+        // gated: dS = Gamma . dA, and T1 = dS . (Gamma . Q_hat K_hat^T) with the
+        // partner lane's 16 P2 values (columns 32 wg + 16..31 of row r64)
+        float qk2[16], t1[32];
+        if (GATED) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) qk2[e] = __shfl_xor_sync(0xffffffffu, qkg[e], 16);
+        }
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           float x[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const int j = 32 * wg + g * 8 + e;
-            x[e] = (!lo || j <= r64) ? f[g * 8 + e] : 0.f;
+            float v = f[g * 8 + e];
+            if (GATED && lo) v *= gamma_ij(gG, r64, j);
+            x[e] = (!lo || j <= r64) ? v : 0.f;
+            if (GATED) {
+              const float qv = (g * 8 + e < 16) ? qkg[(g * 8 + e) & 15] : qk2[(g * 8 + e) & 15];
+              // T1 = dS . QK = dA . (Gamma . QK): the unscaled dA times qkg
+              t1[g * 8 + e] = (lo && j <= r64) ? f[g * 8 + e] * qv : 0.f;
+            }
           }
           il_store8(lo ? sDA : sY, C, r64, 32 * wg + g * 8, x);
+        }
+        if (GATED) {  // T1 row sums (lanes < 16), then this warp's 16 rows per column
+          float rt = 0.f;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) rt += t1[e];
+          if (lo) rowT1[wg * C + r64] = rt;
+          const float cs = reduce_scatter<32>(t1, lane);
+          colT1[wwarp * C + 32 * wg + lane] = cs;
+          // dO <- diag(gamma) dO in place (dA has read it: MB_A): thread = row
+          // tid & 63, column quarter tid >> 6
+          const int row = tid & 63, qt = tid >> 6;
+          const float gr = gam[row];
+#pragma unroll
+          for (int g = 4 * qt; g < 4 * qt + 4; ++g) {
+            float x8[8];
+            il_load8(sDO, C, row, g * 8, x8);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) x8[e] *= gr;
+            il_store8(sDO, C, row, g * 8, x8);
+          }
         }
       }
       simt_signal(&sg[SG_P6], tid);
       BSTAMP(11);
+      if (GATED && c > 0) dh_image();
 
       // ================= P7: G1 = diag(b) G, dbeta part 2
       mbar_wait(&mb[MB_GB], ph);
@@ -761,9 +1030,9 @@ __global__ void __launch_bounds__(NT, 1)
       {
         // lanes < 16 hold the G row (TM_GB), lanes >= 16 the K_hat K_hat^T row
         // (TM_G + 16); each lane pair splits every 16 columns 8 / 8
-        float d2 = 0.f;
+        float d2 = 0.f, t2[16];
         const float bi = sb[r64];
-#pragma unroll 1
+#pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
           const int col = 32 * wg + 16 * cc;
           float g16[16], k16[16], x[8];
@@ -778,14 +1047,36 @@ __global__ void __launch_bounds__(NT, 1)
             const int j = c8 + e;
             const float gr = lo ? g16[e] : x[e];
             const float kk = lo ? x[e] : k16[8 + e];
-            const float gv = (j < r64) ? gr : 0.f;
+            float gv = (j < r64) ? gr : 0.f;
+            if (GATED) gv *= gamma_ij(gG, r64, j);  // Gamma . G
             d2 = fmaf(gv, kk, d2);
             y[e] = bi * gv;
+            if (GATED) t2[cc * 8 + e] = y[e] * kk;  // T2 = G1 . K_hat K_hat^T
           }
           il_store8(sG1, C, r64, c8, y);
         }
         d2 += __shfl_xor_sync(0xffffffffu, d2, 16);
         if (lo) db2[wg * C + r64] = d2;
+        if (GATED) {  // column sums over this warp's 16 rows (lanes of equal lane >> 4)
+          const float cs = reduce_scatter<16>(t2, lane);
+          const int vi = lane & 15;
+          colT2[wwarp * C + 32 * wg + 16 * (vi >> 3) + (lo ? 0 : 8) + (vi & 7)] = cs;
+          // TM_DQ holds (gamma dO) H^T only (dS K_hat is issued after this
+          // phase): lanes >= 16 take q_hat . (gamma dO H^T) of row r64
+          float f[64];
+          ld64(tm, wwarp, TM_DK + 64 * wg, f);
+          if (!lo) {
+            float tq = 0.f;
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+              float x8[8];
+              il_load8(sQ, C, r64, 64 * wg + g * 8, x8);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) tq = fmaf(x8[e], f[g * 8 + e], tq);
+            }
+            tqp[wg * C + r64] = tq;
+          }
+        }
       }
       simt_signal(&sg[SG_P7], tid);
       BSTAMP(13);
@@ -828,6 +1119,38 @@ __global__ void __launch_bounds__(NT, 1)
             x8[e] = l2 ? inv * (f[g * 8 + e] - x8[e] * dot) : f[g * 8 + e];
           il_store8(tile, C, r64, 64 * wg + g * 8, x8);
         }
+      }
+      if (GATED && warp == 0) {
+        // dl/dG of rows lane and 32 + lane (partials of P1-P8), then dg =
+        // reverse cumulative sum within the chunk
+        auto dGrow = [&](int i, float& DDi) {
+          DDi = gD[i] * (ddp[i] + ddp[C + i]);
+          const float ct1 = (colT1[i] + colT1[C + i]) + (colT1[2 * C + i] + colT1[3 * C + i]);
+          const float ct2 = (colT2[i] + colT2[C + i]) + (colT2[2 * C + i] + colT2[3 * C + i]);
+          return (tqp[i] + tqp[C + i]) + (rowT1[i] + rowT1[C + i]) - ct1 +
+                 sb[i] * (db2[i] + db2[C + i]) - ct2 - sb[i] * gam[i] * (pkh[i] + pkh[C + i]) -
+                 DDi;
+        };
+        float DD0, DD1;
+        const float d0 = dGrow(lane, DD0);
+        float d1 = dGrow(32 + lane, DD1);
+        const float sDD = warp_sum(DD0 + DD1);
+        const float shd = warp_sum(lane < 8 ? hdot[lane] : 0.f);
+        if (lane == 31) d1 += sDD + gam[C - 1] * shd;
+        float s1 = d1, s0 = d0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const float y1 = __shfl_down_sync(0xffffffffu, s1, o);
+          const float y0 = __shfl_down_sync(0xffffffffu, s0, o);
+          if (lane + o < 32) {
+            s1 += y1;
+            s0 += y0;
+          }
+        }
+        s0 += __shfl_sync(0xffffffffu, s1, 0);  // + all of rows 32..63
+        float* dg = a.dg + (size_t)unit * a.L + T0 + t0;
+        if (t0 + lane < L) dg[lane] = s0;
+        if (t0 + 32 + lane < L) dg[32 + lane] = s1;
       }
       simt_signal(&sg[SG_P8], tid);
       BSTAMP(15);
@@ -898,7 +1221,9 @@ int tc_bwd(const Args& a0, cudaStream_t s) {
     if (cudaFuncSetAttribute(tc_bwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              SMEM_BYTES) != cudaSuccess ||
         cudaFuncSetAttribute(tc_bwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             SMEM_BYTES) != cudaSuccess)
+                             SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(tc_bwd_kernel<false, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess)
       return DELTANET_ERR_CUDA;
     attr = true;
   }
@@ -921,6 +1246,11 @@ int tc_bwd(const Args& a0, cudaStream_t s) {
       !make_il_map(&mDV, a.dv, BH, a.L, D, C))
     return DELTANET_ERR_CUDA;
   const int nseg = tc_seg_setup(a);
+  if (a.flags & DELTANET_GATED) {  // one CTA per unit (tc_fwd_segments: 1 when gated)
+    if (nseg > 1 || !a.g || !a.dg) return DELTANET_ERR_INVALID_ARG;
+    tc_bwd_kernel<false, true><<<BH, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mDO, mDQ, mDK, mDV, a);
+    return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
+  }
   if (nseg <= 1) {
     tc_bwd_kernel<false><<<BH, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mDO, mDQ, mDK, mDV, a);
     return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;

@@ -166,3 +166,65 @@ def test_bf16_gated_full_size_sampled_units():
                                    gates[bb:bb + 1, h:h + 1])
         compare({"o": o[bb:bb + 1, h:h + 1], "hT": hT[bb:bb + 1, h:h + 1]},
                 {"o": ro, "hT": rhT}, TOL["bf16"])
+
+
+# ------------------------------------------- tcgen05 gated backward (tc_bwd.cu)
+
+@pytest.mark.parametrize("scale", [0.05, 1.0, 4.0])
+@pytest.mark.parametrize("L", [64, 1000])
+def test_bf16_tcgen05_backward(L, scale):
+    """The tcgen05 gated backward (tc_bwd_kernel<false, true>)
+    from a nonzero h0 and dhT, slow to very fast decay (4.0: in-chunk decay
+    products far below fp32's range as ratios), a ragged tail at L = 1000;
+    every gradient incl. dg and dh0 against the fp64 oracle."""
+    import paper_2406_06484_b200 as dn
+    d = dn.make_desc(2, 2, L, 128, 128, gated=True, save_states=False)
+    # path 1 and 2 launches (state recompute + backward): the tcgen05 backward
+    assert dn.deltanet_path(d) == 1 and dn.deltanet_launch_count(d, 1) == 2
+    inp = _case(2, 2, L, 128, 128, 64, "bf16", index=890 + L, scale=scale)
+    rng = np.random.default_rng(L)
+    h0 = 0.3 * rng.standard_normal((2, 2, 128, 128))
+    dhT = 0.3 * rng.standard_normal((2, 2, 128, 128))
+    compare(_gpu(inp, "bf16", 64, h0=h0, dhT=dhT), _ref(inp, h0=h0, dhT=dhT), TOL["bf16"])
+
+
+def test_bf16_tcgen05_backward_no_l2_and_recompute():
+    """Flag off (caller-normalised keys) and the backward without a saved
+    workspace (states recomputed by the gated forward inside the call)."""
+    import paper_2406_06484_b200 as dn
+    inp = _case(1, 2, 200, 128, 128, 64, "bf16", index=897)
+    for f in ("q", "k"):
+        x = inp[f]
+        inp[f] = (x / np.maximum(np.linalg.norm(x, axis=-1, keepdims=True), 1e-6))
+    got = _gpu(inp, "bf16", 64, l2norm=False)
+    compare(got, _ref(inp, l2norm=False), TOL["bf16"])
+    td = torch.bfloat16
+    q, k, v, b, dO = (to_dev(inp[f], td) for f in ("q", "k", "v", "beta", "dO"))
+    g = to_dev(inp["g"], torch.float32)
+    dq, dk, dv, db, dg, _ = dn.deltanet_gated_bwd(q, k, v, b, g, dO, l2norm=False)
+    torch.cuda.synchronize()
+    for key, t in (("dq", dq), ("dk", dk), ("dv", dv), ("dbeta", db), ("dg", dg)):
+        assert np.array_equal(got[key], _np(t)), key
+
+
+def test_bf16_gated_backward_full_size_sampled_units():
+    """BASELINE target shape (B=8 H=16 L=4096) gated forward + backward on the
+    tcgen05 kernels; two sampled units' gradients against the oracle."""
+    import paper_2406_06484_b200 as dn
+    cfg = synth.CONFIGS["target"]
+    inp = synth.make_inputs(cfg)
+    gates = synth.make_gates(cfg)
+    td = torch.bfloat16
+    q, k, v, b, dO = (to_dev(inp[f], td) for f in ("q", "k", "v", "beta", "dO"))
+    g = to_dev(gates, torch.float32)
+    o, hT, ws = dn.deltanet_gated_fwd(q, k, v, b, g)
+    dq, dk, dv, db, dg, dh0 = dn.deltanet_gated_bwd(q, k, v, b, g, dO, workspace=ws)
+    torch.cuda.synchronize()
+    got = {"dq": _np(dq), "dk": _np(dk), "dv": _np(dv), "dbeta": _np(db), "dg": _np(dg),
+           "dh0": _np(dh0)}
+    for (bb, h) in [(0, 0), (cfg.B - 1, cfg.H - 1)]:
+        one = {f: inp[f][bb:bb + 1, h:h + 1] for f in inp}
+        r = oracle.gated_bwd(one["q"], one["k"], one["v"], one["beta"],
+                             gates[bb:bb + 1, h:h + 1], one["dO"])
+        ref = dict(zip(("dq", "dk", "dv", "dbeta", "dg", "dh0"), r))
+        compare({kk: vv[bb:bb + 1, h:h + 1] for kk, vv in got.items()}, ref, TOL["bf16"])

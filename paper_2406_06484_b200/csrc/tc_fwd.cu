@@ -50,15 +50,14 @@ constexpr int OFF_V = OFF_K + 2 * TILE;          // V     IL R=64 x 128
 constexpr int OFF_T = OFF_V + TILE;              // T'    IL R=64 x 64
 constexpr int OFF_TU = OFF_T + C * C * 2;        // T''   IL R=64 x 64
 constexpr int OFF_A = OFF_TU + C * C * 2;        // A[2]  IL R=64 x 64
-constexpr int OFF_W = OFF_A + 2 * C * C * 2;     // W^T[2] IL R=128 x 64
+constexpr int OFF_W = OFF_A + 2 * C * C * 2;     // W^T[2] IL R=128 x 64 (outside SEG1: W^T | K slot 2)
 constexpr int OFF_H = OFF_W + 2 * DK * C * 2;    // H^T   IL R=128 x 128
 constexpr int OFF_Z = OFF_H + DV * DK * 2;       // Z^T   IL R=128 x 64  | O staging
 constexpr int OFF_L = OFF_Z + DV * C * 2;        // L -> X fp32 [64][LS]
 // per-chunk vectors [2][beta, s, -, G, gamma, D][64] (G, gamma, D: gated only)
 constexpr int NVEC = 6;
 constexpr int OFF_VEC = OFF_L + C * LS * 4 + 2 * 128 * 4;  // (LX, partial norms) | vectors
-constexpr int OFF_XB = OFF_VEC + 2 * NVEC * C * 4;  // X bf16 IL R=64 x 64 (saved for the bwd)
-constexpr int SMEM_BYTES = OFF_XB + C * C * 2;
+constexpr int SMEM_BYTES = OFF_VEC + 2 * NVEC * C * 4;
 static_assert(SMEM_BYTES <= 232448 - 1024, "shared memory budget");
 static_assert(REC_Z == C * C * 2 && REC_BYTES == C * C * 2 + DV * C * 2, "record");
 
@@ -140,7 +139,12 @@ __global__ void __launch_bounds__(NT, 1)
                   Args a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   // mbarriers (DESIGN.md §4.1 "fwd pipeline")
-  __shared__ uint64_t qk_full[2], v_full[2], bar_full[2], bar_empty[2];
+  // Q double-buffered by chunk parity; K in NKB slots (3 outside SEG1: the
+  // third slot is W^T's second buffer, W^T then being single-buffered), so
+  // K of chunk c+3 loads when chunk c's chain ends and Q of chunk c+2 as
+  // soon as O = Q H has read Q (q_done): the next Grams never wait on HBM
+  constexpr int NKB = SEG1 ? 2 : 3;
+  __shared__ uint64_t q_full[2], k_full[3], v_full[2], bar_full[2], bar_empty[2], q_done;
   __shared__ uint64_t g_done, g_free, t_ready, w_done, wu_done, w_free;  // prep side
   __shared__ uint64_t up_done, z_free, z_ready, ho_done, h_ready, st_free;  // state side
   __shared__ uint32_t tslot;
@@ -162,11 +166,13 @@ __global__ void __launch_bounds__(NT, 1)
   if (warp == 0) tmem_alloc<512>(&tslot);
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&qk_full[b], 1);
+      mbar_init(&q_full[b], 1);
       mbar_init(&v_full[b], 1);
       mbar_init(&bar_full[b], 1);
       mbar_init(&bar_empty[b], 1);
     }
+    for (int b = 0; b < 3; ++b) mbar_init(&k_full[b], 1);
+    mbar_init(&q_done, 1);
     mbar_init(&g_done, 1);
     mbar_init(&g_free, 1);
     mbar_init(&t_ready, 1);
@@ -188,16 +194,17 @@ __global__ void __launch_bounds__(NT, 1)
   cta_sync();
   const uint32_t tm = tslot;
   auto sQ = [&](int b) { return smem + OFF_Q + b * TILE; };
-  auto sK = [&](int b) { return smem + OFF_K + b * TILE; };
+  // K slot b (0..NKB-1); slot 2 is the memory of W^T[1]
+  auto sK = [&](int b) { return b < 2 ? smem + OFF_K + b * TILE : smem + OFF_W + DK * C * 2; };
   auto sA = [&](int b) { return smem + OFF_A + b * C * C * 2; };
-  auto sW = [&](int b) { return smem + OFF_W + (SEG1 ? 1 : b) * DK * C * 2; };
+  auto sW = [&](int) { return smem + OFF_W + (SEG1 ? 1 : 0) * DK * C * 2; };
+  static_assert(TILE == DK * C * 2, "K slot 2 spans W^T[1]");
   auto vec = [&](int b) { return reinterpret_cast<float*>(smem + OFF_VEC) + b * NVEC * C; };
   uint8_t* sV = smem + OFF_V;
   uint8_t* sT = smem + OFF_T;
   uint8_t* sTu = smem + OFF_TU;
   uint8_t* sH = smem + OFF_H;
   uint8_t* sZ = smem + OFF_Z;
-  uint8_t* sXb = smem + OFF_XB;
   uint8_t* recs = (!SEG1 && (a.flags & DELTANET_SAVE_STATES))
                       ? reinterpret_cast<uint8_t*>(a.scratch) +
                             ((size_t)unit * a.NC + cbase) * REC_BYTES
@@ -240,7 +247,6 @@ __global__ void __launch_bounds__(NT, 1)
       }
       TSTAMP(0);
       if (c >= 2) mbar_wait(&bar_empty[b], ((c >> 1) - 1) & 1);  // chain c-2 released b
-      if (tid == 0 && recs) bulk_wait_read0();  // record stores of chunk c-1 read out
       TSTAMP(1);
       if (half == 0 && w < C) vb[w] = bval;
       if (GATED && half == 0 && w < C) {
@@ -370,33 +376,45 @@ __global__ void __launch_bounds__(NT, 1)
         float4 x4[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) x4[q] = *reinterpret_cast<const float4*>(LX + i * LS + j0 + 4 * q);
+        // beta_j, s_j (and gamma_j) of the 16 columns: vector broadcast loads
+        float4 b4[4], s4[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          b4[q] = *reinterpret_cast<const float4*>(vb + j0 + 4 * q);
+          s4[q] = *reinterpret_cast<const float4*>(vb + C + j0 + 4 * q);
+          if (GATED) {
+            const float4 g4 = *reinterpret_cast<const float4*>(vb + 4 * C + j0 + 4 * q);
+            s4[q].x *= g4.x; s4[q].y *= g4.y; s4[q].z *= g4.z; s4[q].w *= g4.w;
+          }
+        }
+        auto el = [](const float4& v, int r) { return r == 0 ? v.x : r == 1 ? v.y : r == 2 ? v.z : v.w; };
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
           float x[8], y[8], xs[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const int j = j0 + g * 8 + e, q = 2 * g + e / 4, r = e % 4;
-            const float xv = r == 0 ? x4[q].x : r == 1 ? x4[q].y : r == 2 ? x4[q].z : x4[q].w;
-            const float xm = (j <= i) ? xv : 0.f;
+            const float xm = (j <= i) ? el(x4[q], r) : 0.f;
             xs[e] = xm;
-            y[e] = xm * vb[j];  // vb[j]: broadcast across lanes
-            x[e] = y[e] * vb[C + j];
-            if (GATED) x[e] *= vb[4 * C + j];  // W = X diag(beta gamma) K_hat
+            y[e] = xm * el(b4[q], r);
+            x[e] = y[e] * el(s4[q], r);  // gated: W = X diag(beta gamma) K_hat
           }
           il_store8(sT, C, i, j0 + g * 8, x);
           il_store8(sTu, C, i, j0 + g * 8, y);
-          if (recs) il_store8(sXb, C, i, j0 + g * 8, xs);
+          if (recs) {  // the X record, straight from registers (IL image, 16 B per row)
+            uint4 u;
+            u.x = pack_bf16(xs[0], xs[1]);
+            u.y = pack_bf16(xs[2], xs[3]);
+            u.z = pack_bf16(xs[4], xs[5]);
+            u.w = pack_bf16(xs[6], xs[7]);
+            *reinterpret_cast<uint4*>(recs + (size_t)c * REC_BYTES + REC_X +
+                                      il_off(i, j0 + g * 8, C)) = u;
+          }
         }
       }
       fence_proxy_async();
       grp_sync<NP>(BAR_P);
-      if (tid == 0) {
-        mbar_arrive(&t_ready);
-        if (recs) {
-          bulk_store(recs + (size_t)c * REC_BYTES + REC_X, sXb, C * C * 2);
-          bulk_commit();
-        }
-      }
+      if (tid == 0) mbar_arrive(&t_ready);
       TSTAMP(6);
       TSTAMP(7);
       TSTAMP(8);
@@ -652,9 +670,12 @@ __global__ void __launch_bounds__(NT, 1)
     // =====================================================================
     if (lane == 0) {
       for (int c = 0; c < 2 && c < NC; ++c) {
-        mbar_expect_tx(&qk_full[c], 2 * TILE);
-        tma_load_4d(sQ(c), &mQ, 0, T0 + c * C, 0, unit, &qk_full[c]);
-        tma_load_4d(sK(c), &mK, 0, T0 + c * C, 0, unit, &qk_full[c]);
+        mbar_expect_tx(&q_full[c], TILE);
+        tma_load_4d(sQ(c), &mQ, 0, T0 + c * C, 0, unit, &q_full[c]);
+      }
+      for (int c = 0; c < NKB && c < NC; ++c) {
+        mbar_expect_tx(&k_full[c], TILE);
+        tma_load_4d(sK(c), &mK, 0, T0 + c * C, 0, unit, &k_full[c]);
       }
       mbar_expect_tx(&v_full[0], TILE);
       tma_load_4d(sV, &mV, 0, T0, 0, unit, &v_full[0]);
@@ -663,8 +684,9 @@ __global__ void __launch_bounds__(NT, 1)
       const uint32_t at = smem_u32(sT), atu = smem_u32(sTu), av = smem_u32(sV);
       auto gram = [&](int c) {  // G_qk -> lanes 0-15, G_kk -> lanes 16-31 of each quadrant
         const int b = c & 1;
-        const uint32_t aq = smem_u32(sQ(b)), ak = smem_u32(sK(b));
-        mbar_wait(&qk_full[b], (c >> 1) & 1);
+        const uint32_t aq = smem_u32(sQ(b)), ak = smem_u32(sK(c % NKB));
+        mbar_wait(&q_full[b], (c >> 1) & 1);
+        mbar_wait(&k_full[c % NKB], (c / NKB) & 1);
         fence_after_sync();
 #pragma unroll
         for (int k0 = 0; k0 < DK; k0 += 16) {
@@ -677,7 +699,7 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll 1
       for (int c = 0; c < NC; ++c) {
         const int b = c & 1;
-        const uint32_t ak = smem_u32(sK(b));
+        const uint32_t ak = smem_u32(sK(c % NKB));
         // the next chunk's Gram as soon as the prep has read this chunk's and
         // q/k of chunk c+1 have landed (it then runs under this chunk's
         // substitution) -- but never ahead of this chunk's W/U products: if
@@ -685,7 +707,8 @@ __global__ void __launch_bounds__(NT, 1)
         bool gram_pending = c + 1 < NC;
         if (gram_pending) mbar_wait(&g_free, c & 1);
         while (true) {
-          if (gram_pending && mbar_test(&qk_full[(c + 1) & 1], ((c + 1) >> 1) & 1)) {
+          if (gram_pending && mbar_test(&q_full[(c + 1) & 1], ((c + 1) >> 1) & 1) &&
+              mbar_test(&k_full[(c + 1) % NKB], ((c + 1) / NKB) & 1)) {
             gram(c + 1);
             gram_pending = false;
           }
@@ -737,7 +760,7 @@ __global__ void __launch_bounds__(NT, 1)
       for (int c = 0; c < NC; ++c) {
         const int b = c & 1;
         const uint32_t aw = smem_u32(sW(b)), aq = smem_u32(sQ(b)), aa = smem_u32(sA(b)),
-                       ak = smem_u32(sK(b));
+                       ak = smem_u32(sK(c % NKB));
         mbar_wait(&bar_full[b], (c >> 1) & 1);
         mbar_wait(&h_ready, c & 1);  // sH = bf16 image of H_c; sO = O of chunk c-1
         if (c >= 1 && o_out) {
@@ -764,11 +787,17 @@ __global__ void __launch_bounds__(NT, 1)
           for (int k0 = 0; k0 < DK; k0 += 16)
             mma_bf16(tm + TM_O, desc_k(aq, C, k0), desc_k(aH, DV, k0), ido, k0 > 0);
         }
+        mma_commit(&q_done);  // Q[b] read (the state warpgroup's norms precede bar_full)
         // the O store of chunk c-1 must finish reading sO (= sZ) before Z is written
         asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(1) : "memory");
         if (!states) bulk_wait_read0();
         mbar_arrive(&z_free);
         mbar_wait(&z_ready, c & 1);
+        mbar_wait(&q_done, c & 1);
+        if (c + 2 < NC) {  // Q of chunk c+2 into the slot O = Q H has released
+          mbar_expect_tx(&q_full[b], TILE);
+          tma_load_4d(sQ(b), &mQ, 0, T0 + (c + 2) * C, 0, unit, &q_full[b]);
+        }
         fence_after_sync();
         if (states) {  // Z^T of this chunk for the backward (read out before st_free)
           bulk_store(reinterpret_cast<uint8_t*>(a.scratch) + ((size_t)unit * a.NC + cbase + c) * REC_BYTES +
@@ -798,11 +827,11 @@ __global__ void __launch_bounds__(NT, 1)
         }
         mma_commit(&ho_done);
         mbar_wait(&ho_done, c & 1);
-        mbar_arrive(&bar_empty[b]);  // Q/K/A/W[b], vec[b] and U[b] are free for chunk c+2
-        if (c + 2 < NC) {
-          mbar_expect_tx(&qk_full[b], 2 * TILE);
-          tma_load_4d(sQ(b), &mQ, 0, T0 + (c + 2) * C, 0, unit, &qk_full[b]);
-          tma_load_4d(sK(b), &mK, 0, T0 + (c + 2) * C, 0, unit, &qk_full[b]);
+        mbar_arrive(&bar_empty[b]);  // A[b], vec[b] and U[b] are free for chunk c+2
+        if (c + NKB < NC) {  // K of chunk c+NKB into this chunk's K slot
+          const int ks = c % NKB;
+          mbar_expect_tx(&k_full[ks], TILE);
+          tma_load_4d(sK(ks), &mK, 0, T0 + (c + NKB) * C, 0, unit, &k_full[ks]);
         }
         bulk_wait_read0();  // state save done reading sH
         mbar_arrive(&st_free);

@@ -649,7 +649,7 @@ __global__ void __launch_bounds__(NT, 1)
       uint8_t* sK = smem + OFF_K + ks * TILE;
       uint8_t* sQ = qu(ks);         // q -> q_hat -> dq staging
       uint8_t* sDUP = qu(ks ^ 1);   // dU'^T
-      float qkg[16];                // gated: Gamma . Q_hat K_hat^T of P2 (used in P6)
+      uint32_t qkg[8];              // gated: Gamma . Q_hat K_hat^T of P2 (bf16 pairs, for P6)
 
       // ================= P1: k norms ; U' ; R = V - diag(s) K H ; q norms
       BSTAMP(0);
@@ -774,7 +774,12 @@ __global__ void __launch_bounds__(NT, 1)
             float v = lo ? f[g * 8 + e] : x[g * 8 + e];
             if (GATED) v *= gamma_ij(gG, r64, j);  // Gamma . A_m
             a8[e] = (j <= r64) ? ri * v : 0.f;
-            if (GATED) qkg[g * 8 + e] = a8[e] * ss[j];  // Gamma . Q_hat K_hat^T (T1 of P6)
+          }
+          if (GATED) {  // Gamma . Q_hat K_hat^T of this lane's 16 columns (T1 of P6)
+#pragma unroll
+            for (int e = 0; e < 8; e += 2)
+              qkg[g * 4 + e / 2] = pack_bf16(a8[e] * ss[c0 + g * 8 + e],
+                                             a8[e + 1] * ss[c0 + g * 8 + e + 1]);
           }
           il_store8(sA, C, r64, c0 + g * 8, a8);
         }
@@ -871,6 +876,7 @@ __global__ void __launch_bounds__(NT, 1)
           }
           tmem_st_wait();
         }
+        BSTAMP(31);
         {
           // lanes < 16: columns [0,64), lanes >= 16: [64,128) of row r64, for
           // both P (TM_P) and K H (TM_KH); 32 of each half per warpgroup
@@ -974,12 +980,28 @@ __global__ void __launch_bounds__(NT, 1)
       {
         float f[32];
         ld32(tm, wwarp, TM_DA + 32 * wg, f);  // lanes<16: dA row, lanes>=16: Y row
-        // gated: dS = Gamma . dA, and T1 = dS . (Gamma . Q_hat K_hat^T) with the
-        // partner lane's 16 P2 values (columns 32 wg + 16..31 of row r64)
-        float qk2[16], t1[32];
+        // gated: T1 = dS . Q_hat K_hat^T = dA . qkg (P2).  Lane pairs split the
+        // row's 32 columns as in P2 (lo: first 16, hi: last 16; the hi lane
+        // takes its dA values from the lo lane), so every lane sums 16 values.
         if (GATED) {
+          float t1[16];
+          const int cb = 32 * wg + (lo ? 0 : 16);
 #pragma unroll
-          for (int e = 0; e < 16; ++e) qk2[e] = __shfl_xor_sync(0xffffffffu, qkg[e], 16);
+          for (int e = 0; e < 16; ++e) {
+            const float dap = __shfl_xor_sync(0xffffffffu, f[16 + e], 16);
+            const float da = lo ? f[e] : dap;
+            const uint32_t u = qkg[e / 2];
+            const float qv = __uint_as_float((e & 1) ? (u & 0xffff0000u) : (u << 16));
+            t1[e] = (cb + e <= r64) ? da * qv : 0.f;
+          }
+          float rt = 0.f;
+#pragma unroll
+          for (int e = 0; e < 16; ++e) rt += t1[e];
+          rt += __shfl_xor_sync(0xffffffffu, rt, 16);
+          if (lo) rowT1[wg * C + r64] = rt;
+          // this warp's 16 rows summed per column: lane gets column cb + (lane & 15)
+          const float cs = reduce_scatter<16>(t1, lane);
+          colT1[wwarp * C + cb + (lane & 15)] = cs;
         }
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
@@ -988,23 +1010,16 @@ __global__ void __launch_bounds__(NT, 1)
           for (int e = 0; e < 8; ++e) {
             const int j = 32 * wg + g * 8 + e;
             float v = f[g * 8 + e];
-            if (GATED && lo) v *= gamma_ij(gG, r64, j);
-            x[e] = (!lo || j <= r64) ? v : 0.f;
-            if (GATED) {
-              const float qv = (g * 8 + e < 16) ? qkg[(g * 8 + e) & 15] : qk2[(g * 8 + e) & 15];
-              // T1 = dS . QK = dA . (Gamma . QK): the unscaled dA times qkg
-              t1[g * 8 + e] = (lo && j <= r64) ? f[g * 8 + e] * qv : 0.f;
+            if (GATED) {  // dS = Gamma . dA (branch-free: Y rows keep their value)
+              const float gm = gamma_ij(gG, r64, j);
+              v *= lo ? gm : 1.f;
             }
+            x[e] = (!lo || j <= r64) ? v : 0.f;
           }
           il_store8(lo ? sDA : sY, C, r64, 32 * wg + g * 8, x);
         }
-        if (GATED) {  // T1 row sums (lanes < 16), then this warp's 16 rows per column
-          float rt = 0.f;
-#pragma unroll
-          for (int e = 0; e < 32; ++e) rt += t1[e];
-          if (lo) rowT1[wg * C + r64] = rt;
-          const float cs = reduce_scatter<32>(t1, lane);
-          colT1[wwarp * C + 32 * wg + lane] = cs;
+        BSTAMP(28);
+        if (GATED) {
           // dO <- diag(gamma) dO in place (dA has read it: MB_A): thread = row
           // tid & 63, column quarter tid >> 6
           const int row = tid & 63, qt = tid >> 6;

@@ -85,14 +85,30 @@ def test_bwd_timeline(timlib):
     buf = torch.zeros(NC * 32 + B * cfg.H * 4, dtype=torch.int64, device="cuda")
     lib.dn_timing_set_bwd.argtypes = [ctypes.c_void_p]
     assert lib.dn_timing_set_bwd(buf.data_ptr()) == 0
-    d = dn.make_desc(B, cfg.H, cfg.L, 128, 128, 64, td)
+    gated = os.environ.get("DN_TIMING_GATED") == "1"  # the gated backward
+    d = dn.make_desc(B, cfg.H, cfg.L, 128, 128, 64, td, gated=gated)
     ws = torch.empty(dn.deltanet_workspace_bytes(d), dtype=torch.uint8, device="cuda")
     o = torch.empty_like(v)
     g = [torch.empty_like(t) for t in (q, k, v, b)]
+    gate = -0.05 * torch.nn.functional.softplus(torch.randn(b.shape, device="cuda"))
+    dgate = torch.empty_like(gate)
     P = ctypes.c_void_p
     lib.deltanet_fwd.argtypes = [P] * 9 + [ctypes.c_size_t, P]
     lib.deltanet_bwd.argtypes = [P] * 14 + [ctypes.c_size_t, P]
+    lib.deltanet_gated_fwd.argtypes = [P] * 10 + [ctypes.c_size_t, P]
+    lib.deltanet_gated_bwd.argtypes = [P] * 16 + [ctypes.c_size_t, P]
     for _ in range(2):
+        if gated:
+            assert lib.deltanet_gated_fwd(ctypes.addressof(d), q.data_ptr(), k.data_ptr(),
+                                          v.data_ptr(), b.data_ptr(), gate.data_ptr(), None,
+                                          o.data_ptr(), None, ws.data_ptr(), ws.numel(),
+                                          None) == 0
+            assert lib.deltanet_gated_bwd(ctypes.addressof(d), q.data_ptr(), k.data_ptr(),
+                                          v.data_ptr(), b.data_ptr(), gate.data_ptr(), None,
+                                          dO.data_ptr(), None, g[0].data_ptr(), g[1].data_ptr(),
+                                          g[2].data_ptr(), g[3].data_ptr(), dgate.data_ptr(),
+                                          None, ws.data_ptr(), ws.numel(), None) == 0
+            continue
         assert lib.deltanet_fwd(ctypes.addressof(d), q.data_ptr(), k.data_ptr(), v.data_ptr(),
                                 b.data_ptr(), None, o.data_ptr(), None, ws.data_ptr(),
                                 ws.numel(), None) == 0
@@ -128,4 +144,8 @@ def test_bwd_timeline(timlib):
     for s_ in range(16, 28):
         dt = t[2:-2, s_] - t[2:-2, 0]
         rows.append(f"{inames[s_]:28s} {dt.mean():9.0f} cycles after chunk start")
+    if gated:  # sub-phase stamps of the gated path
+        for s_, a_, nm in ((31, 7, "P5 gated DD + D rescale"), (28, 10, "P6 T1 sums + dS"),
+                           (11, 28, "P6 dO scale + signal")):
+            rows.append(f"{nm:28s} {(t[2:-2, s_] - t[2:-2, a_]).mean():9.0f} cycles")
     print("\n" + "\n".join(rows))

@@ -228,3 +228,33 @@ def test_bf16_gated_backward_full_size_sampled_units():
                              gates[bb:bb + 1, h:h + 1], one["dO"])
         ref = dict(zip(("dq", "dk", "dv", "dbeta", "dg", "dh0"), r))
         compare({kk: vv[bb:bb + 1, h:h + 1] for kk, vv in got.items()}, ref, TOL["bf16"])
+
+
+@pytest.mark.parametrize("L", [1, 63, 65, 128])
+def test_bf16_tcgen05_backward_edge_lengths(L):
+    """tcgen05 gated backward at a single token, one partial chunk, one
+    chunk plus one token and exactly two chunks (the chunk-end gate terms
+    and the dH rescale at every boundary), from nonzero h0 and dhT."""
+    inp = _case(1, 2, L, 128, 128, 64, "bf16", index=910 + L, scale=1.0)
+    rng = np.random.default_rng(100 + L)
+    h0 = 0.3 * rng.standard_normal((1, 2, 128, 128))
+    dhT = 0.3 * rng.standard_normal((1, 2, 128, 128))
+    compare(_gpu(inp, "bf16", 64, h0=h0, dhT=dhT), _ref(inp, h0=h0, dhT=dhT), TOL["bf16"])
+
+
+def test_bf16_tcgen05_backward_zero_gate_matches_ungated():
+    """g = 0: the gated tcgen05 backward reduces to the ungated one (every
+    gate factor is exactly 1); same inputs, gradients equal to bf16 output
+    rounding, and dg is the exact derivative at g = 0 (oracle)."""
+    import paper_2406_06484_b200 as dn
+    inp = _case(2, 2, 300, 128, 128, 64, "bf16", index=930)
+    inp["g"] = np.zeros_like(inp["g"])
+    got = _gpu(inp, "bf16", 64)
+    td = torch.bfloat16
+    q, k, v, b, dO = (to_dev(inp[f], td) for f in ("q", "k", "v", "beta", "dO"))
+    o, hT, ws = dn.deltanet_fwd(q, k, v, b)
+    dq, dk, dv, db, dh0 = dn.deltanet_bwd(q, k, v, b, dO, workspace=ws)
+    torch.cuda.synchronize()
+    ung = {"dq": _np(dq), "dk": _np(dk), "dv": _np(dv), "dbeta": _np(db), "dh0": _np(dh0)}
+    compare({kk: got[kk] for kk in ung}, ung, 1e-2)
+    compare({"dg": got["dg"]}, {"dg": _ref(inp)["dg"]}, TOL["bf16"])

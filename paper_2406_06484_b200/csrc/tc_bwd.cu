@@ -62,13 +62,14 @@ constexpr int OFF_R = OFF_Z + TILE;         // R -> Y [0,8K) + G1 [8K,16K)
 // of chunk c in one, dU'^T of chunk c then q of chunk c-1 in the other
 constexpr int OFF_QU1 = OFF_R + TILE;
 constexpr int OFF_A = OFF_QU1 + TILE;       // A_m -> dX -> dA
-constexpr int OFF_VEC = OFF_A + C * C * 2;  // beta, r, s, nq, nk, db1[2], db2[2], dot[2], dotq[2], n2[4]
+constexpr int OFF_VEC = OFF_A + C * C * 2;  // beta, r, s, nq, nk, db1[2], db2[2], dot[2], dotq[2], (4 spare)
 // gated: gate vectors of the chunk and the dl/dG partials
 constexpr int OFF_GV = OFF_VEC + 17 * C * 4;  // gG, gam, gD [64] each
 // colT1[4][64] colT2[4][64] pkh[2][64] DD[2][64] rowT1[2][64] tq[2][64] dG[64] hdot[8] gCn
 constexpr int OFF_GP = OFF_GV + 3 * C * 4;
 constexpr int GP_FLOATS = 4 * C + 4 * C + 2 * C + 2 * C + 2 * C + 2 * C + C + 8 + 8;
-constexpr int SMEM_BYTES = OFF_GP + GP_FLOATS * 4;
+constexpr int OFF_N = OFF_GP + GP_FLOATS * 4;  // record row norms [||k|| | ||q||] fp32
+constexpr int SMEM_BYTES = OFF_N + 2 * C * 4;
 static_assert(SMEM_BYTES <= 232448 - 1024, "shared memory budget");
 
 // ---- TMEM column map (512 columns)
@@ -225,7 +226,6 @@ __global__ void __launch_bounds__(NT, 1)
   float* db2 = db1 + 2 * C;    // [2][64] rowsum(G . K K^T) partials
   float* sdot = db2 + 2 * C;   // [2][64] dk-adjoint dot partials
   float* sdotq = sdot + 2 * C; // [2][64] dq-adjoint dot partials
-  float* n2 = sdotq + 2 * C;   // [4][64] squared-norm partials (column quarters)
   // gated only
   float* gG = reinterpret_cast<float*>(smem + OFF_GV);  // in-chunk cumulative log-gate
   float* gam = gG + C;         // e^G
@@ -288,8 +288,8 @@ __global__ void __launch_bounds__(NT, 1)
     // =====================================================================
     if (lane == 0) {
       // SEG1 reads only dO and X besides q, k
-      constexpr uint32_t MAIN_BYTES =
-          SEG1 ? TILE + C * C * 2 : 3 * TILE + D * D * 2 + C * C * 2;  // dO V Z | H | X
+      constexpr uint32_t MAIN_BYTES = 2 * C * 4 +  // the record's row norms
+          (SEG1 ? TILE + C * C * 2 : 3 * TILE + D * D * 2 + C * C * 2);  // dO V Z | H | X
       auto load_k = [&](int c, int slot) {  // own barrier per slot (one phase per use)
         mbar_expect_tx(&mb[MB_KL0 + slot], TILE);
         tma_load_4d(smem + OFF_K + slot * TILE, &mK, 0, T0 + c * C, 0, unit, &mb[MB_KL0 + slot]);
@@ -297,6 +297,7 @@ __global__ void __launch_bounds__(NT, 1)
       auto load_rest = [&](int c) {  // dO, V, H_t, Z^T (opens the MB_MAIN phase, X included)
         mbar_expect_tx(&mb[MB_MAIN], MAIN_BYTES);
         tma_load_4d(sDO, &mDO, 0, T0 + c * C, 0, unit, &mb[MB_MAIN]);
+        bulk_load(smem + OFF_N, recs + (size_t)c * REC_BYTES + REC_N, 2 * C * 4, &mb[MB_MAIN]);
         if (!SEG1) {
           tma_load_4d(sV, &mV, 0, T0 + c * C, 0, unit, &mb[MB_MAIN]);
           bulk_load(sH, states + (size_t)c * D * D * 2, D * D * 2, &mb[MB_MAIN]);
@@ -670,35 +671,19 @@ __global__ void __launch_bounds__(NT, 1)
         ga = gload(c - 1, lane);  // next chunk processed (summed in P3)
         gb = gload(c - 1, 32 + lane);
       }
-      // squared row norms of a raw 64x128 tile: thread = (row w & 63, column
-      // quarter wg * 2 + (w >> 6)), combined through n2
-      auto row_norms = [&](const uint8_t* tile, float* inv_out, float* n_out) {
-        const int row = w & 63, qt = wg * 2 + (w >> 6);
-        float acc0 = 0.f, acc1 = 0.f;
-#pragma unroll
-        for (int g = 4 * qt; g < 4 * qt + 4; ++g) {
-          float x[8];
-          il_load8(tile, C, row, g * 8, x);
-#pragma unroll
-          for (int e = 0; e < 8; e += 2) {
-            acc0 = fmaf(x[e], x[e], acc0);
-            acc1 = fmaf(x[e + 1], x[e + 1], acc1);
-          }
-        }
-        n2[qt * C + row] = acc0 + acc1;
-        grp_sync<256>(BAR_SIMT);
-        if (tid < C) {
-          const float n = sqrtf((n2[tid] + n2[C + tid]) + (n2[2 * C + tid] + n2[3 * C + tid]));
-          float inv = l2 ? 1.f / fmaxf(n, eps) : 1.f;
-          if (t0 + tid >= L) inv = 0.f;
-          inv_out[tid] = inv;
-          n_out[tid] = n;
-        }
-        grp_sync<256>(BAR_SIMT);
-      };
       mbar_wait(&mb[MB_KL0 + ks], (it >> 1) & 1);
       mbar_wait(&mb[MB_MAIN], ph);
-      row_norms(sK, ss, nk);
+      // row norms of k and q from the forward's record (REC_N): s, r and the
+      // norms the L2 adjoint needs, no pass over the tiles
+      if (tid < 2 * C) {
+        const int row = tid & (C - 1);
+        const float n = reinterpret_cast<const float*>(smem + OFF_N)[tid];
+        float inv = l2 ? 1.f / fmaxf(n, eps) : 1.f;
+        if (t0 + row >= L) inv = 0.f;
+        (tid < C ? ss : sr)[row] = inv;
+        (tid < C ? nk : nq)[row] = n;
+      }
+      grp_sync<256>(BAR_SIMT);
       BSTAMP(1);
       if (GATED) {  // <dH image (dl/dH_{t+1}), H_t>: both bf16 IL R=128 images
         float hd = 0.f;
@@ -751,7 +736,6 @@ __global__ void __launch_bounds__(NT, 1)
       }
       mbar_wait(&mb[MB_QL], ph);
       BSTAMP(3);
-      row_norms(sQ, sr, nq);
 
       // ================= P2: A_m = tril(diag(r) Q K^T) -> bf16 (lanes < 16)
       mbar_wait(&mb[MB_G], ph);

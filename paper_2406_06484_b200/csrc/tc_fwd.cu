@@ -59,7 +59,8 @@ constexpr int NVEC = 6;
 constexpr int OFF_VEC = OFF_L + C * LS * 4 + 2 * 128 * 4;  // (LX, partial norms) | vectors
 constexpr int SMEM_BYTES = OFF_VEC + 2 * NVEC * C * 4;
 static_assert(SMEM_BYTES <= 232448 - 1024, "shared memory budget");
-static_assert(REC_Z == C * C * 2 && REC_BYTES == C * C * 2 + DV * C * 2, "record");
+static_assert(REC_Z == C * C * 2 && REC_N == C * C * 2 + DV * C * 2 &&
+                  REC_BYTES == REC_N + 2 * C * 4, "record");
 
 // TMEM column map (512 columns)
 constexpr uint32_t LO16 = 16u << 16;
@@ -287,9 +288,12 @@ __global__ void __launch_bounds__(NT, 1)
           const int k = i - h;
 #pragma unroll
           for (int e = 0; e < 32; ++e) d = fmaf(f[e], (e == k) ? 1.f : 0.f, d);
-          float inv = l2 ? 1.f / fmaxf(sqrtf(d), a.eps) : 1.f;
+          const float nrm = sqrtf(d);
+          float inv = l2 ? 1.f / fmaxf(nrm, a.eps) : 1.f;
           if (t0 + i >= L) inv = 0.f;  // padded token: exact zero contribution
           vb[C + i] = inv;
+          // ||k_i|| for the backward's record (it then needs no norm pass)
+          if (recs) reinterpret_cast<float*>(recs + (size_t)c * REC_BYTES + REC_N)[i] = nrm;
         }
         TSTAMP(21);
         grp_sync<NP>(BAR_P);  // beta, s (and G) visible
@@ -508,8 +512,11 @@ __global__ void __launch_bounds__(NT, 1)
         }
         wg_sync(BAR_S);
         const int i = wwarp * 16 + (lane & 15);
-        ri = l2 ? 1.f / fmaxf(sqrtf(qn2[i] + qn2[C + i]), a.eps) : 1.f;
+        const float nrm = sqrtf(qn2[i] + qn2[C + i]);
+        ri = l2 ? 1.f / fmaxf(nrm, a.eps) : 1.f;
         if (c * C + i >= L) ri = 0.f;
+        if (recs && lane < 16)  // ||q_i|| for the backward's record
+          reinterpret_cast<float*>(recs + (size_t)c * REC_BYTES + REC_N)[C + i] = nrm;
         DBG(if (lane < 16) dn_dbg[D_R + i] = ri);
       };
       if (GATED) norms();

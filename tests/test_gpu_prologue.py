@@ -83,3 +83,16 @@ def test_deterministic():
     b = _gpu(args, g, "bf16", False)
     for x, y in zip(a[0] + a[1], b[0] + b[1]):
         assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("silu_v", [False, True])
+def test_bf16_tma_tiles(silu_v):
+    """bf16 D = 128 (the TMA-staged kernels): several 1024-token tiles, so
+    the conv window and the dx look-ahead cross tile and stage boundaries,
+    a ragged last tile, and the deterministic dw reduction over tiles."""
+    args, g = _case(2, 2 * 1024 + 77, 3, 128, 128, "bf16", seed=31 + silu_v)
+    fo, bo = _gpu(args, g, "bf16", silu_v)
+    rf = P.prologue_fwd(*args, silu_v=silu_v)
+    rb = P.prologue_bwd(*args, *g, silu_v=silu_v)
+    compare(dict(zip(FWD, fo)), dict(zip(FWD, rf)), TOL["bf16"])
+    compare(dict(zip(BWD, bo)), dict(zip(BWD, rb)), TOL["bf16"])

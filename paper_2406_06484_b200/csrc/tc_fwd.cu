@@ -1033,11 +1033,11 @@ bool tc_supported(const deltanet_desc* d) {
   return d->dtype == DELTANET_BF16 && d->chunk == C && d->Dk == DK && d->Dv == DV && d->L > 0;
 }
 
-// gated DeltaNet (R23) on the tcgen05 kernels: the forward (the gated
-// backward runs on the SIMT path)
+// gated DeltaNet (R23) on the tcgen05 kernels, forward and backward
+//
 bool tc_gated_supported(const deltanet_desc*) { return true; }
 
-// per-chunk records [X | W^T | Z^T] the backward reads (40 KB per chunk per unit)
+// per-chunk records [X | Z^T | row norms] the backward reads (tc_common.cuh REC_*)
 namespace {
 int sm_count() {
   static int n = 0;

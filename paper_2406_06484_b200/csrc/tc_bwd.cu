@@ -84,7 +84,8 @@ constexpr uint32_t TM_KH = 448;                          // (K H)[:, :64] | [:, 
 
 enum { BAR_SIMT = 1 };
 // issuer -> SIMT: MMA commits and TMA arrivals
-enum { MB_G, MB_R, MB_DU, MB_P, MB_DH, MB_A, MB_LD, MB_GB, MB_K, MB_MAIN, MB_QL, MB_KL0, MB_KL1, MB_N };
+enum { MB_G, MB_R, MB_DU, MB_P, MB_DH, MB_A, MB_LD, MB_GB, MB_K, MB_MAIN, MB_QL, MB_KL0, MB_KL1, MB_DHK,
+       MB_N };
 // SIMT -> issuer hand-offs (SG_STG: issuer -> SIMT, staging regions free)
 enum { SG_DHI, SG_A, SG_P3, SG_P5, SG_P6, SG_P7, SG_P8, SG_STG, SG_N };
 
@@ -391,10 +392,8 @@ __global__ void __launch_bounds__(NT, 1)
         ISTAMP(16);
         {
           const uint32_t idg = idesc_bf16(64, 64, false, false);
-          const uint32_t idd = idesc_bf16(128, 64, false, false);
-#pragma unroll
-          for (int k0 = 0; k0 < D; k0 += 16)
-            mma_bf16(tm + TM_DU, desc_k(aDH, D, k0), desc_k(aK, C, k0), idd, k0 > 0);
+          // K H first (the SIMT warps wait on it for R); dH^T K^T is first
+          // needed by P3 and goes after Q K^T (M1b)
           if (!SEG1) {
 #pragma unroll
             for (int k0 = 0; k0 < D; k0 += 16) {
@@ -417,6 +416,13 @@ __global__ void __launch_bounds__(NT, 1)
           for (int k0 = 0; k0 < D; k0 += 16)
             mma_bf16(tm + TM_G, desc_k(aQ, C, k0), desc_k(aK, C, k0), idg, k0 > 0);
           mma_commit(&mb[MB_G]);
+          // dH^T K^T after the products the SIMT warps wait on (K H, Q K^T);
+          // P3 reads it (M2's MB_DU commit covers it)
+          const uint32_t idd = idesc_bf16(128, 64, false, false);
+#pragma unroll
+          for (int k0 = 0; k0 < D; k0 += 16)
+            mma_bf16(tm + TM_DU, desc_k(aDH, D, k0), desc_k(aK, C, k0), idd, k0 > 0);
+          mma_commit(&mb[MB_DHK]);  // the last reader of the raw k tile (P3 normalises it)
         }
         ISTAMP(19);
 
@@ -771,8 +777,9 @@ __global__ void __launch_bounds__(NT, 1)
       simt_signal(&sg[SG_A], tid);
 
       // ================= P3: q_hat, k_hat in place ; dU' = (..) diag(s) -> bf16
-      if (l2) {  // M1 is done reading raw q, k (MB_G); thread: row w & 63 of q
-        // (wg0) or k (wg1), one column half
+      if (wg == 1) mbar_wait(&mb[MB_DHK], ph);  // dH^T K^T has read the raw k tile
+      if (l2) {  // M1 is done reading raw q, k (MB_G, MB_DHK); thread: row w & 63 of
+        // q (wg0) or k (wg1), one column half
         const int row = w & 63;
         uint8_t* tile = wg == 0 ? sQ : sK;
         const float inv = (wg == 0 ? sr : ss)[row];

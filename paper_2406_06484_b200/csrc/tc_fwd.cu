@@ -284,10 +284,19 @@ __global__ void __launch_bounds__(NT, 1)
         // s_i = 1/max(||k_i||, eps) from the Gram diagonal (fp32 sum of exact
         // bf16 products; R9).  r (for q) is computed by the state warpgroup.
         if (lane >= 16 && (i >> 5) == half) {
-          float d = 0.f;  // f[i - h] as arithmetic (no dynamic register indexing)
+          // d = f[i - h] by a 5-level select tree (no dynamic register
+          // indexing, no 32-step dependent chain)
           const int k = i - h;
+          float t16[16], t8[8], t4[4], t2[2];
 #pragma unroll
-          for (int e = 0; e < 32; ++e) d = fmaf(f[e], (e == k) ? 1.f : 0.f, d);
+          for (int e = 0; e < 16; ++e) t16[e] = (k & 16) ? f[16 + e] : f[e];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) t8[e] = (k & 8) ? t16[8 + e] : t16[e];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) t4[e] = (k & 4) ? t8[4 + e] : t8[e];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) t2[e] = (k & 2) ? t4[2 + e] : t4[e];
+          const float d = (k & 1) ? t2[1] : t2[0];
           const float nrm = sqrtf(d);
           float inv = l2 ? 1.f / fmaxf(nrm, a.eps) : 1.f;
           if (t0 + i >= L) inv = 0.f;  // padded token: exact zero contribution

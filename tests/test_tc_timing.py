@@ -40,15 +40,23 @@ def test_fwd_timeline(timlib):
     buf = torch.zeros(NC * 32, dtype=torch.int64, device="cuda")
     lib.dn_timing_set.argtypes = [ctypes.c_void_p]
     assert lib.dn_timing_set(buf.data_ptr()) == 0
-    d = dn.make_desc(B, cfg.H, cfg.L, 128, 128, 64, td)
+    gated = os.environ.get("DN_TIMING_GATED") == "1"  # the gated forward
+    d = dn.make_desc(B, cfg.H, cfg.L, 128, 128, 64, td, gated=gated)
     ws = torch.empty(dn.deltanet_workspace_bytes(d), dtype=torch.uint8, device="cuda")
     o = torch.empty_like(v)
+    gate = -0.05 * torch.nn.functional.softplus(torch.randn(b.shape, device="cuda"))
     P = ctypes.c_void_p
     lib.deltanet_fwd.argtypes = [P] * 9 + [ctypes.c_size_t, P]
+    lib.deltanet_gated_fwd.argtypes = [P] * 10 + [ctypes.c_size_t, P]
     for _ in range(2):
-        rc = lib.deltanet_fwd(ctypes.addressof(d), q.data_ptr(), k.data_ptr(), v.data_ptr(),
-                              b.data_ptr(), None, o.data_ptr(), None, ws.data_ptr(), ws.numel(),
-                              None)
+        if gated:
+            rc = lib.deltanet_gated_fwd(ctypes.addressof(d), q.data_ptr(), k.data_ptr(),
+                                        v.data_ptr(), b.data_ptr(), gate.data_ptr(), None,
+                                        o.data_ptr(), None, ws.data_ptr(), ws.numel(), None)
+        else:
+            rc = lib.deltanet_fwd(ctypes.addressof(d), q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                  b.data_ptr(), None, o.data_ptr(), None, ws.data_ptr(),
+                                  ws.numel(), None)
         assert rc == 0
     torch.cuda.synchronize()
     t = buf.cpu().numpy().reshape(NC, 32).astype(np.int64)

@@ -84,7 +84,7 @@ constexpr uint32_t TM_KH = 448;                          // (K H)[:, :64] | [:, 
 
 enum { BAR_SIMT = 1 };
 // issuer -> SIMT: MMA commits and TMA arrivals
-enum { MB_G, MB_R, MB_DU, MB_P, MB_DH, MB_A, MB_LD, MB_GB, MB_K, MB_MAIN, MB_QL, MB_KL0, MB_KL1, MB_DHK,
+enum { MB_AL, MB_R, MB_DU, MB_P, MB_DH, MB_A, MB_LD, MB_GB, MB_K, MB_MAIN, MB_QL, MB_KL0, MB_KL1, MB_DHK,
        MB_N };
 // SIMT -> issuer hand-offs (SG_STG: issuer -> SIMT, staging regions free)
 enum { SG_DHI, SG_A, SG_P3, SG_P5, SG_P6, SG_P7, SG_P8, SG_STG, SG_N };
@@ -308,6 +308,10 @@ __global__ void __launch_bounds__(NT, 1)
       auto load_x = [&](int c) {
         bulk_load(sX, recs + (size_t)c * REC_BYTES + REC_X, C * C * 2, &mb[MB_MAIN]);
       };
+      auto load_a = [&](int c) {  // the forward's A into sA (free once M6 / M7 are done)
+        mbar_expect_tx(&mb[MB_AL], C * C * 2);
+        bulk_load(sA, recs + (size_t)c * REC_BYTES + REC_A, C * C * 2, &mb[MB_AL]);
+      };
       auto load_q = [&](int c, int slot) {
         mbar_expect_tx(&mb[MB_QL], TILE);
         tma_load_4d(qu(slot), &mQ, 0, T0 + c * C, 0, unit, &mb[MB_QL]);
@@ -316,6 +320,7 @@ __global__ void __launch_bounds__(NT, 1)
         load_k(NC - 1, 0);
         load_rest(NC - 1);
         load_x(NC - 1);
+        load_a(NC - 1);
         load_q(NC - 1, 0);
       }
       mbar_arrive(&sg[SG_STG]);
@@ -351,6 +356,8 @@ __global__ void __launch_bounds__(NT, 1)
           load_rest(c - 1);
           mbar_wait(&mb[MB_GB], ph);  // X read by G
           load_x(c - 1);
+          mbar_wait(&mb[SEG1 ? MB_GB : MB_K], ph);  // dA (in sA) read by M6 (SEG1: A by M2)
+          load_a(c - 1);
         }
       }
       if (NC > 0) {
@@ -392,8 +399,7 @@ __global__ void __launch_bounds__(NT, 1)
         ISTAMP(16);
         {
           const uint32_t idg = idesc_bf16(64, 64, false, false);
-          // K H first (the SIMT warps wait on it for R); dH^T K^T is first
-          // needed by P3 and goes after Q K^T (M1b)
+          // K H first (the SIMT warps wait on it for R)
           if (!SEG1) {
 #pragma unroll
             for (int k0 = 0; k0 < D; k0 += 16) {
@@ -405,19 +411,10 @@ __global__ void __launch_bounds__(NT, 1)
           mma_commit(&mb[MB_R]);
         }
         ISTAMP(17);
-
-        // M1b: Q K^T (raw)
-        mbar_wait(&mb[MB_QL], ph);
-        fence_after_sync();
         ISTAMP(18);
         {
-          const uint32_t idg = idesc_bf16(64, 64, false, false);
-#pragma unroll
-          for (int k0 = 0; k0 < D; k0 += 16)
-            mma_bf16(tm + TM_G, desc_k(aQ, C, k0), desc_k(aK, C, k0), idg, k0 > 0);
-          mma_commit(&mb[MB_G]);
-          // dH^T K^T after the products the SIMT warps wait on (K H, Q K^T);
-          // P3 reads it (M2's MB_DU commit covers it)
+          // dH^T K^T (P3 reads it after M2's MB_DU).  Q K^T is not formed:
+          // the forward's A comes with the record (load_a).
           const uint32_t idd = idesc_bf16(128, 64, false, false);
 #pragma unroll
           for (int k0 = 0; k0 < D; k0 += 16)
@@ -743,28 +740,19 @@ __global__ void __launch_bounds__(NT, 1)
       mbar_wait(&mb[MB_QL], ph);
       BSTAMP(3);
 
-      // ================= P2: A_m = tril(diag(r) Q K^T) -> bf16 (lanes < 16)
-      mbar_wait(&mb[MB_G], ph);
-      fence_after_sync();
+      // ================= P2: A_m = diag(r) A, A = tril(Q K^T) (gated: Gamma . A)
+      // from the forward's record, scaled in place (thread: row r64, 16 columns)
+      mbar_wait(&mb[MB_AL], ph);
       BSTAMP(4);
       {
-        // lanes < 16 hold the Q K^T row; each lane pair splits its 32 columns
-        float f[32], x[16];
-        ld32(tm, wwarp, TM_G + 32 * wg, f);
-#pragma unroll
-        for (int e = 0; e < 16; ++e) x[e] = __shfl_xor_sync(0xffffffffu, f[16 + e], 16);
         const float ri = sr[r64];
         const int c0 = 32 * wg + (lo ? 0 : 16);
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
           float a8[8];
+          il_load8(sA, C, r64, c0 + g * 8, a8);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int j = c0 + g * 8 + e;
-            float v = lo ? f[g * 8 + e] : x[g * 8 + e];
-            if (GATED) v *= gamma_ij(gG, r64, j);  // Gamma . A_m
-            a8[e] = (j <= r64) ? ri * v : 0.f;
-          }
+          for (int e = 0; e < 8; ++e) a8[e] *= ri;
           if (GATED) {  // Gamma . Q_hat K_hat^T of this lane's 16 columns (T1 of P6)
 #pragma unroll
             for (int e = 0; e < 8; e += 2)
@@ -778,8 +766,8 @@ __global__ void __launch_bounds__(NT, 1)
 
       // ================= P3: q_hat, k_hat in place ; dU' = (..) diag(s) -> bf16
       if (wg == 1) mbar_wait(&mb[MB_DHK], ph);  // dH^T K^T has read the raw k tile
-      if (l2) {  // M1 is done reading raw q, k (MB_G, MB_DHK); thread: row w & 63 of
-        // q (wg0) or k (wg1), one column half
+      if (l2) {  // no MMA reads raw q; dH^T K^T and K H have read raw k (MB_DHK);
+        // thread: row w & 63 of q (wg0) or k (wg1), one column half
         const int row = w & 63;
         uint8_t* tile = wg == 0 ? sQ : sK;
         const float inv = (wg == 0 ? sr : ss)[row];

@@ -30,7 +30,8 @@ namespace tc {
 // uses W^T dU' = K_hat^T diag(beta) X^T dU' = K_hat^T dV.)
 constexpr int REC_X = 0, REC_Z = 64 * 64 * 2;
 constexpr int REC_N = REC_Z + 128 * 64 * 2;  // fp32 row norms [||k|| (64) | ||q|| (64)]
-constexpr int REC_BYTES = REC_N + 2 * 64 * 4;  // 24.5 KB
+constexpr int REC_A = REC_N + 2 * 64 * 4;     // A = tril(Q K^T) (gated: Gamma . A), raw, bf16 IL 64x64
+constexpr int REC_BYTES = REC_A + 64 * 64 * 2;  // 32.5 KB
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);

@@ -60,7 +60,7 @@ constexpr int OFF_VEC = OFF_L + C * LS * 4 + 2 * 128 * 4;  // (LX, partial norms
 constexpr int SMEM_BYTES = OFF_VEC + 2 * NVEC * C * 4;
 static_assert(SMEM_BYTES <= 232448 - 1024, "shared memory budget");
 static_assert(REC_Z == C * C * 2 && REC_N == C * C * 2 + DV * C * 2 &&
-                  REC_BYTES == REC_N + 2 * C * 4, "record");
+                  REC_A == REC_N + 2 * C * 4 && REC_BYTES == REC_A + C * C * 2, "record");
 
 // TMEM column map (512 columns)
 constexpr uint32_t LO16 = 16u << 16;
@@ -343,6 +343,15 @@ __global__ void __launch_bounds__(NT, 1)
               a8[e] = (c0 + g * 8 + e <= i) ? qk : 0.f;
             }
             if (!SEG1) il_store8(sA(b), C, i, c0 + g * 8, a8);
+            if (recs) {  // the backward's A (IL image, 16 B per row segment)
+              uint4 u;
+              u.x = pack_bf16(a8[0], a8[1]);
+              u.y = pack_bf16(a8[2], a8[3]);
+              u.z = pack_bf16(a8[4], a8[5]);
+              u.w = pack_bf16(a8[6], a8[7]);
+              *reinterpret_cast<uint4*>(recs + (size_t)c * REC_BYTES + REC_A +
+                                        il_off(i, c0 + g * 8, C)) = u;
+            }
           }
         }
         {  // L = beta_i s_i s_j (k_i . k_j), j < i

@@ -345,23 +345,26 @@ __global__ void prologue_dw_reduce(ProArgs a) {
 // token rows (256 B each) is loaded two stages ahead, stage -1 being the
 // 3-token window before the tile (zero-filled by TMA before t = 0).  Warp w
 // computes tokens [8w, 8w + 8) of a stage, lane = 4 channels.
-constexpr int ST = 64, NBUF = 4, TILE_T = 1024, DT = 128;
-constexpr int TMA_SMEM = NBUF * ST * DT * 2;  // 64 KB
+constexpr int ST = 64, NBUF = 4, TILE_T = 1024, DT = 128, DHF = DT / 2;
+constexpr int TMA_SMEM = NBUF * ST * DHF * 2;  // 32 KB: several CTAs per SM
 
+// grid (B*H, tiles, 3 tensors x 2 channel halves); lane = 2 channels of the
+// half (128 B rows), warp w = tokens [8w, 8w + 8) of a stage
 __global__ void __launch_bounds__(256) prologue_fwd_tma_kernel(
     const __grid_constant__ CUtensorMap mxq, const __grid_constant__ CUtensorMap mxk,
     const __grid_constant__ CUtensorMap mxv, ProArgs a) {
   extern __shared__ __align__(128) uint8_t sbuf[];
   __shared__ uint64_t full[NBUF];
-  // grid (B*H, tiles, 3): consecutive CTAs are the heads of one batch row and
-  // token tile, so the token rows they share ([B,L,H,D]) are read together
-  const int bh = blockIdx.x, tile = blockIdx.y, z = blockIdx.z;
+  // consecutive CTAs are the heads of one batch row and token tile, so the
+  // token rows they share ([B,L,H,D]) are read together
+  const int bh = blockIdx.x, tile = blockIdx.y, z = blockIdx.z >> 1, half = blockIdx.z & 1;
   const int b = bh / a.H, h = bh % a.H, H = a.H, L = a.L;
   const int t_begin = tile * TILE_T;
   const int nst = (min(TILE_T, L - t_begin) + ST - 1) / ST;
   const CUtensorMap* mx = z == 0 ? &mxq : z == 1 ? &mxk : &mxv;
   const Tz tz = pick(a, z);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int SB = ST * DHF * 2;
   if (tid == 0) {
     for (int i = 0; i < NBUF; ++i) tc::mbar_init(&full[i], 1);
     tc::mbar_fence_init();
@@ -370,24 +373,26 @@ __global__ void __launch_bounds__(256) prologue_fwd_tma_kernel(
   __syncthreads();
   auto issue = [&](int s) {  // stage s -> buffer (s + 1) % NBUF
     uint64_t* bar = &full[(s + 1) % NBUF];
-    tc::mbar_expect_tx(bar, ST * DT * 2);
-    tc::tma_load_4d(sbuf + ((s + 1) % NBUF) * ST * DT * 2, mx, h * DT, t_begin + s * ST, b, 0, bar);
+    tc::mbar_expect_tx(bar, SB);
+    tc::tma_load_4d(sbuf + ((s + 1) % NBUF) * SB, mx, h * DT + half * DHF, t_begin + s * ST, b, 0,
+                    bar);
   };
   if (tid == 0)
     for (int s = -1; s <= 1 && s < nst; ++s) issue(s);
-  const int c = h * DT + 4 * lane;
-  float w[4][4];
+  const int c = h * DT + half * DHF + 2 * lane;
+  float w[2][4];
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
+  for (int e = 0; e < 2; ++e) {
     const float4 w4 = *reinterpret_cast<const float4*>(tz.w + (size_t)(c + e) * 4);
     w[e][0] = w4.x; w[e][1] = w4.y; w[e][2] = w4.z; w[e][3] = w4.w;
   }
-  __nv_bfloat16* y = (__nv_bfloat16*)tz.y + ((size_t)b * H + h) * L * DT + 4 * lane;
-  auto row = [&](int s, int r, float (&x)[4]) {  // row r (may be < 0: previous stage)
+  __nv_bfloat16* y = (__nv_bfloat16*)tz.y + ((size_t)b * H + h) * L * DT + half * DHF + 2 * lane;
+  auto row = [&](int s, int r, float (&x)[2]) {  // row r (may be < 0: previous stage)
     const int bi = (r < 0 ? s : s + 1) % NBUF, rr = r < 0 ? r + ST : r;
-    Raw4<__nv_bfloat16> raw;
-    raw.w = *reinterpret_cast<const uint2*>(sbuf + ((size_t)bi * ST + rr) * DT * 2 + 8 * lane);
-    unpack(raw, x);
+    const float2 f = __bfloat1622float2(
+        *reinterpret_cast<const __nv_bfloat162*>(sbuf + (size_t)bi * SB + rr * DHF * 2 + 4 * lane));
+    x[0] = f.x;
+    x[1] = f.y;
   };
 #pragma unroll 1
   for (int s = 0; s < nst; ++s) {
@@ -395,18 +400,18 @@ __global__ void __launch_bounds__(256) prologue_fwd_tma_kernel(
     tc::mbar_wait(&full[s % NBUF], (s >> 2) & 1);            // stage s - 1 (window)
     tc::mbar_wait(&full[(s + 1) % NBUF], ((s + 1) >> 2) & 1);  // stage s
     const int r0 = 8 * warp;
-    float win[3][4];
+    float win[3][2];
 #pragma unroll
     for (int j = 0; j < 3; ++j) row(s, r0 - 3 + j, win[j]);
-    float xt[8][4];
+    float xt[8][2];
 #pragma unroll
     for (int u = 0; u < 8; ++u) row(s, r0 + u, xt[u]);
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int t = t_begin + s * ST + r0 + u;
-      float o[4];
+      float o[2];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
+      for (int e = 0; e < 2; ++e) {
         const float yy = fmaf(w[e][0], win[0][e],
                               fmaf(w[e][1], win[1][e], fmaf(w[e][2], win[2][e], w[e][3] * xt[u][e])));
         o[e] = tz.silu ? yy * sigm(yy) : yy;
@@ -414,7 +419,8 @@ __global__ void __launch_bounds__(256) prologue_fwd_tma_kernel(
         win[1][e] = win[2][e];
         win[2][e] = xt[u][e];
       }
-      if (t < L) store4(y + (size_t)t * DT, o);
+      if (t < L)
+        *reinterpret_cast<__nv_bfloat162*>(y + (size_t)t * DT) = __floats2bfloat162_rn(o[0], o[1]);
     }
     __syncthreads();  // every warp is done with stage s - 1's buffer
   }
@@ -433,15 +439,18 @@ __global__ void prologue_beta_kernel(ProArgs a) {
   }
 }
 
-// ---- bf16, D = 128 backward, TMA-staged like the forward: stages of STB
-// rows of x (token-major) and dout ([B,H,L,D]) in a ring of NBUF; stage -1
-// is the window before the tile, stage nst the 3-row look-ahead after it.
+// ---- bf16, D = 128 backward, TMA-staged like the forward, on 64-channel
+// halves (a CTA per (b, h, tensor, half, tile); lane = 2 channels, 128 B
+// rows) so that stages stay small (8 KB) and ~6 CTAs share an SM: stages of
+// STB rows of x (token-major) and dout ([B,H,L,D]) in a ring of NBUF; stage
+// -1 is the window before the tile, stage nst the 3-row look-ahead after it.
 // Warp w owns rows [8w, 8w + 8) of a stage: it slides over rows 8w - 3 ..
 // 8w + 10, forming dy = dout act'(y) for rows 8w .. 8w + 10 (3 recomputed
-// by the next warp too) and dx for its own rows; dw partials stay in registers over the tile, then reduce over the
-// warps in a fixed order into part[z][b * ntile + tile] (TILE_T tiles).
-constexpr int STB = 32, NWB = 4, RPW = STB / NWB;  // 4 warps of 8 rows
-constexpr int TMA_SMEM_B = NBUF * 2 * STB * DT * 2;  // 64 KB
+// by the next warp too) and dx for its own rows; dw partials stay in
+// registers over the tile, then reduce over the warps in a fixed order into
+// part[z][b * ntile + tile] (TILE_T tiles).
+constexpr int STB = 32, NWB = 4, RPW = STB / NWB, DH = DT / 2;  // 4 warps of 8 rows, 64 channels
+constexpr int TMA_SMEM_B = NBUF * 2 * STB * DH * 2;  // 32 KB
 
 __global__ void __launch_bounds__(32 * NWB) prologue_bwd_tma_kernel(
     const __grid_constant__ CUtensorMap mxq, const __grid_constant__ CUtensorMap mxk,
@@ -449,7 +458,8 @@ __global__ void __launch_bounds__(32 * NWB) prologue_bwd_tma_kernel(
     const __grid_constant__ CUtensorMap mgk, const __grid_constant__ CUtensorMap mgv, ProArgs a) {
   extern __shared__ __align__(128) uint8_t sbuf[];
   __shared__ uint64_t full[NBUF];
-  const int bh = blockIdx.x, tile = blockIdx.y, z = blockIdx.z;  // as the forward
+  // grid (B*H, tiles, 3 tensors x 2 channel halves)
+  const int bh = blockIdx.x, tile = blockIdx.y, z = blockIdx.z >> 1, half = blockIdx.z & 1;
   const int b = bh / a.H, h = bh % a.H, H = a.H, L = a.L;
   const int t_begin = tile * TILE_T;
   const int nst = (min(TILE_T, L - t_begin) + STB - 1) / STB;
@@ -457,7 +467,7 @@ __global__ void __launch_bounds__(32 * NWB) prologue_bwd_tma_kernel(
   const CUtensorMap* mg = z == 0 ? &mgq : z == 1 ? &mgk : &mgv;
   const Tz tz = pick(a, z);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  constexpr int SB = STB * DT * 2;  // bytes of one tile of a stage
+  constexpr int SB = STB * DH * 2;  // bytes of one tile of a stage
   if (tid == 0) {
     for (int i = 0; i < NBUF; ++i) tc::mbar_init(&full[i], 1);
     tc::mbar_fence_init();
@@ -469,27 +479,28 @@ __global__ void __launch_bounds__(32 * NWB) prologue_bwd_tma_kernel(
   auto issue = [&](int s) {
     uint64_t* bar = &full[(s + 1) % NBUF];
     tc::mbar_expect_tx(bar, 2 * SB);
-    tc::tma_load_4d(buf(s), mx, h * DT, t_begin + s * STB, b, 0, bar);
-    tc::tma_load_4d(buf(s) + SB, mg, 0, t_begin + s * STB, bh, 0, bar);
+    tc::tma_load_4d(buf(s), mx, h * DT + half * DH, t_begin + s * STB, b, 0, bar);
+    tc::tma_load_4d(buf(s) + SB, mg, half * DH, t_begin + s * STB, bh, 0, bar);
   };
   if (tid == 0)
     for (int s = -1; s <= 1 && s <= nst; ++s) issue(s);
-  const int c = h * DT + 4 * lane;
-  float w[4][4], dw[4][4];
+  const int c = h * DT + half * DH + 2 * lane;  // first of this lane's two channels
+  float w[2][4], dw[2][4];
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
+  for (int e = 0; e < 2; ++e) {
     const float4 w4 = *reinterpret_cast<const float4*>(tz.w + (size_t)(c + e) * 4);
     w[e][0] = w4.x; w[e][1] = w4.y; w[e][2] = w4.z; w[e][3] = w4.w;
 #pragma unroll
     for (int j = 0; j < 4; ++j) dw[e][j] = 0.f;
   }
   __nv_bfloat16* dx = (__nv_bfloat16*)tz.dx + (size_t)b * L * H * DT + c;  // token stride H*D
-  auto ld = [&](int s, int r, int part, float (&x)[4]) {  // row r of stage s (r may leave it)
+  auto ld = [&](int s, int r, int part, float (&x)[2]) {  // row r of stage s (r may leave it)
     const int ss = r < 0 ? s - 1 : r >= STB ? s + 1 : s;
     const int rr = r < 0 ? r + STB : r >= STB ? r - STB : r;
-    Raw4<__nv_bfloat16> raw;
-    raw.w = *reinterpret_cast<const uint2*>(buf(ss) + part * SB + rr * DT * 2 + 8 * lane);
-    unpack(raw, x);
+    const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(
+        buf(ss) + part * SB + rr * DH * 2 + 4 * lane));
+    x[0] = f.x;
+    x[1] = f.y;
   };
 #pragma unroll 1
   for (int s = 0; s < nst; ++s) {
@@ -498,16 +509,16 @@ __global__ void __launch_bounds__(32 * NWB) prologue_bwd_tma_kernel(
     tc::mbar_wait(&full[(s + 1) % NBUF], ((s + 1) >> 2) & 1);
     tc::mbar_wait(&full[(s + 2) % NBUF], ((s + 2) >> 2) & 1);
     const int r0 = RPW * warp;
-    float xw[4][4], dyw[3][4];
+    float xw[4][2], dyw[3][2];
 #pragma unroll
     for (int j = 0; j < 3; ++j) ld(s, r0 - 3 + j, 0, xw[j + 1]);
 #pragma unroll
     for (int u = 0; u < RPW + 3; ++u) {  // row r0 + u
-      float xt[4], gt[4], dyt[4];
+      float xt[2], gt[2], dyt[2];
       ld(s, r0 + u, 0, xt);
       ld(s, r0 + u, 1, gt);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
+      for (int e = 0; e < 2; ++e) {
         xw[0][e] = xw[1][e];
         xw[1][e] = xw[2][e];
         xw[2][e] = xw[3][e];
@@ -527,15 +538,16 @@ __global__ void __launch_bounds__(32 * NWB) prologue_bwd_tma_kernel(
       }
       if (u >= 3) {  // dx of own row r0 + u - 3 = w3 dy[.] + w2 dy[+1] + w1 dy[+2] + w0 dy[+3]
         const int t = t_begin + s * STB + r0 + u - 3;
-        float o[4];
+        float o[2];
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
+        for (int e = 0; e < 2; ++e)
           o[e] = fmaf(w[e][3], dyw[0][e],
                       fmaf(w[e][2], dyw[1][e], fmaf(w[e][1], dyw[2][e], w[e][0] * dyt[e])));
-        if (t < L) store4(dx + (size_t)t * H * DT, o);
+        if (t < L)
+          *reinterpret_cast<__nv_bfloat162*>(dx + (size_t)t * H * DT) = __floats2bfloat162_rn(o[0], o[1]);
       }
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
+      for (int e = 0; e < 2; ++e) {
         dyw[0][e] = dyw[1][e];
         dyw[1][e] = dyw[2][e];
         dyw[2][e] = dyt[e];
@@ -544,18 +556,19 @@ __global__ void __launch_bounds__(32 * NWB) prologue_bwd_tma_kernel(
     __syncthreads();  // every warp is done with stage s - 1's buffer
   }
   // dw partial of the tile: warps summed in a fixed order (the ring is free)
-  float* red = reinterpret_cast<float*>(sbuf);  // [NWB warps][32 lanes * 16]
+  float* red = reinterpret_cast<float*>(sbuf);  // [NWB warps][32 lanes * 8]
 #pragma unroll
-  for (int e = 0; e < 4; ++e)
+  for (int e = 0; e < 2; ++e)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) red[warp * 512 + lane * 16 + e * 4 + j] = dw[e][j];
+    for (int j = 0; j < 4; ++j) red[warp * 256 + lane * 8 + e * 4 + j] = dw[e][j];
   __syncthreads();
-  for (int i = tid; i < 512; i += 32 * NWB) {
+  for (int i = tid; i < 256; i += 32 * NWB) {
     float sum = 0.f;
-    for (int r = 0; r < NWB; ++r) sum += red[r * 512 + i];
+    for (int r = 0; r < NWB; ++r) sum += red[r * 256 + i];
     const int Dm = a.Dk > a.Dv ? a.Dk : a.Dv;
     const size_t slot = ((size_t)z * a.B * a.ntile + (size_t)b * a.ntile + tile);
-    a.part[(slot * H * Dm + (size_t)h * DT) * 4 + i] = sum;  // i = channel * 4 + tap
+    // i = (channel within the half) * 4 + tap
+    a.part[(slot * H * Dm + (size_t)h * DT + half * DH) * 4 + i] = sum;
   }
 }
 
@@ -575,13 +588,13 @@ __global__ void prologue_beta_bwd_kernel(ProArgs a) {
 }
 
 // [B*H][L][D] contiguous bf16 (the cotangents dq, dk, dv) viewed as
-// {D, L, B*H, 1}, box {D, STB}
+// {D, L, B*H, 1}, box {D/2, STB} (one channel half)
 bool make_head_map(CUtensorMap* m, const void* base, int BH, int L) {
   auto enc = encode_fn();
   if (!enc) return false;
   cuuint64_t dims[4] = {(cuuint64_t)DT, (cuuint64_t)L, (cuuint64_t)BH, 1};
   cuuint64_t strides[3] = {(cuuint64_t)DT * 2, (cuuint64_t)L * DT * 2, (cuuint64_t)BH * L * DT * 2};
-  cuuint32_t box[4] = {(cuuint32_t)DT, (cuuint32_t)STB, 1, 1};
+  cuuint32_t box[4] = {(cuuint32_t)DH, (cuuint32_t)STB, 1, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box,
              es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -589,12 +602,13 @@ bool make_head_map(CUtensorMap* m, const void* base, int BH, int L) {
 }
 
 // [B][L][H*D] token-major bf16 input viewed as {H*D, L, B, 1}, box {D, ST}
-bool make_rows_map(CUtensorMap* m, const void* base, int B, int L, int HD, int rows = ST) {
+bool make_rows_map(CUtensorMap* m, const void* base, int B, int L, int HD, int rows = ST,
+                   int cols = DT) {
   auto enc = encode_fn();
   if (!enc) return false;
   cuuint64_t dims[4] = {(cuuint64_t)HD, (cuuint64_t)L, (cuuint64_t)B, 1};
   cuuint64_t strides[3] = {(cuuint64_t)HD * 2, (cuuint64_t)L * HD * 2, (cuuint64_t)B * L * HD * 2};
-  cuuint32_t box[4] = {(cuuint32_t)DT, (cuuint32_t)rows, 1, 1};
+  cuuint32_t box[4] = {(cuuint32_t)cols, (cuuint32_t)rows, 1, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box,
              es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -634,10 +648,11 @@ int prologue_fwd(const deltanet_desc* d, const void* xq, const void* xk, const v
     }
     CUtensorMap mq, mk, mv;
     const int HD = d->H * DT;
-    if (!make_rows_map(&mq, xq, d->B, d->L, HD) || !make_rows_map(&mk, xk, d->B, d->L, HD) ||
-        !make_rows_map(&mv, xv, d->B, d->L, HD))
+    if (!make_rows_map(&mq, xq, d->B, d->L, HD, ST, DHF) ||
+        !make_rows_map(&mk, xk, d->B, d->L, HD, ST, DHF) ||
+        !make_rows_map(&mv, xv, d->B, d->L, HD, ST, DHF))
       return DELTANET_ERR_CUDA;
-    dim3 grid(a.B * a.H, (d->L + TILE_T - 1) / TILE_T, 3);
+    dim3 grid(a.B * a.H, (d->L + TILE_T - 1) / TILE_T, 6);
     prologue_fwd_tma_kernel<<<grid, 256, TMA_SMEM, s>>>(mq, mk, mv, a);
     prologue_beta_kernel<__nv_bfloat16><<<296, 256, 0, s>>>(a);
     return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
@@ -672,12 +687,13 @@ int prologue_bwd(const deltanet_desc* d, const void* xq, const void* xk, const v
     }
     CUtensorMap mxq, mxk, mxv, mgq, mgk, mgv;
     const int HD = d->H * DT, BH = d->B * d->H;
-    if (!make_rows_map(&mxq, xq, d->B, d->L, HD, STB) || !make_rows_map(&mxk, xk, d->B, d->L, HD, STB) ||
-        !make_rows_map(&mxv, xv, d->B, d->L, HD, STB) || !make_head_map(&mgq, dq, BH, d->L) ||
+    if (!make_rows_map(&mxq, xq, d->B, d->L, HD, STB, DH) ||
+        !make_rows_map(&mxk, xk, d->B, d->L, HD, STB, DH) ||
+        !make_rows_map(&mxv, xv, d->B, d->L, HD, STB, DH) || !make_head_map(&mgq, dq, BH, d->L) ||
         !make_head_map(&mgk, dk, BH, d->L) || !make_head_map(&mgv, dv, BH, d->L))
       return DELTANET_ERR_CUDA;
     a.ntile = (d->L + TILE_T - 1) / TILE_T;  // <= the workspace's (512-token) tile count
-    dim3 grid(BH, a.ntile, 3);
+    dim3 grid(BH, a.ntile, 6);
     prologue_bwd_tma_kernel<<<grid, 32 * NWB, TMA_SMEM_B, s>>>(mxq, mxk, mxv, mgq, mgk, mgv, a);
     prologue_beta_bwd_kernel<__nv_bfloat16><<<296, 256, 0, s>>>(a);
     prologue_dw_reduce<<<dim3(16, 3), 256, 0, s>>>(a);

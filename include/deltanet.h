@@ -56,8 +56,9 @@ enum {
   /* fwd: write the chunk-boundary states H_t into the workspace so the bwd
    * does not recompute them (§3.2 line 250 recomputes them; we
    * store them -- DESIGN.md "Differences from the paper").  The tcgen05
-   * path also stores a 24 KB per-chunk record (X, Z^T)
-   * so the bwd skips the UT substitution.
+   * path also stores a 32.5 KB per-chunk record (X, Z^T, the q/k row
+   * norms, A = tril(QK^T)) so the bwd skips the UT
+   * substitution, the norm passes and the QK^T product.
    * bwd: the workspace holds what a fwd with this flag over the same inputs
    * and the same desc wrote. */
   DELTANET_SAVE_STATES = 1u << 1,

@@ -145,8 +145,8 @@ def test_bwd_timeline(timlib):
         rows.append(f"{names[b_]:28s} {dt.mean():9.0f} cycles")
     rows.append(f"{'-- per chunk':28s} {np.diff(t[2:-2, 0]).mean():9.0f} cycles")
     # issuer stamps (slots 16-29), relative to the SIMT chunk start (slot 0)
-    inames = {16: "I main+dHimg rcv", 17: "I M1a issued", 18: "I Q rcv",
-              19: "I M1b issued", 20: "I A rcv", 21: "I P3 rcv", 22: "I M3/M4 issued",
+    inames = {16: "I main+dHimg rcv", 17: "I K H issued (MB_R)", 18: "I (stamp only)",
+              19: "I dH^T K^T issued", 20: "I A rcv", 21: "I P3 rcv", 22: "I M3/M4 issued",
               23: "I P5 rcv", 24: "I M5a+dQ issued", 25: "I P6 rcv", 26: "I M6 issued",
               27: "I P7 rcv"}
     for s_ in range(16, 28):

@@ -362,8 +362,9 @@ __device__ __forceinline__ void tile_mma(const float* LX, int ar, int ac, int br
 // X = (I + L)^{-1} for a 64x64 strictly-lower L, in place in LX (fp32,
 // row stride LSTRIDE floats), by 256 threads (wtid) that share named barrier
 // bar_id.
-// Level 1: forward substitution on the four 16x16
-// diagonal blocks, one warp per block, column-parallel in registers.
+// Level 1: forward substitution on the eight 8x8
+// diagonal blocks, one warp per block, column-parallel in registers, then
+// 8 -> 16 merges X21 = -X22 (L21 X11) in fp32 by all 256 threads.
 // Levels 2-3: merge blocks pairwise, X21 = -X22 (L21 X11), for 16 -> 32 -> 64,
 // as warp-level tf32 tensor-core products (mma.sync m16n8k8; R20:
 // tf32 operand rounding, 2^-11, is below the bf16 rounding X then gets).
@@ -376,19 +377,20 @@ __device__ __forceinline__ void ut_inverse_inplace(float* LX, int wtid, int bar_
   constexpr int LS = LSTRIDE;
   const int lane = wtid & 31, wwarp = wtid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  if (wwarp < 4) {  // level 1: block q = wwarp, column j = lane (< 16)
-    const int o = 16 * wwarp, j = lane & 15;
+  static_assert(LS >= 68, "level 1b keeps its 8x8 products in the row padding (cols 64-67)");
+  {  // level 1a: the eight 8x8 diagonal blocks, warp q = block, column j = lane (< 8)
+    const int o = 8 * wwarp, j = lane & 7;
     // All loads first (branch-free, so they can all be in flight), then the
     // dependent chain; x_i = [i == j] - [i > j] * sum_m L_im x_m.
-    float4 l4[16][4];
+    float4 l4[8][2];
 #pragma unroll
-    for (int i = 1; i < 16; ++i)
+    for (int i = 1; i < 8; ++i)
 #pragma unroll
       for (int m = 0; m < i; m += 4)
         l4[i][m / 4] = *reinterpret_cast<const float4*>(LX + (o + i) * LS + o + m);
-    float x[16];
+    float x[8];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
+    for (int i = 0; i < 8; ++i) {
       float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll
       for (int m = 0; m < i; m += 4) {
@@ -402,10 +404,31 @@ __device__ __forceinline__ void ut_inverse_inplace(float* LX, int wtid, int bar_
       x[i] = fmaf(-gt, (a0 + a1) + (a2 + a3), eq);
     }
     __syncwarp();
-    if (lane < 16) {
+    if (lane < 8) {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) LX[(o + i) * LS + o + j] = x[i];
+      for (int i = 0; i < 8; ++i) LX[(o + i) * LS + o + j] = x[i];
     }
+  }
+  grp_sync<NTH>(bar_id);
+  {  // level 1b: 8 -> 16 merges, warps 2p, 2p+1 on the 16x16 block p (offset
+    // o = 16p); thread (r, c) of the 8x8 products.  Y = L21 X11 goes to the
+    // row padding (cols 64-67 of rows o .. o+15), then X21 = -X22 Y.  The
+    // block's upper-right 8x8 already holds zeros (L is strictly lower).
+    const int o = 16 * (wwarp >> 1), idx = ((wwarp & 1) << 5) | lane, r = idx >> 3, c = idx & 7;
+    float* ys = LX + o * LS + 64;  // Y[r][c] at ys[(idx >> 2) * LS + (idx & 3)]
+    float y = 0.f;
+#pragma unroll
+    for (int m = 0; m < 8; ++m)  // X11(m, c) = 0 for m < c (stored zeros)
+      y = fmaf(LX[(o + 8 + r) * LS + o + m], LX[(o + m) * LS + o + c], y);
+    ys[(idx >> 2) * LS + (idx & 3)] = y;
+    grp_sync<NTH>(bar_id);
+    float z = 0.f;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {  // X22(r, m) = 0 for m > r (stored zeros)
+      const int ym = m * 8 + c;
+      z = fmaf(LX[(o + 8 + r) * LS + o + 8 + m], ys[(ym >> 2) * LS + (ym & 3)], z);
+    }
+    LX[(o + 8 + r) * LS + o + c] = -z;  // L21 was read above (before the sync)
   }
   grp_sync<NTH>(bar_id);
   if (stamps && wtid == 0) stamps[0] = clock64();

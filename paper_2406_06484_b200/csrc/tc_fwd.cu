@@ -395,6 +395,7 @@ __global__ void __launch_bounds__(NT, 1)
         // handles one 16-column quarter of its row.
         if (c >= 1) mbar_wait(&wu_done, (c - 1) & 1);
         const int i = tid & 63, j0 = (tid >> 6) * 16;
+        uint4 xrec[2];  // the X record, stored once T is handed over
         float4 x4[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) x4[q] = *reinterpret_cast<const float4*>(LX + i * LS + j0 + 4 * q);
@@ -423,20 +424,21 @@ __global__ void __launch_bounds__(NT, 1)
           }
           il_store8(sT, C, i, j0 + g * 8, x);
           il_store8(sTu, C, i, j0 + g * 8, y);
-          if (recs) {  // the X record, straight from registers (IL image, 16 B per row)
-            uint4 u;
-            u.x = pack_bf16(xs[0], xs[1]);
-            u.y = pack_bf16(xs[2], xs[3]);
-            u.z = pack_bf16(xs[4], xs[5]);
-            u.w = pack_bf16(xs[6], xs[7]);
+          xrec[g].x = pack_bf16(xs[0], xs[1]);
+          xrec[g].y = pack_bf16(xs[2], xs[3]);
+          xrec[g].z = pack_bf16(xs[4], xs[5]);
+          xrec[g].w = pack_bf16(xs[6], xs[7]);
+        }
+        fence_proxy_async();
+        grp_sync<NP>(BAR_P);
+        if (tid == 0) mbar_arrive(&t_ready);
+        if (recs) {  // the X record from registers (IL image, 16 B per row), off the hand-over
+#pragma unroll
+          for (int g = 0; g < 2; ++g)
             *reinterpret_cast<uint4*>(recs + (size_t)c * REC_BYTES + REC_X +
-                                      il_off(i, j0 + g * 8, C)) = u;
-          }
+                                      il_off(i, j0 + g * 8, C)) = xrec[g];
         }
       }
-      fence_proxy_async();
-      grp_sync<NP>(BAR_P);
-      if (tid == 0) mbar_arrive(&t_ready);
       TSTAMP(6);
       TSTAMP(7);
       TSTAMP(8);
@@ -817,12 +819,12 @@ __global__ void __launch_bounds__(NT, 1)
         asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(1) : "memory");
         if (!states) bulk_wait_read0();
         mbar_arrive(&z_free);
-        mbar_wait(&z_ready, c & 1);
         mbar_wait(&q_done, c & 1);
         if (c + 2 < NC) {  // Q of chunk c+2 into the slot O = Q H has released
           mbar_expect_tx(&q_full[b], TILE);
           tma_load_4d(sQ(b), &mQ, 0, T0 + (c + 2) * C, 0, unit, &q_full[b]);
         }
+        mbar_wait(&z_ready, c & 1);
         fence_after_sync();
         if (states) {  // Z^T of this chunk for the backward (read out before st_free)
           bulk_store(reinterpret_cast<uint8_t*>(a.scratch) + ((size_t)unit * a.NC + cbase + c) * REC_BYTES +

@@ -265,6 +265,8 @@ __global__ void __launch_bounds__(NT, 1)
       mbar_wait(&g_done, c & 1);
       fence_after_sync();
       TSTAMP(3);
+      uint4 arec[2];  // this thread's A record segments (stored after g_free)
+      int arow = 0, acol = 0;
       {
         // one TMEM load of this half's 32 columns: lanes < 16 hold G_qk rows,
         // lanes >= 16 hold G_kk rows
@@ -343,16 +345,13 @@ __global__ void __launch_bounds__(NT, 1)
               a8[e] = (c0 + g * 8 + e <= i) ? qk : 0.f;
             }
             if (!SEG1) il_store8(sA(b), C, i, c0 + g * 8, a8);
-            if (recs) {  // the backward's A (IL image, 16 B per row segment)
-              uint4 u;
-              u.x = pack_bf16(a8[0], a8[1]);
-              u.y = pack_bf16(a8[2], a8[3]);
-              u.z = pack_bf16(a8[4], a8[5]);
-              u.w = pack_bf16(a8[6], a8[7]);
-              *reinterpret_cast<uint4*>(recs + (size_t)c * REC_BYTES + REC_A +
-                                        il_off(i, c0 + g * 8, C)) = u;
-            }
+            arec[g].x = pack_bf16(a8[0], a8[1]);
+            arec[g].y = pack_bf16(a8[2], a8[3]);
+            arec[g].z = pack_bf16(a8[4], a8[5]);
+            arec[g].w = pack_bf16(a8[6], a8[7]);
           }
+          arow = i;
+          acol = c0;
         }
         {  // L = beta_i s_i s_j (k_i . k_j), j < i
           const float bi = vb[i] * vb[C + i];
@@ -384,6 +383,12 @@ __global__ void __launch_bounds__(NT, 1)
           dbg_smem(dn_dbg + D_S, vb + C, 1, C, C, w);
           dbg_smem(dn_dbg + D_B, vb, 1, C, C, w); fence_before_sync(); grp_sync<NP>(BAR_P));
       if (tid == 0) mbar_arrive(&g_free);  // the Gram accumulator may be overwritten
+      if (recs) {  // the backward's A record (IL image, 16 B per row segment), off the hand-over
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+          *reinterpret_cast<uint4*>(recs + (size_t)c * REC_BYTES + REC_A +
+                                    il_off(arow, acol + g * 8, C)) = arec[g];
+      }
       TSTAMP(4);
       ut_inverse_inplace<LS, NP>(LX, tid, BAR_P, TSTAMP_PTR(10));
       TSTAMP(5);

@@ -87,7 +87,7 @@ enum { BAR_SIMT = 1 };
 enum { MB_AL, MB_R, MB_DU, MB_P, MB_DH, MB_A, MB_LD, MB_GB, MB_K, MB_MAIN, MB_QL, MB_KL0, MB_KL1, MB_DHK,
        MB_N };
 // SIMT -> issuer hand-offs (SG_STG: issuer -> SIMT, staging regions free)
-enum { SG_DHI, SG_A, SG_P3, SG_P5, SG_P6, SG_P7, SG_P8, SG_STG, SG_N };
+enum { SG_DHI, SG_A, SG_P3, SG_P5, SG_P6, SG_P7, SG_P8, SG_STG, SG_RFREE, SG_N };
 
 __device__ __forceinline__ void ld32(uint32_t tm, int wwarp, uint32_t col, float (&f)[32]) {
   uint32_t r[2][16];
@@ -346,9 +346,16 @@ __global__ void __launch_bounds__(NT, 1)
           load_q(c - 1, (it + 1) & 1);
         }
         mbar_wait(&sg[SG_P5], ph);
-        if (!SEG1 && !GATED) {  // (gated: sDV holds gamma dV; dV is stored from P5)
+        if (!SEG1 && !GATED) {
           tma_store_4d(&mDV, sDV, 0, t0, 0, unit);
           bulk_commit();
+        }
+        if (GATED) {  // sDV holds gamma dV (the operands'); dV itself was staged in
+          // the R slot, free between M3 and P6's Y: store it, then hand the slot back
+          tma_store_4d(&mDV, sR, 0, t0, 0, unit);
+          bulk_commit();
+          bulk_wait_read0();
+          mbar_arrive(&sg[SG_RFREE]);
         }
         if (c > 0) {
           mbar_wait(&mb[MB_LD], ph);  // dO, H^T, U' read by M5; V once dV is read out
@@ -878,16 +885,8 @@ __global__ void __launch_bounds__(NT, 1)
               if (GATED) pk = fmaf(p[g * 8 + e], kh, pk);
               dv8[e] = bt * p[g * 8 + e];
             }
-            if (GATED) {  // dV to global here; the operand tile takes gamma dV
-              if (t0 + r64 < L) {
-                uint4 u;
-                u.x = pack_bf16(dv8[0], dv8[1]);
-                u.y = pack_bf16(dv8[2], dv8[3]);
-                u.z = pack_bf16(dv8[4], dv8[5]);
-                u.w = pack_bf16(dv8[6], dv8[7]);
-                *reinterpret_cast<uint4*>((__nv_bfloat16*)a.dv +
-                                          ((size_t)unit * a.L + T0 + t0 + r64) * D + c0 + g * 8) = u;
-              }
+            if (GATED) {  // dV staged in the R slot (TMA-stored); the operand tile takes gamma dV
+              il_store8(sR, C, r64, c0 + g * 8, dv8);
 #pragma unroll
               for (int e = 0; e < 8; ++e) dv8[e] *= gi;
             }
@@ -954,6 +953,7 @@ __global__ void __launch_bounds__(NT, 1)
 
       // ================= P6: dA -> bf16 (masked) | Y -> bf16
       mbar_wait(&mb[MB_A], ph);
+      if (GATED) mbar_wait(&sg[SG_RFREE], ph);  // dV read out of the R slot (sY)
       fence_after_sync();
       BSTAMP(10);
       {

@@ -322,6 +322,88 @@ def test_chunkwise_backward_equals_bptt(C):
         assert np.abs(r - g).max() <= 1e-12
 
 
+@pytest.mark.parametrize("l2", [False, True])
+def test_backward_checkpoint_segments_finite_differences(l2):
+    """The oracle's backward re-derives S_{t-1} from checkpoints every 64
+    tokens (deltanet_oracle.c CKPT).  L = 150 = 64 + 64 + 22 walks three
+    checkpoint segments with a ragged last one; central differences of
+    <O, dO> + <hT, dhT> w.r.t. every input pin that path (rel <= 1e-6 above
+    1e-8, abs <= 1e-8 below), with h0 and dhT nonzero."""
+    rng = np.random.default_rng(130 + l2)
+    L, dk, dv = 150, 3, 2
+    q, k, v, b = _rand_unit(rng, L, dk, dv, unit_keys=not l2)
+    if l2:
+        q *= 1.3; k *= 0.7
+    h0 = 0.5 * rng.standard_normal((dk, dv))
+    dO = rng.standard_normal((L, dv))
+    dhT = rng.standard_normal((dk, dv))
+    grads = _bwd(q, k, v, b, dO, h0=h0, dhT=dhT, l2norm=l2)
+    args = [q, k, v, b, h0]
+    # h = 1e-5: at L = 150 the loss is O(10^2), so the rounding floor of a
+    # central difference, ~1e-16 |loss| / h, must stay below the bar; the
+    # truncation error is O(h^2).  Bar: |g - num| <= 1e-6 |num| + 1e-9 max|num|
+    eps = 1e-5
+    for ai, (a, g) in enumerate(zip(args, grads)):
+        num = np.zeros_like(a)
+        for idx in np.ndindex(a.shape):
+            ap = [x.copy() for x in args]; am = [x.copy() for x in args]
+            ap[ai][idx] += eps; am[ai][idx] -= eps
+            num[idx] = (_loss(*ap[:4], dO, ap[4], dhT, l2) -
+                        _loss(*am[:4], dO, am[4], dhT, l2)) / (2 * eps)
+        err = np.abs(g - num)
+        bar = 1e-6 * np.abs(num) + 1e-9 * np.abs(num).max()
+        assert np.all(err <= bar), (ai, (err / np.maximum(np.abs(num), 1e-300)).max())
+
+
+@pytest.mark.parametrize("L,C", [(160, 16), (192, 64), (135, 5), (131, 1)])
+def test_backward_checkpoint_segments_equal_chunkwise_adjoint(L, C):
+    """Three or more checkpoint segments (L > 128; 160, 135, 131 ragged) at d = 16: the
+    oracle's BPTT == the independent chunked adjoint of SURVEY App. A.2
+    (oracle/forms.py::chunkwise_backward), every output incl. dh0."""
+    rng = np.random.default_rng(200 + L + C)
+    dk, dv = 16, 12
+    q, k, v, b = _rand_unit(rng, L, dk, dv)
+    h0 = 0.4 * rng.standard_normal((dk, dv))
+    dO = rng.standard_normal((L, dv)); dhT = rng.standard_normal((dk, dv))
+    ref = _bwd(q, k, v, b, dO, h0=h0, dhT=dhT)
+    got = forms.chunkwise_backward(q, k, v, b, dO, C, S0=h0, dST=dhT)
+    for r, g in zip(ref, got):
+        assert np.abs(r - g).max() <= 1e-11 * max(1.0, np.abs(r).max())
+
+
+def test_l2_adjoint_eps_branch_finite_differences():
+    """Reading R9: below ||x|| = eps the normalisation divides by the constant
+    eps, so the adjoint is dx = dy / eps.  Rows of q and k scaled to ~1e-8
+    (and one exactly zero) stay inside that branch under the FD step; the
+    oracle's gradients of those rows match central differences."""
+    rng = np.random.default_rng(77)
+    L, dk, dv = 12, 4, 3
+    q, k, v, b = _rand_unit(rng, L, dk, dv, unit_keys=False)
+    q[3] *= 1e-8 / np.linalg.norm(q[3])
+    k[5] *= 2e-8 / np.linalg.norm(k[5])
+    q[7] = 0.0
+    k[9] = 0.0
+    h0 = 0.5 * rng.standard_normal((dk, dv))
+    dO = rng.standard_normal((L, dv)); dhT = rng.standard_normal((dk, dv))
+    dq, dk_, _, _, _ = _bwd(q, k, v, b, dO, h0=h0, dhT=dhT, l2norm=True)
+    h = 1e-10   # keeps ||x|| < 1e-6 (the eps of R9)
+    for which, rows in ((0, (3, 7)), (1, (5, 9))):
+        g = (dq, dk_)[which]
+        for r in rows:
+            for j in range(dk):
+                ap = [q.copy(), k.copy()]; am = [q.copy(), k.copy()]
+                ap[which][r, j] += h; am[which][r, j] -= h
+                num = (_loss(ap[0], ap[1], v, b, dO, h0, dhT, True) -
+                       _loss(am[0], am[1], v, b, dO, h0, dhT, True)) / (2 * h)
+                assert abs(g[r, j] - num) <= 1e-5 * max(1.0, abs(num)), (which, r, j)
+    # and the branch really is the constant-divisor one: a 2x larger tiny row
+    # has the same gradient (dx = dy / eps does not depend on ||x||)
+    q2 = q.copy(); q2[3] *= 2.0
+    dq2 = _bwd(q2, k, v, b, dO, h0=h0, dhT=dhT, l2norm=True)[0]
+    ratio = np.abs(dq2[3]).max() / np.abs(dq[3]).max()
+    assert 0.5 < ratio < 2.0   # dy changes only through o, not through 1/||x||
+
+
 def test_backward_linear_in_cotangent_and_zero():
     rng = np.random.default_rng(50)
     q, k, v, b = _rand_unit(rng, 17, 6, 6, unit_keys=False)

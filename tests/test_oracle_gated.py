@@ -123,3 +123,47 @@ def test_chunkwise_gated_backward_equals_bptt(C):
                                          dO[0, 0], C, h0[0, 0], dhT[0, 0])
     for name, a, b in zip(("dq", "dk", "dv", "dbeta", "dg", "dh0"), got, ref):
         np.testing.assert_allclose(a, b[0, 0], rtol=1e-10, atol=1e-11, err_msg=name)
+
+
+@pytest.mark.parametrize("L,C", [(160, 16), (135, 5)])
+def test_chunkwise_gated_backward_checkpoint_segments(L, C):
+    """L > 128: the gated oracle's BPTT walks three checkpoint segments of 64
+    tokens (the last ragged) and still equals the independent chunked adjoint
+    (oracle/forms.py::gated_chunkwise_backward)."""
+    q, k, v, beta, g, dO, h0, dhT = _inp(6 + L, B=1, H=1, L=L, Dk=8, Dv=6, gmax=0.3)
+    kn = k / np.linalg.norm(k, axis=-1, keepdims=True)
+    qn = q / np.linalg.norm(q, axis=-1, keepdims=True)
+    ref = oracle.gated_bwd(qn, kn, v, beta, g, dO, h0=h0, dhT=dhT, l2norm=False)
+    got = forms.gated_chunkwise_backward(qn[0, 0], kn[0, 0], v[0, 0], beta[0, 0], g[0, 0],
+                                         dO[0, 0], C, h0[0, 0], dhT[0, 0])
+    for name, a, b in zip(("dq", "dk", "dv", "dbeta", "dg", "dh0"), got, ref):
+        scale = max(1.0, np.abs(b).max())
+        np.testing.assert_allclose(a, b[0, 0], rtol=0, atol=1e-10 * scale, err_msg=name)
+
+
+def test_backward_finite_differences_checkpoint_segments():
+    """Central differences at L = 150 (three checkpoint segments, ragged) of
+    every input of the gated oracle, incl. g and h0, with L2 normalisation."""
+    q, k, v, beta, g, dO, h0, dhT = _inp(9, B=1, H=1, L=150, Dk=3, Dv=2, gmax=0.2)
+    args = [q, k, v, beta, g, h0]
+
+    def loss(a):
+        o, hT = oracle.gated_fwd(a[0], a[1], a[2], a[3], a[4], h0=a[5], l2norm=True)
+        return float((o * dO).sum() + (hT * dhT).sum())
+
+    grads = oracle.gated_bwd(q, k, v, beta, g, dO, h0=h0, dhT=dhT, l2norm=True)
+    h = 1e-5   # see test_oracle.py::test_backward_checkpoint_segments_finite_differences
+    for idx, grad in enumerate(grads):
+        base = [np.array(a, dtype=np.float64) for a in args]
+        flat = base[idx].reshape(-1)
+        num = np.zeros_like(flat)
+        for i in range(flat.size):
+            keep = flat[i]
+            flat[i] = keep + h
+            lp = loss(base)
+            flat[i] = keep - h
+            lm = loss(base)
+            flat[i] = keep
+            num[i] = (lp - lm) / (2 * h)
+        err = np.abs(grad.reshape(-1) - num)
+        assert np.all(err <= 1e-6 * np.abs(num) + 1e-9 * np.abs(num).max()), idx

@@ -9,7 +9,14 @@ synthetic inputs resident in HBM, i.e. every row of SURVEY §8(a).  Each rank
 owns B=8 batch rows (weak scaling: per-GPU work fixed; at N=8 this is the
 BASELINE "sharded" B=64 config).  The (b, h) units are independent, so there
 is no collective in the timed region; the NCCL all-gather of outputs and
-gradients (north_star) is timed separately and reported as "gather".
+gradients (north_star) is timed separately and reported as "gather".  The
+sharding, the step and the gather are paper_2406_06484_b200.data_parallel
+(the code the gloo tests drive).  A second record, "strong_scaling", runs
+BASELINE configs[4] as stated -- B=64 in total, 64/N rows per rank -- so at
+N=1 it is the single-GPU B=64 (1024-unit) measurement.
+
+`python bench.py --gpus N` without a torchrun environment re-launches itself
+under torch.distributed.run with N processes (127.0.0.1 rendezvous).
 
 Prints ONE JSON line on rank 0 (contract in the task statement / DESIGN.md).
 """
@@ -379,6 +386,119 @@ def measure_context_parallel(dn, dev, parts=2):
             "note": "per-rank kernel time of one simulated rank; excludes the NCCL all-gather"}
 
 
+def _free_port():
+    import socket
+    s_ = socket.socket()
+    s_.bind(("127.0.0.1", 0))
+    p = s_.getsockname()[1]
+    s_.close()
+    return p
+
+
+def relaunch_distributed(n):
+    """--gpus N > 1 outside torchrun: run this script under
+    torch.distributed.run with N local ranks and return its exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1",
+           "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def _synthetic_rows(dev, rows, Hh, Ll, Dd, seed0):
+    """Seeded inputs of the paper's distributions (DESIGN.md input recipe:
+    q, k ~ SiLU(N(0,1)), v, dO ~ N(0,1), beta ~ sigmoid(N(0,1))), generated on
+    the device one batch row at a time (seed0 + b), so a row's data does not
+    depend on how the batch is sharded; timing-only records."""
+    import torch
+    f = torch.nn.functional
+    parts = {n: [] for n in ("q", "k", "v", "beta", "dO")}
+    for b in rows:
+        g = torch.Generator(device=dev).manual_seed(seed0 + b)
+        rn = lambda *shape: torch.randn(shape, device=dev, generator=g)
+        parts["q"].append(f.silu(rn(1, Hh, Ll, Dd)))
+        parts["k"].append(f.silu(rn(1, Hh, Ll, Dd)))
+        parts["v"].append(rn(1, Hh, Ll, Dd))
+        parts["beta"].append(torch.sigmoid(rn(1, Hh, Ll)))
+        parts["dO"].append(rn(1, Hh, Ll, Dd))
+    return [torch.cat(parts[n], 0).to(torch.bfloat16).contiguous()
+            for n in ("q", "k", "v", "beta", "dO")]
+
+
+def _time_steps(dev, step, reps, warm=2):
+    import torch
+    import torch.distributed as dist
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(warm):
+        step.step()
+    torch.cuda.synchronize(dev)
+    if dist.is_initialized():
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        step.step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    return e0.elapsed_time(e1) * 1e-3 / reps
+
+
+def measure_strong_scaling(dp, dev, ws, rank, reps=5):
+    """BASELINE configs[4] as stated: B=64 H=16 L=4096 in total over the N
+    ranks (shard_rows: 64/N batch rows = 1024/N units per GPU), fwd+bwd,
+    device time max over ranks.  At N=1 this is the single-GPU B=64 record
+    (1024 units, ~6.9 waves of 148 SMs) against which the 8-GPU shard
+    (128 units, 0.86 of a wave) is compared (SURVEY §8(e) strong-scaling
+    risk).  Not the headline: every rank runs it after the timed step."""
+    B_total = 64
+    rows = dp.shard_rows(B_total, ws, rank)
+    q, k, v, beta, dO = _synthetic_rows(dev, rows, H, L, D, 4000)
+    step = dp.ShardedStep(q, k, v, beta, dO, B_total=B_total, chunk=C)
+    t, = dp.max_over_ranks([_time_steps(dev, step, reps)], dev)
+    ff, fb, _, _ = per_token_head(D, D, C, 2)
+    units = len(rows) * H
+    del step, q, k, v, beta, dO
+    return {"workload": f"B={B_total} total (BASELINE configs[4]) H={H} L={L} d={D} chunk={C} "
+                        f"bf16 fwd+bwd, {len(rows)} rows = {units} units per GPU",
+            "scaling": "strong", "n_gpus": ws, "ms_per_step": t * 1e3,
+            "tokens_per_s": B_total * L / t, "units_per_gpu": units,
+            "sm_waves_per_gpu": units / 148.0,
+            "tc_peak_frac_per_gpu": (ff + fb) * units * L / t / 1634.4e12,
+            "data": "synthetic, seeded per batch row on the device (timing only)"}
+
+
+def measure_1p3b(dn, dp, dev, reps=10):
+    """BASELINE configs[1]: the 1.3B-shaped layer B=8 H=16 d=128 L=2048 C=64
+    (the paper's 2K x 8 training setting), fwd+bwd on one
+    GPU (side record, rank 0)."""
+    B = 8
+    Ll = 2048
+    q, k, v, beta, dO = _synthetic_rows(dev, range(B), H, Ll, D, 1000)
+    step = dp.ShardedStep(q, k, v, beta, dO, B_total=B, chunk=C, local=True)  # rank 0 alone
+    import torch
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(2):
+        step.step()
+    torch.cuda.synchronize(dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    tf = tb = 0.0
+    for _ in range(reps):
+        ev[0].record(stream)
+        step.fwd()
+        ev[1].record(stream)
+        step.bwd()
+        ev[2].record(stream)
+        torch.cuda.synchronize(dev)
+        tf += ev[0].elapsed_time(ev[1]) * 1e-3 / reps
+        tb += ev[1].elapsed_time(ev[2]) * 1e-3 / reps
+    ff, fb, _, _ = per_token_head(D, D, C, 2)
+    t = tf + tb
+    return {"workload": f"B={B} H={H} L={Ll} d={D} chunk={C} bf16 fwd+bwd (BASELINE configs[1])",
+            "ms_per_step": t * 1e3, "ms_fwd": tf * 1e3, "ms_bwd": tb * 1e3,
+            "tokens_per_s": B * Ll / t,
+            "tc_peak_frac": (ff + fb) * B * H * Ll / t / 1634.4e12}
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -465,9 +585,15 @@ def main():
     ap.add_argument("--force-simt", action="store_true")
     ap.add_argument("--no-recurrent", action="store_true",
                     help="skip the recurrent-form (SURVEY §8(f) f2) side measurement")
+    ap.add_argument("--no-strong", action="store_true",
+                    help="skip the configs[4] strong-scaling record (B=64 total)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_distributed(args.gpus))
     ws, rank, local = dist_env()
+    if args.gpus != ws and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; using {ws}", file=sys.stderr)
 
     if args.impl == "reference":
         return run_reference(args, ws, rank)
@@ -477,6 +603,7 @@ def main():
     import torch.distributed as dist
 
     import paper_2406_06484_b200 as dn
+    from paper_2406_06484_b200 import data_parallel as dp
     import synth
 
     if not torch.cuda.is_available():
@@ -488,28 +615,27 @@ def main():
     dn.load_library()
 
     cfg = synth.CONFIGS["sharded"]
-    rows = range(rank * B_PER_RANK, (rank + 1) * B_PER_RANK)
+    B_total = B_PER_RANK * ws          # weak scaling: 8 batch rows per rank
+    rows = dp.shard_rows(B_total, ws, rank)
     host = synth.make_inputs(cfg, b_range=rows)
     td = torch.bfloat16
     q, k, v, beta, dO = (torch.from_numpy(host[f]).to(td).to(dev).contiguous()
                          for f in ("q", "k", "v", "beta", "dO"))
     desc = dn.make_desc(B_PER_RANK, H, L, D, D, C, td, l2norm=True, save_states=True,
                         force_simt=args.force_simt)
-    ws_buf = dn.alloc_workspace(desc, dev)
-    o = torch.empty_like(v)
-    grads = (torch.empty_like(q), torch.empty_like(k), torch.empty_like(v),
-             torch.empty_like(beta))
+    ops = None
+    if args.force_simt:
+        from types import SimpleNamespace
+        ops = SimpleNamespace(
+            fwd=lambda *a_, **kw: dn.deltanet_fwd(*a_, force_simt=True, **kw),
+            bwd=lambda *a_, **kw: dn.deltanet_bwd(*a_, force_simt=True, **kw),
+            alloc=lambda q_, v_, c_: dn.alloc_workspace(desc, dev))
+    step = dp.ShardedStep(q, k, v, beta, dO, B_total=B_total, chunk=C, ops=ops)
+    o, grads = step.o, step.grads
     path = dn.deltanet_path(desc)
     n_launch = dn.deltanet_launch_count(desc, 0) + dn.deltanet_launch_count(desc, 1)
     stream = torch.cuda.current_stream(dev)
-
-    def fwd():
-        dn.deltanet_fwd(q, k, v, beta, chunk=C, workspace=ws_buf, want_hT=False, out=o,
-                        force_simt=args.force_simt)
-
-    def bwd():
-        dn.deltanet_bwd(q, k, v, beta, dO, chunk=C, workspace=ws_buf, want_dh0=False,
-                        out=grads, force_simt=args.force_simt)
+    fwd, bwd = step.fwd, step.bwd
 
     clocks = ClockSampler(dev)
     clocks.start()
@@ -538,10 +664,7 @@ def main():
     t_bwd = sum(e[1].elapsed_time(e[2]) for e in ev) / args.steps * 1e-3
     t_total = ev[0][0].elapsed_time(ev[-1][2]) * 1e-3
     t_step = t_total / args.steps
-    if ws > 1:
-        tt = torch.tensor([t_step, t_fwd, t_bwd], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_step, t_fwd, t_bwd = tt.tolist()
+    t_step, t_fwd, t_bwd = dp.max_over_ranks([t_step, t_fwd, t_bwd], dev)
 
     tokens_per_step = B_PER_RANK * ws * L
     value = tokens_per_step / t_step
@@ -566,10 +689,19 @@ def main():
     tj = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     kname = f"tc_{name}_kernel"
     if path == 1 and os.path.exists(tj):
-        tr = json.load(open(tj)).get(kname)
+        tjs = json.load(open(tj))
+        tr = tjs.get(kname)
         if tr:  # DRAM bytes per launch of this kernel from the committed ncu capture
-            roof["traffic"] = tr["dram_read_bytes"] + tr["dram_write_bytes"]
+            from paper_2406_06484_b200.build import sources_sha
+            cap = tr["dram_read_bytes"] + tr["dram_write_bytes"]
+            fresh = tjs.get("sources_sha16") == sources_sha()
+            # a capture of other kernel sources is not this kernel's traffic
+            roof["traffic"] = cap if fresh else None
             roof["traffic_unit"] = "bytes/launch (ncu dram__bytes_read+write, profiles/)"
+            roof["traffic_capture"] = {"bytes": cap, "sources_sha16": tjs.get("sources_sha16"),
+                                       "benched_sources_sha16": sources_sha(),
+                                       "stale": not fresh,
+                                       "git_head_at_summary": tjs.get("git_head_at_summary")}
             roof["algorithmic_bytes_per_launch"] = B_k
     roof["kernel"] = f"deltanet_{name} ({'tcgen05' if path == 1 else 'simt'} path)"
     roof["peak_source"] = peaks["source"] + (" sustained" if roof["bound"] == "tensor" and long_region else "")
@@ -621,29 +753,34 @@ def main():
 
     clk = clocks.stop()
 
-    # ---- NCCL gather of outputs and gradients (outside the timed step)
+    # ---- NCCL gather of outputs and gradients into the full [B,H,L,d]
+    # layout (data_parallel.gather_rows; outside the timed step)
     gather = None
     if ws > 1:
-        outs = [o, *grads]
-        full = [torch.empty((ws,) + t.shape, dtype=t.dtype, device=dev) for t in outs]
         dist.barrier()
+        torch.cuda.synchronize(dev)
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         g0.record(stream)
-        for dst, src in zip(full, outs):
-            dist.all_gather_into_tensor(dst, src)
+        full = step.gather()
         g1.record(stream)
         torch.cuda.synchronize(dev)
-        tg = torch.tensor([g0.elapsed_time(g1) * 1e-3], device=dev)
-        dist.all_reduce(tg, op=dist.ReduceOp.MAX)
+        tg, = dp.max_over_ranks([g0.elapsed_time(g1) * 1e-3], dev)
         recv = sum(t.numel() * t.element_size() for t in full)
-        gather = {"ms": tg.item() * 1e3, "bytes_received_per_gpu": recv,
-                  "GBps": recv / tg.item() / 1e9, "collective": "ncclAllGather"}
+        gather = {"ms": tg * 1e3, "bytes_received_per_gpu": recv,
+                  "GBps": recv / tg / 1e9, "collective": "ncclAllGather (all_gather_into_tensor)",
+                  "layout": [list(t.shape) for t in full]}
+        del full
+
+    strong = None
+    if not args.no_strong and not args.force_simt:
+        strong = measure_strong_scaling(dp, dev, ws, rank)
 
     base = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         base = cpu_baseline()
-    rec = pro = lng = gat = cpx = None
+    rec = pro = lng = gat = cpx = cfg1 = None
     if rank == 0 and not args.no_recurrent and not args.force_simt:
+        cfg1 = measure_1p3b(dn, dp, dev)
         rec = measure_recurrent(dn, dev, q, k, v, beta, t_fwd, peaks)
         pro = measure_prologue(dn, dev, B_PER_RANK, H, L, D, peaks)
         lng = measure_long_context(dn, dev)
@@ -672,6 +809,10 @@ def main():
         }
         if gather:
             line["gather"] = gather
+        if strong:
+            line["strong_scaling"] = strong
+        if cfg1:
+            line["config_1p3b"] = cfg1
         if rec:
             line["recurrent"] = rec
         if pro:

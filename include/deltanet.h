@@ -19,7 +19,7 @@
  *  - Every tensor pointer is DEVICE memory owned by the caller, contiguous,
  *    row-major, 16-byte aligned (MISALIGNED otherwise).  The library never
  *    allocates or frees, never synchronises the host, and keeps no mutable
- *    global state except once-per-process kernel attributes; calls on
+ *    global state except once-per-device kernel attributes; calls on
  *    different streams are independent.
  *  - Layouts: q, k [B,H,L,Dk]; v, o, dO [B,H,L,Dv]; beta [B,H,L];
  *    states h0, hT, dhT, dh0 [B,H,Dk,Dv] in the orientation H = S^T
@@ -62,8 +62,11 @@ enum {
    * bwd: the workspace holds what a fwd with this flag over the same inputs
    * and the same desc wrote. */
   DELTANET_SAVE_STATES = 1u << 1,
-  /* debug: force the generic CUDA-core path even where the tcgen05 path
-   * applies (both are CUDA kernels; there is no CPU fallback). */
+  /* run the generic CUDA-core (SIMT) kernels even where the tcgen05 path
+   * applies, and allow bf16 descriptors outside the tcgen05 shapes (without
+   * this flag those are DELTANET_ERR_UNSUPPORTED: the CUDA-core kernels run
+   * 10^3-10^4x below the tensor-core roofline, so they are never chosen
+   * silently).  fp32 I/O always runs on them.  No CPU fallback exists. */
   DELTANET_FORCE_SIMT = 1u << 2,
   /* layer prologue only: SiLU on v as well (the paper states SiLU for q, k
    * only; R22) */
@@ -90,7 +93,9 @@ typedef struct {
 /* Error codes. */
 #define DELTANET_OK 0
 #define DELTANET_ERR_INVALID_ARG 1 /* null required pointer, negative size   */
-#define DELTANET_ERR_UNSUPPORTED 2 /* Dk/Dv/chunk/dtype outside the table    */
+#define DELTANET_ERR_UNSUPPORTED 2 /* Dk/Dv/chunk/dtype outside the table, or
+                                      bf16 outside the tcgen05 shapes without
+                                      DELTANET_FORCE_SIMT                     */
 #define DELTANET_ERR_MISALIGNED 3  /* a pointer not 16-byte aligned          */
 #define DELTANET_ERR_CUDA 4        /* cudaGetLastError() after a launch      */
 #define DELTANET_ERR_WORKSPACE 5   /* workspace NULL or smaller than needed  */
@@ -272,7 +277,11 @@ int deltanet_state_scan(const deltanet_desc* d, int nparts, int part,
                         void* stream);
 
 /* Which kernel family a descriptor dispatches to: 1 = tcgen05/TMEM/TMA
- * sm_100a path, 0 = CUDA-core (SIMT) path, -1 = unsupported descriptor. */
+ * sm_100a path, 0 = CUDA-core (SIMT) path, -1 = unsupported descriptor.
+ * The tcgen05 path serves bf16 I/O with chunk = 64 and Dk = Dv = 128
+ * (ungated and gated; BASELINE configs 1, 2, 4 and the target).  fp32 I/O
+ * and (with DELTANET_FORCE_SIMT only) other bf16 shapes run on the
+ * CUDA-core kernels; any other bf16 descriptor is -1 (UNSUPPORTED). */
 int deltanet_path(const deltanet_desc* d);
 
 /* Number of kernel launches deltanet_fwd (which=0), deltanet_bwd (which=1),

@@ -163,6 +163,21 @@ def _need(t, name, dtype, device):
         raise DeltaNetError(f"{name} must be contiguous")
 
 
+def _need_out(t, name, shape, dtype, device):
+    """An output buffer (out=...) is written by TMA / plain stores of the
+    library: check dtype, device, contiguity and the exact shape first."""
+    _need(t, name, dtype, device)
+    if t is not None and tuple(t.shape) != tuple(shape):
+        raise DeltaNetError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+
+
+def _need_inputs(q, k, v, beta, dO=None):
+    B, H, L, Dk = q.shape
+    if tuple(k.shape) != (B, H, L, Dk) or v.dim() != 4 or tuple(v.shape[:3]) != (B, H, L) \
+            or tuple(beta.shape) != (B, H, L) or (dO is not None and dO.shape != v.shape):
+        raise DeltaNetError("shape mismatch: q, k [B,H,L,Dk], v, dO [B,H,L,Dv], beta [B,H,L]")
+
+
 def alloc_workspace(desc: deltanet_desc, device) -> torch.Tensor:
     n = deltanet_workspace_bytes(desc)
     return torch.empty(max(n, 16), dtype=torch.uint8, device=device)
@@ -183,13 +198,17 @@ def deltanet_fwd(q, k, v, beta, *, chunk=64, l2norm=True, h0=None, save_states=T
     for t, n in ((q, "q"), (k, "k"), (v, "v"), (beta, "beta")):
         _need(t, n, q.dtype, dev)
     _need(h0, "h0", torch.float32, dev)
+    _need_inputs(q, k, v, beta)
     d = _desc_for(q, v, chunk, l2norm, save_states, force_simt, eps, segments)
     B, H, L, Dk = q.shape
     Dv = v.shape[-1]
+    _need_out(h0, "h0", (B, H, Dk, Dv), torch.float32, dev)
+    _need_out(out, "out", (B, H, L, Dv), q.dtype, dev)
     o = out if out is not None else torch.empty((B, H, L, Dv), dtype=q.dtype, device=dev)
     hT = torch.empty((B, H, Dk, Dv), dtype=torch.float32, device=dev) if want_hT else None
     if workspace is None:
         workspace = alloc_workspace(d, dev)
+    _need(workspace, "workspace", torch.uint8, dev)
     rc = lib.deltanet_fwd(ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(beta), _ptr(h0),
                           _ptr(o), _ptr(hT), _ptr(workspace), workspace.numel(), _stream(dev))
     _check(rc, "deltanet_fwd")
@@ -207,8 +226,12 @@ def deltanet_recurrent_fwd(q, k, v, beta, *, l2norm=True, h0=None, want_hT=True,
         _need(t, n, q.dtype, dev)
     _need(h0, "h0", torch.float32, dev)
     _need(hT, "hT", torch.float32, dev)
+    _need_inputs(q, k, v, beta)
     B, H, L, Dk = q.shape
     Dv = v.shape[-1]
+    for t, n in ((h0, "h0"), (hT, "hT")):
+        _need_out(t, n, (B, H, Dk, Dv), torch.float32, dev)
+    _need_out(out, "out", (B, H, L, Dv), q.dtype, dev)
     d = make_desc(B, H, L, Dk, Dv, 64, q.dtype, l2norm=l2norm, eps=eps)
     o = out if out is not None else torch.empty((B, H, L, Dv), dtype=q.dtype, device=dev)
     if hT is None and want_hT:
@@ -241,6 +264,10 @@ def deltanet_prologue_fwd(xq, xk, xv, xb, wq, wk, wv, *, silu_v=False, out=None)
     B, L, H, Dk = xq.shape
     Dv = xv.shape[-1]
     d = _prologue_desc(xq, xv, silu_v)
+    if out is not None:
+        for t, n, shp in zip(out, ("q", "k", "v", "beta"),
+                             ((B, H, L, Dk), (B, H, L, Dk), (B, H, L, Dv), (B, H, L))):
+            _need_out(t, n, shp, xq.dtype, dev)
     if out is None:
         out = (torch.empty((B, H, L, Dk), dtype=xq.dtype, device=dev),
                torch.empty((B, H, L, Dk), dtype=xq.dtype, device=dev),
@@ -268,6 +295,10 @@ def deltanet_prologue_bwd(xq, xk, xv, xb, wq, wk, wv, dq, dk, dv, dbeta, *, silu
         out = (torch.empty_like(xq), torch.empty_like(xk), torch.empty_like(xv),
                torch.empty_like(xb), torch.empty_like(wq), torch.empty_like(wk),
                torch.empty_like(wv))
+    else:
+        for t, ref, n in zip(out, (xq, xk, xv, xb, wq, wk, wv),
+                             ("dxq", "dxk", "dxv", "dxb", "dwq", "dwk", "dwv")):
+            _need_out(t, n, ref.shape, ref.dtype, dev)
     rc = lib.deltanet_prologue_bwd(ctypes.byref(d), _ptr(xq), _ptr(xk), _ptr(xv), _ptr(xb),
                                    _ptr(wq), _ptr(wk), _ptr(wv), _ptr(dq), _ptr(dk), _ptr(dv),
                                    _ptr(dbeta), *[_ptr(t) for t in out], _ptr(workspace),
@@ -293,16 +324,22 @@ def deltanet_bwd(q, k, v, beta, dO, *, chunk=64, l2norm=True, h0=None, dhT=None,
     d = _desc_for(q, v, chunk, l2norm, states_saved, force_simt, eps, segments)
     B, H, L, Dk = q.shape
     Dv = v.shape[-1]
+    _need_inputs(q, k, v, beta, dO)
     if out is not None:
         dq, dk, dv, db = out
+        for t, ref, n in ((dq, q, "dq"), (dk, k, "dk"), (dv, v, "dv"), (db, beta, "dbeta")):
+            _need_out(t, n, ref.shape, ref.dtype, dev)
     else:
         dq = torch.empty_like(q)
         dk = torch.empty_like(k)
         dv = torch.empty_like(v)
         db = torch.empty_like(beta)
+    for t, n in ((h0, "h0"), (dhT, "dhT")):
+        _need_out(t, n, (B, H, Dk, Dv), torch.float32, dev)
     dh0 = torch.empty((B, H, Dk, Dv), dtype=torch.float32, device=dev) if want_dh0 else None
     if workspace is None:
         workspace = alloc_workspace(d, dev)
+    _need(workspace, "workspace", torch.uint8, dev)
     rc = lib.deltanet_bwd(ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(beta), _ptr(h0),
                           _ptr(dO), _ptr(dhT), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(db),
                           _ptr(dh0), _ptr(workspace), workspace.numel(), _stream(dev))
@@ -325,10 +362,11 @@ def deltanet_fwd_transition(q, k, v, beta, *, l2norm=True, eps=1e-6, psi=None, h
         psi = torch.empty((B, H, Dk, Dk), dtype=torch.float32, device=dev)
     if hloc is None:
         hloc = torch.empty((B, H, Dk, Dv), dtype=torch.float32, device=dev)
-    _need(psi, "psi", torch.float32, dev)
-    _need(hloc, "hloc", torch.float32, dev)
+    _need_out(psi, "psi", (B, H, Dk, Dk), torch.float32, dev)
+    _need_out(hloc, "hloc", (B, H, Dk, Dv), torch.float32, dev)
     if workspace is None:
         workspace = alloc_workspace(d, dev)
+    _need(workspace, "workspace", torch.uint8, dev)
     rc = lib.deltanet_fwd_transition(ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(beta),
                                      _ptr(psi), _ptr(hloc), _ptr(workspace), workspace.numel(),
                                      _stream(dev))
@@ -352,9 +390,10 @@ def deltanet_bwd_transition(q, k, v, beta, dO, *, l2norm=True, eps=1e-6, workspa
     d = make_desc(B, H, L, Dk, Dv, 64, q.dtype, l2norm=l2norm, save_states=states_saved, eps=eps)
     if workspace is None:
         workspace = alloc_workspace(d, dev)
+    _need(workspace, "workspace", torch.uint8, dev)
     if dhloc is None:
         dhloc = torch.empty((B, H, Dk, Dv), dtype=torch.float32, device=dev)
-    _need(dhloc, "dhloc", torch.float32, dev)
+    _need_out(dhloc, "dhloc", (B, H, Dk, Dv), torch.float32, dev)
     rc = lib.deltanet_bwd_transition(ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(beta),
                                      _ptr(dO), _ptr(dhloc), _ptr(workspace), workspace.numel(),
                                      _stream(dev))
@@ -374,7 +413,9 @@ def deltanet_state_scan(psi_all, loc_all, part, *, reverse=False, edge=None, out
         _need(t, n, torch.float32, dev)
     if out is None:
         out = torch.empty((B, H, Dk, Dv), dtype=torch.float32, device=dev)
-    _need(out, "out", torch.float32, dev)
+    _need_out(out, "out", (B, H, Dk, Dv), torch.float32, dev)
+    if tuple(psi_all.shape) != (P, B, H, Dk, Dk):
+        raise DeltaNetError("psi_all must be [P,B,H,Dk,Dk]")
     d = make_desc(B, H, 0, Dk, Dv, 64, torch.bfloat16)
     rc = lib.deltanet_state_scan(ctypes.byref(d), int(P), int(part), int(bool(reverse)),
                                  _ptr(psi_all), _ptr(loc_all), _ptr(edge), _ptr(out),
@@ -393,13 +434,18 @@ def deltanet_gated_fwd(q, k, v, beta, g, *, chunk=64, l2norm=True, h0=None, save
         _need(t, n, q.dtype, dev)
     _need(g, "g", torch.float32, dev)
     _need(h0, "h0", torch.float32, dev)
+    _need_inputs(q, k, v, beta)
     d = _desc_for(q, v, chunk, l2norm, save_states, force_simt, eps, gated=True)
     B, H, L, Dk = q.shape
     Dv = v.shape[-1]
+    _need_out(g, "g", (B, H, L), torch.float32, dev)
+    _need_out(h0, "h0", (B, H, Dk, Dv), torch.float32, dev)
+    _need_out(out, "out", (B, H, L, Dv), q.dtype, dev)
     o = out if out is not None else torch.empty((B, H, L, Dv), dtype=q.dtype, device=dev)
     hT = torch.empty((B, H, Dk, Dv), dtype=torch.float32, device=dev) if want_hT else None
     if workspace is None:
         workspace = alloc_workspace(d, dev)
+    _need(workspace, "workspace", torch.uint8, dev)
     rc = lib.deltanet_gated_fwd(ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(beta), _ptr(g),
                                 _ptr(h0), _ptr(o), _ptr(hT), _ptr(workspace), workspace.numel(),
                                 _stream(dev))
@@ -419,14 +465,19 @@ def deltanet_gated_bwd(q, k, v, beta, g, dO, *, chunk=64, l2norm=True, h0=None, 
         _need(t, n, torch.float32, dev)
     if workspace is None:
         states_saved = False
+    _need_inputs(q, k, v, beta, dO)
     d = _desc_for(q, v, chunk, l2norm, states_saved, force_simt, eps, gated=True)
     B, H, L, Dk = q.shape
     Dv = v.shape[-1]
+    _need_out(g, "g", (B, H, L), torch.float32, dev)
+    for t, n in ((h0, "h0"), (dhT, "dhT")):
+        _need_out(t, n, (B, H, Dk, Dv), torch.float32, dev)
     dq, dk, dv, db = (torch.empty_like(t) for t in (q, k, v, beta))
     dg = torch.empty_like(g)
     dh0 = torch.empty((B, H, Dk, Dv), dtype=torch.float32, device=dev) if want_dh0 else None
     if workspace is None:
         workspace = alloc_workspace(d, dev)
+    _need(workspace, "workspace", torch.uint8, dev)
     rc = lib.deltanet_gated_bwd(ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(beta), _ptr(g),
                                 _ptr(h0), _ptr(dO), _ptr(dhT), _ptr(dq), _ptr(dk), _ptr(dv),
                                 _ptr(db), _ptr(dg), _ptr(dh0), _ptr(workspace),
@@ -445,8 +496,13 @@ def deltanet_gated_recurrent_fwd(q, k, v, beta, g, *, l2norm=True, h0=None, want
         _need(t, n, q.dtype, dev)
     for t, n in ((g, "g"), (h0, "h0"), (hT, "hT")):
         _need(t, n, torch.float32, dev)
+    _need_inputs(q, k, v, beta)
     B, H, L, Dk = q.shape
     Dv = v.shape[-1]
+    _need_out(g, "g", (B, H, L), torch.float32, dev)
+    for t, n in ((h0, "h0"), (hT, "hT")):
+        _need_out(t, n, (B, H, Dk, Dv), torch.float32, dev)
+    _need_out(out, "out", (B, H, L, Dv), q.dtype, dev)
     d = make_desc(B, H, L, Dk, Dv, 64, q.dtype, l2norm=l2norm, eps=eps)
     o = out if out is not None else torch.empty((B, H, L, Dv), dtype=q.dtype, device=dev)
     if hT is None and want_hT:
@@ -471,6 +527,10 @@ def deltanet_fwd_bwd_host(q, k, v, beta, dO, *, out, slabs=8, chunk=64, l2norm=T
             raise DeltaNetError(f"{n} must be a host tensor for deltanet_fwd_bwd_host")
         if not t.is_contiguous() or t.dtype != q.dtype:
             raise DeltaNetError(f"{n} must be contiguous with dtype {q.dtype}")
+    _need_inputs(q, k, v, beta, dO)
+    for t, ref, n in zip(out, (v, q, k, v, beta), "o dq dk dv dbeta".split()):
+        if t.shape != ref.shape:
+            raise DeltaNetError(f"{n} has shape {tuple(t.shape)}, expected {tuple(ref.shape)}")
     B, H, L, Dk = q.shape
     d = make_desc(B, H, L, Dk, v.shape[-1], chunk, q.dtype, l2norm=l2norm, eps=eps)
     need = int(lib.deltanet_fwd_bwd_host_device_bytes(ctypes.byref(d), int(slabs)))

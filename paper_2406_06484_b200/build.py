@@ -30,6 +30,18 @@ def headers():
                   glob.glob(os.path.join(ROOT, "include", "*.h")))
 
 
+def sources_sha() -> str:
+    """sha256 (16 hex) of the kernel sources and the ABI header: ties a
+    profile (profiles/ncu_traffic.json) to the code it measured; .git does
+    not travel to the GPU box, the sources do."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in sources() + headers():
+        h.update(os.path.relpath(f, ROOT).encode())
+        h.update(open(f, "rb").read())
+    return h.hexdigest()[:16]
+
+
 def stale() -> bool:
     if not os.path.exists(LIB):
         return True

@@ -39,6 +39,20 @@ bool use_tc(const deltanet_desc* d) {
 
 bool use_tc_bwd(const deltanet_desc* d) { return use_tc(d); }
 
+// bf16 I/O runs on the tcgen05 kernels only: a bf16 descriptor outside their
+// shapes is UNSUPPORTED unless the caller asks for the CUDA-core kernels
+// explicitly (DELTANET_FORCE_SIMT) -- no silent 10^3-10^4x slower fallback.
+// fp32 I/O (the 1e-4 parity mode) always runs on the CUDA-core kernels.
+int validate_path(const deltanet_desc* d) {
+  int rc = validate(d);
+  if (rc) return rc;
+  deltanet_desc e = *d;  // L = 0 (nothing to compute) keeps its shape's path
+  if (e.L == 0) e.L = 1;
+  if (e.dtype == DELTANET_BF16 && !(e.flags & DELTANET_FORCE_SIMT) && !use_tc(&e))
+    return DELTANET_ERR_UNSUPPORTED;
+  return DELTANET_OK;
+}
+
 size_t elem_bytes(const deltanet_desc* d) { return d->dtype == DELTANET_FP32 ? 4 : 2; }
 
 size_t states_bytes(const deltanet_desc* d) {
@@ -103,7 +117,16 @@ SlabLayout slab_layout(const deltanet_desc* d, int slabs) {
                bb = per_row_tok * eb;
   sl.in_bytes = round_up(sl.rows * qk) * 2 + round_up(sl.rows * vv) * 2 + round_up(sl.rows * bb);
   sl.out_bytes = sl.in_bytes;  // o dq dk dv dbeta have the shapes of v q k dO beta
+  // the shared workspace must fit every slab's descriptor: a short last slab
+  // can pick more sequence segments (more segment scratch) than a full one
+  // (ADVICE r1), so size it for the larger of the two
   sl.ws_bytes = round_up(deltanet_workspace_bytes(&e));
+  const int last = units - (units - 1) / sl.rows * sl.rows;
+  if (units > 0 && last != sl.rows) {
+    e.B = last;
+    const size_t wl = round_up(deltanet_workspace_bytes(&e));
+    if (wl > sl.ws_bytes) sl.ws_bytes = wl;
+  }
   return sl;
 }
 
@@ -112,12 +135,12 @@ SlabLayout slab_layout(const deltanet_desc* d, int slabs) {
 extern "C" {
 
 size_t deltanet_workspace_bytes(const deltanet_desc* d) {
-  if (validate(d) != DELTANET_OK) return 0;
+  if (validate_path(d) != DELTANET_OK) return 0;
   return round_up(states_bytes(d)) + round_up(scratch_bytes(d));
 }
 
 int deltanet_path(const deltanet_desc* d) {
-  if (validate(d) != DELTANET_OK) return -1;
+  if (validate_path(d) != DELTANET_OK) return -1;
   return use_tc(d) ? 1 : 0;
 }
 
@@ -135,7 +158,7 @@ int deltanet_launch_count(const deltanet_desc* d, int which) {
     if (which == 6 && !(d->flags & DELTANET_SAVE_STATES)) return tr + dn::tc_launch_count(d, 0);
     return tr;
   }
-  if (validate(d) != DELTANET_OK) return -1;
+  if (validate_path(d) != DELTANET_OK) return -1;
   if ((size_t)d->B * d->H == 0) return 0;
   if (which == 1 ? use_tc_bwd(d) : use_tc(d)) return dn::tc_launch_count(d, which);
   return 1;
@@ -144,7 +167,7 @@ int deltanet_launch_count(const deltanet_desc* d, int which) {
 static int fwd_impl(const deltanet_desc* d, const void* q, const void* k, const void* v,
                     const void* beta, const float* g, const float* h0, void* o, float* hT,
                     void* workspace, size_t workspace_bytes, void* stream) {
-  int rc = validate(d);
+  int rc = validate_path(d);
   if (rc) return rc;
   const size_t units = (size_t)d->B * d->H;
   const bool tokens = units && d->L > 0;  // L = 0: token tensors may be empty (null)
@@ -181,7 +204,7 @@ static int bwd_impl(const deltanet_desc* d, const void* q, const void* k, const 
                     const void* beta, const float* g, const float* h0, const void* dO,
                     const float* dhT, void* dq, void* dk, void* dv, void* dbeta, float* dg,
                     float* dh0, void* workspace, size_t workspace_bytes, void* stream) {
-  int rc = validate(d);
+  int rc = validate_path(d);
   if (rc) return rc;
   const size_t units = (size_t)d->B * d->H;
   const bool tokens = units && d->L > 0;
@@ -302,7 +325,7 @@ int deltanet_prologue_bwd(const deltanet_desc* d, const void* xq, const void* xk
 
 // ---- host-buffer pipeline (include/deltanet.h deltanet_fwd_bwd_host) ----
 size_t deltanet_fwd_bwd_host_device_bytes(const deltanet_desc* d, int slabs) {
-  if (validate(d) != DELTANET_OK || slabs < 1) return 0;
+  if (validate_path(d) != DELTANET_OK || slabs < 1) return 0;
   const int units = d->B * d->H;
   if (slabs > units) slabs = units > 0 ? units : 1;
   const SlabLayout sl = slab_layout(d, slabs);
@@ -313,7 +336,7 @@ int deltanet_fwd_bwd_host(const deltanet_desc* d, const void* q, const void* k, 
                           const void* beta, const void* dO, void* o, void* dq, void* dk,
                           void* dv, void* dbeta, int slabs, void* dev_buffer,
                           size_t dev_bytes, void* stream) {
-  int rc = validate(d);
+  int rc = validate_path(d);
   if (rc) return rc;
   if (slabs < 1) return DELTANET_ERR_INVALID_ARG;
   const size_t units = (size_t)d->B * d->H;

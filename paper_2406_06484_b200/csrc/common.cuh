@@ -4,9 +4,31 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "../../include/deltanet.h"
 
 namespace dn {
+
+// Current device ordinal (0 if the query fails), for per-device host caches.
+inline int cur_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess) {
+    cudaGetLastError();
+    d = 0;
+  }
+  return d & 63;
+}
+
+// One-time setup flags kept per device: kernel attributes such as the
+// dynamic shared-memory opt-in belong to a device context, so a process that
+// drives several GPUs must set them on each.  Concurrent first calls may both
+// run the (idempotent) setup.
+struct PerDevice {
+  std::atomic<unsigned long long> bits{0};
+  bool done() const { return (bits.load() >> cur_device()) & 1ull; }
+  void mark() { bits.fetch_or(1ull << cur_device()); }
+};
 
 // All tensor arguments of one fwd or bwd call (see include/deltanet.h).
 struct Args {

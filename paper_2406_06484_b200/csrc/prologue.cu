@@ -639,12 +639,12 @@ int prologue_fwd(const deltanet_desc* d, const void* xq, const void* xk, const v
   a.xq = xq; a.xk = xk; a.xv = xv; a.xb = xb; a.wq = wq; a.wk = wk; a.wv = wv;
   a.q = q; a.k = k; a.v = v; a.beta = beta;
   if (d->dtype == DELTANET_BF16 && d->Dk == DT && d->Dv == DT && d->L > 0) {
-    static bool attr = false;
-    if (!attr) {
+    static PerDevice attr;
+    if (!attr.done()) {
       if (cudaFuncSetAttribute(prologue_fwd_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                TMA_SMEM) != cudaSuccess)
         return DELTANET_ERR_CUDA;
-      attr = true;
+      attr.mark();
     }
     CUtensorMap mq, mk, mv;
     const int HD = d->H * DT;
@@ -678,12 +678,12 @@ int prologue_bwd(const deltanet_desc* d, const void* xq, const void* xk, const v
   a.dwq = dwq; a.dwk = dwk; a.dwv = dwv;
   a.part = (float*)ws;
   if (d->dtype == DELTANET_BF16 && d->Dk == DT && d->Dv == DT && d->L > 0) {
-    static bool attr = false;
-    if (!attr) {
+    static PerDevice attr;
+    if (!attr.done()) {
       if (cudaFuncSetAttribute(prologue_bwd_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                TMA_SMEM_B) != cudaSuccess)
         return DELTANET_ERR_CUDA;
-      attr = true;
+      attr.mark();
     }
     CUtensorMap mxq, mxk, mxv, mgq, mgk, mgv;
     const int HD = d->H * DT, BH = d->B * d->H;

@@ -167,13 +167,13 @@ int launch(const Args& a, cudaStream_t s) {
   const int threads = VB * S::TPC;  // 16..256, a multiple of 16
   const int nthreads = (threads + 31) / 32 * 32;
   const size_t smem = (size_t)(2 * TB * S::KS + 2 * TB * VB + 2 * TB) * sizeof(float);
-  static bool attr = false;  // per template instance: the largest (VB = 64) footprint
-  if (!attr) {
+  static PerDevice attr;  // per template instance: the largest (VB = 64) footprint
+  if (!attr.done()) {
     const size_t smax = (size_t)(2 * TB * S::KS + 2 * TB * 64 + 2 * TB) * sizeof(float);
     if (cudaFuncSetAttribute(rec_fwd_kernel<T, DK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smax) != cudaSuccess)
       return DELTANET_ERR_CUDA;
-    attr = true;
+    attr.mark();
   }
   dim3 grid(a.B * a.H, a.Dv / VB);
   rec_fwd_kernel<T, DK><<<grid, nthreads, smem, s>>>(a, VB);

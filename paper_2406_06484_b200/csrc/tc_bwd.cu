@@ -120,9 +120,10 @@ __device__ __forceinline__ float reduce_scatter(float (&v)[N], int lane) {
   }
   return v[0];
 }
-// Gamma(i, j) = e^{G_i - G_j} (j <= i; clamped at 1 above the diagonal)
+// Gamma(i, j) = e^{G_i - G_j} for j <= i; 1 above the diagonal (masked by
+// index, not by clamping the exponent: g > 0 is allowed)
 __device__ __forceinline__ float gamma_ij(const float* gG, int i, int j) {
-  return __expf(fminf(gG[i] - gG[j], 0.f));
+  return __expf(j <= i ? gG[i] - gG[j] : 0.f);
 }
 __device__ __forceinline__ void ld16f(uint32_t tm, int wwarp, uint32_t col, float (&f)[16]) {
   uint32_t r[16];
@@ -1210,8 +1211,8 @@ __global__ void __launch_bounds__(256) seg_scan_bwd_kernel(Args a) {
 int tc_fwd(const Args& a, cudaStream_t s);
 
 int tc_bwd(const Args& a0, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static PerDevice attr;
+  if (!attr.done()) {
     if (cudaFuncSetAttribute(tc_bwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              SMEM_BYTES) != cudaSuccess ||
         cudaFuncSetAttribute(tc_bwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1219,7 +1220,7 @@ int tc_bwd(const Args& a0, cudaStream_t s) {
         cudaFuncSetAttribute(tc_bwd_kernel<false, true>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess)
       return DELTANET_ERR_CUDA;
-    attr = true;
+    attr.mark();
   }
   Args a = a0;
   if (!(a.flags & DELTANET_SAVE_STATES)) {
@@ -1269,12 +1270,12 @@ int tc_bwd_transition(const Args& a0, float* dhloc, cudaStream_t s) {
       !make_il_map(&mDQ, a.q, BH, a.L, D, C) || !make_il_map(&mDK, a.k, BH, a.L, D, C) ||
       !make_il_map(&mDV, a.v, BH, a.L, D, C))
     return DELTANET_ERR_CUDA;
-  static bool attr = false;
-  if (!attr) {
+  static PerDevice attr;
+  if (!attr.done()) {
     if (cudaFuncSetAttribute(tc_bwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              SMEM_BYTES) != cudaSuccess)
       return DELTANET_ERR_CUDA;
-    attr = true;
+    attr.mark();
   }
   const int nseg = tc_seg_setup(a);
   if (nseg <= 1) {

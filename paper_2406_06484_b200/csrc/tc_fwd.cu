@@ -148,6 +148,10 @@ __global__ void __launch_bounds__(NT, 1)
   __shared__ uint64_t q_full[2], k_full[3], v_full[2], bar_full[2], bar_empty[2], q_done;
   __shared__ uint64_t g_done, g_free, t_ready, w_done, wu_done, w_free;  // prep side
   __shared__ uint64_t up_done, z_free, z_ready, ho_done, h_ready, st_free;  // state side
+  // q_read: the state warpgroup's norm pass has finished reading Q[b] (the
+  // chain warp may then overwrite the slot with Q of chunk c+2; ADVICE r1:
+  // q_done alone does not order those generic-proxy reads before the TMA)
+  __shared__ uint64_t q_read;
   __shared__ uint32_t tslot;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -186,6 +190,7 @@ __global__ void __launch_bounds__(NT, 1)
     mbar_init(&ho_done, 1);
     mbar_init(&h_ready, 1);
     mbar_init(&st_free, 1);
+    mbar_init(&q_read, 1);
     mbar_fence_init();
     prefetch_tmap(&mQ);
     prefetch_tmap(&mK);
@@ -328,10 +333,13 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const float4 g4 = *reinterpret_cast<const float4*>(vb + 3 * C + c0 + 4 * q);
-            gam16[4 * q + 0] = __expf(fminf(Gi - g4.x, 0.f));
-            gam16[4 * q + 1] = __expf(fminf(Gi - g4.y, 0.f));
-            gam16[4 * q + 2] = __expf(fminf(Gi - g4.z, 0.f));
-            gam16[4 * q + 3] = __expf(fminf(Gi - g4.w, 0.f));
+            // masked by index, not clamped: with g > 0 allowed, G_i - G_j
+            // may be positive for j <= i; j > i is masked below
+            const int j = c0 + 4 * q;
+            gam16[4 * q + 0] = __expf(j + 0 <= i ? Gi - g4.x : 0.f);
+            gam16[4 * q + 1] = __expf(j + 1 <= i ? Gi - g4.y : 0.f);
+            gam16[4 * q + 2] = __expf(j + 2 <= i ? Gi - g4.z : 0.f);
+            gam16[4 * q + 3] = __expf(j + 3 <= i ? Gi - g4.w : 0.f);
           }
         }
         {  // A = tril(Q K^T), raw (inclusive, R4); gated: Gamma . A
@@ -536,6 +544,7 @@ __global__ void __launch_bounds__(NT, 1)
           for (int g = 0; g < DK / 16; ++g) il_store8(sQ(b), C, row, DK / 2 * hh + g * 8, x + 8 * g);
         }
         wg_sync(BAR_S);
+        if (w == 0) mbar_arrive(&q_read);  // every thread's reads of sQ(b) are done
         const int i = wwarp * 16 + (lane & 15);
         const float nrm = sqrtf(qn2[i] + qn2[C + i]);
         ri = l2 ? 1.f / fmaxf(nrm, a.eps) : 1.f;
@@ -819,13 +828,14 @@ __global__ void __launch_bounds__(NT, 1)
           for (int k0 = 0; k0 < DK; k0 += 16)
             mma_bf16(tm + TM_O, desc_k(aq, C, k0), desc_k(aH, DV, k0), ido, k0 > 0);
         }
-        mma_commit(&q_done);  // Q[b] read (the state warpgroup's norms precede bar_full)
+        mma_commit(&q_done);  // Q[b] read by the tensor core (norm reads: q_read)
         // the O store of chunk c-1 must finish reading sO (= sZ) before Z is written
         asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(1) : "memory");
         if (!states) bulk_wait_read0();
         mbar_arrive(&z_free);
         mbar_wait(&q_done, c & 1);
         if (c + 2 < NC) {  // Q of chunk c+2 into the slot O = Q H has released
+          if (!SEG1) mbar_wait(&q_read, c & 1);  // ... and the norm pass (SEG1 has none)
           mbar_expect_tx(&q_full[b], TILE);
           tma_load_4d(sQ(b), &mQ, 0, T0 + (c + 2) * C, 0, unit, &q_full[b]);
         }
@@ -1064,15 +1074,16 @@ bool tc_gated_supported(const deltanet_desc*) { return true; }
 
 // per-chunk records [X | Z^T | row norms] the backward reads (tc_common.cuh REC_*)
 namespace {
-int sm_count() {
-  static int n = 0;
+int sm_count() {  // per device (a process may drive several GPUs)
+  static std::atomic<int> cache[64];
+  const int dev = cur_device();
+  int n = cache[dev].load();
   if (!n) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess ||
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
       cudaGetLastError();
       n = 148;  // B200
     }
+    cache[dev].store(n);
   }
   return n;
 }
@@ -1132,8 +1143,8 @@ int tc_seg_setup(Args& a) {
 }
 
 int tc_fwd(const Args& a0, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static PerDevice attr;
+  if (!attr.done()) {
     if (cudaFuncSetAttribute(tc_fwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              SMEM_BYTES) != cudaSuccess ||
         cudaFuncSetAttribute(tc_fwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1141,7 +1152,7 @@ int tc_fwd(const Args& a0, cudaStream_t s) {
         cudaFuncSetAttribute(tc_fwd_kernel<false, true>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess)
       return DELTANET_ERR_CUDA;
-    attr = true;
+    attr.mark();
   }
   Args a = a0;
   const int BH = a.B * a.H;
@@ -1176,12 +1187,12 @@ int tc_fwd_transition(const Args& a0, float* psi, float* hloc, cudaStream_t s) {
   if (!make_il_map(&mQ, a.q, BH, a.L, DK, C) || !make_il_map(&mK, a.k, BH, a.L, DK, C) ||
       !make_il_map(&mV, a.v, BH, a.L, DV, C) || !make_il_map(&mO, a.v, BH, a.L, DV, C))
     return DELTANET_ERR_CUDA;
-  static bool attr = false;
-  if (!attr) {
+  static PerDevice attr;
+  if (!attr.done()) {
     if (cudaFuncSetAttribute(tc_fwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              SMEM_BYTES) != cudaSuccess)
       return DELTANET_ERR_CUDA;
-    attr = true;
+    attr.mark();
   }
   a.o = nullptr;
   a.hT = nullptr;

@@ -51,7 +51,7 @@ def test_abi_version_and_strerror(lib):
 
 
 def _desc(**kw):
-    base = dict(B=2, H=3, L=100, Dk=64, Dv=64, chunk=64, dtype=0, flags=1, l2_eps=1e-6)
+    base = dict(B=2, H=3, L=100, Dk=128, Dv=128, chunk=64, dtype=0, flags=1, l2_eps=1e-6)
     base.update(kw)
     return dn.deltanet_desc(**base)
 
@@ -68,6 +68,29 @@ def test_workspace_and_validation(lib):
     assert dn.deltanet_path(_desc(Dk=48)) == -1
     assert dn.deltanet_path(_desc(dtype=1)) == 0                   # fp32 -> SIMT
     assert dn.deltanet_path(_desc(flags=1 | 4)) == 0               # FORCE_SIMT
+    assert dn.deltanet_path(_desc()) == 1                          # tcgen05
+    assert dn.deltanet_path(_desc(L=0)) != -1                     # L = 0: nothing to run
+
+
+@pytest.mark.parametrize("shape", [dict(Dk=64, Dv=64), dict(chunk=128), dict(chunk=32),
+                                   dict(Dk=128, Dv=64), dict(Dk=16, Dv=16, chunk=16)])
+def test_bf16_outside_tcgen05_shapes_is_unsupported(lib, shape):
+    """bf16 descriptors outside the tcgen05 shapes are refused (UNSUPPORTED,
+    before any launch) unless DELTANET_FORCE_SIMT asks for the CUDA-core
+    kernels explicitly: no silent fallback 10^3-10^4x below the roofline.
+    fp32 I/O (the parity mode) always runs on the CUDA-core kernels."""
+    D = ctypes.byref
+    nul = None
+    a = ctypes.c_void_p(16 * 1024)
+    d = _desc(**shape)
+    assert dn.deltanet_path(d) == -1
+    assert dn.deltanet_workspace_bytes(d) == 0
+    assert dn.deltanet_launch_count(d, 0) == -1
+    assert lib.deltanet_fwd(D(d), a, a, a, a, nul, a, nul, a, 1 << 34, nul) == 2
+    assert lib.deltanet_bwd(D(d), a, a, a, a, nul, a, nul, a, a, a, a, nul, a, 1 << 34, nul) == 2
+    forced = _desc(flags=1 | dn.DELTANET_FORCE_SIMT, **shape)
+    assert dn.deltanet_path(forced) == 0 and dn.deltanet_workspace_bytes(forced) > 0
+    assert dn.deltanet_path(_desc(dtype=1, **shape)) == 0
 
 
 def test_errors_before_launch(lib):

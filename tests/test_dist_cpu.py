@@ -1,8 +1,9 @@
 """Multi-process (gloo, world_size 2, CPU) test of the sharding / gather
-logic bench.py uses on 8 B200: rank r owns batch rows [8r, 8r+8) of the
-B=64 "sharded" config, the (b, h) units are independent (no collective in
-the step), and an all-gather of the per-rank outputs reassembles exactly the
-single-process result.  The fp64 oracle stands in for the kernel here (test
+code bench.py uses on N B200 (paper_2406_06484_b200.data_parallel): rank r
+owns the contiguous batch rows shard_rows(B, N, r) of the B=64 "sharded"
+config, the (b, h) units are independent (no collective in the step), and
+an all-gather of the per-rank outputs reassembles exactly the
+single-process result.  The fp64 oracle stands in for the kernels here (test
 infrastructure); the GPU path is covered by tests/test_gpu_parity.py."""
 import os
 import socket
@@ -25,52 +26,88 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, B_per, cfg_kw, out_q):
+def _dp_oracle_ops():
+    """Stand-in for the CUDA calls ShardedStep makes (same signatures), on
+    fp64 CPU tensors: the oracle.  Test infrastructure only."""
+    from types import SimpleNamespace
+    n = lambda t: t.numpy()
+
+    def fwd(q, k, v, beta, *, chunk, workspace, want_hT, out):
+        o, _ = oracle.recurrent_fwd(n(q), n(k), n(v), n(beta), nthreads=1)
+        out.copy_(torch.from_numpy(o))
+
+    def bwd(q, k, v, beta, dO, *, chunk, workspace, want_dh0, out):
+        g = oracle.recurrent_bwd(n(q), n(k), n(v), n(beta), n(dO), nthreads=1)
+        for t, a in zip(out, g[:4]):
+            t.copy_(torch.from_numpy(a))
+    return SimpleNamespace(fwd=fwd, bwd=bwd, alloc=lambda q, v, chunk: None)
+
+
+def _worker(rank, world, port, B_total, cfg_kw, out_q):
+    """One rank of bench.py's data-parallel step, through the package's own
+    sharding code (paper_2406_06484_b200.data_parallel): its rows of the
+    seeded inputs, the local fwd + bwd (oracle ops), the max-over-ranks
+    timing rule, and the gather of outputs and gradients."""
+    from paper_2406_06484_b200 import data_parallel as dp
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     cfg = synth.custom_config(**cfg_kw)
-    rows = range(rank * B_per, (rank + 1) * B_per)
+    rows = dp.shard_rows(B_total, world, rank)
     x = synth.make_inputs(cfg, b_range=rows)
-    o, _ = oracle.recurrent_fwd(x["q"], x["k"], x["v"], x["beta"], nthreads=1)
-    dq, dk, dv, db, _ = oracle.recurrent_bwd(x["q"], x["k"], x["v"], x["beta"], x["dO"],
-                                            nthreads=1)
-    outs = []
-    for t in (o, dq, dk, dv, db):
-        local = torch.from_numpy(np.ascontiguousarray(t))
-        full = [torch.empty_like(local) for _ in range(world)]
-        dist.all_gather(full, local)
-        outs.append(torch.cat(full, 0).numpy())
-    # timing protocol of bench.py: max over ranks
-    t = torch.tensor([float(rank + 1)])
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t = {f: torch.from_numpy(np.ascontiguousarray(x[f], dtype=np.float64))
+         for f in ("q", "k", "v", "beta", "dO")}
+    st = dp.ShardedStep(t["q"], t["k"], t["v"], t["beta"], t["dO"], B_total=B_total,
+                        chunk=cfg.chunk, ops=_dp_oracle_ops())
+    st.step()
+    outs = [a.numpy() for a in st.gather()]
+    tmax = dp.max_over_ranks([rank + 1.0, 10.0 * (rank + 1)], "cpu")
     if rank == 0:
-        out_q.put((outs, t.item()))
+        out_q.put((outs, tmax, st.world, [len(dp.shard_rows(B_total, world, r))
+                                          for r in range(world)]))
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_shard_gather_matches_single_process():
-    world, B_per = 2, 2
-    cfg_kw = dict(B=world * B_per, H=2, L=40, Dk=8, Dv=8, chunk=16, dtype="bf16", index=77)
+@pytest.mark.parametrize("B_total", [4, 5])
+def test_shard_gather_matches_single_process(B_total):
+    """2 gloo ranks: the gathered outputs and gradients have the full
+    [B, H, L, d] layout and equal the single-process result bit for bit
+    (B = 5: uneven slabs 3 + 2, padded in the gather)."""
+    world = 2
+    cfg_kw = dict(B=B_total, H=2, L=40, Dk=8, Dv=8, chunk=16, dtype="bf16", index=77)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, B_per, cfg_kw, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, B_total, cfg_kw, q))
              for r in range(world)]
     for p in procs:
         p.start()
-    outs, tmax = q.get(timeout=120)
+    outs, tmax, n_gpus, sizes = q.get(timeout=120)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    assert tmax == world  # max over ranks
+    assert n_gpus == 2
+    assert sizes == [(B_total + 1) // 2, B_total // 2]
+    assert tmax == [2.0, 20.0]  # max over ranks, element-wise
     cfg = synth.custom_config(**cfg_kw)
     x = synth.make_inputs(cfg)
     o, _ = oracle.recurrent_fwd(x["q"], x["k"], x["v"], x["beta"], nthreads=1)
     ref = [o, *oracle.recurrent_bwd(x["q"], x["k"], x["v"], x["beta"], x["dO"], nthreads=1)[:4]]
-    for a, b in zip(outs, ref):
+    shapes = [(B_total, 2, 40, 8)] * 4 + [(B_total, 2, 40)]
+    for a, b, shp in zip(outs, ref, shapes):
+        assert a.shape == shp
         assert np.array_equal(a, b)
+
+
+def test_shard_rows_cover_the_batch():
+    from paper_2406_06484_b200.data_parallel import shard_rows
+    for B in (1, 7, 8, 64):
+        for world in (1, 2, 3, 8):
+            rs = [shard_rows(B, world, r) for r in range(world)]
+            assert [i for r in rs for i in r] == list(range(B))
+            assert max(map(len, rs)) - min(map(len, rs)) <= 1
+    assert shard_rows(64, 8, 3) == range(24, 32)   # configs[4] at 8 GPUs: 8 rows per rank
 
 
 def test_rank_slab_seeds_are_unit_local():

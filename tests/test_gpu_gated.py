@@ -258,3 +258,18 @@ def test_bf16_tcgen05_backward_zero_gate_matches_ungated():
     ung = {"dq": _np(dq), "dk": _np(dk), "dv": _np(dv), "dbeta": _np(db), "dh0": _np(dh0)}
     compare({kk: got[kk] for kk in ung}, ung, 1e-2)
     compare({"dg": got["dg"]}, {"dg": _ref(inp)["dg"]}, TOL["bf16"])
+
+
+@pytest.mark.parametrize("shift", [0.02, 0.06])
+def test_bf16_tcgen05_positive_log_gates(shift):
+    """deltanet.h accepts any finite g: with g > 0 on some tokens the in-chunk
+    G_i - G_j is positive for j <= i, and Gamma(i, j) = e^{G_i - G_j} > 1 must
+    not be clamped (the tcgen05 kernels masked by clamping the
+    exponent at 0).  g = shift - 0.05 softplus(N(0,1)) mixes signs."""
+    inp = _case(1, 2, 3 * 64 + 21, 128, 128, 64, "bf16", 970)
+    inp["g"] = (inp["g"] + np.float32(shift)).astype(np.float32)
+    assert (inp["g"] > 0).any() and (inp["g"] < 0).any()
+    rng = np.random.default_rng(971)
+    h0 = 0.1 * rng.standard_normal((1, 2, 128, 128))
+    dhT = 0.1 * rng.standard_normal((1, 2, 128, 128))
+    compare(_gpu(inp, "bf16", 64, h0=h0, dhT=dhT), _ref(inp, h0=h0, dhT=dhT), TOL["bf16"])

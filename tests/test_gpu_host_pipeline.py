@@ -88,3 +88,42 @@ def test_small_device_buffer_is_an_error():
                                    *(ctypes.c_void_p(P(t)) for t in out), 2,
                                    ctypes.c_void_p(P(small)), 1024, None)
     assert rc == 5
+
+
+def test_uneven_slabs_with_segments_in_the_last():
+    """B*H = 99 units in 2 slabs at L = 2048.  The full slab (50
+    units) runs one CTA per unit, the short last slab (49) picks the
+    segment-parallel kernels and needs more workspace scratch; the shared
+    workspace is sized for both.  Sampled units against the oracle."""
+    cfg = synth.custom_config(33, 3, 2048, 128, 128, 64, "bf16", index=904)
+    inp = synth.make_inputs(cfg)
+    o, dq, dk, dv, db = _run_host(_host(inp, torch.bfloat16), 2)
+    f = lambda t: t.float().numpy().astype(np.float64)
+    pick = [(0, 0), (16, 1), (16, 2), (32, 2)]  # both slabs, incl. the last unit
+    sel = lambda a: np.stack([a[b, h] for b, h in pick])[:, None]
+    sub = {k_: sel(v_) for k_, v_ in inp.items()}
+    got = {"o": sel(f(o)), "dq": sel(f(dq)), "dk": sel(f(dk)), "dv": sel(f(dv)),
+           "dbeta": sel(f(db))}
+    compare(got, run_oracle(sub), TOL["bf16"], keys=list(got))
+
+
+def test_out_buffers_are_checked():
+    """Mis-shaped or mis-typed out= buffers are refused before any launch
+    (they would be written out of bounds by TMA stores)."""
+    import paper_2406_06484_b200 as dn
+    cfg = synth.custom_config(1, 2, 130, 128, 128, 64, "bf16", index=905)
+    x = {f: t.cuda() for f, t in _host(synth.make_inputs(cfg), torch.bfloat16).items()}
+    args = (x["q"], x["k"], x["v"], x["beta"])
+    with pytest.raises(dn.DeltaNetError):
+        dn.deltanet_fwd(*args, out=torch.empty((1, 2, 129, 128), dtype=torch.bfloat16,
+                                               device="cuda"))
+    with pytest.raises(dn.DeltaNetError):
+        dn.deltanet_fwd(*args, out=torch.empty((1, 2, 130, 128), dtype=torch.float32,
+                                               device="cuda"))
+    o, _, ws = dn.deltanet_fwd(*args)
+    bad = (torch.empty_like(x["q"]), torch.empty_like(x["k"]), torch.empty_like(x["v"]),
+           torch.empty((1, 2, 64), dtype=torch.bfloat16, device="cuda"))
+    with pytest.raises(dn.DeltaNetError):
+        dn.deltanet_bwd(*args, x["dO"], workspace=ws, out=bad)
+    with pytest.raises(dn.DeltaNetError):
+        dn.deltanet_bwd(*args, x["dO"], workspace=ws.view(torch.int32)[:8])

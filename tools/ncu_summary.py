@@ -3,10 +3,16 @@
 markdown table row per kernel plus profiles/ncu_traffic.json.  Profiling aid.
 
     python tools/ncu_summary.py REPORT.ncu-rep [--json profiles/ncu_traffic.json]
+                                [--sha FILE] [--kernels a,b]
+
+--sha FILE: the kernel-sources hash (paper_2406_06484_b200.build.sources_sha)
+written by the capture command on the GPU box; default: the current tree.
+bench.py marks `traffic` stale when it differs from the benched sources.
 """
 import csv
 import io
 import json
+import os
 import subprocess
 import sys
 
@@ -36,10 +42,19 @@ def main():
     out_json = sys.argv[sys.argv.index("--json") + 1] if "--json" in sys.argv else None
     print("| kernel | " + " | ".join(m[0] for m in METRICS) + " |")
     print("|---" * (len(METRICS) + 1) + "|")
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2406_06484_b200.build import sources_sha
+    sha = open(sys.argv[sys.argv.index("--sha") + 1]).read().strip() if "--sha" in sys.argv \
+        else sources_sha()
+    kernels = (sys.argv[sys.argv.index("--kernels") + 1].split(",") if "--kernels" in sys.argv
+               else ["tc_fwd_kernel", "tc_bwd_kernel"])
+    head = subprocess.run(["git", "rev-parse", "--short=12", "HEAD"], capture_output=True,
+                          text=True).stdout.strip()
     js = {"_source": f"ncu --set full --clock-control none, report {rep}; "
                      "dram__bytes_read.sum + dram__bytes_write.sum per launch",
-          "workload": "B=8 H=16 L=4096 d=128 C=64 bf16"}
-    for k in ("tc_fwd_kernel", "tc_bwd_kernel"):
+          "workload": "B=8 H=16 L=4096 d=128 C=64 bf16",
+          "sources_sha16": sha, "git_head_at_summary": head}
+    for k in kernels:
         h, u, v = raw(rep, k)
         cells, vals = [], {}
         for name, m, sc in METRICS:

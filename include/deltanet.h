@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define DELTANET_ABI_VERSION 7
+#define DELTANET_ABI_VERSION 8
 
 typedef enum {
   DELTANET_BF16 = 0, /* bf16 I/O, fp32 accumulation (BASELINE.json north_star) */
@@ -78,7 +78,13 @@ enum {
   /* Gated DeltaNet (set internally by the deltanet_gated_* calls; set it in
    * the descriptor passed to deltanet_workspace_bytes / deltanet_path /
    * deltanet_launch_count to query the gated calls) */
-  DELTANET_GATED = 1u << 5
+  DELTANET_GATED = 1u << 5,
+  /* run the tcgen05 "split" kernels (chunk-parallel prep + per-d_v-block
+   * state chains + chunk-parallel local gradients) at
+   * Dk = Dv = 128 too, where the fused one-CTA-per-unit kernels are the
+   * default (cross-checking and measurement).  Dk = Dv in {64, 256} always
+   * run the split kernels. */
+  DELTANET_FORCE_SPLIT = 1u << 6
 };
 
 typedef struct {
@@ -276,12 +282,15 @@ int deltanet_state_scan(const deltanet_desc* d, int nparts, int part,
                         const float* loc_all, const float* edge, float* out,
                         void* stream);
 
-/* Which kernel family a descriptor dispatches to: 1 = tcgen05/TMEM/TMA
- * sm_100a path, 0 = CUDA-core (SIMT) path, -1 = unsupported descriptor.
- * The tcgen05 path serves bf16 I/O with chunk = 64 and Dk = Dv = 128
- * (ungated and gated; BASELINE configs 1, 2, 4 and the target).  fp32 I/O
- * and (with DELTANET_FORCE_SIMT only) other bf16 shapes run on the
- * CUDA-core kernels; any other bf16 descriptor is -1 (UNSUPPORTED). */
+/* Which kernel family a descriptor dispatches to: 1 = fused tcgen05/TMEM/TMA
+ * sm_100a kernels (one CTA per (b, h) unit), 2 = split tcgen05 kernels
+ * (DESIGN.md §4.10), 0 = CUDA-core (SIMT) path, -1 = unsupported descriptor.
+ * The fused path serves bf16 I/O with chunk = 64 and Dk = Dv = 128
+ * (ungated and gated; BASELINE configs 1, 2, 4 and the target); the split
+ * path bf16, chunk = 64, ungated, Dk = Dv in {64, 256} (configs 3) and, with
+ * DELTANET_FORCE_SPLIT, 128.  fp32 I/O and (with DELTANET_FORCE_SIMT only)
+ * other bf16 shapes run on the CUDA-core kernels; any other bf16 descriptor
+ * is -1 (UNSUPPORTED). */
 int deltanet_path(const deltanet_desc* d);
 
 /* Number of kernel launches deltanet_fwd (which=0), deltanet_bwd (which=1),

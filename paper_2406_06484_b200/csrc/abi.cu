@@ -31,9 +31,15 @@ int validate_rec(const deltanet_desc* d) {
   return DELTANET_OK;
 }
 
-// path choice (the gated forward and backward share the tcgen05 shapes)
+// path choice (the gated forward and backward share the tcgen05 shapes):
+// fused tcgen05 kernels at d = 128, split tcgen05 kernels at d in {64, 256}
+// (or 128 with DELTANET_FORCE_SPLIT), CUDA-core kernels for fp32 / FORCE_SIMT
+bool use_split(const deltanet_desc* d) {
+  return !(d->flags & DELTANET_FORCE_SIMT) && dn::sp_supported(d) &&
+         (d->Dk != 128 || (d->flags & DELTANET_FORCE_SPLIT));
+}
 bool use_tc(const deltanet_desc* d) {
-  return !(d->flags & DELTANET_FORCE_SIMT) && dn::tc_supported(d) &&
+  return !(d->flags & DELTANET_FORCE_SIMT) && !use_split(d) && dn::tc_supported(d) &&
          (!(d->flags & DELTANET_GATED) || dn::tc_gated_supported(d));
 }
 
@@ -48,7 +54,8 @@ int validate_path(const deltanet_desc* d) {
   if (rc) return rc;
   deltanet_desc e = *d;  // L = 0 (nothing to compute) keeps its shape's path
   if (e.L == 0) e.L = 1;
-  if (e.dtype == DELTANET_BF16 && !(e.flags & DELTANET_FORCE_SIMT) && !use_tc(&e))
+  if (e.dtype == DELTANET_BF16 && !(e.flags & DELTANET_FORCE_SIMT) && !use_tc(&e) &&
+      !use_split(&e))
     return DELTANET_ERR_UNSUPPORTED;
   return DELTANET_OK;
 }
@@ -66,6 +73,7 @@ size_t scratch_bytes(const deltanet_desc* d) {
   const size_t simt = (size_t)d->B * d->H *
                       dn::simt_scratch_floats_per_unit(d->L, d->Dk, d->Dv, d->chunk) *
                       sizeof(float);
+  if (use_split(d)) return dn::sp_scratch_bytes(d);
   if (!use_tc(d)) return simt;
   const size_t tc = dn::tc_scratch_bytes(d);
   return tc;
@@ -88,7 +96,8 @@ dn::Args make_args(const deltanet_desc* d, void* ws) {
 int validate_cp(const deltanet_desc* d) {
   int rc = validate(d);
   if (rc) return rc;
-  if (d->flags & (DELTANET_FORCE_SIMT | DELTANET_GATED)) return DELTANET_ERR_UNSUPPORTED;
+  if (d->flags & (DELTANET_FORCE_SIMT | DELTANET_GATED | DELTANET_FORCE_SPLIT))
+    return DELTANET_ERR_UNSUPPORTED;
   deltanet_desc e = *d;
   e.L = 1;
   return dn::tc_supported(&e) ? DELTANET_OK : DELTANET_ERR_UNSUPPORTED;
@@ -141,7 +150,9 @@ size_t deltanet_workspace_bytes(const deltanet_desc* d) {
 
 int deltanet_path(const deltanet_desc* d) {
   if (validate_path(d) != DELTANET_OK) return -1;
-  return use_tc(d) ? 1 : 0;
+  deltanet_desc e = *d;
+  if (e.L == 0) e.L = 1;
+  return use_split(&e) ? 2 : use_tc(&e) ? 1 : 0;
 }
 
 int deltanet_launch_count(const deltanet_desc* d, int which) {
@@ -160,6 +171,7 @@ int deltanet_launch_count(const deltanet_desc* d, int which) {
   }
   if (validate_path(d) != DELTANET_OK) return -1;
   if ((size_t)d->B * d->H == 0) return 0;
+  if (use_split(d)) return dn::sp_launch_count(d, which);
   if (which == 1 ? use_tc_bwd(d) : use_tc(d)) return dn::tc_launch_count(d, which);
   return 1;
 }
@@ -181,6 +193,7 @@ static int fwd_impl(const deltanet_desc* d, const void* q, const void* k, const 
   dn::Args a = make_args(d, workspace);
   a.q = q; a.k = k; a.v = v; a.beta = beta; a.h0 = h0; a.o = o; a.hT = hT; a.g = g;
   cudaStream_t s = (cudaStream_t)stream;
+  if (use_split(d)) return dn::sp_fwd(a, s);
   return use_tc(d) ? dn::tc_fwd(a, s) : dn::simt_fwd(a, d->dtype, s);
 }
 
@@ -221,6 +234,7 @@ static int bwd_impl(const deltanet_desc* d, const void* q, const void* k, const 
   a.q = q; a.k = k; a.v = v; a.beta = beta; a.h0 = h0; a.dO = dO; a.dhT = dhT;
   a.dq = dq; a.dk = dk; a.dv = dv; a.dbeta = dbeta; a.dh0 = dh0; a.g = g; a.dg = dg;
   cudaStream_t s = (cudaStream_t)stream;
+  if (use_split(d)) return dn::sp_bwd(a, s);
   if (use_tc_bwd(d)) return dn::tc_bwd(a, s);
   // the SIMT backward cannot read states saved by a tcgen05 forward (their
   // layout is the bf16 operand image): it recomputes them

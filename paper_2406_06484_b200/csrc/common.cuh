@@ -109,4 +109,11 @@ int cp_compose_bwd(const Args& a, float* dhloc, cudaStream_t s);
 int cp_scan(int units, int nparts, int part, int reverse, const float* psi, const float* loc,
             const float* edge, float* out, cudaStream_t s);
 
+// tcgen05 split path (tc_split.cu)
+bool sp_supported(const deltanet_desc* d);
+size_t sp_scratch_bytes(const deltanet_desc* d);
+int sp_launch_count(const deltanet_desc* d, int which);
+int sp_fwd(const Args& a, cudaStream_t s);
+int sp_bwd(const Args& a, cudaStream_t s);
+
 }  // namespace dn

@@ -44,7 +44,7 @@ def test_no_torch_types_in_abi():
 
 
 def test_abi_version_and_strerror(lib):
-    assert lib.deltanet_abi_version() == 7
+    assert lib.deltanet_abi_version() == 8
     for code in range(6):
         assert dn.deltanet_strerror(code)
     assert "unknown" in dn.deltanet_strerror(99)
@@ -72,7 +72,25 @@ def test_workspace_and_validation(lib):
     assert dn.deltanet_path(_desc(L=0)) != -1                     # L = 0: nothing to run
 
 
-@pytest.mark.parametrize("shape", [dict(Dk=64, Dv=64), dict(chunk=128), dict(chunk=32),
+@pytest.mark.parametrize("D", [64, 256])
+def test_split_path_shapes(lib, D):
+    """Dk = Dv in {64, 256} (BASELINE configs[3] is d = 256) run the split
+    tcgen05 kernels (path 2); d = 128 only with
+    DELTANET_FORCE_SPLIT; gated, other chunks and unequal dims are refused."""
+    d = _desc(Dk=D, Dv=D)
+    assert dn.deltanet_path(d) == 2
+    assert dn.deltanet_workspace_bytes(d) > 0
+    assert dn.deltanet_launch_count(d, 0) == 2 and dn.deltanet_launch_count(d, 1) == 4
+    saved = _desc(Dk=D, Dv=D, flags=1 | dn.DELTANET_SAVE_STATES)
+    assert dn.deltanet_launch_count(saved, 1) == 2  # records from the forward
+    assert dn.deltanet_path(_desc(flags=1 | dn.DELTANET_FORCE_SPLIT)) == 2
+    assert dn.deltanet_path(_desc()) == 1
+    assert dn.deltanet_path(_desc(Dk=D, Dv=D, flags=1 | dn.DELTANET_GATED)) == -1
+    assert dn.deltanet_path(_desc(Dk=D, Dv=D, chunk=32)) == -1
+    assert dn.deltanet_path(_desc(Dk=D, Dv=D, dtype=1)) == 0     # fp32 -> SIMT
+
+
+@pytest.mark.parametrize("shape", [dict(Dk=64, Dv=128), dict(chunk=128), dict(chunk=32),
                                    dict(Dk=128, Dv=64), dict(Dk=16, Dv=16, chunk=16)])
 def test_bf16_outside_tcgen05_shapes_is_unsupported(lib, shape):
     """bf16 descriptors outside the tcgen05 shapes are refused (UNSUPPORTED,

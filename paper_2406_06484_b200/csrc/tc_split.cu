@@ -337,13 +337,13 @@ __global__ void __launch_bounds__(288, 1)
 }
 
 template <int D>
-constexpr int prep_smem() {
+__host__ __device__ constexpr int prep_smem() {
   return 2 * SP<D>::TILE + (C * LS + 2 * 4 * C + C + 2 * C) * 4 + 3 * BLK + SP<D>::WT;
 }
 
 // ============================================================ fwd chain kernel
 template <int D>
-constexpr int fchain_smem() {
+__host__ __device__ constexpr int fchain_smem() {
   return SP<D>::TILE * 3 + 2 * BLK + SP<D>::WT + 2 * BLK + SP<D>::HIMG + 2 * BLK;
 }
 
@@ -578,7 +578,7 @@ __global__ void __launch_bounds__(288, 1)
 
 // ============================================================ bwd chain kernel
 template <int D>
-constexpr int bchain_smem() {
+__host__ __device__ constexpr int bchain_smem() {
   // K[2] Q | dO[2] A X V | Hf dH | dU' dV R | beta [64] db [2][64]
   return 3 * SP<D>::TILE + 5 * BLK + 2 * SP<D>::HIMG + 3 * BLK + 3 * C * 4;
 }
@@ -862,11 +862,11 @@ __global__ void __launch_bounds__(288, 1)
 
 // ============================================================ bwd local kernel
 template <int D>
-constexpr int blocal_set() {  // dO U' dU' R dV (64 x 64 each) | H^T dH^T images
+__host__ __device__ constexpr int blocal_set() {  // dO U' dU' R dV (64 x 64 each) | H^T dH^T images
   return 5 * BLK + 2 * SP<D>::HIMG;
 }
 template <int D>
-constexpr int blocal_smem() {
+__host__ __device__ constexpr int blocal_smem() {
   constexpr int set = blocal_set<D>();
   constexpr int qk = 2 * SP<D>::TILE;
   return (set > qk ? set : qk) + 5 * BLK + (C * 4) * 10;

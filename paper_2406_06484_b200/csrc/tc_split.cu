@@ -56,6 +56,22 @@ constexpr int C = 64, LS = 68;
 constexpr uint32_t LO16 = 16u << 16;
 constexpr int BLK = C * 64 * 2;  // 64 x 64 bf16 IL tile (8 KB)
 
+#ifdef DN_TIMING
+// Test-only phase stamps (tools/sp_timeline.py, -DDN_TIMING): clock64 of CTA
+// (0, 0) of the chain kernels per chunk iteration (32 slots), and of CTA
+// (NC / 2, 0) of the local kernel per sub-step.
+__device__ long long* sp_tim = nullptr;
+__device__ int sp_tim_kernel = 0;  // 1 fwd chain, 2 bwd chain, 3 bwd local
+#define SPT(K, it, slot)                                                                 \
+  do {                                                                                   \
+    if (sp_tim != nullptr && sp_tim_kernel == (K) && blockIdx.y == 0 &&                  \
+        blockIdx.x == ((K) == 3 ? gridDim.x / 2 : 0))                                    \
+      sp_tim[(size_t)(it) * 32 + (slot)] = clock64();                                    \
+  } while (0)
+#else
+#define SPT(K, it, slot) do { } while (0)
+#endif
+
 template <int D>
 struct SP {
   static constexpr int NB = D / 64;        // d_v blocks
@@ -70,7 +86,6 @@ struct SP {
   static constexpr int R2_U = 0, R2_DU = BLK, R2_R = 2 * BLK, R2_DB = 3 * BLK;
   static constexpr int R2_DH = 3 * BLK + 256;
   static constexpr int R2_BYTES = R2_DH + HIMG;
-  static constexpr int TMCOLS = D <= 64 ? 256 : 512;
 };
 
 // workspace layout of the split path (after the states region, which holds
@@ -109,6 +124,16 @@ __device__ __forceinline__ void ld32f(uint32_t tm, int wq, uint32_t col, float (
     for (int j = 0; j < 16; ++j) f[16 * i + j] = __uint_as_float(r[i][j]);
 }
 
+// 8 fp32 -> 8 bf16 (16 B) to global memory
+__device__ __forceinline__ void stg8(void* dst, const float* x) {
+  uint4 v;
+  v.x = pack_bf16(x[0], x[1]);
+  v.y = pack_bf16(x[2], x[3]);
+  v.z = pack_bf16(x[4], x[5]);
+  v.w = pack_bf16(x[6], x[7]);
+  *reinterpret_cast<uint4*>(dst) = v;
+}
+
 // SIMT (256 threads, named barrier 1) -> control thread hand-off
 __device__ __forceinline__ void hand_off(uint64_t* bar, int tid) {
   fence_proxy_async();
@@ -119,7 +144,7 @@ __device__ __forceinline__ void hand_off(uint64_t* bar, int tid) {
 
 // ============================================================== prep kernel
 template <int D>
-__global__ void __launch_bounds__(288, 1)
+__global__ void __launch_bounds__(288, 2)
     sp_prep_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                    const __grid_constant__ CUtensorMap mQh, const __grid_constant__ CUtensorMap mKh,
                    Args a) {
@@ -134,8 +159,11 @@ __global__ void __launch_bounds__(288, 1)
   uint8_t* sT = reinterpret_cast<uint8_t*>(nrm + 2 * C);
   uint8_t* sA = sT + BLK;
   uint8_t* sX = sA + BLK;
-  uint8_t* sW = sX + BLK;
-  __shared__ uint64_t ld_full, norm_done, g_done, t_ready, w_done, w_img;
+  // the W^T image reuses the q_hat tile once the Gram product and the q_hat
+  // store have read it (q_free): 108 KB at d = 256, two CTAs per SM
+  uint8_t* sW = sQ;
+  static_assert(SP<D>::WT == SP<D>::TILE, "W^T image over the q tile");
+  __shared__ uint64_t ld_full, norm_done, g_done, t_ready, w_done, w_img, q_free;
   __shared__ uint32_t tslot;
   constexpr uint32_t TM_G = 0, TM_W = 64;
 
@@ -153,6 +181,7 @@ __global__ void __launch_bounds__(288, 1)
     mbar_init(&t_ready, 1);
     mbar_init(&w_done, 1);
     mbar_init(&w_img, 1);
+    mbar_init(&q_free, 1);
     mbar_fence_init();
     mbar_expect_tx(&ld_full, 2 * S::TILE);
     tma_load_4d(sQ, &mQ, 0, t0, 0, unit, &ld_full);
@@ -176,6 +205,9 @@ __global__ void __launch_bounds__(288, 1)
         mma_bf16(tm + TM_G + LO16, desc_k(ak, C, k0), desc_k(ak, C, k0), idg, k0 > 0);
       }
       mma_commit(&g_done);
+      bulk_wait_read0();  // q_hat / k_hat stores have read the tiles
+      mbar_wait(&g_done, 0);
+      mbar_arrive(&q_free);
       mbar_wait(&t_ready, 0);
       fence_after_sync();
       // W^T = K_hat^T T^T: M = d_k (128-row accumulators; M = 64 at d = 64)
@@ -308,6 +340,7 @@ __global__ void __launch_bounds__(288, 1)
     }
     hand_off(&t_ready, tid);
     mbar_wait(&w_done, 0);
+    mbar_wait(&q_free, 0);
     fence_after_sync();
     // W^T read-out -> bf16 image IL R = D (row = d_k)
     if (D >= 128) {
@@ -338,21 +371,20 @@ __global__ void __launch_bounds__(288, 1)
 
 template <int D>
 __host__ __device__ constexpr int prep_smem() {
-  return 2 * SP<D>::TILE + (C * LS + 2 * 4 * C + C + 2 * C) * 4 + 3 * BLK + SP<D>::WT;
+  return 2 * SP<D>::TILE + (C * LS + 2 * 4 * C + C + 2 * C) * 4 + 3 * BLK;
 }
 
 // ============================================================ fwd chain kernel
 template <int D>
 __host__ __device__ constexpr int fchain_smem() {
-  return SP<D>::TILE * 3 + 2 * BLK + SP<D>::WT + 2 * BLK + SP<D>::HIMG + 2 * BLK;
+  return SP<D>::TILE * 3 + 2 * BLK + SP<D>::WT + 2 * BLK + SP<D>::HIMG + BLK;
 }
 
 template <int D>
 __global__ void __launch_bounds__(288, 1)
     sp_fwd_chain_kernel(const __grid_constant__ CUtensorMap mQh,
                         const __grid_constant__ CUtensorMap mKh,
-                        const __grid_constant__ CUtensorMap mV64,
-                        const __grid_constant__ CUtensorMap mO64, Args a) {
+                        const __grid_constant__ CUtensorMap mV64, Args a) {
   using S = SP<D>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sQ = smem;
@@ -363,11 +395,14 @@ __global__ void __launch_bounds__(288, 1)
   uint8_t* sAb = sW + S::WT;    // 2 slots
   uint8_t* sH = sAb + 2 * BLK;
   uint8_t* sZ = sH + S::HIMG;
-  uint8_t* sO = sZ + BLK;
   __shared__ uint64_t q_full, vt_full, w_full, k_full[2], a_full[2];
-  __shared__ uint64_t up_done, q_done, ho_done, h_img, z_ready, z_free, st_free;
+  __shared__ uint64_t up_done, q_done, ho_done, h_img, z_ready;
   __shared__ uint32_t tslot;
-  constexpr uint32_t TM_H = 0, TM_U = D, TM_O = D | LO16;
+  // H_j^T (64 x D fp32): d_k columns [0, D/2) in lanes 0-15 of each quadrant
+  // (lane offset 0), [D/2, D) in lanes 16-31 (offset 16), so every lane of a
+  // warp converts state; U'^T (offset 0) and O (offset 16) share 64 columns
+  constexpr int HD = D / 2;
+  constexpr uint32_t TM_H = 0, TM_U = HD, TM_O = HD | LO16;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int j = blockIdx.x, unit = blockIdx.y, NC = a.NC;
@@ -378,7 +413,7 @@ __global__ void __launch_bounds__(288, 1)
   uint8_t* himg = reinterpret_cast<uint8_t*>(a.states);
   auto rh = [&](int c) { return himg + (((size_t)unit * NC + c) * S::NB + j) * S::HIMG; };
 
-  if (warp == 0) tmem_alloc<S::TMCOLS>(&tslot);
+  if (warp == 0) tmem_alloc<256>(&tslot);
   if (tid == 256) {
     mbar_init(&q_full, 1);
     mbar_init(&vt_full, 1);
@@ -392,8 +427,6 @@ __global__ void __launch_bounds__(288, 1)
     mbar_init(&ho_done, 1);
     mbar_init(&h_img, 1);
     mbar_init(&z_ready, 1);
-    mbar_init(&z_free, 1);
-    mbar_init(&st_free, 1);
     mbar_fence_init();
   }
   cta_sync();
@@ -430,20 +463,19 @@ __global__ void __launch_bounds__(288, 1)
       const uint32_t id_u = idesc_bf16(64, 64, true, false);
       const uint32_t id_up = idesc_bf16(64, 64, false, true, true);
       const uint32_t id_o = idesc_bf16(64, 64, false, false);
-      const uint32_t id_h = idesc_bf16(64, D, false, true);
+      const uint32_t id_h = idesc_bf16(64, HD, false, true);
 #pragma unroll 1
       for (int c = 0; c < NC; ++c) {
         const int kb = c & 1;
         const uint32_t ph = c & 1, kph = (c >> 1) & 1;
         const uint32_t aK = smem_u32(sKb + kb * S::TILE), aA = smem_u32(sAb + kb * BLK);
-        mbar_wait(&h_img, ph);  // sH = bf16 H_c (this block); sO = O of chunk c-1
-        if (c >= 1 && a.o) tma_store_4d(&mO64, sO, 0, (c - 1) * C, 8 * j, unit);
-        if (rec) bulk_store(rh(c), sH, S::HIMG);
-        bulk_commit();
+        mbar_wait(&h_img, ph);  // sH = bf16 H_c (this block)
+        SPT(1, c, 0);
         mbar_wait(&vt_full, ph);
         mbar_wait(&w_full, ph);
         mbar_wait(&q_full, ph);
         fence_after_sync();
+        SPT(1, c, 1);
         // U^T = V_j^T T^T ; U'^T = U^T - H_j^T W^T
 #pragma unroll
         for (int k0 = 0; k0 < C; k0 += 16)
@@ -457,130 +489,148 @@ __global__ void __launch_bounds__(288, 1)
         for (int k0 = 0; k0 < D; k0 += 16)
           mma_bf16(tm + TM_O, desc_k(aQ, C, k0), desc_k(aH, 64, k0), id_o, k0 > 0);
         mma_commit(&q_done);
+        // the next chunk's V / T / W as soon as U' has read them, its Q as
+        // soon as O = Q H has (both complete before Z is converted: the
+        // state update below queues behind O = Q H on the tensor pipe anyway)
         mbar_wait(&up_done, ph);
         if (c + 1 < NC) load_vtw(c + 1);
         mbar_wait(&q_done, ph);
         if (c + 1 < NC) load_q(c + 1);
-        bulk_wait_read0();  // O(c-1) and the H record have read sO / sH
-        mbar_arrive(&st_free);
         mbar_wait(&z_ready, ph);
-        if (rec) {
-          bulk_store(r2(c) + S::R2_U, sZ, BLK);
-          bulk_commit();
-        }
+        SPT(1, c, 2);
         mbar_wait(&k_full[kb], kph);
         mbar_wait(&a_full[kb], kph);
         fence_after_sync();
-        // H_j^T += U'_j^T K_hat ; O += A U'_j
+        SPT(1, c, 3);
+        // H_j^T += U'_j^T K_hat (two d_k halves at lane offsets 0 / 16) ;
+        // O += A U'_j
 #pragma unroll
-        for (int k0 = 0; k0 < C; k0 += 16)
-          mma_bf16(tm + TM_H, desc_k(aZ, 64, k0), desc_mn(aK, C, k0), id_h, 1);
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int k0 = 0; k0 < C; k0 += 16)
+            mma_bf16(tm + TM_H + (h ? LO16 : 0), desc_k(aZ, 64, k0), desc_mn(aK, C, k0, HD * h),
+                     id_h, 1);
 #pragma unroll
         for (int k0 = 0; k0 < C; k0 += 16)
           mma_bf16(tm + TM_O, desc_k(aA, C, k0), desc_k(aZ, 64, k0), id_o, 1);
         mma_commit(&ho_done);
+        SPT(1, c, 4);
         mbar_wait(&ho_done, ph);
+        SPT(1, c, 5);
         if (c + 2 < NC) load_ka(c + 2);
-        bulk_wait_read0();  // the U' record has read sZ
-        mbar_arrive(&z_free);
       }
-      mbar_wait(&h_img, NC & 1);
-      if (NC > 0 && a.o) {
-        tma_store_4d(&mO64, sO, 0, (NC - 1) * C, 8 * j, unit);
-        bulk_commit();
-      }
-      bulk_wait0();
     }
     __syncwarp();
   } else {
-    // ---------------- SIMT warps 0-7: lanes 0-15 of each quadrant hold the
-    // rows of the M = 64 accumulators at lane offset 0, lanes 16-31 those at
-    // offset 16; warpgroup wg takes half of the columns
+    // ---------------- SIMT warps 0-7.  Every record and O go to global memory
+    // straight from registers (coalesced 16 B stores; no smem staging to wait
+    // for).  Lanes 0-15 of each quadrant hold the
+    // rows of the offset-0 accumulators, lanes 16-31 those at offset 16; for
+    // H, lane half hh = lane >> 4 holds d_k columns [hh D/2, hh D/2 + D/2)
+    // and warpgroup wg a quarter of them
     const int w = tid & 127, wq = w >> 5, wg = tid >> 7;
     const bool lo = lane < 16;
     const int r16 = 16 * wq + (lane & 15);
-    constexpr int HC = D / 2;  // H columns per warpgroup
+    constexpr int QC = D / 4;                       // H columns per thread
+    const int tcol = wg * QC;                       // TMEM column (within TM_H)
+    const int gcol = (lo ? 0 : HD) + wg * QC;       // d_k column
     {  // H_j^T[dv][dk] = h0[dk][64 j + dv] -> TMEM (fp32) and the bf16 image
       const float* h0 = a.h0 ? a.h0 + (size_t)unit * D * D : nullptr;
 #pragma unroll 1
-      for (int c0 = wg * HC; c0 < wg * HC + HC; c0 += 16) {
+      for (int c0 = 0; c0 < QC; c0 += 16) {
         uint32_t r[16];
         float f[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
-          f[e] = (h0 && lo) ? h0[(size_t)(c0 + e) * D + 64 * j + r16] : 0.f;
+          f[e] = h0 ? h0[(size_t)(gcol + c0 + e) * D + 64 * j + r16] : 0.f;
           r[e] = __float_as_uint(f[e]);
         }
-        tmem_st16(taddr(tm, wq * 32, TM_H + c0), r);
-        if (lo) {
-          il_store8(sH, 64, r16, c0, f);
-          il_store8(sH, 64, r16, c0 + 8, f + 8);
+        tmem_st16(taddr(tm, wq * 32, TM_H + tcol + c0), r);
+        il_store8(sH, 64, r16, gcol + c0, f);
+        il_store8(sH, 64, r16, gcol + c0 + 8, f + 8);
+        if (rec && NC > 0) {
+          stg8(rh(0) + il_off(r16, gcol + c0, 64), f);
+          stg8(rh(0) + il_off(r16, gcol + c0 + 8, 64), f + 8);
         }
       }
       tmem_st_wait();
     }
     hand_off(&h_img, tid);
+    __nv_bfloat16* const obase =
+        a.o ? reinterpret_cast<__nv_bfloat16*>(a.o) + (size_t)unit * a.L * D + 64 * j : nullptr;
 #pragma unroll 1
     for (int c = 0; c < NC; ++c) {
       const uint32_t ph = c & 1;
       mbar_wait(&up_done, ph);
-      if (c >= 1) mbar_wait(&z_free, ph ^ 1);
+      if (tid == 0) SPT(1, c, 8);
       fence_after_sync();
-      {  // U'^T (lanes < 16: row dv) -> bf16 sZ (IL R = 64, row dv, col token)
+      if (tid == 0) SPT(1, c, 9);
+      {  // U'^T (lanes < 16: row dv) -> bf16 sZ (IL R = 64, row dv, col token);
+        // its record is stored after the hand-off (off the chain)
         float f[32];
         ld32f(tm, wq, TM_U + 32 * wg, f);
         if (lo) {
 #pragma unroll
           for (int g = 0; g < 4; ++g) il_store8(sZ, 64, r16, 32 * wg + g * 8, f + g * 8);
         }
+        hand_off(&z_ready, tid);
+        if (lo && rec) {
+          uint8_t* rz = r2(c) + S::R2_U;
+#pragma unroll
+          for (int g = 0; g < 4; ++g) stg8(rz + il_off(r16, 32 * wg + g * 8, 64), f + g * 8);
+        }
       }
-      hand_off(&z_ready, tid);
+      if (tid == 0) SPT(1, c, 10);
       mbar_wait(&ho_done, ph);
-      mbar_wait(&st_free, ph);
+      if (tid == 0) SPT(1, c, 11);
       fence_after_sync();
-      // H_j^T -> bf16 image (lanes < 16)
-#pragma unroll 1
-      for (int c0 = wg * HC; c0 < wg * HC + HC; c0 += 32) {
-        float f[32];
-        ld32f(tm, wq, TM_H + c0, f);
-        if (lo) {
+      if (tid == 0) SPT(1, c, 12);
+      // H_{c+1}^T -> bf16 image (all lanes)
 #pragma unroll
-          for (int g = 0; g < 4; ++g) il_store8(sH, 64, r16, c0 + g * 8, f + g * 8);
-        }
+      for (int c0 = 0; c0 < QC; c0 += 16) {
+        float f[16];
+        ld16(tm, wq, TM_H + tcol + c0, f);
+        il_store8(sH, 64, r16, gcol + c0, f);
+        il_store8(sH, 64, r16, gcol + c0 + 8, f + 8);
       }
-      {  // O (lanes >= 16: token row) -> bf16 staging
-        float f[32];
-        ld32f(tm, wq, TM_U + 32 * wg, f);  // lanes >= 16 read TM_O's rows
-        if (!lo) {
-#pragma unroll
-          for (int g = 0; g < 4; ++g) il_store8(sO, C, r16, 32 * wg + g * 8, f + g * 8);
-        }
-      }
+      float fo[32];  // O (lanes >= 16: token row), read before the next O = Q H
+      ld32f(tm, wq, TM_U + 32 * wg, fo);
       hand_off(&h_img, tid);
+      if (tid == 0) SPT(1, c, 13);
+      if (rec && c + 1 < NC) {  // the H_{c+1} record: this thread's image chunks
+        uint8_t* hr = rh(c + 1);
+#pragma unroll
+        for (int c0 = 0; c0 < QC; c0 += 8)
+          *reinterpret_cast<uint4*>(hr + il_off(r16, gcol + c0, 64)) =
+              *reinterpret_cast<const uint4*>(sH + il_off(r16, gcol + c0, 64));
+      }
+      const int tok = c * C + r16;
+      if (!lo && obase && tok < a.L) {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) stg8(obase + (size_t)tok * D + 32 * wg + g * 8, fo + g * 8);
+      }
     }
     if (a.hT) {  // hT[dk][64 j + dv]
       fence_after_sync();
       float* hT = a.hT + (size_t)unit * D * D;
 #pragma unroll 1
-      for (int c0 = wg * HC; c0 < wg * HC + HC; c0 += 16) {
+      for (int c0 = 0; c0 < QC; c0 += 16) {
         float f[16];
-        ld16(tm, wq, TM_H + c0, f);
-        if (lo) {
+        ld16(tm, wq, TM_H + tcol + c0, f);
 #pragma unroll
-          for (int e = 0; e < 16; ++e) hT[(size_t)(c0 + e) * D + 64 * j + r16] = f[e];
-        }
+        for (int e = 0; e < 16; ++e) hT[(size_t)(gcol + c0 + e) * D + 64 * j + r16] = f[e];
       }
     }
   }
   cta_sync();
-  if (warp == 0) tmem_dealloc<S::TMCOLS>(tm);
+  if (warp == 0) tmem_dealloc<256>(tm);
 }
 
 // ============================================================ bwd chain kernel
 template <int D>
 __host__ __device__ constexpr int bchain_smem() {
-  // K[2] Q | dO[2] A X V | Hf dH | dU' dV R | beta [64] db [2][64]
-  return 3 * SP<D>::TILE + 5 * BLK + 2 * SP<D>::HIMG + 3 * BLK + 3 * C * 4;
+  // K[2] Q | dO[2] A X V | Hf dH | dU' dV | beta [64] db [2][64]
+  return 3 * SP<D>::TILE + 5 * BLK + 2 * SP<D>::HIMG + 2 * BLK + 3 * C * 4;
 }
 
 template <int D>
@@ -588,8 +638,7 @@ __global__ void __launch_bounds__(288, 1)
     sp_bwd_chain_kernel(const __grid_constant__ CUtensorMap mQh,
                         const __grid_constant__ CUtensorMap mKh,
                         const __grid_constant__ CUtensorMap mV64,
-                        const __grid_constant__ CUtensorMap mDO64,
-                        const __grid_constant__ CUtensorMap mDV64, Args a) {
+                        const __grid_constant__ CUtensorMap mDO64, Args a) {
   using S = SP<D>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sKb = smem;  // 2 slots
@@ -602,13 +651,16 @@ __global__ void __launch_bounds__(288, 1)
   uint8_t* sDH = sHf + S::HIMG;
   uint8_t* sDU = sDH + S::HIMG;
   uint8_t* sDV = sDU + BLK;
-  uint8_t* sR = sDV + BLK;
-  float* vb = reinterpret_cast<float*>(sR + BLK);
+  float* vb = reinterpret_cast<float*>(sDV + BLK);
   float* dbp = vb + C;  // [2][64]
   __shared__ uint64_t k_full[2], do_full[2], a_full, x_full, v_full, hf_full, q_full;
-  __shared__ uint64_t du_done, r_done, p_done, dh_done, dh_img, du_ready, dv_ready, st_free;
+  __shared__ uint64_t du_done, r_done, p_done, dh_done, dh_img, du_ready, dv_ready, rr_ready;
   __shared__ uint32_t tslot;
-  constexpr uint32_t TM_DH = 0, TM_DU = D, TM_R = D | LO16, TM_P = (D + 64) | LO16;
+  // dH_j^T (64 x D fp32) split by d_k halves over the lane offsets 0 / 16 as
+  // in the forward chain; dU'^T (offset 0) | R' = K_hat H_j (offset 16) share
+  // 64 columns, P (offset 16) 64 more
+  constexpr int HD = D / 2;
+  constexpr uint32_t TM_DH = 0, TM_DU = HD, TM_R = HD | LO16, TM_P = (HD + 64) | LO16;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int j = blockIdx.x, unit = blockIdx.y, NC = a.NC;
@@ -618,7 +670,7 @@ __global__ void __launch_bounds__(288, 1)
   const uint8_t* himg = reinterpret_cast<const uint8_t*>(a.states);
   auto rh = [&](int c) { return himg + (((size_t)unit * NC + c) * S::NB + j) * S::HIMG; };
 
-  if (warp == 0) tmem_alloc<S::TMCOLS>(&tslot);
+  if (warp == 0) tmem_alloc<256>(&tslot);
   if (tid == 256) {
     for (int b = 0; b < 2; ++b) {
       mbar_init(&k_full[b], 1);
@@ -636,7 +688,7 @@ __global__ void __launch_bounds__(288, 1)
     mbar_init(&dh_img, 1);
     mbar_init(&du_ready, 1);
     mbar_init(&dv_ready, 1);
-    mbar_init(&st_free, 1);
+    mbar_init(&rr_ready, 1);
     mbar_fence_init();
   }
   cta_sync();
@@ -686,21 +738,21 @@ __global__ void __launch_bounds__(288, 1)
       const uint32_t id_du1 = idesc_bf16(64, 64, false, false);
       const uint32_t id_du2 = idesc_bf16(64, 64, true, true);
       const uint32_t id_p = idesc_bf16(64, 64, true, false);
-      const uint32_t id_dh = idesc_bf16(64, D, true, true);
-      const uint32_t id_dhn = idesc_bf16(64, D, true, true, true);
+      const uint32_t id_dh = idesc_bf16(64, HD, true, true);
+      const uint32_t id_dhn = idesc_bf16(64, HD, true, true, true);
 #pragma unroll 1
       for (int it = 0; it < NC; ++it) {
         const int c = NC - 1 - it, kb = it & 1;
         const uint32_t ph = it & 1, kph = (it >> 1) & 1;
         const uint32_t aK = smem_u32(sKb + kb * S::TILE), aDO = smem_u32(sDOb + kb * BLK);
         mbar_wait(&dh_img, ph);  // sDH = bf16 dl/dH_{c+1} (this block)
-        bulk_store(r2(c) + S::R2_DH, sDH, S::HIMG);
-        bulk_commit();
+        SPT(2, it, 0);
         mbar_wait(&k_full[kb], kph);
         mbar_wait(&do_full[kb], kph);
         mbar_wait(&a_full, ph);
         fence_after_sync();
-        // dU'^T = dH^T K_hat^T + dO^T A
+        SPT(2, it, 1);
+        // dU'^T = dH^T K_hat^T + dO^T A   (the chain)
 #pragma unroll 4
         for (int k0 = 0; k0 < D; k0 += 16)
           mma_bf16(tm + TM_DU, desc_k(aDH, 64, k0), desc_k(aK, C, k0), id_du1, k0 > 0);
@@ -708,74 +760,84 @@ __global__ void __launch_bounds__(288, 1)
         for (int k0 = 0; k0 < C; k0 += 16)
           mma_bf16(tm + TM_DU, desc_mn(aDO, C, k0), desc_mn(aA, C, k0), id_du2, 1);
         mma_commit(&du_done);
-        // R' = K_hat H_j (H_j of the forward)
+        if (it >= 1) {  // the previous chunk's R phase has read V and R' (rr_ready):
+          // this chunk's forward H_j and V (R' of this chunk comes after its dH update)
+          mbar_wait(&rr_ready, ph ^ 1);
+          SPT(2, it, 5);
+          load_hf(c);
+          load_v(c);
+        }
+        mbar_wait(&du_ready, ph);  // dU'^T in smem (du_done seen by the SIMT warps)
+        SPT(2, it, 2);
+        if (c > 0) load_a(c - 1);
+        mbar_wait(&x_full, ph);
+        fence_after_sync();
+        // P = X^T dU'_j (the chain), then R' = K_hat H_j (forward H_j; off it)
+#pragma unroll
+        for (int k0 = 0; k0 < C; k0 += 16)
+          mma_bf16(tm + TM_P, desc_mn(aX, C, k0), desc_k(aDU, 64, k0), id_p, k0 > 0);
+        mma_commit(&p_done);
+        mbar_wait(&dv_ready, ph);  // dV staged (P read)
+        SPT(2, it, 3);
+        if (c > 0) load_x(c - 1);
+        mbar_wait(&q_full, ph);
+        fence_after_sync();
+        SPT(2, it, 4);
+        // dH_j^T += dO_j^T Q_hat - dV_j^T K_hat  (two d_k halves)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t d = tm + TM_DH + (h ? LO16 : 0);
+#pragma unroll
+          for (int k0 = 0; k0 < C; k0 += 16)
+            mma_bf16(d, desc_mn(aDO, C, k0), desc_mn(aQ, C, k0, HD * h), id_dh, 1);
+#pragma unroll
+          for (int k0 = 0; k0 < C; k0 += 16)
+            mma_bf16(d, desc_mn(aDV, C, k0), desc_mn(aK, C, k0, HD * h), id_dhn, 1);
+        }
+        mma_commit(&dh_done);
+        // R' = K_hat H_j (forward H_j) for R and dbeta: off the chain, after it
         mbar_wait(&hf_full, ph);
         fence_after_sync();
 #pragma unroll 4
         for (int k0 = 0; k0 < D; k0 += 16)
           mma_bf16(tm + TM_R, desc_k(aK, C, k0), desc_k(aHf, 64, k0), id_du1, k0 > 0);
         mma_commit(&r_done);
-        mbar_wait(&du_done, ph);
-        if (c > 0) load_a(c - 1);
-        mbar_wait(&r_done, ph);
-        if (c > 0) load_hf(c - 1);
-        mbar_wait(&du_ready, ph);
-        bulk_store(r2(c) + S::R2_DU, sDU, BLK);
-        bulk_commit();
-        mbar_wait(&x_full, ph);
-        fence_after_sync();
-        // P = X^T dU'_j
-#pragma unroll
-        for (int k0 = 0; k0 < C; k0 += 16)
-          mma_bf16(tm + TM_P, desc_mn(aX, C, k0), desc_k(aDU, 64, k0), id_p, k0 > 0);
-        mma_commit(&p_done);
-        mbar_wait(&p_done, ph);
-        if (c > 0) load_x(c - 1);
-        mbar_wait(&dv_ready, ph);  // sDV, sR written; V read
-        if (c > 0) load_v(c - 1);
-        tma_store_4d(&mDV64, sDV, 0, c * C, 8 * j, unit);
-        bulk_store(r2(c) + S::R2_R, sR, BLK);
-        bulk_commit();
-        mbar_wait(&q_full, ph);
-        fence_after_sync();
-        // dH_j^T += dO_j^T Q_hat - dV_j^T K_hat
-#pragma unroll
-        for (int k0 = 0; k0 < C; k0 += 16)
-          mma_bf16(tm + TM_DH, desc_mn(aDO, C, k0), desc_mn(aQ, C, k0), id_dh, 1);
-#pragma unroll
-        for (int k0 = 0; k0 < C; k0 += 16)
-          mma_bf16(tm + TM_DH, desc_mn(aDV, C, k0), desc_mn(aK, C, k0), id_dhn, 1);
-        mma_commit(&dh_done);
         mbar_wait(&dh_done, ph);
+        SPT(2, it, 6);
         if (c > 0) load_q(c - 1);
         if (c > 1) load_kdo(c - 2, kb);
-        bulk_wait_read0();
-        mbar_arrive(&st_free);
       }
-      bulk_wait0();
     }
     __syncwarp();
   } else {
     const int w = tid & 127, wq = w >> 5, wg = tid >> 7;
     const bool lo = lane < 16;
     const int r16 = 16 * wq + (lane & 15);
-    constexpr int HC = D / 2;
+    constexpr int QC = D / 4;
+    const int tcol = wg * QC, gcol = (lo ? 0 : HD) + wg * QC;
     const __nv_bfloat16* beta = (const __nv_bfloat16*)a.beta + (size_t)unit * a.L;
-    {  // dH_j^T[dv][dk] = dhT[dk][64 j + dv]
+    // every record and dV go to global memory straight from registers
+    // (coalesced 16 B stores; nothing staged for a bulk store to drain)
+    __nv_bfloat16* const dvbase = reinterpret_cast<__nv_bfloat16*>(a.dv) +
+                                  (size_t)unit * a.L * D + 64 * j;
+    {  // dH_j^T[dv][dk] = dhT[dk][64 j + dv]; its image is the record of chunk NC-1
       const float* dhT = a.dhT ? a.dhT + (size_t)unit * D * D : nullptr;
+      uint8_t* hr = NC > 0 ? r2(NC - 1) + S::R2_DH : nullptr;
 #pragma unroll 1
-      for (int c0 = wg * HC; c0 < wg * HC + HC; c0 += 16) {
+      for (int c0 = 0; c0 < QC; c0 += 16) {
         uint32_t r[16];
         float f[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
-          f[e] = (dhT && lo) ? dhT[(size_t)(c0 + e) * D + 64 * j + r16] : 0.f;
+          f[e] = dhT ? dhT[(size_t)(gcol + c0 + e) * D + 64 * j + r16] : 0.f;
           r[e] = __float_as_uint(f[e]);
         }
-        tmem_st16(taddr(tm, wq * 32, TM_DH + c0), r);
-        if (lo) {
-          il_store8(sDH, 64, r16, c0, f);
-          il_store8(sDH, 64, r16, c0 + 8, f + 8);
+        tmem_st16(taddr(tm, wq * 32, TM_DH + tcol + c0), r);
+        il_store8(sDH, 64, r16, gcol + c0, f);
+        il_store8(sDH, 64, r16, gcol + c0 + 8, f + 8);
+        if (hr) {
+          stg8(hr + il_off(r16, gcol + c0, 64), f);
+          stg8(hr + il_off(r16, gcol + c0 + 8, 64), f + 8);
         }
       }
       tmem_st_wait();
@@ -787,89 +849,135 @@ __global__ void __launch_bounds__(288, 1)
       const uint32_t ph = it & 1;
       if (tid < C) vb[tid] = (t0 + tid < a.L) ? __bfloat162float(beta[t0 + tid]) : 0.f;
       mbar_wait(&du_done, ph);
-      if (it >= 1) mbar_wait(&st_free, ph ^ 1);
+      if (tid == 0) SPT(2, it, 8);
       fence_after_sync();
-      {  // dU'^T (lanes < 16: row dv) -> bf16
+      if (tid == 0) SPT(2, it, 9);
+      {  // dU'^T (lanes < 16: row dv) -> bf16 operand; the record after the hand-off
         float f[32];
         ld32f(tm, wq, TM_DU + 32 * wg, f);
         if (lo) {
 #pragma unroll
           for (int g = 0; g < 4; ++g) il_store8(sDU, 64, r16, 32 * wg + g * 8, f + g * 8);
         }
+        hand_off(&du_ready, tid);
+        if (lo) {
+          uint8_t* rd = r2(c) + S::R2_DU;
+#pragma unroll
+          for (int g = 0; g < 4; ++g) stg8(rd + il_off(r16, 32 * wg + g * 8, 64), f + g * 8);
+        }
       }
-      hand_off(&du_ready, tid);
-      mbar_wait(&r_done, ph);
+      if (tid == 0) SPT(2, it, 10);
       mbar_wait(&p_done, ph);
-      mbar_wait(&v_full, ph);
       fence_after_sync();
-      {  // lanes >= 16: token row r16 of R' (K_hat H_j) and of P
-        float rp[32], p[32];
-        ld32f(tm, wq, D + 32 * wg, rp);
-        ld32f(tm, wq, D + 64 + 32 * wg, p);
-        float db = 0.f;
+      if (tid == 0) SPT(2, it, 11);
+      float p[32];  // P (lanes >= 16: token row r16), kept for dbeta
+      {  // dV = diag(beta) P -> bf16 operand; the dv output after the hand-off
+        ld32f(tm, wq, HD + 64 + 32 * wg, p);
+        const float bt = lo ? 0.f : vb[r16];
         if (!lo) {
-          const float bt = vb[r16];
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
-            float v8[8], r8[8], d8[8];
+            float d8[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) d8[e] = bt * p[g * 8 + e];
+            il_store8(sDV, C, r16, 32 * wg + g * 8, d8);
+          }
+        }
+        hand_off(&dv_ready, tid);
+        const int tok = t0 + r16;
+        if (!lo && tok < a.L) {
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+            *reinterpret_cast<uint4*>(dvbase + (size_t)tok * D + 32 * wg + g * 8) =
+                *reinterpret_cast<const uint4*>(sDV + il_off(r16, 32 * wg + g * 8, C));
+        }
+      }
+      if (tid == 0) SPT(2, it, 12);
+      mbar_wait(&dh_done, ph);
+      if (tid == 0) SPT(2, it, 15);
+      fence_after_sync();
+      if (tid == 0) SPT(2, it, 16);
+      // dl/dH_c image (the next chunk's operand); the record of chunk c-1 is
+      // copied out of it after the hand-off
+#pragma unroll
+      for (int c0 = 0; c0 < QC; c0 += 16) {
+        float f[16];
+        ld16(tm, wq, TM_DH + tcol + c0, f);
+        il_store8(sDH, 64, r16, gcol + c0, f);
+        il_store8(sDH, 64, r16, gcol + c0 + 8, f + 8);
+      }
+      hand_off(&dh_img, tid);
+      if (tid == 0) SPT(2, it, 17);
+      if (c > 0) {
+        uint8_t* hr = r2(c - 1) + S::R2_DH;
+#pragma unroll
+        for (int c0 = 0; c0 < QC; c0 += 8)
+          *reinterpret_cast<uint4*>(hr + il_off(r16, gcol + c0, 64)) =
+              *reinterpret_cast<const uint4*>(sDH + il_off(r16, gcol + c0, 64));
+      }
+      mbar_wait(&r_done, ph);
+      mbar_wait(&v_full, ph);
+      fence_after_sync();
+      if (tid == 0) SPT(2, it, 13);
+      {  // R = V_j - K_hat H_j (record) ; rowsum(P . R) (lanes >= 16)
+        float rp[32];
+        ld32f(tm, wq, HD + 32 * wg, rp);
+        if (!lo) {
+          uint8_t* rr = r2(c) + S::R2_R;
+          float db = 0.f;
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            float v8[8], r8[8];
             il_load8(sV, C, r16, 32 * wg + g * 8, v8);
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
               r8[e] = v8[e] - rp[g * 8 + e];
               db = fmaf(p[g * 8 + e], r8[e], db);
-              d8[e] = bt * p[g * 8 + e];
             }
-            il_store8(sR, C, r16, 32 * wg + g * 8, r8);
-            il_store8(sDV, C, r16, 32 * wg + g * 8, d8);
+            stg8(rr + il_off(r16, 32 * wg + g * 8, C), r8);
           }
           dbp[wg * C + r16] = db;
         }
       }
-      hand_off(&dv_ready, tid);
+      hand_off(&rr_ready, tid);
+      if (tid == 0) SPT(2, it, 14);
       if (tid < C)  // rowsum(P_j . R_j) of this block (dbeta part 1)
         reinterpret_cast<float*>(r2(c) + S::R2_DB)[tid] = dbp[tid] + dbp[C + tid];
-      mbar_wait(&dh_done, ph);
-      mbar_wait(&st_free, ph);
-      fence_after_sync();
-#pragma unroll 1
-      for (int c0 = wg * HC; c0 < wg * HC + HC; c0 += 32) {
-        float f[32];
-        ld32f(tm, wq, TM_DH + c0, f);
-        if (lo) {
-#pragma unroll
-          for (int g = 0; g < 4; ++g) il_store8(sDH, 64, r16, c0 + g * 8, f + g * 8);
-        }
-      }
-      hand_off(&dh_img, tid);
     }
     if (a.dh0) {
       fence_after_sync();
       float* dh0 = a.dh0 + (size_t)unit * D * D;
 #pragma unroll 1
-      for (int c0 = wg * HC; c0 < wg * HC + HC; c0 += 16) {
+      for (int c0 = 0; c0 < QC; c0 += 16) {
         float f[16];
-        ld16(tm, wq, TM_DH + c0, f);
-        if (lo) {
+        ld16(tm, wq, TM_DH + tcol + c0, f);
 #pragma unroll
-          for (int e = 0; e < 16; ++e) dh0[(size_t)(c0 + e) * D + 64 * j + r16] = f[e];
-        }
+        for (int e = 0; e < 16; ++e) dh0[(size_t)(gcol + c0 + e) * D + 64 * j + r16] = f[e];
       }
     }
   }
   cta_sync();
-  if (warp == 0) tmem_dealloc<S::TMCOLS>(tm);
+  if (warp == 0) tmem_dealloc<256>(tm);
 }
 
 // ============================================================ bwd local kernel
+// The d_v loop runs in sub-steps (block v, d_k half h): the five 64 x 64
+// tiles of block v (dO, U', dU', R, dV) and the d_k half h of the H^T and
+// dH^T images of block v, each double-buffered, so the next sub-step's loads
+// overlap this one's products.
 template <int D>
-__host__ __device__ constexpr int blocal_set() {  // dO U' dU' R dV (64 x 64 each) | H^T dH^T images
-  return 5 * BLK + 2 * SP<D>::HIMG;
-}
+struct BL {
+  static constexpr int DH = D >= 128 ? 128 : D;    // d_k columns per image half
+  static constexpr int HALVES = D / DH;
+  static constexpr int IH = 64 * DH * 2;           // image half (bytes)
+  static constexpr int SSET = 5 * BLK;             // dO U' dU' R dV
+  static constexpr int ISET = 2 * IH;              // H^T half, dH^T half
+  static constexpr int LOOP = 2 * SSET + 2 * ISET;
+  static constexpr int REG = LOOP > 2 * SP<D>::TILE ? LOOP : 2 * SP<D>::TILE;
+};
 template <int D>
 __host__ __device__ constexpr int blocal_smem() {
-  constexpr int set = blocal_set<D>();
-  constexpr int qk = 2 * SP<D>::TILE;
-  return (set > qk ? set : qk) + 5 * BLK + (C * 4) * 10;
+  return BL<D>::REG + 5 * BLK + (C * 4) * 10;
 }
 
 template <int D>
@@ -881,19 +989,18 @@ __global__ void __launch_bounds__(288, 1)
                         const __grid_constant__ CUtensorMap mDQ,
                         const __grid_constant__ CUtensorMap mDK, Args a) {
   using S = SP<D>;
+  using Bl = BL<D>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  constexpr int SET = blocal_set<D>();
-  constexpr int REG = SET > 2 * S::TILE ? SET : 2 * S::TILE;
-  uint8_t* sDOv = smem;  // v-step set
-  uint8_t* sUv = sDOv + BLK;
-  uint8_t* sDUv = sUv + BLK;
-  uint8_t* sRv = sDUv + BLK;
-  uint8_t* sDVv = sRv + BLK;
-  uint8_t* sHv = sDVv + BLK;
-  uint8_t* sDHv = sHv + S::HIMG;
-  uint8_t* sQ = smem;  // after the v loop
-  uint8_t* sK = smem + S::TILE;
-  uint8_t* sX = smem + REG;
+  auto sset = [&](int b) { return smem + b * Bl::SSET; };  // + 0 dO, 1 U', 2 dU', 3 R, 4 dV (x BLK)
+  auto iset = [&](int b) { return smem + 2 * Bl::SSET + b * Bl::ISET; };  // + 0 H^T, IH dH^T
+  // q_hat / k_hat land in loop buffers as they retire (the S buffer of block
+  // NB-2 and the image buffer of sub-step NS-2), or in the buffers a single
+  // block never uses (NB = 1); dq / dk are staged there in place
+  constexpr int NSS = S::NB * Bl::HALVES;
+  static_assert(Bl::SSET >= S::TILE && Bl::ISET >= S::TILE, "q_hat / k_hat in the loop buffers");
+  uint8_t* sQ = S::NB > 1 ? sset((S::NB - 2) & 1) : sset(1);
+  uint8_t* sK = NSS > 1 ? iset((NSS - 2) & 1) : iset(1);
+  uint8_t* sX = smem + Bl::REG;
   uint8_t* sDA = sX + BLK;
   uint8_t* sDX = sDA + BLK;
   uint8_t* sY = sDX + BLK;
@@ -901,9 +1008,9 @@ __global__ void __launch_bounds__(288, 1)
   float* vb = reinterpret_cast<float*>(sG1 + BLK);  // beta [64]
   float* nrm = vb + C;                              // ||k|| | ||q||  [128]
   float* db2 = nrm + 2 * C;                         // [2][64]
-  float* dot = db2 + 2 * C;                         // [2 (q|k)][2 wg][64] -> uses 4*64
-  __shared__ uint64_t x_full, vs_full, vs_done, v_all, qk_full, dax_ready, y_done, y_ready, kk_done,
-      g_done, g1_ready, k_done, epi_done;
+  float* dot = db2 + 2 * C;                         // [2 (q|k)][2 wg][64]
+  __shared__ uint64_t x_full, s_full[2], i_full[2], i_done[2], v_all, qh_full, kh_full, dax_ready,
+      y_done, y_ready, kk_done, g_done, g1_ready, k_done, epi_done;
   __shared__ uint32_t tslot;
   constexpr uint32_t TM_DQ = 0, TM_DK = LO16, TM_DA = D, TM_DX = D | LO16, TM_Y = D,
                      TM_G = D | LO16, TM_KK = (D + 64) | LO16;
@@ -918,13 +1025,18 @@ __global__ void __launch_bounds__(288, 1)
   const uint8_t* himg = reinterpret_cast<const uint8_t*>(a.states);
   auto rh = [&](int v) { return himg + (((size_t)unit * NC + c) * S::NB + v) * S::HIMG; };
 
+  if (tid == 0) SPT(3, 8, 2);
   if (warp == 0) tmem_alloc<TMC>(&tslot);
   if (tid == 256) {
     mbar_init(&x_full, 1);
-    mbar_init(&vs_full, 1);
-    mbar_init(&vs_done, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&i_full[b], 1);
+      mbar_init(&i_done[b], 1);
+    }
     mbar_init(&v_all, 1);
-    mbar_init(&qk_full, 1);
+    mbar_init(&qh_full, 1);
+    mbar_init(&kh_full, 1);
     mbar_init(&dax_ready, 1);
     mbar_init(&y_done, 1);
     mbar_init(&y_ready, 1);
@@ -943,43 +1055,82 @@ __global__ void __launch_bounds__(288, 1)
       mbar_expect_tx(&x_full, BLK + 2 * C * 4);
       bulk_load(sX, rec1 + S::R1_X, BLK, &x_full);
       bulk_load(nrm, rec1 + S::R1_N, 2 * C * 4, &x_full);
-      const uint32_t id_a = idesc_bf16(64, 64, false, true);   // dA = dO U'^T
-      const uint32_t id_x = idesc_bf16(64, 64, true, false);   // dX' = dU' R^T
-      const uint32_t id_q = idesc_bf16(64, D, false, true);    // dQ += dO H^T
-      const uint32_t id_k = idesc_bf16(64, D, true, true);     // dK += U' dH^T
-      const uint32_t id_kn = idesc_bf16(64, D, false, true, true);  // dK -= dV H^T
+      constexpr int NS = S::NB * Bl::HALVES;  // sub-steps (v, h)
+      auto load_s = [&](int v) {
+        const int b = v & 1;
+        uint8_t* st = sset(b);
+        mbar_expect_tx(&s_full[b], Bl::SSET);
+        tma_load_4d(st, &mDO64, 0, t0, 8 * v, unit, &s_full[b]);
+        tma_load_4d(st + 4 * BLK, &mDV64, 0, t0, 8 * v, unit, &s_full[b]);
+        bulk_load(st + BLK, r2(v) + S::R2_U, BLK, &s_full[b]);
+        bulk_load(st + 2 * BLK, r2(v) + S::R2_DU, BLK, &s_full[b]);
+        bulk_load(st + 3 * BLK, r2(v) + S::R2_R, BLK, &s_full[b]);
+      };
+      auto load_i = [&](int ss) {  // H^T and dH^T images of block v, d_k half h
+        const int v = ss / Bl::HALVES, h = ss % Bl::HALVES, b = ss & 1;
+        uint8_t* it = iset(b);
+        mbar_expect_tx(&i_full[b], Bl::ISET);
+        bulk_load(it, rh(v) + h * Bl::IH, Bl::IH, &i_full[b]);
+        bulk_load(it + Bl::IH, r2(v) + S::R2_DH + h * Bl::IH, Bl::IH, &i_full[b]);
+      };
+      auto load_qh = [&]() {
+        mbar_expect_tx(&qh_full, S::TILE);
+        tma_load_4d(sQ, &mQh, 0, t0, 0, unit, &qh_full);
+      };
+      auto load_kh = [&]() {
+        mbar_expect_tx(&kh_full, S::TILE);
+        tma_load_4d(sK, &mKh, 0, t0, 0, unit, &kh_full);
+      };
+      load_s(0);
+      load_i(0);
+      if (S::NB > 1) load_s(1);
+      if (NS > 1) load_i(1);
+      if (S::NB == 1) load_qh();
+      if (NS == 1) load_kh();
+      const uint32_t id_a = idesc_bf16(64, 64, false, true);           // dA = dO U'^T
+      const uint32_t id_x = idesc_bf16(64, 64, true, false);           // dX' = dU' R^T
+      const uint32_t id_q = idesc_bf16(64, Bl::DH, false, true);       // dQ += dO H^T
+      const uint32_t id_k = idesc_bf16(64, Bl::DH, true, true);        // dK += U' dH^T
+      const uint32_t id_kn = idesc_bf16(64, Bl::DH, false, true, true);  // dK -= dV H^T
 #pragma unroll 1
-      for (int v = 0; v < S::NB; ++v) {
-        mbar_expect_tx(&vs_full, 5 * BLK + 2 * S::HIMG);
-        tma_load_4d(sDOv, &mDO64, 0, t0, 8 * v, unit, &vs_full);
-        tma_load_4d(sDVv, &mDV64, 0, t0, 8 * v, unit, &vs_full);
-        bulk_load(sUv, r2(v) + S::R2_U, BLK, &vs_full);
-        bulk_load(sDUv, r2(v) + S::R2_DU, BLK, &vs_full);
-        bulk_load(sRv, r2(v) + S::R2_R, BLK, &vs_full);
-        bulk_load(sHv, rh(v), S::HIMG, &vs_full);
-        bulk_load(sDHv, r2(v) + S::R2_DH, S::HIMG, &vs_full);
-        mbar_wait(&vs_full, v & 1);
+      for (int ss = 0; ss < NS; ++ss) {
+        const int v = ss / Bl::HALVES, h = ss % Bl::HALVES;
+        SPT(3, ss, 0);
+        mbar_wait(&s_full[v & 1], (v >> 1) & 1);
+        mbar_wait(&i_full[ss & 1], (ss >> 1) & 1);
         fence_after_sync();
-        const uint32_t aDO = smem_u32(sDOv), aU = smem_u32(sUv), aDU = smem_u32(sDUv),
-                       aR = smem_u32(sRv), aDV = smem_u32(sDVv), aH = smem_u32(sHv),
-                       aDH = smem_u32(sDHv);
+        SPT(3, ss, 1);
+        const uint8_t* st = sset(v & 1);
+        const uint8_t* it = iset(ss & 1);
+        const uint32_t aDO = smem_u32(st), aU = smem_u32(st + BLK), aDU = smem_u32(st + 2 * BLK),
+                       aR = smem_u32(st + 3 * BLK), aDV = smem_u32(st + 4 * BLK),
+                       aH = smem_u32(it), aDH = smem_u32(it + Bl::IH);
+        const uint32_t cq = TM_DQ + Bl::DH * h, ck = TM_DK + Bl::DH * h;
 #pragma unroll
         for (int k0 = 0; k0 < 64; k0 += 16) {
           const uint32_t acc = (v > 0 || k0 > 0) ? 1u : 0u;
-          mma_bf16(tm + TM_DA, desc_k(aDO, C, k0), desc_mn(aU, 64, k0), id_a, acc);
-          mma_bf16(tm + TM_DX, desc_mn(aDU, 64, k0), desc_k(aR, C, k0), id_x, acc);
-          mma_bf16(tm + TM_DQ, desc_k(aDO, C, k0), desc_mn(aH, 64, k0), id_q, acc);
-          mma_bf16(tm + TM_DK, desc_mn(aU, 64, k0), desc_mn(aDH, 64, k0), id_k, acc);
-          mma_bf16(tm + TM_DK, desc_k(aDV, C, k0), desc_mn(aH, 64, k0), id_kn, 1);
+          if (h == 0) {
+            mma_bf16(tm + TM_DA, desc_k(aDO, C, k0), desc_mn(aU, 64, k0), id_a, acc);
+            mma_bf16(tm + TM_DX, desc_mn(aDU, 64, k0), desc_k(aR, C, k0), id_x, acc);
+          }
+          mma_bf16(tm + cq, desc_k(aDO, C, k0), desc_mn(aH, 64, k0), id_q, acc);
+          mma_bf16(tm + ck, desc_mn(aU, 64, k0), desc_mn(aDH, 64, k0), id_k, acc);
+          mma_bf16(tm + ck, desc_k(aDV, C, k0), desc_mn(aH, 64, k0), id_kn, 1);
         }
-        mma_commit(&vs_done);
-        if (v == S::NB - 1) mma_commit(&v_all);  // the SIMT warps wait for the last step
-        mbar_wait(&vs_done, v & 1);
+        mma_commit(&i_done[ss & 1]);
+        SPT(3, ss, 2);
+        if (ss >= 1) {  // sub-step ss-1 retired: refill its buffers
+          const int pv = (ss - 1) / Bl::HALVES, ph = (ss - 1) % Bl::HALVES;
+          mbar_wait(&i_done[(ss - 1) & 1], ((ss - 1) >> 1) & 1);
+          if (ss + 1 < NS) load_i(ss + 1);
+          if (ph == Bl::HALVES - 1 && pv + 2 < S::NB) load_s(pv + 2);
+          if (ph == Bl::HALVES - 1 && pv == S::NB - 2) load_qh();  // its S buffer retired
+          if (ss - 1 == NS - 2) load_kh();                         // its image buffer retired
+        }
       }
-      // q_hat, k_hat over the retired set
-      mbar_expect_tx(&qk_full, 2 * S::TILE);
-      tma_load_4d(sQ, &mQh, 0, t0, 0, unit, &qk_full);
-      tma_load_4d(sK, &mKh, 0, t0, 0, unit, &qk_full);
+      mma_commit(&v_all);  // the SIMT warps wait for the whole d_v loop
+      mbar_wait(&v_all, 0);
+      SPT(3, 8, 0);
       const uint32_t aX = smem_u32(sX), aDA = smem_u32(sDA), aDX = smem_u32(sDX),
                      aY = smem_u32(sY), aG1 = smem_u32(sG1), aQ = smem_u32(sQ),
                      aK = smem_u32(sK);
@@ -993,7 +1144,8 @@ __global__ void __launch_bounds__(288, 1)
           mma_bf16(tm + TM_Y, desc_mn(aX, C, k0), desc_mn(aDX, C, k0), id, k0 > 0);
         mma_commit(&y_done);
       }
-      mbar_wait(&qk_full, 0);
+      mbar_wait(&qh_full, 0);
+      mbar_wait(&kh_full, 0);
       fence_after_sync();
       {  // K_hat K_hat^T ; dQ += dA K_hat ; dK += dA^T Q_hat
         const uint32_t id = idesc_bf16(64, 64, false, false);
@@ -1029,6 +1181,7 @@ __global__ void __launch_bounds__(288, 1)
         mma_commit(&k_done);
       }
       mbar_wait(&epi_done, 0);
+      SPT(3, 8, 1);
       tma_store_4d(&mDQ, sQ, 0, t0, 0, unit);
       tma_store_4d(&mDK, sK, 0, t0, 0, unit);
       bulk_commit();
@@ -1041,9 +1194,16 @@ __global__ void __launch_bounds__(288, 1)
     const int r16 = 16 * wq + (lane & 15);
     const __nv_bfloat16* beta = (const __nv_bfloat16*)a.beta + (size_t)unit * a.L;
     if (tid < C) vb[tid] = (t0 + tid < a.L) ? __bfloat162float(beta[t0 + tid]) : 0.f;
+    float db1 = 0.f;  // sum_v rowsum(P_v . R_v) (bwd chain records), loads in flight now
+    if (tid < C) {
+#pragma unroll
+      for (int v = 0; v < S::NB; ++v) db1 += reinterpret_cast<const float*>(r2(v) + S::R2_DB)[tid];
+    }
     mbar_wait(&x_full, 0);
+    if (tid == 0) SPT(3, 9, 0);
     mbar_wait(&v_all, 0);
     fence_after_sync();
+    if (tid == 0) SPT(3, 9, 1);
     grp_sync<256>(1);  // beta visible
     {  // lanes < 16: dA row (masked j <= i); lanes >= 16: dX row = dX' diag(beta)
       float f[32];
@@ -1060,6 +1220,7 @@ __global__ void __launch_bounds__(288, 1)
       }
     }
     hand_off(&dax_ready, tid);
+    if (tid == 0) SPT(3, 9, 2);
     mbar_wait(&y_done, 0);
     fence_after_sync();
     {  // Y (lanes < 16) -> bf16
@@ -1071,8 +1232,10 @@ __global__ void __launch_bounds__(288, 1)
       }
     }
     hand_off(&y_ready, tid);
+    if (tid == 0) SPT(3, 9, 3);
     mbar_wait(&g_done, 0);
     mbar_wait(&kk_done, 0);
+    if (tid == 0) SPT(3, 9, 4);
     fence_after_sync();
     {  // lanes >= 16: G row i and K_hat K_hat^T row i
       float gg[32], kk[32];
@@ -1098,14 +1261,14 @@ __global__ void __launch_bounds__(288, 1)
     }
     hand_off(&g1_ready, tid);
     if (tid < C && t0 + tid < a.L) {  // dbeta = sum_v rowsum(P_v . R_v) + rowsum(G . K K^T)
-      float db = db2[tid] + db2[C + tid];
-#pragma unroll 1
-      for (int v = 0; v < S::NB; ++v) db += reinterpret_cast<const float*>(r2(v) + S::R2_DB)[tid];
+      const float db = db1 + (db2[tid] + db2[C + tid]);
       reinterpret_cast<__nv_bfloat16*>(a.dbeta)[(size_t)unit * a.L + t0 + tid] =
           __float2bfloat16_rn(db);
     }
+    if (tid == 0) SPT(3, 9, 5);
     mbar_wait(&k_done, 0);
     fence_after_sync();
+    if (tid == 0) SPT(3, 9, 6);
     {
       // dq (lanes < 16, TM_DQ) / dk (lanes >= 16, TM_DK) rows: L2 adjoint
       // dx = inv (dx_hat - x_hat (x_hat . dx_hat)) when ||x|| >= eps (R9)
@@ -1148,6 +1311,7 @@ __global__ void __launch_bounds__(288, 1)
       }
     }
     hand_off(&epi_done, tid);
+    if (tid == 0) SPT(3, 9, 7);
   }
   cta_sync();
   if (warp == 0) tmem_dealloc<TMC>(tm);
@@ -1194,14 +1358,14 @@ int sp_fwd_t(const Args& a0, cudaStream_t s) {
   Args a = a0;
   const int BH = a.B * a.H;
   const SpLayout ly = sp_layout<D>(a);
-  CUtensorMap mQ, mK, mQh, mKh, mV64, mO64;
+  CUtensorMap mQ, mK, mQh, mKh, mV64;
   if (!make_map(&mQ, a.q, BH, a.L, D, D / 8) || !make_map(&mK, a.k, BH, a.L, D, D / 8) ||
       !make_map(&mQh, ly.qh, BH, a.L, D, D / 8) || !make_map(&mKh, ly.kh, BH, a.L, D, D / 8) ||
-      !make_map(&mV64, a.v, BH, a.L, D, 8) || !make_map(&mO64, a.o ? a.o : a.v, BH, a.L, D, 8))
+      !make_map(&mV64, a.v, BH, a.L, D, 8))
     return DELTANET_ERR_CUDA;
   if (a.NC > 0)
     sp_prep_kernel<D><<<dim3(a.NC, BH), 288, prep_smem<D>(), s>>>(mQ, mK, mQh, mKh, a);
-  sp_fwd_chain_kernel<D><<<dim3(SP<D>::NB, BH), 288, fchain_smem<D>(), s>>>(mQh, mKh, mV64, mO64, a);
+  sp_fwd_chain_kernel<D><<<dim3(SP<D>::NB, BH), 288, fchain_smem<D>(), s>>>(mQh, mKh, mV64, a);
   return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
 }
 
@@ -1225,7 +1389,7 @@ int sp_bwd_t(const Args& a0, cudaStream_t s) {
       !make_map(&mDK, a.dk, BH, a.L, D, D / 8))
     return DELTANET_ERR_CUDA;
   sp_bwd_chain_kernel<D><<<dim3(SP<D>::NB, BH), 288, bchain_smem<D>(), s>>>(mQh, mKh, mV64,
-                                                                            mDO64, mDV64, a);
+                                                                            mDO64, a);
   if (a.NC > 0)
     sp_bwd_local_kernel<D><<<dim3(a.NC, BH), 288, blocal_smem<D>(), s>>>(mQh, mKh, mDO64, mDV64,
                                                                         mDQ, mDK, a);
@@ -1279,3 +1443,10 @@ int sp_bwd(const Args& a, cudaStream_t s) {
 }
 
 }  // namespace dn
+
+#ifdef DN_TIMING
+extern "C" int sp_timing_set(long long* buf, int kernel) {
+  return cudaMemcpyToSymbol(dn::sp_tim, &buf, sizeof(buf)) != cudaSuccess ||
+         cudaMemcpyToSymbol(dn::sp_tim_kernel, &kernel, sizeof(int)) != cudaSuccess;
+}
+#endif

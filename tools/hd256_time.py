@@ -9,7 +9,18 @@ sys.path.insert(0, '.')
 import paper_2406_06484_b200 as dn  # noqa: E402
 
 
-def run(B, H, L, D, reps=10):
+def clocks():
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+        return (pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h))
+    except Exception as e:  # noqa: BLE001
+        return (None, str(e))
+
+
+def run(B, H, L, D, reps=30):
     g = torch.Generator(device='cuda').manual_seed(0)
     mk = lambda: torch.randn((B, H, L, D), device='cuda', generator=g).to(torch.bfloat16)
     q, k, v, dO = mk(), mk(), mk(), mk()
@@ -18,7 +29,7 @@ def run(B, H, L, D, reps=10):
     r = dn.deltanet_bwd(q, k, v, b, dO, workspace=ws)
     torch.cuda.synchronize()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-    tf = tb = 0.0
+    tf, tb = [], []
     for _ in range(reps):
         ev[0].record()
         o, hT, ws = dn.deltanet_fwd(q, k, v, b, workspace=ws)
@@ -26,11 +37,13 @@ def run(B, H, L, D, reps=10):
         r = dn.deltanet_bwd(q, k, v, b, dO, workspace=ws)
         ev[2].record()
         torch.cuda.synchronize()
-        tf += ev[0].elapsed_time(ev[1])
-        tb += ev[1].elapsed_time(ev[2])
+        tf.append(ev[0].elapsed_time(ev[1]))
+        tb.append(ev[1].elapsed_time(ev[2]))
     d = dn.make_desc(B, H, L, D, D, 64, torch.bfloat16)
-    print(f"B={B} H={H} L={L} d={D} path {dn.deltanet_path(d)}: fwd {tf / reps:.4f} ms, "
-          f"bwd {tb / reps:.4f} ms, step {(tf + tb) / reps:.4f} ms", flush=True)
+    med = lambda x: sorted(x)[len(x) // 2]
+    print(f"B={B} H={H} L={L} d={D} path {dn.deltanet_path(d)}: fwd {med(tf):.4f} ms "
+          f"(min {min(tf):.4f}), bwd {med(tb):.4f} ms (min {min(tb):.4f}), "
+          f"step {med(tf) + med(tb):.4f} ms; sm clock, throttle {clocks()}", flush=True)
 
 
 if __name__ == "__main__":

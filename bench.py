@@ -499,6 +499,57 @@ def measure_1p3b(dn, dp, dev, reps=10):
             "tc_peak_frac": (ff + fb) * B * H * Ll / t / 1634.4e12}
 
 
+def measure_head_dims(dn, dev, peaks, reps=20):
+    """BASELINE configs[3] (head_dim 256: B=4 H=8 L=4096) and the d_head = 64
+    column of fig:kernel_speed (B=8 H=16 L=4096), fwd+bwd
+    on the split tcgen05 kernels, side records (rank 0).
+    Roofline: at d = 256 the layer is tensor-bound on paper (AI ~300 flop/B
+    above the ridge), at d = 64 HBM-bound."""
+    import torch
+    out = {}
+    for name, (Bb, Hh, Ll, Dd) in (("hd256", (4, 8, 4096, 256)), ("d64", (8, 16, 4096, 64))):
+        q, k, v, beta, dO = _synthetic_rows(dev, range(Bb), Hh, Ll, Dd, 3000)
+        o, hT, ws = dn.deltanet_fwd(q, k, v, beta)
+        dn.deltanet_bwd(q, k, v, beta, dO, workspace=ws)
+        torch.cuda.synchronize(dev)
+        stream = torch.cuda.current_stream(dev)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        tf, tb = [], []
+        for _ in range(reps):
+            ev[0].record(stream)
+            dn.deltanet_fwd(q, k, v, beta, workspace=ws)
+            ev[1].record(stream)
+            dn.deltanet_bwd(q, k, v, beta, dO, workspace=ws)
+            ev[2].record(stream)
+            torch.cuda.synchronize(dev)
+            tf.append(ev[0].elapsed_time(ev[1]) * 1e-3)
+            tb.append(ev[1].elapsed_time(ev[2]) * 1e-3)
+        med = lambda x: sorted(x)[len(x) // 2]
+        t_f, t_b = med(tf), med(tb)
+        t = t_f + t_b
+        ff, fb, bf, bb = per_token_head(Dd, Dd, C, 2)
+        n = Bb * Hh * Ll
+        flops, byts = (ff + fb) * n, (bf + bb) * n
+        t_tc, t_hbm = flops / (peaks["tf_burst"] * 1e12), byts / (peaks["hbm_gbs"] * 1e9)
+        bound = "tensor" if t_tc >= t_hbm else "hbm"
+        roof = ({"bound": "tensor", "achieved": flops / t / 1e12, "peak": peaks["tf_burst"],
+                 "unit": "TFLOP/s", "frac": t_tc / t} if bound == "tensor" else
+                {"bound": "hbm", "achieved": byts / t / 1e9, "peak": peaks["hbm_gbs"],
+                 "unit": "GB/s", "frac": t_hbm / t})
+        roof["floor_ms"] = max(t_tc, t_hbm) * 1e3
+        d = dn.make_desc(Bb, Hh, Ll, Dd, Dd, C, torch.bfloat16)
+        out[name] = {"workload": f"B={Bb} H={Hh} L={Ll} d={Dd} chunk={C} bf16 fwd+bwd",
+                     "kernel_path": {2: "tcgen05 split", 1: "tcgen05 fused"}.get(
+                         dn.deltanet_path(d), "simt"),
+                     "launches": dn.deltanet_launch_count(d, 0) + dn.deltanet_launch_count(d, 1),
+                     "ms_per_step": t * 1e3, "ms_fwd": t_f * 1e3, "ms_bwd": t_b * 1e3,
+                     "tokens_per_s": Bb * Ll / t, "tc_peak_frac": flops / t / 1634.4e12,
+                     "roofline": roof}
+        del q, k, v, beta, dO, o, ws
+        torch.cuda.empty_cache()
+    return out
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -778,9 +829,10 @@ def main():
     base = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         base = cpu_baseline()
-    rec = pro = lng = gat = cpx = cfg1 = None
+    rec = pro = lng = gat = cpx = cfg1 = hds = None
     if rank == 0 and not args.no_recurrent and not args.force_simt:
         cfg1 = measure_1p3b(dn, dp, dev)
+        hds = measure_head_dims(dn, dev, peaks)
         rec = measure_recurrent(dn, dev, q, k, v, beta, t_fwd, peaks)
         pro = measure_prologue(dn, dev, B_PER_RANK, H, L, D, peaks)
         lng = measure_long_context(dn, dev)
@@ -813,6 +865,8 @@ def main():
             line["strong_scaling"] = strong
         if cfg1:
             line["config_1p3b"] = cfg1
+        if hds:
+            line["head_dims"] = hds
         if rec:
             line["recurrent"] = rec
         if pro:

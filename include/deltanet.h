@@ -84,7 +84,15 @@ enum {
    * Dk = Dv = 128 too, where the fused one-CTA-per-unit kernels are the
    * default (cross-checking and measurement).  Dk = Dv in {64, 256} always
    * run the split kernels. */
-  DELTANET_FORCE_SPLIT = 1u << 6
+  DELTANET_FORCE_SPLIT = 1u << 6,
+  /* fused tcgen05 kernels (d = 128): round the bf16 operands that are
+   * summed over tokens (Z = diag(s) U' in the forward, the U' record and dA
+   * in the backward) with the rounding error carried along the token axis
+   * (compensated rounding).  Prefix sums then carry ~2 roundings instead of
+   * ~sqrt(C); it matters where those sums telescope (e.g. many identical
+   * keys with beta = 1, R19) and costs ~7% of a fwd+bwd step.
+   * Set it for both deltanet_fwd and deltanet_bwd (the record differs). */
+  DELTANET_COMPENSATED = 1u << 7
 };
 
 typedef struct {

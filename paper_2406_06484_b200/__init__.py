@@ -30,6 +30,7 @@ DELTANET_PROLOGUE_SILU_V = 1 << 3
 DELTANET_FORCE_SIMT = 1 << 2
 DELTANET_NO_SEGMENTS = 1 << 4
 DELTANET_FORCE_SPLIT = 1 << 6
+DELTANET_COMPENSATED = 1 << 7
 DELTANET_GATED = 1 << 5
 
 
@@ -119,22 +120,22 @@ def _check(rc: int, what: str):
 
 def make_desc(B, H, L, Dk, Dv, chunk=64, dtype=torch.bfloat16, l2norm=True,
               save_states=True, force_simt=False, eps=1e-6, segments=True,
-              gated=False, force_split=False) -> deltanet_desc:
+              gated=False, force_split=False, extra_flags=0) -> deltanet_desc:
     dt = {torch.bfloat16: DELTANET_BF16, torch.float32: DELTANET_FP32}[dtype]
     flags = ((DELTANET_L2NORM_QK if l2norm else 0) |
              (DELTANET_SAVE_STATES if save_states else 0) |
              (DELTANET_FORCE_SIMT if force_simt else 0) |
              (0 if segments else DELTANET_NO_SEGMENTS) |
              (DELTANET_GATED if gated else 0) |
-             (DELTANET_FORCE_SPLIT if force_split else 0))
+             (DELTANET_FORCE_SPLIT if force_split else 0) | int(extra_flags))
     return deltanet_desc(B, H, L, Dk, Dv, chunk, dt, flags, eps)
 
 
 def _desc_for(q, v, chunk, l2norm, save_states, force_simt, eps, segments=True, gated=False,
-              force_split=False):
+              force_split=False, extra_flags=0):
     B, H, L, Dk = q.shape
     return make_desc(B, H, L, Dk, v.shape[-1], chunk, q.dtype, l2norm, save_states,
-                     force_simt, eps, segments, gated, force_split)
+                     force_simt, eps, segments, gated, force_split, extra_flags)
 
 
 def deltanet_workspace_bytes(desc: deltanet_desc) -> int:
@@ -192,7 +193,7 @@ def _stream(device):
 
 def deltanet_fwd(q, k, v, beta, *, chunk=64, l2norm=True, h0=None, save_states=True,
                  workspace=None, want_hT=True, force_simt=False, eps=1e-6, out=None,
-                 segments=True, force_split=False):
+                 segments=True, force_split=False, extra_flags=0):
     """Forward of the chunkwise delta rule (§3.2 Eq. 8-11).
     ``segments=False`` forbids the segment-parallel forward (DESIGN.md §4.6);
     ``force_split`` selects the split tcgen05 kernels at d = 128 (§4.10).
@@ -204,7 +205,7 @@ def deltanet_fwd(q, k, v, beta, *, chunk=64, l2norm=True, h0=None, save_states=T
     _need(h0, "h0", torch.float32, dev)
     _need_inputs(q, k, v, beta)
     d = _desc_for(q, v, chunk, l2norm, save_states, force_simt, eps, segments,
-                  force_split=force_split)
+                  force_split=force_split, extra_flags=extra_flags)
     B, H, L, Dk = q.shape
     Dv = v.shape[-1]
     _need_out(h0, "h0", (B, H, Dk, Dv), torch.float32, dev)
@@ -314,7 +315,7 @@ def deltanet_prologue_bwd(xq, xk, xv, xb, wq, wk, wv, dq, dk, dv, dbeta, *, silu
 
 def deltanet_bwd(q, k, v, beta, dO, *, chunk=64, l2norm=True, h0=None, dhT=None,
                  workspace=None, states_saved=True, want_dh0=True, force_simt=False,
-                 eps=1e-6, out=None, segments=True, force_split=False):
+                 eps=1e-6, out=None, segments=True, force_split=False, extra_flags=0):
     """Backward: gradients w.r.t. raw q, k, v, beta (and h0).  With
     states_saved=True the workspace must come from deltanet_fwd(save_states=True)
     on the same inputs.  Returns (dq, dk, dv, dbeta, dh0 or None)."""
@@ -327,7 +328,7 @@ def deltanet_bwd(q, k, v, beta, dO, *, chunk=64, l2norm=True, h0=None, dhT=None,
     if workspace is None:
         states_saved = False
     d = _desc_for(q, v, chunk, l2norm, states_saved, force_simt, eps, segments,
-                  force_split=force_split)
+                  force_split=force_split, extra_flags=extra_flags)
     B, H, L, Dk = q.shape
     Dv = v.shape[-1]
     _need_inputs(q, k, v, beta, dO)

@@ -256,6 +256,7 @@ __global__ void __launch_bounds__(NT, 1)
   const int T0 = cbase * C;
   const int L = a.L - T0;
   const bool l2 = (a.flags & DELTANET_L2NORM_QK) != 0;
+  const bool comp = (a.flags & DELTANET_COMPENSATED) != 0;  // DESIGN.md R19
   const float eps = a.eps;
   const __nv_bfloat16* beta = (const __nv_bfloat16*)a.beta + (size_t)unit * a.L + T0;
   __nv_bfloat16* dbeta = (__nv_bfloat16*)a.dbeta + (size_t)unit * a.L + T0;
@@ -710,7 +711,8 @@ __global__ void __launch_bounds__(NT, 1)
         hd = warp_sum(hd);
         if (lane == 0) hdot[warp] = hd;
       }
-      if (l2 && !SEG1) {  // U'^T[dv][t] = Z^T[dv][t] * max(|k_t|, eps)  (row dv = w)
+      if (l2 && !SEG1 && !comp) {  // U'^T[dv][t] = Z^T[dv][t] * max(|k_t|, eps)  (row dv = w)
+        // (with DELTANET_COMPENSATED the record holds U'^T itself; R19)
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           const int col = 32 * wg + g * 8;
@@ -983,6 +985,7 @@ __global__ void __launch_bounds__(NT, 1)
           const float cs = reduce_scatter<16>(t1, lane);
           colT1[wwarp * C + cb + (lane & 15)] = cs;
         }
+        float err[4] = {0.f, 0.f, 0.f, 0.f};  // DELTANET_COMPENSATED: dA rows
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           float x[8];
@@ -995,6 +998,15 @@ __global__ void __launch_bounds__(NT, 1)
               v *= lo ? gm : 1.f;
             }
             x[e] = (!lo || j <= r64) ? v : 0.f;
+          }
+          if (comp && lo) {  // dQ = dA K_hat sums dA over j: carry the bf16
+            // rounding error along j (4 interleaved 8-column blocks)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const float xv = x[e] + err[g];
+              x[e] = __bfloat162float(__float2bfloat16_rn(xv));
+              err[g] = xv - x[e];
+            }
           }
           il_store8(lo ? sDA : sY, C, r64, 32 * wg + g * 8, x);
         }

@@ -24,9 +24,10 @@ namespace dn {
 namespace tc {
 
 // Per-chunk record the tcgen05 forward writes (with DELTANET_SAVE_STATES)
-// for the backward, next to H_t: smem images of X = (I+L)^{-1} (bf16, IL
-// R=64 x 64, exactly lower-triangular) and Z^T = (diag(s) U')^T (IL R=128 x
-// 64).  Offsets in bytes.  (W is not needed: the backward
+// for the backward, next to H_t: images of X = (I+L)^{-1} (bf16, IL R=64 x
+// 64, exactly lower-triangular) and Z^T = (diag(s) U')^T (IL R=128 x 64) --
+// with DELTANET_COMPENSATED U'^T itself, rounded with the error carried
+// along the tokens (R19).  Offsets in bytes.  (W is not needed: the backward
 // uses W^T dU' = K_hat^T diag(beta) X^T dU' = K_hat^T dV.)
 constexpr int REC_X = 0, REC_Z = 64 * 64 * 2;
 constexpr int REC_N = REC_Z + 128 * 64 * 2;  // fp32 row norms [||k|| (64) | ||q|| (64)]

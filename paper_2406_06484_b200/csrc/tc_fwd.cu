@@ -54,7 +54,7 @@ constexpr int OFF_W = OFF_A + 2 * C * C * 2;     // W^T[2] IL R=128 x 64 (outsid
 constexpr int OFF_H = OFF_W + 2 * DK * C * 2;    // H^T   IL R=128 x 128
 constexpr int OFF_Z = OFF_H + DV * DK * 2;       // Z^T   IL R=128 x 64  | O staging
 constexpr int OFF_L = OFF_Z + DV * C * 2;        // L -> X fp32 [64][LS]
-// per-chunk vectors [2][beta, s, -, G, gamma, D][64] (G, gamma, D: gated only)
+// per-chunk vectors [2][beta, s, 1/s, G, gamma, D][64] (G, gamma, D: gated only)
 constexpr int NVEC = 6;
 constexpr int OFF_VEC = OFF_L + C * LS * 4 + 2 * 128 * 4;  // (LX, partial norms) | vectors
 constexpr int SMEM_BYTES = OFF_VEC + 2 * NVEC * C * 4;
@@ -73,6 +73,19 @@ constexpr uint32_t TM_U0 = 448;                  // U^T  buffer 0
 __device__ __forceinline__ uint32_t tm_u(int b) { return b ? TM_U1 : TM_U0; }
 
 enum { BAR_P = 1, BAR_S = 2 };  // named barriers of the two warpgroups
+
+// 32 fp32 columns [col, col+32) of this warp's 32 TMEM lanes
+__device__ __forceinline__ void ld32_cols(uint32_t tm, int warp, uint32_t col, float (&f)[32]) {
+  uint32_t r[2][16];
+  tmem_ld16(taddr(tm, warp * 32, col), r[0]);
+  tmem_ld16(taddr(tm, warp * 32, col + 16), r[1]);
+  tmem_ld_wait();
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    f[e] = __uint_as_float(r[0][e]);
+    f[16 + e] = __uint_as_float(r[1][e]);
+  }
+}
 
 #ifdef DN_DEBUG
 // Test-only intermediate dumps (tests/test_tc_debug.py builds with -DDN_DEBUG).
@@ -133,7 +146,7 @@ __device__ long long* dn_tim = nullptr;
 // (W = X diag(beta gamma) K_hat), Q rows are scaled by gamma in place before
 // O = Q H, H is rescaled by gamma_63 in TMEM, and the state update takes
 // Z_h = diag(s D) U' from TMEM (bf16 pairs) while O takes Z = diag(s) U'.
-template <bool SEG1, bool GATED = false>
+template <bool SEG1, bool GATED = false, bool COMP = false>
 __global__ void __launch_bounds__(NT, 1)
     tc_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                   const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mO,
@@ -152,6 +165,10 @@ __global__ void __launch_bounds__(NT, 1)
   // chain warp may then overwrite the slot with Q of chunk c+2; ADVICE r1:
   // q_done alone does not order those generic-proxy reads before the TMA)
   __shared__ uint64_t q_read;
+  // u_read: all 128 state threads have read U' of the chunk out of TMEM (the
+  // ungated U' record is formed after z_ready); the U buffer is released
+  // (bar_empty) only after it
+  __shared__ uint64_t u_read;
   __shared__ uint32_t tslot;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -191,6 +208,7 @@ __global__ void __launch_bounds__(NT, 1)
     mbar_init(&h_ready, 1);
     mbar_init(&st_free, 1);
     mbar_init(&q_read, 1);
+    mbar_init(&u_read, 128);
     mbar_fence_init();
     prefetch_tmap(&mQ);
     prefetch_tmap(&mK);
@@ -308,6 +326,7 @@ __global__ void __launch_bounds__(NT, 1)
           float inv = l2 ? 1.f / fmaxf(nrm, a.eps) : 1.f;
           if (t0 + i >= L) inv = 0.f;  // padded token: exact zero contribution
           vb[C + i] = inv;
+          vb[2 * C + i] = l2 ? fmaxf(nrm, a.eps) : 1.f;  // 1 / s (compensated rounding of Z)
           // ||k_i|| for the backward's record (it then needs no norm pass)
           if (recs) reinterpret_cast<float*>(recs + (size_t)c * REC_BYTES + REC_N)[i] = nrm;
         }
@@ -461,6 +480,7 @@ __global__ void __launch_bounds__(NT, 1)
     // Warpgroup S (warps 8-11): state chain conversions + output epilogue
     // =====================================================================
     float* qn2 = LX + C * LS;  // [2][64] partial ||q||^2 (region after LX)
+    constexpr bool comp = COMP;  // DELTANET_COMPENSATED (R19): its own instantiation
     {  // initial state: H^T row dv = w (TMEM lane w) from h0 [dk][dv] (segment
       // starts after the first: the scanned state; SEG1: zero)
       const float* h0 = SEG1 ? nullptr
@@ -572,16 +592,14 @@ __global__ void __launch_bounds__(NT, 1)
       fence_after_sync();
       TSTAMP(17);
       DBG(dbg_tmem(dn_dbg + D_UP, tm, tm_u(b), C, 128, w));
-      {  // Z^T[dv][t] = U'^T[dv][t] * s_t -> bf16 IL tile (row dv)
+      if (!comp) {  // Z^T[dv][t] = U'^T[dv][t] * s_t -> bf16 IL tile (row dv)
         float f[64];
         ld64(tm, wwarp, tm_u(b), f);
 #pragma unroll
         for (int t = 0; t < 64; ++t) f[t] *= vb[C + t];
 #pragma unroll
         for (int g = 0; g < 8; ++g) il_store8(sZ, DV, w, g * 8, f + g * 8);
-        if (GATED) {
-          // Z_h^T = Z^T diag(D) as bf16 pairs over U's first 32 TMEM columns
-          // (the A operand of H^T += Z_h^T K), and H^T *= gamma_63 in TMEM
+        if (GATED) {  // Z_h^T = Z^T diag(D) as bf16 pairs over U's first 32 TMEM columns
 #pragma unroll
           for (int h2 = 0; h2 < 2; ++h2) {
             uint32_t r[16];
@@ -592,6 +610,62 @@ __global__ void __launch_bounds__(NT, 1)
             }
             tmem_st16(taddr(tm, wwarp * 32, tm_u(b) + 16 * h2), r);
           }
+        }
+      } else {
+        // DELTANET_COMPENSATED (R19): Z (the operand of H += K^T Z
+        // and O += A Z) and U' (the backward's record) are rounded to bf16
+        // with the rounding error carried along the token axis, so prefix
+        // sums over tokens carry ~sqrt(4) roundings instead of sqrt(C)
+        // rounding errors are carried (in U' units: Z = s U', and the s_t of
+        // neighbouring tokens may differ by orders of magnitude) along
+        // 8-token blocks, four interleaved per 32-token half (ILP; DESIGN.md
+        // R19).  Only Z is on the state chain; the ungated U' record is
+        // formed after z_ready.
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          float f[32];
+          ld32_cols(tm, wwarp, tm_u(b) + 32 * h2, f);
+          float ez[4] = {0.f, 0.f, 0.f, 0.f}, eu[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+#pragma unroll
+            for (int blk = 0; blk < 4; ++blk) {
+              const int i = 8 * blk + e, t = 32 * h2 + i;
+              const float st = vb[C + t], nt = vb[2 * C + t];  // s_t, 1 / s_t
+              const float u = f[i];
+              const float xz = u + ez[blk];
+              f[i] = __bfloat162float(__float2bfloat16_rn(xz * st));
+              ez[blk] = fmaf(-f[i], nt, xz);
+              if (st == 0.f) f[i] = 0.f;  // padded token: exact zero
+              if (GATED && recs) {  // gated: the U' record inline (U's TMEM columns
+                // 0-31 take Z_h below)
+                const float xu = u + eu[blk];
+                const float ru = __bfloat162float(__float2bfloat16_rn(xu));
+                eu[blk] = xu - ru;
+                *reinterpret_cast<__nv_bfloat16*>(recs + (size_t)c * REC_BYTES + REC_Z +
+                                                  il_off(w, t, DV)) =
+                    __float2bfloat16_rn(st == 0.f ? 0.f : ru);
+              }
+            }
+          }
+#pragma unroll
+          for (int g = 0; g < 4; ++g) il_store8(sZ, DV, w, 32 * h2 + g * 8, f + g * 8);
+          if (GATED) {  // Z_h = Z diag(D) as bf16 pairs into U's columns [16 h2, 16 h2 + 16)
+            // (this half of U' is in registers; the other half lies in columns >= 32)
+            uint32_t zh[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int t = 32 * h2 + 2 * j;
+              zh[j] = pack_bf16(f[2 * j] * vb[5 * C + t], f[2 * j + 1] * vb[5 * C + t + 1]);
+            }
+            tmem_st16(taddr(tm, wwarp * 32, tm_u(b) + 16 * h2), zh);
+          }
+        }
+      }
+      {
+        if (GATED) {
+          // (Z_h^T = Z^T diag(D) is in U's first 32 TMEM columns, the A operand
+          // of H^T += Z_h^T K); H^T *= gamma_63 in TMEM
           const float gC = vb[4 * C + C - 1];
 #pragma unroll 1
           for (int hh = 0; hh < 2; ++hh) {
@@ -675,6 +749,45 @@ __global__ void __launch_bounds__(NT, 1)
       if (w == 0) {
         if (SEG1) mbar_arrive(&w_free);  // T1 consumed by the Psi update (ho_done)
         mbar_arrive(&h_ready);
+      }
+      if (!GATED && recs && comp) {
+        // the backward's U'^T record (IL R = 128 x 64), off the state chain
+        // (after h_ready, where this warpgroup would wait for the prep's next
+        // W^T anyway): U' is still in TMEM -- the chain warp releases the U
+        // buffer (bar_empty) only after u_read -- rounded with the error
+        // carried along the tokens
+        fence_after_sync();
+        uint8_t* rz = recs + (size_t)c * REC_BYTES + REC_Z;
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          float f[32];
+          ld32_cols(tm, wwarp, tm_u(b) + 32 * h2, f);
+          float eu[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+#pragma unroll
+            for (int blk = 0; blk < 4; ++blk) {
+              const int i = 8 * blk + e;
+              const float xu = f[i] + eu[blk];
+              f[i] = __bfloat162float(__float2bfloat16_rn(xu));
+              eu[blk] = xu - f[i];
+              if (vb[C + 32 * h2 + i] == 0.f) f[i] = 0.f;
+            }
+          }
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            uint4 v;
+            v.x = pack_bf16(f[g * 8 + 0], f[g * 8 + 1]);
+            v.y = pack_bf16(f[g * 8 + 2], f[g * 8 + 3]);
+            v.z = pack_bf16(f[g * 8 + 4], f[g * 8 + 5]);
+            v.w = pack_bf16(f[g * 8 + 6], f[g * 8 + 7]);
+            *reinterpret_cast<uint4*>(rz + il_off(w, 32 * h2 + g * 8, DV)) = v;
+          }
+        }
+      }
+      if (comp) {  // every state thread: its U' reads are complete
+        fence_before_sync();
+        mbar_arrive(&u_read);
       }
       TSTAMP(20);
     }
@@ -841,9 +954,11 @@ __global__ void __launch_bounds__(NT, 1)
         }
         mbar_wait(&z_ready, c & 1);
         fence_after_sync();
-        if (states) {  // Z^T of this chunk for the backward (read out before st_free)
-          bulk_store(reinterpret_cast<uint8_t*>(a.scratch) + ((size_t)unit * a.NC + cbase + c) * REC_BYTES +
-                         REC_Z,
+        if (states && !COMP) {
+          // Z^T of this chunk for the backward (read out before st_free); with
+          // DELTANET_COMPENSATED the state warpgroup stores U'^T instead
+          bulk_store(reinterpret_cast<uint8_t*>(a.scratch) +
+                         ((size_t)unit * a.NC + cbase + c) * REC_BYTES + REC_Z,
                      sZ, DV * C * 2);
           bulk_commit();
         }
@@ -869,7 +984,6 @@ __global__ void __launch_bounds__(NT, 1)
         }
         mma_commit(&ho_done);
         mbar_wait(&ho_done, c & 1);
-        mbar_arrive(&bar_empty[b]);  // A[b], vec[b] and U[b] are free for chunk c+2
         if (c + NKB < NC) {  // K of chunk c+NKB into this chunk's K slot
           const int ks = c % NKB;
           mbar_expect_tx(&k_full[ks], TILE);
@@ -877,6 +991,12 @@ __global__ void __launch_bounds__(NT, 1)
         }
         bulk_wait_read0();  // state save done reading sH
         mbar_arrive(&st_free);
+        // (after st_free: the state warpgroup reads U' for its record after
+        // h_ready, which follows its st_free wait)
+        // DELTANET_COMPENSATED: the state warpgroup reads U[b] and vec[b] for
+        // the U' record after h_ready; otherwise its U' reads precede z_ready
+        if (COMP) mbar_wait(&u_read, c & 1);
+        mbar_arrive(&bar_empty[b]);  // A[b], vec[b] and U[b] are free for chunk c+2
       }
       // O of the last chunk
       mbar_wait(&h_ready, NC & 1);
@@ -1150,6 +1270,10 @@ int tc_fwd(const Args& a0, cudaStream_t s) {
         cudaFuncSetAttribute(tc_fwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              SMEM_BYTES) != cudaSuccess ||
         cudaFuncSetAttribute(tc_fwd_kernel<false, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(tc_fwd_kernel<false, false, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(tc_fwd_kernel<false, true, true>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess)
       return DELTANET_ERR_CUDA;
     attr.mark();
@@ -1162,17 +1286,21 @@ int tc_fwd(const Args& a0, cudaStream_t s) {
       !make_il_map(&mO, a.o ? a.o : a.v, BH, a.L, DV, C))  // o == null: states only
     return DELTANET_ERR_CUDA;
   const int nseg = tc_seg_setup(a);
+  const bool comp = (a.flags & DELTANET_COMPENSATED) != 0;  // DESIGN.md R19
   if (a.g) {  // gated DeltaNet (R23): one CTA per unit
-    tc_fwd_kernel<false, true><<<BH, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);
+    if (comp) tc_fwd_kernel<false, true, true><<<BH, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);
+    else tc_fwd_kernel<false, true><<<BH, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);
     return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
   }
   if (nseg <= 1) {
-    tc_fwd_kernel<false><<<BH, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);
+    if (comp) tc_fwd_kernel<false, false, true><<<BH, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);
+    else tc_fwd_kernel<false><<<BH, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);
     return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
   }
   tc_fwd_kernel<true><<<BH * nseg, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);   // pass 1
   seg_scan_kernel<<<dim3(BH, DV / 16), 256, 0, s>>>(a);                     // pass 2
-  tc_fwd_kernel<false><<<BH * nseg, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);  // pass 3
+  if (comp) tc_fwd_kernel<false, false, true><<<BH * nseg, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);
+  else tc_fwd_kernel<false><<<BH * nseg, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);  // pass 3
   return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
 }
 

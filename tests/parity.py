@@ -36,7 +36,7 @@ def to_dev(a, dtype, dev="cuda"):
 
 
 def run_gpu(inp, dtype, chunk, l2norm=True, h0=None, dhT=None, force_simt=False,
-            save_states=True, segments=True, force_split=False):
+            save_states=True, segments=True, force_split=False, extra_flags=0):
     import paper_2406_06484_b200 as dn
     td = torch_dtype(dtype)
     q, k, v, b, dO = (to_dev(inp[f], td) for f in ("q", "k", "v", "beta", "dO"))
@@ -44,11 +44,13 @@ def run_gpu(inp, dtype, chunk, l2norm=True, h0=None, dhT=None, force_simt=False,
     dhTt = None if dhT is None else to_dev(dhT, torch.float32)
     o, hT, ws = dn.deltanet_fwd(q, k, v, b, chunk=chunk, l2norm=l2norm, h0=h0t,
                                 save_states=save_states, force_simt=force_simt,
-                                segments=segments, force_split=force_split)
+                                segments=segments, force_split=force_split,
+                                extra_flags=extra_flags)
     g = dn.deltanet_bwd(q, k, v, b, dO, chunk=chunk, l2norm=l2norm, h0=h0t, dhT=dhTt,
                         workspace=ws if save_states else None,
                         states_saved=save_states, force_simt=force_simt,
-                        segments=segments, force_split=force_split)
+                        segments=segments, force_split=force_split,
+                        extra_flags=extra_flags)
     torch.cuda.synchronize()
     f = lambda t: None if t is None else t.float().cpu().numpy().astype(np.float64)
     return {"o": f(o), "hT": f(hT), "dq": f(g[0]), "dk": f(g[1]), "dv": f(g[2]),

@@ -115,17 +115,21 @@ def test_bf16_with_initial_state():
 
 
 @pytest.mark.parametrize("keys", ["gaussian", "identical"])
-def test_bf16_key_distributions(keys):
+@pytest.mark.parametrize("compensated", [False, True])
+def test_bf16_key_distributions(keys, compensated):
     """Gaussian keys: the north_star bar.  "identical" (every key of a unit
     equal, beta = 1) is an adversarial case outside the paper's workload:
     T^{-1} is bidiagonal, U = T^{-1} V holds differences v_i - v_{i-1}, and the
-    state update telescopes a sum of C bf16-rounded MMA operands, so the
-    expected error is ~sqrt(C) 2^-9 = 0.016 of the result (forward); the
-    backward differentiates those differences again (P = X^T dU' holds
-    dU'_t - dU'_{t+1}), roughly doubling it.  Its bar is 6e-2 (R19)."""
+    state update, the intra-chunk output and dQ = dA K_hat sum C bf16-rounded
+    operands whose sum telescopes: ~sqrt(C) 2^-9 of the result (hT 0.021,
+    dq 0.023 measured).  DELTANET_COMPENSATED carries the rounding error
+    along the tokens (R19) and brings it under the north_star bar
+    2e-2 (hT 0.008, dq 0.018); without it this case keeps the bar 3e-2."""
+    import paper_2406_06484_b200 as dn
     cfg, inp = _case(1, 2, 192, 128, 128, 64, "bf16", keys=keys, index=502)
-    got = run_gpu(inp, "bf16", 64)
-    compare(got, run_oracle(inp), TOL["bf16"] if keys != "identical" else 6e-2)
+    got = run_gpu(inp, "bf16", 64, extra_flags=dn.DELTANET_COMPENSATED if compensated else 0)
+    bar = TOL["bf16"] if (keys != "identical" or compensated) else 3e-2
+    compare(got, run_oracle(inp), bar)
 
 
 def test_bf16_deterministic():

@@ -266,16 +266,17 @@ def test_bf16_long_context_sampled_units():
 
 @pytest.mark.parametrize("name", ["hd256", "sharded"])
 def test_bf16_remaining_configs_sampled_units(name):
-    """BASELINE configs[3] (d=256; until its tcgen05 kernels exist it runs
-    on the CUDA-core kernels, which bf16 reaches only with FORCE_SIMT) and
-    configs[4] (B=64: 1024 units, several waves) at full size; two sampled
-    units against the oracle."""
+    """BASELINE configs[3] (d=256, the split tcgen05 kernels; every unit is
+    checked in test_gpu_split.py) and configs[4] (B=64: 1024 units, several
+    waves) at full size on their default paths; two sampled units against
+    the oracle."""
     import paper_2406_06484_b200 as dn
     cfg = synth.CONFIGS[name]
     units = [(0, 0), (cfg.B - 1, cfg.H - 1)]
     inp = synth.make_inputs(cfg)
     d = dn.make_desc(cfg.B, cfg.H, cfg.L, cfg.Dk, cfg.Dv, cfg.chunk, torch.bfloat16)
-    got = run_gpu(inp, "bf16", cfg.chunk, force_simt=dn.deltanet_path(d) != 1)
+    assert dn.deltanet_path(d) == (2 if cfg.Dk == 256 else 1)
+    got = run_gpu(inp, "bf16", cfg.chunk)
     for (b, h) in units:
         one = {f: inp[f][b:b + 1, h:h + 1] for f in inp}
         ref = run_oracle(one)

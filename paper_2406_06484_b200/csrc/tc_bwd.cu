@@ -85,9 +85,9 @@ constexpr uint32_t TM_KH = 448;                          // (K H)[:, :64] | [:, 
 enum { BAR_SIMT = 1 };
 // issuer -> SIMT: MMA commits and TMA arrivals
 enum { MB_AL, MB_R, MB_DU, MB_P, MB_DH, MB_A, MB_LD, MB_GB, MB_K, MB_MAIN, MB_QL, MB_KL0, MB_KL1, MB_DHK,
-       MB_N };
+       MB_P1, MB_N };
 // SIMT -> issuer hand-offs (SG_STG: issuer -> SIMT, staging regions free)
-enum { SG_DHI, SG_A, SG_P3, SG_P5, SG_P6, SG_P7, SG_P8, SG_STG, SG_RFREE, SG_N };
+enum { SG_DHI, SG_A, SG_P3, SG_P5, SG_P6, SG_P7, SG_P8, SG_STG, SG_RFREE, SG_P5A, SG_N };
 
 __device__ __forceinline__ void ld32(uint32_t tm, int wwarp, uint32_t col, float (&f)[32]) {
   uint32_t r[2][16];
@@ -446,6 +446,14 @@ __global__ void __launch_bounds__(NT, 1)
                      GATED ? k0 > 0 : 1);
           mma_commit(&mb[MB_DU]);
         }
+        if (!GATED && !SEG1) {
+          // M2b: dQ = dO H^T now, under P3 (the tensor pipe would idle there;
+          // TM_DQ was read by P8 of chunk c+1, which precedes SG_A of chunk c)
+          const uint32_t id_q = idesc_bf16(64, 128, false, true);
+#pragma unroll
+          for (int k0 = 0; k0 < D; k0 += 16)
+            mma_bf16(tm + TM_DQ, desc_k(aDO, C, k0), desc_mn(aH, D, k0), id_q, k0 > 0);
+        }
 
         // M3: P = X^T dU' (two N=64 halves), dX' = dU' R^T
         // M4a: dH += Q_hat^T dO ; dK = U' dH^T (dH image of chunk c+1) ; K_hat K_hat^T
@@ -483,6 +491,7 @@ __global__ void __launch_bounds__(NT, 1)
             mma_bf16(tm + TM_P + LO16, desc_mn(aX, C, k0), desc_k(aDUP + HALF_ROWS, D, k0), idp,
                      k0 > 0);
           }
+          mma_commit(&mb[MB_P1]);  // P alone: P5 starts on dV while dX' runs
           if (!SEG1) {
 #pragma unroll
             for (int k0 = 0; k0 < D; k0 += 16)
@@ -508,8 +517,10 @@ __global__ void __launch_bounds__(NT, 1)
         ISTAMP(22);
 
         // M4b: dH -= W^T dU' = K_hat^T dV  (W = X diag(b) K_hat, dV = diag(b) X^T dU')
-        // M5: dA, Y | dQ = dO H^T, dK -= dV H^T
-        mbar_wait(&sg[SG_P5], ph);
+        // M5: dA, Y | dK -= dV H^T (ungated: dQ = dO H^T was M2b)
+        // (ungated full backward: M4b as soon as dV is staged, SG_P5A, so
+        // the dH update overlaps P5's dX conversion)
+        mbar_wait(&sg[(!GATED && !SEG1) ? SG_P5A : SG_P5], ph);
         fence_after_sync();
         ISTAMP(23);
         {
@@ -523,9 +534,12 @@ __global__ void __launch_bounds__(NT, 1)
             mma_commit(&mb[MB_GB]);
             continue;
           }
+          if (!GATED) {  // dX staged (Y reads it)
+            mbar_wait(&sg[SG_P5], ph);
+            fence_after_sync();
+          }
           const uint32_t id_da = idesc_bf16(64, 64, false, true);
           const uint32_t id_y = idesc_bf16(64, 64, true, true);
-          const uint32_t id_q = idesc_bf16(64, 128, false, true);
           const uint32_t id_k2 = idesc_bf16(64, 128, false, true, true);
 #pragma unroll
           for (int k0 = 0; k0 < D; k0 += 16)
@@ -535,10 +549,8 @@ __global__ void __launch_bounds__(NT, 1)
             mma_bf16(tm + TM_Y, desc_mn(aX, C, k0), desc_mn(aDX, C, k0), id_y, k0 > 0);
           mma_commit(&mb[MB_A]);
 #pragma unroll
-          for (int k0 = 0; k0 < D; k0 += 16) {
-            if (!GATED) mma_bf16(tm + TM_DQ, desc_k(aDO, C, k0), desc_mn(aH, D, k0), id_q, k0 > 0);
+          for (int k0 = 0; k0 < D; k0 += 16)
             mma_bf16(tm + TM_DK, desc_k(aDV, C, k0), desc_mn(aH, D, k0), id_k2, 1);
-          }
           if (!GATED) mma_commit(&mb[MB_LD]);
         }
         ISTAMP(24);
@@ -823,7 +835,7 @@ __global__ void __launch_bounds__(NT, 1)
 
       // ================= P5: P, R -> dV, dbeta part ; dX  (SEG1: dV only)
       if (tid < C && c > 0) bnext = __bfloat162float(beta[t0 - C + tid]);
-      mbar_wait(&mb[MB_P], ph);
+      mbar_wait(&mb[(!GATED && !SEG1) ? MB_P1 : MB_P], ph);  // (ungated: P; dX' below)
       fence_after_sync();
       BSTAMP(7);
       if (SEG1) {  // dV = diag(beta) P only (the chain's K_hat^T dV)
@@ -901,6 +913,11 @@ __global__ void __launch_bounds__(NT, 1)
             pk += __shfl_xor_sync(0xffffffffu, pk, 16);
             if (lo) pkh[wg * C + r64] = pk;
           }
+        }
+        if (!GATED) {  // dV staged: M4b (the dH update) can start; then dX'
+          simt_signal(&sg[SG_P5A], tid);
+          mbar_wait(&mb[MB_P], ph);
+          fence_after_sync();
         }
 #pragma unroll 1
         for (int cc = 0; cc < 2; ++cc) {  // dX = dX' diag(beta) (lanes < 16: dX' rows)

@@ -1218,7 +1218,7 @@ __global__ void __launch_bounds__(256) seg_scan_bwd_kernel(Args a) {
     float acc[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[e] = hl[e];
-#pragma unroll 4
+#pragma unroll 32  // row i of Psi: 32 consecutive loads in flight per thread
     for (int r = 0; r < D; ++r) {
       const float pv = psi[r];  // Psi[i][r]
 #pragma unroll

@@ -1031,7 +1031,7 @@ __global__ void __launch_bounds__(256) seg_scan_kernel(Args a) {
     float acc[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[e] = hl[e];
-#pragma unroll 4
+#pragma unroll 16  // 16 global loads in flight per thread (latency-bound otherwise)
     for (int r = 0; r < DK; ++r) {
       const float pv = psi[(size_t)r * DK + i];  // Psi[r][i]
 #pragma unroll

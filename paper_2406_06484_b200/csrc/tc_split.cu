@@ -91,16 +91,18 @@ struct SP {
 // workspace layout of the split path (after the states region, which holds
 // the H_j^T images [unit][chunk][block], 64 x D bf16 each)
 struct SpLayout {
-  __nv_bfloat16 *qh, *kh;  // [BH][L][D] normalised q, k
+  // normalised q, k as per-(unit, chunk) IL smem images (64 x D bf16 each):
+  // one contiguous bulk copy per tile (a [B,H,L,D] TMA box moves 16 B rows)
+  uint8_t *qh, *kh;
   uint8_t *rec1, *rec2;
 };
 template <int D>
 __host__ __device__ inline SpLayout sp_layout(const Args& a) {
   SpLayout s;
-  const size_t qk = ((size_t)a.B * a.H * a.L * D * 2 + 255) & ~(size_t)255;
+  const size_t qk = (size_t)a.B * a.H * a.NC * SP<D>::TILE;
   uint8_t* base = reinterpret_cast<uint8_t*>(a.scratch);
-  s.qh = reinterpret_cast<__nv_bfloat16*>(base);
-  s.kh = reinterpret_cast<__nv_bfloat16*>(base + qk);
+  s.qh = base;
+  s.kh = base + qk;
   s.rec1 = base + 2 * qk;
   s.rec2 = s.rec1 + (size_t)a.B * a.H * a.NC * SP<D>::R1_BYTES;
   return s;
@@ -146,7 +148,6 @@ __device__ __forceinline__ void hand_off(uint64_t* bar, int tid) {
 template <int D>
 __global__ void __launch_bounds__(288, 2)
     sp_prep_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
-                   const __grid_constant__ CUtensorMap mQh, const __grid_constant__ CUtensorMap mKh,
                    Args a) {
   using S = SP<D>;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -194,8 +195,9 @@ __global__ void __launch_bounds__(288, 2)
     if (lane == 0) {
       const uint32_t aq = smem_u32(sQ), ak = smem_u32(sK), at = smem_u32(sT);
       mbar_wait(&norm_done, 0);
-      tma_store_4d(&mQh, sQ, 0, t0, 0, unit);
-      tma_store_4d(&mKh, sK, 0, t0, 0, unit);
+      const size_t img = ((size_t)unit * a.NC + c) * S::TILE;
+      bulk_store(ly.qh + img, sQ, S::TILE);
+      bulk_store(ly.kh + img, sK, S::TILE);
       bulk_commit();
       fence_after_sync();
       const uint32_t idg = idesc_bf16(64, 64, false, false);
@@ -382,9 +384,7 @@ __host__ __device__ constexpr int fchain_smem() {
 
 template <int D>
 __global__ void __launch_bounds__(288, 1)
-    sp_fwd_chain_kernel(const __grid_constant__ CUtensorMap mQh,
-                        const __grid_constant__ CUtensorMap mKh,
-                        const __grid_constant__ CUtensorMap mV64, Args a) {
+    sp_fwd_chain_kernel(const __grid_constant__ CUtensorMap mV64, Args a) {
   using S = SP<D>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sQ = smem;
@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(288, 1)
     if (lane == 0) {
       auto load_q = [&](int c) {
         mbar_expect_tx(&q_full, S::TILE);
-        tma_load_4d(sQ, &mQh, 0, c * C, 0, unit, &q_full);
+        bulk_load(sQ, ly.qh + ((size_t)unit * NC + c) * S::TILE, S::TILE, &q_full);
       };
       auto load_vtw = [&](int c) {
         mbar_expect_tx(&vt_full, 2 * BLK);
@@ -448,7 +448,8 @@ __global__ void __launch_bounds__(288, 1)
       auto load_ka = [&](int c) {
         const int b = c & 1;
         mbar_expect_tx(&k_full[b], S::TILE);
-        tma_load_4d(sKb + b * S::TILE, &mKh, 0, c * C, 0, unit, &k_full[b]);
+        bulk_load(sKb + b * S::TILE, ly.kh + ((size_t)unit * NC + c) * S::TILE, S::TILE,
+                  &k_full[b]);
         mbar_expect_tx(&a_full[b], BLK);
         bulk_load(sAb + b * BLK, r1(c) + S::R1_A, BLK, &a_full[b]);
       };
@@ -635,9 +636,7 @@ __host__ __device__ constexpr int bchain_smem() {
 
 template <int D>
 __global__ void __launch_bounds__(288, 1)
-    sp_bwd_chain_kernel(const __grid_constant__ CUtensorMap mQh,
-                        const __grid_constant__ CUtensorMap mKh,
-                        const __grid_constant__ CUtensorMap mV64,
+    sp_bwd_chain_kernel(const __grid_constant__ CUtensorMap mV64,
                         const __grid_constant__ CUtensorMap mDO64, Args a) {
   using S = SP<D>;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -699,7 +698,8 @@ __global__ void __launch_bounds__(288, 1)
       // slots by iteration parity: chunk c = NC-1-it uses slot it & 1
       auto load_kdo = [&](int c, int slot) {
         mbar_expect_tx(&k_full[slot], S::TILE);
-        tma_load_4d(sKb + slot * S::TILE, &mKh, 0, c * C, 0, unit, &k_full[slot]);
+        bulk_load(sKb + slot * S::TILE, ly.kh + ((size_t)unit * NC + c) * S::TILE, S::TILE,
+                  &k_full[slot]);
         mbar_expect_tx(&do_full[slot], BLK);
         tma_load_4d(sDOb + slot * BLK, &mDO64, 0, c * C, 8 * j, unit, &do_full[slot]);
       };
@@ -721,7 +721,7 @@ __global__ void __launch_bounds__(288, 1)
       };
       auto load_q = [&](int c) {
         mbar_expect_tx(&q_full, S::TILE);
-        tma_load_4d(sQ, &mQh, 0, c * C, 0, unit, &q_full);
+        bulk_load(sQ, ly.qh + ((size_t)unit * NC + c) * S::TILE, S::TILE, &q_full);
       };
       if (NC > 0) {
         load_kdo(NC - 1, 0);
@@ -982,9 +982,7 @@ __host__ __device__ constexpr int blocal_smem() {
 
 template <int D>
 __global__ void __launch_bounds__(288, 1)
-    sp_bwd_local_kernel(const __grid_constant__ CUtensorMap mQh,
-                        const __grid_constant__ CUtensorMap mKh,
-                        const __grid_constant__ CUtensorMap mDO64,
+    sp_bwd_local_kernel(const __grid_constant__ CUtensorMap mDO64,
                         const __grid_constant__ CUtensorMap mDV64,
                         const __grid_constant__ CUtensorMap mDQ,
                         const __grid_constant__ CUtensorMap mDK, Args a) {
@@ -1075,11 +1073,11 @@ __global__ void __launch_bounds__(288, 1)
       };
       auto load_qh = [&]() {
         mbar_expect_tx(&qh_full, S::TILE);
-        tma_load_4d(sQ, &mQh, 0, t0, 0, unit, &qh_full);
+        bulk_load(sQ, ly.qh + ((size_t)unit * NC + c) * S::TILE, S::TILE, &qh_full);
       };
       auto load_kh = [&]() {
         mbar_expect_tx(&kh_full, S::TILE);
-        tma_load_4d(sK, &mKh, 0, t0, 0, unit, &kh_full);
+        bulk_load(sK, ly.kh + ((size_t)unit * NC + c) * S::TILE, S::TILE, &kh_full);
       };
       load_s(0);
       load_i(0);
@@ -1358,14 +1356,13 @@ int sp_fwd_t(const Args& a0, cudaStream_t s) {
   Args a = a0;
   const int BH = a.B * a.H;
   const SpLayout ly = sp_layout<D>(a);
-  CUtensorMap mQ, mK, mQh, mKh, mV64;
+  CUtensorMap mQ, mK, mV64;
   if (!make_map(&mQ, a.q, BH, a.L, D, D / 8) || !make_map(&mK, a.k, BH, a.L, D, D / 8) ||
-      !make_map(&mQh, ly.qh, BH, a.L, D, D / 8) || !make_map(&mKh, ly.kh, BH, a.L, D, D / 8) ||
       !make_map(&mV64, a.v, BH, a.L, D, 8))
     return DELTANET_ERR_CUDA;
   if (a.NC > 0)
-    sp_prep_kernel<D><<<dim3(a.NC, BH), 288, prep_smem<D>(), s>>>(mQ, mK, mQh, mKh, a);
-  sp_fwd_chain_kernel<D><<<dim3(SP<D>::NB, BH), 288, fchain_smem<D>(), s>>>(mQh, mKh, mV64, a);
+    sp_prep_kernel<D><<<dim3(a.NC, BH), 288, prep_smem<D>(), s>>>(mQ, mK, a);
+  sp_fwd_chain_kernel<D><<<dim3(SP<D>::NB, BH), 288, fchain_smem<D>(), s>>>(mV64, a);
   return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
 }
 
@@ -1382,16 +1379,14 @@ int sp_bwd_t(const Args& a0, cudaStream_t s) {
   }
   const int BH = a.B * a.H;
   const SpLayout ly = sp_layout<D>(a);
-  CUtensorMap mQh, mKh, mV64, mDO64, mDV64, mDQ, mDK;
-  if (!make_map(&mQh, ly.qh, BH, a.L, D, D / 8) || !make_map(&mKh, ly.kh, BH, a.L, D, D / 8) ||
-      !make_map(&mV64, a.v, BH, a.L, D, 8) || !make_map(&mDO64, a.dO, BH, a.L, D, 8) ||
+  CUtensorMap mV64, mDO64, mDV64, mDQ, mDK;
+  if (!make_map(&mV64, a.v, BH, a.L, D, 8) || !make_map(&mDO64, a.dO, BH, a.L, D, 8) ||
       !make_map(&mDV64, a.dv, BH, a.L, D, 8) || !make_map(&mDQ, a.dq, BH, a.L, D, D / 8) ||
       !make_map(&mDK, a.dk, BH, a.L, D, D / 8))
     return DELTANET_ERR_CUDA;
-  sp_bwd_chain_kernel<D><<<dim3(SP<D>::NB, BH), 288, bchain_smem<D>(), s>>>(mQh, mKh, mV64,
-                                                                            mDO64, a);
+  sp_bwd_chain_kernel<D><<<dim3(SP<D>::NB, BH), 288, bchain_smem<D>(), s>>>(mV64, mDO64, a);
   if (a.NC > 0)
-    sp_bwd_local_kernel<D><<<dim3(a.NC, BH), 288, blocal_smem<D>(), s>>>(mQh, mKh, mDO64, mDV64,
+    sp_bwd_local_kernel<D><<<dim3(a.NC, BH), 288, blocal_smem<D>(), s>>>(mDO64, mDV64,
                                                                         mDQ, mDK, a);
   return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
 }
@@ -1407,7 +1402,7 @@ bool sp_supported(const deltanet_desc* d) {
 size_t sp_scratch_bytes(const deltanet_desc* d) {
   const int D = d->Dk;
   const size_t BH = (size_t)d->B * d->H, NC = (size_t)(d->L + C - 1) / C;
-  const size_t qk = (BH * d->L * D * 2 + 255) & ~(size_t)255;
+  const size_t qk = BH * NC * (size_t)C * D * 2;  // q_hat / k_hat images
   size_t r1 = 0, r2 = 0;
   switch (D) {
     case 64: r1 = SP<64>::R1_BYTES; r2 = SP<64>::NB * (size_t)SP<64>::R2_BYTES; break;

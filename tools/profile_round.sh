@@ -12,7 +12,8 @@ TAG=${1:-r02}
 mkdir -p gpurun_out
 python -c "from paper_2406_06484_b200.build import sources_sha; print(sources_sha())" \
   > gpurun_out/sha_$TAG.txt
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
+  -k regex:"tc_|sp_|simt_|rec_fwd|prologue|seg_scan|cp_" \
   --log-file gpurun_out/launches_$TAG.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/launches_$TAG.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on \
@@ -22,4 +23,5 @@ timeout 900 ncu --set full --clock-control none --import-source on \
 timeout 900 ncu --set full --clock-control none --import-source on \
   -k regex:"sp_" -s 4 -c 4 -o gpurun_out/prof_${TAG}_split -f \
   python tools/hd256_time.py 256 > gpurun_out/prof_${TAG}_split.log 2>&1
+timeout 600 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
 ls -la gpurun_out/*$TAG*

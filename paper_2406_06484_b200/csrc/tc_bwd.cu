@@ -1204,23 +1204,24 @@ __global__ void __launch_bounds__(NT, 1)
 // the backward's per-chunk maps are the transposes of the forward's).  A CTA
 // scans one 16-column block; fp32.
 __global__ void __launch_bounds__(256) seg_scan_bwd_kernel(Args a) {
-  __shared__ float Hs[D][16];
+  extern __shared__ __align__(16) float scan_sm[];
+  float* Ps = scan_sm;  // Psi_s, row stride PSI_LD (tc_common.cuh stage_psi)
+  float(*Hs)[16] = reinterpret_cast<float(*)[16]>(scan_sm + D * PSI_LD);
   const int unit = blockIdx.x, j0 = blockIdx.y * 16, nseg = a.nseg;
   const int tid = threadIdx.x, i = tid >> 1, jj = (tid & 1) * 8;
   for (int e = tid; e < D * 16; e += blockDim.x) {
     const int r = e / 16, cc = e % 16;
     Hs[r][cc] = a.dhT ? a.dhT[(size_t)unit * D * D + (size_t)r * D + j0 + cc] : 0.f;
   }
-  __syncthreads();
   for (int sg = nseg - 1; sg >= 1; --sg) {
-    const float* psi = a.psi + ((size_t)unit * nseg + sg) * D * D + (size_t)i * D;
     const float* hl = a.hloc + ((size_t)unit * nseg + sg) * D * D + (size_t)i * D + j0 + jj;
     float acc[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[e] = hl[e];
-#pragma unroll 32  // row i of Psi: 32 consecutive loads in flight per thread
+    stage_psi(Ps, a.psi + ((size_t)unit * nseg + sg) * D * D, tid);
+#pragma unroll 8
     for (int r = 0; r < D; ++r) {
-      const float pv = psi[r];  // Psi[i][r]
+      const float pv = Ps[i * PSI_LD + r];  // Psi[i][r]
 #pragma unroll
       for (int e = 0; e < 8; ++e) acc[e] = fmaf(pv, Hs[r][jj + e], acc[e]);
     }
@@ -1231,9 +1232,9 @@ __global__ void __launch_bounds__(256) seg_scan_bwd_kernel(Args a) {
       Hs[i][jj + e] = acc[e];
       out[e] = acc[e];
     }
-    __syncthreads();
   }
 }
+constexpr int SEG_SCAN_BWD_SMEM = PSI_SMEM;
 
 }  // namespace
 
@@ -1281,7 +1282,16 @@ int tc_bwd(const Args& a0, cudaStream_t s) {
   }
   // segment-parallel backward, with the forward's Psi
   tc_bwd_kernel<true><<<BH * nseg, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mDO, mDQ, mDK, mDV, a);
-  seg_scan_bwd_kernel<<<dim3(BH, D / 16), 256, 0, s>>>(a);
+  {
+    static PerDevice sattr;
+    if (!sattr.done()) {
+      if (cudaFuncSetAttribute(seg_scan_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               SEG_SCAN_BWD_SMEM) != cudaSuccess)
+        return DELTANET_ERR_CUDA;
+      sattr.mark();
+    }
+  }
+  seg_scan_bwd_kernel<<<dim3(BH, D / 16), 256, SEG_SCAN_BWD_SMEM, s>>>(a);
   tc_bwd_kernel<false><<<BH * nseg, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mDO, mDQ, mDK, mDV, a);
   return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
 }

@@ -501,3 +501,34 @@ __device__ __forceinline__ void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, ui
 
 }  // namespace tc
 }  // namespace dn
+
+namespace dn {
+namespace tc {
+
+// Segment / context-parallel scans (tc_fwd.cu, tc_bwd.cu): stage a 128 x 128
+// fp32 matrix (64 KB, global) in shared memory with row stride 129 floats
+// (conflict-free reads along rows and along columns), 256 threads with all
+// of their 16 float4 loads in flight; the scans are latency-bound otherwise.
+constexpr int PSI_LD = 129;
+constexpr int PSI_SMEM = (128 * PSI_LD + 128 * 16) * 4;  // + the 128 x 16 state block
+__device__ __forceinline__ void stage_psi(float* Ps, const float* psi, int tid) {
+  float4 v[16];
+  const float4* src = reinterpret_cast<const float4*>(psi);
+#pragma unroll
+  for (int q = 0; q < 16; ++q) v[q] = src[tid + 256 * q];
+  __syncthreads();  // the previous step's readers of Ps (and writers of the state) are done
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int f = (tid + 256 * q) * 4, row = f >> 7, col = f & 127;
+    float* d = Ps + row * PSI_LD + col;
+    d[0] = v[q].x;
+    d[1] = v[q].y;
+    d[2] = v[q].z;
+    d[3] = v[q].w;
+  }
+  __syncthreads();
+}
+
+}  // namespace tc
+}  // namespace dn
+

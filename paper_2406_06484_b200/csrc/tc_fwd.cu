@@ -1017,23 +1017,24 @@ __global__ void __launch_bounds__(NT, 1)
 // from H_start(0) = h0.  The columns of H evolve independently: a CTA scans
 // one 16-column block; fp32 throughout.
 __global__ void __launch_bounds__(256) seg_scan_kernel(Args a) {
-  __shared__ float Hs[DK][16];
+  extern __shared__ __align__(16) float scan_sm[];
+  float* Ps = scan_sm;  // Psi_s, row stride PSI_LD (tc_common.cuh stage_psi)
+  float(*Hs)[16] = reinterpret_cast<float(*)[16]>(scan_sm + DK * PSI_LD);
   const int unit = blockIdx.x, j0 = blockIdx.y * 16, nseg = a.nseg;
   const int tid = threadIdx.x, i = tid >> 1, jj = (tid & 1) * 8;
   for (int e = tid; e < DK * 16; e += blockDim.x) {
     const int r = e / 16, cc = e % 16;
     Hs[r][cc] = a.h0 ? a.h0[(size_t)unit * DK * DV + (size_t)r * DV + j0 + cc] : 0.f;
   }
-  __syncthreads();
   for (int sg = 0; sg + 1 < nseg; ++sg) {
-    const float* psi = a.psi + ((size_t)unit * nseg + sg) * DK * DK;
     const float* hl = a.hloc + ((size_t)unit * nseg + sg) * DK * DV + (size_t)i * DV + j0 + jj;
     float acc[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[e] = hl[e];
-#pragma unroll 16  // 16 global loads in flight per thread (latency-bound otherwise)
+    stage_psi(Ps, a.psi + ((size_t)unit * nseg + sg) * DK * DK, tid);
+#pragma unroll 8
     for (int r = 0; r < DK; ++r) {
-      const float pv = psi[(size_t)r * DK + i];  // Psi[r][i]
+      const float pv = Ps[r * PSI_LD + i];  // Psi[r][i]
 #pragma unroll
       for (int e = 0; e < 8; ++e) acc[e] = fmaf(pv, Hs[r][jj + e], acc[e]);
     }
@@ -1044,7 +1045,6 @@ __global__ void __launch_bounds__(256) seg_scan_kernel(Args a) {
       Hs[i][jj + e] = acc[e];
       out[e] = acc[e];
     }
-    __syncthreads();
   }
 }
 
@@ -1059,33 +1059,34 @@ struct ScanArgs {
   float* out;
 };
 __global__ void __launch_bounds__(256) cp_scan_kernel(ScanArgs sa) {
-  __shared__ float Hs[DK][16];
+  extern __shared__ __align__(16) float scan_sm[];
+  float* Ps = scan_sm;
+  float(*Hs)[16] = reinterpret_cast<float(*)[16]>(scan_sm + DK * PSI_LD);
   const int unit = blockIdx.x, j0 = blockIdx.y * 16;
   const int tid = threadIdx.x, i = tid >> 1, jj = (tid & 1) * 8;
   for (int e = tid; e < DK * 16; e += blockDim.x) {
     const int r = e / 16, cc = e % 16;
     Hs[r][cc] = sa.edge ? sa.edge[(size_t)unit * DK * DV + (size_t)r * DV + j0 + cc] : 0.f;
   }
-  __syncthreads();
   const int n = sa.reverse ? sa.nparts - 1 - sa.part : sa.part;
   for (int step = 0; step < n; ++step) {
     const int p = sa.reverse ? sa.nparts - 1 - step : step;
-    const float* psi = sa.psi + ((size_t)p * sa.units + unit) * DK * DK;
     const float* lc = sa.loc + ((size_t)p * sa.units + unit) * DK * DV + (size_t)i * DV + j0 + jj;
     float acc[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[e] = lc[e];
-#pragma unroll 4
+    stage_psi(Ps, sa.psi + ((size_t)p * sa.units + unit) * DK * DK, tid);
+#pragma unroll 8
     for (int r = 0; r < DK; ++r) {
-      const float pv = sa.reverse ? psi[(size_t)i * DK + r] : psi[(size_t)r * DK + i];
+      const float pv = sa.reverse ? Ps[i * PSI_LD + r] : Ps[r * PSI_LD + i];
 #pragma unroll
       for (int e = 0; e < 8; ++e) acc[e] = fmaf(pv, Hs[r][jj + e], acc[e]);
     }
     __syncthreads();
 #pragma unroll
     for (int e = 0; e < 8; ++e) Hs[i][jj + e] = acc[e];
-    __syncthreads();
   }
+  __syncthreads();
   for (int e = tid; e < DK * 16; e += blockDim.x) {
     const int r = e / 16, cc = e % 16;
     sa.out[(size_t)unit * DK * DV + (size_t)r * DV + j0 + cc] = Hs[r][cc];
@@ -1100,7 +1101,9 @@ __global__ void __launch_bounds__(256) cp_scan_kernel(ScanArgs sa) {
 __global__ void __launch_bounds__(256) cp_compose_kernel(int nseg, int bwd, const float* psi_s,
                                                          const float* loc_s, float* psi_out,
                                                          float* loc_out) {
-  __shared__ float Xs[DK][16];
+  extern __shared__ __align__(16) float scan_sm[];
+  float* Ps = scan_sm;
+  float(*Xs)[16] = reinterpret_cast<float(*)[16]>(scan_sm + DK * PSI_LD);
   const int unit = blockIdx.x;
   const bool do_psi = !bwd && blockIdx.y < DK / 16;
   const int j0 = (do_psi ? blockIdx.y : blockIdx.y - (bwd ? 0 : DK / 16)) * 16;
@@ -1111,29 +1114,28 @@ __global__ void __launch_bounds__(256) cp_compose_kernel(int nseg, int bwd, cons
     const int r = e / 16, cc = e % 16;
     Xs[r][cc] = do_psi ? P[(size_t)(nseg - 1) * DK * DK + (size_t)r * DK + j0 + cc] : 0.f;
   }
-  __syncthreads();
   const int n = do_psi ? nseg - 1 : nseg;
   for (int step = 0; step < n; ++step) {
     // fwd Psi: s = S-2 .. 0 (X <- Psi_s X); fwd Hloc: s = 0 .. S-1 (Psi_s^T);
     // bwd: s = S-1 .. 0 (Psi_s)
     const int sg = do_psi ? nseg - 2 - step : bwd ? nseg - 1 - step : step;
-    const float* ps = P + (size_t)sg * DK * DK;
     float acc[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e)
       acc[e] = do_psi ? 0.f : H[(size_t)sg * DK * DV + (size_t)i * DV + j0 + jj + e];
+    stage_psi(Ps, P + (size_t)sg * DK * DK, tid);
     const bool tr = !do_psi && !bwd;
-#pragma unroll 4
+#pragma unroll 8
     for (int r = 0; r < DK; ++r) {
-      const float pv = tr ? ps[(size_t)r * DK + i] : ps[(size_t)i * DK + r];
+      const float pv = tr ? Ps[r * PSI_LD + i] : Ps[i * PSI_LD + r];
 #pragma unroll
       for (int e = 0; e < 8; ++e) acc[e] = fmaf(pv, Xs[r][jj + e], acc[e]);
     }
     __syncthreads();
 #pragma unroll
     for (int e = 0; e < 8; ++e) Xs[i][jj + e] = acc[e];
-    __syncthreads();
   }
+  __syncthreads();
   float* out = do_psi ? psi_out + (size_t)unit * DK * DK : loc_out + (size_t)unit * DK * DV;
   for (int e = tid; e < DK * 16; e += blockDim.x) {
     const int r = e / 16, cc = e % 16;
@@ -1213,6 +1215,21 @@ size_t rec_bytes(int B, int H, int L) {
 }
 }  // namespace
 
+// dynamic shared memory opt-in of the scan kernels outside tc_fwd (per device)
+int scan_attrs() {
+  static PerDevice attr;
+  if (attr.done()) return DELTANET_OK;
+  if (cudaFuncSetAttribute(seg_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           PSI_SMEM) != cudaSuccess ||
+      cudaFuncSetAttribute(cp_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           PSI_SMEM) != cudaSuccess ||
+      cudaFuncSetAttribute(cp_compose_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           PSI_SMEM) != cudaSuccess)
+    return DELTANET_ERR_CUDA;
+  attr.mark();
+  return DELTANET_OK;
+}
+
 // Sequence segments per unit of the tcgen05 forward: when
 // B*H units leave SMs idle, each unit's chunks are split over up to
 // SMs / units CTAs (segments of >= 8 chunks, at most 16).
@@ -1274,7 +1291,8 @@ int tc_fwd(const Args& a0, cudaStream_t s) {
         cudaFuncSetAttribute(tc_fwd_kernel<false, false, true>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess ||
         cudaFuncSetAttribute(tc_fwd_kernel<false, true, true>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess)
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess ||
+        scan_attrs() != DELTANET_OK)
       return DELTANET_ERR_CUDA;
     attr.mark();
   }
@@ -1298,7 +1316,7 @@ int tc_fwd(const Args& a0, cudaStream_t s) {
     return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
   }
   tc_fwd_kernel<true><<<BH * nseg, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);   // pass 1
-  seg_scan_kernel<<<dim3(BH, DV / 16), 256, 0, s>>>(a);                     // pass 2
+  seg_scan_kernel<<<dim3(BH, DV / 16), 256, PSI_SMEM, s>>>(a);              // pass 2
   if (comp) tc_fwd_kernel<false, false, true><<<BH * nseg, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);
   else tc_fwd_kernel<false><<<BH * nseg, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);  // pass 3
   return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
@@ -1332,14 +1350,17 @@ int tc_fwd_transition(const Args& a0, float* psi, float* hloc, cudaStream_t s) {
     a.psi = psi;
     tc_fwd_kernel<true><<<BH, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);
   } else {
+    if (int rc = scan_attrs()) return rc;
     tc_fwd_kernel<true><<<BH * nseg, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);
-    cp_compose_kernel<<<dim3(BH, 2 * DK / 16), 256, 0, s>>>(nseg, 0, a.psi, a.hloc, psi, hloc);
+    cp_compose_kernel<<<dim3(BH, 2 * DK / 16), 256, PSI_SMEM, s>>>(nseg, 0, a.psi, a.hloc, psi,
+                                                                    hloc);
   }
   return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
 }
 
 int cp_compose_bwd(const Args& a, float* dhloc, cudaStream_t s) {
-  cp_compose_kernel<<<dim3(a.B * a.H, DV / 16), 256, 0, s>>>(a.nseg, 1, a.psi, a.hloc, nullptr,
+  if (int rc = scan_attrs()) return rc;
+  cp_compose_kernel<<<dim3(a.B * a.H, DV / 16), 256, PSI_SMEM, s>>>(a.nseg, 1, a.psi, a.hloc, nullptr,
                                                              dhloc);
   return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
 }
@@ -1352,7 +1373,8 @@ int cp_empty(int units, float* psi, float* loc, cudaStream_t s) {
 int cp_scan(int units, int nparts, int part, int reverse, const float* psi, const float* loc,
             const float* edge, float* out, cudaStream_t s) {
   ScanArgs sa{units, nparts, part, reverse, psi, loc, edge, out};
-  cp_scan_kernel<<<dim3(units, DV / 16), 256, 0, s>>>(sa);
+  if (int rc = scan_attrs()) return rc;
+  cp_scan_kernel<<<dim3(units, DV / 16), 256, PSI_SMEM, s>>>(sa);
   return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
 }
 

@@ -58,6 +58,35 @@ __device__ __forceinline__ uint64_t desc_mn(uint32_t base, int R, int k0, int n0
   return sdesc(base + (uint32_t)(n0 / 8) * R * 16 + (uint32_t)k0 * 16, 128, (uint32_t)R * 16);
 }
 
+// ---- "SW" tiles: the SWIZZLE_128B canonical layout, which a TMA box with
+// 128 B rows writes directly (8x fewer TMA requests than the IL box's 16 B
+// rows; tools/probes/tma_probe.cu).  A logical R x Cc bf16 matrix (Cc a
+// multiple of 64) is stored as Cc/64 column blocks of R rows x 128 B; inside
+// a block, row r is at r*128 and its 16 B chunk j at chunk (j ^ (r & 7)):
+//     byte offset of X[r][c] = (c/64)*R*128 + r*128 + (((c%64)/8) ^ (r%8))*16 + (c%8)*2
+// Tiles are 1024 B aligned (the swizzle XORs absolute address bits [4,7)
+// with [7,10)).  The same tile serves as
+//   - a K-major operand (M/N = row r, reduction over c): SBO = 1024 B (next 8
+//     rows), K-step of 16 columns = +32 B inside a block (next block at 64);
+//   - an MN-major operand (M/N = column c, reduction over r): LBO = R*128 B
+//     (next 64-column block), SBO = 1024 B (next 8 rows), K-step of 16 rows
+//     = +2048 B.
+__host__ __device__ __forceinline__ uint32_t sw_off(int r, int c, int R) {
+  return (uint32_t)((c >> 6) * R * 128 + r * 128 + ((((c & 63) >> 3) ^ (r & 7)) << 4) + (c & 7) * 2);
+}
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = sdesc(saddr, lbo, sbo);
+  d |= (uint64_t)2u << 61;  // layout type SWIZZLE_128B (sm_100 encoding)
+  return d;
+}
+__device__ __forceinline__ uint64_t desc_k_sw(uint32_t base, int R, int k0) {
+  return sdesc_sw128(base + (uint32_t)(k0 >> 6) * R * 128 + (uint32_t)(k0 & 63) * 2, 16, 1024);
+}
+__device__ __forceinline__ uint64_t desc_mn_sw(uint32_t base, int R, int k0, int n0 = 0) {
+  return sdesc_sw128(base + (uint32_t)(n0 >> 6) * R * 128 + (uint32_t)k0 * 128, (uint32_t)R * 128,
+                     1024);
+}
+
 // Instruction descriptor, kind::f16, A/B bf16, D fp32.
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool b_mn,
                                                   bool neg_a = false) {
@@ -196,6 +225,28 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void*
       "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(smem_src))
       : "memory");
 }
+// A chunk tile [rows tokens][128 columns] of a [BH][L][128] bf16 tensor as a
+// SW tile (two 64-column boxes of a make_sw_map map), and its store.
+__device__ __forceinline__ void tma_load_sw(void* smem_dst, const CUtensorMap* map, int t,
+                                            int unit, uint64_t* bar, int rows = 64) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(smem_dst) + h * rows * 128),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(64 * h), "r"(t), "r"(unit), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_sw(const CUtensorMap* map, const void* smem_src, int t,
+                                             int unit, int rows = 64) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+    asm volatile(
+        "cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+            reinterpret_cast<uint64_t>(map)),
+        "r"(64 * h), "r"(t), "r"(unit), "r"(smem_u32(smem_src) + h * rows * 128)
+        : "memory");
+}
 __device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes,
                                           uint64_t* bar) {
   asm volatile(
@@ -218,6 +269,21 @@ __device__ __forceinline__ void bulk_wait_read0() {
 __device__ __forceinline__ void bulk_wait0() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
+// L2 prefetch of a TMA tile (no shared memory, no completion): a later
+// tma_load_4d of the same box then hits L2 instead of waiting on HBM
+__device__ __forceinline__ void tma_prefetch_4d(const CUtensorMap* map, int c0, int c1, int c2,
+                                                int c3) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
+// L2 prefetch of a contiguous global range (bytes: a multiple of 16)
+__device__ __forceinline__ void bulk_prefetch(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(src)),
+               "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -239,6 +305,26 @@ __device__ __forceinline__ void il_store8(uint8_t* tile, int R, int r, int c0, c
   v.z = pack_bf16(x[4], x[5]);
   v.w = pack_bf16(x[6], x[7]);
   *reinterpret_cast<uint4*>(tile + il_off(r, c0, R)) = v;
+}
+
+// Store / load 8 consecutive columns [c0, c0+8) of row r (c0 % 8 == 0) of a SW tile.
+__device__ __forceinline__ void sw_store8(uint8_t* tile, int R, int r, int c0, const float* x) {
+  uint4 v;
+  v.x = pack_bf16(x[0], x[1]);
+  v.y = pack_bf16(x[2], x[3]);
+  v.z = pack_bf16(x[4], x[5]);
+  v.w = pack_bf16(x[6], x[7]);
+  *reinterpret_cast<uint4*>(tile + sw_off(r, c0, R)) = v;
+}
+__device__ __forceinline__ void sw_load8(const uint8_t* tile, int R, int r, int c0, float* x) {
+  const uint4 v = *reinterpret_cast<const uint4*>(tile + sw_off(r, c0, R));
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    float2 f = __bfloat1622float2(h[e]);
+    x[2 * e] = f.x;
+    x[2 * e + 1] = f.y;
+  }
 }
 
 // ------------------------------------------------------------------ CTA helpers
@@ -277,6 +363,9 @@ __device__ __forceinline__ void il_load8(const uint8_t* tile, int R, int r, int 
 // host: 4-D TMA view of a [B*H][L][D] bf16 tensor whose box {8, rows, D/8, 1}
 // lands in shared memory as the IL layout with R = rows (tc_fwd.cu).
 bool make_il_map(CUtensorMap* m, const void* base, int BH, int L, int D, int rows);
+// 3-D view {D, L, B*H} of a [B*H][L][D] bf16 tensor (D = 128); a box {64,
+// rows, 1} lands in smem as one 64-column block of a SW tile (SWIZZLE_128B)
+bool make_sw_map(CUtensorMap* m, const void* base, int BH, int L, int D, int rows);
 // cuTensorMapEncodeTiled through the runtime's driver entry point (tc_fwd.cu)
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn();
 

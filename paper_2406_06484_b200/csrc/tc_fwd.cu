@@ -44,8 +44,9 @@ constexpr int LS = 68;  // row stride (floats) of the fp32 substitution buffer
 
 // dynamic shared memory map (bytes)
 constexpr int TILE = C * DK * 2;                 // 16 KB chunk tile
-constexpr int OFF_Q = 0;                         // Q[2]  IL R=64 x 128
-constexpr int OFF_K = OFF_Q + 2 * TILE;          // K[2]  IL R=64 x 128
+constexpr int NQB = 2;                           // Q slots (chunk c in slot c % NQB)
+constexpr int OFF_Q = 0;                         // Q[NQB] IL R=64 x 128
+constexpr int OFF_K = OFF_Q + NQB * TILE;        // K[2]  IL R=64 x 128
 constexpr int OFF_V = OFF_K + 2 * TILE;          // V     IL R=64 x 128
 constexpr int OFF_T = OFF_V + TILE;              // T'    IL R=64 x 64
 constexpr int OFF_TU = OFF_T + C * C * 2;        // T''   IL R=64 x 64
@@ -131,7 +132,13 @@ __device__ long long* dn_tim = nullptr;
   do {                                                                     \
     if (dn_tim != nullptr && blockIdx.x == 0) dn_tim[(size_t)c * 32 + (slot)] = clock64(); \
   } while (0)
+// stamp filed under another chunk (load issue times, by target chunk)
+#define TSTAMPC(cc, slot)                                                  \
+  do {                                                                     \
+    if (dn_tim != nullptr && blockIdx.x == 0 && (cc) < NC) dn_tim[(size_t)(cc) * 32 + (slot)] = clock64(); \
+  } while (0)
 #else
+#define TSTAMPC(cc, slot) do { } while (0)
 #define TSTAMP1(slot) do { } while (0)
 #define TSTAMP(slot) do { } while (0)
 #define TSTAMP_PTR(slot) nullptr
@@ -158,8 +165,10 @@ __global__ void __launch_bounds__(NT, 1)
   // K of chunk c+3 loads when chunk c's chain ends and Q of chunk c+2 as
   // soon as O = Q H has read Q (q_done): the next Grams never wait on HBM
   constexpr int NKB = SEG1 ? 2 : 3;
-  __shared__ uint64_t q_full[2], k_full[3], v_full[2], bar_full[2], bar_empty[2], q_done;
-  __shared__ uint64_t g_done, g_free, t_ready, w_done, wu_done, w_free;  // prep side
+  __shared__ uint64_t q_full[NQB], k_full[3], v_full[2], bar_full[2], bar_empty[2], q_done;
+  // Gram: gk_done / gk_free for K K^T (lanes 16-31 of each quadrant), g_done /
+  // g_free for Q K^T (lanes 0-15); the two halves are issued and released apart
+  __shared__ uint64_t gk_done, gk_free, g_done, g_free, t_ready, w_done, wu_done, w_free;  // prep side
   __shared__ uint64_t up_done, z_free, z_ready, ho_done, h_ready, st_free;  // state side
   // q_read: the state warpgroup's norm pass has finished reading Q[b] (the
   // chain warp may then overwrite the slot with Q of chunk c+2; ADVICE r1:
@@ -171,6 +180,8 @@ __global__ void __launch_bounds__(NT, 1)
   __shared__ uint64_t u_read;
   __shared__ uint32_t tslot;
 
+  // SW tiles need 1024 B alignment (the swizzle acts on absolute address bits)
+  if ((smem_u32(smem) & 1023u) != 0) __trap();
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int w = tid & 127;            // thread index inside a 128-thread group
   const int wwarp = w >> 5;           // TMEM lane quadrant of this warp
@@ -188,14 +199,16 @@ __global__ void __launch_bounds__(NT, 1)
   if (warp == 0) tmem_alloc<512>(&tslot);
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&q_full[b], 1);
       mbar_init(&v_full[b], 1);
       mbar_init(&bar_full[b], 1);
       mbar_init(&bar_empty[b], 1);
     }
     for (int b = 0; b < 3; ++b) mbar_init(&k_full[b], 1);
+    for (int b = 0; b < NQB; ++b) mbar_init(&q_full[b], 1);
     mbar_init(&q_done, 1);
     mbar_init(&g_done, 1);
+    mbar_init(&gk_done, 1);
+    mbar_init(&gk_free, 1);
     mbar_init(&g_free, 1);
     mbar_init(&t_ready, 1);
     mbar_init(&w_done, 1);
@@ -248,7 +261,7 @@ __global__ void __launch_bounds__(NT, 1)
     // =====================================================================
     const __nv_bfloat16* beta = (const __nv_bfloat16*)a.beta + (size_t)unit * a.L + T0;
     // beta is prefetched into a register one chunk ahead (global latency)
-    float bnext = (w < C && w < L) ? __bfloat162float(beta[w]) : 0.f;
+    uint16_t bnext = (w < C && w < L) ? ldg_u16(beta + w) : (uint16_t)0;  // raw bf16 bits
     // gated: own log-gate and the warp-0 counterpart (lane), one chunk ahead
     const float* gsrc = GATED ? a.g + (size_t)unit * a.L + T0 : nullptr;
     float gnext = 0.f, g0next = 0.f;
@@ -260,8 +273,8 @@ __global__ void __launch_bounds__(NT, 1)
     for (int c = 0; c < NC; ++c) {
       const int b = c & 1, t0 = c * C;
       float* vb = vec(b);  // beta, s, -, G, gamma, D of this chunk
-      const float bval = bnext;
-      bnext = (w < C && t0 + C + w < L) ? __bfloat162float(beta[t0 + C + w]) : 0.f;
+      const float bval = bf16_bits(bnext);
+      bnext = (w < C && t0 + C + w < L) ? ldg_u16(beta + t0 + C + w) : (uint16_t)0;
       float gval = 0.f, g0val = 0.f;
       if (GATED) {
         gval = gnext;
@@ -285,30 +298,40 @@ __global__ void __launch_bounds__(NT, 1)
         vb[3 * C + w] = x + (w >= 32 ? t0s : 0.f);
       }
       TSTAMP(2);
-      mbar_wait(&g_done, c & 1);
+      // The Gram pair is split (K K^T first, Q K^T later): L and the
+      // substitution need only K K^T; A = tril(Q K^T) is formed by the state
+      // warpgroup just before the chain needs it.
+      mbar_wait(&gk_done, c & 1);
       fence_after_sync();
       TSTAMP(3);
-      uint4 arec[2];  // this thread's A record segments (stored after g_free)
-      int arow = 0, acol = 0;
-      {
-        // one TMEM load of this half's 32 columns: lanes < 16 hold G_qk rows,
-        // lanes >= 16 hold G_kk rows
-        float f[32];
-        {
-          uint32_t r[2][16];
-          tmem_ld16(taddr(tm, wwarp * 32, TM_G + 32 * half), r[0]);
-          tmem_ld16(taddr(tm, wwarp * 32, TM_G + 32 * half + 16), r[1]);
-          tmem_ld_wait();
+      const int i = wwarp * 16 + (lane & 15), h = 32 * half;
+      // lane pair (lo: G_qk row i, hi: G_kk row i) trades halves, so both
+      // lanes write 16 columns of L, with no divergence
+      const bool lo = lane < 16;
+      const int c0 = h + (lo ? 0 : 16);
+      // gated: Gamma(i, j) = e^{G_i - G_j} for the 16 columns [c0, c0+16) of this lane
+      // (masked by index, not clamped: with g > 0 allowed, G_i - G_j may be
+      // positive for j <= i; j > i is masked by the callers)
+      auto gamma16 = [&](float (&gam16)[16]) {
+        const float Gi = vb[3 * C + i];
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            f[e] = __uint_as_float(r[0][e]);
-            f[16 + e] = __uint_as_float(r[1][e]);
-          }
+        for (int q = 0; q < 4; ++q) {
+          const float4 g4 = *reinterpret_cast<const float4*>(vb + 3 * C + c0 + 4 * q);
+          const int j = c0 + 4 * q;
+          gam16[4 * q + 0] = __expf(j + 0 <= i ? Gi - g4.x : 0.f);
+          gam16[4 * q + 1] = __expf(j + 1 <= i ? Gi - g4.y : 0.f);
+          gam16[4 * q + 2] = __expf(j + 2 <= i ? Gi - g4.z : 0.f);
+          gam16[4 * q + 3] = __expf(j + 3 <= i ? Gi - g4.w : 0.f);
         }
-        const int i = wwarp * 16 + (lane & 15), h = 32 * half;
+      };
+      {
+        // S2a: this half's 32 columns; lanes >= 16 hold G_kk rows (lanes < 16:
+        // the G_qk half, possibly still in flight -- not used here)
+        float f[32];
+        ld32_cols(tm, wwarp, TM_G + 32 * half, f);
         // s_i = 1/max(||k_i||, eps) from the Gram diagonal (fp32 sum of exact
         // bf16 products; R9).  r (for q) is computed by the state warpgroup.
-        if (lane >= 16 && (i >> 5) == half) {
+        if (!lo && (i >> 5) == half) {
           // d = f[i - h] by a 5-level select tree (no dynamic register
           // indexing, no 32-step dependent chain)
           const int k = i - h;
@@ -338,48 +361,12 @@ __global__ void __launch_bounds__(NT, 1)
           vb[4 * C + w] = __expf(Gw);
           vb[5 * C + w] = __expf(vb[3 * C + C - 1] - Gw);
         }
-        // lane pair (lo: G_qk row i, hi: G_kk row i) trades halves, so both
-        // lanes write 16 columns of A and 16 of L with no divergence
-        const bool lo = lane < 16;
+        // lo lanes take G_kk columns [h, h+16) from their hi partner
         float x[16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) x[e] = __shfl_xor_sync(0xffffffffu, lo ? f[16 + e] : f[e], 16);
-        const int c0 = h + (lo ? 0 : 16);
-        // gated: Gamma(i, j) = e^{G_i - G_j} for the 16 columns of this lane
+        for (int e = 0; e < 16; ++e) x[e] = __shfl_xor_sync(0xffffffffu, f[e], 16);
         float gam16[16];
-        if (GATED) {
-          const float Gi = vb[3 * C + i];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float4 g4 = *reinterpret_cast<const float4*>(vb + 3 * C + c0 + 4 * q);
-            // masked by index, not clamped: with g > 0 allowed, G_i - G_j
-            // may be positive for j <= i; j > i is masked below
-            const int j = c0 + 4 * q;
-            gam16[4 * q + 0] = __expf(j + 0 <= i ? Gi - g4.x : 0.f);
-            gam16[4 * q + 1] = __expf(j + 1 <= i ? Gi - g4.y : 0.f);
-            gam16[4 * q + 2] = __expf(j + 2 <= i ? Gi - g4.z : 0.f);
-            gam16[4 * q + 3] = __expf(j + 3 <= i ? Gi - g4.w : 0.f);
-          }
-        }
-        {  // A = tril(Q K^T), raw (inclusive, R4); gated: Gamma . A
-#pragma unroll
-          for (int g = 0; g < 2; ++g) {
-            float a8[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              float qk = lo ? f[g * 8 + e] : x[g * 8 + e];
-              if (GATED) qk *= gam16[g * 8 + e];
-              a8[e] = (c0 + g * 8 + e <= i) ? qk : 0.f;
-            }
-            if (!SEG1) il_store8(sA(b), C, i, c0 + g * 8, a8);
-            arec[g].x = pack_bf16(a8[0], a8[1]);
-            arec[g].y = pack_bf16(a8[2], a8[3]);
-            arec[g].z = pack_bf16(a8[4], a8[5]);
-            arec[g].w = pack_bf16(a8[6], a8[7]);
-          }
-          arow = i;
-          acol = c0;
-        }
+        if (GATED) gamma16(gam16);
         {  // L = beta_i s_i s_j (k_i . k_j), j < i
           const float bi = vb[i] * vb[C + i];
           float4 s4[4];  // all loads first: no smem aliasing stalls
@@ -406,20 +393,14 @@ __global__ void __launch_bounds__(NT, 1)
       TSTAMP(23);
       fence_before_sync();
       grp_sync<NP>(BAR_P);
-      DBG(dbg_smem(dn_dbg + D_L, LX, C, C, LS, w); dbg_tmem(dn_dbg + D_GQK, tm, TM_G, C, 64, w);
-          dbg_smem(dn_dbg + D_S, vb + C, 1, C, C, w);
+      DBG(dbg_smem(dn_dbg + D_L, LX, C, C, LS, w); dbg_smem(dn_dbg + D_S, vb + C, 1, C, C, w);
           dbg_smem(dn_dbg + D_B, vb, 1, C, C, w); fence_before_sync(); grp_sync<NP>(BAR_P));
-      if (tid == 0) mbar_arrive(&g_free);  // the Gram accumulator may be overwritten
-      if (recs) {  // the backward's A record (IL image, 16 B per row segment), off the hand-over
-#pragma unroll
-        for (int g = 0; g < 2; ++g)
-          *reinterpret_cast<uint4*>(recs + (size_t)c * REC_BYTES + REC_A +
-                                    il_off(arow, acol + g * 8, C)) = arec[g];
-      }
+      if (tid == 0) mbar_arrive(&gk_free);  // G_kk may be overwritten (next chunk's K K^T)
       TSTAMP(4);
       ut_inverse_inplace<LS, NP>(LX, tid, BAR_P, TSTAMP_PTR(10));
       TSTAMP(5);
       DBG(dbg_smem(dn_dbg + D_X, LX, C, C, LS, w));
+      TSTAMP(9);
       {
         // T'[i][j] = X[i][j] beta_j s_j, T''[i][j] = X[i][j] beta_j  (j <= i).
         // (T' / T'' of chunk c-1 are free once its W/U products completed.)
@@ -548,7 +529,7 @@ __global__ void __launch_bounds__(NT, 1)
         const int row = w & 63, hh = w >> 6;
         float x[DK / 2];
 #pragma unroll
-        for (int g = 0; g < DK / 16; ++g) il_load8(sQ(b), C, row, DK / 2 * hh + g * 8, x + 8 * g);
+        for (int g = 0; g < DK / 16; ++g) sw_load8(sQ(c % NQB), C, row, DK / 2 * hh + g * 8, x + 8 * g);
         float acc0 = 0.f, acc1 = 0.f;
 #pragma unroll
         for (int e = 0; e < DK / 2; e += 2) {
@@ -561,7 +542,7 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
           for (int e = 0; e < DK / 2; ++e) x[e] *= gr;
 #pragma unroll
-          for (int g = 0; g < DK / 16; ++g) il_store8(sQ(b), C, row, DK / 2 * hh + g * 8, x + 8 * g);
+          for (int g = 0; g < DK / 16; ++g) sw_store8(sQ(c % NQB), C, row, DK / 2 * hh + g * 8, x + 8 * g);
         }
         wg_sync(BAR_S);
         if (w == 0) mbar_arrive(&q_read);  // every thread's reads of sQ(b) are done
@@ -587,6 +568,40 @@ __global__ void __launch_bounds__(NT, 1)
         mbar_arrive(&bar_full[b]);
       }
       if (!SEG1 && !GATED) norms();
+      if (!SEG1) {
+        // A = tril(Q K^T), raw (inclusive, R4; gated: Gamma . A) -> sA(b), the
+        // operand of this chunk's O += A Z, and the backward's A record.  Done
+        // here (the state warpgroup waits for the U' product anyway) rather than
+        // by the prep warps, whose chunk loop is the forward's critical path.
+        // G_qk row i sits in lanes < 16 of each quadrant; lo lanes write columns
+        // [0, 32) of it, their hi partners [32, 64).
+        mbar_wait(&g_done, c & 1);
+        fence_after_sync();
+        DBG(dbg_tmem(dn_dbg + D_GQK, tm, TM_G, C, 64, w));
+        float f[64];
+        ld64(tm, wwarp, TM_G, f);
+        const bool lo = lane < 16;
+        const int i = wwarp * 16 + (lane & 15), c0 = lo ? 0 : 32;
+        float x[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) x[e] = __shfl_xor_sync(0xffffffffu, f[32 + e], 16);
+        const float Gi = GATED ? vb[3 * C + i] : 0.f;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          float a8[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int j = c0 + g * 8 + e;
+            float qk = lo ? f[g * 8 + e] : x[g * 8 + e];
+            // gated: Gamma(i, j) = e^{G_i - G_j}, masked by index (not clamped:
+            // g > 0 is allowed)
+            if (GATED) qk *= __expf(j <= i ? Gi - vb[3 * C + j] : 0.f);
+            a8[e] = (j <= i) ? qk : 0.f;
+          }
+          il_store8(sA(b), C, i, c0 + g * 8, a8);
+          if (recs) il_store8(recs + (size_t)c * REC_BYTES + REC_A, C, i, c0 + g * 8, a8);
+        }
+      }
       mbar_wait(&up_done, c & 1);
       mbar_wait(&z_free, c & 1);
       fence_after_sync();
@@ -703,7 +718,10 @@ __global__ void __launch_bounds__(NT, 1)
       fence_proxy_async();
       fence_before_sync();
       wg_sync(BAR_S);
-      if (w == 0) mbar_arrive(&z_ready);
+      if (w == 0) {
+        mbar_arrive(&z_ready);
+        if (!SEG1) mbar_arrive(&g_free);  // G_qk read: the next chunk's Q K^T may land
+      }
       TSTAMP(18);
       mbar_wait(&ho_done, c & 1);
       mbar_wait(&st_free, c & 1);
@@ -738,7 +756,7 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
               for (int e = 0; e < 64; ++e) f[e] *= ri;
 #pragma unroll
-              for (int g = 0; g < 8; ++g) il_store8(sO, C, i, 64 * half + g * 8, f + g * 8);
+              for (int g = 0; g < 8; ++g) sw_store8(sO, C, i, 64 * half + g * 8, f + g * 8);
             }
           }
         }
@@ -823,48 +841,62 @@ __global__ void __launch_bounds__(NT, 1)
     // Warp 12: prep MMA issue + TMA loads of V (and of Q/K for chunks 0, 1)
     // =====================================================================
     if (lane == 0) {
-      for (int c = 0; c < 2 && c < NC; ++c) {
+      for (int c = 0; c < NQB && c < NC && !SEG1; ++c) {  // (SEG1 needs no Q)
         mbar_expect_tx(&q_full[c], TILE);
-        tma_load_4d(sQ(c), &mQ, 0, T0 + c * C, 0, unit, &q_full[c]);
+        tma_load_sw(sQ(c), &mQ, T0 + c * C, unit, &q_full[c]);
       }
       for (int c = 0; c < NKB && c < NC; ++c) {
         mbar_expect_tx(&k_full[c], TILE);
-        tma_load_4d(sK(c), &mK, 0, T0 + c * C, 0, unit, &k_full[c]);
+        tma_load_sw(sK(c), &mK, T0 + c * C, unit, &k_full[c]);
       }
       mbar_expect_tx(&v_full[0], TILE);
-      tma_load_4d(sV, &mV, 0, T0, 0, unit, &v_full[0]);
+      tma_load_sw(sV, &mV, T0, unit, &v_full[0]);
       const uint32_t idg = idesc_bf16(64, 64, false, false);
       const uint32_t idw = idesc_bf16(128, 64, true, false);
       const uint32_t at = smem_u32(sT), atu = smem_u32(sTu), av = smem_u32(sV);
-      auto gram = [&](int c) {  // G_qk -> lanes 0-15, G_kk -> lanes 16-31 of each quadrant
-        const int b = c & 1;
-        const uint32_t aq = smem_u32(sQ(b)), ak = smem_u32(sK(c % NKB));
-        mbar_wait(&q_full[b], (c >> 1) & 1);
+      auto gram_k = [&](int c) {  // G_kk -> lanes 16-31 of each quadrant
+        const uint32_t ak = smem_u32(sK(c % NKB));
         mbar_wait(&k_full[c % NKB], (c / NKB) & 1);
         fence_after_sync();
 #pragma unroll
-        for (int k0 = 0; k0 < DK; k0 += 16) {
-          mma_bf16(tm + TM_G, desc_k(aq, C, k0), desc_k(ak, C, k0), idg, k0 > 0);
-          mma_bf16(tm + TM_G + LO16, desc_k(ak, C, k0), desc_k(ak, C, k0), idg, k0 > 0);
-        }
+        for (int k0 = 0; k0 < DK; k0 += 16)
+          mma_bf16(tm + TM_G + LO16, desc_k_sw(ak, C, k0), desc_k_sw(ak, C, k0), idg, k0 > 0);
+        mma_commit(&gk_done);
+      };
+      auto gram_q = [&](int c) {  // G_qk -> lanes 0-15 of each quadrant
+        const uint32_t aq = smem_u32(sQ(c % NQB)), ak = smem_u32(sK(c % NKB));
+        mbar_wait(&q_full[c % NQB], (c / NQB) & 1);
+        mbar_wait(&k_full[c % NKB], (c / NKB) & 1);
+        fence_after_sync();
+        TSTAMP1(28);
+#pragma unroll
+        for (int k0 = 0; k0 < DK; k0 += 16)
+          mma_bf16(tm + TM_G, desc_k_sw(aq, C, k0), desc_k_sw(ak, C, k0), idg, k0 > 0);
         mma_commit(&g_done);
       };
-      if (NC > 0) gram(0);
+      if (NC > 0) {
+        gram_k(0);
+        if (!SEG1) gram_q(0);
+      }
 #pragma unroll 1
       for (int c = 0; c < NC; ++c) {
         const int b = c & 1;
         const uint32_t ak = smem_u32(sK(c % NKB));
-        // the next chunk's Gram as soon as the prep has read this chunk's and
-        // q/k of chunk c+1 have landed (it then runs under this chunk's
-        // substitution) -- but never ahead of this chunk's W/U products: if
-        // T is ready first, the Gram waits until after them
-        bool gram_pending = c + 1 < NC;
-        if (gram_pending) mbar_wait(&g_free, c & 1);
+        // the next chunk's Gram halves as soon as the prep has read this
+        // chunk's (gk_free after L; g_free once the state warpgroup has formed A)
+        // and their tiles have
+        // landed (K K^T then runs under this chunk's substitution) -- but
+        // never ahead of this chunk's W/U products: if T is ready first, the
+        // remaining halves wait until after them
+        bool pk = c + 1 < NC, pq = !SEG1 && c + 1 < NC;
+        bool kfree = false;
         while (true) {
-          if (gram_pending && mbar_test(&q_full[(c + 1) & 1], ((c + 1) >> 1) & 1) &&
-              mbar_test(&k_full[(c + 1) % NKB], ((c + 1) / NKB) & 1)) {
-            gram(c + 1);
-            gram_pending = false;
+          if (pk) {
+            if (!kfree) kfree = mbar_test(&gk_free, c & 1);
+            if (kfree && mbar_test(&k_full[(c + 1) % NKB], ((c + 1) / NKB) & 1)) {
+              gram_k(c + 1);
+              pk = false;
+            }
           }
           if (mbar_test(&t_ready, c & 1)) break;
         }
@@ -878,18 +910,25 @@ __global__ void __launch_bounds__(NT, 1)
         fence_after_sync();
 #pragma unroll
         for (int k0 = 0; k0 < C; k0 += 16)
-          mma_bf16(tm + TM_W, desc_mn(ak, C, k0), desc_k(at, C, k0), idw, k0 > 0);
+          mma_bf16(tm + TM_W, desc_mn_sw(ak, C, k0), desc_k(at, C, k0), idw, k0 > 0);
         mma_commit(&w_done);
 #pragma unroll
         for (int k0 = 0; k0 < C; k0 += 16)
-          mma_bf16(tm + tm_u(b), desc_mn(av, C, k0), desc_k(atu, C, k0), idw, k0 > 0);
+          mma_bf16(tm + tm_u(b), desc_mn_sw(av, C, k0), desc_k(atu, C, k0), idw, k0 > 0);
         mma_commit(&wu_done);
-        if (gram_pending) gram(c + 1);
+        if (pk) {
+          mbar_wait(&gk_free, c & 1);
+          gram_k(c + 1);
+        }
         mbar_wait(&wu_done, c & 1);
         if (c + 1 < NC) {  // V (and T, T'') free again: prefetch the next chunk's V
           const int nb = (c + 1) & 1;
           mbar_expect_tx(&v_full[nb], TILE);
-          tma_load_4d(sV, &mV, 0, T0 + (c + 1) * C, 0, unit, &v_full[nb]);
+          tma_load_sw(sV, &mV, T0 + (c + 1) * C, unit, &v_full[nb]);
+        }
+        if (pq) {  // the state warpgroup has read this chunk's G_qk (g_free, with z_ready)
+          mbar_wait(&g_free, c & 1);
+          gram_q(c + 1);
         }
       }
     }
@@ -899,10 +938,10 @@ __global__ void __launch_bounds__(NT, 1)
     // Warp 13: state-chain MMA issue, state save, O store, next Q/K loads
     // =====================================================================
     if (lane == 0) {
+      void* const o_out = SEG1 ? nullptr : a.o;
       uint8_t* states = (!SEG1 && (a.flags & DELTANET_SAVE_STATES))
                             ? (uint8_t*)a.states + ((size_t)unit * a.NC + cbase) * (DK * DV * 2)
                             : nullptr;
-      void* const o_out = SEG1 ? nullptr : a.o;
       const uint32_t aPsi = smem_u32(sPsi);
       const uint32_t idt = idesc_bf16(128, 64, false, true);    // T1 = Psi W^T
       const uint32_t idp = idesc_bf16(128, 128, false, true);   // Psi += (-T1 s) K
@@ -913,12 +952,12 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll 1
       for (int c = 0; c < NC; ++c) {
         const int b = c & 1;
-        const uint32_t aw = smem_u32(sW(b)), aq = smem_u32(sQ(b)), aa = smem_u32(sA(b)),
+        const uint32_t aw = smem_u32(sW(b)), aq = smem_u32(sQ(c % NQB)), aa = smem_u32(sA(b)),
                        ak = smem_u32(sK(c % NKB));
         mbar_wait(&bar_full[b], (c >> 1) & 1);
         mbar_wait(&h_ready, c & 1);  // sH = bf16 image of H_c; sO = O of chunk c-1
         if (c >= 1 && o_out) {
-          tma_store_4d(&mO, sO, 0, T0 + (c - 1) * C, 0, unit);
+          tma_store_sw(&mO, sO, T0 + (c - 1) * C, unit);
           bulk_commit();
         }
         if (states) {  // save H_c (bf16 smem image) for the backward
@@ -939,7 +978,7 @@ __global__ void __launch_bounds__(NT, 1)
         if (!SEG1) {
 #pragma unroll
           for (int k0 = 0; k0 < DK; k0 += 16)
-            mma_bf16(tm + TM_O, desc_k(aq, C, k0), desc_k(aH, DV, k0), ido, k0 > 0);
+            mma_bf16(tm + TM_O, desc_k_sw(aq, C, k0), desc_k(aH, DV, k0), ido, k0 > 0);
         }
         mma_commit(&q_done);  // Q[b] read by the tensor core (norm reads: q_read)
         // the O store of chunk c-1 must finish reading sO (= sZ) before Z is written
@@ -947,10 +986,12 @@ __global__ void __launch_bounds__(NT, 1)
         if (!states) bulk_wait_read0();
         mbar_arrive(&z_free);
         mbar_wait(&q_done, c & 1);
-        if (c + 2 < NC) {  // Q of chunk c+2 into the slot O = Q H has released
+        if (!SEG1 && c + NQB < NC) {  // Q of chunk c+NQB into the slot O = Q H has released
           if (!SEG1) mbar_wait(&q_read, c & 1);  // ... and the norm pass (SEG1 has none)
-          mbar_expect_tx(&q_full[b], TILE);
-          tma_load_4d(sQ(b), &mQ, 0, T0 + (c + 2) * C, 0, unit, &q_full[b]);
+          const int qs = c % NQB;
+          mbar_expect_tx(&q_full[qs], TILE);
+          tma_load_sw(sQ(qs), &mQ, T0 + (c + NQB) * C, unit, &q_full[qs]);
+          TSTAMPC(c + NQB, 29);
         }
         mbar_wait(&z_ready, c & 1);
         fence_after_sync();
@@ -967,16 +1008,16 @@ __global__ void __launch_bounds__(NT, 1)
         if (GATED) {
 #pragma unroll
           for (int k0 = 0; k0 < C; k0 += 16)
-            mma_bf16_ts(tm + TM_H, tm + tm_u(b) + k0 / 2, desc_mn(ak, C, k0), idh, 1);
+            mma_bf16_ts(tm + TM_H, tm + tm_u(b) + k0 / 2, desc_mn_sw(ak, C, k0), idh, 1);
         } else {
 #pragma unroll
           for (int k0 = 0; k0 < C; k0 += 16)
-            mma_bf16(tm + TM_H, desc_k(aZ, DV, k0), desc_mn(ak, C, k0), idh, 1);
+            mma_bf16(tm + TM_H, desc_k(aZ, DV, k0), desc_mn_sw(ak, C, k0), idh, 1);
         }
         if (SEG1) {  // Psi += (-T1 diag(s)) K, A from TMEM (bf16 pairs in TM_W)
 #pragma unroll
           for (int k0 = 0; k0 < C; k0 += 16)
-            mma_bf16_ts(tm + TM_O, tm + TM_W + k0 / 2, desc_mn(ak, C, k0), idp, 1);
+            mma_bf16_ts(tm + TM_O, tm + TM_W + k0 / 2, desc_mn_sw(ak, C, k0), idp, 1);
         } else {
 #pragma unroll
           for (int k0 = 0; k0 < C; k0 += 16)
@@ -987,7 +1028,8 @@ __global__ void __launch_bounds__(NT, 1)
         if (c + NKB < NC) {  // K of chunk c+NKB into this chunk's K slot
           const int ks = c % NKB;
           mbar_expect_tx(&k_full[ks], TILE);
-          tma_load_4d(sK(ks), &mK, 0, T0 + (c + NKB) * C, 0, unit, &k_full[ks]);
+          tma_load_sw(sK(ks), &mK, T0 + (c + NKB) * C, unit, &k_full[ks]);
+          TSTAMPC(c + NKB, 30);
         }
         bulk_wait_read0();  // state save done reading sH
         mbar_arrive(&st_free);
@@ -1001,7 +1043,7 @@ __global__ void __launch_bounds__(NT, 1)
       // O of the last chunk
       mbar_wait(&h_ready, NC & 1);
       if (o_out && NC > 0) {
-        tma_store_4d(&mO, sO, 0, T0 + (NC - 1) * C, 0, unit);
+        tma_store_sw(&mO, sO, T0 + (NC - 1) * C, unit);
         bulk_commit();
       }
       bulk_wait0();
@@ -1186,6 +1228,19 @@ bool make_il_map(CUtensorMap* m, const void* base, int BH, int L, int D, int row
   return r == CUDA_SUCCESS;
 }
 
+bool make_sw_map(CUtensorMap* m, const void* base, int BH, int L, int D, int rows) {
+  auto enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)L, (cuuint64_t)BH};
+  cuuint64_t strides[2] = {(cuuint64_t)D * 2, (cuuint64_t)L * D * 2};
+  cuuint32_t box[3] = {64, (cuuint32_t)rows, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 bool tc_supported(const deltanet_desc* d) {
   return d->dtype == DELTANET_BF16 && d->chunk == C && d->Dk == DK && d->Dv == DV && d->L > 0;
 }
@@ -1299,9 +1354,9 @@ int tc_fwd(const Args& a0, cudaStream_t s) {
   Args a = a0;
   const int BH = a.B * a.H;
   CUtensorMap mQ, mK, mV, mO;
-  if (!make_il_map(&mQ, a.q, BH, a.L, DK, C) || !make_il_map(&mK, a.k, BH, a.L, DK, C) ||
-      !make_il_map(&mV, a.v, BH, a.L, DV, C) ||
-      !make_il_map(&mO, a.o ? a.o : a.v, BH, a.L, DV, C))  // o == null: states only
+  if (!make_sw_map(&mQ, a.q, BH, a.L, DK, C) || !make_sw_map(&mK, a.k, BH, a.L, DK, C) ||
+      !make_sw_map(&mV, a.v, BH, a.L, DV, C) ||
+      !make_sw_map(&mO, a.o ? a.o : a.v, BH, a.L, DV, C))  // o == null: states only
     return DELTANET_ERR_CUDA;
   const int nseg = tc_seg_setup(a);
   const bool comp = (a.flags & DELTANET_COMPENSATED) != 0;  // DESIGN.md R19
@@ -1330,8 +1385,8 @@ int tc_fwd_transition(const Args& a0, float* psi, float* hloc, cudaStream_t s) {
   Args a = a0;
   const int BH = a.B * a.H;
   CUtensorMap mQ, mK, mV, mO;
-  if (!make_il_map(&mQ, a.q, BH, a.L, DK, C) || !make_il_map(&mK, a.k, BH, a.L, DK, C) ||
-      !make_il_map(&mV, a.v, BH, a.L, DV, C) || !make_il_map(&mO, a.v, BH, a.L, DV, C))
+  if (!make_sw_map(&mQ, a.q, BH, a.L, DK, C) || !make_sw_map(&mK, a.k, BH, a.L, DK, C) ||
+      !make_sw_map(&mV, a.v, BH, a.L, DV, C) || !make_sw_map(&mO, a.v, BH, a.L, DV, C))
     return DELTANET_ERR_CUDA;
   static PerDevice attr;
   if (!attr.done()) {

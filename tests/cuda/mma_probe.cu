@@ -385,3 +385,73 @@ extern "C" long long probe_mma_batch(int N, int lane16, int n) {
   cudaFree(d);
   return h;
 }
+
+// SWIZZLE_128B ("SW") operand tiles (tc_common.cuh sw_off / desc_k_sw /
+// desc_mn_sw): sw bit 0 = A in the SW layout, bit 1 = B; M=128 or 64.
+__global__ void probe_sw_kernel(const __nv_bfloat16* A, const __nv_bfloat16* B, float* D, int M,
+                                int N, int K, int a_mn, int b_mn, int sw) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + ((M * K * 2 + 1023) / 1024) * 1024;
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const bool swa = sw & 1, swb = sw & 2;
+  for (int e = tid; e < M * K; e += blockDim.x) {
+    int m = e / K, k = e % K;
+    uint32_t off = a_mn ? (swa ? sw_off(k, m, K) : il_off(k, m, K))
+                        : (swa ? sw_off(m, k, M) : il_off(m, k, M));
+    *reinterpret_cast<__nv_bfloat16*>(sA + off) = A[e];
+  }
+  for (int e = tid; e < N * K; e += blockDim.x) {
+    int n = e / K, k = e % K;
+    uint32_t off = b_mn ? (swb ? sw_off(k, n, K) : il_off(k, n, K))
+                        : (swb ? sw_off(n, k, N) : il_off(n, k, N));
+    *reinterpret_cast<__nv_bfloat16*>(sB + off) = B[e];
+  }
+  fence_proxy_async();
+  if (warp == 0) tmem_alloc<512>(&tslot);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    mbar_fence_init();
+  }
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tm = tslot;
+  if (tid == 0) {
+    const uint32_t id = idesc_bf16(M, N, a_mn, b_mn, false);
+    const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+    for (int k0 = 0; k0 < K; k0 += 16) {
+      uint64_t ad = a_mn ? (swa ? desc_mn_sw(a0, K, k0) : desc_mn(a0, K, k0))
+                         : (swa ? desc_k_sw(a0, M, k0) : desc_k(a0, M, k0));
+      uint64_t bd = b_mn ? (swb ? desc_mn_sw(b0, K, k0) : desc_mn(b0, K, k0))
+                         : (swb ? desc_k_sw(b0, N, k0) : desc_k(b0, N, k0));
+      mma_bf16(tm, ad, bd, id, k0 > 0 ? 1u : 0u);
+    }
+    mma_commit(&bar);
+  }
+  mbar_wait(&bar, 0);
+  fence_after_sync();
+  for (int c0 = 0; c0 < N; c0 += 16) {
+    uint32_t r[16];
+    tmem_ld16(taddr(tm, warp * 32, c0), r);
+    tmem_ld_wait();
+    int m = (M == 128) ? tid : (lane < 16 ? warp * 16 + lane : -1);
+    if (m >= 0)
+      for (int j = 0; j < 16; ++j) D[m * N + c0 + j] = __uint_as_float(r[j]);
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tm);
+}
+
+extern "C" int probe_mma_sw(const void* A, const void* B, float* D, int M, int N, int K, int a_mn,
+                            int b_mn, int sw) {
+  size_t smem = ((size_t)(M * K * 2 + 1023) / 1024) * 1024 + (size_t)N * K * 2;
+  cudaFuncSetAttribute(probe_sw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  probe_sw_kernel<<<1, 128, smem>>>((const __nv_bfloat16*)A, (const __nv_bfloat16*)B, D, M, N, K,
+                                    a_mn, b_mn, sw);
+  cudaError_t e = cudaDeviceSynchronize();
+  return (int)e;
+}

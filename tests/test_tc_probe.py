@@ -33,6 +33,8 @@ def probe():
     L.probe_mma_issue.restype = ctypes.c_longlong
     L.probe_mma_batch.argtypes = [ctypes.c_int] * 3
     L.probe_mma_batch.restype = ctypes.c_longlong
+    L.probe_mma_sw.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int] * 6
+    L.probe_mma_sw.restype = ctypes.c_int
     return L
 
 
@@ -155,3 +157,22 @@ def test_mma_m64_batches(probe):
             cyc = probe.probe_mma_batch(N, l16, n)
             rows.append(f"M=64 N={N} lane16_alternate={l16}: {cyc / n:6.1f} cyc/mma")
     print("\n" + "\n".join(rows))
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 64, 64), (128, 128, 64), (128, 64, 128),
+                                   (64, 64, 128), (64, 128, 128), (64, 128, 64)])
+@pytest.mark.parametrize("a_mn", [0, 1])
+@pytest.mark.parametrize("b_mn", [0, 1])
+@pytest.mark.parametrize("sw", [1, 2, 3])
+def test_mma_sw128_layouts(probe, M, N, K, a_mn, b_mn, sw):
+    """SWIZZLE_128B tiles (tc_common.cuh sw_off, desc_k_sw, desc_mn_sw) as
+    K-major and MN-major operands, alone or mixed with IL tiles."""
+    g = torch.Generator().manual_seed(M * 1000 + N * 10 + K + a_mn * 7 + b_mn * 3 + sw)
+    A = torch.randn(M, K, generator=g).bfloat16()
+    B = torch.randn(N, K, generator=g).bfloat16()
+    ref = A.float() @ B.float().T
+    Ad, Bd = A.cuda(), B.cuda()
+    D = torch.zeros(M, N, device="cuda")
+    assert probe.probe_mma_sw(Ad.data_ptr(), Bd.data_ptr(), D.data_ptr(), M, N, K, a_mn, b_mn, sw) == 0
+    err = (D.cpu() - ref).abs().max().item()
+    assert err <= 1e-3 * ref.abs().max().item(), err

@@ -74,7 +74,8 @@ def test_fwd_timeline(timlib):
         per = np.diff(t[2:-2, grp[0]]).mean()
         rows.append(f"{'-- per chunk (' + ('P' if grp[0] == 0 else 'S') + ')':28s} {per:9.0f} cycles")
     for s_, nm in ((24, "M t_ready rcv"), (25, "M w_free rcv"), (26, "M bar_empty rcv"),
-                   (27, "M v_full rcv")):
+                   (27, "M v_full rcv"), (28, "M Gram issued (this chunk)"),
+                   (29, "W13 Q load issued (this chunk)"), (30, "W13 K load issued (this chunk)")):
         dt = t[2:-2, s_] - t[2:-2, 0]
         rows.append(f"{nm:28s} {dt.mean():9.0f} cycles after prep chunk start")
     print("\n" + "\n".join(rows))

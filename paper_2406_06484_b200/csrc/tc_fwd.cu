@@ -407,6 +407,7 @@ __global__ void __launch_bounds__(NT, 1)
         // Lanes map to consecutive rows (conflict-free IL stores); each thread
         // handles one 16-column quarter of its row.
         if (c >= 1) mbar_wait(&wu_done, (c - 1) & 1);
+        TSTAMP(15);
         const int i = tid & 63, j0 = (tid >> 6) * 16;
         uint4 xrec[2];  // the X record, stored once T is handed over
         float4 x4[4];
@@ -444,6 +445,7 @@ __global__ void __launch_bounds__(NT, 1)
         }
         fence_proxy_async();
         grp_sync<NP>(BAR_P);
+        TSTAMP(31);
         if (tid == 0) mbar_arrive(&t_ready);
         if (recs) {  // the X record from registers (IL image, 16 B per row), off the hand-over
 #pragma unroll

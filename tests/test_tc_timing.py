@@ -62,12 +62,14 @@ def test_fwd_timeline(timlib):
     t = buf.cpu().numpy().reshape(NC, 32).astype(np.int64)
     names = {0: "P start", 1: "P tma+empty wait", 2: "P norms", 3: "P gram wait",
              21: " S2 tmem ld + s", 22: " S2 sync", 23: " S2 A/L writes",
-             4: "P S2 sync + g_free", 10: " sub L1", 11: " sub L2a", 12: " sub L2b", 13: " sub L3a",
-             14: " sub L3b", 5: "P substitution", 6: "P T writes", 7: "P WU wait",
+             4: "P S2 sync + gk_free", 10: " sub L1", 15: " T: wu_done(c-1) wait",
+             31: " T: writes + fence + sync", 11: " sub L2a", 12: " sub L2b", 13: " sub L3a",
+             14: " sub L3b", 5: "P substitution", 6: " T: X record stores", 7: "P WU wait",
              8: "P W conv + full", 16: "S start", 17: "S full/up'/zfree wait", 18: "S Z conv",
              19: "S ho/st wait", 20: "S H/O conv"}
     rows = []
-    for grp in ([0, 1, 2, 3, 21, 22, 23, 4, 10, 11, 12, 13, 14, 5, 6, 7, 8], [16, 17, 18, 19, 20]):
+    for grp in ([0, 1, 2, 3, 21, 22, 23, 4, 10, 11, 12, 13, 14, 5, 15, 31, 6, 7, 8],
+                [16, 17, 18, 19, 20]):
         for a_, b_ in zip(grp[:-1], grp[1:]):
             dt = (t[2:-2, b_] - t[2:-2, a_])
             rows.append(f"{names[b_]:28s} {dt.mean():9.0f} cycles")

@@ -16,7 +16,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def child(lib, B, H, L):
+def child(lib, B, H, L, gated=False):
     sys.path.insert(0, ROOT)
     import torch
     import paper_2406_06484_b200 as dn
@@ -27,15 +27,22 @@ def child(lib, B, H, L):
     q, k = f.silu(mk()).bfloat16(), f.silu(mk()).bfloat16()
     v, dO = mk().bfloat16(), mk().bfloat16()
     b = torch.sigmoid(torch.randn((B, H, L), device="cuda", generator=g)).bfloat16()
-    o, hT, ws = dn.deltanet_fwd(q, k, v, b)
-    dn.deltanet_bwd(q, k, v, b, dO, workspace=ws)
+    gt = -0.05 * f.softplus(torch.randn((B, H, L), device="cuda", generator=g))
+    if gated:
+        fwd = lambda ws=None: dn.deltanet_gated_fwd(q, k, v, b, gt, workspace=ws)
+        bwd = lambda ws: dn.deltanet_gated_bwd(q, k, v, b, gt, dO, workspace=ws)
+    else:
+        fwd = lambda ws=None: dn.deltanet_fwd(q, k, v, b, workspace=ws)
+        bwd = lambda ws: dn.deltanet_bwd(q, k, v, b, dO, workspace=ws)
+    o, hT, ws = fwd()
+    bwd(ws)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
     tf, tb = [], []
     for i in range(35):
         ev[0].record()
-        o, hT, ws = dn.deltanet_fwd(q, k, v, b, workspace=ws)
+        o, hT, ws = fwd(ws)
         ev[1].record()
-        dn.deltanet_bwd(q, k, v, b, dO, workspace=ws)
+        bwd(ws)
         ev[2].record()
         torch.cuda.synchronize()
         if i >= 5:
@@ -49,20 +56,22 @@ def main():
     args = sys.argv[1:]
     if args and args[0] == "--child":
         B, H, L = (int(x) for x in args[2].split(","))
-        return child(args[1], B, H, L)
-    rounds, shape, libs = 3, "8,16,4096", []
+        return child(args[1], B, H, L, len(args) > 3 and args[3] == "gated")
+    rounds, shape, libs, mode = 3, "8,16,4096", [], []
     it = iter(args)
     for a in it:
         if a == "--rounds":
             rounds = int(next(it))
         elif a == "--shape":
             shape = next(it)
+        elif a == "--gated":
+            mode = ["gated"]
         else:
             libs.append(os.path.abspath(a))
     res = {l: [] for l in libs}
     for _ in range(rounds):
         for l in libs:
-            out = subprocess.run([sys.executable, __file__, "--child", l, shape],
+            out = subprocess.run([sys.executable, __file__, "--child", l, shape] + mode,
                                  capture_output=True, text=True)
             line = [x for x in out.stdout.splitlines() if x.startswith("{")]
             if not line:

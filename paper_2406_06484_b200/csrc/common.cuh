@@ -51,6 +51,9 @@ struct Args {
   float* hseg;  // [B*H][nseg][Dk][Dv] state at each segment start (pass 3 input)
   float* hloc;  // [B*H][nseg][Dk][Dv] segment-local end state from zero (pass 1)
   float* psi;   // [B*H][nseg][Dk][Dk] segment transition (pass 1)
+  // [B*H][NC] per-chunk prep records [T' | T'' | s | 1/s] written by pass 1
+  // and read by pass 3 instead of redoing the substitution (tc_fwd.cu PREC_*)
+  uint8_t* prec;
   // Gated DeltaNet (R23): log-decay g [B*H][L]
   // fp32 (null = ungated) and its gradient
   const float* g;

@@ -63,6 +63,12 @@ static_assert(SMEM_BYTES <= 232448 - 1024, "shared memory budget");
 static_assert(REC_Z == C * C * 2 && REC_N == C * C * 2 + DV * C * 2 &&
                   REC_A == REC_N + 2 * C * 4 && REC_BYTES == REC_A + C * C * 2, "record");
 
+// Prep record of the segmented forward: pass 1 stores, per
+// chunk, the bf16 IL images of T' and T'' and the fp32 row scales s, 1/s;
+// pass 3 loads them with one bulk copy each instead of redoing the Gram
+// conversion, the substitution and the T writes (bit-identical operands).
+constexpr int PREC_T = 0, PREC_S = 2 * C * C * 2, PREC_BYTES = PREC_S + 2 * C * 4;
+
 // TMEM column map (512 columns)
 constexpr uint32_t LO16 = 16u << 16;
 constexpr uint32_t TM_H = 0;                     // H^T  M=128, 128 cols (S)
@@ -153,7 +159,9 @@ __device__ long long* dn_tim = nullptr;
 // (W = X diag(beta gamma) K_hat), Q rows are scaled by gamma in place before
 // O = Q H, H is rescaled by gamma_63 in TMEM, and the state update takes
 // Z_h = diag(s D) U' from TMEM (bf16 pairs) while O takes Z = diag(s) U'.
-template <bool SEG1, bool GATED = false, bool COMP = false>
+// PRE = pass 3 of the segmented forward with pass 1's prep records (T', T'',
+// s, 1/s per chunk): the prep warps only load them.
+template <bool SEG1, bool GATED = false, bool COMP = false, bool PRE = false>
 __global__ void __launch_bounds__(NT, 1)
     tc_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                   const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mO,
@@ -169,6 +177,7 @@ __global__ void __launch_bounds__(NT, 1)
   // Gram: gk_done / gk_free for K K^T (lanes 16-31 of each quadrant), g_done /
   // g_free for Q K^T (lanes 0-15); the two halves are issued and released apart
   __shared__ uint64_t gk_done, gk_free, g_done, g_free, t_ready, w_done, wu_done, w_free;  // prep side
+  __shared__ uint64_t pr_full;  // pass 3: the chunk's prep record has landed
   __shared__ uint64_t up_done, z_free, z_ready, ho_done, h_ready, st_free;  // state side
   // q_read: the state warpgroup's norm pass has finished reading Q[b] (the
   // chain warp may then overwrite the slot with Q of chunk c+2; ADVICE r1:
@@ -209,6 +218,7 @@ __global__ void __launch_bounds__(NT, 1)
     mbar_init(&g_done, 1);
     mbar_init(&gk_done, 1);
     mbar_init(&gk_free, 1);
+    mbar_init(&pr_full, 1);
     mbar_init(&g_free, 1);
     mbar_init(&t_ready, 1);
     mbar_init(&w_done, 1);
@@ -242,10 +252,15 @@ __global__ void __launch_bounds__(NT, 1)
   uint8_t* sTu = smem + OFF_TU;
   uint8_t* sH = smem + OFF_H;
   uint8_t* sZ = smem + OFF_Z;
-  uint8_t* recs = (!SEG1 && (a.flags & DELTANET_SAVE_STATES))
+  // pass 1 with prep records also writes the X and ||k|| records (pass 3 then
+  // takes T', T'' and s from its prep record and writes neither)
+  uint8_t* recs = ((!SEG1 || a.prec) && (a.flags & DELTANET_SAVE_STATES))
                       ? reinterpret_cast<uint8_t*>(a.scratch) +
                             ((size_t)unit * a.NC + cbase) * REC_BYTES
                       : nullptr;
+  uint8_t* const prec =
+      a.prec ? a.prec + ((size_t)unit * a.NC + cbase) * PREC_BYTES : nullptr;
+  constexpr bool pre = PRE;  // pass 3 from prep records
   // SEG1: the Psi image [dk][dk] bf16 (IL R=128) over A[0], A[1], W[0]; W in W[1]
   uint8_t* sPsi = smem + OFF_A;
   static_assert(OFF_W == OFF_A + 2 * C * C * 2 && 2 * C * C * 2 + DK * C * 2 == DK * DK * 2,
@@ -286,6 +301,20 @@ __global__ void __launch_bounds__(NT, 1)
       if (c >= 2) mbar_wait(&bar_empty[b], ((c >> 1) - 1) & 1);  // chain c-2 released b
       TSTAMP(1);
       if (half == 0 && w < C) vb[w] = bval;
+      if (pre) {
+        // pass 3: T', T'' and s, 1/s from pass 1's prep record (T' / T'' of
+        // chunk c-1 are free once its W/U products completed)
+        if (tid == 0) {
+          if (c >= 1) mbar_wait(&wu_done, (c - 1) & 1);
+          mbar_expect_tx(&pr_full, 2 * C * C * 2 + 2 * C * 4);
+          bulk_load(sT, prec + (size_t)c * PREC_BYTES + PREC_T, 2 * C * C * 2, &pr_full);
+          bulk_load(vb + C, prec + (size_t)c * PREC_BYTES + PREC_S, 2 * C * 4, &pr_full);
+        }
+        mbar_wait(&pr_full, c & 1);
+        grp_sync<NP>(BAR_P);  // beta written by every thread that holds one
+        if (tid == 0) mbar_arrive(&t_ready);
+        continue;
+      }
       if (GATED && half == 0 && w < C) {
         // G_w = sum_{j <= w} g_j: warp inclusive scan + warp 0's total
         float x = gval, t0s = g0val;
@@ -410,6 +439,7 @@ __global__ void __launch_bounds__(NT, 1)
         TSTAMP(15);
         const int i = tid & 63, j0 = (tid >> 6) * 16;
         uint4 xrec[2];  // the X record, stored once T is handed over
+        uint4 trec[2], turec[2];  // SEG1 with prep records: T', T'' segments
         float4 x4[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) x4[q] = *reinterpret_cast<const float4*>(LX + i * LS + j0 + 4 * q);
@@ -438,6 +468,12 @@ __global__ void __launch_bounds__(NT, 1)
           }
           il_store8(sT, C, i, j0 + g * 8, x);
           il_store8(sTu, C, i, j0 + g * 8, y);
+          if (SEG1) {
+            trec[g] = make_uint4(pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]), pack_bf16(x[4], x[5]),
+                                 pack_bf16(x[6], x[7]));
+            turec[g] = make_uint4(pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]),
+                                  pack_bf16(y[4], y[5]), pack_bf16(y[6], y[7]));
+          }
           xrec[g].x = pack_bf16(xs[0], xs[1]);
           xrec[g].y = pack_bf16(xs[2], xs[3]);
           xrec[g].z = pack_bf16(xs[4], xs[5]);
@@ -447,6 +483,15 @@ __global__ void __launch_bounds__(NT, 1)
         grp_sync<NP>(BAR_P);
         TSTAMP(31);
         if (tid == 0) mbar_arrive(&t_ready);
+        if (SEG1 && prec) {  // pass 1: the prep record for pass 3 (T', T'' images; s, 1/s)
+          uint8_t* pr = prec + (size_t)c * PREC_BYTES;
+#pragma unroll
+          for (int g = 0; g < 2; ++g) {
+            *reinterpret_cast<uint4*>(pr + PREC_T + il_off(i, j0 + g * 8, C)) = trec[g];
+            *reinterpret_cast<uint4*>(pr + PREC_T + C * C * 2 + il_off(i, j0 + g * 8, C)) = turec[g];
+          }
+          if (tid < 2 * C) reinterpret_cast<float*>(pr + PREC_S)[tid] = vb[C + tid];
+        }
         if (recs) {  // the X record from registers (IL image, 16 B per row), off the hand-over
 #pragma unroll
           for (int g = 0; g < 2; ++g)
@@ -877,7 +922,7 @@ __global__ void __launch_bounds__(NT, 1)
         mma_commit(&g_done);
       };
       if (NC > 0) {
-        gram_k(0);
+        if (!pre) gram_k(0);  // (pass 3 from prep records needs no K K^T)
         if (!SEG1) gram_q(0);
       }
 #pragma unroll 1
@@ -890,7 +935,7 @@ __global__ void __launch_bounds__(NT, 1)
         // landed (K K^T then runs under this chunk's substitution) -- but
         // never ahead of this chunk's W/U products: if T is ready first, the
         // remaining halves wait until after them
-        bool pk = c + 1 < NC, pq = !SEG1 && c + 1 < NC;
+        bool pk = !pre && c + 1 < NC, pq = !SEG1 && c + 1 < NC;
         bool kfree = false;
         while (true) {
           if (pk) {
@@ -1307,7 +1352,8 @@ int tc_fwd_segments(const deltanet_desc* d) {
 size_t tc_scratch_bytes(const deltanet_desc* d) {
   const int nseg = tc_fwd_segments(d);
   const size_t seg = nseg > 1 ? (size_t)d->B * d->H * nseg * (2 * DK * DV + DK * DK) * 4 : 0;
-  return round256(rec_bytes(d->B, d->H, d->L)) + seg;
+  const size_t prec = nseg > 1 ? (size_t)d->B * d->H * ((d->L + C - 1) / C) * PREC_BYTES : 0;
+  return round256(rec_bytes(d->B, d->H, d->L)) + round256(seg) + prec;
 }
 
 // fwd: 1 kernel (3 when segmented); bwd: 1 kernel (3 when segmented), plus
@@ -1333,6 +1379,10 @@ int tc_seg_setup(Args& a) {
   a.hloc = base;
   a.psi = a.hloc + (size_t)BH * nseg * DK * DV;
   a.hseg = a.psi + (size_t)BH * nseg * DK * DK;
+  // prep records of pass 1 for pass 3 (forward, with the per-chunk records)
+  a.prec = (a.flags & DELTANET_SAVE_STATES)
+               ? (uint8_t*)base + round256((size_t)BH * nseg * (2 * DK * DV + DK * DK) * 4)
+               : nullptr;
   return nseg;
 }
 
@@ -1348,6 +1398,8 @@ int tc_fwd(const Args& a0, cudaStream_t s) {
         cudaFuncSetAttribute(tc_fwd_kernel<false, false, true>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess ||
         cudaFuncSetAttribute(tc_fwd_kernel<false, true, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess ||
+        cudaFuncSetAttribute(tc_fwd_kernel<false, false, false, true>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess ||
         scan_attrs() != DELTANET_OK)
       return DELTANET_ERR_CUDA;
@@ -1372,9 +1424,12 @@ int tc_fwd(const Args& a0, cudaStream_t s) {
     else tc_fwd_kernel<false><<<BH, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);
     return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
   }
+  if (comp) a.prec = nullptr;  // (the compensated pass 3 redoes its prep)
   tc_fwd_kernel<true><<<BH * nseg, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);   // pass 1
   seg_scan_kernel<<<dim3(BH, DV / 16), 256, PSI_SMEM, s>>>(a);              // pass 2
   if (comp) tc_fwd_kernel<false, false, true><<<BH * nseg, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);
+  else if (a.prec)  // pass 3 from pass 1's prep records
+    tc_fwd_kernel<false, false, false, true><<<BH * nseg, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);
   else tc_fwd_kernel<false><<<BH * nseg, NT, SMEM_BYTES, s>>>(mQ, mK, mV, mO, a);  // pass 3
   return cudaGetLastError() == cudaSuccess ? DELTANET_OK : DELTANET_ERR_CUDA;
 }
@@ -1401,6 +1456,7 @@ int tc_fwd_transition(const Args& a0, float* psi, float* hloc, cudaStream_t s) {
   a.hT = nullptr;
   a.h0 = nullptr;
   const int nseg = a.scratch ? tc_seg_setup(a) : 1;
+  a.prec = nullptr;  // no pass 3 here
   if (nseg <= 1) {
     a.nseg = 1;
     a.hloc = hloc;

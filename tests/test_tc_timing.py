@@ -31,7 +31,8 @@ def timlib():
 def test_fwd_timeline(timlib):
     import paper_2406_06484_b200 as dn
     lib = timlib
-    cfg = synth.CONFIGS["target"]
+    # DN_TIMING_CFG=long: the segmented forward (CTA 0 = pass 3's first segment)
+    cfg = synth.CONFIGS[os.environ.get("DN_TIMING_CFG", "target")]
     B = int(os.environ.get("DN_TIMING_B", cfg.B))  # full bench batch: HBM contended
     x = synth.make_inputs(cfg, b_range=range(B))
     td = torch.bfloat16
@@ -60,6 +61,7 @@ def test_fwd_timeline(timlib):
         assert rc == 0
     torch.cuda.synchronize()
     t = buf.cpu().numpy().reshape(NC, 32).astype(np.int64)
+    t = t[:int((t[:, 0] != 0).sum())]  # segmented: CTA 0 walks its segment only
     names = {0: "P start", 1: "P tma+empty wait", 2: "P norms", 3: "P gram wait",
              21: " S2 tmem ld + s", 22: " S2 sync", 23: " S2 A/L writes",
              4: "P S2 sync + gk_free", 10: " sub L1", 15: " T: wu_done(c-1) wait",

@@ -6,7 +6,7 @@ import pytest
 import torch
 
 import synth
-from parity import TOL, compare, normwise, run_gpu, run_oracle
+from parity import TOL, compare, normwise, run_gpu, run_oracle, to_dev
 
 pytestmark = pytest.mark.gpu
 
@@ -248,6 +248,28 @@ def test_bf16_segments_match_serial():
     a = run_gpu(inp, "bf16", 64)
     b = run_gpu(inp, "bf16", 64, segments=False)
     compare({k: a[k] for k in ("o", "hT")}, {k: b[k] for k in ("o", "hT")}, TOL["bf16"])
+
+
+def test_bf16_segment_prep_records_bitwise():
+    """Segmented forward, pass 3 from pass 1's prep records (T', T'' images,
+    s, 1/s) vs pass 3 redoing its prep (without saved
+    states there are no prep records): identical operands, so o and hT are
+    bitwise equal; a ragged tail and a nonzero h0 included."""
+    import paper_2406_06484_b200 as dn
+    cfg, inp = _case(1, 3, 64 * 40 + 23, 128, 128, 64, "bf16", index=527)
+    dev = lambda x, dt=torch.bfloat16: to_dev(x, dt)
+    q, k, v, b = (dev(inp[f]) for f in ("q", "k", "v", "beta"))
+    h0n = (0.1 * np.random.default_rng(7).standard_normal((1, 3, 128, 128))).astype(np.float32)
+    h0 = dev(h0n, torch.float32)
+    d = dn.make_desc(1, 3, cfg.L, 128, 128, 64, torch.bfloat16)
+    assert dn.deltanet_launch_count(d, 0) == 3, "expected the segmented forward"
+    o1, h1, _ = dn.deltanet_fwd(q, k, v, b, h0=h0, save_states=True)
+    o2, h2, _ = dn.deltanet_fwd(q, k, v, b, h0=h0, save_states=False)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2) and torch.equal(h1, h2)
+    ref = run_oracle(inp, h0=h0n.astype(np.float64))
+    compare({"o": o1.float().cpu().numpy(), "hT": h1.cpu().numpy()},
+            {"o": ref["o"], "hT": ref["hT"]}, TOL["bf16"])
 
 
 def test_bf16_long_context_sampled_units():

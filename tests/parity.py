@@ -78,3 +78,22 @@ def compare(got, ref, tol, keys=None):
     bad = {k: e for k, e in errs.items() if not e <= tol}
     assert not bad, f"normwise errors above {tol}: {bad} (all: {errs})"
     return errs
+
+
+def row_guard(got, ref, key, tol, rows=64):
+    """Localised errors in low-magnitude stretches of a per-token output
+    (dbeta, dg) are invisible in the tensor-max metric.  Per unit and per
+    window of `rows` tokens: max|x - ref| / max(|ref| over the window, the
+    unit's RMS) <= tol.  (The RMS floor keeps windows whose reference is
+    accidentally ~0 from dividing by ~0.)"""
+    x = np.asarray(got[key], np.float64)
+    r = np.asarray(ref[key], np.float64)
+    L = r.shape[-1]
+    rms = np.sqrt((r ** 2).mean(axis=-1, keepdims=True))
+    worst = 0.0
+    for t0 in range(0, L, rows):
+        xs, rs = x[..., t0:t0 + rows], r[..., t0:t0 + rows]
+        den = np.maximum(np.abs(rs).max(axis=-1), rms[..., 0])
+        worst = max(worst, float((np.abs(xs - rs).max(axis=-1) / den).max()))
+    assert worst <= tol, f"{key}: per-window normwise error {worst:.3g} > {tol}"
+    return worst

@@ -6,7 +6,7 @@ import pytest
 import torch
 
 import synth
-from parity import TOL, compare, normwise, run_gpu, run_oracle, to_dev
+from parity import TOL, compare, normwise, row_guard as _row_guard, run_gpu, run_oracle, to_dev
 
 pytestmark = pytest.mark.gpu
 
@@ -149,25 +149,6 @@ def _per_unit(got, ref, tol, B, H):
             sub = {k: (None if v is None else v[b:b + 1, h:h + 1]) for k, v in got.items()}
             one = {k: (None if v is None else v[b:b + 1, h:h + 1]) for k, v in ref.items()}
             compare(sub, one, tol)
-
-
-def _row_guard(got, ref, key, tol, rows=64):
-    """Localised errors in low-magnitude stretches of a per-token output
-    (dbeta, dg) are invisible in the tensor-max metric.  Per unit and per
-    window of `rows` tokens: max|x - ref| / max(|ref| over the window, the
-    unit's RMS) <= tol.  (The RMS floor keeps windows whose reference is
-    accidentally ~0 from dividing by ~0.)"""
-    x = np.asarray(got[key], np.float64)
-    r = np.asarray(ref[key], np.float64)
-    L = r.shape[-1]
-    rms = np.sqrt((r ** 2).mean(axis=-1, keepdims=True))
-    worst = 0.0
-    for t0 in range(0, L, rows):
-        xs, rs = x[..., t0:t0 + rows], r[..., t0:t0 + rows]
-        den = np.maximum(np.abs(rs).max(axis=-1), rms[..., 0])
-        worst = max(worst, float((np.abs(xs - rs).max(axis=-1) / den).max()))
-    assert worst <= tol, f"{key}: per-window normwise error {worst:.3g} > {tol}"
-    return worst
 
 
 def test_bf16_target_full_size_all_units():

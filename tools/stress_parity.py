@@ -52,7 +52,15 @@ def main(n=12, seed=7):
         for o2 in outs[1:]:
             assert np.array_equal(outs[0][key], o2[key]), f"non-deterministic {key}"
     print("deterministic over 3 runs at the target shape")
+    # and at the long-context shape (segmented forward with prep records)
+    cfg = synth.CONFIGS["long"]
+    inp = synth.make_inputs(cfg)
+    outs = [run_gpu(inp, "bf16", 64) for _ in range(2)]
+    for key in outs[0]:
+        if outs[0][key] is not None:
+            assert np.array_equal(outs[0][key], outs[1][key]), f"non-deterministic {key} (long)"
+    print("deterministic over 2 runs at the long-context shape")
 
 
 if __name__ == "__main__":
-    main()
+    main(int(sys.argv[1]) if len(sys.argv) > 1 else 12)

@@ -261,6 +261,10 @@ __global__ void __launch_bounds__(NT, 1)
   uint8_t* const prec =
       a.prec ? a.prec + ((size_t)unit * a.NC + cbase) * PREC_BYTES : nullptr;
   constexpr bool pre = PRE;  // pass 3 from prep records
+  // compensated mode: A = tril(Q K^T) is formed by the prep warps from a
+  // joint Gram commit (its state warpgroup carries the rounding chains and is
+  // the busier side there)
+  constexpr bool APREP = COMP && !SEG1;
   // SEG1: the Psi image [dk][dk] bf16 (IL R=128) over A[0], A[1], W[0]; W in W[1]
   uint8_t* sPsi = smem + OFF_A;
   static_assert(OFF_W == OFF_A + 2 * C * C * 2 && 2 * C * C * 2 + DK * C * 2 == DK * DK * 2,
@@ -416,6 +420,23 @@ __global__ void __launch_bounds__(NT, 1)
             v.z = (j + 2 < i) ? bi * s4[q].z * kk[2] : 0.f;
             v.w = (j + 3 < i) ? bi * s4[q].w * kk[3] : 0.f;
             *reinterpret_cast<float4*>(LX + i * LS + j) = v;
+          }
+        }
+        if (APREP) {  // A = tril(Q K^T) (raw, inclusive, R4; gated: Gamma . A) and its record
+          float xa[16];  // hi lanes: G_qk columns [h+16, h+32) from the lo partner
+#pragma unroll
+          for (int e = 0; e < 16; ++e) xa[e] = __shfl_xor_sync(0xffffffffu, f[16 + e], 16);
+#pragma unroll
+          for (int g = 0; g < 2; ++g) {
+            float a8[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              float qk = lo ? f[g * 8 + e] : xa[g * 8 + e];
+              if (GATED) qk *= gam16[g * 8 + e];
+              a8[e] = (c0 + g * 8 + e <= i) ? qk : 0.f;
+            }
+            il_store8(sA(b), C, i, c0 + g * 8, a8);
+            if (recs) il_store8(recs + (size_t)c * REC_BYTES + REC_A, C, i, c0 + g * 8, a8);
           }
         }
       }
@@ -615,7 +636,7 @@ __global__ void __launch_bounds__(NT, 1)
         mbar_arrive(&bar_full[b]);
       }
       if (!SEG1 && !GATED) norms();
-      if (!SEG1) {
+      if (!SEG1 && !APREP) {
         // A = tril(Q K^T), raw (inclusive, R4; gated: Gamma . A) -> sA(b), the
         // operand of this chunk's O += A Z, and the backward's A record.  Done
         // here (the state warpgroup waits for the U' product anyway) rather than
@@ -767,7 +788,7 @@ __global__ void __launch_bounds__(NT, 1)
       wg_sync(BAR_S);
       if (w == 0) {
         mbar_arrive(&z_ready);
-        if (!SEG1) mbar_arrive(&g_free);  // G_qk read: the next chunk's Q K^T may land
+        if (!SEG1 && !APREP) mbar_arrive(&g_free);  // G_qk read: the next chunk's Q K^T may land
       }
       TSTAMP(18);
       mbar_wait(&ho_done, c & 1);
@@ -901,13 +922,16 @@ __global__ void __launch_bounds__(NT, 1)
       const uint32_t idg = idesc_bf16(64, 64, false, false);
       const uint32_t idw = idesc_bf16(128, 64, true, false);
       const uint32_t at = smem_u32(sT), atu = smem_u32(sTu), av = smem_u32(sV);
-      auto gram_k = [&](int c) {  // G_kk -> lanes 16-31 of each quadrant
-        const uint32_t ak = smem_u32(sK(c % NKB));
+      auto gram_k = [&](int c) {  // G_kk -> lanes 16-31 of each quadrant (APREP: and G_qk)
+        const uint32_t ak = smem_u32(sK(c % NKB)), aq = smem_u32(sQ(c % NQB));
         mbar_wait(&k_full[c % NKB], (c / NKB) & 1);
+        if (APREP) mbar_wait(&q_full[c % NQB], (c / NQB) & 1);
         fence_after_sync();
 #pragma unroll
-        for (int k0 = 0; k0 < DK; k0 += 16)
+        for (int k0 = 0; k0 < DK; k0 += 16) {
           mma_bf16(tm + TM_G + LO16, desc_k_sw(ak, C, k0), desc_k_sw(ak, C, k0), idg, k0 > 0);
+          if (APREP) mma_bf16(tm + TM_G, desc_k_sw(aq, C, k0), desc_k_sw(ak, C, k0), idg, k0 > 0);
+        }
         mma_commit(&gk_done);
       };
       auto gram_q = [&](int c) {  // G_qk -> lanes 0-15 of each quadrant
@@ -923,7 +947,7 @@ __global__ void __launch_bounds__(NT, 1)
       };
       if (NC > 0) {
         if (!pre) gram_k(0);  // (pass 3 from prep records needs no K K^T)
-        if (!SEG1) gram_q(0);
+        if (!SEG1 && !APREP) gram_q(0);
       }
 #pragma unroll 1
       for (int c = 0; c < NC; ++c) {
@@ -935,12 +959,13 @@ __global__ void __launch_bounds__(NT, 1)
         // landed (K K^T then runs under this chunk's substitution) -- but
         // never ahead of this chunk's W/U products: if T is ready first, the
         // remaining halves wait until after them
-        bool pk = !pre && c + 1 < NC, pq = !SEG1 && c + 1 < NC;
+        bool pk = !pre && c + 1 < NC, pq = !SEG1 && !APREP && c + 1 < NC;
         bool kfree = false;
         while (true) {
           if (pk) {
             if (!kfree) kfree = mbar_test(&gk_free, c & 1);
-            if (kfree && mbar_test(&k_full[(c + 1) % NKB], ((c + 1) / NKB) & 1)) {
+            if (kfree && mbar_test(&k_full[(c + 1) % NKB], ((c + 1) / NKB) & 1) &&
+                (!APREP || mbar_test(&q_full[(c + 1) % NQB], ((c + 1) / NQB) & 1))) {
               gram_k(c + 1);
               pk = false;
             }

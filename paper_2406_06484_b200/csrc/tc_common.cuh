@@ -1,6 +1,7 @@
 // tc_common.cuh -- sm_100a primitives: tcgen05 MMA/TMEM, mbarrier, TMA.
 //
-// Operand layout used by every tensor-core tile in this library ("IL",
+// Operand layout of the tensor-core tiles ("IL"; the forward's Q, K, V and
+// O tiles use the SW layout further below instead,
 // SWIZZLE_NONE canonical layout): a logical R x Cc bf16 matrix X (row-major,
 // columns contiguous) is stored as core matrices of 8 rows x 16 bytes:
 //     byte offset of X[r][c] = ((c / 8) * R + r) * 16 + (c % 8) * 2

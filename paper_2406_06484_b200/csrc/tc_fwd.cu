@@ -19,14 +19,17 @@
 //   H^T += Z^T K                                       Eq. 8, M=128
 // Algebra of the folded normalisation: DESIGN.md §4.1.
 //
-// Warp specialisation: warpgroup P (warps 0-3) runs the
-// state-independent "prep" of chunk t+1 (norms, A, L, substitution, T, W)
-// while warpgroup S (warps 4-7) runs the conversions of the state chain and
-// the output epilogue of chunk t.  Warp 8 issues the prep MMAs and the V
-// loads; warp 9 issues the chain MMAs, the state save, the O store and the
-// next Q/K loads, so no compute warp ever stalls on an MMA issue queue.
-// Q/K/A/W tiles and the U accumulator are double-buffered by chunk parity;
-// mbarriers hand every buffer over (full/empty, *_done/*_free/*_ready).
+// Warp specialisation: warps 0-7 ("prep") run the
+// state-independent part of chunk t+1 (row norms and L from G_kk, the
+// substitution, T', T'') while warps 8-11 ("state") run chunk t's chain
+// conversions (W^T, A from G_qk, Z, H^T) and the output epilogue.  Warp 12
+// issues the prep MMAs (the two Gram halves, W, U) and the V loads; warp 13
+// issues the chain MMAs, the O store, the record copies and the next Q/K
+// loads, so no compute warp ever stalls on an MMA issue queue.  Q, K, V and
+// O are SW (SWIZZLE_128B) tiles, moved by TMA boxes of 128 B rows
+// (tc_common.cuh sw_off).  Q, A and the U accumulator are double-buffered by
+// chunk parity, K has three slots; mbarriers hand every buffer over
+// (full/empty, *_done/*_free/*_ready).
 #include <cudaTypedefs.h>
 #include <stdio.h>
 

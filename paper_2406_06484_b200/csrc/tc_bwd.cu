@@ -125,6 +125,23 @@ __device__ __forceinline__ float reduce_scatter(float (&v)[N], int lane) {
 __device__ __forceinline__ float gamma_ij(const float* gG, int i, int j) {
   return __expf(j <= i ? gG[i] - gG[j] : 0.f);
 }
+// Two 32-column loads behind one wait (the TMEM load latency is paid once)
+__device__ __forceinline__ void ld32x2(uint32_t tm, int wwarp, uint32_t ca, float (&fa)[32],
+                                       uint32_t cb, float (&fb)[32]) {
+  uint32_t r[4][16];
+  tmem_ld16(taddr(tm, wwarp * 32, ca), r[0]);
+  tmem_ld16(taddr(tm, wwarp * 32, ca + 16), r[1]);
+  tmem_ld16(taddr(tm, wwarp * 32, cb), r[2]);
+  tmem_ld16(taddr(tm, wwarp * 32, cb + 16), r[3]);
+  tmem_ld_wait();
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    fa[j] = __uint_as_float(r[0][j]);
+    fa[16 + j] = __uint_as_float(r[1][j]);
+    fb[j] = __uint_as_float(r[2][j]);
+    fb[16 + j] = __uint_as_float(r[3][j]);
+  }
+}
 __device__ __forceinline__ void ld16f(uint32_t tm, int wwarp, uint32_t col, float (&f)[16]) {
   uint32_t r[16];
   tmem_ld16(taddr(tm, wwarp * 32, col), r);
@@ -882,8 +899,14 @@ __global__ void __launch_bounds__(NT, 1)
           // lanes < 16: columns [0,64), lanes >= 16: [64,128) of row r64, for
           // both P (TM_P) and K H (TM_KH); 32 of each half per warpgroup
           float p[32], f[32];
-          ld32(tm, wwarp, TM_P + 32 * wg, p);
-          ld32(tm, wwarp, TM_KH + 32 * wg, f);
+          // (gated: both behind one wait; the ungated kernel measured faster
+          // with two -- DESIGN.md §11)
+          if (GATED) {
+            ld32x2(tm, wwarp, TM_P + 32 * wg, p, TM_KH + 32 * wg, f);
+          } else {
+            ld32(tm, wwarp, TM_P + 32 * wg, p);
+            ld32(tm, wwarp, TM_KH + 32 * wg, f);
+          }
           const float bt = sb[r64], si = ss[r64];
           const float gi = GATED ? gam[r64] : 1.f;
           const int c0 = (lo ? 0 : 64) + 32 * wg;
@@ -919,11 +942,10 @@ __global__ void __launch_bounds__(NT, 1)
           mbar_wait(&mb[MB_P], ph);
           fence_after_sync();
         }
-#pragma unroll 1
-        for (int cc = 0; cc < 2; ++cc) {  // dX = dX' diag(beta) (lanes < 16: dX' rows)
+        // dX = dX' diag(beta) (lanes < 16: dX' rows), 16 columns at a time
+        auto dx16 = [&](int cc, const float (&f)[16]) {
           const int col = 32 * wg + 16 * cc;
-          float f[16], x[8];
-          ld16f(tm, wwarp, TM_DX + col, f);
+          float x[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) x[e] = __shfl_xor_sync(0xffffffffu, f[8 + e], 16);
           if (lo) {
@@ -936,6 +958,24 @@ __global__ void __launch_bounds__(NT, 1)
           x[0] *= b0.x; x[1] *= b0.y; x[2] *= b0.z; x[3] *= b0.w;
           x[4] *= b1.x; x[5] *= b1.y; x[6] *= b1.z; x[7] *= b1.w;
           il_store8(sDX, C, r64, c8, x);
+        };
+        if (GATED) {  // both halves behind one TMEM wait
+          float fdx[32];
+          ld32(tm, wwarp, TM_DX + 32 * wg, fdx);
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            float f[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) f[e] = fdx[16 * cc + e];
+            dx16(cc, f);
+          }
+        } else {
+#pragma unroll 1
+          for (int cc = 0; cc < 2; ++cc) {
+            float f[16];
+            ld16f(tm, wwarp, TM_DX + 32 * wg + 16 * cc, f);
+            dx16(cc, f);
+          }
         }
       }
       simt_signal(&sg[SG_P5], tid);
@@ -1056,12 +1096,23 @@ __global__ void __launch_bounds__(NT, 1)
         // (TM_G + 16); each lane pair splits every 16 columns 8 / 8
         float d2 = 0.f, t2[16];
         const float bi = sb[r64];
+        // gated: G and K_hat K_hat^T columns [32 wg, 32 wg + 32) behind one wait
+        float g32[32], k32[32];
+        if (GATED) ld32x2(tm, wwarp, TM_GB + 32 * wg, g32, TM_G + 32 * wg, k32);
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
           const int col = 32 * wg + 16 * cc;
           float g16[16], k16[16], x[8];
-          ld16f(tm, wwarp, TM_GB + col, g16);
-          ld16f(tm, wwarp, TM_G + col, k16);
+          if (GATED) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              g16[e] = g32[16 * cc + e];
+              k16[e] = k32[16 * cc + e];
+            }
+          } else {
+            ld16f(tm, wwarp, TM_GB + col, g16);
+            ld16f(tm, wwarp, TM_G + col, k16);
+          }
 #pragma unroll
           for (int e = 0; e < 8; ++e) x[e] = __shfl_xor_sync(0xffffffffu, lo ? g16[8 + e] : k16[e], 16);
           const int c8 = col + (lo ? 0 : 8);

@@ -209,3 +209,15 @@ def test_gated_errors_before_launch(lib):
     ok = _desc(Dk=128, Dv=128, chunk=64, flags=dn.DELTANET_GATED)
     assert lib.deltanet_fwd_transition(D(ok), a, a, a, a, a, a, a, 1 << 34, nul) == 2
     assert dn.deltanet_launch_count(dg, 0) == 1
+
+
+def test_workspace_holds_segment_prep_records(lib):
+    """A segmented forward (few units, many chunks) reserves
+    pass 1's per-chunk prep records [T' | T'' | s | 1/s] (16.5 KB per chunk
+    per unit) beyond the same shape without segments."""
+    B, H, L = 1, 2, 64 * 40
+    seg = _desc(B=B, H=H, L=L, flags=1 | 2)
+    noseg = _desc(B=B, H=H, L=L, flags=1 | 2 | dn.DELTANET_NO_SEGMENTS)
+    assert dn.deltanet_launch_count(seg, 0) == 3 and dn.deltanet_launch_count(noseg, 0) == 1
+    prec = B * H * (L // 64) * (2 * 64 * 64 * 2 + 2 * 64 * 4)
+    assert dn.deltanet_workspace_bytes(seg) - dn.deltanet_workspace_bytes(noseg) >= prec
